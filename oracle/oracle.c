@@ -1,0 +1,389 @@
+/*
+ * ORACLE -- plain, slow, single-threaded CPU reference for the hot path of
+ * arXiv 2404.16039 ("vectorized" page-wise linear algebra + P1 FEM assembly).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product (paper_2404_16039_b200/, include/vb.h, libvb.so) never links,
+ * includes or calls anything here, and nothing here includes product code.
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -shared -fPIC (oracle/build.py).
+ * fp64 throughout (the paper's MATLAB default, P:461 / BASELINE.md).
+ *
+ * Citation keys: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * O1..O12 = SURVEY.md §8(c) oracle algorithm rows.
+ *
+ * Page layout (O1): entry (i,j) of page k of a
+ * rows x cols page array lives at p[(i + j*rows)*ld + k]; ld == 0 means the
+ * single object is broadcast to every page (eq:copy).
+ *
+ * Every function below writes the plain definition out; there is no blocking,
+ * fusion or reordering.  Parity pins live in tests/test_oracle_*.py.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_OK 0
+#define ORC_ERR_DIM (-2)
+#define ORC_ERR_ARG (-1)
+
+/* O1: page accessor (P:248-266 with W as the page index).  ld == 0 is the
+ * copy map eq:copy: ONE rows x cols object, stored column-major
+ * and contiguous, is used as every page. */
+static double at(const double* p, int64_t ld, int rows, int i, int j, int64_t k) {
+    if (ld == 0) return p[i + j * rows];
+    return p[(int64_t)(i + j * rows) * ld + k];
+}
+
+/* O2: page-wise matrix multiplication Z_k = op(X_k) op(Y_k)
+ * (eq:pagewisemultGeneral / layeredMultiplication; pagemtimes
+ * semantics P:391).  op = transpose when tX/tY != 0.  Sum over l ascending,
+ * plain multiply-then-add (no FMA: -ffp-contract=off). */
+int orc_page_mtimes(int64_t np, const double* X, int xr, int xc, int64_t ldx, int tX,
+                    const double* Y, int yr, int yc, int64_t ldy, int tY,
+                    double* Z, int64_t ldz) {
+    int m = tX ? xc : xr, kx = tX ? xr : xc;
+    int ky = tY ? yc : yr, n = tY ? yr : yc;
+    if (kx != ky) return ORC_ERR_DIM;
+    for (int64_t k = 0; k < np; k++)
+        for (int i = 0; i < m; i++)
+            for (int j = 0; j < n; j++) {
+                double s = 0.0;
+                for (int l = 0; l < kx; l++) {
+                    double a = tX ? at(X, ldx, xr, l, i, k) : at(X, ldx, xr, i, l, k);
+                    double b = tY ? at(Y, ldy, yr, j, l, k) : at(Y, ldy, yr, l, j, k);
+                    s = s + a * b;
+                }
+                Z[(int64_t)(i + j * m) * ldz + k] = s;
+            }
+    return ORC_OK;
+}
+
+/* O3: page-wise transpose (layeredTransposeHom/Ten). */
+int orc_page_transpose(int64_t np, const double* X, int rows, int cols, int64_t ldx,
+                       double* Z, int64_t ldz) {
+    for (int64_t k = 0; k < np; k++)
+        for (int i = 0; i < rows; i++)
+            for (int j = 0; j < cols; j++)
+                Z[(int64_t)(j + i * cols) * ldz + k] = at(X, ldx, rows, i, j, k);
+    return ORC_OK;
+}
+
+/* O4: determinant by Laplace (cofactor) expansion along row 0 with recursive
+ * minors -- the textbook definition (layeredDeterminant). a is an
+ * n x n matrix stored a[i*4 + j] (row-major scratch, n <= 4). */
+static double det_laplace(const double* a, int n) {
+    if (n == 1) return a[0];
+    if (n == 2) return a[0 * 4 + 0] * a[1 * 4 + 1] - a[0 * 4 + 1] * a[1 * 4 + 0];
+    double s = 0.0;
+    for (int c = 0; c < n; c++) {
+        double sub[16];
+        for (int i = 1; i < n; i++) {
+            int jj = 0;
+            for (int j = 0; j < n; j++) {
+                if (j == c) continue;
+                sub[(i - 1) * 4 + jj] = a[i * 4 + j];
+                jj++;
+            }
+        }
+        double cof = det_laplace(sub, n - 1);
+        double term = a[0 * 4 + c] * cof;
+        s = (c % 2 == 0) ? s + term : s - term;
+    }
+    return s;
+}
+
+/* minor(r, c): determinant of a with row r and column c removed. */
+static double minor_rc(const double* a, int n, int r, int c) {
+    double sub[16];
+    int ii = 0;
+    for (int i = 0; i < n; i++) {
+        if (i == r) continue;
+        int jj = 0;
+        for (int j = 0; j < n; j++) {
+            if (j == c) continue;
+            sub[ii * 4 + jj] = a[i * 4 + j];
+            jj++;
+        }
+        ii++;
+    }
+    return det_laplace(sub, n - 1);
+}
+
+static void load_page(const double* X, int64_t ldx, int n, int64_t k, double* a) {
+    for (int i = 0; i < n; i++)
+        for (int j = 0; j < n; j++) a[i * 4 + j] = at(X, ldx, n, i, j, k);
+}
+
+int orc_page_det(int64_t np, int n, const double* X, int64_t ldx, double* det) {
+    if (n < 1 || n > 4) return ORC_ERR_DIM;
+    double a[16];
+    for (int64_t k = 0; k < np; k++) {
+        load_page(X, ldx, n, k, a);
+        det[k] = det_laplace(a, n);
+    }
+    return ORC_OK;
+}
+
+/* O5: inverse by the adjugate, inv(i,j) = (-1)^(i+j) minor(j,i) / det
+ * (layeredInverse; aminv returns the determinant too).
+ * Singular pages follow IEEE (division by zero), SURVEY B3. */
+int orc_page_inv(int64_t np, int n, const double* X, int64_t ldx,
+                 double* Xinv, int64_t ldinv, double* det) {
+    if (n < 1 || n > 4) return ORC_ERR_DIM;
+    double a[16];
+    for (int64_t k = 0; k < np; k++) {
+        load_page(X, ldx, n, k, a);
+        double d = det_laplace(a, n);
+        for (int i = 0; i < n; i++)
+            for (int j = 0; j < n; j++) {
+                double cof = (n == 1) ? 1.0 : minor_rc(a, n, j, i);
+                if ((i + j) % 2) cof = -cof;
+                Xinv[(int64_t)(i + j * n) * ldinv + k] = cof / d;
+            }
+        if (det) det[k] = d;
+    }
+    return ORC_OK;
+}
+
+/* O6: cross product c = a x b of 3-vector pages (BASELINE.json north_star;
+ * the columns of cof(A) are cross products of A's columns). */
+int orc_page_cross(int64_t np, const double* A, int64_t lda, const double* B, int64_t ldb,
+                   double* C, int64_t ldc) {
+    for (int64_t k = 0; k < np; k++) {
+        double a1 = at(A, lda, 3, 0, 0, k), a2 = at(A, lda, 3, 1, 0, k), a3 = at(A, lda, 3, 2, 0, k);
+        double b1 = at(B, ldb, 3, 0, 0, k), b2 = at(B, ldb, 3, 1, 0, k), b3 = at(B, ldb, 3, 2, 0, k);
+        C[0 * ldc + k] = a2 * b3 - a3 * b2;
+        C[1 * ldc + k] = a3 * b1 - a1 * b3;
+        C[2 * ldc + k] = a1 * b2 - a2 * b1;
+    }
+    return ORC_OK;
+}
+
+/* O8: gather, create_coords3D (Code coords3D): coords3D(:,a,e) =
+ * coords(elems(e,a),:) and vectors3D(:,a,e) = coords3D(:,a,e) - coords3D(:,end,e).
+ * Outputs are page arrays (dim x nv and dim x (nv-1) pages, ld = ne). */
+int orc_create_coords3D(int dim, int nv, int64_t ne, const double* coords, int64_t node_stride,
+                        int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                        double* coords3D, double* vectors3D) {
+    for (int64_t e = 0; e < ne; e++)
+        for (int a = 0; a < nv; a++) {
+            int64_t v = elems[a * elem_ld + e];
+            for (int c = 0; c < dim; c++) {
+                double x = coords[c * comp_stride + v * node_stride];
+                if (coords3D) coords3D[(int64_t)(c + a * dim) * ne + e] = x;
+            }
+        }
+    if (vectors3D)
+        for (int64_t e = 0; e < ne; e++) {
+            int64_t vl = elems[(nv - 1) * elem_ld + e];
+            for (int a = 0; a < nv - 1; a++) {
+                int64_t v = elems[a * elem_ld + e];
+                for (int c = 0; c < dim; c++)
+                    vectors3D[(int64_t)(c + a * dim) * ne + e] =
+                        coords[c * comp_stride + v * node_stride] - coords[c * comp_stride + vl * node_stride];
+            }
+        }
+    return ORC_OK;
+}
+
+/* O7: surface geometry of a triangulated closed surface (config 3):
+ * n = (b-a) x (c-a); |n| = sqrt(n.n); nhat = n/|n|; area = |n|/2;
+ * volume = sum_f (1/6) a.n, the divergence theorem with F = x/3
+ * (surf_int), summed in face order with Neumaier compensation. */
+int orc_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, const double* xyz,
+                    int64_t node_stride, int64_t comp_stride, double* n_out, double* nhat_out,
+                    double* area_out, double* volume_out) {
+    double s = 0.0, comp = 0.0;
+    for (int64_t f = 0; f < nf; f++) {
+        int64_t va = tri[0 * tri_ld + f], vb = tri[1 * tri_ld + f], vc = tri[2 * tri_ld + f];
+        double a[3], b[3], c[3], u[3], w[3], n[3];
+        for (int d = 0; d < 3; d++) {
+            a[d] = xyz[d * comp_stride + va * node_stride];
+            b[d] = xyz[d * comp_stride + vb * node_stride];
+            c[d] = xyz[d * comp_stride + vc * node_stride];
+            u[d] = b[d] - a[d];
+            w[d] = c[d] - a[d];
+        }
+        n[0] = u[1] * w[2] - u[2] * w[1];
+        n[1] = u[2] * w[0] - u[0] * w[2];
+        n[2] = u[0] * w[1] - u[1] * w[0];
+        double len = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+        for (int d = 0; d < 3; d++) {
+            if (n_out) n_out[d * nf + f] = n[d];
+            if (nhat_out) nhat_out[d * nf + f] = n[d] / len;
+        }
+        if (area_out) area_out[f] = len / 2.0;
+        double x = (a[0] * n[0] + a[1] * n[1] + a[2] * n[2]) / 6.0;
+        double t = s + x;  /* Neumaier */
+        if (fabs(s) >= fabs(x)) comp += (s - t) + x;
+        else comp += (x - t) + s;
+        s = t;
+    }
+    if (volume_out) *volume_out = s + comp;
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------- FEM P1 */
+
+static int64_t factorial(int d) { int64_t f = 1; for (int i = 2; i <= d; i++) f *= i; return f; }
+
+/* O9: P1 element matrices with c_K = c_M = 1 (eq:K_M P:967-975 with the
+ * RV2013 case c = 1; Code phider P:929-947; Code stiff_scalar_P1 P:978-1004):
+ *   tjac = D * X^T, i.e. J[r][c] = x_{r+1}[c] - x_0[c]     (smamt)
+ *   detJ (O4), |T| = |detJ| / d!
+ *   Jinv = adjugate / detJ (O5)                             (aminv)
+ *   G = Jinv * D, D = [-1 | I]                              (amsm)
+ *   K_e[a][b] = |T| * sum_r G[r][a] G[r][b]  (r ascending)   (amtam)
+ *   M_e[a][b] = |T| / ((d+1)(d+2)) * (1 + delta_ab)          (BASELINE north_star)
+ * X is the element's vertex coordinates, X[c*nv + a] = coordinate c of vertex a.
+ * Ke, Me are nv x nv, stored Ke[a*nv + b]. */
+void orc_p1_local(int dim, const double* X, double* Ke, double* Me) {
+    int nv = dim + 1;
+    double J[16], Jinv[16], G[4 * 4];
+    for (int r = 0; r < dim; r++)
+        for (int c = 0; c < dim; c++) J[r * 4 + c] = X[c * nv + (r + 1)] - X[c * nv + 0];
+    double detJ = det_laplace(J, dim);
+    double T = fabs(detJ) / (double)factorial(dim);
+    for (int i = 0; i < dim; i++)
+        for (int j = 0; j < dim; j++) {
+            double cof = (dim == 1) ? 1.0 : minor_rc(J, dim, j, i);
+            if ((i + j) % 2) cof = -cof;
+            Jinv[i * 4 + j] = cof / detJ;
+        }
+    /* G = Jinv * D with D[r][0] = -1, D[r][a] = delta_{r, a-1} */
+    for (int r = 0; r < dim; r++)
+        for (int a = 0; a < nv; a++) {
+            double s = 0.0;
+            for (int l = 0; l < dim; l++) {
+                double dla = (a == 0) ? -1.0 : (l == a - 1 ? 1.0 : 0.0);
+                s = s + Jinv[r * 4 + l] * dla;
+            }
+            G[r * 4 + a] = s;
+        }
+    double mscale = T / (double)((dim + 1) * (dim + 2));
+    for (int a = 0; a < nv; a++)
+        for (int b = 0; b < nv; b++) {
+            double s = 0.0;
+            for (int r = 0; r < dim; r++) s = s + G[r * 4 + a] * G[r * 4 + b];
+            Ke[a * nv + b] = T * s;
+            Me[a * nv + b] = mscale * (a == b ? 2.0 : 1.0);
+        }
+}
+
+/* Local matrices of all elements as page arrays K3D/M3D (nv x nv pages,
+ * ld = ne), the second output of stiffness_matrixP1. */
+int orc_p1_local_all(int dim, int64_t ne, const double* coords, int64_t node_stride,
+                     int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                     double* K3D, double* M3D) {
+    int nv = dim + 1;
+    for (int64_t e = 0; e < ne; e++) {
+        double X[16], Ke[16], Me[16];
+        for (int a = 0; a < nv; a++) {
+            int64_t v = elems[a * elem_ld + e];
+            for (int c = 0; c < dim; c++) X[c * nv + a] = coords[c * comp_stride + v * node_stride];
+        }
+        orc_p1_local(dim, X, Ke, Me);
+        for (int a = 0; a < nv; a++)
+            for (int b = 0; b < nv; b++) {
+                if (K3D) K3D[(int64_t)(a + b * nv) * ne + e] = Ke[a * nv + b];
+                if (M3D) M3D[(int64_t)(a + b * nv) * ne + e] = Me[a * nv + b];
+            }
+    }
+    return ORC_OK;
+}
+
+static int cmp_i32(const void* x, const void* y) {
+    int32_t a = *(const int32_t*)x, b = *(const int32_t*)y;
+    return (a > b) - (a < b);
+}
+
+/* O10: topological CSR pattern of sparse(X3D(:),Y3D(:),...):
+ * for e, a, b: push elems[e][b] into rows[elems[e][a]]; per row sort + unique
+ * (explicit zeros kept); row_ptr = exclusive scan of row sizes.
+ * Returns nnz.  With col_idx == NULL only row_ptr is written. */
+int64_t orc_p1_pattern(int dim, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
+                       int32_t* row_ptr, int32_t* col_idx) {
+    int nv = dim + 1;
+    int64_t* cnt = calloc((size_t)nn + 1, sizeof(int64_t));
+    if (!cnt) return -1;
+    for (int64_t e = 0; e < ne; e++)
+        for (int a = 0; a < nv; a++) cnt[elems[a * elem_ld + e] + 1] += nv;
+    for (int64_t v = 0; v < nn; v++) cnt[v + 1] += cnt[v];
+    int32_t* push = malloc((size_t)(cnt[nn] ? cnt[nn] : 1) * sizeof(int32_t));
+    int64_t* fill = malloc((size_t)(nn ? nn : 1) * sizeof(int64_t));
+    if (!push || !fill) { free(cnt); free(push); free(fill); return -1; }
+    for (int64_t v = 0; v < nn; v++) fill[v] = cnt[v];
+    for (int64_t e = 0; e < ne; e++)
+        for (int a = 0; a < nv; a++) {
+            int64_t r = elems[a * elem_ld + e];
+            for (int b = 0; b < nv; b++) push[fill[r]++] = elems[b * elem_ld + e];
+        }
+    int64_t nnz = 0;
+    for (int64_t v = 0; v < nn; v++) {
+        int32_t* seg = push + cnt[v];
+        int64_t len = cnt[v + 1] - cnt[v];
+        qsort(seg, (size_t)len, sizeof(int32_t), cmp_i32);
+        int64_t u = 0;
+        for (int64_t i = 0; i < len; i++)
+            if (i == 0 || seg[i] != seg[i - 1]) seg[u++] = seg[i];
+        row_ptr[v] = (int32_t)nnz;
+        if (col_idx) memcpy(col_idx + nnz, seg, (size_t)u * sizeof(int32_t));
+        nnz += u;
+    }
+    row_ptr[nn] = (int32_t)nnz;
+    free(cnt); free(push); free(fill);
+    return nnz;
+}
+
+static int64_t find_col(const int32_t* row_ptr, const int32_t* col_idx, int64_t r, int32_t c) {
+    int64_t lo = row_ptr[r], hi = row_ptr[r + 1];
+    while (lo < hi) {
+        int64_t mid = lo + (hi - lo) / 2;
+        if (col_idx[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    return (lo < row_ptr[r + 1] && col_idx[lo] == c) ? lo : -1;
+}
+
+/* O11: assembly = MATLAB sparse() with duplicates summed:
+ * zero K, M; for e ascending, a ascending, b ascending:
+ *   p = position of col elems[e][b] in row elems[e][a] (binary search);
+ *   K[p] += K_e[a][b]; M[p] += M_e[a][b].
+ * If row_mask != NULL only rows with row_mask[r] != 0 are accumulated (the
+ * same sums, restricted; used for sampled parity at full size) and only
+ * elements touching such a row are evaluated.  K or M may be NULL.
+ * Returns 0, or -3 if a (row, col) pair is missing from the pattern. */
+int orc_p1_assemble(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                    int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                    const int32_t* row_ptr, const int32_t* col_idx,
+                    double* K, double* M, const uint8_t* row_mask) {
+    int nv = dim + 1;
+    int64_t nnz = row_ptr[nn];
+    if (K) for (int64_t p = 0; p < nnz; p++) K[p] = 0.0;
+    if (M) for (int64_t p = 0; p < nnz; p++) M[p] = 0.0;
+    for (int64_t e = 0; e < ne; e++) {
+        int32_t vid[4];
+        int touch = 0;
+        for (int a = 0; a < nv; a++) {
+            vid[a] = elems[a * elem_ld + e];
+            if (!row_mask || row_mask[vid[a]]) touch = 1;
+        }
+        if (!touch) continue;
+        double X[16], Ke[16], Me[16];
+        for (int a = 0; a < nv; a++)
+            for (int c = 0; c < dim; c++) X[c * nv + a] = coords[c * comp_stride + (int64_t)vid[a] * node_stride];
+        orc_p1_local(dim, X, Ke, Me);
+        for (int a = 0; a < nv; a++) {
+            if (row_mask && !row_mask[vid[a]]) continue;
+            for (int b = 0; b < nv; b++) {
+                int64_t p = find_col(row_ptr, col_idx, vid[a], vid[b]);
+                if (p < 0) return -3;
+                if (K) K[p] += Ke[a * nv + b];
+                if (M) M[p] += Me[a * nv + b];
+            }
+        }
+    }
+    return ORC_OK;
+}

@@ -1,0 +1,161 @@
+"""Synthetic meshes with the shapes of the paper's workloads (no method arithmetic).
+
+Recipes (BASELINE.json configs; restated in DESIGN.md):
+
+* ``square_p1(n)`` -- unit square, n x n cells, node id = i + (n+1) j at
+  (i/n, j/n); cell (i, j) taken x-fastest, split along the SW-NE diagonal into
+  (v00, v10, v11) and (v00, v11, v01) (counter-clockwise).  Configs 1 and 4
+  (P:1082-1096 use unit-square meshes).
+* ``cube_kuhn_p1(n)`` -- unit cube, n^3 cells, node id = i + (n+1)(j + (n+1)k);
+  cell x-fastest; 6 Kuhn tetrahedra per cell, one per axis permutation p in
+  lexicographic order: v0, v0+e_p0, v0+e_p0+e_p1, v0+(1,1,1).  Config 5; the
+  node counts (2^L+1)^3 match P:1113-1125.
+* jitter: one U[-1,1) draw per node and coordinate (stream 1, index
+  v*dim + c, node-id order, drawn for every node) scaled by amp*h and applied
+  to interior nodes only, so the domain stays the exact unit square / cube.
+* ``icosphere(level)`` -- the 12-vertex icosahedron normalised to r = 1,
+  ``level`` rounds of 1 -> 4 midpoint subdivision (midpoints re-normalised to
+  r = 1 every round, new vertex ids in order of first creation while scanning
+  faces in order and edges (a,b), (b,c), (c,a)), then radius 1 + amp*U[-1,1)
+  per vertex (stream 2).  Config 3.
+"""
+import numpy as np
+
+from .rng import uniform_pm1
+
+JITTER_STREAM = 1
+RADIUS_STREAM = 2
+
+
+def square_counts(n):
+    nn = (n + 1) ** 2
+    ne = 2 * n * n
+    return nn, ne
+
+
+def cube_counts(n):
+    nn = (n + 1) ** 3
+    ne = 6 * n ** 3
+    return nn, ne
+
+
+def icosphere_counts(level):
+    f = 20 * 4 ** level
+    v = 10 * 4 ** level + 2
+    return v, f
+
+
+def _interior_mask(idx_per_axis, n):
+    m = np.ones(idx_per_axis[0].shape, dtype=bool)
+    for ia in idx_per_axis:
+        m &= (ia > 0) & (ia < n)
+    return m
+
+
+def square_p1(n, jitter=0.1, seed=0):
+    """Return (coords (2, nn) float64, elems (3, ne) int32)."""
+    n1 = n + 1
+    v = np.arange(n1 * n1, dtype=np.int64)
+    i = v % n1
+    j = v // n1
+    coords = np.empty((2, n1 * n1), dtype=np.float64)
+    coords[0] = i / n
+    coords[1] = j / n
+    if jitter:
+        r = uniform_pm1(seed, JITTER_STREAM, 2 * n1 * n1).reshape(n1 * n1, 2)
+        inner = _interior_mask((i, j), n)
+        h = 1.0 / n
+        coords[0, inner] += jitter * h * r[inner, 0]
+        coords[1, inner] += jitter * h * r[inner, 1]
+    c = np.arange(n * n, dtype=np.int64)
+    ci = c % n
+    cj = c // n
+    v00 = ci + n1 * cj
+    v10 = v00 + 1
+    v01 = v00 + n1
+    v11 = v01 + 1
+    elems = np.empty((3, 2 * n * n), dtype=np.int32)
+    elems[:, 0::2] = np.stack([v00, v10, v11])
+    elems[:, 1::2] = np.stack([v00, v11, v01])
+    return coords, elems
+
+
+_KUHN_PERMS = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+
+
+def cube_kuhn_p1(n, jitter=0.05, seed=0):
+    """Return (coords (3, nn) float64, elems (4, ne) int32)."""
+    n1 = n + 1
+    nn = n1 ** 3
+    v = np.arange(nn, dtype=np.int64)
+    i = v % n1
+    j = (v // n1) % n1
+    k = v // (n1 * n1)
+    coords = np.empty((3, nn), dtype=np.float64)
+    coords[0] = i / n
+    coords[1] = j / n
+    coords[2] = k / n
+    if jitter:
+        r = uniform_pm1(seed, JITTER_STREAM, 3 * nn).reshape(nn, 3)
+        inner = _interior_mask((i, j, k), n)
+        h = 1.0 / n
+        for c in range(3):
+            coords[c, inner] += jitter * h * r[inner, c]
+    c = np.arange(n ** 3, dtype=np.int64)
+    ci = c % n
+    cj = (c // n) % n
+    ck = c // (n * n)
+    v0 = ci + n1 * (cj + n1 * ck)
+    step = (1, n1, n1 * n1)
+    elems = np.empty((4, 6 * n ** 3), dtype=np.int32)
+    for t, p in enumerate(_KUHN_PERMS):
+        a1 = v0 + step[p[0]]
+        a2 = a1 + step[p[1]]
+        a3 = a2 + step[p[2]]
+        elems[:, t::6] = np.stack([v0, a1, a2, a3])
+    return coords, elems
+
+
+_PHI = (1.0 + 5.0 ** 0.5) / 2.0
+_ICO_V = np.array([
+    [-1, _PHI, 0], [1, _PHI, 0], [-1, -_PHI, 0], [1, -_PHI, 0],
+    [0, -1, _PHI], [0, 1, _PHI], [0, -1, -_PHI], [0, 1, -_PHI],
+    [_PHI, 0, -1], [_PHI, 0, 1], [-_PHI, 0, -1], [-_PHI, 0, 1]], dtype=np.float64)
+_ICO_F = np.array([
+    [0, 11, 5], [0, 5, 1], [0, 1, 7], [0, 7, 10], [0, 10, 11],
+    [1, 5, 9], [5, 11, 4], [11, 10, 2], [10, 7, 6], [7, 1, 8],
+    [3, 9, 4], [3, 4, 2], [3, 2, 6], [3, 6, 8], [3, 8, 9],
+    [4, 9, 5], [2, 4, 11], [6, 2, 10], [8, 6, 7], [9, 8, 1]], dtype=np.int64)
+
+
+def _normalise_rows(x):
+    return x / np.sqrt((x * x).sum(axis=1, keepdims=True))
+
+
+def icosphere(level, perturb=0.01, seed=0):
+    """Return (xyz (3, V) float64, tri (3, F) int32)."""
+    verts = _normalise_rows(_ICO_V.copy())
+    faces = _ICO_F.copy()
+    for _ in range(level):
+        nv = verts.shape[0]
+        a, b, c = faces[:, 0], faces[:, 1], faces[:, 2]
+        e = np.stack([np.stack([a, b], 1), np.stack([b, c], 1), np.stack([c, a], 1)], 1).reshape(-1, 2)
+        key = np.minimum(e[:, 0], e[:, 1]) * nv + np.maximum(e[:, 0], e[:, 1])
+        uniq, first, inv = np.unique(key, return_index=True, return_inverse=True)
+        order = np.argsort(first, kind="stable")          # unique edges by first creation
+        rank = np.empty_like(order)
+        rank[order] = np.arange(order.size)
+        mid_id = nv + rank[inv]                           # id of midpoint of each face edge
+        ue = e[first[order]]
+        mids = _normalise_rows(0.5 * (verts[ue[:, 0]] + verts[ue[:, 1]]))
+        verts = np.concatenate([verts, mids], 0)
+        m = mid_id.reshape(-1, 3)
+        ab, bc, ca = m[:, 0], m[:, 1], m[:, 2]
+        faces = np.stack([np.stack([a, ab, ca], 1), np.stack([b, bc, ab], 1),
+                          np.stack([c, ca, bc], 1), np.stack([ab, bc, ca], 1)], 1).reshape(-1, 3)
+    if perturb:
+        r = 1.0 + perturb * uniform_pm1(seed, RADIUS_STREAM, verts.shape[0])
+        verts = verts * r[:, None]
+    xyz = np.ascontiguousarray(verts.T)
+    tri = np.ascontiguousarray(faces.T.astype(np.int32))
+    return xyz, tri
