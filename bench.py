@@ -1,0 +1,476 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path (BASELINE.json metric: "3D P1 K+M assembled
+elements/s (fp64) and achieved HBM GB/s vs B200 peak").
+
+Headline workload (the configuration the metric is quoted on, configs[4]):
+3D P1 K+M assembly, unit cube 128^3 cells x 6 Kuhn tets = 12,582,912 tets,
+2,146,689 nodes, interior nodes jittered by 0.05h (seed 0).  A step is one
+fem_p1_assemble call (the fused numeric assembly: gather -> Jacobian -> det ->
+adjugate inverse -> gradients -> K_e, M_e -> CSR K and M) on the resident
+pattern / plan, which is built once per mesh by fem_p1_pattern and timed
+separately (config.pattern_ms).  `e2e` is the same metric through the public
+API from pinned host buffers: H2D of coords+elems, fem_p1_pattern (both
+phases), fem_p1_assemble, D2H of row_ptr, col_idx, K and M -- every step.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl vb|reference]
+       [--variant gather|atomic] [--quick]
+Multi-GPU (torchrun): one independent replica of the workload per rank
+("replicas only"), weak scaling, max-over-ranks time.
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "3D P1 K+M assembled elements/s (fp64)"
+UNIT = "elements/s"
+WORKLOAD5 = ("configs[4]: 3D P1 tetrahedral K+M assembly, unit cube 128^3 cells x 6 Kuhn tets "
+             "(12,582,912 tets, 2,146,689 nodes), interior vertices jittered 0.05h seed 0, CSR K and M")
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md, MEASURED_PEAKS.json absent)"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index=0, period=0.01):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover - no NVML
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def alg_bytes_assembly(dim, nn, ne, nnz):
+    """ALG bytes: coords read + connectivity read + K, M written once."""
+    return nn * dim * 8 + ne * (dim + 1) * 4 + 2 * nnz * 8
+
+
+def design_bytes_assembly(dim, nn, ne, nnz):
+    """ALG + the nv^2 int32 element-to-nnz scatter map of the north-star design."""
+    return alg_bytes_assembly(dim, nn, ne, nnz) + ne * (dim + 1) ** 2 * 4
+
+
+def load_traffic(kernel_key):
+    """dram bytes per launch from the committed ncu summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["kernels"][kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------- vb arm
+def run_vb(args):
+    import torch
+    import torch.distributed as tdist
+
+    import synth
+    from paper_2404_16039_b200 import vb
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    peak, peak_src = peaks()
+    mode = vb.VB_ASSEMBLE_GATHER if args.variant == "gather" else vb.VB_ASSEMBLE_ATOMIC
+
+    coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    cd = torch.from_numpy(coords).to(dev)
+    ed = torch.from_numpy(elems).to(dev)
+
+    # plan (pattern + scatter/gather plans), timed once separately
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = vb.P1Plan(ed, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC), gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+    torch.cuda.synchronize()
+    pattern_ms = (time.perf_counter() - t0) * 1e3
+    nnz = plan.nnz
+    K = torch.empty(nnz, dtype=torch.float64, device=dev)
+    M = torch.empty(nnz, dtype=torch.float64, device=dev)
+
+    def step():
+        vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if ws > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if ws > 1:
+        tdist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = [a.elapsed_time(b) for a, b in ev]
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * ne * args.steps / (total_ms * 1e-3)
+
+    avg_launch_ms = statistics.mean(launch_ms)
+    alg = alg_bytes_assembly(dim, nn, ne, nnz)
+    achieved = alg / (avg_launch_ms * 1e-3) / 1e9
+    kname = "assemble_gather_k<3>" if mode == vb.VB_ASSEMBLE_GATHER else "assemble_atomic_k<3>"
+    traffic = load_traffic(kname)
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic,
+            "kernel": kname, "bytes_model": "ALG: coords read + elems read + K,M written once "
+                                              "(%.1f MB/launch = %.1f B/tet)" % (alg / 1e6, alg / ne),
+            "peak_source": peak_src, "launch_ms_avg": round(avg_launch_ms, 5),
+            "design_bytes_frac": round(design_bytes_assembly(dim, nn, ne, nnz) / (avg_launch_ms * 1e-3) / 1e9 / peak, 4)}
+
+    # e2e through the public API from pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hc = torch.from_numpy(coords).pin_memory()
+        he = torch.from_numpy(elems).pin_memory()
+        n_e2e = max(1, min(args.steps, args.e2e_steps))
+        hK = torch.empty(nnz, dtype=torch.float64).pin_memory()
+        hM = torch.empty(nnz, dtype=torch.float64).pin_memory()
+        hrp = torch.empty(nn + 1, dtype=torch.int32).pin_memory()
+        hci = torch.empty(nnz, dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            c2 = hc.to(dev, non_blocking=True)
+            e2 = he.to(dev, non_blocking=True)
+            p2 = vb.P1Plan(e2, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
+                           gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+            K2, M2, _, _ = vb.fem_p1_assemble(c2, e2, p2, mode=mode)
+            hrp.copy_(p2.row_ptr, non_blocking=True)
+            hci.copy_(p2.col_idx, non_blocking=True)
+            hK.copy_(K2, non_blocking=True)
+            hM.copy_(M2, non_blocking=True)
+            torch.cuda.synchronize()
+
+        e2e_step()
+        if ws > 1:
+            tdist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a.elapsed_time(b)
+        if ws > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": ws * ne * n_e2e / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": coords.nbytes + elems.nbytes,
+               "d2h_bytes_per_step": (nn + 1) * 4 + nnz * 4 + 2 * nnz * 8,
+               "steps": n_e2e, "ms_per_step": e2e_ms / n_e2e,
+               "includes": "H2D coords+elems, fem_p1_pattern (count+fill), fem_p1_assemble, D2H row_ptr/col_idx/K/M"}
+
+    secondary = None
+    if rank == 0 and not args.quick:
+        secondary = run_secondary(args, dev, peak, plan, cd, ed, coords, elems)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(coords, elems, args.cpu_layers)
+
+    if ws > 1:
+        tdist.destroy_process_group()
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded Kuhn-cube mesh, synth/)",
+        "config": {"workload": WORKLOAD5, "variant": args.variant,
+                   "timed": "fem_p1_assemble per step (numeric K+M assembly on the resident plan)",
+                   "pattern_ms": round(pattern_ms, 3), "nnz": nnz, "ne": ne, "nn": nn,
+                   "l2": "no flush: every step streams %.0f MB (> 126 MB L2)" % (alg / 1e6),
+                   "parallelism": "replicas" if ws > 1 else "single GPU"},
+        "roofline": roof, "gpu_launches": args.steps * (1 if mode == vb.VB_ASSEMBLE_GATHER else 2),
+        "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
+    }
+    if secondary is not None:
+        line["secondary"] = secondary
+    print(json.dumps(line), flush=True)
+
+
+def time_kernel(fn, reps, flush=None):
+    """Median device time (ms) of fn() over reps, L2 flushed before each rep."""
+    import torch
+    stream = torch.cuda.current_stream()
+    out = []
+    for _ in range(3):
+        fn()
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        fn()
+        b.record(stream)
+        b.synchronize()
+        out.append(a.elapsed_time(b))
+    return statistics.median(out), min(out)
+
+
+def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
+    """Every other §8(a) row on its BASELINE config, L2 flushed between reps."""
+    import torch
+
+    import synth
+    from paper_2404_16039_b200 import vb
+    flush = torch.empty(2 * 132644864 // 4, dtype=torch.float32, device=dev)   # 2x L2
+    res = []
+
+    def rec(name, units, unit_name, nbytes, t):
+        med, mn = t
+        res.append({"name": name, "ms": round(med, 5), "ms_min": round(mn, 5),
+                    unit_name + "_per_s": units / (med * 1e-3), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1),
+                    "frac": round(nbytes / (med * 1e-3) / 1e9 / peak, 4)})
+
+    # other assembly variant on config 5
+    nn5, ne5 = coords5.shape[1], elems5.shape[1]
+    other = "atomic" if args.variant == "gather" else "gather"
+    p_other = vb.P1Plan(ed5, nn5, scatter_map=(other == "atomic"), gather_plan=(other == "gather"))
+    mo = vb.VB_ASSEMBLE_ATOMIC if other == "atomic" else vb.VB_ASSEMBLE_GATHER
+    K = torch.empty(p_other.nnz, dtype=torch.float64, device=dev)
+    M = torch.empty(p_other.nnz, dtype=torch.float64, device=dev)
+    rec("config5 assembly variant=%s" % other, ne5, "elements", alg_bytes_assembly(3, nn5, ne5, p_other.nnz),
+        time_kernel(lambda: vb.fem_p1_assemble(cd5, ed5, p_other, mode=mo, K=K, M=M), 10))
+    del p_other, K, M
+    # pattern build on config 5 (one-time plan)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        vb.P1Plan(ed5, nn5, scatter_map=True, gather_plan=True)
+    torch.cuda.synchronize()
+    res.append({"name": "config5 fem_p1_pattern (count+fill, elem2nnz + gather plan)",
+                "ms": round((time.perf_counter() - t0) * 1e3 / 2, 3)})
+    # config 4: 2D at scale
+    c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
+    cd4, ed4 = torch.from_numpy(c4).to(dev), torch.from_numpy(e4).to(dev)
+    p4 = vb.P1Plan(ed4, c4.shape[1])
+    K4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
+    M4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
+    for name, mode in (("gather", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+        rec("config4 2D assembly variant=%s" % name, e4.shape[1], "elements",
+            alg_bytes_assembly(2, c4.shape[1], e4.shape[1], p4.nnz),
+            time_kernel(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode, K=K4, M=M4), 10))
+    del p4, K4, M4, cd4, ed4
+    # config 1: latency only
+    c1, e1 = synth.square_p1(32, jitter=0.1, seed=0)
+    cd1, ed1 = torch.from_numpy(c1).to(dev), torch.from_numpy(e1).to(dev)
+    p1 = vb.P1Plan(ed1, c1.shape[1])
+    rec("config1 2D 32x32 assembly (latency-bound)", e1.shape[1], "elements",
+        alg_bytes_assembly(2, c1.shape[1], e1.shape[1], p1.nnz),
+        time_kernel(lambda: vb.fem_p1_assemble(cd1, ed1, p1), 20))
+    # config 3: surface geometry
+    xyz, tri = synth.icosphere(10, perturb=0.01, seed=0)
+    xd, td = torch.from_numpy(xyz).to(dev), torch.from_numpy(tri).to(dev)
+    out = vb.vb_tri_surface(xd, td)
+    F, V = tri.shape[1], xyz.shape[1]
+    rec("config3 tri_surface (n, nhat, area, volume)", F, "triangles", F * (12 + 56) + V * 24,
+        time_kernel(lambda: vb.vb_tri_surface(xd, td, out=out, work=out["work"]), 10, flush))
+    del xd, td, out
+    # config 2: page sweep
+    N = 1 << 20
+    for n in (2, 3, 4):
+        A = torch.from_numpy(synth.normal_pages(n, n, N, stream=10)).to(dev)
+        B = torch.from_numpy(synth.normal_pages(n, n, N, stream=11)).to(dev)
+        Z = torch.empty_like(A)
+        for tag, tX, tY in (("A*B", 0, 0), ("A*B^T", 0, 1), ("A^T*B", 1, 0)):
+            rec("config2 mtimes %s n=%d" % (tag, n), N, "pages", 24 * n * n * N,
+                time_kernel(lambda: vb.vb_page_mtimes(A, B, tX, tY, Z=Z), 20, flush))
+        rec("config2 transpose n=%d" % n, N, "pages", 16 * n * n * N,
+            time_kernel(lambda: vb.vb_page_transpose(A, Z=Z), 20, flush))
+        d = torch.empty(N, dtype=torch.float64, device=dev)
+        rec("config2 det n=%d" % n, N, "pages", (n * n + 1) * 8 * N,
+            time_kernel(lambda: vb.vb_page_det(A, det=d), 20, flush))
+        X, _ = synth.inverse_pages(n, N, seed=0)
+        Xd = torch.from_numpy(X).to(dev)
+        rec("config2 inv+det n=%d" % n, N, "pages", (2 * n * n + 1) * 8 * N,
+            time_kernel(lambda: vb.vb_page_inv(Xd, Xinv=Z, det=d), 20, flush))
+        del A, B, Z, Xd
+    a3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=60)).to(dev)
+    b3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=61)).to(dev)
+    c3 = torch.empty_like(a3)
+    rec("config2 cross", N, "pages", 72 * N, time_kernel(lambda: vb.vb_page_cross(a3, b3, Cout=c3), 20, flush))
+    return res
+
+
+# ---------------------------------------------------------------------- CPU oracle
+def cpu_baseline(coords, elems, layers, plan_cache=None):
+    """The oracle as it stands (single thread, C, -O2) on a bounded sample of the
+    same workload: the first `layers` z-layers of cells of the config-5 mesh.
+    Like the GPU arm, value = numeric K+M assembly on a resident pattern; the
+    oracle's pattern build is timed and reported beside it."""
+    import oracle
+    nn = coords.shape[1]
+    ne_s = layers * 128 * 128 * 6
+    el = np.ascontiguousarray(elems[:, :ne_s])
+    t0 = time.perf_counter()
+    if plan_cache is not None and plan_cache.get("layers") == layers:
+        rp, ci = plan_cache["rp"], plan_cache["ci"]
+    else:
+        rp, ci = oracle.p1_pattern(el, nn)
+        if plan_cache is not None:
+            plan_cache.update(layers=layers, rp=rp, ci=ci, t=time.perf_counter() - t0)
+    t_pat = plan_cache["t"] if plan_cache is not None else time.perf_counter() - t0
+    t1 = time.perf_counter()
+    oracle.p1_assemble(coords, el, rp, ci)
+    t2 = time.perf_counter()
+    return {"value": ne_s / (t2 - t1), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "first %d of 128 z-layers of the config-5 mesh (%d tets): K+M assembly %.3f s on the "
+                      "oracle's pattern (built in %.3f s, not in value); single-threaded C (oracle/oracle.c, "
+                      "gcc -O2 -ffp-contract=off)" % (layers, ne_s, t2 - t1, t_pat),
+            "host_cpu": host_cpu(), "seconds": t2 - t1}
+
+
+def host_cpu():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + " (nproc %d)" % os.cpu_count()
+    except Exception:
+        pass
+    return "unknown (nproc %s)" % os.cpu_count()
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) on the host
+    cores, rank 0 only.  Each step assembles a bounded sample of the config-5
+    workload (whole z-layers), sized from a one-layer calibration so that the
+    whole --steps/--warmup run takes about --ref-budget seconds."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import synth
+    coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
+    cal = cpu_baseline(coords, elems, 1)
+    per_step = args.ref_budget / max(1, args.steps + args.warmup)
+    layers = int(max(1, min(128, round(per_step / max(cal["seconds"], 1e-6)))))
+    cache = {}
+    times = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(coords, elems, layers, cache)
+        if i >= args.warmup:
+            times.append(cb["seconds"])
+    ne_s = layers * 128 * 128 * 6
+    total = sum(times)
+    value = ne_s * len(times) / total
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Kuhn-cube mesh)",
+            "config": {"workload": WORKLOAD5, "sample_per_step": "first %d z-layers (%d tets)" % (layers, ne_s),
+                       "timed": "oracle K+M assembly per step on a resident pattern (as the GPU arm)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": cb["sample"],
+                             "host_cpu": cb["host_cpu"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="vb", choices=["vb", "reference"])
+    ap.add_argument("--variant", default="gather", choices=["gather", "atomic"])
+    ap.add_argument("--quick", action="store_true", help="headline only (no secondary rows)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-layers", type=int, default=8)
+    ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_vb(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,216 @@
+/*
+ * vb.h -- C ABI of the B200-native page-wise fp64 linear algebra and P1 FEM
+ * assembly library (libvb.so), the hot path of arXiv 2404.16039.
+ *
+ * Citation keys: P:n = PAPER.md line n (arXiv 2404.16039 LaTeX source);
+ * S:n = SPEC.md line n; SURVEY.md §8 rows a1..a17.
+ *
+ * ------------------------------------------------------------------ conventions
+ * Memory.  Every array argument is a DEVICE pointer owned by the caller.  The
+ *   library never allocates device memory, never frees, and keeps no pointer
+ *   after a call returns.  Scratch space is passed as (work, work_bytes): call
+ *   once with work == NULL to query *work_bytes, then again with a buffer of at
+ *   least that size (16-byte aligned).
+ * Streams.  All work is enqueued on `stream` (a cudaStream_t; NULL = legacy
+ *   default stream).  Calls return after enqueueing, except where a host
+ *   synchronisation is documented (fem_p1_pattern's count phase reads nnz).
+ *   Calls on different streams with disjoint buffers are thread-safe.
+ * Page layout (SURVEY B2, P:248-266 with the index space W as the page index,
+ *   S:32): a batch of N pages of r x c matrices is stored struct-of-arrays:
+ *   entry (i, j) of page k is at  p[(i + j*r) * ld + k]  (column-major entry
+ *   order as in MATLAB, one contiguous plane of N values per entry), ld >= N.
+ *   ld == 0 is the copy map eq:copy: ONE r x c object stored
+ *   column-major and contiguous (p[i + j*r]) is used for every page -- this is
+ *   how amsm/amsv/smamt/svamt broadcast single objects.
+ *   A contiguous torch tensor of shape (c, r, N) is a valid operand, ld = N.
+ *   Fast paths need 16-byte aligned planes and even ld; other inputs take a
+ *   scalar path of the same kernels (no other backend exists).
+ * Outputs are overwritten, never accumulated, and must not alias any input.
+ * Indices are 0-based int32 (MATLAB is 1-based).  Vertex indices
+ *   out of [0, nn) are a precondition violation and are not checked on the
+ *   hot path.
+ * Errors.  Argument/shape errors return a negative vb_status synchronously
+ *   and set a thread-local message (vb_last_error) naming the offending
+ *   argument.  Numerical singularity is NOT an error (inverse_W is only
+ *   defined where det != 0): results follow IEEE arithmetic and
+ *   are flagged where documented.  VB_ERR_CUDA reports a launch failure.
+ */
+#ifndef VB_H_
+#define VB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define VB_API __attribute__((visibility("default")))
+#else
+#define VB_API
+#endif
+
+typedef struct CUstream_st* vb_stream_t; /* == cudaStream_t */
+
+typedef enum {
+    VB_OK = 0,
+    VB_ERR_ARG = -1,         /* NULL pointer, negative size, bad flag, bad ld   */
+    VB_ERR_DIM = -2,         /* inner dimensions disagree / page not square     */
+    VB_ERR_UNSUPPORTED = -3, /* page size outside 1..4, dim outside {2,3}, ...  */
+    VB_ERR_OVERFLOW = -4,    /* a count does not fit int32 (nnz, ne*nv*nv, ...) */
+    VB_ERR_WORKSPACE = -5,   /* work buffer missing or smaller than queried     */
+    VB_ERR_CUDA = -6         /* a CUDA launch or copy failed                    */
+} vb_status;
+
+/* Message of the last failing call on this host thread ("" if none). */
+VB_API const char* vb_last_error(void);
+/* ABI version, currently 1. */
+VB_API int vb_abi_version(void);
+
+/* ---------------------------------------------------------- a1 page product
+ * Z_k = op(X_k) * op(Y_k) for k = 0..npages-1, op(A) = A or A^T by the flag.
+ * Page-wise matrix multiplication eq:pagewisemultGeneral / layeredMultiplication
+ * = MATLAB pagemtimes(X, tX, Y, tY).  Every library
+ * product of P:380-411 is one call: amtam = (tX=1, tY=0) (reading B1),
+ * avtam/avtav = X of r x 1 pages with tX=1, astam = X of 1 x 1 pages,
+ * amsm/amsv = ldy 0, smamt = ldx 0 with tY=1, svamt = ldx 0, tX=1, tY=1.
+ * xrows/xcols, yrows/ycols describe the STORED X, Y (each 1..4).
+ * Z is (rows of op(X)) x (cols of op(Y)), ldz >= npages.
+ * Errors: VB_ERR_DIM if the inner dimensions of op(X), op(Y) differ;
+ * VB_ERR_UNSUPPORTED if any dimension is outside 1..4; VB_ERR_ARG for ld < npages
+ * (other than 0 on an input) or NULL pointers with npages > 0. npages == 0 is a no-op. */
+VB_API vb_status vb_page_mtimes(int64_t npages,
+                         const double* X, int xrows, int xcols, int64_t ldx, int transX,
+                         const double* Y, int yrows, int ycols, int64_t ldy, int transY,
+                         double* Z, int64_t ldz, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a2 page transpose
+ * Z_k = X_k^T (layeredTransposeHom/Ten P:268-279; amt = pagetranspose P:415).
+ * X is rows x cols (1..4 each), Z is cols x rows.  Exact (a permutation of
+ * planes).  ldx may be 0 (broadcast). */
+VB_API vb_status vb_page_transpose(int64_t npages, const double* X, int rows, int cols, int64_t ldx,
+                            double* Z, int64_t ldz, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a3 page determinant
+ * det[k] = det X_k for n x n pages, n in 1..4 (layeredDeterminant P:331-336;
+ * amdet P:418-420).  Closed forms: n<=3 cofactor expansion, n=4 Laplace
+ * expansion by the 2x2 minors of rows (0,1) and (2,3).  det is one plane of
+ * npages values. */
+VB_API vb_status vb_page_det(int64_t npages, int n, const double* X, int64_t ldx,
+                      double* det, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a4 page inverse
+ * Xinv_k = adj(X_k) / det X_k (layeredInverse P:338-352; aminv P:414, which
+ * also returns the determinant), n in 1..4, one reciprocal per page.
+ * det (nullable) receives the signed determinants (reading B6).
+ * first_singular (nullable, DEVICE int64 scalar): set in-stream to the
+ * smallest page index k with |det X_k| <= sing_tol * ||X_k||_inf^n, or to
+ * npages if there is none (SPEC S:141 uses sing_tol = 1e-14).  Singular pages
+ * still produce IEEE results (inf/nan). */
+VB_API vb_status vb_page_inv(int64_t npages, int n, const double* X, int64_t ldx,
+                      double* Xinv, int64_t ldinv, double* det,
+                      int64_t* first_singular, double sing_tol, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a5 page cross product
+ * C_k = A_k x B_k for 3-vector pages (3 x 1; BASELINE.json north_star; the
+ * cofactor columns of eq:transformNormal P:354-374 are such products). */
+VB_API vb_status vb_page_cross(int64_t npages, const double* A, int64_t lda, const double* B, int64_t ldb,
+                        double* C, int64_t ldc, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a7 gather (coords3D)
+ * create_coords3D (Code coords3D): coords3D is a dim x nv page
+ * array (ld = ne) with column a of page e = coordinates of vertex elems[a][e];
+ * vectors3D (nullable) is dim x (nv-1) with column a = x_a - x_{nv-1}
+ * (vectors from the LAST local node).  coords are addressed
+ * coords[c*comp_stride + v*node_stride] (SoA: node_stride 1, comp_stride nn;
+ * AoS/padded AoS: node_stride dim or 4, comp_stride 1).  elems[a*elem_ld + e].
+ * dim in {2,3}, nv in 2..4. */
+VB_API vb_status vb_create_coords3D(int dim, int nv, int64_t ne,
+                             const double* coords, int64_t node_stride, int64_t comp_stride,
+                             const int32_t* elems, int64_t elem_ld,
+                             double* coords3D, double* vectors3D, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a6 surface geometry
+ * For each triangle f = (a, b, c) (tri[v*tri_ld + f], v = 0..2) of a closed
+ * surface with vertex coordinates xyz (strided as above):
+ *   n_f = (b-a) x (c-a)        (3 planes, ld = nf; nullable)
+ *   nhat_f = n_f / |n_f|       (3 planes, ld = nf; nullable)
+ *   area_f = |n_f| / 2         (1 plane; nullable)
+ *   *volume = sum_f (1/6) a . n_f   (DEVICE scalar, nullable): the divergence
+ *   theorem with F = x/3 (surf_int).  The sum uses a fixed-shape
+ *   tree (per-block then one block), so it is bitwise reproducible run to run.
+ * Requires work (query with work == NULL) when volume != NULL. */
+VB_API vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, int64_t nverts,
+                         const double* xyz, int64_t node_stride, int64_t comp_stride,
+                         double* n, double* nhat, double* area, double* volume,
+                         void* work, size_t* work_bytes, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a14/a15 pattern + plans
+ * Topological CSR pattern of K = sparse(X3D(:), Y3D(:), K3D(:), nn, nn)
+ * (reading B12: every pair (i, j) of vertices sharing an element,
+ * diagonal included, kept even where the value cancels), columns ascending.
+ * dim in {2,3} (nv = dim+1 vertices per element), elems[a*elem_ld + e].
+ *
+ * Count phase (col_idx == NULL): writes row_ptr[0..nn], then SYNCHRONISES the
+ *   stream and stores nnz in *nnz_out (host int64).
+ * Fill phase (col_idx != NULL, col_cap >= nnz, row_ptr from the count phase;
+ *   also synchronises the stream, to check col_cap and the row-length flags):
+ *   writes col_idx[0..nnz) and the optional scatter plans:
+ *   elem2nnz (nullable): int32, nv*nv planes of ne: plane (a*nv + b) entry e is
+ *     the position in col_idx of column elems[b][e] in row elems[a][e]
+ *     (the scatter map of VB_ASSEMBLE_ATOMIC);
+ *   node_elem_ptr (nullable, nn+1 int32) / node_elem (nv*ne int32) /
+ *     node_elem_slot (nv*ne uint32): the gather plan of VB_ASSEMBLE_GATHER:
+ *     for row v, entries node_elem_ptr[v]..node_elem_ptr[v+1]-1 list the
+ *     incidences (e, a) with elems[a][e] == v, packed e*4 + a, ascending e;
+ *     node_elem_slot packs, in byte b, the in-row offset of column elems[b][e]
+ *     in row v (so rows must have <= 255 entries; VB_ERR_UNSUPPORTED otherwise).
+ * Errors: VB_ERR_OVERFLOW if nnz >= 2^31 or ne*nv*nv >= 2^31 or ne >= 2^29;
+ *   VB_ERR_UNSUPPORTED if a row has more than 4096 distinct columns;
+ *   VB_ERR_ARG if col_cap < nnz.  Deterministic: identical outputs every run. */
+VB_API vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne,
+                         const int32_t* elems, int64_t elem_ld,
+                         void* work, size_t* work_bytes,
+                         int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                         int32_t* elem2nnz,
+                         int32_t* node_elem_ptr, int32_t* node_elem, uint32_t* node_elem_slot,
+                         int64_t* nnz_out, vb_stream_t stream);
+
+/* ---------------------------------------------------------- a7..a17 assembly
+ * Global P1 stiffness and mass matrices with c_K = c_M = 1 (eq:K_M P:967-975,
+ * stiffness_matrixP1 P:978-1004, mass_matrixP1 P:1007), written
+ * as CSR values on the pattern of fem_p1_pattern.  Per element:
+ *   tjac = D X^T  (J[r][c] = x_{r+1}[c] - x_0[c]),  |T| = |det tjac| / d!,
+ *   G = tjac^{-1} D (D = [-1 | I]),  K_e = |T| G^T G,
+ *   M_e = |T| / ((d+1)(d+2)) (1 + delta_ab).
+ * mode VB_ASSEMBLE_ATOMIC: one thread per element, K_e/M_e added into
+ *   K_vals/M_vals through elem2nnz with fp64 atomics (targets are zero-filled
+ *   by the call); summation order unspecified (reading B13).
+ * mode VB_ASSEMBLE_GATHER: deterministic segmented reduction: one thread per
+ *   row v sums the contributions of its incidences in ascending element order
+ *   (the oracle's order) in on-chip memory and writes each CSR entry once; no
+ *   atomics, no zero-fill; needs node_elem_ptr/node_elem/node_elem_slot.
+ *   Bitwise reproducible.
+ * K_vals / M_vals (nnz each) are nullable (skip that matrix).
+ * K_local / M_local (nullable): K3D / M3D page arrays (nv x nv pages, ld = ne),
+ *   the second outputs of stiffness_matrixP1 / mass_matrixP1.
+ * coords strided as in vb_create_coords3D.
+ * Degenerate elements (det = 0) propagate inf/nan. */
+#define VB_ASSEMBLE_ATOMIC 0
+#define VB_ASSEMBLE_GATHER 1
+VB_API vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne,
+                          const double* coords, int64_t node_stride, int64_t comp_stride,
+                          const int32_t* elems, int64_t elem_ld,
+                          const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
+                          const int32_t* elem2nnz,
+                          const int32_t* node_elem_ptr, const int32_t* node_elem,
+                          const uint32_t* node_elem_slot,
+                          double* K_vals, double* M_vals,
+                          double* K_local, double* M_local,
+                          int mode, vb_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VB_H_ */

@@ -1,0 +1,147 @@
+// ABI glue: error reporting, device queries and the device-wide scan used by
+// the pattern build ("built once on the GPU by sort/unique/scan").
+#include <cstdarg>
+#include <cstring>
+
+#include "vb_internal.cuh"
+
+namespace vb {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+void clear_error() { g_err[0] = 0; }
+
+int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+        cached[dev] = n;
+    }
+    return cached[dev];
+}
+
+// ------------------------------------------------------------------ scan
+constexpr int SCAN_THREADS = 256;
+constexpr int SCAN_ITEMS = 16;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long* sh) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    long long t = 0;
+    if (threadIdx.x < 32) {
+        t = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    }
+    __syncthreads();
+    return t;  // valid in thread 0
+}
+
+// exclusive scan of v across the block; returns the block total in *tot
+__device__ __forceinline__ long long block_exscan_ll(long long v, long long* sh, long long* tot) {
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    long long x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, x, o);
+        if (l >= o) x += y;
+    }
+    if (l == 31) sh[w] = x;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int nw = blockDim.x >> 5;
+        long long s = (l < nw) ? sh[l] : 0;
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, s, o);
+            if (l >= o) s += y;
+        }
+        sh[32 + l] = s;  // inclusive scan of warp sums
+    }
+    __syncthreads();
+    long long warp_off = (w > 0) ? sh[32 + w - 1] : 0;
+    *tot = sh[32 + (blockDim.x >> 5) - 1];
+    __syncthreads();
+    return warp_off + x - v;
+}
+
+__global__ void scan_reduce_k(const int32_t* __restrict__ in, int64_t n, long long* __restrict__ part) {
+    __shared__ long long sh[64];
+    int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+    long long s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+        int64_t idx = base + (int64_t)i * SCAN_THREADS + threadIdx.x;
+        if (idx < n) s += in[idx];
+    }
+    long long t = block_sum_ll(s, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
+__global__ void scan_partials_k(long long* __restrict__ part, int64_t nb, int64_t* __restrict__ total) {
+    __shared__ long long sh[64];
+    long long carry = 0;
+    for (int64_t b0 = 0; b0 < nb; b0 += blockDim.x) {
+        int64_t i = b0 + threadIdx.x;
+        long long v = (i < nb) ? part[i] : 0;
+        long long tot;
+        long long ex = block_exscan_ll(v, sh, &tot);
+        if (i < nb) part[i] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0 && total) *total = carry;
+}
+
+__global__ void scan_down_k(const int32_t* __restrict__ in, int32_t* __restrict__ out, int64_t n,
+                            const long long* __restrict__ part) {
+    __shared__ long long sh[64];
+    int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    int32_t v[SCAN_ITEMS];
+    long long s = 0;
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+        int64_t idx = base + i;
+        v[i] = (idx < n) ? in[idx] : 0;
+        s += v[i];
+    }
+    long long tot;
+    long long off = part[blockIdx.x] + block_exscan_ll(s, sh, &tot);
+#pragma unroll
+    for (int i = 0; i < SCAN_ITEMS; i++) {
+        int64_t idx = base + i;
+        if (idx < n) out[idx] = (int32_t)off;
+        off += v[i];
+    }
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = (int32_t)(part[blockIdx.x] + tot);
+}
+
+size_t scan_tmp_bytes(int64_t n) {
+    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb < 1) nb = 1;
+    return (size_t)(nb * sizeof(long long) + 256) & ~(size_t)255;
+}
+
+vb_status exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* tmp, cudaStream_t s,
+                             int64_t* total_dev) {
+    int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (nb < 1) nb = 1;
+    long long* part = reinterpret_cast<long long*>(tmp);
+    scan_reduce_k<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, n, part);
+    scan_partials_k<<<1, 1024, 0, s>>>(part, nb, total_dev);
+    scan_down_k<<<(unsigned)nb, SCAN_THREADS, 0, s>>>(in, out, n, part);
+    return launch_check("exclusive_scan");
+}
+
+}  // namespace vb
+
+extern "C" const char* vb_last_error(void) { return vb::g_err; }
+extern "C" int vb_abi_version(void) { return 1; }

@@ -1,0 +1,307 @@
+// a14/a15: topological CSR pattern of sparse(X3D(:),Y3D(:),...)
+// and the two scatter plans, built on the GPU without a global sort:
+//   1. node degree histogram, exclusive scan, bucket fill -> node->element
+//      incidence lists (packed e*4+a), each list sorted ascending (determinism);
+//   2. one thread per row builds the sorted unique column set of its row from
+//      the vertices of its incident elements in a per-thread shared-memory list
+//      (rows longer than ROW_CAP go to a single-thread fallback with a
+//      4096-entry list); row lengths -> scan -> row_ptr;
+//   3. fill: the same per-row sets are written to col_idx, and every incidence
+//      (e, a) of row v records the in-row position of each of its element's
+//      vertices: elem2nnz (atomic scatter plan) and node_elem_slot (gather plan).
+#include "vb_internal.cuh"
+
+namespace vb {
+namespace {
+
+constexpr int PAT_BLOCK = 128;
+constexpr int ROW_CAP = 64;       // per-thread sorted unique list (fast path)
+constexpr int ROW_CAP_BIG = 4096; // single-thread fallback list
+constexpr int FLAG_OVERFLOW_ROWS = 0;  // number of rows that took the fallback
+constexpr int FLAG_TOO_LONG = 1;       // a row exceeded ROW_CAP_BIG
+constexpr int FLAG_SLOT_RANGE = 2;     // a row had > 255 entries while slots requested
+
+__global__ void degree_k(int64_t ne, int nv, const int32_t* __restrict__ elems, int64_t eld, int32_t* __restrict__ deg) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride)
+        for (int a = 0; a < nv; a++) atomicAdd(deg + elems[a * eld + e], 1);
+}
+
+__global__ void bucket_fill_k(int64_t ne, int nv, const int32_t* __restrict__ elems, int64_t eld,
+                              int32_t* __restrict__ cursor, int32_t* __restrict__ node_elem) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride)
+        for (int a = 0; a < nv; a++) {
+            int pos = atomicAdd(cursor + elems[a * eld + e], 1);
+            node_elem[pos] = (int32_t)(e * 4 + a);
+        }
+}
+
+// insertion sort of each node's incidence list (ascending e, hence ascending e*4+a)
+__global__ void sort_incidences_k(int64_t nn, const int32_t* __restrict__ nptr, int32_t* __restrict__ node_elem) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
+        int lo = nptr[v], hi = nptr[v + 1];
+        for (int i = lo + 1; i < hi; i++) {
+            int32_t x = node_elem[i];
+            int j = i - 1;
+            while (j >= lo && node_elem[j] > x) {
+                node_elem[j + 1] = node_elem[j];
+                j--;
+            }
+            node_elem[j + 1] = x;
+        }
+    }
+}
+
+// sorted-unique insertion into a list with element stride `st`; returns false on overflow
+__device__ __forceinline__ int lower_bound_s(const int32_t* L, int st, int cnt, int32_t w) {
+    int lo = 0, hi = cnt;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (L[mid * st] < w) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ bool insert_unique(int32_t* L, int st, int& cnt, int cap, int32_t w) {
+    int pos = lower_bound_s(L, st, cnt, w);
+    if (pos < cnt && L[pos * st] == w) return true;
+    if (cnt == cap) return false;
+    for (int i = cnt; i > pos; i--) L[i * st] = L[(i - 1) * st];
+    L[pos * st] = w;
+    cnt++;
+    return true;
+}
+
+// Build row v's sorted unique column list into L (stride st, capacity cap).
+// Returns the count, or -1 on overflow.
+__device__ int build_row(int64_t v, int nv, const int32_t* __restrict__ elems, int64_t eld,
+                         const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
+                         int32_t* L, int st, int cap) {
+    int cnt = 0;
+    int lo = nptr[v], hi = nptr[v + 1];
+    for (int i = lo; i < hi; i++) {
+        int32_t ea = node_elem[i];
+        int64_t e = ea >> 2;
+        for (int b = 0; b < nv; b++)
+            if (!insert_unique(L, st, cnt, cap, elems[b * eld + e])) return -1;
+    }
+    return cnt;
+}
+
+// write col_idx and the plans for row v whose list L (stride st) has cnt entries
+__device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* __restrict__ elems, int64_t eld,
+                         const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
+                         const int32_t* L, int st, const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
+                         int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots, int* flags) {
+    int32_t base = row_ptr[v];
+    for (int i = 0; i < cnt; i++) col_idx[base + i] = L[i * st];
+    if (!elem2nnz && !slots) return;
+    if (slots && cnt > 255) atomicExch(flags + FLAG_SLOT_RANGE, 1);
+    int lo = nptr[v], hi = nptr[v + 1];
+    for (int i = lo; i < hi; i++) {
+        int32_t ea = node_elem[i];
+        int64_t e = ea >> 2;
+        int a = ea & 3;
+        uint32_t packed = 0;
+        for (int b = 0; b < nv; b++) {
+            int pos = lower_bound_s(L, st, cnt, elems[b * eld + e]);
+            if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
+            packed |= (uint32_t)(pos & 0xff) << (8 * b);
+        }
+        if (slots) slots[i] = packed;
+    }
+}
+
+__global__ void __launch_bounds__(PAT_BLOCK) row_count_k(int64_t nn, int nv, const int32_t* __restrict__ elems,
+                                                         int64_t eld, const int32_t* __restrict__ nptr,
+                                                         const int32_t* __restrict__ node_elem,
+                                                         int32_t* __restrict__ row_len, int32_t* __restrict__ ovf_list,
+                                                         int* flags) {
+    __shared__ int32_t Ls[ROW_CAP * PAT_BLOCK];
+    int32_t* L = Ls + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
+        int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, PAT_BLOCK, ROW_CAP);
+        if (cnt < 0) {
+            int k = atomicAdd(flags + FLAG_OVERFLOW_ROWS, 1);
+            ovf_list[k] = (int32_t)v;
+            cnt = 0;  // fixed by the fallback
+        }
+        row_len[v] = cnt;
+    }
+}
+
+// fallback for rows with more than ROW_CAP columns: one thread per row, big list
+__global__ void row_count_big_k(int nv, const int32_t* __restrict__ elems, int64_t eld, const int32_t* __restrict__ nptr,
+                                const int32_t* __restrict__ node_elem, int32_t* __restrict__ row_len,
+                                const int32_t* __restrict__ ovf_list, int* flags) {
+    __shared__ int32_t L[ROW_CAP_BIG];
+    int n_ovf = flags[FLAG_OVERFLOW_ROWS];
+    for (int k = blockIdx.x; k < n_ovf; k += gridDim.x) {
+        if (threadIdx.x == 0) {
+            int64_t v = ovf_list[k];
+            int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, 1, ROW_CAP_BIG);
+            if (cnt < 0) { atomicExch(flags + FLAG_TOO_LONG, 1); cnt = 0; }
+            row_len[v] = cnt;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(PAT_BLOCK) row_fill_k(int64_t nn, int64_t ne, int nv, const int32_t* __restrict__ elems,
+                                                        int64_t eld, const int32_t* __restrict__ nptr,
+                                                        const int32_t* __restrict__ node_elem,
+                                                        const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
+                                                        int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots,
+                                                        int* flags) {
+    __shared__ int32_t Ls[ROW_CAP * PAT_BLOCK];
+    int32_t* L = Ls + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
+        int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, PAT_BLOCK, ROW_CAP);
+        if (cnt < 0) continue;  // fallback rows
+        emit_row(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, PAT_BLOCK, row_ptr, col_idx, elem2nnz, slots, flags);
+    }
+}
+
+__global__ void row_fill_big_k(int64_t ne, int nv, const int32_t* __restrict__ elems, int64_t eld,
+                               const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
+                               const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
+                               int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots,
+                               const int32_t* __restrict__ ovf_list, int* flags) {
+    __shared__ int32_t L[ROW_CAP_BIG];
+    int n_ovf = flags[FLAG_OVERFLOW_ROWS];
+    for (int k = blockIdx.x; k < n_ovf; k += gridDim.x) {
+        if (threadIdx.x == 0) {
+            int64_t v = ovf_list[k];
+            int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, 1, ROW_CAP_BIG);
+            if (cnt >= 0) emit_row(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, 1, row_ptr, col_idx, elem2nnz, slots, flags);
+        }
+        __syncthreads();
+    }
+}
+
+struct Work {
+    int32_t* cursor;    // nn+1
+    int32_t* nptr;      // nn+1
+    int32_t* node_elem; // nv*ne
+    int32_t* row_len;   // nn+1
+    int32_t* ovf;       // nn
+    int* flags;         // 4 ints
+    int64_t* total;     // 2 int64
+    void* scan_tmp;
+    size_t bytes;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+Work carve(void* base, int64_t nn, int64_t ne, int nv) {
+    Work w{};
+    char* p = reinterpret_cast<char*>(base);
+    size_t off = 0;
+    auto take = [&](size_t b) { char* r = p ? p + off : nullptr; off += al(b); return r; };
+    w.cursor = (int32_t*)take(4 * (nn + 1));
+    w.nptr = (int32_t*)take(4 * (nn + 1));
+    w.node_elem = (int32_t*)take(4 * (size_t)nv * ne + 4);
+    w.row_len = (int32_t*)take(4 * (nn + 1));
+    w.ovf = (int32_t*)take(4 * (nn + 1));
+    w.flags = (int*)take(64);
+    w.total = (int64_t*)take(64);
+    int64_t smax = nn > nv * ne ? nn : nv * ne;
+    w.scan_tmp = take(scan_tmp_bytes(smax + 1));
+    w.bytes = off;
+    return w;
+}
+
+}  // namespace
+}  // namespace vb
+
+using namespace vb;
+
+extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld, void* work,
+                                    size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                                    int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem,
+                                    uint32_t* node_elem_slot, int64_t* nnz_out, vb_stream_t stream) {
+    clear_error();
+    if (dim != 2 && dim != 3) { set_error("fem_p1_pattern: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
+    if (nn < 0 || ne < 0) { set_error("fem_p1_pattern: negative nn or ne"); return VB_ERR_ARG; }
+    const int nv = dim + 1;
+    if (ne >= (1ll << 29) || (int64_t)nv * nv * ne >= (1ll << 31) || nn >= (1ll << 31) - 1) {
+        set_error("fem_p1_pattern: ne=%lld / nn=%lld too large for int32 plans", (long long)ne, (long long)nn);
+        return VB_ERR_OVERFLOW;
+    }
+    Work w = carve(nullptr, nn, ne, nv);
+    if (!work) {
+        if (!work_bytes) { set_error("fem_p1_pattern: work and work_bytes both NULL"); return VB_ERR_ARG; }
+        *work_bytes = w.bytes;
+        return VB_OK;
+    }
+    if (work_bytes && *work_bytes < w.bytes) { set_error("fem_p1_pattern: work buffer too small (%zu < %zu)", *work_bytes, w.bytes); return VB_ERR_WORKSPACE; }
+    if (!row_ptr) { set_error("fem_p1_pattern: NULL row_ptr"); return VB_ERR_ARG; }
+    if (ne > 0 && !elems) { set_error("fem_p1_pattern: NULL elems"); return VB_ERR_ARG; }
+    if (elem_ld < ne) { set_error("fem_p1_pattern: elem_ld < ne"); return VB_ERR_ARG; }
+    if ((node_elem_ptr != nullptr) != (node_elem != nullptr) || (node_elem_slot && !node_elem)) {
+        set_error("fem_p1_pattern: node_elem_ptr, node_elem (and node_elem_slot) must be given together");
+        return VB_ERR_ARG;
+    }
+    w = carve(work, nn, ne, nv);
+    cudaStream_t s = cs(stream);
+    int32_t* nptr = node_elem_ptr ? node_elem_ptr : w.nptr;
+    int32_t* nelem = node_elem ? node_elem : w.node_elem;
+
+    // 1. node -> element incidences
+    cudaMemsetAsync(w.cursor, 0, 4 * (nn + 1), s);
+    cudaMemsetAsync(w.flags, 0, 64, s);
+    unsigned ge = grid_for(ne, 256, 8);
+    unsigned gn = grid_for(nn, 256, 8);
+    if (ne > 0) degree_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor);
+    vb_status st = exclusive_scan_i32(w.cursor, nptr, nn, w.scan_tmp, s, nullptr);
+    if (st != VB_OK) return st;
+    cudaMemcpyAsync(w.cursor, nptr, 4 * (nn + 1), cudaMemcpyDeviceToDevice, s);
+    if (ne > 0) bucket_fill_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor, nelem);
+    if (nn > 0) sort_incidences_k<<<gn, 256, 0, s>>>(nn, nptr, nelem);
+    if ((st = launch_check("fem_p1_pattern(incidences)")) != VB_OK) return st;
+
+    unsigned gr = grid_for(nn, PAT_BLOCK, 4);
+    if (!col_idx) {
+        // 2. count
+        if (nn > 0) row_count_k<<<gr, PAT_BLOCK, 0, s>>>(nn, nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        row_count_big_k<<<64, 32, 0, s>>>(nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        if ((st = exclusive_scan_i32(w.row_len, row_ptr, nn, w.scan_tmp, s, w.total)) != VB_OK) return st;
+        int64_t host[2] = {0, 0};
+        int hflags[4] = {0, 0, 0, 0};
+        cudaMemcpyAsync(host, w.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
+        cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
+        if (hflags[FLAG_TOO_LONG]) { set_error("fem_p1_pattern: a row has more than %d distinct columns", ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
+        if (host[0] >= (1ll << 31)) { set_error("fem_p1_pattern: nnz=%lld does not fit int32", (long long)host[0]); return VB_ERR_OVERFLOW; }
+        if (nnz_out) *nnz_out = host[0];
+        return VB_OK;
+    }
+    // 3. fill (row_ptr from the count phase); check the capacity before writing
+    int32_t nnz32 = 0;
+    cudaMemcpyAsync(&nnz32, row_ptr + nn, 4, cudaMemcpyDeviceToHost, s);
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    if (nnz32 < 0 || nnz32 > col_cap) { set_error("fem_p1_pattern: col_cap=%lld < nnz=%d", (long long)col_cap, nnz32); return VB_ERR_ARG; }
+    if (nn > 0) {
+        // the fallback row list is rebuilt by the count kernel's overflow path
+        row_count_k<<<gr, PAT_BLOCK, 0, s>>>(nn, nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        row_fill_k<<<gr, PAT_BLOCK, 0, s>>>(nn, ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
+                                            node_elem_slot, w.flags);
+        row_fill_big_k<<<64, 32, 0, s>>>(ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
+                                          node_elem_slot, w.ovf, w.flags);
+    }
+    if ((st = launch_check("fem_p1_pattern(fill)")) != VB_OK) return st;
+    int hflags[4] = {0, 0, 0, 0};
+    cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    if (hflags[FLAG_TOO_LONG]) { set_error("fem_p1_pattern: a row has more than %d distinct columns", ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
+    if (hflags[FLAG_SLOT_RANGE]) { set_error("fem_p1_pattern: a row has more than 255 entries; gather plan unsupported, use elem2nnz"); return VB_ERR_UNSUPPORTED; }
+    if (nnz_out) *nnz_out = nnz32;
+    return VB_OK;
+}

@@ -1,0 +1,102 @@
+// a6: fused surface geometry over a triangulated closed surface (config 3):
+// gather the three vertices of each face, n = (b-a) x (c-a), |n|, nhat, area,
+// and the divergence-theorem volume sum (1/6) sum a.n reduced with
+// a fixed-shape tree (block partials in a fixed grid, then one block) so the
+// volume is bitwise reproducible.
+#include "vb_internal.cuh"
+
+namespace vb {
+namespace {
+
+constexpr int SURF_BLOCK = 256;
+constexpr int SURF_BLOCKS_PER_SM = 8;
+
+__global__ void __launch_bounds__(SURF_BLOCK) tri_surface_k(int64_t nf, const int32_t* __restrict__ tri, int64_t tld,
+                                                            const double* __restrict__ xyz, int64_t ns, int64_t cst,
+                                                            double* __restrict__ n_out, double* __restrict__ nh_out,
+                                                            double* __restrict__ area, double* __restrict__ part) {
+    double vol = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += stride) {
+        int64_t ia = __ldcs(tri + f), ib = __ldcs(tri + tld + f), ic = __ldcs(tri + 2 * tld + f);
+        double a[3], u[3], w[3];
+#pragma unroll
+        for (int d = 0; d < 3; d++) {
+            a[d] = __ldg(xyz + d * cst + ia * ns);
+            u[d] = __ldg(xyz + d * cst + ib * ns) - a[d];
+            w[d] = __ldg(xyz + d * cst + ic * ns) - a[d];
+        }
+        double n0 = fma(u[1], w[2], -u[2] * w[1]);
+        double n1 = fma(u[2], w[0], -u[0] * w[2]);
+        double n2 = fma(u[0], w[1], -u[1] * w[0]);
+        double len = sqrt(fma(n0, n0, fma(n1, n1, n2 * n2)));
+        if (n_out) {
+            stcs(n_out + f, n0);
+            stcs(n_out + nf + f, n1);
+            stcs(n_out + 2 * nf + f, n2);
+        }
+        if (nh_out) {
+            double r = 1.0 / len;
+            stcs(nh_out + f, n0 * r);
+            stcs(nh_out + nf + f, n1 * r);
+            stcs(nh_out + 2 * nf + f, n2 * r);
+        }
+        if (area) stcs(area + f, 0.5 * len);
+        vol += fma(a[0], n0, fma(a[1], n1, a[2] * n2));
+    }
+    if (part) {
+        __shared__ double sh[SURF_BLOCK / 32];
+        for (int o = 16; o > 0; o >>= 1) vol += __shfl_xor_sync(0xffffffffu, vol, o);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = vol;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = (threadIdx.x < SURF_BLOCK / 32) ? sh[threadIdx.x] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (threadIdx.x == 0) part[blockIdx.x] = t;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(1024) sum_parts_k(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = sh[threadIdx.x];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) *out = t / 6.0;
+    }
+}
+
+}  // namespace
+}  // namespace vb
+
+using namespace vb;
+
+extern "C" vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, int64_t nverts, const double* xyz,
+                                    int64_t node_stride, int64_t comp_stride, double* n, double* nhat, double* area,
+                                    double* volume, void* work, size_t* work_bytes, vb_stream_t stream) {
+    clear_error();
+    if (nf < 0 || nverts < 0) { set_error("vb_tri_surface: negative size"); return VB_ERR_ARG; }
+    unsigned g = grid_for(nf, SURF_BLOCK, SURF_BLOCKS_PER_SM);
+    size_t need = volume ? ((size_t)g * sizeof(double) + 255) & ~(size_t)255 : 0;
+    if (!work) {
+        if (!work_bytes) { set_error("vb_tri_surface: work and work_bytes both NULL"); return VB_ERR_ARG; }
+        *work_bytes = need;
+        return VB_OK;
+    }
+    if (work_bytes && *work_bytes < need) { set_error("vb_tri_surface: work buffer too small (%zu < %zu)", *work_bytes, need); return VB_ERR_WORKSPACE; }
+    if (nf > 0 && (!tri || !xyz)) { set_error("vb_tri_surface: NULL %s", !tri ? "tri" : "xyz"); return VB_ERR_ARG; }
+    if (tri_ld < nf) { set_error("vb_tri_surface: tri_ld < nf"); return VB_ERR_ARG; }
+    auto s = cs(stream);
+    double* part = volume ? reinterpret_cast<double*>(work) : nullptr;
+    if (nf > 0) tri_surface_k<<<g, SURF_BLOCK, 0, s>>>(nf, tri, tri_ld, xyz, node_stride, comp_stride, n, nhat, area, part);
+    if (volume) {
+        if (nf == 0) { cudaMemsetAsync(volume, 0, sizeof(double), s); return launch_check("vb_tri_surface"); }
+        sum_parts_k<<<1, 1024, 0, s>>>(part, (int)g, volume);
+    }
+    return launch_check("vb_tri_surface");
+}

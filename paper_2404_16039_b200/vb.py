@@ -1,0 +1,268 @@
+"""Thin Python binding of libvb.so (include/vb.h) -- argument marshalling only.
+
+Every function has the name of the C entry point it calls and runs nothing but
+that call: torch is used for device memory (output allocation) and the current
+CUDA stream.  There is no CPU path: if libvb.so is missing or CUDA is not
+available the calls raise.
+
+Layouts (include/vb.h): a page batch of N r x c pages is a contiguous float64
+CUDA tensor of shape (c, r, N) (column-major entries, page-contiguous planes);
+a single object broadcast to every page (eq:copy) is a tensor of
+shape (c, r, 1) used with npages > 1 (ld = 0).  Meshes: coords (dim, nn)
+float64, elems (nv, ne) int32.
+"""
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvb.so")
+
+VB_ASSEMBLE_ATOMIC = 0
+VB_ASSEMBLE_GATHER = 1
+
+_STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORTED",
+           -4: "VB_ERR_OVERFLOW", -5: "VB_ERR_WORKSPACE", -6: "VB_ERR_CUDA"}
+
+EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
+           "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
+           "fem_p1_assemble")
+
+
+class VbError(RuntimeError):
+    def __init__(self, status, message):
+        super().__init__("%s (%d): %s" % (_STATUS.get(status, "?"), status, message))
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libvb.so (raises if it is missing -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError("libvb.so not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        i64, i32, d, p, sz = C.c_int64, C.c_int, C.c_double, C.c_void_p, C.POINTER(C.c_size_t)
+        sig = {
+            "vb_last_error": (C.c_char_p, []),
+            "vb_abi_version": (i32, []),
+            "vb_page_mtimes": (i32, [i64, p, i32, i32, i64, i32, p, i32, i32, i64, i32, p, i64, p]),
+            "vb_page_transpose": (i32, [i64, p, i32, i32, i64, p, i64, p]),
+            "vb_page_det": (i32, [i64, i32, p, i64, p, p]),
+            "vb_page_inv": (i32, [i64, i32, p, i64, p, i64, p, p, d, p]),
+            "vb_page_cross": (i32, [i64, p, i64, p, i64, p, i64, p]),
+            "vb_create_coords3D": (i32, [i32, i32, i64, p, i64, i64, p, i64, p, p, p]),
+            "vb_tri_surface": (i32, [i64, p, i64, i64, p, i64, i64, p, p, p, p, p, sz, p]),
+            "fem_p1_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p,
+                                     C.POINTER(C.c_int64), p]),
+            "fem_p1_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, p,
+                                      p, p, p, p, i32, p]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise VbError(rc, lib().vb_last_error().decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("libvb takes device tensors only (got a %s tensor)" % t.device)
+    if not t.is_contiguous():
+        raise ValueError("libvb takes contiguous tensors")
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _f64(t):
+    if t.dtype != torch.float64:
+        raise TypeError("expected float64, got %s" % t.dtype)
+    return t
+
+
+def _ld(t, npages):
+    n = t.shape[-1]
+    return 0 if (n == 1 and npages != 1) else n
+
+
+# ------------------------------------------------------------------ page ops
+def vb_page_mtimes(X, Y, transX=False, transY=False, Z=None, stream=None):
+    """Z_k = op(X_k) op(Y_k).  X: (xcols, xrows, N|1), Y: (ycols, yrows, N|1)."""
+    _f64(X), _f64(Y)
+    xc, xr, nx = X.shape
+    yc, yr, ny = Y.shape
+    npages = max(nx, ny)
+    m = xc if transX else xr
+    n = yr if transY else yc
+    if Z is None:
+        Z = torch.empty((n, m, npages), dtype=torch.float64, device=X.device)
+    _check(lib().vb_page_mtimes(npages, _ptr(X), xr, xc, _ld(X, npages), int(bool(transX)),
+                                _ptr(Y), yr, yc, _ld(Y, npages), int(bool(transY)),
+                                _ptr(Z), Z.shape[-1], _stream(stream)))
+    return Z
+
+
+def vb_page_transpose(X, Z=None, stream=None):
+    _f64(X)
+    c, r, n = X.shape
+    if Z is None:
+        Z = torch.empty((r, c, n), dtype=torch.float64, device=X.device)
+    _check(lib().vb_page_transpose(n, _ptr(X), r, c, n, _ptr(Z), Z.shape[-1], _stream(stream)))
+    return Z
+
+
+def vb_page_det(X, det=None, stream=None):
+    _f64(X)
+    n, n2, N = X.shape
+    if det is None:
+        det = torch.empty((N,), dtype=torch.float64, device=X.device)
+    _check(lib().vb_page_det(N, n if n == n2 else -1, _ptr(X), N, _ptr(det), _stream(stream)))
+    return det
+
+
+def vb_page_inv(X, Xinv=None, det=None, first_singular=None, sing_tol=1e-14, want_det=True, stream=None):
+    """Returns (Xinv, det or None, first_singular device int64 tensor or None)."""
+    _f64(X)
+    n, n2, N = X.shape
+    if n != n2:
+        raise ValueError("vb_page_inv: pages are %dx%d, not square" % (n2, n))
+    if Xinv is None:
+        Xinv = torch.empty_like(X)
+    if det is None and want_det:
+        det = torch.empty((N,), dtype=torch.float64, device=X.device)
+    _check(lib().vb_page_inv(N, n, _ptr(X), N, _ptr(Xinv), Xinv.shape[-1], _ptr(det), _ptr(first_singular),
+                             float(sing_tol), _stream(stream)))
+    return Xinv, det, first_singular
+
+
+def vb_page_cross(A, B, Cout=None, stream=None):
+    _f64(A), _f64(B)
+    N = max(A.shape[-1], B.shape[-1])
+    if Cout is None:
+        Cout = torch.empty((1, 3, N), dtype=torch.float64, device=A.device)
+    _check(lib().vb_page_cross(N, _ptr(A), _ld(A, N), _ptr(B), _ld(B, N), _ptr(Cout), N, _stream(stream)))
+    return Cout
+
+
+def vb_create_coords3D(coords, elems, want_coords3D=True, want_vectors3D=True, stream=None):
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    c3 = torch.empty((nv, dim, ne), dtype=torch.float64, device=coords.device) if want_coords3D else None
+    v3 = torch.empty((nv - 1, dim, ne), dtype=torch.float64, device=coords.device) if want_vectors3D else None
+    _check(lib().vb_create_coords3D(dim, nv, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(c3), _ptr(v3),
+                                    _stream(stream)))
+    return c3, v3
+
+
+def vb_tri_surface(xyz, tri, want_n=True, want_nhat=True, want_area=True, want_volume=True, work=None, out=None,
+                   stream=None):
+    """Returns dict with n (3,F), nhat (3,F), area (F,), volume (1,) device tensors."""
+    _f64(xyz)
+    nverts = xyz.shape[1]
+    nf = tri.shape[1]
+    dev = xyz.device
+    o = dict(out or {})
+    if want_n and "n" not in o:
+        o["n"] = torch.empty((3, nf), dtype=torch.float64, device=dev)
+    if want_nhat and "nhat" not in o:
+        o["nhat"] = torch.empty((3, nf), dtype=torch.float64, device=dev)
+    if want_area and "area" not in o:
+        o["area"] = torch.empty((nf,), dtype=torch.float64, device=dev)
+    if want_volume and "volume" not in o:
+        o["volume"] = torch.empty((1,), dtype=torch.float64, device=dev)
+    sz = C.c_size_t(0)
+    vol = o.get("volume")
+    _check(lib().vb_tri_surface(nf, None, nf, nverts, None, 1, nverts, None, None, None, _ptr(vol), None,
+                                C.byref(sz), _stream(stream)))
+    if work is None or work.numel() < sz.value:
+        work = torch.empty((max(sz.value, 1),), dtype=torch.uint8, device=dev)
+    sz2 = C.c_size_t(work.numel())
+    _check(lib().vb_tri_surface(nf, _ptr(tri), nf, nverts, _ptr(xyz), 1, nverts, _ptr(o.get("n")),
+                                _ptr(o.get("nhat")), _ptr(o.get("area")), _ptr(vol), _ptr(work), C.byref(sz2),
+                                _stream(stream)))
+    o["work"] = work
+    return o
+
+
+# ------------------------------------------------------------------ FEM P1
+class P1Plan:
+    """CSR pattern + scatter plans of a P1 mesh (fem_p1_pattern, both phases).
+
+    Attributes: row_ptr (nn+1), col_idx (nnz) int32; elem2nnz (nv*nv, ne) int32
+    or None; node_elem_ptr (nn+1), node_elem (nv*ne) int32 and node_elem_slot
+    (nv*ne) int32 (uint32 bits) or None; nnz."""
+
+    def __init__(self, elems, nn, scatter_map=True, gather_plan=True, stream=None):
+        if elems.dtype != torch.int32:
+            raise TypeError("elems must be int32")
+        nv, ne = elems.shape
+        self.dim, self.nn, self.ne, self.nv = nv - 1, int(nn), int(ne), nv
+        dev = elems.device
+        L = lib()
+        sz = C.c_size_t(0)
+        nnz = C.c_int64(0)
+        st = _stream(stream)
+        _check(L.fem_p1_pattern(self.dim, nn, ne, None, ne, None, C.byref(sz), None, None, 0, None, None, None, None,
+                                None, st))
+        self.work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
+        self.row_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
+        _check(L.fem_p1_pattern(self.dim, nn, ne, _ptr(elems), ne, _ptr(self.work), C.byref(sz), _ptr(self.row_ptr),
+                                None, 0, None, None, None, None, C.byref(nnz), st))
+        self.nnz = int(nnz.value)
+        self.col_idx = torch.empty((max(self.nnz, 1),), dtype=torch.int32, device=dev)
+        self.elem2nnz = torch.empty((nv * nv, ne), dtype=torch.int32, device=dev) if scatter_map else None
+        if gather_plan:
+            self.node_elem_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
+            self.node_elem = torch.empty((max(nv * ne, 1),), dtype=torch.int32, device=dev)
+            self.node_elem_slot = torch.empty((max(nv * ne, 1),), dtype=torch.int32, device=dev)
+        else:
+            self.node_elem_ptr = self.node_elem = self.node_elem_slot = None
+        _check(L.fem_p1_pattern(self.dim, nn, ne, _ptr(elems), ne, _ptr(self.work), C.byref(sz), _ptr(self.row_ptr),
+                                _ptr(self.col_idx), self.col_idx.numel(), _ptr(self.elem2nnz), _ptr(self.node_elem_ptr),
+                                _ptr(self.node_elem), _ptr(self.node_elem_slot), C.byref(nnz), st))
+        self.col_idx = self.col_idx[:self.nnz]
+        self.work = None   # the pattern workspace is not needed after the plan exists
+
+
+def fem_p1_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
+    return P1Plan(elems, nn, scatter_map, gather_plan, stream)
+
+
+def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False,
+                    K=None, M=None, stream=None):
+    """Returns (K_vals, M_vals, K_local, M_local) (None where not requested)."""
+    _f64(coords)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    dev = coords.device
+    if want_K and K is None:
+        K = torch.empty((plan.nnz,), dtype=torch.float64, device=dev)
+    if want_M and M is None:
+        M = torch.empty((plan.nnz,), dtype=torch.float64, device=dev)
+    if not want_K:
+        K = None
+    if not want_M:
+        M = None
+    Kl = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
+                                 _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
+                                 _ptr(plan.node_elem), _ptr(plan.node_elem_slot), _ptr(K), _ptr(M), _ptr(Kl),
+                                 _ptr(Ml), int(mode), _stream(stream)))
+    return K, M, Kl, Ml

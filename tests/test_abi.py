@@ -1,0 +1,93 @@
+"""C-ABI contract tests that need no GPU: libvb.so loads, exports every
+symbol include/vb.h declares, and argument/shape errors are reported
+synchronously (before any CUDA call) with a message naming the argument."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2404_16039_b200 import _build
+    _build.build()
+    from paper_2404_16039_b200 import vb
+    return vb.lib()
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "vb.h")).read()
+    return sorted(set(re.findall(r"VB_API\s+[\w\s\*]+?\b(\w+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_entry_points():
+    names = declared_symbols()
+    for n in ("vb_page_mtimes", "vb_page_transpose", "vb_page_det", "vb_page_inv", "vb_page_cross",
+              "fem_p1_pattern", "fem_p1_assemble"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(L):
+    from paper_2404_16039_b200 import vb
+    out = subprocess.check_output(["nm", "-D", "--defined-only", vb.LIB_PATH]).decode()
+    exported = set(re.findall(r" T (\w+)$", out, flags=re.M))
+    for n in declared_symbols():
+        assert n in exported, n
+        assert hasattr(L, n)
+    assert set(vb.EXPORTS) == set(declared_symbols())
+    assert L.vb_abi_version() == 1
+
+
+def test_sm100a_code_only(L):
+    from paper_2404_16039_b200 import vb
+    out = subprocess.check_output(["cuobjdump", "--list-elf", vb.LIB_PATH]).decode()
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+FAKE = C.c_void_p(0x1000)
+
+
+def test_mtimes_dimension_errors(L):
+    rc = L.vb_page_mtimes(8, FAKE, 3, 2, 8, 0, FAKE, 3, 3, 8, 0, FAKE, 8, None)
+    assert rc == -2 and b"inner dimension" in L.vb_last_error()
+    rc = L.vb_page_mtimes(8, FAKE, 5, 2, 8, 0, FAKE, 2, 3, 8, 0, FAKE, 8, None)
+    assert rc == -3
+    rc = L.vb_page_mtimes(8, FAKE, 3, 2, 4, 0, FAKE, 2, 3, 8, 0, FAKE, 8, None)
+    assert rc == -1 and b"leading dimension" in L.vb_last_error()
+    rc = L.vb_page_mtimes(8, None, 3, 2, 8, 0, FAKE, 2, 3, 8, 0, FAKE, 8, None)
+    assert rc == -1 and b"NULL X" in L.vb_last_error()
+    assert L.vb_page_mtimes(0, None, 3, 2, 0, 0, None, 2, 3, 0, 0, None, 0, None) == 0   # empty batch
+
+
+def test_det_inv_transpose_cross_errors(L):
+    assert L.vb_page_det(4, 5, FAKE, 4, FAKE, None) == -3
+    assert L.vb_page_det(-1, 2, FAKE, 4, FAKE, None) == -1
+    assert L.vb_page_inv(4, 0, FAKE, 4, FAKE, 4, None, None, 1e-14, None) == -3
+    assert L.vb_page_transpose(4, FAKE, 2, 7, 4, FAKE, 4, None) == -3
+    assert L.vb_page_cross(4, FAKE, 2, FAKE, 4, FAKE, 4, None) == -1
+
+
+def test_fem_argument_errors(L):
+    nnz = C.c_int64(0)
+    sz = C.c_size_t(0)
+    assert L.fem_p1_pattern(4, 10, 10, FAKE, 10, None, C.byref(sz), FAKE, None, 0, None, None, None, None,
+                            C.byref(nnz), None) == -3
+    assert L.fem_p1_pattern(3, 10, 1 << 29, FAKE, 1 << 29, None, C.byref(sz), FAKE, None, 0, None, None, None, None,
+                            C.byref(nnz), None) == -4
+    # work-size query needs no GPU and grows with the mesh
+    assert L.fem_p1_pattern(3, 1000, 6000, None, 6000, None, C.byref(sz), None, None, 0, None, None, None, None,
+                            None, None) == 0
+    small = sz.value
+    assert L.fem_p1_pattern(3, 2000, 12000, None, 12000, None, C.byref(sz), None, None, 0, None, None, None, None,
+                            None, None) == 0
+    assert sz.value > small
+    assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, None,
+                             None, None, 7, None) == -1
+    assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, None,
+                             None, None, 0, None) == -1                     # atomic mode without elem2nnz
+    assert b"elem2nnz" in L.vb_last_error()

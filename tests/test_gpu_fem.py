@@ -1,0 +1,269 @@
+"""GPU parity of the P1 assembly path (a6-a17) against the CPU oracle through
+the C ABI: the CSR pattern and the scatter plans bit-exact, K/M within 1e-12
+relative max-norm (BASELINE.json north_star), the deterministic variant
+bitwise reproducible, plus edge cases (empty mesh, isolated nodes, a single
+element, rows longer than the fast-path capacity) and full-size checks of
+configs 3-5 on sampled rows / faces in the launch configuration bench.py times."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2404_16039_b200 import vb
+
+pytestmark = pytest.mark.gpu
+MODES = [vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC]
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return torch.device("cuda:0")
+
+
+def g(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def h(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def relmax(got, ref):
+    return np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)
+
+
+def mesh(kind, n, seed=0):
+    if kind == "2d":
+        return synth.square_p1(n, jitter=0.1, seed=seed)
+    return synth.cube_kuhn_p1(n, jitter=0.05, seed=seed)
+
+
+def expected_elem2nnz(elems, rp, ci):
+    nv, ne = elems.shape
+    out = np.empty((nv * nv, ne), dtype=np.int64)
+    for a in range(nv):
+        r = elems[a].astype(np.int64)
+        for b in range(nv):
+            c = elems[b]
+            # position of c within row r of the oracle's CSR
+            lo = rp[r].astype(np.int64)
+            hi = rp[r + 1].astype(np.int64)
+            pos = np.empty(ne, dtype=np.int64)
+            for e in range(ne):
+                pos[e] = lo[e] + np.searchsorted(ci[lo[e]:hi[e]], c[e])
+            out[a * nv + b] = pos
+    return out
+
+
+# ---------------------------------------------------------------- pattern + plans
+@pytest.mark.parametrize("kind,n", [("2d", 1), ("2d", 7), ("2d", 32), ("3d", 1), ("3d", 4), ("3d", 9)])
+def test_pattern_and_plans_bit_exact(dev, kind, n):
+    coords, elems = mesh(kind, n)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    plan = vb.P1Plan(g(elems, dev), nn)
+    assert np.array_equal(h(plan.row_ptr), rp)
+    assert np.array_equal(h(plan.col_idx), ci)
+    assert np.array_equal(h(plan.elem2nnz), expected_elem2nnz(elems, rp, ci))
+    # gather plan: incidences of each node, ascending e, with the right slots
+    nptr, nel, nsl = h(plan.node_elem_ptr), h(plan.node_elem), h(plan.node_elem_slot).view(np.uint32)
+    nv = elems.shape[0]
+    for v in range(0, nn, max(1, nn // 97)):
+        inc = nel[nptr[v]:nptr[v + 1]]
+        e, a = inc >> 2, inc & 3
+        assert np.all(np.diff(e) > 0) and np.all(elems[a, e] == v)
+        assert len(inc) == np.count_nonzero(elems == v)
+        for k, (ee, aa) in enumerate(zip(e, a)):
+            sl = nsl[nptr[v] + k]
+            for b in range(nv):
+                assert ci[rp[v] + ((sl >> (8 * b)) & 0xFF)] == elems[b, ee]
+
+
+# ---------------------------------------------------------------- assembly
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("kind,n", [("2d", 1), ("2d", 32), ("2d", 50), ("3d", 1), ("3d", 6), ("3d", 11)])
+def test_assembly_parity(dev, kind, n, mode):
+    coords, elems = mesh(kind, n, seed=1)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    K, M, Kl, Ml = vb.fem_p1_assemble(cd, ed, plan, mode=mode, want_local=True)
+    assert relmax(h(K), Ko) <= 1e-12
+    assert relmax(h(M), Mo) <= 1e-12
+    K3o, M3o = oracle.p1_local_all(coords, elems)
+    assert relmax(h(Kl), K3o) <= 1e-12 and relmax(h(Ml), M3o) <= 1e-12
+
+
+def test_gather_variant_bitwise_reproducible(dev):
+    coords, elems = mesh("3d", 12, seed=2)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, coords.shape[1])
+    K1, M1, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER)
+    K1, M1 = h(K1), h(M1)
+    for _ in range(3):
+        K2, M2, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER)
+        assert np.array_equal(h(K2), K1) and np.array_equal(h(M2), M1)
+
+
+def test_unjittered_square_stencil_bitwise_on_gpu(dev):
+    coords, elems = synth.square_p1(32, jitter=0.0)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, _ = oracle.p1_assemble(coords, elems, rp, ci)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    for mode in MODES:
+        K, _, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode)
+        assert np.array_equal(h(K), Ko)           # dyadic values: exact in any order
+
+
+def test_invariants_on_gpu_output(dev):
+    coords, elems = mesh("3d", 10, seed=5)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, coords.shape[1])
+    K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan)
+    rp, ci, K, M = h(plan.row_ptr), h(plan.col_idx), h(K), h(M)
+    rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    Kone = np.zeros(len(rp) - 1)
+    np.add.at(Kone, rows, K)
+    assert np.max(np.abs(Kone)) <= 1e-13 * np.max(np.abs(K))
+    assert abs(math.fsum(M) - 1.0) <= 1e-13
+    a = np.array([1.0, 2.0, 3.0])
+    u = a @ coords
+    Ku = np.zeros(len(rp) - 1)
+    np.add.at(Ku, rows, K * u[ci])
+    assert abs(math.fsum(u * Ku) - 14.0) <= 1e-12 * 14.0
+
+
+# ---------------------------------------------------------------- edge cases
+def test_empty_mesh_and_isolated_nodes(dev):
+    # no elements at all
+    ed = torch.zeros((4, 0), dtype=torch.int32, device=dev)
+    plan = vb.P1Plan(ed, 5)
+    assert plan.nnz == 0 and np.array_equal(h(plan.row_ptr), np.zeros(6, dtype=np.int32))
+    cd = torch.zeros((3, 5), dtype=torch.float64, device=dev)
+    for mode in MODES:
+        vb.fem_p1_assemble(cd, ed, plan, mode=mode)
+    # one element plus isolated nodes (empty rows)
+    coords = np.zeros((3, 9))
+    coords[:, [2, 5, 6, 8]] = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], dtype=np.float64).T
+    elems = np.array([[2], [5], [6], [8]], dtype=np.int32)
+    rp, ci = oracle.p1_pattern(elems, 9)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan = vb.P1Plan(g(elems, dev), 9)
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    for mode in MODES:
+        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
+        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+
+
+def fan_mesh(k, fans=1):
+    """`fans` centre nodes (ids 0..fans-1), each surrounded by its own k-gon of
+    triangles, so row c has k+1 entries.  Several fans put more than the
+    shared-memory budget of CSR entries into the first CTA's row range."""
+    t = 2 * np.pi * np.arange(k) / k
+    nn = fans * (k + 1)
+    coords = np.zeros((2, nn))
+    el = []
+    for f in range(fans):
+        ring = fans + f * k + np.arange(k)
+        coords[0, f] = 3.0 * f
+        coords[0, ring] = 3.0 * f + np.cos(t)
+        coords[1, ring] = np.sin(t)
+        i = np.arange(k)
+        el.append(np.stack([np.full(k, f), ring[i], ring[(i + 1) % k]]))
+    return coords, np.ascontiguousarray(np.concatenate(el, axis=1).astype(np.int32))
+
+
+@pytest.mark.parametrize("k,fans", [(100, 1), (200, 1), (200, 8)])
+def test_long_rows_fallback_paths(dev, k, fans):
+    """Rows longer than the 64-entry fast path (pattern fallback) and a CTA whose
+    CSR range exceeds the shared-memory budget (in-place gather)."""
+    coords, elems = fan_mesh(k, fans)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan = vb.P1Plan(g(elems, dev), nn)
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    for mode in MODES:
+        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
+        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+
+
+def test_rows_over_255_need_the_scatter_map(dev):
+    coords, elems = fan_mesh(300)
+    nn = coords.shape[1]
+    with pytest.raises(vb.VbError, match="255"):
+        vb.P1Plan(g(elems, dev), nn)
+    plan = vb.P1Plan(g(elems, dev), nn, gather_plan=False)
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=vb.VB_ASSEMBLE_ATOMIC)
+    assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+
+
+# ---------------------------------------------------------------- full-size configs
+def sampled_rows(nn, count=4000, seed=0):
+    rng = np.random.default_rng(seed)
+    mask = np.zeros(nn, dtype=np.uint8)
+    mask[rng.choice(nn, size=count, replace=False)] = 1
+    mask[[0, nn - 1]] = 1
+    return mask
+
+
+@pytest.mark.parametrize("cfg", ["config5", "config4"])
+def test_full_size_assembly_sampled(dev, cfg):
+    """configs[4] (128^3 Kuhn, 12.58M tets) and configs[3] (2048^2 square,
+    8.39M triangles): pattern bit-exact in full, K/M on sampled rows."""
+    if cfg == "config5":
+        coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
+    else:
+        coords, elems = synth.square_p1(2048, jitter=0.1, seed=0)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    assert np.array_equal(h(plan.row_ptr), rp)
+    assert np.array_equal(h(plan.col_idx), ci)
+    mask = sampled_rows(nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci, row_mask=mask)
+    rows = np.repeat(np.arange(nn), np.diff(rp))
+    sel = mask[rows] == 1
+    for mode in MODES:
+        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode)
+        K, M = h(K), h(M)
+        assert relmax(K[sel], Ko[sel]) <= 1e-12
+        assert relmax(M[sel], Mo[sel]) <= 1e-12
+        assert abs(math.fsum(M) - 1.0) <= 1e-12                      # whole-matrix property
+
+
+@pytest.mark.parametrize("level", [3, 6])
+def test_surface_parity(dev, level):
+    xyz, tri = synth.icosphere(level, perturb=0.01, seed=0)
+    o = vb.vb_tri_surface(g(xyz, dev), g(tri, dev))
+    n, nh, ar, vol = oracle.tri_surface(xyz, tri)
+    assert relmax(h(o["n"]), n) <= 1e-12
+    assert relmax(h(o["nhat"]), nh) <= 1e-12
+    assert relmax(h(o["area"]), ar) <= 1e-12
+    assert abs(h(o["volume"])[0] - vol) <= 1e-12 * abs(vol)
+    o2 = vb.vb_tri_surface(g(xyz, dev), g(tri, dev))
+    assert h(o2["volume"])[0] == h(o["volume"])[0]                     # fixed-shape reduction
+
+
+def test_surface_full_size_config3(dev):
+    """configs[2]: level-10 icosphere (20.97M faces), all faces compared."""
+    xyz, tri = synth.icosphere(10, perturb=0.01, seed=0)
+    o = vb.vb_tri_surface(g(xyz, dev), g(tri, dev))
+    n, nh, ar, vol = oracle.tri_surface(xyz, tri)
+    assert relmax(h(o["n"]), n) <= 1e-12
+    assert relmax(h(o["nhat"]), nh) <= 1e-12
+    assert relmax(h(o["area"]), ar) <= 1e-12
+    assert abs(h(o["volume"])[0] - vol) <= 1e-12 * abs(vol)
+    assert abs(vol - 4.0 * math.pi / 3.0) < 2e-3                     # near the unit ball (radii +-1%)
