@@ -164,8 +164,10 @@ VB_API vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, 
  *     node_elem_slot (nv*ne uint32): the gather plan of VB_ASSEMBLE_GATHER:
  *     for row v, entries node_elem_ptr[v]..node_elem_ptr[v+1]-1 list the
  *     incidences (e, a) with elems[a][e] == v, packed e*4 + a, ascending e;
- *     node_elem_slot packs, in byte b, the in-row offset of column elems[b][e]
- *     in row v (so rows must have <= 255 entries; VB_ERR_UNSUPPORTED otherwise).
+ *     node_elem_slot packs in-row offsets (positions within row v's columns):
+ *     byte 0 = offset of v itself (the diagonal), bytes 1..nv-1 = offsets of
+ *     the element's other vertices elems[b][e], b != a, in ascending b (so
+ *     rows must have <= 255 entries; VB_ERR_UNSUPPORTED otherwise).
  * Errors: VB_ERR_OVERFLOW if nnz >= 2^31 or ne*nv*nv >= 2^31 or ne >= 2^29;
  *   VB_ERR_UNSUPPORTED if a row has more than 4096 distinct columns;
  *   VB_ERR_ARG if col_cap < nnz.  Deterministic: identical outputs every run. */

@@ -157,50 +157,103 @@ __global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restr
 }
 
 // ------------------------------------------------------------ gather (deterministic) variant
-constexpr int GATHER_BLOCK = 128;
+// One thread owns row v.  The edge vectors f_s = x_{col(s)} - x_v to every
+// column of the row are formed once per row (shared memory, indexed by the
+// in-row slot).  Each incidence (e, a) of v then needs only its plan word
+// (slots of v and of the element's other vertices): with v as the base vertex
+// (any base gives the same K_e) the element's tjac rows are
+// f_1..f_d, adj(tjac) has columns h_j = cross products of the other f's,
+//   grad phi_{o_j} = h_j / det,  grad phi_a = h_a / det,  h_a = -sum_j h_j,
+//   K_e[a][o_j] = (h_a . h_j) / (d! |det|),  K_e[a][a] = -sum_j K_e[a][o_j],
+//   M_e[a][o_j] = |det| / (d! (d+1)(d+2)),    M_e[a][a] = 2 M_e[a][o_j],
+// summed in ascending element order (deterministic; the oracle's order).
+constexpr int GATHER_BLOCK = 64;
 template <int DIM>
 struct GatherCfg {
-    static constexpr int SLOTS_PER_ROW = DIM == 2 ? 10 : 20;           // smem budget per row (average)
-    static constexpr int CAP = GATHER_BLOCK * SLOTS_PER_ROW;          // doubles per matrix per CTA
+    static constexpr int ROW_CAP = DIM == 2 ? 8 : 16;        // columns per row kept in smem (edge vectors)
+    static constexpr int CTA_CAP = GATHER_BLOCK * ROW_CAP;   // CSR entries per CTA kept in smem
+    static constexpr size_t SMEM = (size_t)(ROW_CAP * DIM * GATHER_BLOCK + 2 * CTA_CAP) * sizeof(double);
 };
 
-// Accumulate row v (owned by this thread) into accK/accM (indices relative to
-// the row start `lo`).  ACC points to shared or global memory.
-template <int DIM>
-__device__ __forceinline__ void gather_row(int64_t v, const double* __restrict__ coords, int64_t ns, int64_t cst,
-                                           const int32_t* __restrict__ elems, int64_t eld,
-                                           const int32_t* __restrict__ nptr, const int32_t* __restrict__ nelem,
-                                           const uint32_t* __restrict__ nslot, double* accK, double* accM) {
-    constexpr int NV = DIM + 1;
-    int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
+template <int DIM, bool FAST>
+__device__ __forceinline__ void edge_vec(int s, const double* F, int lo, const int32_t* __restrict__ col_idx,
+                                         const double* __restrict__ coords, int64_t ns, int64_t cst,
+                                         const double (&xv)[DIM], double (&f)[DIM]) {
+    if (FAST) {
+#pragma unroll
+        for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * GATHER_BLOCK];
+    } else {
+        int64_t w = __ldg(col_idx + lo + s);
+#pragma unroll
+        for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
+    }
+}
+
+template <int DIM, bool FAST, typename Acc>
+__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __restrict__ nslot, const double* F, int lo,
+                                           const int32_t* __restrict__ col_idx, const double* __restrict__ coords,
+                                           int64_t ns, int64_t cst, const double (&xv)[DIM], Acc* accK, Acc* accM) {
+#pragma unroll 2
     for (int i = i0; i < i1; i++) {
-        int32_t ea = __ldcs(nelem + i);
         uint32_t sl = __ldcs(nslot + i);
-        int64_t e = ea >> 2;
-        int a = ea & 3;
-        int32_t vid[NV];
-        double x[NV][DIM], H[DIM][NV];
-        load_element<DIM>(e, elems, eld, coords, ns, cst, vid, x);
-        double det = element_H<DIM>(x, H);
-        double adet = fabs(det);
-        double s = P1<DIM>::INV_DFACT / adet;
-        double m = P1<DIM>::MFACT * adet;
-        double h[DIM];
+        int s0 = sl & 0xff;
+        if constexpr (DIM == 3) {
+            int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff, s3 = sl >> 24;
+            double f1[3], f2[3], f3[3];
+            edge_vec<3, FAST>(s1, F, lo, col_idx, coords, ns, cst, xv, f1);
+            edge_vec<3, FAST>(s2, F, lo, col_idx, coords, ns, cst, xv, f2);
+            edge_vec<3, FAST>(s3, F, lo, col_idx, coords, ns, cst, xv, f3);
+            double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
+                            fma(f2[0], f3[1], -f2[1] * f3[0])};
+            double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
+                            fma(f3[0], f1[1], -f3[1] * f1[0])};
+            double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
+                            fma(f1[0], f2[1], -f1[1] * f2[0])};
+            double det = fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2]));
+            double ad = fabs(det);
+            double r = 1.0 / (6.0 * ad);
+            double ha[3];
 #pragma unroll
-        for (int r = 0; r < DIM; r++) {
-            double t = H[r][0];
-#pragma unroll
-            for (int b = 1; b < NV; b++) t = (a == b) ? H[r][b] : t;
-            h[r] = s * t;
-        }
-#pragma unroll
-        for (int b = 0; b < NV; b++) {
-            double d = h[0] * H[0][b];
-#pragma unroll
-            for (int r = 1; r < DIM; r++) d = fma(h[r], H[r][b], d);
-            int slot = (sl >> (8 * b)) & 0xff;
-            if (accK) accK[slot] += d;
-            if (accM) accM[slot] += (a == b) ? 2.0 * m : m;
+            for (int c = 0; c < 3; c++) ha[c] = -r * (h1[c] + h2[c] + h3[c]);
+            double k1 = fma(ha[0], h1[0], fma(ha[1], h1[1], ha[2] * h1[2]));
+            double k2 = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
+            double k3 = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
+            double m = ad * (1.0 / 120.0);
+            if (accK) {
+                accK[s1] += k1;
+                accK[s2] += k2;
+                accK[s3] += k3;
+                accK[s0] -= (k1 + k2) + k3;
+            }
+            if (accM) {
+                accM[s1] += m;
+                accM[s2] += m;
+                accM[s3] += m;
+                accM[s0] += 2.0 * m;
+            }
+        } else {
+            int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
+            double f1[2], f2[2];
+            edge_vec<2, FAST>(s1, F, lo, col_idx, coords, ns, cst, xv, f1);
+            edge_vec<2, FAST>(s2, F, lo, col_idx, coords, ns, cst, xv, f2);
+            // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
+            double det = fma(f1[0], f2[1], -f1[1] * f2[0]);
+            double ad = fabs(det);
+            double r = 1.0 / (2.0 * ad);
+            double hax = -r * (f2[1] - f1[1]), hay = -r * (f1[0] - f2[0]);
+            double k1 = fma(hax, f2[1], -hay * f2[0]);
+            double k2 = fma(-hax, f1[1], hay * f1[0]);
+            double m = ad * (1.0 / 24.0);
+            if (accK) {
+                accK[s1] += k1;
+                accK[s2] += k2;
+                accK[s0] -= k1 + k2;
+            }
+            if (accM) {
+                accM[s1] += m;
+                accM[s2] += m;
+                accM[s0] += 2.0 * m;
+            }
         }
     }
 }
@@ -208,49 +261,68 @@ __device__ __forceinline__ void gather_row(int64_t v, const double* __restrict__
 template <int DIM>
 __global__ void __launch_bounds__(GATHER_BLOCK) assemble_gather_k(int64_t nn, const double* __restrict__ coords,
                                                                   int64_t ns, int64_t cst,
-                                                                  const int32_t* __restrict__ elems, int64_t eld,
                                                                   const int32_t* __restrict__ row_ptr,
+                                                                  const int32_t* __restrict__ col_idx,
                                                                   const int32_t* __restrict__ nptr,
-                                                                  const int32_t* __restrict__ nelem,
                                                                   const uint32_t* __restrict__ nslot,
                                                                   double* __restrict__ K, double* __restrict__ M) {
-    constexpr int CAP = GatherCfg<DIM>::CAP;
+    using Cfg = GatherCfg<DIM>;
     extern __shared__ double smem[];
-    double* sK = smem;
-    double* sM = smem + CAP;
+    double* F = smem + threadIdx.x;                                  // [ROW_CAP*DIM][GATHER_BLOCK]
+    double* sK = smem + Cfg::ROW_CAP * DIM * GATHER_BLOCK;            // CTA-contiguous CSR range
+    double* sM = sK + Cfg::CTA_CAP;
     for (int64_t r0 = (int64_t)blockIdx.x * GATHER_BLOCK; r0 < nn; r0 += (int64_t)gridDim.x * GATHER_BLOCK) {
         int64_t rend = r0 + GATHER_BLOCK < nn ? r0 + GATHER_BLOCK : nn;
         int32_t p0 = __ldg(row_ptr + r0), p1 = __ldg(row_ptr + rend);
+        const bool cta_smem = (p1 - p0) <= Cfg::CTA_CAP;
         int64_t v = r0 + threadIdx.x;
-        bool own = v < rend;
-        if (p1 - p0 <= CAP) {
-            // zero the CTA's range, accumulate per row in smem, write the range once
+        const bool own = v < rend;
+        if (cta_smem) {
             for (int q = threadIdx.x; q < p1 - p0; q += GATHER_BLOCK) {
                 sK[q] = 0.0;
                 sM[q] = 0.0;
             }
-            __syncthreads();
-            if (own) {
-                int lo = __ldg(row_ptr + v) - p0;
-                gather_row<DIM>(v, coords, ns, cst, elems, eld, nptr, nelem, nslot, K ? sK + lo : nullptr,
-                                M ? sM + lo : nullptr);
+        }
+        __syncthreads();
+        if (own) {
+            int lo = __ldg(row_ptr + v), L = __ldg(row_ptr + v + 1) - lo;
+            int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
+            double xv[DIM];
+#pragma unroll
+            for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + v * ns);
+            const bool fast = L <= Cfg::ROW_CAP;
+            if (fast) {
+                for (int s = 0; s < L; s++) {
+                    int64_t w = __ldg(col_idx + lo + s);
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) F[(s * DIM + c) * GATHER_BLOCK] = __ldg(coords + c * cst + w * ns) - xv[c];
+                }
             }
-            __syncthreads();
+            if (cta_smem) {
+                double* aK = K ? sK + (lo - p0) : nullptr;
+                double* aM = M ? sM + (lo - p0) : nullptr;
+                if (fast) gather_row<DIM, true>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
+                else gather_row<DIM, false>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
+            } else {
+                // CTA range larger than the smem budget: same ownership, accumulate in place in HBM
+                for (int q = 0; q < L; q++) {
+                    if (K) K[lo + q] = 0.0;
+                    if (M) M[lo + q] = 0.0;
+                }
+                double* aK = K ? K + lo : nullptr;
+                double* aM = M ? M + lo : nullptr;
+                if (fast) gather_row<DIM, true>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
+                else gather_row<DIM, false>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
+            }
+        }
+        __syncthreads();
+        if (cta_smem) {
             for (int q = threadIdx.x; q < p1 - p0; q += GATHER_BLOCK) {
                 if (K) stcs(K + p0 + q, sK[q]);
                 if (M) stcs(M + p0 + q, sM[q]);
             }
-            __syncthreads();
-        } else if (own) {
-            // long rows: same per-row ownership, accumulated in place in HBM
-            int lo = __ldg(row_ptr + v), hi = __ldg(row_ptr + v + 1);
-            for (int q = lo; q < hi; q++) {
-                if (K) K[q] = 0.0;
-                if (M) M[q] = 0.0;
-            }
-            gather_row<DIM>(v, coords, ns, cst, elems, eld, nptr, nelem, nslot, K ? K + lo : nullptr,
-                            M ? M + lo : nullptr);
         }
+        __syncthreads();
     }
 }
 
@@ -271,7 +343,6 @@ extern "C" vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne, const doub
     if (mode != VB_ASSEMBLE_ATOMIC && mode != VB_ASSEMBLE_GATHER) { set_error("fem_p1_assemble: unknown mode %d", mode); return VB_ERR_ARG; }
     if (ne > 0 && (!coords || !elems)) { set_error("fem_p1_assemble: NULL %s", !coords ? "coords" : "elems"); return VB_ERR_ARG; }
     if (elem_ld < ne) { set_error("fem_p1_assemble: elem_ld < ne"); return VB_ERR_ARG; }
-    (void)col_idx;
     cudaStream_t s = cs(stream);
     const bool want_global = K_vals || M_vals;
     vb_status st = VB_OK;
@@ -294,21 +365,18 @@ extern "C" vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne, const doub
         return launch_check("fem_p1_assemble(atomic)");
     }
     // gather mode
-    if (want_global && (!row_ptr || !node_elem_ptr || !node_elem || !node_elem_slot)) {
-        set_error("fem_p1_assemble: gather mode needs row_ptr, node_elem_ptr, node_elem, node_elem_slot");
+    if (want_global && (!row_ptr || !col_idx || !node_elem_ptr || !node_elem_slot)) {
+        set_error("fem_p1_assemble: gather mode needs row_ptr, col_idx, node_elem_ptr, node_elem_slot");
         return VB_ERR_ARG;
     }
     if (want_global && nn > 0) {
+        unsigned g = (unsigned)((nn + GATHER_BLOCK - 1) / GATHER_BLOCK);
         if (dim == 2) {
-            size_t sm = 2 * GatherCfg<2>::CAP * sizeof(double);
-            unsigned g = (unsigned)((nn + GATHER_BLOCK - 1) / GATHER_BLOCK);
-            assemble_gather_k<2><<<g, GATHER_BLOCK, sm, s>>>(nn, coords, node_stride, comp_stride, elems, elem_ld, row_ptr,
-                                                             node_elem_ptr, node_elem, node_elem_slot, K_vals, M_vals);
+            assemble_gather_k<2><<<g, GATHER_BLOCK, GatherCfg<2>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
+                                                                         col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
         } else {
-            size_t sm = 2 * GatherCfg<3>::CAP * sizeof(double);
-            unsigned g = (unsigned)((nn + GATHER_BLOCK - 1) / GATHER_BLOCK);
-            assemble_gather_k<3><<<g, GATHER_BLOCK, sm, s>>>(nn, coords, node_stride, comp_stride, elems, elem_ld, row_ptr,
-                                                             node_elem_ptr, node_elem, node_elem_slot, K_vals, M_vals);
+            assemble_gather_k<3><<<g, GATHER_BLOCK, GatherCfg<3>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
+                                                                         col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
         }
         if ((st = launch_check("fem_p1_assemble(gather)")) != VB_OK) return st;
     }

@@ -104,11 +104,15 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
         int32_t ea = node_elem[i];
         int64_t e = ea >> 2;
         int a = ea & 3;
+        // byte 0: in-row offset of the row's own vertex (the diagonal); bytes
+        // 1..nv-1: offsets of the element's other vertices, ascending local index
         uint32_t packed = 0;
+        int byte = 1;
         for (int b = 0; b < nv; b++) {
             int pos = lower_bound_s(L, st, cnt, elems[b * eld + e]);
             if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
-            packed |= (uint32_t)(pos & 0xff) << (8 * b);
+            int sh = (b == a) ? 0 : 8 * byte++;
+            packed |= (uint32_t)(pos & 0xff) << sh;
         }
         if (slots) slots[i] = packed;
     }

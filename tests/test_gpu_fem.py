@@ -80,8 +80,10 @@ def test_pattern_and_plans_bit_exact(dev, kind, n):
         assert len(inc) == np.count_nonzero(elems == v)
         for k, (ee, aa) in enumerate(zip(e, a)):
             sl = nsl[nptr[v] + k]
-            for b in range(nv):
-                assert ci[rp[v] + ((sl >> (8 * b)) & 0xFF)] == elems[b, ee]
+            others = [b for b in range(nv) if b != aa]
+            assert ci[rp[v] + (sl & 0xFF)] == v                          # byte 0: the diagonal
+            for j, b in enumerate(others):
+                assert ci[rp[v] + ((sl >> (8 * (j + 1))) & 0xFF)] == elems[b, ee]
 
 
 # ---------------------------------------------------------------- assembly
