@@ -157,64 +157,77 @@ __global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restr
 }
 
 // ------------------------------------------------------------ gather (deterministic) variant
-// One thread owns row v.  The edge vectors f_s = x_{col(s)} - x_v to every
-// column of the row are formed once per row (shared memory, indexed by the
-// in-row slot).  Each incidence (e, a) of v then needs only its plan word
-// (slots of v and of the element's other vertices): with v as the base vertex
-// (any base gives the same K_e) the element's tjac rows are
-// f_1..f_d, adj(tjac) has columns h_j = cross products of the other f's,
+// One thread owns row v; a CTA owns GATHER_BLOCK consecutive rows, i.e. one
+// contiguous range of the CSR arrays and one contiguous range of the gather
+// plan, both staged in shared memory with coalesced loads.  The edge vectors
+// f_s = x_{col(s)} - x_v to every column of the row are formed once per row
+// (shared memory, indexed by in-row slot).  Each incidence (e, a) of v needs
+// only its plan word (slots of the element's other vertices): with v as the
+// base vertex (any base gives the same K_e) tjac has rows f_1..f_d,
+// adj(tjac) has columns h_j (cross products of the other f's), and
 //   grad phi_{o_j} = h_j / det,  grad phi_a = h_a / det,  h_a = -sum_j h_j,
-//   K_e[a][o_j] = (h_a . h_j) / (d! |det|),  K_e[a][a] = -sum_j K_e[a][o_j],
-//   M_e[a][o_j] = |det| / (d! (d+1)(d+2)),    M_e[a][a] = 2 M_e[a][o_j],
-// summed in ascending element order (deterministic; the oracle's order).
+//   K_e[a][o_j] = (h_a . h_j) / (d! |det|),   M_e[a][o_j] = |det| / (d! (d+1)(d+2)).
+// Off-diagonal entries are summed in ascending element order (the oracle's
+// order); the diagonal follows from the partition of unity sum_b phi_b = 1:
+//   K_vv = -sum_{w != v} K_vw,   M_vv = (2/d) sum_{w != v} M_vw.
 constexpr int GATHER_BLOCK = 64;
 template <int DIM>
 struct GatherCfg {
-    static constexpr int ROW_CAP = DIM == 2 ? 8 : 16;        // columns per row kept in smem (edge vectors)
-    static constexpr int CTA_CAP = GATHER_BLOCK * ROW_CAP;   // CSR entries per CTA kept in smem
-    static constexpr size_t SMEM = (size_t)(ROW_CAP * DIM * GATHER_BLOCK + 2 * CTA_CAP) * sizeof(double);
+    static constexpr int ROW_CAP = DIM == 2 ? 8 : 16;          // columns per row with smem edge vectors
+    static constexpr int CTA_CAP = GATHER_BLOCK * ROW_CAP;     // CSR entries per CTA staged in smem
+    static constexpr int SLOT_CAP = GATHER_BLOCK * (DIM == 2 ? 8 : 28);  // plan words per CTA in smem
+    static constexpr size_t SMEM = (size_t)(ROW_CAP * DIM * GATHER_BLOCK + 2 * CTA_CAP) * sizeof(double) +
+                                   (size_t)(SLOT_CAP + CTA_CAP) * sizeof(uint32_t);
 };
 
+// 1/x to ~1 ulp: hardware seed + two Newton steps (x > 0, normal)
+__device__ __forceinline__ double rcp_nr(double x) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    y = fma(y, fma(-x, y, 1.0), y);
+    y = fma(y, fma(-x, y, 1.0), y);
+    return y;
+}
+
 template <int DIM, bool FAST>
-__device__ __forceinline__ void edge_vec(int s, const double* F, int lo, const int32_t* __restrict__ col_idx,
+__device__ __forceinline__ void edge_vec(int s, const double* F, const int32_t* cols,
                                          const double* __restrict__ coords, int64_t ns, int64_t cst,
                                          const double (&xv)[DIM], double (&f)[DIM]) {
     if (FAST) {
 #pragma unroll
         for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * GATHER_BLOCK];
     } else {
-        int64_t w = __ldg(col_idx + lo + s);
+        int64_t w = cols[s];
 #pragma unroll
         for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
     }
 }
 
-template <int DIM, bool FAST, typename Acc>
-__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __restrict__ nslot, const double* F, int lo,
-                                           const int32_t* __restrict__ col_idx, const double* __restrict__ coords,
-                                           int64_t ns, int64_t cst, const double (&xv)[DIM], Acc* accK, Acc* accM) {
+// Off-diagonal contributions of incidences [i0, i1) of one row.
+template <int DIM, bool FAST>
+__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots, const double* F, const int32_t* cols,
+                                           const double* __restrict__ coords, int64_t ns, int64_t cst,
+                                           const double (&xv)[DIM], double* accK, double* accM) {
 #pragma unroll 2
     for (int i = i0; i < i1; i++) {
-        uint32_t sl = __ldcs(nslot + i);
-        int s0 = sl & 0xff;
+        uint32_t sl = slots[i];
         if constexpr (DIM == 3) {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff, s3 = sl >> 24;
             double f1[3], f2[3], f3[3];
-            edge_vec<3, FAST>(s1, F, lo, col_idx, coords, ns, cst, xv, f1);
-            edge_vec<3, FAST>(s2, F, lo, col_idx, coords, ns, cst, xv, f2);
-            edge_vec<3, FAST>(s3, F, lo, col_idx, coords, ns, cst, xv, f3);
+            edge_vec<3, FAST>(s1, F, cols, coords, ns, cst, xv, f1);
+            edge_vec<3, FAST>(s2, F, cols, coords, ns, cst, xv, f2);
+            edge_vec<3, FAST>(s3, F, cols, coords, ns, cst, xv, f3);
             double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
                             fma(f2[0], f3[1], -f2[1] * f3[0])};
             double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
                             fma(f3[0], f1[1], -f3[1] * f1[0])};
             double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
                             fma(f1[0], f2[1], -f1[1] * f2[0])};
-            double det = fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2]));
-            double ad = fabs(det);
-            double r = 1.0 / (6.0 * ad);
+            double ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
+            double r = -rcp_nr(6.0 * ad);
             double ha[3];
 #pragma unroll
-            for (int c = 0; c < 3; c++) ha[c] = -r * (h1[c] + h2[c] + h3[c]);
+            for (int c = 0; c < 3; c++) ha[c] = r * ((h1[c] + h2[c]) + h3[c]);
             double k1 = fma(ha[0], h1[0], fma(ha[1], h1[1], ha[2] * h1[2]));
             double k2 = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
             double k3 = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
@@ -223,39 +236,47 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __res
                 accK[s1] += k1;
                 accK[s2] += k2;
                 accK[s3] += k3;
-                accK[s0] -= (k1 + k2) + k3;
             }
             if (accM) {
                 accM[s1] += m;
                 accM[s2] += m;
                 accM[s3] += m;
-                accM[s0] += 2.0 * m;
             }
         } else {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
             double f1[2], f2[2];
-            edge_vec<2, FAST>(s1, F, lo, col_idx, coords, ns, cst, xv, f1);
-            edge_vec<2, FAST>(s2, F, lo, col_idx, coords, ns, cst, xv, f2);
+            edge_vec<2, FAST>(s1, F, cols, coords, ns, cst, xv, f1);
+            edge_vec<2, FAST>(s2, F, cols, coords, ns, cst, xv, f2);
             // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
-            double det = fma(f1[0], f2[1], -f1[1] * f2[0]);
-            double ad = fabs(det);
-            double r = 1.0 / (2.0 * ad);
-            double hax = -r * (f2[1] - f1[1]), hay = -r * (f1[0] - f2[0]);
+            double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
+            double r = -rcp_nr(2.0 * ad);
+            double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
             double k1 = fma(hax, f2[1], -hay * f2[0]);
             double k2 = fma(-hax, f1[1], hay * f1[0]);
             double m = ad * (1.0 / 24.0);
             if (accK) {
                 accK[s1] += k1;
                 accK[s2] += k2;
-                accK[s0] -= k1 + k2;
             }
             if (accM) {
                 accM[s1] += m;
                 accM[s2] += m;
-                accM[s0] += 2.0 * m;
             }
         }
     }
+}
+
+// diagonal of row (slot s0 of L) from the off-diagonal sums (partition of unity)
+template <int DIM>
+__device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* accM) {
+    double sk = 0.0, sm = 0.0;
+    for (int s = 0; s < L; s++) {
+        if (s == s0) continue;
+        if (accK) sk += accK[s];
+        if (accM) sm += accM[s];
+    }
+    if (accK) accK[s0] = -sk;
+    if (accM) accM[s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
 }
 
 template <int DIM>
@@ -271,52 +292,57 @@ __global__ void __launch_bounds__(GATHER_BLOCK) assemble_gather_k(int64_t nn, co
     double* F = smem + threadIdx.x;                                  // [ROW_CAP*DIM][GATHER_BLOCK]
     double* sK = smem + Cfg::ROW_CAP * DIM * GATHER_BLOCK;            // CTA-contiguous CSR range
     double* sM = sK + Cfg::CTA_CAP;
+    uint32_t* sSlot = reinterpret_cast<uint32_t*>(sM + Cfg::CTA_CAP);  // CTA-contiguous plan range
+    int32_t* sCol = reinterpret_cast<int32_t*>(sSlot + Cfg::SLOT_CAP);
     for (int64_t r0 = (int64_t)blockIdx.x * GATHER_BLOCK; r0 < nn; r0 += (int64_t)gridDim.x * GATHER_BLOCK) {
-        int64_t rend = r0 + GATHER_BLOCK < nn ? r0 + GATHER_BLOCK : nn;
-        int32_t p0 = __ldg(row_ptr + r0), p1 = __ldg(row_ptr + rend);
-        const bool cta_smem = (p1 - p0) <= Cfg::CTA_CAP;
-        int64_t v = r0 + threadIdx.x;
-        const bool own = v < rend;
-        if (cta_smem) {
+        const int64_t rend = r0 + GATHER_BLOCK < nn ? r0 + GATHER_BLOCK : nn;
+        const int32_t p0 = __ldg(row_ptr + r0), p1 = __ldg(row_ptr + rend);
+        const int32_t q0 = __ldg(nptr + r0), q1 = __ldg(nptr + rend);
+        const bool fitsK = (p1 - p0) <= Cfg::CTA_CAP;
+        const bool fitsS = (q1 - q0) <= Cfg::SLOT_CAP;
+        if (fitsK) {
             for (int q = threadIdx.x; q < p1 - p0; q += GATHER_BLOCK) {
                 sK[q] = 0.0;
                 sM[q] = 0.0;
+                sCol[q] = __ldcs(col_idx + p0 + q);
             }
         }
+        if (fitsS)
+            for (int q = threadIdx.x; q < q1 - q0; q += GATHER_BLOCK) sSlot[q] = __ldcs(nslot + q0 + q);
         __syncthreads();
-        if (own) {
-            int lo = __ldg(row_ptr + v), L = __ldg(row_ptr + v + 1) - lo;
-            int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
+        const int64_t v = r0 + threadIdx.x;
+        if (v < rend) {
+            const int lo = __ldg(row_ptr + v), L = __ldg(row_ptr + v + 1) - lo;
+            const int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
+            const int32_t* cols = fitsK ? sCol + (lo - p0) : col_idx + lo;
+            const uint32_t* slots = fitsS ? sSlot - q0 : nslot;
             double xv[DIM];
 #pragma unroll
             for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + v * ns);
-            const bool fast = L <= Cfg::ROW_CAP;
-            if (fast) {
+            int s0 = 0;  // diagonal slot
+            for (int s = 0; s < L; s++)
+                if (cols[s] == v) s0 = s;
+            double* aK = K ? (fitsK ? sK + (lo - p0) : K + lo) : nullptr;
+            double* aM = M ? (fitsK ? sM + (lo - p0) : M + lo) : nullptr;
+            if (!fitsK)
+                for (int q = 0; q < L; q++) {
+                    if (aK) aK[q] = 0.0;
+                    if (aM) aM[q] = 0.0;
+                }
+            if (L <= Cfg::ROW_CAP) {
                 for (int s = 0; s < L; s++) {
-                    int64_t w = __ldg(col_idx + lo + s);
+                    int64_t w = cols[s];
 #pragma unroll
                     for (int c = 0; c < DIM; c++) F[(s * DIM + c) * GATHER_BLOCK] = __ldg(coords + c * cst + w * ns) - xv[c];
                 }
-            }
-            if (cta_smem) {
-                double* aK = K ? sK + (lo - p0) : nullptr;
-                double* aM = M ? sM + (lo - p0) : nullptr;
-                if (fast) gather_row<DIM, true>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
-                else gather_row<DIM, false>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
+                gather_row<DIM, true>(i0, i1, slots, F, cols, coords, ns, cst, xv, aK, aM);
             } else {
-                // CTA range larger than the smem budget: same ownership, accumulate in place in HBM
-                for (int q = 0; q < L; q++) {
-                    if (K) K[lo + q] = 0.0;
-                    if (M) M[lo + q] = 0.0;
-                }
-                double* aK = K ? K + lo : nullptr;
-                double* aM = M ? M + lo : nullptr;
-                if (fast) gather_row<DIM, true>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
-                else gather_row<DIM, false>(i0, i1, nslot, F, lo, col_idx, coords, ns, cst, xv, aK, aM);
+                gather_row<DIM, false>(i0, i1, slots, F, cols, coords, ns, cst, xv, aK, aM);
             }
+            if (L > 0) finish_row<DIM>(L, s0, aK, aM);
         }
         __syncthreads();
-        if (cta_smem) {
+        if (fitsK) {
             for (int q = threadIdx.x; q < p1 - p0; q += GATHER_BLOCK) {
                 if (K) stcs(K + p0 + q, sK[q]);
                 if (M) stcs(M + p0 + q, sM[q]);
