@@ -396,6 +396,12 @@ extern "C" vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne, const doub
         return VB_ERR_ARG;
     }
     if (want_global && nn > 0) {
+        static bool smem_opt_in = false;  // > 48 KB dynamic shared memory needs an opt-in per kernel
+        if (!smem_opt_in) {
+            cudaFuncSetAttribute(assemble_gather_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GatherCfg<2>::SMEM);
+            cudaFuncSetAttribute(assemble_gather_k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GatherCfg<3>::SMEM);
+            smem_opt_in = true;
+        }
         unsigned g = (unsigned)((nn + GATHER_BLOCK - 1) / GATHER_BLOCK);
         if (dim == 2) {
             assemble_gather_k<2><<<g, GATHER_BLOCK, GatherCfg<2>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
