@@ -170,13 +170,12 @@ __global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restr
 // Off-diagonal entries are summed in ascending element order (the oracle's
 // order); the diagonal follows from the partition of unity sum_b phi_b = 1:
 //   K_vv = -sum_{w != v} K_vw,   M_vv = (2/d) sum_{w != v} M_vw.
-constexpr int GATHER_BLOCK = 64;
+constexpr int GATHER_BLOCK = 32;
 template <int DIM>
 struct GatherCfg {
-    static constexpr int ROW_CAP = DIM == 2 ? 8 : 16;          // columns per row with smem edge vectors
-    static constexpr int CTA_CAP = GATHER_BLOCK * ROW_CAP;     // CSR entries per CTA staged in smem
-    static constexpr int SLOT_CAP = GATHER_BLOCK * (DIM == 2 ? 8 : 28);  // plan words per CTA in smem
-    static constexpr size_t SMEM = (size_t)(ROW_CAP * DIM * GATHER_BLOCK + 2 * CTA_CAP) * sizeof(double) +
+    static constexpr int CTA_CAP = GATHER_BLOCK * (DIM == 2 ? 8 : 16);   // CSR entries per CTA staged in smem
+    static constexpr int SLOT_CAP = GATHER_BLOCK * (DIM == 2 ? 8 : 28);  // plan words per CTA staged in smem
+    static constexpr size_t SMEM = (size_t)(DIM + 2) * CTA_CAP * sizeof(double) +
                                    (size_t)(SLOT_CAP + CTA_CAP) * sizeof(uint32_t);
 };
 
@@ -189,34 +188,19 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return y;
 }
 
-template <int DIM, bool FAST>
-__device__ __forceinline__ void edge_vec(int s, const double* F, const int32_t* cols,
-                                         const double* __restrict__ coords, int64_t ns, int64_t cst,
-                                         const double (&xv)[DIM], double (&f)[DIM]) {
-    if (FAST) {
-#pragma unroll
-        for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * GATHER_BLOCK];
-    } else {
-        int64_t w = cols[s];
-#pragma unroll
-        for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
-    }
-}
-
-// Off-diagonal contributions of incidences [i0, i1) of one row.
-template <int DIM, bool FAST>
-__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots, const double* F, const int32_t* cols,
-                                           const double* __restrict__ coords, int64_t ns, int64_t cst,
-                                           const double (&xv)[DIM], double* accK, double* accM) {
+// Off-diagonal contributions of incidences [i0, i1) of one row.  EV(s, f)
+// yields the edge vector from the row's vertex to its column s.
+template <int DIM, typename EV>
+__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots, EV ev, double* accK, double* accM) {
 #pragma unroll 2
     for (int i = i0; i < i1; i++) {
         uint32_t sl = slots[i];
         if constexpr (DIM == 3) {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff, s3 = sl >> 24;
             double f1[3], f2[3], f3[3];
-            edge_vec<3, FAST>(s1, F, cols, coords, ns, cst, xv, f1);
-            edge_vec<3, FAST>(s2, F, cols, coords, ns, cst, xv, f2);
-            edge_vec<3, FAST>(s3, F, cols, coords, ns, cst, xv, f3);
+            ev(s1, f1);
+            ev(s2, f2);
+            ev(s3, f3);
             double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
                             fma(f2[0], f3[1], -f2[1] * f3[0])};
             double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
@@ -245,8 +229,8 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots
         } else {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
             double f1[2], f2[2];
-            edge_vec<2, FAST>(s1, F, cols, coords, ns, cst, xv, f1);
-            edge_vec<2, FAST>(s2, F, cols, coords, ns, cst, xv, f2);
+            ev(s1, f1);
+            ev(s2, f2);
             // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
             double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
             double r = -rcp_nr(2.0 * ad);
@@ -266,7 +250,7 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots
     }
 }
 
-// diagonal of row (slot s0 of L) from the off-diagonal sums (partition of unity)
+// diagonal of a row (slot s0 of L) from the off-diagonal sums (partition of unity)
 template <int DIM>
 __device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* accM) {
     double sk = 0.0, sm = 0.0;
@@ -288,67 +272,90 @@ __global__ void __launch_bounds__(GATHER_BLOCK) assemble_gather_k(int64_t nn, co
                                                                   const uint32_t* __restrict__ nslot,
                                                                   double* __restrict__ K, double* __restrict__ M) {
     using Cfg = GatherCfg<DIM>;
+    constexpr int CAP = Cfg::CTA_CAP;
     extern __shared__ double smem[];
-    double* F = smem + threadIdx.x;                                  // [ROW_CAP*DIM][GATHER_BLOCK]
-    double* sK = smem + Cfg::ROW_CAP * DIM * GATHER_BLOCK;            // CTA-contiguous CSR range
-    double* sM = sK + Cfg::CTA_CAP;
-    uint32_t* sSlot = reinterpret_cast<uint32_t*>(sM + Cfg::CTA_CAP);  // CTA-contiguous plan range
+    double* F = smem;                        // [DIM][CAP]  column coordinates, then edge vectors
+    double* sK = smem + DIM * CAP;           // [CAP] CTA-contiguous CSR range of K
+    double* sM = sK + CAP;                   // [CAP]
+    uint32_t* sSlot = reinterpret_cast<uint32_t*>(sM + CAP);     // [SLOT_CAP] plan range
     int32_t* sCol = reinterpret_cast<int32_t*>(sSlot + Cfg::SLOT_CAP);
+    const int t = threadIdx.x;
     for (int64_t r0 = (int64_t)blockIdx.x * GATHER_BLOCK; r0 < nn; r0 += (int64_t)gridDim.x * GATHER_BLOCK) {
         const int64_t rend = r0 + GATHER_BLOCK < nn ? r0 + GATHER_BLOCK : nn;
         const int32_t p0 = __ldg(row_ptr + r0), p1 = __ldg(row_ptr + rend);
         const int32_t q0 = __ldg(nptr + r0), q1 = __ldg(nptr + rend);
-        const bool fitsK = (p1 - p0) <= Cfg::CTA_CAP;
-        const bool fitsS = (q1 - q0) <= Cfg::SLOT_CAP;
-        if (fitsK) {
-            for (int q = threadIdx.x; q < p1 - p0; q += GATHER_BLOCK) {
-                sK[q] = 0.0;
-                sM[q] = 0.0;
-                sCol[q] = __ldcs(col_idx + p0 + q);
-            }
-        }
-        if (fitsS)
-            for (int q = threadIdx.x; q < q1 - q0; q += GATHER_BLOCK) sSlot[q] = __ldcs(nslot + q0 + q);
-        __syncthreads();
-        const int64_t v = r0 + threadIdx.x;
-        if (v < rend) {
-            const int lo = __ldg(row_ptr + v), L = __ldg(row_ptr + v + 1) - lo;
-            const int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
-            const int32_t* cols = fitsK ? sCol + (lo - p0) : col_idx + lo;
-            const uint32_t* slots = fitsS ? sSlot - q0 : nslot;
-            double xv[DIM];
+        const int np = p1 - p0, nq = q1 - q0;
+        const int64_t v = r0 + t;
+        const bool own = v < rend;
+        int lo = 0, L = 0, i0 = 0, i1 = 0;
+        double xv[DIM];
+        if (own) {
+            lo = __ldg(row_ptr + v);
+            L = __ldg(row_ptr + v + 1) - lo;
+            i0 = __ldg(nptr + v);
+            i1 = __ldg(nptr + v + 1);
 #pragma unroll
             for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + v * ns);
-            int s0 = 0;  // diagonal slot
-            for (int s = 0; s < L; s++)
-                if (cols[s] == v) s0 = s;
-            double* aK = K ? (fitsK ? sK + (lo - p0) : K + lo) : nullptr;
-            double* aM = M ? (fitsK ? sM + (lo - p0) : M + lo) : nullptr;
-            if (!fitsK)
-                for (int q = 0; q < L; q++) {
-                    if (aK) aK[q] = 0.0;
-                    if (aM) aM[q] = 0.0;
-                }
-            if (L <= Cfg::ROW_CAP) {
-                for (int s = 0; s < L; s++) {
-                    int64_t w = cols[s];
-#pragma unroll
-                    for (int c = 0; c < DIM; c++) F[(s * DIM + c) * GATHER_BLOCK] = __ldg(coords + c * cst + w * ns) - xv[c];
-                }
-                gather_row<DIM, true>(i0, i1, slots, F, cols, coords, ns, cst, xv, aK, aM);
-            } else {
-                gather_row<DIM, false>(i0, i1, slots, F, cols, coords, ns, cst, xv, aK, aM);
-            }
-            if (L > 0) finish_row<DIM>(L, s0, aK, aM);
         }
-        __syncthreads();
-        if (fitsK) {
-            for (int q = threadIdx.x; q < p1 - p0; q += GATHER_BLOCK) {
+        if (np <= CAP && nq <= Cfg::SLOT_CAP) {
+            // stage the CTA's CSR columns and plan words (coalesced), zero the accumulators
+#pragma unroll 4
+            for (int q = t; q < np; q += GATHER_BLOCK) sCol[q] = __ldcs(col_idx + p0 + q);
+#pragma unroll 4
+            for (int q = t; q < nq; q += GATHER_BLOCK) sSlot[q] = __ldcs(nslot + q0 + q);
+            __syncthreads();
+            // gather the coordinates of every column of the CTA's range (independent loads)
+#pragma unroll 4
+            for (int q = t; q < np; q += GATHER_BLOCK) {
+                int64_t w = sCol[q];
+#pragma unroll
+                for (int c = 0; c < DIM; c++) F[c * CAP + q] = __ldg(coords + c * cst + w * ns);
+                sK[q] = 0.0;
+                sM[q] = 0.0;
+            }
+            __syncthreads();
+            if (own) {
+                const int b = lo - p0;
+                int s0 = 0;
+                for (int s = 0; s < L; s++) {
+                    if (sCol[b + s] == v) s0 = s;
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) F[c * CAP + b + s] -= xv[c];
+                }
+                auto ev = [&](int s, double(&f)[DIM]) {
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) f[c] = F[c * CAP + b + s];
+                };
+                double* aK = K ? sK + b : nullptr;
+                double* aM = M ? sM + b : nullptr;
+                gather_row<DIM>(i0, i1, sSlot - q0, ev, aK, aM);
+                if (L > 0) finish_row<DIM>(L, s0, aK, aM);
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int q = t; q < np; q += GATHER_BLOCK) {
                 if (K) stcs(K + p0 + q, sK[q]);
                 if (M) stcs(M + p0 + q, sM[q]);
             }
+            __syncthreads();
+        } else if (own) {
+            // CTA range larger than the smem budget: same ownership, everything in place in HBM
+            double* aK = K ? K + lo : nullptr;
+            double* aM = M ? M + lo : nullptr;
+            int s0 = 0;
+            for (int q = 0; q < L; q++) {
+                if (aK) aK[q] = 0.0;
+                if (aM) aM[q] = 0.0;
+                if (__ldg(col_idx + lo + q) == v) s0 = q;
+            }
+            auto ev = [&](int s, double(&f)[DIM]) {
+                int64_t w = __ldg(col_idx + lo + s);
+#pragma unroll
+                for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
+            };
+            gather_row<DIM>(i0, i1, nslot, ev, aK, aM);
+            if (L > 0) finish_row<DIM>(L, s0, aK, aM);
         }
-        __syncthreads();
     }
 }
 
