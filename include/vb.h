@@ -192,7 +192,12 @@ VB_API vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne,
  * mode VB_ASSEMBLE_GATHER: deterministic segmented reduction: one thread per
  *   row v sums the contributions of its incidences in ascending element order
  *   (the oracle's order) in on-chip memory and writes each CSR entry once; no
- *   atomics, no zero-fill; needs node_elem_ptr/node_elem/node_elem_slot.
+ *   atomics, no zero-fill.  Needs col_idx, node_elem_ptr and node_elem_slot
+ *   (node_elem is not read).  col_idx and node_elem_slot are streamed with
+ *   16-byte TMA bulk copies: both must be 16-byte aligned and readable up to
+ *   the next multiple of 4 entries (torch allocations satisfy this).
+ *   Diagonals follow from the partition of unity sum_b phi_b = 1
+ *   (K_vv = -sum_{w!=v} K_vw, M_vv = (2/d) sum_{w!=v} M_vw).
  *   Bitwise reproducible.
  * K_vals / M_vals (nnz each) are nullable (skip that matrix).
  * K_local / M_local (nullable): K3D / M3D page arrays (nv x nv pages, ld = ne),

@@ -170,14 +170,53 @@ __global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restr
 // Off-diagonal entries are summed in ascending element order (the oracle's
 // order); the diagonal follows from the partition of unity sum_b phi_b = 1:
 //   K_vv = -sum_{w != v} K_vw,   M_vv = (2/d) sum_{w != v} M_vw.
-constexpr int GATHER_BLOCK = 32;
+// Persistent, software-pipelined: each CTA is one warp owning blocks of 32
+// consecutive rows.  While block k is computed, the CSR columns and plan words
+// of block k+2 stream in through TMA bulk copies (cp.async.bulk + mbarrier) and
+// the coordinates of every column of block k+1 are gathered with cp.async, so
+// no thread waits on HBM/L2 latency in the compute phase.
+constexpr int GATHER_ROWS = 32;
 template <int DIM>
 struct GatherCfg {
-    static constexpr int CTA_CAP = GATHER_BLOCK * (DIM == 2 ? 8 : 16);   // CSR entries per CTA staged in smem
-    static constexpr int SLOT_CAP = GATHER_BLOCK * (DIM == 2 ? 8 : 28);  // plan words per CTA staged in smem
-    static constexpr size_t SMEM = (size_t)(DIM + 2) * CTA_CAP * sizeof(double) +
-                                   (size_t)(SLOT_CAP + CTA_CAP) * sizeof(uint32_t);
+    static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? 8 : 16);        // CSR entries per block in smem
+    static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block in smem
+    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
+    static constexpr int RING = 3;
+    static constexpr size_t RING_BYTES = (size_t)(COLS_PAD + SLOTS_PAD) * 4;
+    static constexpr size_t F_OFF = RING * RING_BYTES;
+    static constexpr size_t ACC_OFF = F_OFF + (size_t)2 * DIM * CAP * 8;
+    static constexpr size_t BAR_OFF = ACC_OFF + (size_t)2 * CAP * 8;
+    static constexpr size_t SMEM = BAR_OFF + RING * 8;
+    static_assert(RING_BYTES % 16 == 0, "TMA destinations must stay 16-byte aligned");
 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // 1/x to ~1 ulp: hardware seed + two Newton steps (x > 0, normal)
 __device__ __forceinline__ double rcp_nr(double x) {
@@ -188,8 +227,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return y;
 }
 
-// Off-diagonal contributions of incidences [i0, i1) of one row.  EV(s, f)
-// yields the edge vector from the row's vertex to its column s.
+// Off-diagonal contributions of incidences [i0, i1) of one row: K into accK,
+// |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row).  EV(s, f) yields
+// the edge vector from the row's vertex to its column s.
 template <int DIM, typename EV>
 __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots, EV ev, double* accK, double* accM) {
 #pragma unroll 2
@@ -208,23 +248,22 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots
             double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
                             fma(f1[0], f2[1], -f1[1] * f2[0])};
             double ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
-            double r = -rcp_nr(6.0 * ad);
+            double r = rcp_nr(ad) * (-1.0 / 6.0);
             double ha[3];
 #pragma unroll
             for (int c = 0; c < 3; c++) ha[c] = r * ((h1[c] + h2[c]) + h3[c]);
             double k1 = fma(ha[0], h1[0], fma(ha[1], h1[1], ha[2] * h1[2]));
             double k2 = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
             double k3 = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
-            double m = ad * (1.0 / 120.0);
             if (accK) {
                 accK[s1] += k1;
                 accK[s2] += k2;
                 accK[s3] += k3;
             }
             if (accM) {
-                accM[s1] += m;
-                accM[s2] += m;
-                accM[s3] += m;
+                accM[s1] += ad;
+                accM[s2] += ad;
+                accM[s3] += ad;
             }
         } else {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
@@ -233,113 +272,208 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots
             ev(s2, f2);
             // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
             double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
-            double r = -rcp_nr(2.0 * ad);
+            double r = rcp_nr(ad) * -0.5;
             double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
             double k1 = fma(hax, f2[1], -hay * f2[0]);
             double k2 = fma(-hax, f1[1], hay * f1[0]);
-            double m = ad * (1.0 / 24.0);
             if (accK) {
                 accK[s1] += k1;
                 accK[s2] += k2;
             }
             if (accM) {
-                accM[s1] += m;
-                accM[s2] += m;
+                accM[s1] += ad;
+                accM[s2] += ad;
             }
         }
     }
 }
 
-// diagonal of a row (slot s0 of L) from the off-diagonal sums (partition of unity)
+// Diagonal of a row (slot s0 of L) from the off-diagonal sums (partition of
+// unity), and the |det| sums of M scaled to M entries.
 template <int DIM>
 __device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* accM) {
+    constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;     // 1/(d! (d+1)(d+2))
     double sk = 0.0, sm = 0.0;
     for (int s = 0; s < L; s++) {
         if (s == s0) continue;
         if (accK) sk += accK[s];
-        if (accM) sm += accM[s];
+        if (accM) {
+            double m = accM[s] * MS;
+            accM[s] = m;
+            sm += m;
+        }
     }
     if (accK) accK[s0] = -sk;
     if (accM) accM[s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
 }
 
+struct BlockBounds {
+    int64_t r0, r1;
+    int32_t p0, p1, q0, q1;
+    bool valid, fit;
+};
+
 template <int DIM>
-__global__ void __launch_bounds__(GATHER_BLOCK) assemble_gather_k(int64_t nn, const double* __restrict__ coords,
-                                                                  int64_t ns, int64_t cst,
-                                                                  const int32_t* __restrict__ row_ptr,
-                                                                  const int32_t* __restrict__ col_idx,
-                                                                  const int32_t* __restrict__ nptr,
-                                                                  const uint32_t* __restrict__ nslot,
-                                                                  double* __restrict__ K, double* __restrict__ M) {
+__device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, int64_t nn,
+                                                    const int32_t* __restrict__ row_ptr,
+                                                    const int32_t* __restrict__ nptr) {
+    BlockBounds B{};
+    B.valid = b < nblocks;
+    if (!B.valid) return B;
+    B.r0 = b * GATHER_ROWS;
+    B.r1 = B.r0 + GATHER_ROWS < nn ? B.r0 + GATHER_ROWS : nn;
+    B.p0 = __ldg(row_ptr + B.r0);
+    B.p1 = __ldg(row_ptr + B.r1);
+    B.q0 = __ldg(nptr + B.r0);
+    B.q1 = __ldg(nptr + B.r1);
+    B.fit = (B.p1 - B.p0) <= GatherCfg<DIM>::CAP && (B.q1 - B.q0) <= GatherCfg<DIM>::SLOT_CAP;
+    return B;
+}
+
+template <int DIM>
+struct GatherSmem {
+    char* base;
+    __device__ int32_t* cols(int r) { return reinterpret_cast<int32_t*>(base + r * GatherCfg<DIM>::RING_BYTES); }
+    __device__ uint32_t* slots(int r) {
+        return reinterpret_cast<uint32_t*>(base + r * GatherCfg<DIM>::RING_BYTES + GatherCfg<DIM>::COLS_PAD * 4);
+    }
+    __device__ double* F(int f) { return reinterpret_cast<double*>(base + GatherCfg<DIM>::F_OFF) + f * DIM * GatherCfg<DIM>::CAP; }
+    __device__ double* accK() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::ACC_OFF); }
+    __device__ double* accM() { return accK() + GatherCfg<DIM>::CAP; }
+    __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + GatherCfg<DIM>::BAR_OFF) + r; }
+};
+
+// byte offset (in 4-byte words) of element x within its 16-byte aligned TMA chunk
+__device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
+
+template <int DIM>
+__device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const BlockBounds& B,
+                                          const int32_t* __restrict__ col_idx, const uint32_t* __restrict__ nslot) {
+    if (!B.valid) return;
+    if (!B.fit) {  // keep the barrier's phase count in step with the ring: arrive with no bytes
+        mbar_expect_tx(S.bar(r), 0);
+        return;
+    }
+    uint32_t c0 = (uint32_t)B.p0 & ~3u, c1 = ((uint32_t)B.p1 + 3u) & ~3u;
+    uint32_t s0 = (uint32_t)B.q0 & ~3u, s1 = ((uint32_t)B.q1 + 3u) & ~3u;
+    uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * 4;
+    mbar_expect_tx(S.bar(r), bc + bs);
+    if (bc) tma_load_1d(S.cols(r), col_idx + c0, bc, S.bar(r));
+    if (bs) tma_load_1d(S.slots(r), nslot + s0, bs, S.bar(r));
+}
+
+template <int DIM>
+__device__ __forceinline__ void issue_gather(GatherSmem<DIM>& S, int r, int f, const BlockBounds& B,
+                                             const double* __restrict__ coords, int64_t ns, int64_t cst) {
+    if (!B.valid || !B.fit) return;
+    const int32_t* cols = S.cols(r) + tma_shift(B.p0);
+    double* F = S.F(f);
+    const int np = B.p1 - B.p0;
+    for (int q = threadIdx.x; q < np; q += GATHER_ROWS) {
+        int64_t w = cols[q];
+#pragma unroll
+        for (int c = 0; c < DIM; c++) cp_async8(F + c * GatherCfg<DIM>::CAP + q, coords + c * cst + w * ns);
+    }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, const double* __restrict__ coords,
+                                                                 int64_t ns, int64_t cst,
+                                                                 const int32_t* __restrict__ row_ptr,
+                                                                 const int32_t* __restrict__ col_idx,
+                                                                 const int32_t* __restrict__ nptr,
+                                                                 const uint32_t* __restrict__ nslot,
+                                                                 double* __restrict__ K, double* __restrict__ M) {
     using Cfg = GatherCfg<DIM>;
-    constexpr int CAP = Cfg::CTA_CAP;
-    extern __shared__ double smem[];
-    double* F = smem;                        // [DIM][CAP]  column coordinates, then edge vectors
-    double* sK = smem + DIM * CAP;           // [CAP] CTA-contiguous CSR range of K
-    double* sM = sK + CAP;                   // [CAP]
-    uint32_t* sSlot = reinterpret_cast<uint32_t*>(sM + CAP);     // [SLOT_CAP] plan range
-    int32_t* sCol = reinterpret_cast<int32_t*>(sSlot + Cfg::SLOT_CAP);
+    constexpr int CAP = Cfg::CAP;
+    extern __shared__ __align__(16) char smem_raw[];
+    GatherSmem<DIM> S{smem_raw};
     const int t = threadIdx.x;
-    for (int64_t r0 = (int64_t)blockIdx.x * GATHER_BLOCK; r0 < nn; r0 += (int64_t)gridDim.x * GATHER_BLOCK) {
-        const int64_t rend = r0 + GATHER_BLOCK < nn ? r0 + GATHER_BLOCK : nn;
-        const int32_t p0 = __ldg(row_ptr + r0), p1 = __ldg(row_ptr + rend);
-        const int32_t q0 = __ldg(nptr + r0), q1 = __ldg(nptr + rend);
-        const int np = p1 - p0, nq = q1 - q0;
-        const int64_t v = r0 + t;
-        const bool own = v < rend;
+    const int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
+    const int64_t gstep = gridDim.x;
+    if (t == 0)
+        for (int r = 0; r < Cfg::RING; r++) mbar_init(S.bar(r));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+
+    // prologue: TMA for blocks 0 and 1 of this CTA, coordinate gather for block 0
+    BlockBounds B0 = block_bounds<DIM>(blockIdx.x, nblocks, nn, row_ptr, nptr);
+    BlockBounds B1 = block_bounds<DIM>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
+    BlockBounds B2 = block_bounds<DIM>(blockIdx.x + 2 * gstep, nblocks, nn, row_ptr, nptr);
+    if (t == 0) {
+        issue_tma<DIM>(S, 0, B0, col_idx, nslot);
+        issue_tma<DIM>(S, 1, B1, col_idx, nslot);
+    }
+    if (B0.valid) mbar_wait(S.bar(0), 0);
+    issue_gather<DIM>(S, 0, 0, B0, coords, ns, cst);
+    cp_async_commit();
+
+    for (int64_t k = 0;; k++) {
+        const int64_t b = blockIdx.x + k * gstep;
+        if (b >= nblocks) break;
+        const int rc = (int)(k % 3), rn = (int)((k + 1) % 3), rnn = (int)((k + 2) % 3);
+        const int fc = (int)(k & 1);
+        // per-row bounds of this block (latency overlaps the waits below)
+        const int64_t v = B0.r0 + t;
+        const bool own = v < B0.r1;
         int lo = 0, L = 0, i0 = 0, i1 = 0;
-        double xv[DIM];
         if (own) {
             lo = __ldg(row_ptr + v);
             L = __ldg(row_ptr + v + 1) - lo;
             i0 = __ldg(nptr + v);
             i1 = __ldg(nptr + v + 1);
-#pragma unroll
-            for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + v * ns);
         }
-        if (np <= CAP && nq <= Cfg::SLOT_CAP) {
-            // stage the CTA's CSR columns and plan words (coalesced), zero the accumulators
-#pragma unroll 4
-            for (int q = t; q < np; q += GATHER_BLOCK) sCol[q] = __ldcs(col_idx + p0 + q);
-#pragma unroll 4
-            for (int q = t; q < nq; q += GATHER_BLOCK) sSlot[q] = __ldcs(nslot + q0 + q);
-            __syncthreads();
-            // gather the coordinates of every column of the CTA's range (independent loads)
-#pragma unroll 4
-            for (int q = t; q < np; q += GATHER_BLOCK) {
-                int64_t w = sCol[q];
-#pragma unroll
-                for (int c = 0; c < DIM; c++) F[c * CAP + q] = __ldg(coords + c * cst + w * ns);
+        // stage k+1: its columns have landed -> gather its coordinates
+        if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) / 3) & 1));
+        issue_gather<DIM>(S, rn, fc ^ 1, B1, coords, ns, cst);
+        cp_async_commit();
+        // stage k+2: stream its columns and plan words (ring slot of block k-1 is free)
+        if (t == 0) issue_tma<DIM>(S, rnn, B2, col_idx, nslot);
+        BlockBounds B3 = block_bounds<DIM>(blockIdx.x + (k + 3) * gstep, nblocks, nn, row_ptr, nptr);
+        // stage k: wait for its coordinates
+        cp_async_wait<1>();
+        __syncwarp();
+
+        if (B0.fit) {
+            const int np = B0.p1 - B0.p0;
+            double* F = S.F(fc);
+            double* sK = S.accK();
+            double* sM = S.accM();
+            const int32_t* cols = S.cols(rc) + tma_shift(B0.p0);
+            const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
+            for (int q = t; q < np; q += GATHER_ROWS) {
                 sK[q] = 0.0;
                 sM[q] = 0.0;
             }
-            __syncthreads();
-            if (own) {
-                const int b = lo - p0;
+            __syncwarp();
+            if (own && L > 0) {
+                const int bse = lo - B0.p0;
                 int s0 = 0;
-                for (int s = 0; s < L; s++) {
-                    if (sCol[b + s] == v) s0 = s;
+                for (int s = 0; s < L; s++)
+                    if (cols[bse + s] == v) s0 = s;
+                double xv[DIM];
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) F[c * CAP + b + s] -= xv[c];
-                }
+                for (int c = 0; c < DIM; c++) xv[c] = F[c * CAP + bse + s0];
+                for (int s = 0; s < L; s++)
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) F[c * CAP + bse + s] -= xv[c];
                 auto ev = [&](int s, double(&f)[DIM]) {
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) f[c] = F[c * CAP + b + s];
+                    for (int c = 0; c < DIM; c++) f[c] = F[c * CAP + bse + s];
                 };
-                double* aK = K ? sK + b : nullptr;
-                double* aM = M ? sM + b : nullptr;
-                gather_row<DIM>(i0, i1, sSlot - q0, ev, aK, aM);
-                if (L > 0) finish_row<DIM>(L, s0, aK, aM);
+                double* aK = K ? sK + bse : nullptr;
+                double* aM = M ? sM + bse : nullptr;
+                gather_row<DIM>(i0, i1, slots, ev, aK, aM);
+                finish_row<DIM>(L, s0, aK, aM);
             }
-            __syncthreads();
-#pragma unroll 4
-            for (int q = t; q < np; q += GATHER_BLOCK) {
-                if (K) stcs(K + p0 + q, sK[q]);
-                if (M) stcs(M + p0 + q, sM[q]);
+            __syncwarp();
+            for (int q = t; q < np; q += GATHER_ROWS) {
+                if (K) stcs(K + B0.p0 + q, sK[q]);
+                if (M) stcs(M + B0.p0 + q, sM[q]);
             }
-            __syncthreads();
-        } else if (own) {
-            // CTA range larger than the smem budget: same ownership, everything in place in HBM
+            __syncwarp();
+        } else if (own && L > 0) {
+            // block larger than the smem budget: same ownership, everything in place in HBM
             double* aK = K ? K + lo : nullptr;
             double* aM = M ? M + lo : nullptr;
             int s0 = 0;
@@ -348,15 +482,22 @@ __global__ void __launch_bounds__(GATHER_BLOCK) assemble_gather_k(int64_t nn, co
                 if (aM) aM[q] = 0.0;
                 if (__ldg(col_idx + lo + q) == v) s0 = q;
             }
+            double xv[DIM];
+#pragma unroll
+            for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + v * ns);
             auto ev = [&](int s, double(&f)[DIM]) {
                 int64_t w = __ldg(col_idx + lo + s);
 #pragma unroll
                 for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
             };
             gather_row<DIM>(i0, i1, nslot, ev, aK, aM);
-            if (L > 0) finish_row<DIM>(L, s0, aK, aM);
+            finish_row<DIM>(L, s0, aK, aM);
         }
+        B0 = B1;
+        B1 = B2;
+        B2 = B3;
     }
+    cp_async_wait<0>();
 }
 
 }  // namespace
@@ -403,19 +544,23 @@ extern "C" vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne, const doub
         return VB_ERR_ARG;
     }
     if (want_global && nn > 0) {
-        static bool smem_opt_in = false;  // > 48 KB dynamic shared memory needs an opt-in per kernel
-        if (!smem_opt_in) {
+        static int ctas_per_sm[2] = {0, 0};  // > 48 KB dynamic smem needs an opt-in; persistent grid size
+        if (!ctas_per_sm[0]) {
             cudaFuncSetAttribute(assemble_gather_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GatherCfg<2>::SMEM);
             cudaFuncSetAttribute(assemble_gather_k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GatherCfg<3>::SMEM);
-            smem_opt_in = true;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm[0], assemble_gather_k<2>, GATHER_ROWS, GatherCfg<2>::SMEM);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm[1], assemble_gather_k<3>, GATHER_ROWS, GatherCfg<3>::SMEM);
+            for (int& c : ctas_per_sm) c = c > 0 ? c : 1;
         }
-        unsigned g = (unsigned)((nn + GATHER_BLOCK - 1) / GATHER_BLOCK);
+        int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
+        int64_t cap = (int64_t)sm_count() * ctas_per_sm[dim == 3];
+        unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
         if (dim == 2) {
-            assemble_gather_k<2><<<g, GATHER_BLOCK, GatherCfg<2>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
-                                                                         col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
+            assemble_gather_k<2><<<g, GATHER_ROWS, GatherCfg<2>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
+                                                                        col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
         } else {
-            assemble_gather_k<3><<<g, GATHER_BLOCK, GatherCfg<3>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
-                                                                         col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
+            assemble_gather_k<3><<<g, GATHER_ROWS, GatherCfg<3>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
+                                                                        col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
         }
         if ((st = launch_check("fem_p1_assemble(gather)")) != VB_OK) return st;
     }

@@ -201,6 +201,10 @@ def vb_tri_surface(xyz, tri, want_n=True, want_nhat=True, want_area=True, want_v
 
 
 # ------------------------------------------------------------------ FEM P1
+def _pad4(n):
+    return max(4, (n + 3) // 4 * 4)
+
+
 class P1Plan:
     """CSR pattern + scatter plans of a P1 mesh (fem_p1_pattern, both phases).
 
@@ -225,17 +229,19 @@ class P1Plan:
         _check(L.fem_p1_pattern(self.dim, nn, ne, _ptr(elems), ne, _ptr(self.work), C.byref(sz), _ptr(self.row_ptr),
                                 None, 0, None, None, None, None, C.byref(nnz), st))
         self.nnz = int(nnz.value)
-        self.col_idx = torch.empty((max(self.nnz, 1),), dtype=torch.int32, device=dev)
+        # gather mode streams col_idx / node_elem_slot in 16-byte chunks: pad to a multiple of 4 entries
+        self.col_idx = torch.zeros((_pad4(self.nnz),), dtype=torch.int32, device=dev)
         self.elem2nnz = torch.empty((nv * nv, ne), dtype=torch.int32, device=dev) if scatter_map else None
         if gather_plan:
             self.node_elem_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
             self.node_elem = torch.empty((max(nv * ne, 1),), dtype=torch.int32, device=dev)
-            self.node_elem_slot = torch.empty((max(nv * ne, 1),), dtype=torch.int32, device=dev)
+            self.node_elem_slot = torch.zeros((_pad4(nv * ne),), dtype=torch.int32, device=dev)
         else:
             self.node_elem_ptr = self.node_elem = self.node_elem_slot = None
         _check(L.fem_p1_pattern(self.dim, nn, ne, _ptr(elems), ne, _ptr(self.work), C.byref(sz), _ptr(self.row_ptr),
                                 _ptr(self.col_idx), self.col_idx.numel(), _ptr(self.elem2nnz), _ptr(self.node_elem_ptr),
                                 _ptr(self.node_elem), _ptr(self.node_elem_slot), C.byref(nnz), st))
+        self.col_idx_padded = self.col_idx
         self.col_idx = self.col_idx[:self.nnz]
         self.work = None   # the pattern workspace is not needed after the plan exists
 
