@@ -171,20 +171,21 @@ __global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restr
 // order); the diagonal follows from the partition of unity sum_b phi_b = 1:
 //   K_vv = -sum_{w != v} K_vw,   M_vv = (2/d) sum_{w != v} M_vw.
 // Persistent, software-pipelined: each CTA is one warp owning blocks of 32
-// consecutive rows.  While block k is computed, the CSR columns and plan words
-// of block k+2 stream in through TMA bulk copies (cp.async.bulk + mbarrier) and
-// the coordinates of every column of block k+1 are gathered with cp.async, so
-// no thread waits on HBM/L2 latency in the compute phase.
+// consecutive rows.  The CSR columns and plan words of block k+1 stream in
+// through TMA bulk copies (cp.async.bulk + mbarrier) while block k is computed;
+// the coordinates of every column of block k+1 are then gathered with cp.async
+// (one request per lane and coordinate, all in flight at once) and their latency
+// is covered by the other CTAs resident on the SM.
 constexpr int GATHER_ROWS = 32;
 template <int DIM>
 struct GatherCfg {
     static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? 8 : 16);        // CSR entries per block in smem
     static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block in smem
     static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
-    static constexpr int RING = 3;
+    static constexpr int RING = 2;
     static constexpr size_t RING_BYTES = (size_t)(COLS_PAD + SLOTS_PAD) * 4;
     static constexpr size_t F_OFF = RING * RING_BYTES;
-    static constexpr size_t ACC_OFF = F_OFF + (size_t)2 * DIM * CAP * 8;
+    static constexpr size_t ACC_OFF = F_OFF + (size_t)DIM * CAP * 8;
     static constexpr size_t BAR_OFF = ACC_OFF + (size_t)2 * CAP * 8;
     static constexpr size_t SMEM = BAR_OFF + RING * 8;
     static_assert(RING_BYTES % 16 == 0, "TMA destinations must stay 16-byte aligned");
@@ -231,7 +232,8 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row).  EV(s, f) yields
 // the edge vector from the row's vertex to its column s.
 template <int DIM, typename EV>
-__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots, EV ev, double* accK, double* accM) {
+__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
+                                           double* __restrict__ accK, double* __restrict__ accM) {
 #pragma unroll 2
     for (int i = i0; i < i1; i++) {
         uint32_t sl = slots[i];
@@ -255,15 +257,18 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots
             double k1 = fma(ha[0], h1[0], fma(ha[1], h1[1], ha[2] * h1[2]));
             double k2 = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
             double k3 = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
+            // s1, s2, s3 are distinct (distinct vertices): load all, then store all
             if (accK) {
-                accK[s1] += k1;
-                accK[s2] += k2;
-                accK[s3] += k3;
+                double a1 = accK[s1], a2 = accK[s2], a3 = accK[s3];
+                accK[s1] = a1 + k1;
+                accK[s2] = a2 + k2;
+                accK[s3] = a3 + k3;
             }
             if (accM) {
-                accM[s1] += ad;
-                accM[s2] += ad;
-                accM[s3] += ad;
+                double a1 = accM[s1], a2 = accM[s2], a3 = accM[s3];
+                accM[s1] = a1 + ad;
+                accM[s2] = a2 + ad;
+                accM[s3] = a3 + ad;
             }
         } else {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
@@ -277,12 +282,14 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* slots
             double k1 = fma(hax, f2[1], -hay * f2[0]);
             double k2 = fma(-hax, f1[1], hay * f1[0]);
             if (accK) {
-                accK[s1] += k1;
-                accK[s2] += k2;
+                double a1 = accK[s1], a2 = accK[s2];
+                accK[s1] = a1 + k1;
+                accK[s2] = a2 + k2;
             }
             if (accM) {
-                accM[s1] += ad;
-                accM[s2] += ad;
+                double a1 = accM[s1], a2 = accM[s2];
+                accM[s1] = a1 + ad;
+                accM[s2] = a2 + ad;
             }
         }
     }
@@ -337,7 +344,7 @@ struct GatherSmem {
     __device__ uint32_t* slots(int r) {
         return reinterpret_cast<uint32_t*>(base + r * GatherCfg<DIM>::RING_BYTES + GatherCfg<DIM>::COLS_PAD * 4);
     }
-    __device__ double* F(int f) { return reinterpret_cast<double*>(base + GatherCfg<DIM>::F_OFF) + f * DIM * GatherCfg<DIM>::CAP; }
+    __device__ double* F() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::F_OFF); }
     __device__ double* accK() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::ACC_OFF); }
     __device__ double* accM() { return accK() + GatherCfg<DIM>::CAP; }
     __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + GatherCfg<DIM>::BAR_OFF) + r; }
@@ -363,11 +370,11 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
 }
 
 template <int DIM>
-__device__ __forceinline__ void issue_gather(GatherSmem<DIM>& S, int r, int f, const BlockBounds& B,
+__device__ __forceinline__ void issue_gather(GatherSmem<DIM>& S, int r, const BlockBounds& B,
                                              const double* __restrict__ coords, int64_t ns, int64_t cst) {
     if (!B.valid || !B.fit) return;
     const int32_t* cols = S.cols(r) + tma_shift(B.p0);
-    double* F = S.F(f);
+    double* F = S.F();
     const int np = B.p1 - B.p0;
     for (int q = threadIdx.x; q < np; q += GATHER_ROWS) {
         int64_t w = cols[q];
@@ -396,24 +403,22 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
 
-    // prologue: TMA for blocks 0 and 1 of this CTA, coordinate gather for block 0
+    // prologue: TMA for this CTA's first block, then its coordinate gather
     BlockBounds B0 = block_bounds<DIM>(blockIdx.x, nblocks, nn, row_ptr, nptr);
     BlockBounds B1 = block_bounds<DIM>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
-    BlockBounds B2 = block_bounds<DIM>(blockIdx.x + 2 * gstep, nblocks, nn, row_ptr, nptr);
-    if (t == 0) {
-        issue_tma<DIM>(S, 0, B0, col_idx, nslot);
-        issue_tma<DIM>(S, 1, B1, col_idx, nslot);
-    }
+    if (t == 0) issue_tma<DIM>(S, 0, B0, col_idx, nslot);
     if (B0.valid) mbar_wait(S.bar(0), 0);
-    issue_gather<DIM>(S, 0, 0, B0, coords, ns, cst);
+    issue_gather<DIM>(S, 0, B0, coords, ns, cst);
     cp_async_commit();
 
     for (int64_t k = 0;; k++) {
         const int64_t b = blockIdx.x + k * gstep;
         if (b >= nblocks) break;
-        const int rc = (int)(k % 3), rn = (int)((k + 1) % 3), rnn = (int)((k + 2) % 3);
-        const int fc = (int)(k & 1);
-        // per-row bounds of this block (latency overlaps the waits below)
+        const int rc = (int)(k & 1), rn = rc ^ 1;
+        // stage k+1: stream its columns and plan words (ring slot of block k-1 is free)
+        if (t == 0) issue_tma<DIM>(S, rn, B1, col_idx, nslot);
+        BlockBounds B2 = block_bounds<DIM>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
+        // per-row bounds of block k
         const int64_t v = B0.r0 + t;
         const bool own = v < B0.r1;
         int lo = 0, L = 0, i0 = 0, i1 = 0;
@@ -423,20 +428,13 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             i0 = __ldg(nptr + v);
             i1 = __ldg(nptr + v + 1);
         }
-        // stage k+1: its columns have landed -> gather its coordinates
-        if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) / 3) & 1));
-        issue_gather<DIM>(S, rn, fc ^ 1, B1, coords, ns, cst);
-        cp_async_commit();
-        // stage k+2: stream its columns and plan words (ring slot of block k-1 is free)
-        if (t == 0) issue_tma<DIM>(S, rnn, B2, col_idx, nslot);
-        BlockBounds B3 = block_bounds<DIM>(blockIdx.x + (k + 3) * gstep, nblocks, nn, row_ptr, nptr);
-        // stage k: wait for its coordinates
-        cp_async_wait<1>();
+        // stage k: its coordinates
+        cp_async_wait<0>();
         __syncwarp();
 
         if (B0.fit) {
             const int np = B0.p1 - B0.p0;
-            double* F = S.F(fc);
+            double* F = S.F();
             double* sK = S.accK();
             double* sM = S.accM();
             const int32_t* cols = S.cols(rc) + tma_shift(B0.p0);
@@ -493,9 +491,13 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             gather_row<DIM>(i0, i1, nslot, ev, aK, aM);
             finish_row<DIM>(L, s0, aK, aM);
         }
+        __syncwarp();
+        // stage k+1: its columns have landed -> gather its coordinates into F (free now)
+        if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) >> 1) & 1));
+        issue_gather<DIM>(S, rn, B1, coords, ns, cst);
+        cp_async_commit();
         B0 = B1;
         B1 = B2;
-        B2 = B3;
     }
     cp_async_wait<0>();
 }
