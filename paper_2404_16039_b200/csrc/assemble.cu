@@ -171,24 +171,29 @@ __global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restr
 // order); the diagonal follows from the partition of unity sum_b phi_b = 1:
 //   K_vv = -sum_{w != v} K_vw,   M_vv = (2/d) sum_{w != v} M_vw.
 // Persistent, software-pipelined: each CTA is one warp owning blocks of 32
-// consecutive rows.  The CSR columns and plan words of block k+1 stream in
-// through TMA bulk copies (cp.async.bulk + mbarrier) while block k is computed;
-// the coordinates of every column of block k+1 are then gathered with cp.async
-// (one request per lane and coordinate, all in flight at once) and their latency
-// is covered by the other CTAs resident on the SM.
+// consecutive rows (lane = row).  The CSR columns and plan words of block k+1
+// stream in through TMA bulk copies (cp.async.bulk + mbarrier) while block k is
+// computed; each lane then gathers the coordinates of its next row's columns
+// with cp.async (all requests in flight at once); that latency is covered by
+// the other CTAs resident on the SM.  Per-row data (edge vectors, K and M
+// accumulators) live in a lane-interleaved shared-memory layout ([slot][lane]),
+// so every shared access of the inner loop is bank-conflict free; results are
+// transposed to CSR order through shared memory and stored coalesced.
 constexpr int GATHER_ROWS = 32;
 template <int DIM>
 struct GatherCfg {
-    static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? 8 : 16);        // CSR entries per block in smem
-    static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block in smem
+    static constexpr int RS = DIM == 2 ? 8 : 16;                        // max columns per row (fast path)
+    static constexpr int CAP = GATHER_ROWS * RS;                         // CSR entries per block
+    static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block
     static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
     static constexpr int RING = 2;
     static constexpr size_t RING_BYTES = (size_t)(COLS_PAD + SLOTS_PAD) * 4;
-    static constexpr size_t F_OFF = RING * RING_BYTES;
-    static constexpr size_t ACC_OFF = F_OFF + (size_t)DIM * CAP * 8;
+    static constexpr size_t F_OFF = RING * RING_BYTES;                   // [RS*DIM][32] edge vectors / CSR staging
+    static constexpr size_t ACC_OFF = F_OFF + (size_t)DIM * CAP * 8;     // [RS][32] K, then [RS][32] M
     static constexpr size_t BAR_OFF = ACC_OFF + (size_t)2 * CAP * 8;
     static constexpr size_t SMEM = BAR_OFF + RING * 8;
     static_assert(RING_BYTES % 16 == 0, "TMA destinations must stay 16-byte aligned");
+    static_assert(DIM >= 2, "staging of K and M in CSR order reuses the edge-vector buffer");
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -229,9 +234,10 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // Off-diagonal contributions of incidences [i0, i1) of one row: K into accK,
-// |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row).  EV(s, f) yields
-// the edge vector from the row's vertex to its column s.
-template <int DIM, typename EV>
+// |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row); slot s of the
+// row lives at acc[s * ST].  EV(s, f) yields the edge vector from the row's
+// vertex to its column s.
+template <int DIM, int ST, typename EV>
 __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
                                            double* __restrict__ accK, double* __restrict__ accM) {
 #pragma unroll 2
@@ -259,16 +265,16 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __res
             double k3 = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
             // s1, s2, s3 are distinct (distinct vertices): load all, then store all
             if (accK) {
-                double a1 = accK[s1], a2 = accK[s2], a3 = accK[s3];
-                accK[s1] = a1 + k1;
-                accK[s2] = a2 + k2;
-                accK[s3] = a3 + k3;
+                double a1 = accK[s1 * ST], a2 = accK[s2 * ST], a3 = accK[s3 * ST];
+                accK[s1 * ST] = a1 + k1;
+                accK[s2 * ST] = a2 + k2;
+                accK[s3 * ST] = a3 + k3;
             }
             if (accM) {
-                double a1 = accM[s1], a2 = accM[s2], a3 = accM[s3];
-                accM[s1] = a1 + ad;
-                accM[s2] = a2 + ad;
-                accM[s3] = a3 + ad;
+                double a1 = accM[s1 * ST], a2 = accM[s2 * ST], a3 = accM[s3 * ST];
+                accM[s1 * ST] = a1 + ad;
+                accM[s2 * ST] = a2 + ad;
+                accM[s3 * ST] = a3 + ad;
             }
         } else {
             int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
@@ -282,14 +288,14 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __res
             double k1 = fma(hax, f2[1], -hay * f2[0]);
             double k2 = fma(-hax, f1[1], hay * f1[0]);
             if (accK) {
-                double a1 = accK[s1], a2 = accK[s2];
-                accK[s1] = a1 + k1;
-                accK[s2] = a2 + k2;
+                double a1 = accK[s1 * ST], a2 = accK[s2 * ST];
+                accK[s1 * ST] = a1 + k1;
+                accK[s2 * ST] = a2 + k2;
             }
             if (accM) {
-                double a1 = accM[s1], a2 = accM[s2];
-                accM[s1] = a1 + ad;
-                accM[s2] = a2 + ad;
+                double a1 = accM[s1 * ST], a2 = accM[s2 * ST];
+                accM[s1 * ST] = a1 + ad;
+                accM[s2 * ST] = a2 + ad;
             }
         }
     }
@@ -297,21 +303,21 @@ __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __res
 
 // Diagonal of a row (slot s0 of L) from the off-diagonal sums (partition of
 // unity), and the |det| sums of M scaled to M entries.
-template <int DIM>
+template <int DIM, int ST>
 __device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* accM) {
     constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;     // 1/(d! (d+1)(d+2))
     double sk = 0.0, sm = 0.0;
     for (int s = 0; s < L; s++) {
         if (s == s0) continue;
-        if (accK) sk += accK[s];
+        if (accK) sk += accK[s * ST];
         if (accM) {
-            double m = accM[s] * MS;
-            accM[s] = m;
+            double m = accM[s * ST] * MS;
+            accM[s * ST] = m;
             sm += m;
         }
     }
-    if (accK) accK[s0] = -sk;
-    if (accM) accM[s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
+    if (accK) accK[s0 * ST] = -sk;
+    if (accM) accM[s0 * ST] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
 }
 
 struct BlockBounds {
@@ -337,6 +343,13 @@ __device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, 
     return B;
 }
 
+// per-lane view of one row of a block
+struct RowInfo {
+    int64_t v;
+    int lo, L, i0, i1, s0;
+    bool own;
+};
+
 template <int DIM>
 struct GatherSmem {
     char* base;
@@ -350,7 +363,7 @@ struct GatherSmem {
     __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + GatherCfg<DIM>::BAR_OFF) + r; }
 };
 
-// byte offset (in 4-byte words) of element x within its 16-byte aligned TMA chunk
+// word offset of element x within its 16-byte aligned TMA chunk
 __device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
 
 template <int DIM>
@@ -369,18 +382,34 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
     if (bs) tma_load_1d(S.slots(r), nslot + s0, bs, S.bar(r));
 }
 
+// Load the lane's row of block B; if the whole block fits the fast path, find the
+// diagonal slot and gather the row's column coordinates into F[slot][c][lane].
 template <int DIM>
-__device__ __forceinline__ void issue_gather(GatherSmem<DIM>& S, int r, const BlockBounds& B,
-                                             const double* __restrict__ coords, int64_t ns, int64_t cst) {
-    if (!B.valid || !B.fit) return;
-    const int32_t* cols = S.cols(r) + tma_shift(B.p0);
-    double* F = S.F();
-    const int np = B.p1 - B.p0;
-    for (int q = threadIdx.x; q < np; q += GATHER_ROWS) {
-        int64_t w = cols[q];
-#pragma unroll
-        for (int c = 0; c < DIM; c++) cp_async8(F + c * GatherCfg<DIM>::CAP + q, coords + c * cst + w * ns);
+__device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBounds& B, RowInfo& R,
+                                              const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
+                                              const double* __restrict__ coords, int64_t ns, int64_t cst) {
+    const int t = threadIdx.x;
+    R.v = B.r0 + t;
+    R.own = B.valid && R.v < B.r1;
+    R.lo = R.L = R.i0 = R.i1 = R.s0 = 0;
+    if (R.own) {
+        R.lo = __ldg(row_ptr + R.v);
+        R.L = __ldg(row_ptr + R.v + 1) - R.lo;
+        R.i0 = __ldg(nptr + R.v);
+        R.i1 = __ldg(nptr + R.v + 1);
     }
+    const bool fast = __all_sync(0xffffffffu, R.L <= GatherCfg<DIM>::RS) && B.valid && B.fit;
+    if (fast && R.own) {
+        const int32_t* cols = S.cols(r) + tma_shift(B.p0) + (R.lo - B.p0);
+        double* F = S.F();
+        for (int s = 0; s < R.L; s++) {
+            int64_t w = cols[s];
+            if (w == R.v) R.s0 = s;
+#pragma unroll
+            for (int c = 0; c < DIM; c++) cp_async8(F + (s * DIM + c) * GATHER_ROWS + t, coords + c * cst + w * ns);
+        }
+    }
+    return fast;
 }
 
 template <int DIM>
@@ -392,11 +421,11 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                                                                  const uint32_t* __restrict__ nslot,
                                                                  double* __restrict__ K, double* __restrict__ M) {
     using Cfg = GatherCfg<DIM>;
-    constexpr int CAP = Cfg::CAP;
+    constexpr int W = GATHER_ROWS;
     extern __shared__ __align__(16) char smem_raw[];
     GatherSmem<DIM> S{smem_raw};
     const int t = threadIdx.x;
-    const int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
+    const int64_t nblocks = (nn + W - 1) / W;
     const int64_t gstep = gridDim.x;
     if (t == 0)
         for (int r = 0; r < Cfg::RING; r++) mbar_init(S.bar(r));
@@ -408,9 +437,13 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     BlockBounds B1 = block_bounds<DIM>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
     if (t == 0) issue_tma<DIM>(S, 0, B0, col_idx, nslot);
     if (B0.valid) mbar_wait(S.bar(0), 0);
-    issue_gather<DIM>(S, 0, B0, coords, ns, cst);
+    RowInfo R0;
+    bool fast0 = prepare_block<DIM>(S, 0, B0, R0, row_ptr, nptr, coords, ns, cst);
     cp_async_commit();
 
+    double* F = S.F();
+    double* aKs = S.accK() + t;
+    double* aMs = S.accM() + t;
     for (int64_t k = 0;; k++) {
         const int64_t b = blockIdx.x + k * gstep;
         if (b >= nblocks) break;
@@ -418,83 +451,72 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         // stage k+1: stream its columns and plan words (ring slot of block k-1 is free)
         if (t == 0) issue_tma<DIM>(S, rn, B1, col_idx, nslot);
         BlockBounds B2 = block_bounds<DIM>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
-        // per-row bounds of block k
-        const int64_t v = B0.r0 + t;
-        const bool own = v < B0.r1;
-        int lo = 0, L = 0, i0 = 0, i1 = 0;
-        if (own) {
-            lo = __ldg(row_ptr + v);
-            L = __ldg(row_ptr + v + 1) - lo;
-            i0 = __ldg(nptr + v);
-            i1 = __ldg(nptr + v + 1);
-        }
-        // stage k: its coordinates
+        // stage k: its coordinates have landed
         cp_async_wait<0>();
         __syncwarp();
-
-        if (B0.fit) {
-            const int np = B0.p1 - B0.p0;
-            double* F = S.F();
-            double* sK = S.accK();
-            double* sM = S.accM();
-            const int32_t* cols = S.cols(rc) + tma_shift(B0.p0);
+        const RowInfo& R = R0;
+        if (fast0) {
             const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
-            for (int q = t; q < np; q += GATHER_ROWS) {
-                sK[q] = 0.0;
-                sM[q] = 0.0;
-            }
-            __syncwarp();
-            if (own && L > 0) {
-                const int bse = lo - B0.p0;
-                int s0 = 0;
-                for (int s = 0; s < L; s++)
-                    if (cols[bse + s] == v) s0 = s;
+            double* aK = K ? aKs : nullptr;
+            double* aM = M ? aMs : nullptr;
+            if (R.own) {
+                for (int s = 0; s < R.L; s++) {
+                    aKs[s * W] = 0.0;
+                    aMs[s * W] = 0.0;
+                }
                 double xv[DIM];
 #pragma unroll
-                for (int c = 0; c < DIM; c++) xv[c] = F[c * CAP + bse + s0];
-                for (int s = 0; s < L; s++)
+                for (int c = 0; c < DIM; c++) xv[c] = F[(R.s0 * DIM + c) * W + t];
+                for (int s = 0; s < R.L; s++)
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) F[c * CAP + bse + s] -= xv[c];
+                    for (int c = 0; c < DIM; c++) F[(s * DIM + c) * W + t] -= xv[c];
                 auto ev = [&](int s, double(&f)[DIM]) {
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) f[c] = F[c * CAP + bse + s];
+                    for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * W + t];
                 };
-                double* aK = K ? sK + bse : nullptr;
-                double* aM = M ? sM + bse : nullptr;
-                gather_row<DIM>(i0, i1, slots, ev, aK, aM);
-                finish_row<DIM>(L, s0, aK, aM);
+                gather_row<DIM, W>(R.i0, R.i1, slots, ev, aK, aM);
+                finish_row<DIM, W>(R.L, R.s0, aK, aM);
             }
             __syncwarp();
-            for (int q = t; q < np; q += GATHER_ROWS) {
-                if (K) stcs(K + B0.p0 + q, sK[q]);
-                if (M) stcs(M + B0.p0 + q, sM[q]);
-            }
+            // transpose to CSR order through the (now dead) edge-vector buffer, store coalesced
+            const int np = B0.p1 - B0.p0;
+            double* stK = F;
+            double* stM = F + Cfg::CAP;
+            if (R.own)
+                for (int s = 0; s < R.L; s++) {
+                    stK[R.lo - B0.p0 + s] = aKs[s * W];
+                    stM[R.lo - B0.p0 + s] = aMs[s * W];
+                }
             __syncwarp();
-        } else if (own && L > 0) {
-            // block larger than the smem budget: same ownership, everything in place in HBM
-            double* aK = K ? K + lo : nullptr;
-            double* aM = M ? M + lo : nullptr;
+            for (int q = t; q < np; q += W) {
+                if (K) stcs(K + B0.p0 + q, stK[q]);
+                if (M) stcs(M + B0.p0 + q, stM[q]);
+            }
+        } else if (R.own && R.L > 0) {
+            // block outside the smem budget: same ownership, everything in place in HBM
+            double* aK = K ? K + R.lo : nullptr;
+            double* aM = M ? M + R.lo : nullptr;
             int s0 = 0;
-            for (int q = 0; q < L; q++) {
+            for (int q = 0; q < R.L; q++) {
                 if (aK) aK[q] = 0.0;
                 if (aM) aM[q] = 0.0;
-                if (__ldg(col_idx + lo + q) == v) s0 = q;
+                if (__ldg(col_idx + R.lo + q) == R.v) s0 = q;
             }
             double xv[DIM];
 #pragma unroll
-            for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + v * ns);
+            for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + R.v * ns);
             auto ev = [&](int s, double(&f)[DIM]) {
-                int64_t w = __ldg(col_idx + lo + s);
+                int64_t w = __ldg(col_idx + R.lo + s);
 #pragma unroll
                 for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
             };
-            gather_row<DIM>(i0, i1, nslot, ev, aK, aM);
-            finish_row<DIM>(L, s0, aK, aM);
+            gather_row<DIM, 1>(R.i0, R.i1, nslot, ev, aK, aM);
+            finish_row<DIM, 1>(R.L, s0, aK, aM);
         }
         __syncwarp();
         // stage k+1: its columns have landed -> gather its coordinates into F (free now)
         if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) >> 1) & 1));
-        issue_gather<DIM>(S, rn, B1, coords, ns, cst);
+        fast0 = prepare_block<DIM>(S, rn, B1, R0, row_ptr, nptr, coords, ns, cst);
         cp_async_commit();
         B0 = B1;
         B1 = B2;
