@@ -233,72 +233,104 @@ __device__ __forceinline__ double rcp_nr(double x) {
     return y;
 }
 
+// One incidence: the element's K_e[a][o_j] (k[j]) and |det| (ad) with v = a as
+// base vertex, from the edge vectors f_j = x_{o_j} - x_v (j = 1..d).
+template <int DIM>
+struct IncOut {
+    double k[DIM];
+    double ad;
+    int s[DIM];
+};
+
+template <int DIM, typename EV>
+__device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev) {
+    IncOut<DIM> o;
+    if constexpr (DIM == 3) {
+        o.s[0] = (sl >> 8) & 0xff;
+        o.s[1] = (sl >> 16) & 0xff;
+        o.s[2] = sl >> 24;
+        double f1[3], f2[3], f3[3];
+        ev(o.s[0], f1);
+        ev(o.s[1], f2);
+        ev(o.s[2], f3);
+        double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
+                        fma(f2[0], f3[1], -f2[1] * f3[0])};
+        double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
+                        fma(f3[0], f1[1], -f3[1] * f1[0])};
+        double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
+                        fma(f1[0], f2[1], -f1[1] * f2[0])};
+        double ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
+        double r = rcp_nr(ad) * (-1.0 / 6.0);
+        double ha[3];
+#pragma unroll
+        for (int c = 0; c < 3; c++) ha[c] = r * ((h1[c] + h2[c]) + h3[c]);
+        o.k[0] = fma(ha[0], h1[0], fma(ha[1], h1[1], ha[2] * h1[2]));
+        o.k[1] = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
+        o.k[2] = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
+        o.ad = ad;
+    } else {
+        o.s[0] = (sl >> 8) & 0xff;
+        o.s[1] = (sl >> 16) & 0xff;
+        double f1[2], f2[2];
+        ev(o.s[0], f1);
+        ev(o.s[1], f2);
+        // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
+        double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
+        double r = rcp_nr(ad) * -0.5;
+        double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
+        o.k[0] = fma(hax, f2[1], -hay * f2[0]);
+        o.k[1] = fma(-hax, f1[1], hay * f1[0]);
+        o.ad = ad;
+    }
+    return o;
+}
+
+// acc[s*ST] += contributions of one incidence (its d slots are distinct
+// vertices: load all, then store all)
+template <int DIM, int ST, bool WK, bool WM>
+__device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restrict__ accK, double* __restrict__ accM) {
+    if constexpr (WK) {
+        double a[DIM];
+#pragma unroll
+        for (int j = 0; j < DIM; j++) a[j] = accK[o.s[j] * ST];
+#pragma unroll
+        for (int j = 0; j < DIM; j++) accK[o.s[j] * ST] = a[j] + o.k[j];
+    }
+    if constexpr (WM) {
+        double a[DIM];
+#pragma unroll
+        for (int j = 0; j < DIM; j++) a[j] = accM[o.s[j] * ST];
+#pragma unroll
+        for (int j = 0; j < DIM; j++) accM[o.s[j] * ST] = a[j] + o.ad;
+    }
+}
+
 // Off-diagonal contributions of incidences [i0, i1) of one row: K into accK,
 // |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row); slot s of the
 // row lives at acc[s * ST].  EV(s, f) yields the edge vector from the row's
-// vertex to its column s.
+// vertex to its column s.  Incidences are evaluated two at a time (all loads
+// and arithmetic of both before any accumulator store) and accumulated in
+// ascending element order.
+template <int DIM, int ST, bool WK, bool WM, typename EV>
+__device__ __forceinline__ void gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
+                                             double* __restrict__ accK, double* __restrict__ accM) {
+    int i = i0;
+    for (; i + 1 < i1; i += 2) {
+        uint32_t sa = slots[i], sb = slots[i + 1];
+        IncOut<DIM> oa = incidence<DIM>(sa, ev);
+        IncOut<DIM> ob = incidence<DIM>(sb, ev);
+        accumulate<DIM, ST, WK, WM>(oa, accK, accM);
+        accumulate<DIM, ST, WK, WM>(ob, accK, accM);
+    }
+    if (i < i1) accumulate<DIM, ST, WK, WM>(incidence<DIM>(slots[i], ev), accK, accM);
+}
+
 template <int DIM, int ST, typename EV>
 __device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
                                            double* __restrict__ accK, double* __restrict__ accM) {
-#pragma unroll 2
-    for (int i = i0; i < i1; i++) {
-        uint32_t sl = slots[i];
-        if constexpr (DIM == 3) {
-            int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff, s3 = sl >> 24;
-            double f1[3], f2[3], f3[3];
-            ev(s1, f1);
-            ev(s2, f2);
-            ev(s3, f3);
-            double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
-                            fma(f2[0], f3[1], -f2[1] * f3[0])};
-            double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
-                            fma(f3[0], f1[1], -f3[1] * f1[0])};
-            double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
-                            fma(f1[0], f2[1], -f1[1] * f2[0])};
-            double ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
-            double r = rcp_nr(ad) * (-1.0 / 6.0);
-            double ha[3];
-#pragma unroll
-            for (int c = 0; c < 3; c++) ha[c] = r * ((h1[c] + h2[c]) + h3[c]);
-            double k1 = fma(ha[0], h1[0], fma(ha[1], h1[1], ha[2] * h1[2]));
-            double k2 = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
-            double k3 = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
-            // s1, s2, s3 are distinct (distinct vertices): load all, then store all
-            if (accK) {
-                double a1 = accK[s1 * ST], a2 = accK[s2 * ST], a3 = accK[s3 * ST];
-                accK[s1 * ST] = a1 + k1;
-                accK[s2 * ST] = a2 + k2;
-                accK[s3 * ST] = a3 + k3;
-            }
-            if (accM) {
-                double a1 = accM[s1 * ST], a2 = accM[s2 * ST], a3 = accM[s3 * ST];
-                accM[s1 * ST] = a1 + ad;
-                accM[s2 * ST] = a2 + ad;
-                accM[s3 * ST] = a3 + ad;
-            }
-        } else {
-            int s1 = (sl >> 8) & 0xff, s2 = (sl >> 16) & 0xff;
-            double f1[2], f2[2];
-            ev(s1, f1);
-            ev(s2, f2);
-            // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
-            double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
-            double r = rcp_nr(ad) * -0.5;
-            double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
-            double k1 = fma(hax, f2[1], -hay * f2[0]);
-            double k2 = fma(-hax, f1[1], hay * f1[0]);
-            if (accK) {
-                double a1 = accK[s1 * ST], a2 = accK[s2 * ST];
-                accK[s1 * ST] = a1 + k1;
-                accK[s2 * ST] = a2 + k2;
-            }
-            if (accM) {
-                double a1 = accM[s1 * ST], a2 = accM[s2 * ST];
-                accM[s1 * ST] = a1 + ad;
-                accM[s2 * ST] = a2 + ad;
-            }
-        }
-    }
+    if (accK && accM) gather_row_t<DIM, ST, true, true>(i0, i1, slots, ev, accK, accM);
+    else if (accK) gather_row_t<DIM, ST, true, false>(i0, i1, slots, ev, accK, accM);
+    else if (accM) gather_row_t<DIM, ST, false, true>(i0, i1, slots, ev, accK, accM);
 }
 
 // Diagonal of a row (slot s0 of L) from the off-diagonal sums (partition of
