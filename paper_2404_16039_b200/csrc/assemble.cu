@@ -308,21 +308,22 @@ __device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restr
 // Off-diagonal contributions of incidences [i0, i1) of one row: K into accK,
 // |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row); slot s of the
 // row lives at acc[s * ST].  EV(s, f) yields the edge vector from the row's
-// vertex to its column s.  Incidences are evaluated two at a time (all loads
-// and arithmetic of both before any accumulator store) and accumulated in
+// vertex to its column s.  Incidences are evaluated four at a time (all loads
+// and arithmetic of all before any accumulator store) and accumulated in
 // ascending element order.
 template <int DIM, int ST, bool WK, bool WM, typename EV>
 __device__ __forceinline__ void gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
                                              double* __restrict__ accK, double* __restrict__ accM) {
+    constexpr int U = 4;
     int i = i0;
-    for (; i + 1 < i1; i += 2) {
-        uint32_t sa = slots[i], sb = slots[i + 1];
-        IncOut<DIM> oa = incidence<DIM>(sa, ev);
-        IncOut<DIM> ob = incidence<DIM>(sb, ev);
-        accumulate<DIM, ST, WK, WM>(oa, accK, accM);
-        accumulate<DIM, ST, WK, WM>(ob, accK, accM);
+    for (; i + U - 1 < i1; i += U) {
+        IncOut<DIM> o[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) o[u] = incidence<DIM>(slots[i + u], ev);
+#pragma unroll
+        for (int u = 0; u < U; u++) accumulate<DIM, ST, WK, WM>(o[u], accK, accM);
     }
-    if (i < i1) accumulate<DIM, ST, WK, WM>(incidence<DIM>(slots[i], ev), accK, accM);
+    for (; i < i1; i++) accumulate<DIM, ST, WK, WM>(incidence<DIM>(slots[i], ev), accK, accM);
 }
 
 template <int DIM, int ST, typename EV>
