@@ -500,26 +500,33 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                 double xv[DIM];
 #pragma unroll
                 for (int c = 0; c < DIM; c++) xv[c] = F[(R.s0 * DIM + c) * W + t];
-                for (int s = 0; s < R.L; s++)
-#pragma unroll
-                    for (int c = 0; c < DIM; c++) F[(s * DIM + c) * W + t] -= xv[c];
                 auto ev = [&](int s, double(&f)[DIM]) {
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * W + t];
+                    for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * W + t] - xv[c];
                 };
                 gather_row<DIM, W>(R.i0, R.i1, slots, ev, aK, aM);
-                finish_row<DIM, W>(R.L, R.s0, aK, aM);
             }
             __syncwarp();
-            // transpose to CSR order through the (now dead) edge-vector buffer, store coalesced
+            // finish the row (diagonal from the partition of unity, M scale) while
+            // transposing it to CSR order through the (now dead) edge-vector buffer
             const int np = B0.p1 - B0.p0;
             double* stK = F;
             double* stM = F + Cfg::CAP;
-            if (R.own)
+            if (R.own && R.L > 0) {
+                constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;     // 1/(d! (d+1)(d+2))
+                double sk = 0.0, sm = 0.0;
+                const int b = R.lo - B0.p0;
                 for (int s = 0; s < R.L; s++) {
-                    stK[R.lo - B0.p0 + s] = aKs[s * W];
-                    stM[R.lo - B0.p0 + s] = aMs[s * W];
+                    if (s == R.s0) continue;
+                    double kk = aKs[s * W], mm = aMs[s * W] * MS;
+                    sk += kk;
+                    sm += mm;
+                    stK[b + s] = kk;
+                    stM[b + s] = mm;
                 }
+                stK[b + R.s0] = -sk;
+                stM[b + R.s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
+            }
             __syncwarp();
             for (int q = t; q < np; q += W) {
                 if (K) stcs(K + B0.p0 + q, stK[q]);
