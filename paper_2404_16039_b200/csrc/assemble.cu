@@ -317,24 +317,9 @@ __device__ __forceinline__ void gather_row_t(int i0, int i1, const uint32_t* __r
     constexpr int U = 4;
     int i = i0;
     for (; i + U - 1 < i1; i += U) {
-        uint32_t sl[U];
-        if constexpr (ST != 1) {
-            // shared-memory plan words: two 16-byte loads cover words i..i+3 (word w
-            // of the TMA'd range sits at a 16-byte boundary iff w % 4 == 0)
-            const uint4* q = reinterpret_cast<const uint4*>(slots + (i & ~3));
-            const uint4 a = q[0], b = q[1];
-            const int off = i & 3;
-            const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-            for (int u = 0; u < U; u++)
-                sl[u] = off == 0 ? w[u] : off == 1 ? w[u + 1] : off == 2 ? w[u + 2] : w[u + 3];
-        } else {
-#pragma unroll
-            for (int u = 0; u < U; u++) sl[u] = slots[i + u];
-        }
         IncOut<DIM> o[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) o[u] = incidence<DIM>(sl[u], ev);
+        for (int u = 0; u < U; u++) o[u] = incidence<DIM>(slots[i + u], ev);
 #pragma unroll
         for (int u = 0; u < U; u++) accumulate<DIM, ST, WK, WM>(o[u], accK, accM);
     }
