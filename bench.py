@@ -105,6 +105,22 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(x, device=None):
+    """Max of a host float over all ranks (identity without a process group)."""
+    import torch
+    import torch.distributed as tdist
+    if not (tdist.is_available() and tdist.is_initialized()) or tdist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device if device is not None else "cpu")
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def weak_value(world_size, units_per_rank, steps, max_ms):
+    """Whole-job throughput of N independent replicas timed by the slowest rank."""
+    return world_size * units_per_rank * steps / (max_ms * 1e-3)
+
+
 def alg_bytes_assembly(dim, nn, ne, nnz):
     """ALG bytes: coords read + connectivity read + K, M written once."""
     return nn * dim * 8 + ne * (dim + 1) * 4 + 2 * nnz * 8
@@ -180,14 +196,10 @@ def run_vb(args):
         torch.cuda.synchronize()
     if ws > 1:
         tdist.barrier()
-    total_ms = t_start.elapsed_time(t_end)
+    total_ms = max_over_ranks(t_start.elapsed_time(t_end), dev)
     launch_ms = [a.elapsed_time(b) for a, b in ev]
-    if ws > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = ws * ne * args.steps / (total_ms * 1e-3)
+    value = weak_value(ws, ne, args.steps, total_ms)
 
     avg_launch_ms = statistics.mean(launch_ms)
     alg = alg_bytes_assembly(dim, nn, ne, nnz)
@@ -234,12 +246,8 @@ def run_vb(args):
             e2e_step()
         b.record(stream)
         torch.cuda.synchronize()
-        e2e_ms = a.elapsed_time(b)
-        if ws > 1:
-            t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": ws * ne * n_e2e / (e2e_ms * 1e-3), "unit": UNIT,
+        e2e_ms = max_over_ranks(a.elapsed_time(b), dev)
+        e2e = {"value": weak_value(ws, ne, n_e2e, e2e_ms), "unit": UNIT,
                "h2d_bytes_per_step": coords.nbytes + elems.nbytes,
                "d2h_bytes_per_step": (nn + 1) * 4 + nnz * 4 + 2 * nnz * 8,
                "steps": n_e2e, "ms_per_step": e2e_ms / n_e2e,
