@@ -49,6 +49,9 @@ def lib():
             "orc_p1_local_all": (i32, [i32, i64, p, i64, i64, p, i64, p, p]),
             "orc_p1_pattern": (i64, [i32, i64, i64, p, i64, p, p]),
             "orc_p1_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, p, p, p]),
+            "orc_quad_rule": (i32, [i32, i32, p, p]),
+            "orc_p1_local_coef": (i32, [i32, p, i32, d, p, d, p, p, p]),
+            "orc_p1_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i32, d, p, d, p, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -204,4 +207,48 @@ def p1_assemble(coords, elems, row_ptr, col_idx, row_mask=None):
     rc = lib().orc_p1_assemble(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne,
                                _p(row_ptr), _p(col_idx), _p(K), _p(M), _p(mask))
     _check(rc, "assemble")
+    return K, M
+
+
+# ------------------------------------------------------------------ NEXT-1
+def quad_rule(dim, gqo):
+    """(lam (nip, dim+1) barycentric points, w (nip,)) of intquad(gqo, dim)."""
+    lam = np.empty(16)
+    w = np.empty(4)
+    nip = lib().orc_quad_rule(dim, gqo, _p(lam), _p(w))
+    if nip < 0:
+        raise ValueError("no quadrature rule for dim=%d gqo=%d" % (dim, gqo))
+    return lam[:nip * (dim + 1)].reshape(nip, dim + 1).copy(), w[:nip].copy()
+
+
+def _coef(dim, c):
+    a, b = c
+    bb = np.zeros(3)
+    bb[:dim] = np.asarray(b, dtype=np.float64)[:dim]
+    return float(a), bb
+
+
+def p1_local_coef(X, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0))):
+    """Element matrices with c(x) = a * exp(b . x); X (dim, nv)."""
+    X = _f64(X)
+    dim, nv = X.shape
+    (ka, kb), (ma, mb) = _coef(dim, cK), _coef(dim, cM)
+    Ke = np.empty((nv, nv))
+    Me = np.empty((nv, nv))
+    _check(lib().orc_p1_local_coef(dim, _p(X), gqo, ka, _p(kb), ma, _p(mb), _p(Ke), _p(Me)), "local_coef")
+    return Ke, Me
+
+
+def p1_assemble_coef(coords, elems, row_ptr, col_idx, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)),
+                     cM=(1.0, (1.0, 1.0, 1.0))):
+    coords, elems = _f64(coords), _i32(elems)
+    row_ptr, col_idx = _i32(row_ptr), _i32(col_idx)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    (ka, kb), (ma, mb) = _coef(dim, cK), _coef(dim, cM)
+    nnz = int(row_ptr[-1])
+    K = np.empty(nnz)
+    M = np.empty(nnz)
+    _check(lib().orc_p1_assemble_coef(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne, _p(row_ptr), _p(col_idx),
+                                      gqo, ka, _p(kb), ma, _p(mb), _p(K), _p(M)), "assemble_coef")
     return K, M

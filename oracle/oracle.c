@@ -387,3 +387,131 @@ int orc_p1_assemble(int dim, int64_t nn, int64_t ne, const double* coords, int64
     }
     return ORC_OK;
 }
+
+/* ------------------------------------------------------- NEXT-1: coefficients */
+
+/* intquad(gqo, dim): quadrature on the reference simplex as
+ * barycentric points lam[q*(dim+1) + a] and weights w[q] summing to |T_ref| =
+ * 1/d!.  The paper's own point sets are not printed; reading:
+ * gqo = 1: the centroid; gqo = 2: the symmetric degree-2 rules -- 2D: the three
+ * points (2/3, 1/6, 1/6) and permutations, w = 1/6; 3D: the four points
+ * (a, b, b, b) and permutations, a = (5 + 3 sqrt5)/20, b = (5 - sqrt5)/20,
+ * w = 1/24.  Returns nip, or -1 if (dim, gqo) is not supported. */
+int orc_quad_rule(int dim, int gqo, double* lam, double* w) {
+    int nv = dim + 1;
+    if (gqo == 1) {
+        for (int a = 0; a < nv; a++) lam[a] = 1.0 / (double)nv;
+        w[0] = 1.0 / (double)factorial(dim);
+        return 1;
+    }
+    if (gqo == 2 && dim == 2) {
+        for (int q = 0; q < 3; q++) {
+            for (int a = 0; a < 3; a++) lam[q * 3 + a] = (a == q) ? 2.0 / 3.0 : 1.0 / 6.0;
+            w[q] = 1.0 / 6.0;
+        }
+        return 3;
+    }
+    if (gqo == 2 && dim == 3) {
+        double pa = (5.0 + 3.0 * sqrt(5.0)) / 20.0, pb = (5.0 - sqrt(5.0)) / 20.0;
+        for (int q = 0; q < 4; q++) {
+            for (int a = 0; a < 4; a++) lam[q * 4 + a] = (a == q) ? pa : pb;
+            w[q] = 1.0 / 24.0;
+        }
+        return 4;
+    }
+    return -1;
+}
+
+/* c(x) = ca * exp(cb . x): the coefficient functions of eq:K_M;
+ * c = 1 is ca = 1, cb = 0; the paper's benchmarks use ca = 1, cb = (1,..,1)
+ * (c = e^{x1+x2(+x3)}).  coeffs_in_ip evaluates it at
+ * the quadrature points x_q = sum_a lam_qa x_a. */
+static double coef_eval(int dim, double ca, const double* cb, const double* x) {
+    double s = 0.0;
+    for (int c = 0; c < dim; c++) s = s + cb[c] * x[c];
+    return ca * exp(s);
+}
+
+/* Element matrices with coefficients, step by step as Code stiff_scalar_P1
+ * and the mass analogue of Code mass_scalar_P2:
+ *   for each quadrature point q:  K_e += w_q * (|det| * (c_K(x_q) * G^T G))
+ *                                  M_e += w_q * (|det| * (c_M(x_q) * phi_q phi_q^T))
+ * with G = tjac^{-1} D from phider, phi_q = lam_q for P1. */
+int orc_p1_local_coef(int dim, const double* X, int gqo, double cKa, const double* cKb, double cMa,
+                      const double* cMb, double* Ke, double* Me) {
+    int nv = dim + 1;
+    double lam[16], w[4];
+    int nip = orc_quad_rule(dim, gqo, lam, w);
+    if (nip < 0) return ORC_ERR_ARG;
+    double J[16], Jinv[16], G[16];
+    for (int r = 0; r < dim; r++)
+        for (int c = 0; c < dim; c++) J[r * 4 + c] = X[c * nv + (r + 1)] - X[c * nv + 0];
+    double detJ = det_laplace(J, dim);
+    double adet = fabs(detJ);
+    for (int i = 0; i < dim; i++)
+        for (int j = 0; j < dim; j++) {
+            double cof = minor_rc(J, dim, j, i);
+            if ((i + j) % 2) cof = -cof;
+            Jinv[i * 4 + j] = cof / detJ;
+        }
+    for (int r = 0; r < dim; r++)
+        for (int a = 0; a < nv; a++) {
+            double s = 0.0;
+            for (int l = 0; l < dim; l++) {
+                double dla = (a == 0) ? -1.0 : (l == a - 1 ? 1.0 : 0.0);
+                s = s + Jinv[r * 4 + l] * dla;
+            }
+            G[r * 4 + a] = s;
+        }
+    for (int p = 0; p < nv * nv; p++) {
+        Ke[p] = 0.0;
+        Me[p] = 0.0;
+    }
+    for (int q = 0; q < nip; q++) {
+        double xq[3];
+        for (int c = 0; c < dim; c++) {
+            double s = 0.0;
+            for (int a = 0; a < nv; a++) s = s + lam[q * nv + a] * X[c * nv + a];
+            xq[c] = s;
+        }
+        double cK = coef_eval(dim, cKa, cKb, xq), cM = coef_eval(dim, cMa, cMb, xq);
+        for (int a = 0; a < nv; a++)
+            for (int b = 0; b < nv; b++) {
+                double gtg = 0.0;
+                for (int r = 0; r < dim; r++) gtg = gtg + G[r * 4 + a] * G[r * 4 + b];
+                Ke[a * nv + b] = Ke[a * nv + b] + w[q] * (adet * (cK * gtg));
+                Me[a * nv + b] = Me[a * nv + b] + w[q] * (adet * (cM * (lam[q * nv + a] * lam[q * nv + b])));
+            }
+    }
+    return ORC_OK;
+}
+
+/* Assembly with coefficients: O11 with orc_p1_local_coef in place of O9. */
+int orc_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                         int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                         const int32_t* row_ptr, const int32_t* col_idx, int gqo, double cKa,
+                         const double* cKb, double cMa, const double* cMb, double* K, double* M) {
+    int nv = dim + 1;
+    int64_t nnz = row_ptr[nn];
+    for (int64_t p = 0; p < nnz; p++) {
+        K[p] = 0.0;
+        M[p] = 0.0;
+    }
+    for (int64_t e = 0; e < ne; e++) {
+        int32_t vid[4];
+        double X[16], Ke[16], Me[16];
+        for (int a = 0; a < nv; a++) vid[a] = elems[a * elem_ld + e];
+        for (int a = 0; a < nv; a++)
+            for (int c = 0; c < dim; c++) X[c * nv + a] = coords[c * comp_stride + (int64_t)vid[a] * node_stride];
+        int rc = orc_p1_local_coef(dim, X, gqo, cKa, cKb, cMa, cMb, Ke, Me);
+        if (rc) return rc;
+        for (int a = 0; a < nv; a++)
+            for (int b = 0; b < nv; b++) {
+                int64_t p = find_col(row_ptr, col_idx, vid[a], vid[b]);
+                if (p < 0) return -3;
+                K[p] += Ke[a * nv + b];
+                M[p] += Me[a * nv + b];
+            }
+    }
+    return ORC_OK;
+}

@@ -83,8 +83,14 @@ def square_p1(n, jitter=0.1, seed=0):
 _KUHN_PERMS = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
 
 
-def cube_kuhn_p1(n, jitter=0.05, seed=0):
-    """Return (coords (3, nn) float64, elems (4, ne) int32)."""
+def cube_kuhn_p1(n, jitter=0.05, seed=0, flip=(0, 0, 0)):
+    """Return (coords (3, nn) float64, elems (4, ne) int32).
+
+    ``flip`` picks the cell diagonal shared by the 6 Kuhn tets: axis d is walked
+    from the cell's far side when flip[d] = 1.  flip = (0, 0, 0) is the
+    (0,0,0)-(1,1,1) diagonal of BASELINE configs[4]; flip = (0, 0, 1) (the
+    (0,0,1)-(1,1,0) diagonal) reproduces the error columns of the paper's 3D P1
+    table (tab:KM_P1_3D) -- see tests/golden/paper_tables_p1.json."""
     n1 = n + 1
     nn = n1 ** 3
     v = np.arange(nn, dtype=np.int64)
@@ -105,14 +111,37 @@ def cube_kuhn_p1(n, jitter=0.05, seed=0):
     ci = c % n
     cj = (c // n) % n
     ck = c // (n * n)
-    v0 = ci + n1 * (cj + n1 * ck)
-    step = (1, n1, n1 * n1)
+    fl = [int(bool(f)) for f in flip]
+    v0 = (ci + fl[0]) + n1 * ((cj + fl[1]) + n1 * (ck + fl[2]))
+    step = (1 - 2 * fl[0], n1 * (1 - 2 * fl[1]), n1 * n1 * (1 - 2 * fl[2]))
     elems = np.empty((4, 6 * n ** 3), dtype=np.int32)
     for t, p in enumerate(_KUHN_PERMS):
         a1 = v0 + step[p[0]]
         a2 = a1 + step[p[1]]
         a3 = a2 + step[p[2]]
         elems[:, t::6] = np.stack([v0, a1, a2, a3])
+    return coords, elems
+
+
+def square_crossed_p1(n):
+    """Unit square, n x n cells, each split into 4 triangles by its centre node
+    (the paper's 2D meshes: (n+1)^2 + n^2 nodes).  Corner node id
+    i + (n+1) j at (i/n, j/n); centre of cell (i, j) (x-fastest) has id
+    (n+1)^2 + i + n j; cell triangles (v00, v10, m), (v10, v11, m), (v11, v01, m),
+    (v01, v00, m) in that order.  Returns (coords (2, nn), elems (3, 4n^2))."""
+    n1 = n + 1
+    v = np.arange(n1 * n1, dtype=np.int64)
+    c = np.arange(n * n, dtype=np.int64)
+    ci, cj = c % n, c // n
+    coords = np.concatenate([np.stack([(v % n1) / n, (v // n1) / n]),
+                             np.stack([(ci + 0.5) / n, (cj + 0.5) / n])], axis=1)
+    v00 = ci + n1 * cj
+    v10, v01 = v00 + 1, v00 + n1
+    v11 = v01 + 1
+    m = n1 * n1 + c
+    elems = np.empty((3, 4 * n * n), dtype=np.int32)
+    for t, (a, b) in enumerate(((v00, v10), (v10, v11), (v11, v01), (v01, v00))):
+        elems[:, t::4] = np.stack([a, b, m])
     return coords, elems
 
 
