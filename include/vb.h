@@ -217,6 +217,29 @@ VB_API vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne,
                           double* K_local, double* M_local,
                           int mode, vb_stream_t stream);
 
+/* ---------------------------------------------------------- NEXT-1: coefficients
+ * As fem_p1_assemble, with the coefficient functions of eq:K_M
+ *   c_K(x) = cK_a * exp(cK_b . x),   c_M(x) = cM_a * exp(cM_b . x)
+ * (cK_b, cM_b: HOST arrays of dim doubles, NULL = 0; c = 1 is a = 1, b = 0; the
+ * paper's benchmarks use a = 1, b = (1, .., 1)) integrated with
+ * intquad(gqo) as Code stiff_scalar_P1:
+ *   K_e = sum_q w_q |det| c_K(x_q) G^T G,   M_e = sum_q w_q |det| c_M(x_q) phi_q phi_q^T,
+ * gqo = 1 (centroid) or 2 (symmetric degree-2 rules: 3 points in 2D, 4 in 3D;
+ * reading in DESIGN.md §4).  Both modes; in gather mode the diagonal of M is
+ * the row sum of M_e (sum_b phi_b = 1) minus the off-diagonals.
+ * Errors as fem_p1_assemble, plus VB_ERR_UNSUPPORTED for other gqo. */
+VB_API vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne,
+                          const double* coords, int64_t node_stride, int64_t comp_stride,
+                          const int32_t* elems, int64_t elem_ld,
+                          const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
+                          const int32_t* elem2nnz,
+                          const int32_t* node_elem_ptr, const int32_t* node_elem,
+                          const uint32_t* node_elem_slot,
+                          int gqo, double cK_a, const double* cK_b, double cM_a, const double* cM_b,
+                          double* K_vals, double* M_vals,
+                          double* K_local, double* M_local,
+                          int mode, vb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,6 +25,27 @@ struct P1 {
     static constexpr double MFACT = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;  // 1/(d! (d+1)(d+2))
 };
 
+// Coefficients c(x) = a exp(b . x) for K and M and the intquad order (NEXT-1).
+struct CoefSpec {
+    double ka, kb[3], ma, mb[3];
+    int gqo;
+    bool same;  // c_K == c_M: evaluate once
+};
+
+// intquad(2, dim): symmetric degree-2 rules, point q = (ALPHA at vertex q, BETA
+// elsewhere), weight W each; WSUM = |T_ref| = 1/d! (reading: DESIGN.md §4).
+template <int DIM>
+struct QuadRule;
+template <>
+struct QuadRule<2> {
+    static constexpr double ALPHA = 2.0 / 3.0, BETA = 1.0 / 6.0, W = 1.0 / 6.0, WSUM = 0.5, DFACT = 2.0;
+};
+template <>
+struct QuadRule<3> {
+    static constexpr double ALPHA = 0.58541019662496845446, BETA = 0.13819660112501051518, W = 1.0 / 24.0,
+                            WSUM = 1.0 / 6.0, DFACT = 6.0;
+};
+
 // H = adj(tjac) D (DIM x NV) and detJ from the element's vertex coordinates x[NV][DIM].
 template <int DIM>
 __device__ __forceinline__ double element_H(const double (&x)[DIM + 1][DIM], double (&H)[DIM][DIM + 1]) {
@@ -85,13 +106,55 @@ __global__ void zero2_k(double* __restrict__ a, double* __restrict__ b, int64_t 
     }
 }
 
-// ------------------------------------------------------------ atomic variant
+// Element factors with coefficients (NEXT-1): kbar = d! sum_q w_q c_K(x_q) scales
+// the c = 1 stiffness; Mloc[a][b] = |det| sum_q w_q c_M(x_q) lam_a(q) lam_b(q).
 template <int DIM>
+__device__ __forceinline__ double elem_coef(const double (&x)[DIM + 1][DIM], double adet, const CoefSpec& cp,
+                                            double (&Mloc)[DIM + 1][DIM + 1]) {
+    constexpr int NV = DIM + 1;
+    const bool one = cp.gqo == 1;
+    const double al = one ? 1.0 / NV : QuadRule<DIM>::ALPHA, be = one ? 1.0 / NV : QuadRule<DIM>::BETA;
+    const double wq = one ? QuadRule<DIM>::WSUM : QuadRule<DIM>::W;
+    const int nip = one ? 1 : NV;
+    double sk = 0.0;
+#pragma unroll
+    for (int a = 0; a < NV; a++)
+#pragma unroll
+        for (int b = 0; b < NV; b++) Mloc[a][b] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NV; q++) {
+        if (q >= nip) break;
+        double ek = 0.0, em = 0.0;
+#pragma unroll
+        for (int c = 0; c < DIM; c++) {
+            double xc = 0.0;
+#pragma unroll
+            for (int a = 0; a < NV; a++) xc = fma(a == q ? al : be, x[a][c], xc);
+            ek = fma(cp.kb[c], xc, ek);
+            em = fma(cp.mb[c], xc, em);
+        }
+        const double ck = cp.ka * exp(ek);
+        const double cm = cp.same ? ck : cp.ma * exp(em);
+        sk += ck;
+#pragma unroll
+        for (int a = 0; a < NV; a++)
+#pragma unroll
+            for (int b = 0; b < NV; b++) Mloc[a][b] = fma(cm * (a == q ? al : be), b == q ? al : be, Mloc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < NV; a++)
+#pragma unroll
+        for (int b = 0; b < NV; b++) Mloc[a][b] *= adet * wq;
+    return QuadRule<DIM>::DFACT * wq * sk;
+}
+
+// ------------------------------------------------------------ atomic variant
+template <int DIM, bool COEF>
 __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
                                                          int64_t cst, const int32_t* __restrict__ elems, int64_t eld,
                                                          const int32_t* __restrict__ e2n, double* __restrict__ K,
                                                          double* __restrict__ M, double* __restrict__ Kl,
-                                                         double* __restrict__ Ml) {
+                                                         double* __restrict__ Ml, const CoefSpec cp) {
     constexpr int NV = DIM + 1;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
@@ -102,6 +165,8 @@ __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const doubl
         double adet = fabs(det);
         double s = P1<DIM>::INV_DFACT / adet;
         double m = P1<DIM>::MFACT * adet;
+        double Mloc[NV][NV];
+        if constexpr (COEF) s *= elem_coef<DIM>(x, adet, cp, Mloc);
 #pragma unroll
         for (int a = 0; a < NV; a++)
 #pragma unroll
@@ -110,48 +175,23 @@ __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const doubl
 #pragma unroll
                 for (int r = 1; r < DIM; r++) d = fma(H[r][a], H[r][b], d);
                 double k = s * d;
-                double mm = (a == b) ? 2.0 * m : m;
-                int32_t pab = __ldcs(e2n + (int64_t)(a * NV + b) * ne + e);
-                if (K) atomicAdd(K + pab, k);
-                if (M) atomicAdd(M + pab, mm);
+                double mm = COEF ? Mloc[a][b] : ((a == b) ? 2.0 * m : m);
+                if (K || M) {
+                    int32_t pab = __ldcs(e2n + (int64_t)(a * NV + b) * ne + e);
+                    if (K) atomicAdd(K + pab, k);
+                    if (M) atomicAdd(M + pab, mm);
+                }
                 if (Kl) stcs(Kl + (int64_t)(a + b * NV) * ne + e, k);
                 if (Ml) stcs(Ml + (int64_t)(a + b * NV) * ne + e, mm);
                 if (a != b) {
-                    int32_t pba = __ldcs(e2n + (int64_t)(b * NV + a) * ne + e);
-                    if (K) atomicAdd(K + pba, k);
-                    if (M) atomicAdd(M + pba, mm);
+                    if (K || M) {
+                        int32_t pba = __ldcs(e2n + (int64_t)(b * NV + a) * ne + e);
+                        if (K) atomicAdd(K + pba, k);
+                        if (M) atomicAdd(M + pba, mm);
+                    }
                     if (Kl) stcs(Kl + (int64_t)(b + a * NV) * ne + e, k);
                     if (Ml) stcs(Ml + (int64_t)(b + a * NV) * ne + e, mm);
                 }
-            }
-    }
-}
-
-// ------------------------------------------------------------ local matrices only
-template <int DIM>
-__global__ void __launch_bounds__(256) local_k(int64_t ne, const double* __restrict__ coords, int64_t ns, int64_t cst,
-                                               const int32_t* __restrict__ elems, int64_t eld, double* __restrict__ Kl,
-                                               double* __restrict__ Ml) {
-    constexpr int NV = DIM + 1;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
-        int32_t vid[NV];
-        double x[NV][DIM], H[DIM][NV];
-        load_element<DIM>(e, elems, eld, coords, ns, cst, vid, x);
-        double det = element_H<DIM>(x, H);
-        double adet = fabs(det);
-        double s = P1<DIM>::INV_DFACT / adet;
-        double m = P1<DIM>::MFACT * adet;
-#pragma unroll
-        for (int a = 0; a < NV; a++)
-#pragma unroll
-            for (int b = a; b < NV; b++) {
-                double d = H[0][a] * H[0][b];
-#pragma unroll
-                for (int r = 1; r < DIM; r++) d = fma(H[r][a], H[r][b], d);
-                double k = s * d, mm = (a == b) ? 2.0 * m : m;
-                if (Kl) { stcs(Kl + (int64_t)(a + b * NV) * ne + e, k); if (a != b) stcs(Kl + (int64_t)(b + a * NV) * ne + e, k); }
-                if (Ml) { stcs(Ml + (int64_t)(a + b * NV) * ne + e, mm); if (a != b) stcs(Ml + (int64_t)(b + a * NV) * ne + e, mm); }
             }
     }
 }
@@ -234,16 +274,68 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // One incidence: the element's K_e[a][o_j] (k[j]) and |det| (ad) with v = a as
-// base vertex, from the edge vectors f_j = x_{o_j} - x_v (j = 1..d).
+// base vertex, from the edge vectors f_j = x_{o_j} - x_v (j = 1..d).  With
+// coefficients (COEF) also M_e[a][o_j] (m[j]) and the row sum
+// sum_b M_e[a][b] (mrow), and k scaled by the quadrature average of c_K.
 template <int DIM>
 struct IncOut {
     double k[DIM];
     double ad;
     int s[DIM];
+    double m[DIM];
+    double mrow;
 };
 
-template <int DIM, typename EV>
-__device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev) {
+// Coefficient-weighted evaluation (NEXT-1, Code stiff_scalar_P1 P:978-1004 with
+// c(x) = a exp(b . x)): intquad(gqo) points in barycentric form, "point q near
+// vertex q" (symmetric rules), vertex 0 = the row's vertex, 1..d = the others.
+template <int DIM>
+__device__ __forceinline__ void apply_coef(IncOut<DIM>& o, const double (&xv)[DIM], const double (&f)[DIM][DIM],
+                                           const CoefSpec& cp) {
+    constexpr int NV = DIM + 1;
+    const bool one = cp.gqo == 1;
+    const double al = one ? 1.0 / NV : QuadRule<DIM>::ALPHA, be = one ? 1.0 / NV : QuadRule<DIM>::BETA;
+    const double wq = one ? QuadRule<DIM>::WSUM : QuadRule<DIM>::W;
+    const int nip = one ? 1 : NV;
+    double sk = 0.0, mrow = 0.0, mj[DIM];
+#pragma unroll
+    for (int j = 0; j < DIM; j++) mj[j] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NV; q++) {
+        if (q >= nip) break;
+        double x[DIM];
+#pragma unroll
+        for (int c = 0; c < DIM; c++) {
+            double s = xv[c];
+#pragma unroll
+            for (int j = 0; j < DIM; j++) s = fma(q == j + 1 ? al : be, f[j][c], s);
+            x[c] = s;
+        }
+        double ek = 0.0, em = 0.0;
+#pragma unroll
+        for (int c = 0; c < DIM; c++) {
+            ek = fma(cp.kb[c], x[c], ek);
+            em = fma(cp.mb[c], x[c], em);
+        }
+        const double ck = cp.ka * exp(ek);
+        const double cm = cp.same ? ck : cp.ma * exp(em);
+        sk += ck;
+        const double la = q == 0 ? al : be;
+        mrow = fma(cm, la, mrow);
+#pragma unroll
+        for (int j = 0; j < DIM; j++) mj[j] = fma(cm * la, q == j + 1 ? al : be, mj[j]);
+    }
+    const double kbar = QuadRule<DIM>::DFACT * wq * sk;   // d! sum_q w_q c_K(x_q): 1 for c = 1
+#pragma unroll
+    for (int j = 0; j < DIM; j++) {
+        o.k[j] *= kbar;
+        o.m[j] = o.ad * wq * mj[j];
+    }
+    o.mrow = o.ad * wq * mrow;
+}
+
+template <int DIM, bool COEF, typename EV>
+__device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, const double (&xv)[DIM], const CoefSpec& cp) {
     IncOut<DIM> o;
     if constexpr (DIM == 3) {
         o.s[0] = (sl >> 8) & 0xff;
@@ -268,6 +360,10 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev) {
         o.k[1] = fma(ha[0], h2[0], fma(ha[1], h2[1], ha[2] * h2[2]));
         o.k[2] = fma(ha[0], h3[0], fma(ha[1], h3[1], ha[2] * h3[2]));
         o.ad = ad;
+        if constexpr (COEF) {
+            const double f[3][3] = {{f1[0], f1[1], f1[2]}, {f2[0], f2[1], f2[2]}, {f3[0], f3[1], f3[2]}};
+            apply_coef<3>(o, xv, f, cp);
+        }
     } else {
         o.s[0] = (sl >> 8) & 0xff;
         o.s[1] = (sl >> 16) & 0xff;
@@ -281,14 +377,19 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev) {
         o.k[0] = fma(hax, f2[1], -hay * f2[0]);
         o.k[1] = fma(-hax, f1[1], hay * f1[0]);
         o.ad = ad;
+        if constexpr (COEF) {
+            const double f[2][2] = {{f1[0], f1[1]}, {f2[0], f2[1]}};
+            apply_coef<2>(o, xv, f, cp);
+        }
     }
     return o;
 }
 
 // acc[s*ST] += contributions of one incidence (its d slots are distinct
 // vertices: load all, then store all)
-template <int DIM, int ST, bool WK, bool WM>
-__device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restrict__ accK, double* __restrict__ accM) {
+template <int DIM, int ST, bool WK, bool WM, bool COEF>
+__device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restrict__ accK, double* __restrict__ accM,
+                                           double& mrow) {
     if constexpr (WK) {
         double a[DIM];
 #pragma unroll
@@ -301,44 +402,51 @@ __device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restr
 #pragma unroll
         for (int j = 0; j < DIM; j++) a[j] = accM[o.s[j] * ST];
 #pragma unroll
-        for (int j = 0; j < DIM; j++) accM[o.s[j] * ST] = a[j] + o.ad;
+        for (int j = 0; j < DIM; j++) accM[o.s[j] * ST] = a[j] + (COEF ? o.m[j] : o.ad);
+        if constexpr (COEF) mrow += o.mrow;
     }
 }
 
 // Off-diagonal contributions of incidences [i0, i1) of one row: K into accK,
-// |det| into accM (scaled by 1/(d!(d+1)(d+2)) in finish_row); slot s of the
-// row lives at acc[s * ST].  EV(s, f) yields the edge vector from the row's
-// vertex to its column s.  Incidences are evaluated four at a time (all loads
-// and arithmetic of all before any accumulator store) and accumulated in
-// ascending element order.
-template <int DIM, int ST, bool WK, bool WM, typename EV>
-__device__ __forceinline__ void gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
-                                             double* __restrict__ accK, double* __restrict__ accM) {
-    constexpr int U = 4;
+// M into accM (c = 1: |det|, scaled by 1/(d!(d+1)(d+2)) in finish_row); slot s
+// of the row lives at acc[s * ST].  EV(s, f) yields the edge vector from the
+// row's vertex to its column s.  Incidences are evaluated U at a time (all
+// loads and arithmetic before any accumulator store) and accumulated in
+// ascending element order.  Returns the row sum of M (COEF only).
+template <int DIM, int ST, bool WK, bool WM, bool COEF, typename EV>
+__device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
+                                               double* __restrict__ accK, double* __restrict__ accM,
+                                               const double (&xv)[DIM], const CoefSpec& cp) {
+    constexpr int U = COEF ? 2 : 4;
+    double mrow = 0.0;
     int i = i0;
     for (; i + U - 1 < i1; i += U) {
         IncOut<DIM> o[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) o[u] = incidence<DIM>(slots[i + u], ev);
+        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF>(slots[i + u], ev, xv, cp);
 #pragma unroll
-        for (int u = 0; u < U; u++) accumulate<DIM, ST, WK, WM>(o[u], accK, accM);
+        for (int u = 0; u < U; u++) accumulate<DIM, ST, WK, WM, COEF>(o[u], accK, accM, mrow);
     }
-    for (; i < i1; i++) accumulate<DIM, ST, WK, WM>(incidence<DIM>(slots[i], ev), accK, accM);
+    for (; i < i1; i++) accumulate<DIM, ST, WK, WM, COEF>(incidence<DIM, COEF>(slots[i], ev, xv, cp), accK, accM, mrow);
+    return mrow;
 }
 
-template <int DIM, int ST, typename EV>
-__device__ __forceinline__ void gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
-                                           double* __restrict__ accK, double* __restrict__ accM) {
-    if (accK && accM) gather_row_t<DIM, ST, true, true>(i0, i1, slots, ev, accK, accM);
-    else if (accK) gather_row_t<DIM, ST, true, false>(i0, i1, slots, ev, accK, accM);
-    else if (accM) gather_row_t<DIM, ST, false, true>(i0, i1, slots, ev, accK, accM);
+template <int DIM, int ST, bool COEF, typename EV>
+__device__ __forceinline__ double gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
+                                             double* __restrict__ accK, double* __restrict__ accM,
+                                             const double (&xv)[DIM], const CoefSpec& cp) {
+    if (accK && accM) return gather_row_t<DIM, ST, true, true, COEF>(i0, i1, slots, ev, accK, accM, xv, cp);
+    if (accK) return gather_row_t<DIM, ST, true, false, COEF>(i0, i1, slots, ev, accK, accM, xv, cp);
+    if (accM) return gather_row_t<DIM, ST, false, true, COEF>(i0, i1, slots, ev, accK, accM, xv, cp);
+    return 0.0;
 }
 
 // Diagonal of a row (slot s0 of L) from the off-diagonal sums (partition of
-// unity), and the |det| sums of M scaled to M entries.
-template <int DIM, int ST>
-__device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* accM) {
-    constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;     // 1/(d! (d+1)(d+2))
+// unity): K_vv = -sum_{w!=v} K_vw; M_vv = (2/d) sum_{w!=v} M_vw for c = 1
+// (the |det| sums are scaled here), M_vv = rowsum - sum_{w!=v} M_vw otherwise.
+template <int DIM, int ST, bool COEF>
+__device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* accM, double mrow) {
+    constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);     // 1/(d! (d+1)(d+2))
     double sk = 0.0, sm = 0.0;
     for (int s = 0; s < L; s++) {
         if (s == s0) continue;
@@ -350,7 +458,7 @@ __device__ __forceinline__ void finish_row(int L, int s0, double* accK, double* 
         }
     }
     if (accK) accK[s0 * ST] = -sk;
-    if (accM) accM[s0 * ST] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
+    if (accM) accM[s0 * ST] = COEF ? mrow - sm : (DIM == 3 ? sm * (2.0 / 3.0) : sm);
 }
 
 struct BlockBounds {
@@ -445,14 +553,15 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBo
     return fast;
 }
 
-template <int DIM>
+template <int DIM, bool COEF>
 __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, const double* __restrict__ coords,
                                                                  int64_t ns, int64_t cst,
                                                                  const int32_t* __restrict__ row_ptr,
                                                                  const int32_t* __restrict__ col_idx,
                                                                  const int32_t* __restrict__ nptr,
                                                                  const uint32_t* __restrict__ nslot,
-                                                                 double* __restrict__ K, double* __restrict__ M) {
+                                                                 double* __restrict__ K, double* __restrict__ M,
+                                                                 const CoefSpec cp) {
     using Cfg = GatherCfg<DIM>;
     constexpr int W = GATHER_ROWS;
     extern __shared__ __align__(16) char smem_raw[];
@@ -492,6 +601,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
             double* aK = K ? aKs : nullptr;
             double* aM = M ? aMs : nullptr;
+            double mrow = 0.0;
             if (R.own) {
                 for (int s = 0; s < R.L; s++) {
                     aKs[s * W] = 0.0;
@@ -504,7 +614,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #pragma unroll
                     for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * W + t] - xv[c];
                 };
-                gather_row<DIM, W>(R.i0, R.i1, slots, ev, aK, aM);
+                mrow = gather_row<DIM, W, COEF>(R.i0, R.i1, slots, ev, aK, aM, xv, cp);
             }
             __syncwarp();
             // finish the row (diagonal from the partition of unity, M scale) while
@@ -513,7 +623,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             double* stK = F;
             double* stM = F + Cfg::CAP;
             if (R.own && R.L > 0) {
-                constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;     // 1/(d! (d+1)(d+2))
+                constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);  // 1/(d! (d+1)(d+2))
                 double sk = 0.0, sm = 0.0;
                 const int b = R.lo - B0.p0;
                 for (int s = 0; s < R.L; s++) {
@@ -525,7 +635,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                     stM[b + s] = mm;
                 }
                 stK[b + R.s0] = -sk;
-                stM[b + R.s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
+                stM[b + R.s0] = COEF ? mrow - sm : (DIM == 3 ? sm * (2.0 / 3.0) : sm);
             }
             __syncwarp();
             for (int q = t; q < np; q += W) {
@@ -550,8 +660,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #pragma unroll
                 for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
             };
-            gather_row<DIM, 1>(R.i0, R.i1, nslot, ev, aK, aM);
-            finish_row<DIM, 1>(R.L, s0, aK, aM);
+            double mrow = gather_row<DIM, 1, COEF>(R.i0, R.i1, nslot, ev, aK, aM, xv, cp);
+            finish_row<DIM, 1, COEF>(R.L, s0, aK, aM, mrow);
         }
         __syncwarp();
         // stage k+1: its columns have landed -> gather its coordinates into F (free now)
@@ -569,70 +679,129 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 
 using namespace vb;
 
+namespace {
+
+template <int DIM, bool COEF>
+void launch_gather(unsigned g, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
+                   const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const uint32_t* nslot,
+                   double* K, double* M, const CoefSpec& cp) {
+    assemble_gather_k<DIM, COEF><<<g, GATHER_ROWS, GatherCfg<DIM>::SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx,
+                                                                            nptr, nslot, K, M, cp);
+}
+
+template <int DIM, bool COEF>
+int gather_ctas_per_sm() {
+    static int n = 0;  // > 48 KB dynamic smem needs an opt-in; persistent grid size
+    if (!n) {
+        cudaFuncSetAttribute(assemble_gather_k<DIM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)GatherCfg<DIM>::SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF>, GATHER_ROWS,
+                                                      GatherCfg<DIM>::SMEM);
+        if (n < 1) n = 1;
+    }
+    return n;
+}
+
+template <int DIM, bool COEF>
+void launch_element(unsigned g, cudaStream_t s, int64_t ne, const double* coords, int64_t ns, int64_t cst,
+                    const int32_t* elems, int64_t eld, const int32_t* e2n, double* K, double* M, double* Kl, double* Ml,
+                    const CoefSpec& cp) {
+    assemble_atomic_k<DIM, COEF><<<g, 256, 0, s>>>(ne, coords, ns, cst, elems, eld, e2n, K, M, Kl, Ml, cp);
+}
+
+template <int DIM>
+vb_status assemble_impl(const char* fn, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                        int64_t comp_stride, const int32_t* elems, int64_t elem_ld, const int32_t* row_ptr,
+                        const int32_t* col_idx, int64_t nnz, const int32_t* elem2nnz, const int32_t* node_elem_ptr,
+                        const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
+                        double* M_local, int mode, const CoefSpec* coef, cudaStream_t s) {
+    const bool want_global = K_vals || M_vals;
+    const CoefSpec cp = coef ? *coef : CoefSpec{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
+    const bool C = coef != nullptr;
+    vb_status st = VB_OK;
+    if (mode == VB_ASSEMBLE_ATOMIC) {
+        if (want_global && (!elem2nnz || !row_ptr)) { set_error("%s: atomic mode needs elem2nnz and row_ptr", fn); return VB_ERR_ARG; }
+        if (want_global && nnz > 0) {
+            zero2_k<<<grid_for(nnz, 256, 8), 256, 0, s>>>(K_vals, M_vals, nnz);
+            if ((st = launch_check(fn)) != VB_OK) return st;
+        }
+        if (ne == 0 || (!want_global && !K_local && !M_local)) return VB_OK;
+        unsigned g = grid_for(ne, 256, 8);
+        if (C) launch_element<DIM, true>(g, s, ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, K_vals, M_vals, K_local, M_local, cp);
+        else launch_element<DIM, false>(g, s, ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, K_vals, M_vals, K_local, M_local, cp);
+        return launch_check(fn);
+    }
+    // gather mode
+    if (want_global && (!row_ptr || !col_idx || !node_elem_ptr || !node_elem_slot)) {
+        set_error("%s: gather mode needs row_ptr, col_idx, node_elem_ptr, node_elem_slot", fn);
+        return VB_ERR_ARG;
+    }
+    if (want_global && nn > 0) {
+        int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
+        int64_t cap = (int64_t)sm_count() * (C ? gather_ctas_per_sm<DIM, true>() : gather_ctas_per_sm<DIM, false>());
+        unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
+        if (C) launch_gather<DIM, true>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
+        else launch_gather<DIM, false>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
+        if ((st = launch_check(fn)) != VB_OK) return st;
+    }
+    if ((K_local || M_local) && ne > 0) {
+        unsigned g = grid_for(ne, 256, 8);
+        if (C) launch_element<DIM, true>(g, s, ne, coords, node_stride, comp_stride, elems, elem_ld, nullptr, nullptr, nullptr, K_local, M_local, cp);
+        else launch_element<DIM, false>(g, s, ne, coords, node_stride, comp_stride, elems, elem_ld, nullptr, nullptr, nullptr, K_local, M_local, cp);
+        if ((st = launch_check(fn)) != VB_OK) return st;
+    }
+    return VB_OK;
+}
+
+vb_status assemble_entry(const char* fn, int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                         int64_t comp_stride, const int32_t* elems, int64_t elem_ld, const int32_t* row_ptr,
+                         const int32_t* col_idx, int64_t nnz, const int32_t* elem2nnz, const int32_t* node_elem_ptr,
+                         const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
+                         double* M_local, int mode, const CoefSpec* coef, vb_stream_t stream) {
+    clear_error();
+    if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
+    if (nn < 0 || ne < 0 || nnz < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
+    if (mode != VB_ASSEMBLE_ATOMIC && mode != VB_ASSEMBLE_GATHER) { set_error("%s: unknown mode %d", fn, mode); return VB_ERR_ARG; }
+    if (ne > 0 && (!coords || !elems)) { set_error("%s: NULL %s", fn, !coords ? "coords" : "elems"); return VB_ERR_ARG; }
+    if (elem_ld < ne) { set_error("%s: elem_ld < ne", fn); return VB_ERR_ARG; }
+    auto f = dim == 2 ? assemble_impl<2> : assemble_impl<3>;
+    return f(fn, nn, ne, coords, node_stride, comp_stride, elems, elem_ld, row_ptr, col_idx, nnz, elem2nnz,
+             node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local, M_local, mode, coef, cs(stream));
+}
+
+}  // namespace
+
 extern "C" vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
                                      int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
                                      const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
                                      const int32_t* elem2nnz, const int32_t* node_elem_ptr, const int32_t* node_elem,
                                      const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
                                      double* M_local, int mode, vb_stream_t stream) {
+    (void)node_elem;
+    return assemble_entry("fem_p1_assemble", dim, nn, ne, coords, node_stride, comp_stride, elems, elem_ld, row_ptr,
+                          col_idx, nnz, elem2nnz, node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local, M_local,
+                          mode, nullptr, stream);
+}
+
+extern "C" vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                                          int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                                          const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
+                                          const int32_t* elem2nnz, const int32_t* node_elem_ptr,
+                                          const int32_t* node_elem, const uint32_t* node_elem_slot, int gqo,
+                                          double cK_a, const double* cK_b, double cM_a, const double* cM_b,
+                                          double* K_vals, double* M_vals, double* K_local, double* M_local, int mode,
+                                          vb_stream_t stream) {
+    (void)node_elem;
     clear_error();
-    if (dim != 2 && dim != 3) { set_error("fem_p1_assemble: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
-    if (nn < 0 || ne < 0 || nnz < 0) { set_error("fem_p1_assemble: negative size"); return VB_ERR_ARG; }
-    if (mode != VB_ASSEMBLE_ATOMIC && mode != VB_ASSEMBLE_GATHER) { set_error("fem_p1_assemble: unknown mode %d", mode); return VB_ERR_ARG; }
-    if (ne > 0 && (!coords || !elems)) { set_error("fem_p1_assemble: NULL %s", !coords ? "coords" : "elems"); return VB_ERR_ARG; }
-    if (elem_ld < ne) { set_error("fem_p1_assemble: elem_ld < ne"); return VB_ERR_ARG; }
-    cudaStream_t s = cs(stream);
-    const bool want_global = K_vals || M_vals;
-    vb_status st = VB_OK;
-    if (mode == VB_ASSEMBLE_ATOMIC) {
-        if (want_global && (!elem2nnz || !row_ptr)) { set_error("fem_p1_assemble: atomic mode needs elem2nnz and row_ptr"); return VB_ERR_ARG; }
-        if (want_global && nnz > 0) {
-            zero2_k<<<grid_for(nnz, 256, 8), 256, 0, s>>>(K_vals, M_vals, nnz);
-            if ((st = launch_check("fem_p1_assemble(zero)")) != VB_OK) return st;
-        }
-        if (ne == 0 || (!want_global && !K_local && !M_local)) return VB_OK;
-        unsigned g = grid_for(ne, 256, 8);
-        if (!want_global) {
-            if (dim == 2) local_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, K_local, M_local);
-            else local_k<3><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, K_local, M_local);
-        } else if (dim == 2) {
-            assemble_atomic_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, K_vals, M_vals, K_local, M_local);
-        } else {
-            assemble_atomic_k<3><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, K_vals, M_vals, K_local, M_local);
-        }
-        return launch_check("fem_p1_assemble(atomic)");
+    if (gqo != 1 && gqo != 2) { set_error("fem_p1_assemble_coef: gqo=%d, supported 1 and 2", gqo); return VB_ERR_UNSUPPORTED; }
+    if (dim != 2 && dim != 3) { set_error("fem_p1_assemble_coef: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
+    CoefSpec cp{cK_a, {0, 0, 0}, cM_a, {0, 0, 0}, gqo, false};
+    for (int c = 0; c < dim; c++) {
+        cp.kb[c] = cK_b ? cK_b[c] : 0.0;
+        cp.mb[c] = cM_b ? cM_b[c] : 0.0;
     }
-    // gather mode
-    if (want_global && (!row_ptr || !col_idx || !node_elem_ptr || !node_elem_slot)) {
-        set_error("fem_p1_assemble: gather mode needs row_ptr, col_idx, node_elem_ptr, node_elem_slot");
-        return VB_ERR_ARG;
-    }
-    if (want_global && nn > 0) {
-        static int ctas_per_sm[2] = {0, 0};  // > 48 KB dynamic smem needs an opt-in; persistent grid size
-        if (!ctas_per_sm[0]) {
-            cudaFuncSetAttribute(assemble_gather_k<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GatherCfg<2>::SMEM);
-            cudaFuncSetAttribute(assemble_gather_k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GatherCfg<3>::SMEM);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm[0], assemble_gather_k<2>, GATHER_ROWS, GatherCfg<2>::SMEM);
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm[1], assemble_gather_k<3>, GATHER_ROWS, GatherCfg<3>::SMEM);
-            for (int& c : ctas_per_sm) c = c > 0 ? c : 1;
-        }
-        int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
-        int64_t cap = (int64_t)sm_count() * ctas_per_sm[dim == 3];
-        unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
-        if (dim == 2) {
-            assemble_gather_k<2><<<g, GATHER_ROWS, GatherCfg<2>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
-                                                                        col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
-        } else {
-            assemble_gather_k<3><<<g, GATHER_ROWS, GatherCfg<3>::SMEM, s>>>(nn, coords, node_stride, comp_stride, row_ptr,
-                                                                        col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals);
-        }
-        if ((st = launch_check("fem_p1_assemble(gather)")) != VB_OK) return st;
-    }
-    if ((K_local || M_local) && ne > 0) {
-        unsigned g = grid_for(ne, 256, 8);
-        if (dim == 2) local_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, K_local, M_local);
-        else local_k<3><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, K_local, M_local);
-        if ((st = launch_check("fem_p1_assemble(local)")) != VB_OK) return st;
-    }
-    return VB_OK;
+    cp.same = cK_a == cM_a && cp.kb[0] == cp.mb[0] && cp.kb[1] == cp.mb[1] && cp.kb[2] == cp.mb[2];
+    return assemble_entry("fem_p1_assemble_coef", dim, nn, ne, coords, node_stride, comp_stride, elems, elem_ld,
+                          row_ptr, col_idx, nnz, elem2nnz, node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local,
+                          M_local, mode, &cp, stream);
 }

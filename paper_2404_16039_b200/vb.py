@@ -27,7 +27,7 @@ _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORT
 
 EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
-           "fem_p1_assemble")
+           "fem_p1_assemble", "fem_p1_assemble_coef")
 
 
 class VbError(RuntimeError):
@@ -61,6 +61,8 @@ def lib():
                                      C.POINTER(C.c_int64), p]),
             "fem_p1_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, p,
                                       p, p, p, p, i32, p]),
+            "fem_p1_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, p,
+                                           i32, d, p, d, p, p, p, p, p, i32, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -271,4 +273,27 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
                                  _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
                                  _ptr(plan.node_elem), _ptr(plan.node_elem_slot), _ptr(K), _ptr(M), _ptr(Kl),
                                  _ptr(Ml), int(mode), _stream(stream)))
+    return K, M, Kl, Ml
+
+
+def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0)),
+                         mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False, K=None, M=None,
+                         stream=None):
+    """Coefficient-weighted K, M with c(x) = a * exp(b . x) (NEXT-1).  Returns
+    (K_vals, M_vals, K_local, M_local)."""
+    _f64(coords)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    dev = coords.device
+    K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
+    M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
+    Kl = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    kb = (C.c_double * 3)(*[float(x) for x in list(cK[1])[:3]] + [0.0] * (3 - len(list(cK[1])[:3])))
+    mb = (C.c_double * 3)(*[float(x) for x in list(cM[1])[:3]] + [0.0] * (3 - len(list(cM[1])[:3])))
+    _check(lib().fem_p1_assemble_coef(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
+                                      _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
+                                      _ptr(plan.node_elem), _ptr(plan.node_elem_slot), int(gqo), float(cK[0]),
+                                      C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), _ptr(K), _ptr(M),
+                                      _ptr(Kl), _ptr(Ml), int(mode), _stream(stream)))
     return K, M, Kl, Ml
