@@ -334,6 +334,19 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     torch.cuda.synchronize()
     res.append({"name": "config5 fem_p1_pattern (count+fill, elem2nnz + gather plan)",
                 "ms": round((time.perf_counter() - t0) * 1e3 / 2, 3)})
+    # NEXT-1: the paper's own timed workload, Table tab:KM_P1_3D level 7 (the config-5 mesh size, the
+    # paper's Kuhn variant, c_K = c_M = e^{x1+x2+x3}, gqo = 2); paper: K 66.6 s + M 20.4 s, hardware not stated
+    cp_, ep_ = synth.cube_kuhn_p1(128, jitter=0.0, flip=(0, 0, 1))
+    cdp, edp = torch.from_numpy(cp_).to(dev), torch.from_numpy(ep_).to(dev)
+    pp = vb.P1Plan(edp, cp_.shape[1])
+    Kp = torch.empty(pp.nnz, dtype=torch.float64, device=dev)
+    Mp = torch.empty(pp.nnz, dtype=torch.float64, device=dev)
+    for name, mode in (("gather", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+        rec("NEXT-1 paper tab:KM_P1_3D level 7, c=exp(x+y+z), gqo=2, variant=%s (paper: K 66.6 s + M 20.4 s, "
+            "MATLAB, hardware not stated)" % name, ep_.shape[1], "elements",
+            alg_bytes_assembly(3, cp_.shape[1], ep_.shape[1], pp.nnz),
+            time_kernel(lambda: vb.fem_p1_assemble_coef(cdp, edp, pp, gqo=2, mode=mode, K=Kp, M=Mp), 10))
+    del pp, Kp, Mp, cdp, edp
     # config 4: 2D at scale
     c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
     cd4, ed4 = torch.from_numpy(c4).to(dev), torch.from_numpy(e4).to(dev)

@@ -240,6 +240,39 @@ VB_API vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne,
                           double* K_local, double* M_local,
                           int mode, vb_stream_t stream);
 
+/* ---------------------------------------------------------- NEXT-2: rhs, energies
+ * intquad(gqo, dim) as used by the kernels: writes the barycentric
+ * points lam[q*(dim+1) + a] and weights w[q] (HOST arrays, nullable; at most 4
+ * points) and returns nip, or a negative vb_status.  gqo 1: centroid; gqo 2:
+ * symmetric degree-2 rules (reading).  Weights sum to 1/d!. */
+VB_API int vb_quad_rule(int dim, int gqo, double* lam, double* w);
+
+/* P1 load vector, Code rhs_vectorP1:
+ *   b2D(a, e) = sum_q w_q |det_e| f(x_qe) phi_a(ip_q),   b = accumarray(elems, b2D)
+ * fq: f at the integration points of intquad(gqo) (nip planes of ne values,
+ * point order of vb_quad_rule; the caller evaluates f there, e.g. at
+ * X_ip = amsm(coords3D, lam^T) via vb_create_coords3D + vb_page_mtimes, as the
+ * paper's Code surface_integral does).  b2D (nv planes of ne) and
+ * b (nn) are nullable outputs.  mode VB_ASSEMBLE_ATOMIC: fp64 atomics into b
+ * (zero-filled by the call); VB_ASSEMBLE_GATHER: deterministic per-node sums
+ * in ascending element order, needs b2D, node_elem_ptr and node_elem (the plan
+ * of fem_p1_pattern). */
+VB_API vb_status fem_p1_rhs(int dim, int64_t nn, int64_t ne,
+                            const double* coords, int64_t node_stride, int64_t comp_stride,
+                            const int32_t* elems, int64_t elem_ld, int gqo, const double* fq,
+                            double* b2D, double* b,
+                            const int32_t* node_elem_ptr, const int32_t* node_elem,
+                            int mode, vb_stream_t stream);
+
+/* avtamav (page-wise bilinear form eq:layeredBilin P:292-301):
+ * s_k = a_k^T M_k b_k for pages a (n x 1), M (n x m), b (m x 1), n, m in 1..4;
+ * ld = 0 broadcasts a single object.  With a = b = the element restriction of
+ * a nodal vector (vb_create_coords3D with dim = 1) and M = K3D this gives the
+ * element energies 2 J_{1,k} of eq:Jk_comps. */
+VB_API vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A, int64_t lda,
+                                  const double* Mx, int64_t ldm, const double* B, int64_t ldb,
+                                  double* s, vb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,6 +52,8 @@ def lib():
             "orc_quad_rule": (i32, [i32, i32, p, p]),
             "orc_p1_local_coef": (i32, [i32, p, i32, d, p, d, p, p, p]),
             "orc_p1_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i32, d, p, d, p, p, p]),
+            "orc_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p]),
+            "orc_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -252,3 +254,24 @@ def p1_assemble_coef(coords, elems, row_ptr, col_idx, gqo=2, cK=(1.0, (1.0, 1.0,
     _check(lib().orc_p1_assemble_coef(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne, _p(row_ptr), _p(col_idx),
                                       gqo, ka, _p(kb), ma, _p(mb), _p(K), _p(M)), "assemble_coef")
     return K, M
+
+
+# ------------------------------------------------------------------ NEXT-2
+def page_bilinear(A, Mx, B):
+    """avtamav: s_k = a_k^T M_k b_k.  A (1, n, N), Mx (m, n, N), B (1, m, N)."""
+    A, Mx, B = _f64(A), _f64(Mx), _f64(B)
+    m, n, N = Mx.shape
+    s = np.empty(N)
+    _check(lib().orc_page_bilinear(N, n, m, _p(A), A.shape[-1], _p(Mx), N, _p(B), B.shape[-1], _p(s)), "bilinear")
+    return s
+
+
+def p1_rhs(coords, elems, fq, gqo=2):
+    """(b (nn,), b2D (nv, ne)) of Code rhs_vectorP1 with f values fq (nip, ne)."""
+    coords, elems, fq = _f64(coords), _i32(elems), _f64(fq)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    b = np.empty(nn)
+    b2 = np.empty((nv, ne))
+    _check(lib().orc_p1_rhs(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne, gqo, _p(fq), _p(b2), _p(b)), "rhs")
+    return b, b2

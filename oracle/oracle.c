@@ -515,3 +515,59 @@ int orc_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const double* coords, 
     }
     return ORC_OK;
 }
+
+/* ------------------------------------------------------- NEXT-2: rhs, energies */
+
+/* avtamav (eq:layeredBilin P:292-301): s_k = a_k^T M_k b_k for
+ * pages a (n x 1), M (n x m), b (m x 1); computed as sum_i a_i (sum_j M_ij b_j),
+ * j and i ascending. */
+int orc_page_bilinear(int64_t np, int n, int m, const double* A, int64_t lda, const double* Mx, int64_t ldm,
+                      const double* B, int64_t ldb, double* s) {
+    for (int64_t k = 0; k < np; k++) {
+        double acc = 0.0;
+        for (int i = 0; i < n; i++) {
+            double t = 0.0;
+            for (int j = 0; j < m; j++) t = t + at(Mx, ldm, n, i, j, k) * at(B, ldb, m, j, 0, k);
+            acc = acc + at(A, lda, n, i, 0, k) * t;
+        }
+        s[k] = acc;
+    }
+    return ORC_OK;
+}
+
+/* Code rhs_vectorP1: b2D(j, e) = sum_i w_i |det_e| f(x_ie) phi_j(ip_i)
+ * (loop over integration points as written: b2D = b2D + w(i)*detj_abs'.*integrand_i,
+ * detj_abs = sizes*factorial(dim)), then b = accumarray(elems(:), b2D(:)) (e
+ * ascending, local vertex ascending).  fq holds f at the integration points,
+ * plane i (ld = ne), in the point order of orc_quad_rule.  b2D (nv planes of
+ * ne) and b (nn) are nullable. */
+int orc_p1_rhs(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride, int64_t comp_stride,
+               const int32_t* elems, int64_t elem_ld, int gqo, const double* fq, double* b2D, double* b) {
+    int nv = dim + 1;
+    double lam[16], w[4];
+    int nip = orc_quad_rule(dim, gqo, lam, w);
+    if (nip < 0) return ORC_ERR_ARG;
+    if (b)
+        for (int64_t v = 0; v < nn; v++) b[v] = 0.0;
+    for (int64_t e = 0; e < ne; e++) {
+        double X[16], J[16];
+        for (int a = 0; a < nv; a++) {
+            int64_t v = elems[a * elem_ld + e];
+            for (int c = 0; c < dim; c++) X[c * nv + a] = coords[c * comp_stride + v * node_stride];
+        }
+        for (int r = 0; r < dim; r++)
+            for (int c = 0; c < dim; c++) J[r * 4 + c] = X[c * nv + (r + 1)] - X[c * nv + 0];
+        double detj_abs = fabs(det_laplace(J, dim));
+        double loc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int i = 0; i < nip; i++)
+            for (int a = 0; a < nv; a++) {
+                double integrand = fq[(int64_t)i * ne + e] * lam[i * nv + a];
+                loc[a] = loc[a] + w[i] * (detj_abs * integrand);
+            }
+        for (int a = 0; a < nv; a++) {
+            if (b2D) b2D[(int64_t)a * ne + e] = loc[a];
+            if (b) b[elems[a * elem_ld + e]] += loc[a];
+        }
+    }
+    return ORC_OK;
+}

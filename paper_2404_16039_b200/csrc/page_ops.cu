@@ -443,14 +443,16 @@ extern "C" vb_status vb_create_coords3D(int dim, int nv, int64_t ne, const doubl
                                         double* vectors3D, vb_stream_t stream) {
     clear_error();
     if (ne < 0) { set_error("vb_create_coords3D: ne < 0"); return VB_ERR_ARG; }
-    if ((dim != 2 && dim != 3) || nv < 2 || nv > 4) { set_error("vb_create_coords3D: need dim in {2,3}, nv in 2..4"); return VB_ERR_UNSUPPORTED; }
+    if (dim < 1 || dim > 3 || nv < 2 || nv > 4) { set_error("vb_create_coords3D: need dim in 1..3, nv in 2..4"); return VB_ERR_UNSUPPORTED; }
     if (ne == 0) return VB_OK;
     if (!coords || !elems || (!coords3D && !vectors3D)) { set_error("vb_create_coords3D: NULL argument"); return VB_ERR_ARG; }
     if (elem_ld < ne) { set_error("vb_create_coords3D: elem_ld < ne"); return VB_ERR_ARG; }
     unsigned g = grid_for(ne, PAGE_BLOCK, PAGE_BLOCKS_PER_SM);
     auto s = cs(stream);
 #define VB_GATHER(D, V) gather_k<D, V><<<g, PAGE_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, coords3D, vectors3D)
-    if (dim == 2) {
+    if (dim == 1) {
+        if (nv == 2) VB_GATHER(1, 2); else if (nv == 3) VB_GATHER(1, 3); else VB_GATHER(1, 4);
+    } else if (dim == 2) {
         if (nv == 2) VB_GATHER(2, 2); else if (nv == 3) VB_GATHER(2, 3); else VB_GATHER(2, 4);
     } else {
         if (nv == 2) VB_GATHER(3, 2); else if (nv == 3) VB_GATHER(3, 3); else VB_GATHER(3, 4);

@@ -1,0 +1,208 @@
+// NEXT-2: P1 load vector (Code rhs_vectorP1) and the page-wise
+// bilinear form avtamav (eq:layeredBilin P:292-301) used for the
+// element energies J_{i,k}.
+#include "vb_internal.cuh"
+
+namespace vb {
+namespace {
+
+// intquad(gqo, dim) in barycentric form: gqo = 1 centroid, gqo = 2 the
+// symmetric degree-2 rules (point q = ALPHA at vertex q, BETA elsewhere)
+// (reading: DESIGN.md §4).
+struct Rule {
+    int nip;
+    double lam[4][4];
+    double w[4];
+};
+
+bool make_rule(int dim, int gqo, Rule& R) {
+    const int nv = dim + 1;
+    const double dfact = dim == 2 ? 2.0 : (dim == 3 ? 6.0 : 1.0);
+    if (gqo == 1) {
+        R.nip = 1;
+        for (int a = 0; a < nv; a++) R.lam[0][a] = 1.0 / nv;
+        R.w[0] = 1.0 / dfact;
+        return true;
+    }
+    if (gqo == 2 && (dim == 2 || dim == 3)) {
+        const double al = dim == 2 ? 2.0 / 3.0 : 0.58541019662496845446;
+        const double be = dim == 2 ? 1.0 / 6.0 : 0.13819660112501051518;
+        R.nip = nv;
+        for (int q = 0; q < nv; q++) {
+            for (int a = 0; a < nv; a++) R.lam[q][a] = a == q ? al : be;
+            R.w[q] = 1.0 / (dfact * nv);
+        }
+        return true;
+    }
+    return false;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) rhs_elem_k(int64_t ne, const double* __restrict__ coords, int64_t ns, int64_t cst,
+                                                  const int32_t* __restrict__ elems, int64_t eld,
+                                                  const double* __restrict__ fq, const Rule R, double* __restrict__ b2D,
+                                                  double* __restrict__ b) {
+    constexpr int NV = DIM + 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+        int32_t vid[NV];
+        double x[NV][DIM];
+#pragma unroll
+        for (int a = 0; a < NV; a++) {
+            vid[a] = __ldg(elems + a * eld + e);
+#pragma unroll
+            for (int c = 0; c < DIM; c++) x[a][c] = __ldg(coords + c * cst + (int64_t)vid[a] * ns);
+        }
+        double det;
+        if constexpr (DIM == 2) {
+            det = fma(x[1][0] - x[0][0], x[2][1] - x[0][1], -(x[1][1] - x[0][1]) * (x[2][0] - x[0][0]));
+        } else {
+            double J[3][3];
+#pragma unroll
+            for (int r = 0; r < 3; r++)
+#pragma unroll
+                for (int c = 0; c < 3; c++) J[r][c] = x[r + 1][c] - x[0][c];
+            det = J[0][0] * fma(J[1][1], J[2][2], -J[1][2] * J[2][1]) +
+                  J[0][1] * fma(J[1][2], J[2][0], -J[1][0] * J[2][2]) +
+                  J[0][2] * fma(J[1][0], J[2][1], -J[1][1] * J[2][0]);
+        }
+        const double ad = fabs(det);
+        double loc[NV];
+#pragma unroll
+        for (int a = 0; a < NV; a++) loc[a] = 0.0;
+        for (int i = 0; i < R.nip; i++) {
+            const double fw = R.w[i] * ad * __ldcs(fq + (int64_t)i * ne + e);
+#pragma unroll
+            for (int a = 0; a < NV; a++) loc[a] = fma(fw, R.lam[i][a], loc[a]);
+        }
+#pragma unroll
+        for (int a = 0; a < NV; a++) {
+            if (b2D) stcs(b2D + (int64_t)a * ne + e, loc[a]);
+            if (b) atomicAdd(b + vid[a], loc[a]);
+        }
+    }
+}
+
+// accumarray, deterministic: b_v = sum over v's incidences (ascending e) of b2D(a, e)
+__global__ void __launch_bounds__(256) rhs_gather_k(int64_t nn, int64_t ne, const int32_t* __restrict__ nptr,
+                                                    const int32_t* __restrict__ nelem, const double* __restrict__ b2D,
+                                                    double* __restrict__ b) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
+        double s = 0.0;
+        for (int i = __ldg(nptr + v), i1 = __ldg(nptr + v + 1); i < i1; i++) {
+            const int32_t ea = __ldg(nelem + i);
+            s += b2D[(int64_t)(ea & 3) * ne + (ea >> 2)];
+        }
+        b[v] = s;
+    }
+}
+
+__global__ void zero_k(double* __restrict__ a, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = 0.0;
+}
+
+// s_k = a_k^T M_k b_k: sum_i a_i (sum_j M_ij b_j), pages in registers
+template <int N, int M>
+__global__ void __launch_bounds__(256) bilinear_k(int64_t np, const double* __restrict__ A, int64_t lda,
+                                                  const double* __restrict__ Mx, int64_t ldm,
+                                                  const double* __restrict__ B, int64_t ldb, double* __restrict__ s) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < np; k += stride) {
+        double bj[M];
+#pragma unroll
+        for (int j = 0; j < M; j++) bj[j] = ldb ? __ldcs(B + (int64_t)j * ldb + k) : __ldg(B + j);
+        double acc = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            double t = 0.0;
+#pragma unroll
+            for (int j = 0; j < M; j++) t = fma(ldm ? __ldcs(Mx + (int64_t)(i + j * N) * ldm + k) : __ldg(Mx + i + j * N), bj[j], t);
+            acc = fma(lda ? __ldcs(A + (int64_t)i * lda + k) : __ldg(A + i), t, acc);
+        }
+        stcs(s + k, acc);
+    }
+}
+
+typedef void (*bil_fn)(int64_t, const double*, int64_t, const double*, int64_t, const double*, int64_t, double*);
+template <int N>
+bil_fn pick_m(int m) {
+    switch (m) {
+        case 1: return bilinear_k<N, 1>;
+        case 2: return bilinear_k<N, 2>;
+        case 3: return bilinear_k<N, 3>;
+        default: return bilinear_k<N, 4>;
+    }
+}
+bil_fn pick_bilinear(int n, int m) {
+    switch (n) {
+        case 1: return pick_m<1>(m);
+        case 2: return pick_m<2>(m);
+        case 3: return pick_m<3>(m);
+        default: return pick_m<4>(m);
+    }
+}
+
+}  // namespace
+}  // namespace vb
+
+using namespace vb;
+
+extern "C" int vb_quad_rule(int dim, int gqo, double* lam, double* w) {
+    clear_error();
+    Rule R;
+    if (!make_rule(dim, gqo, R)) {
+        set_error("vb_quad_rule: no rule for dim=%d gqo=%d", dim, gqo);
+        return VB_ERR_UNSUPPORTED;
+    }
+    for (int q = 0; q < R.nip; q++) {
+        for (int a = 0; a <= dim; a++)
+            if (lam) lam[q * (dim + 1) + a] = R.lam[q][a];
+        if (w) w[q] = R.w[q];
+    }
+    return R.nip;
+}
+
+extern "C" vb_status fem_p1_rhs(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                                int64_t comp_stride, const int32_t* elems, int64_t elem_ld, int gqo, const double* fq,
+                                double* b2D, double* b, const int32_t* node_elem_ptr, const int32_t* node_elem,
+                                int mode, vb_stream_t stream) {
+    clear_error();
+    if (dim != 2 && dim != 3) { set_error("fem_p1_rhs: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
+    if (nn < 0 || ne < 0) { set_error("fem_p1_rhs: negative size"); return VB_ERR_ARG; }
+    Rule R;
+    if (!make_rule(dim, gqo, R)) { set_error("fem_p1_rhs: gqo=%d unsupported", gqo); return VB_ERR_UNSUPPORTED; }
+    if (mode != VB_ASSEMBLE_ATOMIC && mode != VB_ASSEMBLE_GATHER) { set_error("fem_p1_rhs: unknown mode %d", mode); return VB_ERR_ARG; }
+    if (ne > 0 && (!coords || !elems || !fq)) { set_error("fem_p1_rhs: NULL coords, elems or fq"); return VB_ERR_ARG; }
+    if (elem_ld < ne) { set_error("fem_p1_rhs: elem_ld < ne"); return VB_ERR_ARG; }
+    if (mode == VB_ASSEMBLE_GATHER && b && (!b2D || !node_elem_ptr || !node_elem)) {
+        set_error("fem_p1_rhs: gather mode needs b2D, node_elem_ptr and node_elem");
+        return VB_ERR_ARG;
+    }
+    cudaStream_t s = cs(stream);
+    const bool atomic = mode == VB_ASSEMBLE_ATOMIC;
+    if (b && atomic && nn > 0) zero_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(b, nn);
+    if (ne > 0 && (b2D || (b && atomic))) {
+        unsigned g = grid_for(ne, 256, 8);
+        double* bb = atomic ? b : nullptr;
+        if (dim == 2) rhs_elem_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
+        else rhs_elem_k<3><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
+    }
+    if (b && !atomic && nn > 0)
+        rhs_gather_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, ne, node_elem_ptr, node_elem, b2D, b);
+    return launch_check("fem_p1_rhs");
+}
+
+extern "C" vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A, int64_t lda, const double* Mx,
+                                      int64_t ldm, const double* B, int64_t ldb, double* s, vb_stream_t stream) {
+    clear_error();
+    if (npages < 0) { set_error("vb_page_bilinear: npages < 0"); return VB_ERR_ARG; }
+    if (n < 1 || n > 4 || m < 1 || m > 4) { set_error("vb_page_bilinear: n, m must be 1..4"); return VB_ERR_UNSUPPORTED; }
+    if (npages == 0) return VB_OK;
+    if (!A || !Mx || !B || !s) { set_error("vb_page_bilinear: NULL argument"); return VB_ERR_ARG; }
+    for (int64_t ld : {lda, ldm, ldb})
+        if (ld != 0 && ld < npages) { set_error("vb_page_bilinear: leading dimension < npages"); return VB_ERR_ARG; }
+    pick_bilinear(n, m)<<<grid_for(npages, 256, 8), 256, 0, cs(stream)>>>(npages, A, lda, Mx, ldm, B, ldb, s);
+    return launch_check("vb_page_bilinear");
+}

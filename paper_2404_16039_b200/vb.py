@@ -27,7 +27,7 @@ _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORT
 
 EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
-           "fem_p1_assemble", "fem_p1_assemble_coef")
+           "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear")
 
 
 class VbError(RuntimeError):
@@ -63,6 +63,9 @@ def lib():
                                       p, p, p, p, i32, p]),
             "fem_p1_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, p,
                                            i32, d, p, d, p, p, p, p, p, i32, p]),
+            "vb_quad_rule": (i32, [i32, i32, p, p]),
+            "fem_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p, p, p, i32, p]),
+            "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -297,3 +300,43 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
                                       C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), _ptr(K), _ptr(M),
                                       _ptr(Kl), _ptr(Ml), int(mode), _stream(stream)))
     return K, M, Kl, Ml
+
+
+# ------------------------------------------------------------------ NEXT-2
+def vb_quad_rule(dim, gqo):
+    """(lam (nip, dim+1) numpy, w (nip,) numpy) of intquad(gqo, dim) as the kernels use it."""
+    import numpy as np
+    lam = np.zeros(16)
+    w = np.zeros(4)
+    nip = lib().vb_quad_rule(dim, gqo, lam.ctypes.data_as(C.c_void_p), w.ctypes.data_as(C.c_void_p))
+    if nip < 0:
+        _check(nip)
+    return lam[:nip * (dim + 1)].reshape(nip, dim + 1).copy(), w[:nip].copy()
+
+
+def fem_p1_rhs(coords, elems, fq, plan=None, gqo=2, mode=VB_ASSEMBLE_GATHER, want_b2D=True, stream=None):
+    """(b (nn,), b2D (nv, ne)) of Code rhs_vectorP1 with f values fq (nip, ne) at the
+    integration points.  Gather mode needs the plan (node_elem_ptr, node_elem)."""
+    _f64(coords), _f64(fq)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    dev = coords.device
+    b = torch.empty((nn,), dtype=torch.float64, device=dev)
+    b2 = torch.empty((nv, ne), dtype=torch.float64, device=dev) if (want_b2D or mode == VB_ASSEMBLE_GATHER) else None
+    nptr = plan.node_elem_ptr if plan is not None else None
+    nel = plan.node_elem if plan is not None else None
+    _check(lib().fem_p1_rhs(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, int(gqo), _ptr(fq), _ptr(b2), _ptr(b),
+                            _ptr(nptr), _ptr(nel), int(mode), _stream(stream)))
+    return b, b2
+
+
+def vb_page_bilinear(A, Mx, B, s=None, stream=None):
+    """avtamav: s_k = a_k^T M_k b_k.  A (1, n, N|1), Mx (m, n, N|1), B (1, m, N|1)."""
+    _f64(A), _f64(Mx), _f64(B)
+    m, n, nm = Mx.shape
+    N = max(A.shape[-1], nm, B.shape[-1])
+    if s is None:
+        s = torch.empty((N,), dtype=torch.float64, device=Mx.device)
+    _check(lib().vb_page_bilinear(N, n, m, _ptr(A), _ld(A, N), _ptr(Mx), _ld(Mx, N), _ptr(B), _ld(B, N), _ptr(s),
+                                  _stream(stream)))
+    return s
