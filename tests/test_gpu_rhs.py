@@ -39,7 +39,7 @@ def test_quad_rule_matches_oracle():
         for gqo in (1, 2):
             lam, w = vb.vb_quad_rule(dim, gqo)
             lo, wo = oracle.quad_rule(dim, gqo)
-            assert np.max(np.abs(lam - lo)) <= 1e-16 and np.max(np.abs(w - wo)) <= 1e-17
+            assert np.max(np.abs(lam - lo)) <= 2.3e-16 and np.max(np.abs(w - wo)) <= 1e-17   # 1 ulp
 
 
 @pytest.mark.parametrize("mode", [vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC])
