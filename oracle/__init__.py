@@ -260,9 +260,13 @@ def p1_assemble_coef(coords, elems, row_ptr, col_idx, gqo=2, cK=(1.0, (1.0, 1.0,
 def page_bilinear(A, Mx, B):
     """avtamav: s_k = a_k^T M_k b_k.  A (1, n, N), Mx (m, n, N), B (1, m, N)."""
     A, Mx, B = _f64(A), _f64(Mx), _f64(B)
-    m, n, N = Mx.shape
+    m, n, _ = Mx.shape
+    N = max(A.shape[-1], Mx.shape[-1], B.shape[-1])
+
+    def ld(X):                       # eq:copy broadcast of a single object
+        return 0 if (X.shape[-1] == 1 and N > 1) else X.shape[-1]
     s = np.empty(N)
-    _check(lib().orc_page_bilinear(N, n, m, _p(A), A.shape[-1], _p(Mx), N, _p(B), B.shape[-1], _p(s)), "bilinear")
+    _check(lib().orc_page_bilinear(N, n, m, _p(A), ld(A), _p(Mx), ld(Mx), _p(B), ld(B), _p(s)), "bilinear")
     return s
 
 
