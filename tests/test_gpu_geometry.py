@@ -63,7 +63,7 @@ def test_volumes_and_normals_parity(dev, n):
     # normal of face j is orthogonal to the face's edges (vectors from the last node)
     X = coords[:, elems]                                                    # 3 x 4 x ne
     faces = [(1, 2, 3), (0, 2, 3), (0, 1, 3), (0, 1, 2)]                    # face opposite vertex j of normalsRef's order
-    nrm = N.transpose(1, 0, 2)                                              # 4 x 3 x ne: column j = normal j
+    nrm = N                                                                 # (4, 3, ne): nrm[j] = column j = normal j
     for j in range(4):
         p, q, r = faces[j]
         for a, b in ((p, q), (q, r)):
