@@ -396,6 +396,32 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     b3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=61)).to(dev)
     c3 = torch.empty_like(a3)
     rec("config2 cross", N, "pages", 72 * N, time_kernel(lambda: vb.vb_page_cross(a3, b3, Cout=c3), 20, flush))
+    del a3, b3, c3
+    # NEXT-2: load vector on the config-5 mesh (f given at the 4 integration points of every tet)
+    nq = 4
+    fq = torch.ones((nq, ne5), dtype=torch.float64, device=dev)
+    p5 = vb.P1Plan(ed5, nn5, scatter_map=False)
+    rec("NEXT-2 fem_p1_rhs config5 (b2D + deterministic accumarray)", ne5, "elements",
+        nn5 * 24 + ne5 * 16 + ne5 * nq * 8 + ne5 * 4 * 8 * 2 + nn5 * 8,
+        time_kernel(lambda: vb.fem_p1_rhs(cd5, ed5, fq, plan=p5), 10))
+    del p5, fq
+    # NEXT-4: volumes (amdet(vectors3D)/6) and normals (amsm(amt(aminv(vectors3D)), normalsRef)) of all
+    # 12.58M tets of the config-5 mesh; paper (sphere, 12.58M tets): volumes 4.42 s incl. mesh generation
+    nref = torch.tensor([[-1, 0, 0], [0, -1, 0], [0, 0, -1], [1, 1, 1]], dtype=torch.float64,
+                        device=dev).reshape(4, 3, 1).contiguous()
+
+    def volumes():
+        _, v3 = vb.vb_create_coords3D(cd5, ed5, want_coords3D=False)
+        return vb.vb_page_det(v3)
+
+    def normals():
+        _, v3 = vb.vb_create_coords3D(cd5, ed5, want_coords3D=False)
+        vinv, _, _ = vb.vb_page_inv(v3, want_det=False)
+        return vb.vb_page_mtimes(vb.vb_page_transpose(vinv), nref)
+    rec("NEXT-4 tet volumes config5 (create_coords3D + page_det)", ne5, "elements",
+        ne5 * (16 + 72 * 2 + 8) + nn5 * 24, time_kernel(volumes, 10))
+    rec("NEXT-4 tet normals config5 (create_coords3D + page_inv + page_transpose + page_mtimes)", ne5, "elements",
+        ne5 * (16 + 72 * 6 + 96) + nn5 * 24, time_kernel(normals, 5))
     return res
 
 
