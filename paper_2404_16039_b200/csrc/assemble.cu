@@ -225,7 +225,9 @@ struct GatherCfg {
     static constexpr int RS = DIM == 2 ? 8 : 16;                        // max columns per row (fast path)
     static constexpr int CAP = GATHER_ROWS * RS;                         // CSR entries per block
     static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block
-    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
+    // columns are read straight from L2 by each lane in prepare_block (COLS_PAD = 0 keeps
+    // them out of shared memory, which buys an eighth resident CTA per SM)
+    static constexpr int COLS_PAD = 0, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
     static constexpr int RING = 2;
     static constexpr size_t RING_BYTES = (size_t)(COLS_PAD + SLOTS_PAD) * 4;
     static constexpr size_t F_OFF = RING * RING_BYTES;                   // [RS*DIM][32] edge vectors / CSR staging
@@ -515,11 +517,10 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
         mbar_expect_tx(S.bar(r), 0);
         return;
     }
-    uint32_t c0 = (uint32_t)B.p0 & ~3u, c1 = ((uint32_t)B.p1 + 3u) & ~3u;
+    (void)col_idx;
     uint32_t s0 = (uint32_t)B.q0 & ~3u, s1 = ((uint32_t)B.q1 + 3u) & ~3u;
-    uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * 4;
-    mbar_expect_tx(S.bar(r), bc + bs);
-    if (bc) tma_load_1d(S.cols(r), col_idx + c0, bc, S.bar(r));
+    uint32_t bs = (s1 - s0) * 4;
+    mbar_expect_tx(S.bar(r), bs);
     if (bs) tma_load_1d(S.slots(r), nslot + s0, bs, S.bar(r));
 }
 
@@ -528,6 +529,7 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
 template <int DIM>
 __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBounds& B, RowInfo& R,
                                               const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
+                                              const int32_t* __restrict__ col_idx,
                                               const double* __restrict__ coords, int64_t ns, int64_t cst) {
     const int t = threadIdx.x;
     R.v = B.r0 + t;
@@ -541,7 +543,7 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBo
     }
     const bool fast = __all_sync(0xffffffffu, R.L <= GatherCfg<DIM>::RS) && B.valid && B.fit;
     if (fast && R.own) {
-        const int32_t* cols = S.cols(r) + tma_shift(B.p0) + (R.lo - B.p0);
+        const int32_t* cols = col_idx + R.lo;
         double* F = S.F();
         for (int s = 0; s < R.L; s++) {
             int64_t w = cols[s];
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     if (t == 0) issue_tma<DIM>(S, 0, B0, col_idx, nslot);
     if (B0.valid) mbar_wait(S.bar(0), 0);
     RowInfo R0;
-    bool fast0 = prepare_block<DIM>(S, 0, B0, R0, row_ptr, nptr, coords, ns, cst);
+    bool fast0 = prepare_block<DIM>(S, 0, B0, R0, row_ptr, nptr, col_idx, coords, ns, cst);
     cp_async_commit();
 
     double* F = S.F();
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         __syncwarp();
         // stage k+1: its columns have landed -> gather its coordinates into F (free now)
         if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) >> 1) & 1));
-        fast0 = prepare_block<DIM>(S, rn, B1, R0, row_ptr, nptr, coords, ns, cst);
+        fast0 = prepare_block<DIM>(S, rn, B1, R0, row_ptr, nptr, col_idx, coords, ns, cst);
         cp_async_commit();
         B0 = B1;
         B1 = B2;
