@@ -225,9 +225,7 @@ struct GatherCfg {
     static constexpr int RS = DIM == 2 ? 8 : 16;                        // max columns per row (fast path)
     static constexpr int CAP = GATHER_ROWS * RS;                         // CSR entries per block
     static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block
-    // columns are read straight from L2 by each lane in prepare_block (COLS_PAD = 0 keeps
-    // them out of shared memory, which buys an eighth resident CTA per SM)
-    static constexpr int COLS_PAD = 0, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
+    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
     static constexpr int RING = 2;
     static constexpr size_t RING_BYTES = (size_t)(COLS_PAD + SLOTS_PAD) * 4;
     static constexpr size_t F_OFF = RING * RING_BYTES;                   // [RS*DIM][32] edge vectors / CSR staging
@@ -517,10 +515,11 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
         mbar_expect_tx(S.bar(r), 0);
         return;
     }
-    (void)col_idx;
+    uint32_t c0 = (uint32_t)B.p0 & ~3u, c1 = ((uint32_t)B.p1 + 3u) & ~3u;
     uint32_t s0 = (uint32_t)B.q0 & ~3u, s1 = ((uint32_t)B.q1 + 3u) & ~3u;
-    uint32_t bs = (s1 - s0) * 4;
-    mbar_expect_tx(S.bar(r), bs);
+    uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * 4;
+    mbar_expect_tx(S.bar(r), bc + bs);
+    if (bc) tma_load_1d(S.cols(r), col_idx + c0, bc, S.bar(r));
     if (bs) tma_load_1d(S.slots(r), nslot + s0, bs, S.bar(r));
 }
 
@@ -543,7 +542,8 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBo
     }
     const bool fast = __all_sync(0xffffffffu, R.L <= GatherCfg<DIM>::RS) && B.valid && B.fit;
     if (fast && R.own) {
-        const int32_t* cols = col_idx + R.lo;
+        (void)col_idx;
+        const int32_t* cols = S.cols(r) + tma_shift(B.p0) + (R.lo - B.p0);
         double* F = S.F();
         for (int s = 0; s < R.L; s++) {
             int64_t w = cols[s];
