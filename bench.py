@@ -137,7 +137,10 @@ def load_traffic(kernel_key):
     try:
         with open(path) as f:
             d = json.load(f)
-        return d["kernels"][kernel_key]["dram_bytes_per_launch"]
+        for k in (kernel_key, kernel_key.replace(">", ", 0>")):      # template spelling of later captures
+            if k in d["kernels"]:
+                return d["kernels"][k]["dram_bytes_per_launch"]
+        return None
     except Exception:
         return None
 
