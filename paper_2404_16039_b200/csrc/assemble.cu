@@ -417,7 +417,10 @@ template <int DIM, int ST, bool WK, bool WM, bool COEF, typename EV>
 __device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
                                                double* __restrict__ accK, double* __restrict__ accM,
                                                const double (&xv)[DIM], const CoefSpec& cp) {
-    constexpr int U = COEF ? 2 : 4;
+#ifndef VB_GATHER_U
+#define VB_GATHER_U 4
+#endif
+    constexpr int U = COEF ? 2 : VB_GATHER_U;
     double mrow = 0.0;
     int i = i0;
     for (; i + U - 1 < i1; i += U) {

@@ -17,7 +17,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvb.so")
+LIB_PATH = os.environ.get("VB_LIBVB") or os.path.join(_HERE, "libvb.so")   # VB_LIBVB: A/B builds (tools/)
 
 VB_ASSEMBLE_ATOMIC = 0
 VB_ASSEMBLE_GATHER = 1
