@@ -390,6 +390,16 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, const doubl
 template <int DIM, int ST, bool WK, bool WM, bool COEF>
 __device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restrict__ accK, double* __restrict__ accM,
                                            double& mrow) {
+    if constexpr (WK && WM && ST == 2 * GATHER_ROWS) {   // packed (K, M) pairs: accM == accK + 1
+        double2 a[DIM];
+#pragma unroll
+        for (int j = 0; j < DIM; j++) a[j] = *reinterpret_cast<const double2*>(accK + o.s[j] * ST);
+#pragma unroll
+        for (int j = 0; j < DIM; j++)
+            *reinterpret_cast<double2*>(accK + o.s[j] * ST) = make_double2(a[j].x + o.k[j], a[j].y + (COEF ? o.m[j] : o.ad));
+        if constexpr (COEF) mrow += o.mrow;
+        return;
+    }
     if constexpr (WK) {
         double a[DIM];
 #pragma unroll
@@ -589,8 +599,14 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     cp_async_commit();
 
     double* F = S.F();
-    double* aKs = S.accK() + t;
-    double* aMs = S.accM() + t;
+#ifndef VB_GATHER_PACKED
+#define VB_GATHER_PACKED 0
+#endif
+    // accumulators: [slot][lane] planes of K then M, or (packed) interleaved (K, M)
+    // pairs so one 16-byte access serves both matrices
+    constexpr int STF = VB_GATHER_PACKED ? 2 * W : W;
+    double* aKs = VB_GATHER_PACKED ? S.accK() + 2 * t : S.accK() + t;
+    double* aMs = VB_GATHER_PACKED ? aKs + 1 : S.accM() + t;
     for (int64_t k = 0;; k++) {
         const int64_t b = blockIdx.x + k * gstep;
         if (b >= nblocks) break;
@@ -609,8 +625,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             double mrow = 0.0;
             if (R.own) {
                 for (int s = 0; s < R.L; s++) {
-                    aKs[s * W] = 0.0;
-                    aMs[s * W] = 0.0;
+                    aKs[s * STF] = 0.0;
+                    aMs[s * STF] = 0.0;
                 }
                 double xv[DIM];
 #pragma unroll
@@ -619,7 +635,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #pragma unroll
                     for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * W + t] - xv[c];
                 };
-                mrow = gather_row<DIM, W, COEF>(R.i0, R.i1, slots, ev, aK, aM, xv, cp);
+                mrow = gather_row<DIM, STF, COEF>(R.i0, R.i1, slots, ev, aK, aM, xv, cp);
             }
             __syncwarp();
             // finish the row (diagonal from the partition of unity, M scale) while
@@ -633,7 +649,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                 const int b = R.lo - B0.p0;
                 for (int s = 0; s < R.L; s++) {
                     if (s == R.s0) continue;
-                    double kk = aKs[s * W], mm = aMs[s * W] * MS;
+                    double kk = aKs[s * STF], mm = aMs[s * STF] * MS;
                     sk += kk;
                     sm += mm;
                     stK[b + s] = kk;
