@@ -517,6 +517,15 @@ struct GatherSmem {
     __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + GatherCfg<DIM>::BAR_OFF) + r; }
 };
 
+// Edge-vector / column-coordinate buffer F: coordinates (x, y) of slot s of lane
+// t interleaved as one 16-byte pair per (s, t), z in a separate [slot][lane]
+// plane -- every access of the inner loop is bank-conflict free and (x, y) is
+// a single 128-bit shared load.
+template <int DIM>
+__device__ __forceinline__ int fidx(int s, int c, int t) {
+    return c < 2 ? (s * GATHER_ROWS + t) * 2 + c : 2 * GatherCfg<DIM>::CAP + s * GATHER_ROWS + t;
+}
+
 // word offset of element x within its 16-byte aligned TMA chunk
 __device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
 
@@ -562,7 +571,7 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBo
             int64_t w = cols[s];
             if (w == R.v) R.s0 = s;
 #pragma unroll
-            for (int c = 0; c < DIM; c++) cp_async8(F + (s * DIM + c) * GATHER_ROWS + t, coords + c * cst + w * ns);
+            for (int c = 0; c < DIM; c++) cp_async8(F + fidx<DIM>(s, c, t), coords + c * cst + w * ns);
         }
     }
     return fast;
@@ -600,7 +609,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 
     double* F = S.F();
 #ifndef VB_GATHER_PACKED
-#define VB_GATHER_PACKED 0
+#define VB_GATHER_PACKED 1
 #endif
     // accumulators: [slot][lane] planes of K then M, or (packed) interleaved (K, M)
     // pairs so one 16-byte access serves both matrices
@@ -630,10 +639,11 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                 }
                 double xv[DIM];
 #pragma unroll
-                for (int c = 0; c < DIM; c++) xv[c] = F[(R.s0 * DIM + c) * W + t];
+                for (int c = 0; c < DIM; c++) xv[c] = F[fidx<DIM>(R.s0, c, t)];
                 auto ev = [&](int s, double(&f)[DIM]) {
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * W + t] - xv[c];
+                    for (int c = 0; c < 2; c++) f[c] = F[fidx<DIM>(s, c, t)] - xv[c];   // (x, y): one 16-byte load
+                    if constexpr (DIM == 3) f[2] = F[fidx<DIM>(s, 2, t)] - xv[2];
                 };
                 mrow = gather_row<DIM, STF, COEF>(R.i0, R.i1, slots, ev, aK, aM, xv, cp);
             }
