@@ -38,10 +38,32 @@ __global__ void bucket_fill_k(int64_t ne, int nv, const int32_t* __restrict__ el
 }
 
 // insertion sort of each node's incidence list (ascending e, hence ascending e*4+a)
-__global__ void sort_incidences_k(int64_t nn, const int32_t* __restrict__ nptr, int32_t* __restrict__ node_elem) {
+// Lists of up to SORT_CAP entries are loaded into a per-thread shared-memory
+// strip (stride SORT_BLOCK, bank-conflict free), sorted there and written back
+// coalesced per thread; longer lists are sorted in place in global memory.
+constexpr int SORT_BLOCK = 128;
+constexpr int SORT_CAP = 48;
+__global__ void __launch_bounds__(SORT_BLOCK) sort_incidences_k(int64_t nn, const int32_t* __restrict__ nptr,
+                                                                int32_t* __restrict__ node_elem) {
+    __shared__ int32_t strip[SORT_CAP * SORT_BLOCK];
+    int32_t* L = strip + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
         int lo = nptr[v], hi = nptr[v + 1];
+        const int n = hi - lo;
+        if (n <= SORT_CAP) {
+            for (int i = 0; i < n; i++) {
+                int32_t x = node_elem[lo + i];
+                int j = i - 1;
+                while (j >= 0 && L[j * SORT_BLOCK] > x) {
+                    L[(j + 1) * SORT_BLOCK] = L[j * SORT_BLOCK];
+                    j--;
+                }
+                L[(j + 1) * SORT_BLOCK] = x;
+            }
+            for (int i = 0; i < n; i++) node_elem[lo + i] = L[i * SORT_BLOCK];
+            continue;
+        }
         for (int i = lo + 1; i < hi; i++) {
             int32_t x = node_elem[i];
             int j = i - 1;
@@ -265,7 +287,7 @@ extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32
     if (st != VB_OK) return st;
     cudaMemcpyAsync(w.cursor, nptr, 4 * (nn + 1), cudaMemcpyDeviceToDevice, s);
     if (ne > 0) bucket_fill_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor, nelem);
-    if (nn > 0) sort_incidences_k<<<gn, 256, 0, s>>>(nn, nptr, nelem);
+    if (nn > 0) sort_incidences_k<<<grid_for(nn, SORT_BLOCK, 8), SORT_BLOCK, 0, s>>>(nn, nptr, nelem);
     if ((st = launch_check("fem_p1_pattern(incidences)")) != VB_OK) return st;
 
     unsigned gr = grid_for(nn, PAT_BLOCK, 4);
