@@ -181,13 +181,16 @@ __global__ void __launch_bounds__(PAT_BLOCK) row_fill_k(int64_t nn, int64_t ne, 
                                                         const int32_t* __restrict__ node_elem,
                                                         const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
                                                         int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots,
-                                                        int* flags) {
+                                                        int32_t* __restrict__ ovf_list, int* flags) {
     __shared__ int32_t Ls[ROW_CAP * PAT_BLOCK];
     int32_t* L = Ls + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
         int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, PAT_BLOCK, ROW_CAP);
-        if (cnt < 0) continue;  // fallback rows
+        if (cnt < 0) {  // long row: the single-thread fallback fills it
+            ovf_list[atomicAdd(flags + FLAG_OVERFLOW_ROWS, 1)] = (int32_t)v;
+            continue;
+        }
         emit_row(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, PAT_BLOCK, row_ptr, col_idx, elem2nnz, slots, flags);
     }
 }
@@ -314,10 +317,9 @@ extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32
     if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
     if (nnz32 < 0 || nnz32 > col_cap) { set_error("fem_p1_pattern: col_cap=%lld < nnz=%d", (long long)col_cap, nnz32); return VB_ERR_ARG; }
     if (nn > 0) {
-        // the fallback row list is rebuilt by the count kernel's overflow path
-        row_count_k<<<gr, PAT_BLOCK, 0, s>>>(nn, nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        // rows longer than ROW_CAP are collected by row_fill_k and filled by the fallback
         row_fill_k<<<gr, PAT_BLOCK, 0, s>>>(nn, ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
-                                            node_elem_slot, w.flags);
+                                            node_elem_slot, w.ovf, w.flags);
         row_fill_big_k<<<64, 32, 0, s>>>(ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
                                           node_elem_slot, w.ovf, w.flags);
     }
