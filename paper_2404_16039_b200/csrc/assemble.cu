@@ -640,9 +640,11 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #pragma unroll
                 for (int c = 0; c < DIM; c++) xv[c] = F[fidx<DIM>(R.s0, c, t)];
                 auto ev = [&](int s, double(&f)[DIM]) {
+                    VB_CHECK(s < R.L && s != R.s0);
 #pragma unroll
                     for (int c = 0; c < DIM; c++) f[c] = F[fidx<DIM>(s, c, t)] - xv[c];
                 };
+                VB_CHECK(R.i0 >= B0.q0 && R.i1 <= B0.q1 && R.lo >= B0.p0 && R.lo + R.L <= B0.p1);
                 mrow = gather_row<DIM, STF, COEF>(R.i0, R.i1, slots, ev, aK, aM, xv, cp);
             }
             __syncwarp();
@@ -685,6 +687,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #pragma unroll
             for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + R.v * ns);
             auto ev = [&](int s, double(&f)[DIM]) {
+                VB_CHECK(s < R.L && s != s0);
                 int64_t w = __ldg(col_idx + R.lo + s);
 #pragma unroll
                 for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];

@@ -132,6 +132,7 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
         int byte = 1;
         for (int b = 0; b < nv; b++) {
             int pos = lower_bound_s(L, st, cnt, elems[b * eld + e]);
+            VB_CHECK(pos < cnt && L[pos * st] == elems[b * eld + e]);   // every vertex is in the row
             if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
             int sh = (b == a) ? 0 : 8 * byte++;
             packed |= (uint32_t)(pos & 0xff) << sh;

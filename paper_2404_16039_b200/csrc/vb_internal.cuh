@@ -38,6 +38,19 @@ inline unsigned grid_for(int64_t units, int block, int blocks_per_sm, int waves 
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Device-side bounds checks, compiled in only for the debug variant
+// (tools/build_variant.py debug -DVB_DEBUG_BOUNDS): a failed check traps.
+#ifdef VB_DEBUG_BOUNDS
+#define VB_CHECK(cond)      \
+    do {                    \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define VB_CHECK(cond) \
+    do {               \
+    } while (0)
+#endif
+
 // streaming (evict-first) loads/stores for data touched once
 __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 __device__ __forceinline__ double2 ldcs2(const double* p) { return __ldcs(reinterpret_cast<const double2*>(p)); }
