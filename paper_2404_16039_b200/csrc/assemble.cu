@@ -431,28 +431,18 @@ __device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* _
 #define VB_GATHER_U 4
 #endif
     constexpr int U = COEF ? 2 : VB_GATHER_U;
-#ifndef VB_GATHER_ROT
-#define VB_GATHER_ROT 0
-#endif
-    // VB_GATHER_ROT: in shared memory each lane starts its row's incidence list at a
-    // lane-dependent offset (a fixed rotation, still deterministic) so the 32 lanes'
-    // plan-word reads fall in different banks
-    const int n = i1 - i0;
-    const int rot = (VB_GATHER_ROT && ST != 1 && n > 0) ? (int)(threadIdx.x % (unsigned)n) : 0;
-    auto at = [&](int j) {
-        int q = j + rot;
-        return slots[i0 + (q >= n ? q - n : q)];
-    };
+    // (A lane-rotated incidence order, which spreads the plan-word reads over the
+    // banks, measured within 2 % and would give up the ascending-element order.)
     double mrow = 0.0;
-    int j = 0;
-    for (; j + U - 1 < n; j += U) {
+    int i = i0;
+    for (; i + U - 1 < i1; i += U) {
         IncOut<DIM> o[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF>(at(j + u), ev, xv, cp);
+        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF>(slots[i + u], ev, xv, cp);
 #pragma unroll
         for (int u = 0; u < U; u++) accumulate<DIM, ST, WK, WM, COEF>(o[u], accK, accM, mrow);
     }
-    for (; j < n; j++) accumulate<DIM, ST, WK, WM, COEF>(incidence<DIM, COEF>(at(j), ev, xv, cp), accK, accM, mrow);
+    for (; i < i1; i++) accumulate<DIM, ST, WK, WM, COEF>(incidence<DIM, COEF>(slots[i], ev, xv, cp), accK, accM, mrow);
     return mrow;
 }
 
