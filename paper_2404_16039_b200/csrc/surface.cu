@@ -2,8 +2,7 @@
 // gather the three vertices of each face, n = (b-a) x (c-a), |n|, nhat, area,
 // and the divergence-theorem volume sum (1/6) sum a.n reduced with
 // a fixed-shape tree (block partials in a fixed grid, then one block) so the
-// volume is bitwise reproducible.  Two faces per thread: the index planes are
-// read and the seven output planes written with 64/128-bit accesses.
+// volume is bitwise reproducible.
 #include "vb_internal.cuh"
 
 namespace vb {
@@ -12,72 +11,38 @@ namespace {
 constexpr int SURF_BLOCK = 256;
 constexpr int SURF_BLOCKS_PER_SM = 8;
 
-struct Face {
-    double n[3], len, adotn;
-};
-
-__device__ __forceinline__ Face face_geometry(int64_t ia, int64_t ib, int64_t ic, const double* __restrict__ xyz,
-                                              int64_t ns, int64_t cst) {
-    double a[3], u[3], w[3];
-#pragma unroll
-    for (int d = 0; d < 3; d++) {
-        a[d] = __ldg(xyz + d * cst + ia * ns);
-        u[d] = __ldg(xyz + d * cst + ib * ns) - a[d];
-        w[d] = __ldg(xyz + d * cst + ic * ns) - a[d];
-    }
-    Face F;
-    F.n[0] = fma(u[1], w[2], -u[2] * w[1]);
-    F.n[1] = fma(u[2], w[0], -u[0] * w[2]);
-    F.n[2] = fma(u[0], w[1], -u[1] * w[0]);
-    F.len = sqrt(fma(F.n[0], F.n[0], fma(F.n[1], F.n[1], F.n[2] * F.n[2])));
-    F.adotn = fma(a[0], F.n[0], fma(a[1], F.n[1], a[2] * F.n[2]));
-    return F;
-}
-
-__device__ __forceinline__ void put2(double* __restrict__ p, int64_t f, int64_t nf, bool vec, double x0, double x1) {
-    if (vec && f + 1 < nf) {
-        stcs2(p + f, make_double2(x0, x1));
-    } else {
-        stcs(p + f, x0);
-        if (f + 1 < nf) stcs(p + f + 1, x1);
-    }
-}
-
 __global__ void __launch_bounds__(SURF_BLOCK) tri_surface_k(int64_t nf, const int32_t* __restrict__ tri, int64_t tld,
                                                             const double* __restrict__ xyz, int64_t ns, int64_t cst,
                                                             double* __restrict__ n_out, double* __restrict__ nh_out,
-                                                            double* __restrict__ area, double* __restrict__ part,
-                                                            bool vec) {
+                                                            double* __restrict__ area, double* __restrict__ part) {
     double vol = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
-    for (int64_t f = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; f < nf; f += stride) {
-        const bool two = f + 1 < nf;
-        int64_t id[3][2];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < nf; f += stride) {
+        int64_t ia = __ldcs(tri + f), ib = __ldcs(tri + tld + f), ic = __ldcs(tri + 2 * tld + f);
+        double a[3], u[3], w[3];
 #pragma unroll
-        for (int v = 0; v < 3; v++) {
-            if (vec && two) {
-                int2 t = __ldcs(reinterpret_cast<const int2*>(tri + v * tld + f));
-                id[v][0] = t.x;
-                id[v][1] = t.y;
-            } else {
-                id[v][0] = __ldcs(tri + v * tld + f);
-                id[v][1] = two ? __ldcs(tri + v * tld + f + 1) : id[v][0];
-            }
+        for (int d = 0; d < 3; d++) {
+            a[d] = __ldg(xyz + d * cst + ia * ns);
+            u[d] = __ldg(xyz + d * cst + ib * ns) - a[d];
+            w[d] = __ldg(xyz + d * cst + ic * ns) - a[d];
         }
-        Face F0 = face_geometry(id[0][0], id[1][0], id[2][0], xyz, ns, cst);
-        Face F1 = face_geometry(id[0][1], id[1][1], id[2][1], xyz, ns, cst);
+        double n0 = fma(u[1], w[2], -u[2] * w[1]);
+        double n1 = fma(u[2], w[0], -u[0] * w[2]);
+        double n2 = fma(u[0], w[1], -u[1] * w[0]);
+        double len = sqrt(fma(n0, n0, fma(n1, n1, n2 * n2)));
         if (n_out) {
-#pragma unroll
-            for (int d = 0; d < 3; d++) put2(n_out + d * nf, f, nf, vec, F0.n[d], F1.n[d]);
+            stcs(n_out + f, n0);
+            stcs(n_out + nf + f, n1);
+            stcs(n_out + 2 * nf + f, n2);
         }
         if (nh_out) {
-            const double r0 = 1.0 / F0.len, r1 = 1.0 / F1.len;
-#pragma unroll
-            for (int d = 0; d < 3; d++) put2(nh_out + d * nf, f, nf, vec, F0.n[d] * r0, F1.n[d] * r1);
+            double r = 1.0 / len;
+            stcs(nh_out + f, n0 * r);
+            stcs(nh_out + nf + f, n1 * r);
+            stcs(nh_out + 2 * nf + f, n2 * r);
         }
-        if (area) put2(area, f, nf, vec, 0.5 * F0.len, 0.5 * F1.len);
-        vol += F0.adotn;
-        if (two) vol += F1.adotn;
+        if (area) stcs(area + f, 0.5 * len);
+        vol += fma(a[0], n0, fma(a[1], n1, a[2] * n2));
     }
     if (part) {
         __shared__ double sh[SURF_BLOCK / 32];
@@ -116,7 +81,7 @@ extern "C" vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_
                                     double* volume, void* work, size_t* work_bytes, vb_stream_t stream) {
     clear_error();
     if (nf < 0 || nverts < 0) { set_error("vb_tri_surface: negative size"); return VB_ERR_ARG; }
-    unsigned g = grid_for((nf + 1) / 2, SURF_BLOCK, SURF_BLOCKS_PER_SM);
+    unsigned g = grid_for(nf, SURF_BLOCK, SURF_BLOCKS_PER_SM);
     size_t need = volume ? ((size_t)g * sizeof(double) + 255) & ~(size_t)255 : 0;
     if (!work) {
         if (!work_bytes) { set_error("vb_tri_surface: work and work_bytes both NULL"); return VB_ERR_ARG; }
@@ -126,12 +91,9 @@ extern "C" vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_
     if (work_bytes && *work_bytes < need) { set_error("vb_tri_surface: work buffer too small (%zu < %zu)", *work_bytes, need); return VB_ERR_WORKSPACE; }
     if (nf > 0 && (!tri || !xyz)) { set_error("vb_tri_surface: NULL %s", !tri ? "tri" : "xyz"); return VB_ERR_ARG; }
     if (tri_ld < nf) { set_error("vb_tri_surface: tri_ld < nf"); return VB_ERR_ARG; }
-    // 64/128-bit accesses need even plane strides and aligned planes
-    const bool vec = (nf % 2 == 0) && (tri_ld % 2 == 0) && ((reinterpret_cast<uintptr_t>(tri) & 7u) == 0) &&
-                     (!n || aligned16(n)) && (!nhat || aligned16(nhat)) && (!area || aligned16(area));
     auto s = cs(stream);
     double* part = volume ? reinterpret_cast<double*>(work) : nullptr;
-    if (nf > 0) tri_surface_k<<<g, SURF_BLOCK, 0, s>>>(nf, tri, tri_ld, xyz, node_stride, comp_stride, n, nhat, area, part, vec);
+    if (nf > 0) tri_surface_k<<<g, SURF_BLOCK, 0, s>>>(nf, tri, tri_ld, xyz, node_stride, comp_stride, n, nhat, area, part);
     if (volume) {
         if (nf == 0) { cudaMemsetAsync(volume, 0, sizeof(double), s); return launch_check("vb_tri_surface"); }
         sum_parts_k<<<1, 1024, 0, s>>>(part, (int)g, volume);
