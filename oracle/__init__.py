@@ -54,6 +54,9 @@ def lib():
             "orc_p1_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i32, d, p, d, p, p, p]),
             "orc_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p]),
             "orc_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p]),
+            "orc_pattern": (i64, [i32, i64, i64, p, i64, p, p]),
+            "orc_p2_local_coef": (i32, [i32, p, i32, d, p, d, p, p, p]),
+            "orc_p2_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i32, d, p, d, p, p, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -215,8 +218,8 @@ def p1_assemble(coords, elems, row_ptr, col_idx, row_mask=None):
 # ------------------------------------------------------------------ NEXT-1
 def quad_rule(dim, gqo):
     """(lam (nip, dim+1) barycentric points, w (nip,)) of intquad(gqo, dim)."""
-    lam = np.empty(16)
-    w = np.empty(4)
+    lam = np.empty(64)
+    w = np.empty(16)
     nip = lib().orc_quad_rule(dim, gqo, _p(lam), _p(w))
     if nip < 0:
         raise ValueError("no quadrature rule for dim=%d gqo=%d" % (dim, gqo))
@@ -279,3 +282,43 @@ def p1_rhs(coords, elems, fq, gqo=2):
     b2 = np.empty((nv, ne))
     _check(lib().orc_p1_rhs(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne, gqo, _p(fq), _p(b2), _p(b)), "rhs")
     return b, b2
+
+
+# ------------------------------------------------------------------ NEXT-3 (P2)
+def pattern(elems, nn):
+    """Topological CSR pattern for elements with any number of nodes (P2: 6 / 10)."""
+    elems = _i32(elems)
+    nv, ne = elems.shape
+    row_ptr = np.empty(nn + 1, dtype=np.int32)
+    nnz = lib().orc_pattern(nv, nn, ne, _p(elems), ne, _p(row_ptr), None)
+    if nnz < 0:
+        raise MemoryError("oracle pattern")
+    col_idx = np.empty(max(nnz, 1), dtype=np.int32)
+    assert lib().orc_pattern(nv, nn, ne, _p(elems), ne, _p(row_ptr), _p(col_idx)) == nnz
+    return row_ptr, col_idx[:nnz]
+
+
+def p2_local_coef(X, gqo=4, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0))):
+    """P2 element matrices; X (dim, nlb) node coordinates (vertices, then edges)."""
+    X = _f64(X)
+    dim, nlb = X.shape
+    (ka, kb), (ma, mb) = _coef(dim, cK), _coef(dim, cM)
+    Ke = np.empty((nlb, nlb))
+    Me = np.empty((nlb, nlb))
+    _check(lib().orc_p2_local_coef(dim, _p(X), gqo, ka, _p(kb), ma, _p(mb), _p(Ke), _p(Me)), "p2_local")
+    return Ke, Me
+
+
+def p2_assemble_coef(coords, elems, row_ptr, col_idx, gqo=4, cK=(1.0, (1.0, 1.0, 1.0)),
+                     cM=(1.0, (1.0, 1.0, 1.0))):
+    coords, elems = _f64(coords), _i32(elems)
+    row_ptr, col_idx = _i32(row_ptr), _i32(col_idx)
+    dim, nn = coords.shape
+    nlb, ne = elems.shape
+    (ka, kb), (ma, mb) = _coef(dim, cK), _coef(dim, cM)
+    nnz = int(row_ptr[-1])
+    K = np.empty(nnz)
+    M = np.empty(nnz)
+    _check(lib().orc_p2_assemble_coef(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne, _p(row_ptr), _p(col_idx),
+                                      gqo, ka, _p(kb), ma, _p(mb), _p(K), _p(M)), "p2_assemble")
+    return K, M

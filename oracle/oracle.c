@@ -303,10 +303,16 @@ static int cmp_i32(const void* x, const void* y) {
 /* O10: topological CSR pattern of sparse(X3D(:),Y3D(:),...):
  * for e, a, b: push elems[e][b] into rows[elems[e][a]]; per row sort + unique
  * (explicit zeros kept); row_ptr = exclusive scan of row sizes.
- * Returns nnz.  With col_idx == NULL only row_ptr is written. */
+ * Returns nnz.  With col_idx == NULL only row_ptr is written.  orc_pattern
+ * takes the number of nodes per element (P2: 6 or 10). */
+int64_t orc_pattern(int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
+                    int32_t* row_ptr, int32_t* col_idx);
 int64_t orc_p1_pattern(int dim, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
                        int32_t* row_ptr, int32_t* col_idx) {
-    int nv = dim + 1;
+    return orc_pattern(dim + 1, nn, ne, elems, elem_ld, row_ptr, col_idx);
+}
+int64_t orc_pattern(int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
+                    int32_t* row_ptr, int32_t* col_idx) {
     int64_t* cnt = calloc((size_t)nn + 1, sizeof(int64_t));
     if (!cnt) return -1;
     for (int64_t e = 0; e < ne; e++)
@@ -419,6 +425,40 @@ int orc_quad_rule(int dim, int gqo, double* lam, double* w) {
         }
         return 4;
     }
+    /* gqo = 4 (P2): degree-4 rules -- 2D: Dunavant's 6 points,
+     * (1-2a, a, a) and permutations for (a, w) = (0.44594849091596488632,
+     * 0.22338158967801146570/2), (0.09157621350977074346, 0.10995174365532186764/2);
+     * 3D: Keast's 11 points -- centroid with w = -74/5625, (11/14, 1/14, 1/14, 1/14)
+     * and permutations with w = 343/45000, (a, a, b, b) and permutations with
+     * a = (1 + sqrt(5/14))/4, b = (1 - sqrt(5/14))/4, w = 56/2250. */
+    if (gqo == 4 && dim == 2) {
+        const double as[2] = {0.44594849091596488632, 0.09157621350977074346};
+        const double ws[2] = {0.22338158967801146570, 0.10995174365532186764};
+        int q = 0;
+        for (int k = 0; k < 2; k++)
+            for (int p = 0; p < 3; p++) {
+                for (int a = 0; a < 3; a++) lam[q * 3 + a] = (a == p) ? 1.0 - 2.0 * as[k] : as[k];
+                w[q] = ws[k] / 2.0;
+                q++;
+            }
+        return 6;
+    }
+    if (gqo == 4 && dim == 3) {
+        int q = 0;
+        for (int a = 0; a < 4; a++) lam[a] = 0.25;
+        w[q++] = -74.0 / 5625.0;
+        for (int p = 0; p < 4; p++) {
+            for (int a = 0; a < 4; a++) lam[q * 4 + a] = (a == p) ? 11.0 / 14.0 : 1.0 / 14.0;
+            w[q++] = 343.0 / 45000.0;
+        }
+        const double pa = (1.0 + sqrt(5.0 / 14.0)) / 4.0, pb = (1.0 - sqrt(5.0 / 14.0)) / 4.0;
+        for (int i = 0; i < 4; i++)
+            for (int j = i + 1; j < 4; j++) {
+                for (int a = 0; a < 4; a++) lam[q * 4 + a] = (a == i || a == j) ? pa : pb;
+                w[q++] = 56.0 / 2250.0;
+            }
+        return 11;
+    }
     return -1;
 }
 
@@ -440,7 +480,7 @@ static double coef_eval(int dim, double ca, const double* cb, const double* x) {
 int orc_p1_local_coef(int dim, const double* X, int gqo, double cKa, const double* cKb, double cMa,
                       const double* cMb, double* Ke, double* Me) {
     int nv = dim + 1;
-    double lam[16], w[4];
+    double lam[64], w[16];
     int nip = orc_quad_rule(dim, gqo, lam, w);
     if (nip < 0) return ORC_ERR_ARG;
     double J[16], Jinv[16], G[16];
@@ -544,7 +584,7 @@ int orc_page_bilinear(int64_t np, int n, int m, const double* A, int64_t lda, co
 int orc_p1_rhs(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride, int64_t comp_stride,
                const int32_t* elems, int64_t elem_ld, int gqo, const double* fq, double* b2D, double* b) {
     int nv = dim + 1;
-    double lam[16], w[4];
+    double lam[64], w[16];
     int nip = orc_quad_rule(dim, gqo, lam, w);
     if (nip < 0) return ORC_ERR_ARG;
     if (b)
@@ -568,6 +608,122 @@ int orc_p1_rhs(int dim, int64_t nn, int64_t ne, const double* coords, int64_t no
             if (b2D) b2D[(int64_t)a * ne + e] = loc[a];
             if (b) b[elems[a * elem_ld + e]] += loc[a];
         }
+    }
+    return ORC_OK;
+}
+
+/* ------------------------------------------------------- NEXT-3: P2 elements */
+
+static const int P2_EDGE_2D[3][2] = {{0, 1}, {1, 2}, {0, 2}};
+static const int P2_EDGE_3D[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+
+/* shapefun / shapeder for P2: vertex a: lam_a (2 lam_a - 1); edge
+ * (i, j): 4 lam_i lam_j (node order: vertices, then edges in the canonical
+ * order of SPEC S:304).  Reference coordinates xi_r = lam_{r+1}, lam_0 = 1 - sum xi;
+ * dshape[r][k] = d phi_k / d xi_r. */
+static void p2_shape(int dim, const double* lam, double* phi, double* dshape /* dim x nlb, [r*10 + k] */) {
+    int nv = dim + 1, ne = dim == 2 ? 3 : 6;
+    const int(*E)[2] = dim == 2 ? P2_EDGE_2D : P2_EDGE_3D;
+    double dl[10][4];  /* d phi_k / d lam_b */
+    for (int k = 0; k < 10; k++)
+        for (int b = 0; b < 4; b++) dl[k][b] = 0.0;
+    for (int a = 0; a < nv; a++) {
+        phi[a] = lam[a] * (2.0 * lam[a] - 1.0);
+        dl[a][a] = 4.0 * lam[a] - 1.0;
+    }
+    for (int k = 0; k < ne; k++) {
+        int i = E[k][0], j = E[k][1];
+        phi[nv + k] = 4.0 * lam[i] * lam[j];
+        dl[nv + k][i] = 4.0 * lam[j];
+        dl[nv + k][j] = 4.0 * lam[i];
+    }
+    for (int r = 0; r < dim; r++)
+        for (int k = 0; k < nv + ne; k++) dshape[r * 10 + k] = dl[k][r + 1] - dl[k][0];
+}
+
+/* Element matrices of stiffness_matrixP2 / mass_matrixP2, point by
+ * point as Code phider and Code mass_scalar_P2:
+ *   tjac = dshape * X^T over all nlb nodes (the iso-parametric map), jacinv, detj,
+ *   dphi = jacinv * dshape;  K_e += w_q (|det| (c_K(x_q) dphi^T dphi));
+ *   M_e += w_q (|det| (c_M(x_q) phi phi^T)),  x_q = sum_k phi_k(q) x_k.
+ * X[c*nlb + k]: coordinate c of node k.  Ke, Me: nlb x nlb row-major. */
+int orc_p2_local_coef(int dim, const double* X, int gqo, double cKa, const double* cKb, double cMa,
+                      const double* cMb, double* Ke, double* Me) {
+    int nv = dim + 1, nlb = dim == 2 ? 6 : 10;
+    double lam[64], w[16];
+    int nip = orc_quad_rule(dim, gqo, lam, w);
+    if (nip < 0) return ORC_ERR_ARG;
+    for (int p = 0; p < nlb * nlb; p++) {
+        Ke[p] = 0.0;
+        Me[p] = 0.0;
+    }
+    for (int q = 0; q < nip; q++) {
+        double phi[10], ds[30], J[16], Jinv[16], dphi[30];
+        p2_shape(dim, lam + q * nv, phi, ds);
+        for (int r = 0; r < dim; r++)
+            for (int c = 0; c < dim; c++) {
+                double s = 0.0;
+                for (int k = 0; k < nlb; k++) s = s + ds[r * 10 + k] * X[c * nlb + k];
+                J[r * 4 + c] = s;
+            }
+        double detJ = det_laplace(J, dim);
+        for (int i = 0; i < dim; i++)
+            for (int j = 0; j < dim; j++) {
+                double cof = minor_rc(J, dim, j, i);
+                if ((i + j) % 2) cof = -cof;
+                Jinv[i * 4 + j] = cof / detJ;
+            }
+        for (int r = 0; r < dim; r++)
+            for (int k = 0; k < nlb; k++) {
+                double s = 0.0;
+                for (int l = 0; l < dim; l++) s = s + Jinv[r * 4 + l] * ds[l * 10 + k];
+                dphi[r * 10 + k] = s;
+            }
+        double xq[3];
+        for (int c = 0; c < dim; c++) {
+            double s = 0.0;
+            for (int k = 0; k < nlb; k++) s = s + phi[k] * X[c * nlb + k];
+            xq[c] = s;
+        }
+        double cK = coef_eval(dim, cKa, cKb, xq), cM = coef_eval(dim, cMa, cMb, xq);
+        double adet = fabs(detJ);
+        for (int a = 0; a < nlb; a++)
+            for (int b = 0; b < nlb; b++) {
+                double gtg = 0.0;
+                for (int r = 0; r < dim; r++) gtg = gtg + dphi[r * 10 + a] * dphi[r * 10 + b];
+                Ke[a * nlb + b] = Ke[a * nlb + b] + w[q] * (adet * (cK * gtg));
+                Me[a * nlb + b] = Me[a * nlb + b] + w[q] * (adet * (cM * (phi[a] * phi[b])));
+            }
+    }
+    return ORC_OK;
+}
+
+/* P2 assembly: sparse() of the nlb x nlb element matrices, O11 order. */
+int orc_p2_assemble_coef(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                         int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                         const int32_t* row_ptr, const int32_t* col_idx, int gqo, double cKa,
+                         const double* cKb, double cMa, const double* cMb, double* K, double* M) {
+    int nlb = dim == 2 ? 6 : 10;
+    int64_t nnz = row_ptr[nn];
+    for (int64_t p = 0; p < nnz; p++) {
+        K[p] = 0.0;
+        M[p] = 0.0;
+    }
+    for (int64_t e = 0; e < ne; e++) {
+        int32_t vid[10];
+        double X[30], Ke[100], Me[100];
+        for (int a = 0; a < nlb; a++) vid[a] = elems[a * elem_ld + e];
+        for (int a = 0; a < nlb; a++)
+            for (int c = 0; c < dim; c++) X[c * nlb + a] = coords[c * comp_stride + (int64_t)vid[a] * node_stride];
+        int rc = orc_p2_local_coef(dim, X, gqo, cKa, cKb, cMa, cMb, Ke, Me);
+        if (rc) return rc;
+        for (int a = 0; a < nlb; a++)
+            for (int b = 0; b < nlb; b++) {
+                int64_t p = find_col(row_ptr, col_idx, vid[a], vid[b]);
+                if (p < 0) return -3;
+                K[p] += Ke[a * nlb + b];
+                M[p] += Me[a * nlb + b];
+            }
     }
     return ORC_OK;
 }

@@ -18,7 +18,7 @@ Layouts produced here are the ones the C ABI consumes (include/vb.h):
 """
 from .rng import splitmix64_u64, uniform01, uniform_pm1, normal
 from .meshes import (square_p1, square_crossed_p1, cube_kuhn_p1, icosphere, square_counts,
-                     cube_counts, icosphere_counts)
+                     cube_counts, icosphere_counts, p2_from_p1, P2_EDGES)
 from .pages import normal_pages, inverse_pages, integer_pages
 
 __all__ = [

@@ -145,6 +145,33 @@ def square_crossed_p1(n):
     return coords, elems
 
 
+P2_EDGES = {2: ((0, 1), (1, 2), (0, 2)),
+            3: ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))}
+
+
+def p2_from_p1(coords, elems):
+    """P2 mesh from a P1 mesh (the paper's "additional vertices located at the
+    midpoints of the edges"): midpoint nodes appended after the
+    vertices, ids in order of first creation scanning elements in order and each
+    element's edges in the canonical order P2_EDGES (2D edges
+    (1,2),(2,3),(1,3) -> local nodes 4,5,6; 3D (1,2),(1,3),(1,4),(2,3),(2,4),(3,4)
+    -> 5..10).  Returns (coords (dim, nn + n_edges), elems (nlb, ne) int32)."""
+    dim, nn = coords.shape
+    pairs = P2_EDGES[dim]
+    e64 = elems.astype(np.int64)
+    E = np.stack([np.stack([e64[a], e64[b]], 1) for a, b in pairs], 1).reshape(-1, 2)
+    key = np.minimum(E[:, 0], E[:, 1]) * nn + np.maximum(E[:, 0], E[:, 1])
+    _, first, inv = np.unique(key, return_index=True, return_inverse=True)
+    order = np.argsort(first, kind="stable")
+    rank = np.empty_like(order)
+    rank[order] = np.arange(order.size)
+    mid = nn + rank[inv].reshape(-1, len(pairs))
+    ue = E[first[order]]
+    coords2 = np.concatenate([coords, 0.5 * (coords[:, ue[:, 0]] + coords[:, ue[:, 1]])], axis=1)
+    elems2 = np.concatenate([elems, mid.T.astype(np.int32)], axis=0)
+    return np.ascontiguousarray(coords2), np.ascontiguousarray(elems2)
+
+
 _PHI = (1.0 + 5.0 ** 0.5) / 2.0
 _ICO_V = np.array([
     [-1, _PHI, 0], [1, _PHI, 0], [-1, -_PHI, 0], [1, -_PHI, 0],
