@@ -273,6 +273,35 @@ VB_API vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A,
                                   const double* Mx, int64_t ldm, const double* B, int64_t ldb,
                                   double* s, vb_stream_t stream);
 
+/* ---------------------------------------------------------- NEXT-3: P2 elements
+ * Topological CSR pattern (as fem_p1_pattern, same two phases and
+ * synchronisation) for elements with nv nodes, 2 <= nv <= 16 (P2: 6 in 2D, 10
+ * in 3D; sparse() of P:1033-1036), with the nv^2-plane element-to-nnz map
+ * elem2nnz (nullable).  Requires ne < 2^27.  No gather plan. */
+VB_API vb_status fem_pattern(int nv, int64_t nn, int64_t ne,
+                             const int32_t* elems, int64_t elem_ld,
+                             void* work, size_t* work_bytes,
+                             int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                             int32_t* elem2nnz, int64_t* nnz_out, vb_stream_t stream);
+
+/* P2 stiffness and mass matrices (stiffness_matrixP2 / mass_matrixP2,
+ * P:1009-1049) with c_K = cK_a exp(cK_b . x), c_M = cM_a exp(cM_b . x) (host
+ * arrays, NULL = 0) and intquad(gqo), gqo in {1, 2, 4} (4: Dunavant's 6-point
+ * rule in 2D, Keast's 11-point rule in 3D; the paper uses 4; reading in
+ * DESIGN.md §4).  elems: nlb = 6 (2D) / 10 (3D) node planes, vertices first,
+ * then edge midpoints in the order (1,2),(2,3),(1,3) / (1,2),(1,3),(1,4),(2,3),
+ * (2,4),(3,4); edges must be straight (midpoints exact).
+ * K_vals/M_vals (nnz, nullable) are zero-filled and accumulated with fp64
+ * atomics through elem2nnz from fem_pattern; K_local/M_local (nullable):
+ * nlb x nlb page arrays (ld = ne). */
+VB_API vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne,
+                                 const double* coords, int64_t node_stride, int64_t comp_stride,
+                                 const int32_t* elems, int64_t elem_ld,
+                                 const int32_t* elem2nnz, int64_t nnz,
+                                 int gqo, double cK_a, const double* cK_b, double cM_a, const double* cM_b,
+                                 double* K_vals, double* M_vals, double* K_local, double* M_local,
+                                 vb_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,22 +1,23 @@
 // a14/a15: topological CSR pattern of sparse(X3D(:),Y3D(:),...)
 // and the two scatter plans, built on the GPU without a global sort:
 //   1. node degree histogram, exclusive scan, bucket fill -> node->element
-//      incidence lists (packed e*4+a), each list sorted ascending (determinism);
+//      incidence lists (packed e << SH | a), each list sorted ascending (determinism);
 //   2. one thread per row builds the sorted unique column set of its row from
 //      the vertices of its incident elements in a per-thread shared-memory list
-//      (rows longer than ROW_CAP go to a single-thread fallback with a
-//      4096-entry list); row lengths -> scan -> row_ptr;
+//      (rows longer than CAP go to a single-thread fallback with a 4096-entry
+//      list); row lengths -> scan -> row_ptr;
 //   3. fill: the same per-row sets are written to col_idx, and every incidence
 //      (e, a) of row v records the in-row position of each of its element's
 //      vertices: elem2nnz (atomic scatter plan) and node_elem_slot (gather plan).
+// fem_p1_pattern: P1 (nv = dim+1 <= 4, packing e*4+a, 64-entry rows);
+// fem_pattern: any element with nv <= 16 nodes (P2: 6 / 10; packing e*16+a,
+// 128-entry rows), no gather plan.
 #include "vb_internal.cuh"
 
 namespace vb {
 namespace {
 
-constexpr int PAT_BLOCK = 128;
-constexpr int ROW_CAP = 64;       // per-thread sorted unique list (fast path)
-constexpr int ROW_CAP_BIG = 4096; // single-thread fallback list
+constexpr int ROW_CAP_BIG = 4096;      // single-thread fallback list
 constexpr int FLAG_OVERFLOW_ROWS = 0;  // number of rows that took the fallback
 constexpr int FLAG_TOO_LONG = 1;       // a row exceeded ROW_CAP_BIG
 constexpr int FLAG_SLOT_RANGE = 2;     // a row had > 255 entries while slots requested
@@ -27,20 +28,21 @@ __global__ void degree_k(int64_t ne, int nv, const int32_t* __restrict__ elems, 
         for (int a = 0; a < nv; a++) atomicAdd(deg + elems[a * eld + e], 1);
 }
 
+template <int SH>
 __global__ void bucket_fill_k(int64_t ne, int nv, const int32_t* __restrict__ elems, int64_t eld,
                               int32_t* __restrict__ cursor, int32_t* __restrict__ node_elem) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride)
         for (int a = 0; a < nv; a++) {
             int pos = atomicAdd(cursor + elems[a * eld + e], 1);
-            node_elem[pos] = (int32_t)(e * 4 + a);
+            node_elem[pos] = (int32_t)((e << SH) + a);
         }
 }
 
-// insertion sort of each node's incidence list (ascending e, hence ascending e*4+a)
+// insertion sort of each node's incidence list (ascending e, hence ascending e << SH | a).
 // Lists of up to SORT_CAP entries are loaded into a per-thread shared-memory
-// strip (stride SORT_BLOCK, bank-conflict free), sorted there and written back
-// coalesced per thread; longer lists are sorted in place in global memory.
+// strip (stride SORT_BLOCK, bank-conflict free), sorted there and written back;
+// longer lists are sorted in place in global memory.
 constexpr int SORT_BLOCK = 128;
 constexpr int SORT_CAP = 48;
 __global__ void __launch_bounds__(SORT_BLOCK) sort_incidences_k(int64_t nn, const int32_t* __restrict__ nptr,
@@ -98,14 +100,14 @@ __device__ __forceinline__ bool insert_unique(int32_t* L, int st, int& cnt, int 
 
 // Build row v's sorted unique column list into L (stride st, capacity cap).
 // Returns the count, or -1 on overflow.
+template <int SH>
 __device__ int build_row(int64_t v, int nv, const int32_t* __restrict__ elems, int64_t eld,
                          const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
                          int32_t* L, int st, int cap) {
     int cnt = 0;
     int lo = nptr[v], hi = nptr[v + 1];
     for (int i = lo; i < hi; i++) {
-        int32_t ea = node_elem[i];
-        int64_t e = ea >> 2;
+        int64_t e = node_elem[i] >> SH;
         for (int b = 0; b < nv; b++)
             if (!insert_unique(L, st, cnt, cap, elems[b * eld + e])) return -1;
     }
@@ -113,6 +115,7 @@ __device__ int build_row(int64_t v, int nv, const int32_t* __restrict__ elems, i
 }
 
 // write col_idx and the plans for row v whose list L (stride st) has cnt entries
+template <int SH>
 __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* __restrict__ elems, int64_t eld,
                          const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
                          const int32_t* L, int st, const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
@@ -124,8 +127,8 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
     int lo = nptr[v], hi = nptr[v + 1];
     for (int i = lo; i < hi; i++) {
         int32_t ea = node_elem[i];
-        int64_t e = ea >> 2;
-        int a = ea & 3;
+        int64_t e = ea >> SH;
+        int a = ea & ((1 << SH) - 1);
         // byte 0: in-row offset of the row's own vertex (the diagonal); bytes
         // 1..nv-1: offsets of the element's other vertices, ascending local index
         uint32_t packed = 0;
@@ -135,22 +138,23 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
             VB_CHECK(pos < cnt && L[pos * st] == elems[b * eld + e]);   // every vertex is in the row
             if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
             int sh = (b == a) ? 0 : 8 * byte++;
-            packed |= (uint32_t)(pos & 0xff) << sh;
+            if (sh < 32) packed |= (uint32_t)(pos & 0xff) << sh;
         }
         if (slots) slots[i] = packed;
     }
 }
 
-__global__ void __launch_bounds__(PAT_BLOCK) row_count_k(int64_t nn, int nv, const int32_t* __restrict__ elems,
-                                                         int64_t eld, const int32_t* __restrict__ nptr,
-                                                         const int32_t* __restrict__ node_elem,
-                                                         int32_t* __restrict__ row_len, int32_t* __restrict__ ovf_list,
-                                                         int* flags) {
-    __shared__ int32_t Ls[ROW_CAP * PAT_BLOCK];
+template <int SH, int CAP, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) row_count_k(int64_t nn, int nv, const int32_t* __restrict__ elems,
+                                                     int64_t eld, const int32_t* __restrict__ nptr,
+                                                     const int32_t* __restrict__ node_elem,
+                                                     int32_t* __restrict__ row_len, int32_t* __restrict__ ovf_list,
+                                                     int* flags) {
+    __shared__ int32_t Ls[CAP * BLOCK];
     int32_t* L = Ls + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
-        int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, PAT_BLOCK, ROW_CAP);
+        int cnt = build_row<SH>(v, nv, elems, eld, nptr, node_elem, L, BLOCK, CAP);
         if (cnt < 0) {
             int k = atomicAdd(flags + FLAG_OVERFLOW_ROWS, 1);
             ovf_list[k] = (int32_t)v;
@@ -160,7 +164,8 @@ __global__ void __launch_bounds__(PAT_BLOCK) row_count_k(int64_t nn, int nv, con
     }
 }
 
-// fallback for rows with more than ROW_CAP columns: one thread per row, big list
+// fallback for rows with more than CAP columns: one thread per row, big list
+template <int SH>
 __global__ void row_count_big_k(int nv, const int32_t* __restrict__ elems, int64_t eld, const int32_t* __restrict__ nptr,
                                 const int32_t* __restrict__ node_elem, int32_t* __restrict__ row_len,
                                 const int32_t* __restrict__ ovf_list, int* flags) {
@@ -169,7 +174,7 @@ __global__ void row_count_big_k(int nv, const int32_t* __restrict__ elems, int64
     for (int k = blockIdx.x; k < n_ovf; k += gridDim.x) {
         if (threadIdx.x == 0) {
             int64_t v = ovf_list[k];
-            int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, 1, ROW_CAP_BIG);
+            int cnt = build_row<SH>(v, nv, elems, eld, nptr, node_elem, L, 1, ROW_CAP_BIG);
             if (cnt < 0) { atomicExch(flags + FLAG_TOO_LONG, 1); cnt = 0; }
             row_len[v] = cnt;
         }
@@ -177,25 +182,27 @@ __global__ void row_count_big_k(int nv, const int32_t* __restrict__ elems, int64
     }
 }
 
-__global__ void __launch_bounds__(PAT_BLOCK) row_fill_k(int64_t nn, int64_t ne, int nv, const int32_t* __restrict__ elems,
-                                                        int64_t eld, const int32_t* __restrict__ nptr,
-                                                        const int32_t* __restrict__ node_elem,
-                                                        const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
-                                                        int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots,
-                                                        int32_t* __restrict__ ovf_list, int* flags) {
-    __shared__ int32_t Ls[ROW_CAP * PAT_BLOCK];
+template <int SH, int CAP, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) row_fill_k(int64_t nn, int64_t ne, int nv, const int32_t* __restrict__ elems,
+                                                    int64_t eld, const int32_t* __restrict__ nptr,
+                                                    const int32_t* __restrict__ node_elem,
+                                                    const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
+                                                    int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots,
+                                                    int32_t* __restrict__ ovf_list, int* flags) {
+    __shared__ int32_t Ls[CAP * BLOCK];
     int32_t* L = Ls + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
-        int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, PAT_BLOCK, ROW_CAP);
+        int cnt = build_row<SH>(v, nv, elems, eld, nptr, node_elem, L, BLOCK, CAP);
         if (cnt < 0) {  // long row: the single-thread fallback fills it
             ovf_list[atomicAdd(flags + FLAG_OVERFLOW_ROWS, 1)] = (int32_t)v;
             continue;
         }
-        emit_row(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, PAT_BLOCK, row_ptr, col_idx, elem2nnz, slots, flags);
+        emit_row<SH>(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, BLOCK, row_ptr, col_idx, elem2nnz, slots, flags);
     }
 }
 
+template <int SH>
 __global__ void row_fill_big_k(int64_t ne, int nv, const int32_t* __restrict__ elems, int64_t eld,
                                const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
                                const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
@@ -206,8 +213,9 @@ __global__ void row_fill_big_k(int64_t ne, int nv, const int32_t* __restrict__ e
     for (int k = blockIdx.x; k < n_ovf; k += gridDim.x) {
         if (threadIdx.x == 0) {
             int64_t v = ovf_list[k];
-            int cnt = build_row(v, nv, elems, eld, nptr, node_elem, L, 1, ROW_CAP_BIG);
-            if (cnt >= 0) emit_row(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, 1, row_ptr, col_idx, elem2nnz, slots, flags);
+            int cnt = build_row<SH>(v, nv, elems, eld, nptr, node_elem, L, 1, ROW_CAP_BIG);
+            if (cnt >= 0)
+                emit_row<SH>(v, cnt, nv, ne, elems, eld, nptr, node_elem, L, 1, row_ptr, col_idx, elem2nnz, slots, flags);
         }
         __syncthreads();
     }
@@ -245,35 +253,28 @@ Work carve(void* base, int64_t nn, int64_t ne, int nv) {
     return w;
 }
 
-}  // namespace
-}  // namespace vb
-
-using namespace vb;
-
-extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld, void* work,
-                                    size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
-                                    int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem,
-                                    uint32_t* node_elem_slot, int64_t* nnz_out, vb_stream_t stream) {
-    clear_error();
-    if (dim != 2 && dim != 3) { set_error("fem_p1_pattern: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
-    if (nn < 0 || ne < 0) { set_error("fem_p1_pattern: negative nn or ne"); return VB_ERR_ARG; }
-    const int nv = dim + 1;
-    if (ne >= (1ll << 29) || (int64_t)nv * nv * ne >= (1ll << 31) || nn >= (1ll << 31) - 1) {
-        set_error("fem_p1_pattern: ne=%lld / nn=%lld too large for int32 plans", (long long)ne, (long long)nn);
+template <int SH, int CAP, int BLOCK>
+vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
+                       void* work, size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                       int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem, uint32_t* node_elem_slot,
+                       int64_t* nnz_out, vb_stream_t stream) {
+    if (nn < 0 || ne < 0) { set_error("%s: negative nn or ne", fn); return VB_ERR_ARG; }
+    if (ne >= (1ll << (31 - SH)) || (int64_t)nv * nv * ne >= (1ll << 31) || nn >= (1ll << 31) - 1) {
+        set_error("%s: ne=%lld / nn=%lld too large for int32 plans", fn, (long long)ne, (long long)nn);
         return VB_ERR_OVERFLOW;
     }
     Work w = carve(nullptr, nn, ne, nv);
     if (!work) {
-        if (!work_bytes) { set_error("fem_p1_pattern: work and work_bytes both NULL"); return VB_ERR_ARG; }
+        if (!work_bytes) { set_error("%s: work and work_bytes both NULL", fn); return VB_ERR_ARG; }
         *work_bytes = w.bytes;
         return VB_OK;
     }
-    if (work_bytes && *work_bytes < w.bytes) { set_error("fem_p1_pattern: work buffer too small (%zu < %zu)", *work_bytes, w.bytes); return VB_ERR_WORKSPACE; }
-    if (!row_ptr) { set_error("fem_p1_pattern: NULL row_ptr"); return VB_ERR_ARG; }
-    if (ne > 0 && !elems) { set_error("fem_p1_pattern: NULL elems"); return VB_ERR_ARG; }
-    if (elem_ld < ne) { set_error("fem_p1_pattern: elem_ld < ne"); return VB_ERR_ARG; }
+    if (work_bytes && *work_bytes < w.bytes) { set_error("%s: work buffer too small (%zu < %zu)", fn, *work_bytes, w.bytes); return VB_ERR_WORKSPACE; }
+    if (!row_ptr) { set_error("%s: NULL row_ptr", fn); return VB_ERR_ARG; }
+    if (ne > 0 && !elems) { set_error("%s: NULL elems", fn); return VB_ERR_ARG; }
+    if (elem_ld < ne) { set_error("%s: elem_ld < ne", fn); return VB_ERR_ARG; }
     if ((node_elem_ptr != nullptr) != (node_elem != nullptr) || (node_elem_slot && !node_elem)) {
-        set_error("fem_p1_pattern: node_elem_ptr, node_elem (and node_elem_slot) must be given together");
+        set_error("%s: node_elem_ptr, node_elem (and node_elem_slot) must be given together", fn);
         return VB_ERR_ARG;
     }
     w = carve(work, nn, ne, nv);
@@ -285,29 +286,28 @@ extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32
     cudaMemsetAsync(w.cursor, 0, 4 * (nn + 1), s);
     cudaMemsetAsync(w.flags, 0, 64, s);
     unsigned ge = grid_for(ne, 256, 8);
-    unsigned gn = grid_for(nn, 256, 8);
     if (ne > 0) degree_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor);
     vb_status st = exclusive_scan_i32(w.cursor, nptr, nn, w.scan_tmp, s, nullptr);
     if (st != VB_OK) return st;
     cudaMemcpyAsync(w.cursor, nptr, 4 * (nn + 1), cudaMemcpyDeviceToDevice, s);
-    if (ne > 0) bucket_fill_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor, nelem);
+    if (ne > 0) bucket_fill_k<SH><<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor, nelem);
     if (nn > 0) sort_incidences_k<<<grid_for(nn, SORT_BLOCK, 8), SORT_BLOCK, 0, s>>>(nn, nptr, nelem);
-    if ((st = launch_check("fem_p1_pattern(incidences)")) != VB_OK) return st;
+    if ((st = launch_check(fn)) != VB_OK) return st;
 
-    unsigned gr = grid_for(nn, PAT_BLOCK, 4);
+    unsigned gr = grid_for(nn, BLOCK, 4);
     if (!col_idx) {
         // 2. count
-        if (nn > 0) row_count_k<<<gr, PAT_BLOCK, 0, s>>>(nn, nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
-        row_count_big_k<<<64, 32, 0, s>>>(nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        if (nn > 0) row_count_k<SH, CAP, BLOCK><<<gr, BLOCK, 0, s>>>(nn, nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        row_count_big_k<SH><<<64, 32, 0, s>>>(nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
         if ((st = exclusive_scan_i32(w.row_len, row_ptr, nn, w.scan_tmp, s, w.total)) != VB_OK) return st;
         int64_t host[2] = {0, 0};
         int hflags[4] = {0, 0, 0, 0};
         cudaMemcpyAsync(host, w.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
         cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
         cudaError_t e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
-        if (hflags[FLAG_TOO_LONG]) { set_error("fem_p1_pattern: a row has more than %d distinct columns", ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
-        if (host[0] >= (1ll << 31)) { set_error("fem_p1_pattern: nnz=%lld does not fit int32", (long long)host[0]); return VB_ERR_OVERFLOW; }
+        if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+        if (hflags[FLAG_TOO_LONG]) { set_error("%s: a row has more than %d distinct columns", fn, ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
+        if (host[0] >= (1ll << 31)) { set_error("%s: nnz=%lld does not fit int32", fn, (long long)host[0]); return VB_ERR_OVERFLOW; }
         if (nnz_out) *nnz_out = host[0];
         return VB_OK;
     }
@@ -315,22 +315,47 @@ extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32
     int32_t nnz32 = 0;
     cudaMemcpyAsync(&nnz32, row_ptr + nn, 4, cudaMemcpyDeviceToHost, s);
     cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
-    if (nnz32 < 0 || nnz32 > col_cap) { set_error("fem_p1_pattern: col_cap=%lld < nnz=%d", (long long)col_cap, nnz32); return VB_ERR_ARG; }
+    if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    if (nnz32 < 0 || nnz32 > col_cap) { set_error("%s: col_cap=%lld < nnz=%d", fn, (long long)col_cap, nnz32); return VB_ERR_ARG; }
     if (nn > 0) {
-        // rows longer than ROW_CAP are collected by row_fill_k and filled by the fallback
-        row_fill_k<<<gr, PAT_BLOCK, 0, s>>>(nn, ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
-                                            node_elem_slot, w.ovf, w.flags);
-        row_fill_big_k<<<64, 32, 0, s>>>(ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
-                                          node_elem_slot, w.ovf, w.flags);
+        // rows longer than CAP are collected by row_fill_k and filled by the fallback
+        row_fill_k<SH, CAP, BLOCK><<<gr, BLOCK, 0, s>>>(nn, ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx,
+                                                        elem2nnz, node_elem_slot, w.ovf, w.flags);
+        row_fill_big_k<SH><<<64, 32, 0, s>>>(ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
+                                              node_elem_slot, w.ovf, w.flags);
     }
-    if ((st = launch_check("fem_p1_pattern(fill)")) != VB_OK) return st;
+    if ((st = launch_check(fn)) != VB_OK) return st;
     int hflags[4] = {0, 0, 0, 0};
     cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) { set_error("fem_p1_pattern: %s", cudaGetErrorString(e)); return VB_ERR_CUDA; }
-    if (hflags[FLAG_TOO_LONG]) { set_error("fem_p1_pattern: a row has more than %d distinct columns", ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
-    if (hflags[FLAG_SLOT_RANGE]) { set_error("fem_p1_pattern: a row has more than 255 entries; gather plan unsupported, use elem2nnz"); return VB_ERR_UNSUPPORTED; }
+    if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    if (hflags[FLAG_TOO_LONG]) { set_error("%s: a row has more than %d distinct columns", fn, ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
+    if (hflags[FLAG_SLOT_RANGE]) { set_error("%s: a row has more than 255 entries; gather plan unsupported, use elem2nnz", fn); return VB_ERR_UNSUPPORTED; }
     if (nnz_out) *nnz_out = nnz32;
     return VB_OK;
+}
+
+}  // namespace
+}  // namespace vb
+
+using namespace vb;
+
+extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld, void* work,
+                                    size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                                    int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem,
+                                    uint32_t* node_elem_slot, int64_t* nnz_out, vb_stream_t stream) {
+    clear_error();
+    if (dim != 2 && dim != 3) { set_error("fem_p1_pattern: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
+    return pattern_impl<2, 64, 128>("fem_p1_pattern", dim + 1, nn, ne, elems, elem_ld, work, work_bytes, row_ptr,
+                                    col_idx, col_cap, elem2nnz, node_elem_ptr, node_elem, node_elem_slot, nnz_out,
+                                    stream);
+}
+
+extern "C" vb_status fem_pattern(int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld, void* work,
+                                 size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                                 int32_t* elem2nnz, int64_t* nnz_out, vb_stream_t stream) {
+    clear_error();
+    if (nv < 2 || nv > 16) { set_error("fem_pattern: nv=%d, need 2..16 nodes per element", nv); return VB_ERR_UNSUPPORTED; }
+    return pattern_impl<4, 128, 64>("fem_pattern", nv, nn, ne, elems, elem_ld, work, work_bytes, row_ptr, col_idx,
+                                    col_cap, elem2nnz, nullptr, nullptr, nullptr, nnz_out, stream);
 }

@@ -27,7 +27,8 @@ _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORT
 
 EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
-           "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear")
+           "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
+           "fem_pattern", "fem_p2_assemble")
 
 
 class VbError(RuntimeError):
@@ -66,6 +67,9 @@ def lib():
             "vb_quad_rule": (i32, [i32, i32, p, p]),
             "fem_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p, p, p, i32, p]),
             "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
+            "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, C.POINTER(C.c_int64), p]),
+            "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, i64, i32, d, p, d, p, p, p, p, p,
+                                      p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -340,3 +344,53 @@ def vb_page_bilinear(A, Mx, B, s=None, stream=None):
     _check(lib().vb_page_bilinear(N, n, m, _ptr(A), _ld(A, N), _ptr(Mx), _ld(Mx, N), _ptr(B), _ld(B, N), _ptr(s),
                                   _stream(stream)))
     return s
+
+
+# ------------------------------------------------------------------ NEXT-3 (P2)
+class Plan:
+    """Generic CSR pattern + scatter map (fem_pattern) for elements with any node count."""
+
+    def __init__(self, elems, nn, scatter_map=True, stream=None):
+        if elems.dtype != torch.int32:
+            raise TypeError("elems must be int32")
+        nv, ne = elems.shape
+        self.nv, self.nn, self.ne = nv, int(nn), int(ne)
+        dev = elems.device
+        L = lib()
+        sz = C.c_size_t(0)
+        nnz = C.c_int64(0)
+        st = _stream(stream)
+        _check(L.fem_pattern(nv, nn, ne, None, ne, None, C.byref(sz), None, None, 0, None, None, st))
+        work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
+        self.row_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
+        _check(L.fem_pattern(nv, nn, ne, _ptr(elems), ne, _ptr(work), C.byref(sz), _ptr(self.row_ptr), None, 0, None,
+                             C.byref(nnz), st))
+        self.nnz = int(nnz.value)
+        col = torch.zeros((max(4, (self.nnz + 3) // 4 * 4),), dtype=torch.int32, device=dev)
+        self.elem2nnz = torch.empty((nv * nv, ne), dtype=torch.int32, device=dev) if scatter_map else None
+        _check(L.fem_pattern(nv, nn, ne, _ptr(elems), ne, _ptr(work), C.byref(sz), _ptr(self.row_ptr), _ptr(col),
+                             col.numel(), _ptr(self.elem2nnz), C.byref(nnz), st))
+        self.col_idx = col[:self.nnz]
+
+
+def fem_pattern(elems, nn, scatter_map=True, stream=None):
+    return Plan(elems, nn, scatter_map, stream)
+
+
+def fem_p2_assemble(coords, elems, plan, gqo=4, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0)),
+                    want_K=True, want_M=True, want_local=False, K=None, M=None, stream=None):
+    """P2 stiffness / mass (NEXT-3).  Returns (K_vals, M_vals, K_local, M_local)."""
+    _f64(coords)
+    dim, nn = coords.shape
+    nlb, ne = elems.shape
+    dev = coords.device
+    K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
+    M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
+    Kl = torch.empty((nlb, nlb, ne), dtype=torch.float64, device=dev) if want_local else None
+    Ml = torch.empty((nlb, nlb, ne), dtype=torch.float64, device=dev) if want_local else None
+    kb = (C.c_double * 3)(*(list(map(float, cK[1]))[:3] + [0.0] * (3 - len(list(cK[1])[:3]))))
+    mb = (C.c_double * 3)(*(list(map(float, cM[1]))[:3] + [0.0] * (3 - len(list(cM[1])[:3]))))
+    _check(lib().fem_p2_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.elem2nnz), plan.nnz,
+                                 int(gqo), float(cK[0]), C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p),
+                                 _ptr(K), _ptr(M), _ptr(Kl), _ptr(Ml), _stream(stream)))
+    return K, M, Kl, Ml
