@@ -81,8 +81,10 @@ def within_last_digit(x, printed, units=1.0):
     return abs(x - printed) <= units * 10 ** (e - 2) * 1.0001
 
 
-@pytest.mark.parametrize("dim,level", [(2, 6), (2, 7), (3, 4), (3, 6)])
+@pytest.mark.parametrize("dim,level", [(2, 6), (3, 4), (3, 5), (3, 6)])
 def test_paper_p2_tables_on_gpu(dev, golden, dim, level):
+    # (2D level 7, e_K = 3.67e-9 against I_K = 14.56, sits at the round-off floor of
+    # the quadratic form: the 1e-12 entrywise agreement does not fix its third digit)
     g1, g2 = golden("paper_tables_p1.json"), golden("paper_tables_p2.json")
     row = [r for r in g2["p2_%dd" % dim] if r["level"] == level][0]
     if dim == 2:
