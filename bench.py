@@ -364,6 +364,18 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
             alg_bytes_assembly(3, cp_.shape[1], ep_.shape[1], pp.nnz),
             time_kernel(lambda: vb.fem_p1_assemble_coef(cdp, edp, pp, gqo=2, mode=mode, K=Kp, M=Mp), 10))
     del pp, Kp, Mp, cdp, edp
+    # NEXT-3: P2, Table tab:KM_P2_3D level 6 (64^3 cells, 2,146,689 P2 nodes, c = e^{x+y+z}, gqo = 4);
+    # paper: K 87.6 s + M 16.4 s, hardware not stated
+    c2_, e2_ = synth.p2_from_p1(*synth.cube_kuhn_p1(64, jitter=0.0, flip=(0, 0, 1)))
+    cd2, ed2 = torch.from_numpy(c2_).to(dev), torch.from_numpy(e2_).to(dev)
+    p2p = vb.Plan(ed2, c2_.shape[1])
+    K2 = torch.empty(p2p.nnz, dtype=torch.float64, device=dev)
+    M2 = torch.empty(p2p.nnz, dtype=torch.float64, device=dev)
+    rec("NEXT-3 paper tab:KM_P2_3D level 6, P2, c=exp(x+y+z), gqo=4, atomic (paper: K 87.6 s + M 16.4 s, MATLAB, "
+        "hardware not stated)", e2_.shape[1], "elements",
+        c2_.shape[1] * 24 + e2_.size * 4 + e2_.shape[1] * 100 * 4 + 2 * p2p.nnz * 8 * 3,
+        time_kernel(lambda: vb.fem_p2_assemble(cd2, ed2, p2p, gqo=4, K=K2, M=M2), 5))
+    del p2p, K2, M2, cd2, ed2
     # config 4: 2D at scale
     c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
     cd4, ed4 = torch.from_numpy(c4).to(dev), torch.from_numpy(e4).to(dev)
