@@ -220,19 +220,57 @@ __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const doubl
 // so every shared access of the inner loop is bank-conflict free; results are
 // transposed to CSR order through shared memory and stored coalesced.
 constexpr int GATHER_ROWS = 32;
+// Shared-memory budget of one warp-CTA.  Per row of its block (averages over the
+// block's 32 rows): CAP CSR entries, SLOT plan words.  Each row keeps its first
+// RS columns in conflict-free [slot][lane] arrays; columns past RS go to an
+// overflow area of OVF entries per block (CSR-like, rows in lane order).  A row
+// that does not fit is computed by its lane in place in HBM.  The defaults keep
+// 7 CTAs per SM in 3D (Kuhn rows: <= 15 columns, <= 24 incidences; Delaunay
+// rows: mean ~16, ~26 incidences, ~40 % above 16 columns, <= ~60 overflow
+// entries per block) and 16 in 2D.
+#ifndef VB_GATHER_RS3
+#define VB_GATHER_RS3 16
+#endif
+#ifndef VB_GATHER_CAP3
+#define VB_GATHER_CAP3 17
+#endif
+#ifndef VB_GATHER_SLOT3
+#define VB_GATHER_SLOT3 28
+#endif
+#ifndef VB_GATHER_OVF3
+#define VB_GATHER_OVF3 56
+#endif
+#ifndef VB_GATHER_RS2
+#define VB_GATHER_RS2 8
+#endif
+#ifndef VB_GATHER_CAP2
+#define VB_GATHER_CAP2 8
+#endif
+#ifndef VB_GATHER_SLOT2
+#define VB_GATHER_SLOT2 8
+#endif
+#ifndef VB_GATHER_OVF2
+#define VB_GATHER_OVF2 32
+#endif
 template <int DIM>
 struct GatherCfg {
-    static constexpr int RS = DIM == 2 ? 8 : 16;                        // max columns per row (fast path)
-    static constexpr int CAP = GATHER_ROWS * RS;                         // CSR entries per block
-    static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? 8 : 28);   // plan words per block
+    static constexpr int RS = DIM == 2 ? VB_GATHER_RS2 : VB_GATHER_RS3;  // columns per row in the lane arrays
+    static constexpr int OVF = DIM == 2 ? VB_GATHER_OVF2 : VB_GATHER_OVF3;  // overflow columns per block
+    static constexpr int LANE_CAP = GATHER_ROWS * RS;
+    static constexpr int ACC_N = LANE_CAP + OVF;                         // accumulator / edge-vector slots
+    static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_CAP2 : VB_GATHER_CAP3);  // CSR entries of a block
+    static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_SLOT2 : VB_GATHER_SLOT3);  // plan words
     static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
-    static constexpr int RING = 2;
-    static constexpr size_t RING_BYTES = (size_t)(COLS_PAD + SLOTS_PAD) * 4;
-    static constexpr size_t F_OFF = RING * RING_BYTES;                   // [RS*DIM][32] edge vectors / CSR staging
-    static constexpr size_t ACC_OFF = F_OFF + (size_t)DIM * CAP * 8;     // [RS][32] K, then [RS][32] M
-    static constexpr size_t BAR_OFF = ACC_OFF + (size_t)2 * CAP * 8;
+    static constexpr int RING = 2;                                       // plan words: double-buffered
+    static constexpr size_t COLS_BYTES = (size_t)COLS_PAD * 4;           // columns: one buffer (consumed early)
+    static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * 4;
+    static constexpr size_t SLOTS_OFF = COLS_BYTES;
+    static constexpr size_t F_OFF = SLOTS_OFF + RING * SLOTS_BYTES;      // edge vectors / CSR staging
+    static constexpr size_t ACC_OFF = F_OFF + (size_t)DIM * ACC_N * 8;   // (K, M) pairs
+    static constexpr size_t BAR_OFF = ACC_OFF + (size_t)2 * ACC_N * 8;
     static constexpr size_t SMEM = BAR_OFF + RING * 8;
-    static_assert(RING_BYTES % 16 == 0, "TMA destinations must stay 16-byte aligned");
+    static_assert(2 * CAP <= DIM * ACC_N, "K and M staging fit in the edge-vector buffer");
+    static_assert(COLS_BYTES % 16 == 0 && SLOTS_BYTES % 16 == 0, "TMA destinations must stay 16-byte aligned");
     static_assert(DIM >= 2, "staging of K and M in CSR order reuses the edge-vector buffer");
 };
 
@@ -385,46 +423,51 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, const doubl
     return o;
 }
 
-// acc[s*ST] += contributions of one incidence (its d slots are distinct
-// vertices: load all, then store all)
-template <int DIM, int ST, bool WK, bool WM, bool COEF>
+// Accumulators of slot s at acc[ix(s)]: K at accK[ix(s)], M at accM[ix(s)], or
+// (PACKED) the (K, M) pair at accK + ix(s), one 16-byte access for both.  An
+// incidence's d slots are distinct vertices: load all, then store all.
+template <int DIM, bool PACKED, bool WK, bool WM, bool COEF, typename IX>
 __device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restrict__ accK, double* __restrict__ accM,
-                                           double& mrow) {
-    if constexpr (WK && WM && ST == 2 * GATHER_ROWS) {   // packed (K, M) pairs: accM == accK + 1
+                                           IX ix, double& mrow) {
+    int x[DIM];
+#pragma unroll
+    for (int j = 0; j < DIM; j++) x[j] = ix(o.s[j]);
+    if constexpr (PACKED) {
+        static_assert(WK && WM, "packed pairs carry both matrices");
         double2 a[DIM];
 #pragma unroll
-        for (int j = 0; j < DIM; j++) a[j] = *reinterpret_cast<const double2*>(accK + o.s[j] * ST);
+        for (int j = 0; j < DIM; j++) a[j] = *reinterpret_cast<const double2*>(accK + x[j]);
 #pragma unroll
         for (int j = 0; j < DIM; j++)
-            *reinterpret_cast<double2*>(accK + o.s[j] * ST) = make_double2(a[j].x + o.k[j], a[j].y + (COEF ? o.m[j] : o.ad));
+            *reinterpret_cast<double2*>(accK + x[j]) = make_double2(a[j].x + o.k[j], a[j].y + (COEF ? o.m[j] : o.ad));
         if constexpr (COEF) mrow += o.mrow;
         return;
     }
     if constexpr (WK) {
         double a[DIM];
 #pragma unroll
-        for (int j = 0; j < DIM; j++) a[j] = accK[o.s[j] * ST];
+        for (int j = 0; j < DIM; j++) a[j] = accK[x[j]];
 #pragma unroll
-        for (int j = 0; j < DIM; j++) accK[o.s[j] * ST] = a[j] + o.k[j];
+        for (int j = 0; j < DIM; j++) accK[x[j]] = a[j] + o.k[j];
     }
     if constexpr (WM) {
         double a[DIM];
 #pragma unroll
-        for (int j = 0; j < DIM; j++) a[j] = accM[o.s[j] * ST];
+        for (int j = 0; j < DIM; j++) a[j] = accM[x[j]];
 #pragma unroll
-        for (int j = 0; j < DIM; j++) accM[o.s[j] * ST] = a[j] + (COEF ? o.m[j] : o.ad);
+        for (int j = 0; j < DIM; j++) accM[x[j]] = a[j] + (COEF ? o.m[j] : o.ad);
         if constexpr (COEF) mrow += o.mrow;
     }
 }
 
 // Off-diagonal contributions of incidences [i0, i1) of one row: K into accK,
-// M into accM (c = 1: |det|, scaled by 1/(d!(d+1)(d+2)) in finish_row); slot s
-// of the row lives at acc[s * ST].  EV(s, f) yields the edge vector from the
-// row's vertex to its column s.  Incidences are evaluated U at a time (all
-// loads and arithmetic before any accumulator store) and accumulated in
+// M into accM (c = 1: |det|, scaled by 1/(d!(d+1)(d+2)) when the row is
+// finished); slot s of the row at acc[ix(s)].  EV(s, f) yields the edge vector
+// from the row's vertex to its column s.  Incidences are evaluated U at a time
+// (all loads and arithmetic before any accumulator store) and accumulated in
 // ascending element order.  Returns the row sum of M (COEF only).
-template <int DIM, int ST, bool WK, bool WM, bool COEF, typename EV>
-__device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
+template <int DIM, bool PACKED, bool WK, bool WM, bool COEF, typename EV, typename IX>
+__device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, IX ix,
                                                double* __restrict__ accK, double* __restrict__ accM,
                                                const double (&xv)[DIM], const CoefSpec& cp) {
 #ifndef VB_GATHER_U
@@ -440,19 +483,21 @@ __device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* _
 #pragma unroll
         for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF>(slots[i + u], ev, xv, cp);
 #pragma unroll
-        for (int u = 0; u < U; u++) accumulate<DIM, ST, WK, WM, COEF>(o[u], accK, accM, mrow);
+        for (int u = 0; u < U; u++) accumulate<DIM, PACKED, WK, WM, COEF>(o[u], accK, accM, ix, mrow);
     }
-    for (; i < i1; i++) accumulate<DIM, ST, WK, WM, COEF>(incidence<DIM, COEF>(slots[i], ev, xv, cp), accK, accM, mrow);
+    for (; i < i1; i++)
+        accumulate<DIM, PACKED, WK, WM, COEF>(incidence<DIM, COEF>(slots[i], ev, xv, cp), accK, accM, ix, mrow);
     return mrow;
 }
 
-template <int DIM, int ST, bool COEF, typename EV>
-__device__ __forceinline__ double gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev,
+// PAIRS: accM == accK + 1 (interleaved pairs), packed access when both are wanted
+template <int DIM, bool PAIRS, bool COEF, typename EV, typename IX>
+__device__ __forceinline__ double gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, IX ix,
                                              double* __restrict__ accK, double* __restrict__ accM,
                                              const double (&xv)[DIM], const CoefSpec& cp) {
-    if (accK && accM) return gather_row_t<DIM, ST, true, true, COEF>(i0, i1, slots, ev, accK, accM, xv, cp);
-    if (accK) return gather_row_t<DIM, ST, true, false, COEF>(i0, i1, slots, ev, accK, accM, xv, cp);
-    if (accM) return gather_row_t<DIM, ST, false, true, COEF>(i0, i1, slots, ev, accK, accM, xv, cp);
+    if (accK && accM) return gather_row_t<DIM, PAIRS, true, true, COEF>(i0, i1, slots, ev, ix, accK, accM, xv, cp);
+    if (accK) return gather_row_t<DIM, false, true, false, COEF>(i0, i1, slots, ev, ix, accK, accM, xv, cp);
+    if (accM) return gather_row_t<DIM, false, false, true, COEF>(i0, i1, slots, ev, ix, accK, accM, xv, cp);
     return 0.0;
 }
 
@@ -503,33 +548,51 @@ __device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, 
 struct RowInfo {
     int64_t v;
     int lo, L, i0, i1, s0;
-    bool own;
+    int ov;      // first overflow entry of the row (columns RS..L-1)
+    bool own;    // the lane has a row
+    bool fast;   // the row is computed in shared memory
+    bool ovb;    // some row of the block uses the overflow area (warp-uniform)
 };
 
 template <int DIM>
 struct GatherSmem {
     char* base;
-    __device__ int32_t* cols(int r) { return reinterpret_cast<int32_t*>(base + r * GatherCfg<DIM>::RING_BYTES); }
+    __device__ int32_t* cols() { return reinterpret_cast<int32_t*>(base); }
     __device__ uint32_t* slots(int r) {
-        return reinterpret_cast<uint32_t*>(base + r * GatherCfg<DIM>::RING_BYTES + GatherCfg<DIM>::COLS_PAD * 4);
+        return reinterpret_cast<uint32_t*>(base + GatherCfg<DIM>::SLOTS_OFF + r * GatherCfg<DIM>::SLOTS_BYTES);
     }
     __device__ double* F() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::F_OFF); }
-    __device__ double* accK() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::ACC_OFF); }
-    __device__ double* accM() { return accK() + GatherCfg<DIM>::CAP; }
+    __device__ double* acc() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::ACC_OFF); }
     __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + GatherCfg<DIM>::BAR_OFF) + r; }
 };
 
-// Edge-vector / column-coordinate buffer F: coordinate c of slot s of lane t at
-// [slot][coord][lane] -- every access of the inner loop is bank-conflict free.
-// (Interleaving (x, y) pairs for 128-bit loads measured slower: 0.549 vs 0.530 ms.)
-template <int DIM>
-__device__ __forceinline__ int fidx(int s, int c, int t) {
-    return (s * DIM + c) * GATHER_ROWS + t;
-}
+// Where slot s of lane t lives.  Edge-vector / column-coordinate buffer F:
+// coordinate c of slot s < RS at [slot][coord][lane] -- every access of the
+// inner loop is bank-conflict free; slot s >= RS at overflow entry ov + s - RS.
+// Accumulators: (K, M) pair of slot s < RS at [slot][lane], else overflow.
+// Blocks without overflow rows (all of Kuhn's) use the map without the select
+// (OV = false): the select on every access cost 20 % on config 5.
+// (Interleaving (x, y) pairs for 128-bit F loads measured slower: 0.549 vs 0.530 ms.)
+template <int DIM, bool OV>
+struct LaneMap {
+    int t, ov;
+    __device__ __forceinline__ int f(int s, int c) const {
+        using C = GatherCfg<DIM>;
+        if constexpr (!OV) return (s * DIM + c) * GATHER_ROWS + t;
+        return s < C::RS ? (s * DIM + c) * GATHER_ROWS + t : DIM * C::LANE_CAP + (ov + s - C::RS) * DIM + c;
+    }
+    __device__ __forceinline__ int a(int s) const {   // in doubles: K at a(s), M at a(s) + 1
+        using C = GatherCfg<DIM>;
+        if constexpr (!OV) return 2 * (s * GATHER_ROWS + t);
+        return 2 * (s < C::RS ? s * GATHER_ROWS + t : C::LANE_CAP + ov + s - C::RS);
+    }
+};
 
 // word offset of element x within its 16-byte aligned TMA chunk
 __device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
 
+// lane 0 only: stream block B's columns (single buffer: the previous block's were
+// consumed by its coordinate gather) and plan words (ring slot r)
 template <int DIM>
 __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const BlockBounds& B,
                                           const int32_t* __restrict__ col_idx, const uint32_t* __restrict__ nslot) {
@@ -541,18 +604,23 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
     uint32_t c0 = (uint32_t)B.p0 & ~3u, c1 = ((uint32_t)B.p1 + 3u) & ~3u;
     uint32_t s0 = (uint32_t)B.q0 & ~3u, s1 = ((uint32_t)B.q1 + 3u) & ~3u;
     uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * 4;
+    // generic-proxy reads of the column buffer (previous block) before the async-proxy overwrite
+#ifndef VB_GATHER_NOFENCE
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
     mbar_expect_tx(S.bar(r), bc + bs);
-    if (bc) tma_load_1d(S.cols(r), col_idx + c0, bc, S.bar(r));
+    if (bc) tma_load_1d(S.cols(), col_idx + c0, bc, S.bar(r));
     if (bs) tma_load_1d(S.slots(r), nslot + s0, bs, S.bar(r));
 }
 
-// Load the lane's row of block B; if the whole block fits the fast path, find the
-// diagonal slot and gather the row's column coordinates into F[slot][c][lane].
+// Load the lane's row of block B.  If the block is staged (its CSR and plan
+// ranges fit), place the row (lane arrays + overflow), find its diagonal slot and
+// gather its column coordinates into F.  Returns whether the block is staged.
 template <int DIM>
-__device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBounds& B, RowInfo& R,
+__device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, BlockBounds& B, RowInfo& R,
                                               const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
-                                              const int32_t* __restrict__ col_idx,
                                               const double* __restrict__ coords, int64_t ns, int64_t cst) {
+    using C = GatherCfg<DIM>;
     const int t = threadIdx.x;
     R.v = B.r0 + t;
     R.own = B.valid && R.v < B.r1;
@@ -563,19 +631,39 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, int r, BlockBo
         R.i0 = __ldg(nptr + R.v);
         R.i1 = __ldg(nptr + R.v + 1);
     }
-    const bool fast = __all_sync(0xffffffffu, R.L <= GatherCfg<DIM>::RS) && B.valid && B.fit;
-    if (fast && R.own) {
-        (void)col_idx;
-        const int32_t* cols = S.cols(r) + tma_shift(B.p0) + (R.lo - B.p0);
-        double* F = S.F();
-        for (int s = 0; s < R.L; s++) {
-            int64_t w = cols[s];
-            if (w == R.v) R.s0 = s;
+    const bool staged = B.valid && B.fit;
+    // overflow placement: exclusive warp scan of the columns past RS
+    const int ex = staged && R.own && R.L > C::RS ? R.L - C::RS : 0;
+    int inc = ex;
+    if (__any_sync(0xffffffffu, ex > 0)) {
 #pragma unroll
-            for (int c = 0; c < DIM; c++) cp_async8(F + fidx<DIM>(s, c, t), coords + c * cst + w * ns);
+        for (int d = 1; d < GATHER_ROWS; d <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, d);
+            if (t >= d) inc += y;
         }
     }
-    return fast;
+    R.ov = inc - ex;
+    R.fast = staged && R.own && R.L > 0 && (ex == 0 || inc <= C::OVF);
+    R.ovb = __any_sync(0xffffffffu, R.fast && ex > 0);
+#ifdef VB_GATHER_NOOVF
+    if (ex > 0) R.fast = false;
+    R.ovb = false;
+#endif
+    if (R.fast) {
+        const int32_t* cols = S.cols() + tma_shift(B.p0) + (R.lo - B.p0);
+        double* F = S.F();
+        auto gather = [&](auto lm) {
+            for (int s = 0; s < R.L; s++) {
+                int64_t w = cols[s];
+                if (w == R.v) R.s0 = s;
+#pragma unroll
+                for (int c = 0; c < DIM; c++) cp_async8(F + lm.f(s, c), coords + c * cst + w * ns);
+            }
+        };
+        if (R.ovb) gather(LaneMap<DIM, true>{t, R.ov});
+        else gather(LaneMap<DIM, false>{t, R.ov});
+    }
+    return staged;
 }
 
 template <int DIM, bool COEF>
@@ -589,6 +677,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                                                                  const CoefSpec cp) {
     using Cfg = GatherCfg<DIM>;
     constexpr int W = GATHER_ROWS;
+    constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);  // 1/(d! (d+1)(d+2))
     extern __shared__ __align__(16) char smem_raw[];
     GatherSmem<DIM> S{smem_raw};
     const int t = threadIdx.x;
@@ -604,79 +693,76 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     BlockBounds B1 = block_bounds<DIM>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
     if (t == 0) issue_tma<DIM>(S, 0, B0, col_idx, nslot);
     if (B0.valid) mbar_wait(S.bar(0), 0);
-    RowInfo R0;
-    bool fast0 = prepare_block<DIM>(S, 0, B0, R0, row_ptr, nptr, col_idx, coords, ns, cst);
+    RowInfo R;
+    bool staged = prepare_block<DIM>(S, B0, R, row_ptr, nptr, coords, ns, cst);
     cp_async_commit();
 
     double* F = S.F();
-#ifndef VB_GATHER_PACKED
-#define VB_GATHER_PACKED 1
-#endif
-    // accumulators: [slot][lane] planes of K then M, or (packed) interleaved (K, M)
-    // pairs so one 16-byte access serves both matrices
-    constexpr int STF = VB_GATHER_PACKED ? 2 * W : W;
-    double* aKs = VB_GATHER_PACKED ? S.accK() + 2 * t : S.accK() + t;
-    double* aMs = VB_GATHER_PACKED ? aKs + 1 : S.accM() + t;
+    double* acc = S.acc();
     for (int64_t k = 0;; k++) {
         const int64_t b = blockIdx.x + k * gstep;
         if (b >= nblocks) break;
         const int rc = (int)(k & 1), rn = rc ^ 1;
-        // stage k+1: stream its columns and plan words (ring slot of block k-1 is free)
+        // stage k+1: stream its columns and plan words (every lane is past its column reads)
+        __syncwarp();
         if (t == 0) issue_tma<DIM>(S, rn, B1, col_idx, nslot);
         BlockBounds B2 = block_bounds<DIM>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
         // stage k: its coordinates have landed
         cp_async_wait<0>();
         __syncwarp();
-        const RowInfo& R = R0;
-        if (fast0) {
+        if (staged) {
             const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
-            double* aK = K ? aKs : nullptr;
-            double* aM = M ? aMs : nullptr;
-            double mrow = 0.0;
-            if (R.own) {
-                for (int s = 0; s < R.L; s++) {
-                    aKs[s * STF] = 0.0;
-                    aMs[s * STF] = 0.0;
-                }
-                double xv[DIM];
-#pragma unroll
-                for (int c = 0; c < DIM; c++) xv[c] = F[fidx<DIM>(R.s0, c, t)];
-                auto ev = [&](int s, double(&f)[DIM]) {
-                    VB_CHECK(s < R.L && s != R.s0);
-#pragma unroll
-                    for (int c = 0; c < DIM; c++) f[c] = F[fidx<DIM>(s, c, t)] - xv[c];
-                };
-                VB_CHECK(R.i0 >= B0.q0 && R.i1 <= B0.q1 && R.lo >= B0.p0 && R.lo + R.L <= B0.p1);
-                mrow = gather_row<DIM, STF, COEF>(R.i0, R.i1, slots, ev, aK, aM, xv, cp);
-            }
-            __syncwarp();
-            // finish the row (diagonal from the partition of unity, M scale) while
-            // transposing it to CSR order through the (now dead) edge-vector buffer
             const int np = B0.p1 - B0.p0;
-            double* stK = F;
-            double* stM = F + Cfg::CAP;
-            if (R.own && R.L > 0) {
-                constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);  // 1/(d! (d+1)(d+2))
-                double sk = 0.0, sm = 0.0;
-                const int b = R.lo - B0.p0;
-                for (int s = 0; s < R.L; s++) {
-                    if (s == R.s0) continue;
-                    double kk = aKs[s * STF], mm = aMs[s * STF] * MS;
-                    sk += kk;
-                    sm += mm;
-                    stK[b + s] = kk;
-                    stM[b + s] = mm;
+            auto run = [&](auto lm) {
+                double mrow = 0.0;
+                if (R.fast) {
+                    for (int s = 0; s < R.L; s++) *reinterpret_cast<double2*>(acc + lm.a(s)) = make_double2(0.0, 0.0);
+                    double xv[DIM];
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) xv[c] = F[lm.f(R.s0, c)];
+                    auto ev = [&](int s, double(&f)[DIM]) {
+                        VB_CHECK(s < R.L && s != R.s0);
+#pragma unroll
+                        for (int c = 0; c < DIM; c++) f[c] = F[lm.f(s, c)] - xv[c];
+                    };
+                    auto ix = [&](int s) { return lm.a(s); };
+                    VB_CHECK(R.i0 >= B0.q0 && R.i1 <= B0.q1 && R.lo >= B0.p0 && R.lo + R.L <= B0.p1);
+                    mrow = gather_row<DIM, true, COEF>(R.i0, R.i1, slots, ev, ix, K ? acc : nullptr,
+                                                       M ? acc + 1 : nullptr, xv, cp);
                 }
-                stK[b + R.s0] = -sk;
-                stM[b + R.s0] = COEF ? mrow - sm : (DIM == 3 ? sm * (2.0 / 3.0) : sm);
-            }
-            __syncwarp();
-            for (int q = t; q < np; q += W) {
-                if (K) stcs(K + B0.p0 + q, stK[q]);
-                if (M) stcs(M + B0.p0 + q, stM[q]);
-            }
-        } else if (R.own && R.L > 0) {
-            // block outside the smem budget: same ownership, everything in place in HBM
+                __syncwarp();
+                // finish the row (diagonal from the partition of unity, M scale) while
+                // transposing it to CSR order through the (now dead) edge-vector buffer
+                double* stK = F;
+                double* stM = F + Cfg::CAP;
+                if (R.fast) {
+                    double sk = 0.0, sm = 0.0;
+                    const int b = R.lo - B0.p0;
+                    for (int s = 0; s < R.L; s++) {
+                        if (s == R.s0) continue;
+                        const double2 km = *reinterpret_cast<const double2*>(acc + lm.a(s));
+                        const double mm = km.y * MS;
+                        sk += km.x;
+                        sm += mm;
+                        stK[b + s] = km.x;
+                        stM[b + s] = mm;
+                    }
+                    stK[b + R.s0] = -sk;
+                    stM[b + R.s0] = COEF ? mrow - sm : (DIM == 3 ? sm * (2.0 / 3.0) : sm);
+                }
+                __syncwarp();
+                for (int q = t; q < np; q += W) {
+                    if (K) stcs(K + B0.p0 + q, stK[q]);
+                    if (M) stcs(M + B0.p0 + q, stM[q]);
+                }
+            };
+            if (R.ovb) run(LaneMap<DIM, true>{t, R.ov});
+            else run(LaneMap<DIM, false>{t, R.ov});
+        }
+        __syncwarp();   // orders the staged stores above before the in-place rows below
+        if (R.own && R.L > 0 && !R.fast) {
+            // rows that did not fit, or blocks outside the smem budget: same ownership,
+            // everything in place in HBM (overwrites what the staged store left there)
             double* aK = K ? K + R.lo : nullptr;
             double* aM = M ? M + R.lo : nullptr;
             int s0 = 0;
@@ -694,13 +780,14 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #pragma unroll
                 for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
             };
-            double mrow = gather_row<DIM, 1, COEF>(R.i0, R.i1, nslot, ev, aK, aM, xv, cp);
+            auto ix = [](int s) { return s; };
+            double mrow = gather_row<DIM, false, COEF>(R.i0, R.i1, nslot, ev, ix, aK, aM, xv, cp);
             finish_row<DIM, 1, COEF>(R.L, s0, aK, aM, mrow);
         }
         __syncwarp();
         // stage k+1: its columns have landed -> gather its coordinates into F (free now)
         if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) >> 1) & 1));
-        fast0 = prepare_block<DIM>(S, rn, B1, R0, row_ptr, nptr, col_idx, coords, ns, cst);
+        staged = prepare_block<DIM>(S, B1, R, row_ptr, nptr, coords, ns, cst);
         cp_async_commit();
         B0 = B1;
         B1 = B2;

@@ -215,3 +215,46 @@ def icosphere(level, perturb=0.01, seed=0):
     xyz = np.ascontiguousarray(verts.T)
     tri = np.ascontiguousarray(faces.T.astype(np.int32))
     return xyz, tri
+
+
+DELAUNAY_STREAM = 3
+PERMUTE_STREAM = 4
+
+
+def delaunay_p1(dim, n, jitter=0.35, seed=0):
+    """Unstructured P1 mesh: the (n+1)^dim grid of the unit square / cube with
+    every node moved by jitter*h*U[-1,1) per coordinate (stream 3, boundary
+    nodes kept on their faces), triangulated by scipy's Delaunay (Qhull).  Row
+    lengths then follow the Delaunay degree distribution (3D: mean ~15.5, many
+    rows above 16) instead of the fixed Kuhn/square stencils."""
+    from scipy.spatial import Delaunay
+
+    n1 = n + 1
+    axes = np.meshgrid(*([np.arange(n1)] * dim), indexing="ij")
+    idx = np.stack([a.ravel(order="F") for a in axes])          # x fastest
+    nn = idx.shape[1]
+    d = uniform_pm1(seed, DELAUNAY_STREAM, nn * dim).reshape(nn, dim).T
+    inner = (idx > 0) & (idx < n)                               # per coordinate
+    coords = (idx + np.where(inner, jitter * d, 0.0)) / n
+    tri = Delaunay(coords.T, qhull_options="Qbb Qc Qz Q12" if dim == 3 else "Qbb Qc Qz")
+    elems = np.ascontiguousarray(tri.simplices.T.astype(np.int32))
+    return np.ascontiguousarray(coords), elems
+
+
+def permute_mesh(coords, elems, seed=0):
+    """Relabel nodes, reorder elements and rotate each element's vertex list by
+    seeded random permutations (stream 4): the same mesh in another numbering,
+    so nothing may rely on the generators' locality or ordering."""
+    nv, ne = elems.shape
+    nn = coords.shape[1]
+    keys = uniform_pm1(seed, PERMUTE_STREAM, nn + ne + ne)
+    new_of_old = np.empty(nn, dtype=np.int64)
+    new_of_old[np.argsort(keys[:nn], kind="stable")] = np.arange(nn)
+    c2 = np.empty_like(coords)
+    c2[:, new_of_old] = coords
+    order = np.argsort(keys[nn:nn + ne], kind="stable")
+    rot = (np.floor((keys[nn + ne:] + 1.0) * 0.5 * nv).astype(np.int64) % nv)[order]
+    e2 = new_of_old[elems[:, order]]
+    rows = (np.arange(nv)[:, None] + rot[None, :]) % nv
+    e2 = np.take_along_axis(e2, rows, axis=0)
+    return np.ascontiguousarray(c2), np.ascontiguousarray(e2.astype(np.int32))

@@ -269,3 +269,29 @@ def test_surface_full_size_config3(dev):
     assert relmax(h(o["area"]), ar) <= 1e-12
     assert abs(h(o["volume"])[0] - vol) <= 1e-12 * abs(vol)
     assert abs(vol - 4.0 * math.pi / 3.0) < 2e-3                     # near the unit ball (radii +-1%)
+
+
+# ---------------------------------------------------------------- unstructured meshes
+@pytest.mark.parametrize("permute", [False, True])
+@pytest.mark.parametrize("dim,n", [(2, 40), (3, 7), (3, 13)])
+def test_delaunay_meshes_parity(dev, dim, n, permute):
+    """Delaunay meshes (3D: ~30% of rows longer than the 16-column per-lane
+    arrays, so staged blocks mix smem rows and in-place rows), optionally in a
+    random node/element/vertex numbering."""
+    coords, elems = synth.delaunay_p1(dim, n, seed=4)
+    if permute:
+        coords, elems = synth.permute_mesh(coords, elems, seed=5)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan = vb.P1Plan(g(elems, dev), nn)
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    assert np.array_equal(h(plan.elem2nnz), expected_elem2nnz(elems, rp, ci))
+    for mode in MODES:
+        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
+        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+    cK, cM = (2.0, (0.4, -0.3, 0.2)), (0.5, (-0.6, 0.1, 0.8))
+    Ko, Mo = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cK, cM=cM)
+    for mode in MODES:
+        K, M = vb.fem_p1_assemble_coef(g(coords, dev), g(elems, dev), plan, gqo=2, cK=cK, cM=cM, mode=mode)[:2]
+        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12

@@ -314,3 +314,32 @@ def test_jittered_meshes_keep_orientation():
             J = X[:, 1:, :] - X[:, :1, :]
             return np.sign(np.linalg.det(J.transpose(2, 0, 1)))
         assert np.array_equal(signs(c0, e0), signs(c1, e1))
+
+
+@pytest.mark.parametrize("dim,n", [(2, 12), (3, 5)])
+def test_delaunay_invariants_and_numbering_independence(dim, n):
+    """Unstructured (Delaunay) meshes: K 1 = 0, sum M = |Omega|, u^T K u =
+    |a|^2 for linear u, and the assembled operator does not depend on node,
+    element or vertex numbering (same entries after relabelling)."""
+    coords, elems = synth.delaunay_p1(dim, n, seed=2)
+    nn = coords.shape[1]
+    rp, ci, K, M = assemble(coords, elems)
+    Kinf = np.max(np.abs(K))
+    assert np.max(np.abs(csr_matvec(rp, ci, K, np.ones(nn)))) <= 1e-13 * Kinf
+    assert abs(math.fsum(M) - 1.0) <= 1e-13
+    a = np.arange(1.0, dim + 1.0)
+    u = a @ coords
+    assert abs(math.fsum(u * csr_matvec(rp, ci, K, u)) - float(a @ a)) <= 1e-12 * float(a @ a)
+    c2, e2 = synth.permute_mesh(coords, elems, seed=3)
+    rp2, ci2, K2, M2 = assemble(c2, e2)
+    # node map old -> new from the coordinates (all distinct)
+    new_of_old = np.lexsort(c2[::-1])[np.argsort(np.lexsort(coords[::-1]))]
+    assert np.array_equal(c2[:, new_of_old], coords)
+    D1 = np.zeros((nn, nn)), np.zeros((nn, nn))
+    rows = np.repeat(np.arange(nn), np.diff(rp))
+    rows2 = np.repeat(np.arange(nn), np.diff(rp2))
+    for D, v in zip(D1, (K, M)):
+        D[new_of_old[rows], new_of_old[ci]] = v
+    assert np.max(np.abs(D1[0][rows2, ci2] - K2)) <= 1e-13 * Kinf
+    assert np.max(np.abs(D1[1][rows2, ci2] - M2)) <= 1e-13 * np.max(M)
+    assert np.count_nonzero(np.diff(rp2)) == nn and len(ci2) == len(ci)
