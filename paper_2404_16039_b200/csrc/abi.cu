@@ -29,6 +29,48 @@ int sm_count() {
     return cached[dev];
 }
 
+// ------------------------------------------------------------------ small read-backs
+namespace {
+__global__ void read_small_k(const unsigned char* __restrict__ src, unsigned char* dst, int bytes) {
+    for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+}
+struct MappedSlot {
+    unsigned char* h = nullptr;
+    unsigned char* d = nullptr;
+    int dev = -1;
+};
+}  // namespace
+
+vb_status read_small(cudaStream_t s, const void* src, size_t bytes, void* dst, const char* fn) {
+    thread_local MappedSlot slot;   // one 64-byte mapped buffer per host thread (per device)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (bytes > 64) { set_error("%s: read_small of %zu bytes", fn, bytes); return VB_ERR_ARG; }
+    if (slot.h && slot.dev != dev) { cudaFreeHost(slot.h); slot.h = slot.d = nullptr; }
+    if (!slot.h) {
+        if (cudaHostAlloc((void**)&slot.h, 64, cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer((void**)&slot.d, slot.h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            if (slot.h) cudaFreeHost(slot.h);
+            slot.h = slot.d = nullptr;
+        } else {
+            slot.dev = dev;
+        }
+    }
+    cudaError_t e;
+    if (slot.h) {
+        read_small_k<<<1, 32, 0, s>>>(static_cast<const unsigned char*>(src), slot.d, (int)bytes);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) memcpy(dst, (const void*)slot.h, bytes);
+    } else {   // no mapped memory: plain copy
+        e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    }
+    if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    return VB_OK;
+}
+
 // ------------------------------------------------------------------ scan
 constexpr int SCAN_THREADS = 256;
 constexpr int SCAN_ITEMS = 16;

@@ -260,7 +260,11 @@ struct GatherCfg {
     static constexpr int ACC_N = LANE_CAP + OVF;                         // accumulator / edge-vector slots
     static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_CAP2 : VB_GATHER_CAP3);  // CSR entries of a block
     static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_SLOT2 : VB_GATHER_SLOT3);  // plan words
+#ifdef VB_GATHER_SLOTS_GLOBAL
+    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = 0;   // plan words read through L1
+#else
     static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
+#endif
     static constexpr int RING = 2;                                       // plan words: double-buffered
     static constexpr size_t COLS_BYTES = (size_t)COLS_PAD * 4;           // columns: one buffer (consumed early)
     static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * 4;
@@ -540,7 +544,10 @@ __device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, 
     B.p1 = __ldg(row_ptr + B.r1);
     B.q0 = __ldg(nptr + B.r0);
     B.q1 = __ldg(nptr + B.r1);
-    B.fit = (B.p1 - B.p0) <= GatherCfg<DIM>::CAP && (B.q1 - B.q0) <= GatherCfg<DIM>::SLOT_CAP;
+    B.fit = (B.p1 - B.p0) <= GatherCfg<DIM>::CAP;
+#ifndef VB_GATHER_SLOTS_GLOBAL
+    B.fit = B.fit && (B.q1 - B.q0) <= GatherCfg<DIM>::SLOT_CAP;
+#endif
     return B;
 }
 
@@ -607,6 +614,11 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
     // generic-proxy reads of the column buffer (previous block) before the async-proxy overwrite
 #ifndef VB_GATHER_NOFENCE
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+#ifdef VB_GATHER_SLOTS_GLOBAL
+    bs = 0;
+    (void)s0;
+    (void)s1;
 #endif
     mbar_expect_tx(S.bar(r), bc + bs);
     if (bc) tma_load_1d(S.cols(), col_idx + c0, bc, S.bar(r));
@@ -711,7 +723,12 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         cp_async_wait<0>();
         __syncwarp();
         if (staged) {
+#ifdef VB_GATHER_SLOTS_GLOBAL
+            const uint32_t* slots = nslot;
+            (void)rc;
+#else
             const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
+#endif
             const int np = B0.p1 - B0.p0;
             auto run = [&](auto lm) {
                 double mrow = 0.0;

@@ -302,10 +302,8 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
         if ((st = exclusive_scan_i32(w.row_len, row_ptr, nn, w.scan_tmp, s, w.total)) != VB_OK) return st;
         int64_t host[2] = {0, 0};
         int hflags[4] = {0, 0, 0, 0};
-        cudaMemcpyAsync(host, w.total, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-        cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
-        cudaError_t e = cudaStreamSynchronize(s);
-        if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+        if ((st = read_small(s, w.total, sizeof(int64_t), host, fn)) != VB_OK) return st;
+        if ((st = read_small(s, w.flags, sizeof(hflags), hflags, fn)) != VB_OK) return st;
         if (hflags[FLAG_TOO_LONG]) { set_error("%s: a row has more than %d distinct columns", fn, ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
         if (host[0] >= (1ll << 31)) { set_error("%s: nnz=%lld does not fit int32", fn, (long long)host[0]); return VB_ERR_OVERFLOW; }
         if (nnz_out) *nnz_out = host[0];
@@ -313,9 +311,7 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
     }
     // 3. fill (row_ptr from the count phase); check the capacity before writing
     int32_t nnz32 = 0;
-    cudaMemcpyAsync(&nnz32, row_ptr + nn, 4, cudaMemcpyDeviceToHost, s);
-    cudaError_t e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    if ((st = read_small(s, row_ptr + nn, 4, &nnz32, fn)) != VB_OK) return st;
     if (nnz32 < 0 || nnz32 > col_cap) { set_error("%s: col_cap=%lld < nnz=%d", fn, (long long)col_cap, nnz32); return VB_ERR_ARG; }
     if (nn > 0) {
         // rows longer than CAP are collected by row_fill_k and filled by the fallback
@@ -326,9 +322,7 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
     }
     if ((st = launch_check(fn)) != VB_OK) return st;
     int hflags[4] = {0, 0, 0, 0};
-    cudaMemcpyAsync(hflags, w.flags, sizeof(hflags), cudaMemcpyDeviceToHost, s);
-    e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    if ((st = read_small(s, w.flags, sizeof(hflags), hflags, fn)) != VB_OK) return st;
     if (hflags[FLAG_TOO_LONG]) { set_error("%s: a row has more than %d distinct columns", fn, ROW_CAP_BIG); return VB_ERR_UNSUPPORTED; }
     if (hflags[FLAG_SLOT_RANGE]) { set_error("%s: a row has more than 255 entries; gather plan unsupported, use elem2nnz", fn); return VB_ERR_UNSUPPORTED; }
     if (nnz_out) *nnz_out = nnz32;

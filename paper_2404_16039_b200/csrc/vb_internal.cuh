@@ -27,6 +27,13 @@ inline vb_status launch_check(const char* what) {
     return VB_OK;
 }
 
+// Read `bytes` (<= 64) of device memory into host memory: enqueued on `s`, then
+// synchronises `s`.  Goes through a small mapped pinned buffer written by a
+// one-thread kernel, so the read-back never waits in a copy-engine queue behind
+// large async copies that other streams have in flight (a pageable
+// cudaMemcpyAsync would).  Returns VB_ERR_CUDA (message set) on failure.
+vb_status read_small(cudaStream_t s, const void* src, size_t bytes, void* dst, const char* fn);
+
 // Grid for a grid-stride kernel over `units` work items of `block` threads:
 // never more than `waves` full waves of resident blocks.
 inline unsigned grid_for(int64_t units, int block, int blocks_per_sm, int waves = 1) {
