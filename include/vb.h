@@ -155,7 +155,12 @@ VB_API vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, 
  * Count phase (col_idx == NULL): writes row_ptr[0..nn], then SYNCHRONISES the
  *   stream and stores nnz in *nnz_out (host int64).
  * Fill phase (col_idx != NULL, col_cap >= nnz, row_ptr from the count phase;
- *   also synchronises the stream, to check col_cap and the row-length flags):
+ *   also synchronises the stream, to check col_cap and the row-length flags).
+ *   Given the count phase's work buffer (same elems pointer, sizes and elem_ld,
+ *   recorded there by the count phase), it reuses the node->element incidence
+ *   lists and the row lists the count phase left in work; with any other work
+ *   buffer it rebuilds them (same results, slower).  elems must therefore not
+ *   change between a count and a fill call that share a work buffer.  Writes:
  *   writes col_idx[0..nnz) and the optional scatter plans:
  *   elem2nnz (nullable): int32, nv*nv planes of ne: plane (a*nv + b) entry e is
  *     the position in col_idx of column elems[b][e] in row elems[a][e]

@@ -98,18 +98,51 @@ __device__ __forceinline__ bool insert_unique(int32_t* L, int st, int& cnt, int 
     return true;
 }
 
-// Build row v's sorted unique column list into L (stride st, capacity cap).
+// Incidences are processed in chunks of CH: all their element ids, then all
+// their vertex ids, are loaded before any list work, so a thread keeps CH (x nv)
+// independent global loads in flight instead of one dependent pair at a time.
+template <int SH>
+struct Chunk {
+    static constexpr int NVM = 1 << SH;       // max vertices per element of this packing
+    static constexpr int CH = SH == 2 ? 8 : 2;
+};
+
+// vertices of the incidences [i0, i0 + CH) of a row (-1 past hi / past nv)
+template <int SH>
+__device__ __forceinline__ void load_chunk(int i0, int hi, int nv, const int32_t* __restrict__ elems, int64_t eld,
+                                           const int32_t* __restrict__ node_elem, int32_t (&ea)[Chunk<SH>::CH],
+                                           int32_t (&w)[Chunk<SH>::CH][Chunk<SH>::NVM]) {
+    constexpr int CH = Chunk<SH>::CH, NVM = Chunk<SH>::NVM;
+#pragma unroll
+    for (int k = 0; k < CH; k++) ea[k] = i0 + k < hi ? __ldg(node_elem + i0 + k) : -1;
+#pragma unroll
+    for (int k = 0; k < CH; k++)
+#pragma unroll
+        for (int b = 0; b < NVM; b++)
+            w[k][b] = (ea[k] >= 0 && b < nv) ? __ldg(elems + b * eld + (ea[k] >> SH)) : -1;
+}
+
+// Build row v's sorted unique column list into L (stride st, capacity cap):
+// v itself, then the other vertices of every incident element.
 // Returns the count, or -1 on overflow.
 template <int SH>
 __device__ int build_row(int64_t v, int nv, const int32_t* __restrict__ elems, int64_t eld,
                          const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
                          int32_t* L, int st, int cap) {
-    int cnt = 0;
+    constexpr int CH = Chunk<SH>::CH, NVM = Chunk<SH>::NVM;
     int lo = nptr[v], hi = nptr[v + 1];
-    for (int i = lo; i < hi; i++) {
-        int64_t e = node_elem[i] >> SH;
-        for (int b = 0; b < nv; b++)
-            if (!insert_unique(L, st, cnt, cap, elems[b * eld + e])) return -1;
+    if (lo == hi) return 0;
+    int cnt = 1;
+    L[0] = (int32_t)v;
+    for (int i0 = lo; i0 < hi; i0 += CH) {
+        int32_t ea[CH], w[CH][NVM];
+        load_chunk<SH>(i0, hi, nv, elems, eld, node_elem, ea, w);
+#pragma unroll
+        for (int k = 0; k < CH; k++)
+#pragma unroll
+            for (int b = 0; b < NVM; b++)
+                if (w[k][b] >= 0 && b != (ea[k] & (NVM - 1)))
+                    if (!insert_unique(L, st, cnt, cap, w[k][b])) return -1;
     }
     return cnt;
 }
@@ -120,36 +153,48 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
                          const int32_t* __restrict__ nptr, const int32_t* __restrict__ node_elem,
                          const int32_t* L, int st, const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
                          int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots, int* flags) {
+    constexpr int CH = Chunk<SH>::CH, NVM = Chunk<SH>::NVM;
     int32_t base = row_ptr[v];
     for (int i = 0; i < cnt; i++) col_idx[base + i] = L[i * st];
     if (!elem2nnz && !slots) return;
     if (slots && cnt > 255) atomicExch(flags + FLAG_SLOT_RANGE, 1);
     int lo = nptr[v], hi = nptr[v + 1];
-    for (int i = lo; i < hi; i++) {
-        int32_t ea = node_elem[i];
-        int64_t e = ea >> SH;
-        int a = ea & ((1 << SH) - 1);
-        // byte 0: in-row offset of the row's own vertex (the diagonal); bytes
-        // 1..nv-1: offsets of the element's other vertices, ascending local index
-        uint32_t packed = 0;
-        int byte = 1;
-        for (int b = 0; b < nv; b++) {
-            int pos = lower_bound_s(L, st, cnt, elems[b * eld + e]);
-            VB_CHECK(pos < cnt && L[pos * st] == elems[b * eld + e]);   // every vertex is in the row
-            if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
-            int sh = (b == a) ? 0 : 8 * byte++;
-            if (sh < 32) packed |= (uint32_t)(pos & 0xff) << sh;
+    for (int i0 = lo; i0 < hi; i0 += CH) {
+        int32_t ea[CH], w[CH][NVM];
+        load_chunk<SH>(i0, hi, nv, elems, eld, node_elem, ea, w);
+#pragma unroll
+        for (int k = 0; k < CH; k++) {
+            if (ea[k] < 0) break;
+            int64_t e = ea[k] >> SH;
+            int a = ea[k] & (NVM - 1);
+            // byte 0: in-row offset of the row's own vertex (the diagonal); bytes
+            // 1..nv-1: offsets of the element's other vertices, ascending local index
+            uint32_t packed = 0;
+            int byte = 1;
+#pragma unroll
+            for (int b = 0; b < NVM; b++) {
+                if (b >= nv) break;
+                int pos = lower_bound_s(L, st, cnt, w[k][b]);
+                VB_CHECK(pos < cnt && L[pos * st] == w[k][b]);   // every vertex is in the row
+                if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
+                int sh = (b == a) ? 0 : 8 * byte++;
+                if (sh < 32) packed |= (uint32_t)(pos & 0xff) << sh;
+            }
+            if (slots) slots[i0 + k] = packed;
         }
-        if (slots) slots[i] = packed;
     }
 }
+
+// Row lists of up to RL entries are kept in the work buffer (stride RL) by the
+// count phase, so the fill phase need not rebuild them.
+constexpr int RL = 32;
 
 template <int SH, int CAP, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) row_count_k(int64_t nn, int nv, const int32_t* __restrict__ elems,
                                                      int64_t eld, const int32_t* __restrict__ nptr,
                                                      const int32_t* __restrict__ node_elem,
                                                      int32_t* __restrict__ row_len, int32_t* __restrict__ ovf_list,
-                                                     int* flags) {
+                                                     int32_t* __restrict__ rowlist, int* flags) {
     __shared__ int32_t Ls[CAP * BLOCK];
     int32_t* L = Ls + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -159,6 +204,9 @@ __global__ void __launch_bounds__(BLOCK) row_count_k(int64_t nn, int nv, const i
             int k = atomicAdd(flags + FLAG_OVERFLOW_ROWS, 1);
             ovf_list[k] = (int32_t)v;
             cnt = 0;  // fixed by the fallback
+        } else if (cnt <= RL) {
+            int32_t* out = rowlist + v * RL;
+            for (int i = 0; i < cnt; i++) out[i] = L[i * BLOCK];
         }
         row_len[v] = cnt;
     }
@@ -182,18 +230,27 @@ __global__ void row_count_big_k(int nv, const int32_t* __restrict__ elems, int64
     }
 }
 
+// rowlist != NULL: rows of <= RL entries take their list from the count phase
+// (row_ptr gives the length); longer rows are rebuilt.
 template <int SH, int CAP, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) row_fill_k(int64_t nn, int64_t ne, int nv, const int32_t* __restrict__ elems,
                                                     int64_t eld, const int32_t* __restrict__ nptr,
                                                     const int32_t* __restrict__ node_elem,
                                                     const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
                                                     int32_t* __restrict__ elem2nnz, uint32_t* __restrict__ slots,
+                                                    const int32_t* __restrict__ rowlist,
                                                     int32_t* __restrict__ ovf_list, int* flags) {
     __shared__ int32_t Ls[CAP * BLOCK];
     int32_t* L = Ls + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
-        int cnt = build_row<SH>(v, nv, elems, eld, nptr, node_elem, L, BLOCK, CAP);
+        int cnt = row_ptr[v + 1] - row_ptr[v];
+        if (rowlist && cnt <= RL) {
+            const int32_t* in = rowlist + v * RL;
+            for (int i = 0; i < cnt; i++) L[i * BLOCK] = in[i];
+        } else {
+            cnt = build_row<SH>(v, nv, elems, eld, nptr, node_elem, L, BLOCK, CAP);
+        }
         if (cnt < 0) {  // long row: the single-thread fallback fills it
             ovf_list[atomicAdd(flags + FLAG_OVERFLOW_ROWS, 1)] = (int32_t)v;
             continue;
@@ -221,12 +278,22 @@ __global__ void row_fill_big_k(int64_t ne, int nv, const int32_t* __restrict__ e
     }
 }
 
+// State the count phase leaves in the work buffer for the fill phase.
+struct Stamp {
+    int64_t magic, nn, ne, nv, elem_ld;
+    const void* elems;
+    int64_t pad[2];
+};
+constexpr int64_t STAMP_MAGIC = 0x5642504154543031ll;   // "VBPATT01"
+
 struct Work {
+    Stamp* stamp;       // 64 bytes
     int32_t* cursor;    // nn+1
     int32_t* nptr;      // nn+1
     int32_t* node_elem; // nv*ne
     int32_t* row_len;   // nn+1
     int32_t* ovf;       // nn
+    int32_t* rowlist;   // nn*RL
     int* flags;         // 4 ints
     int64_t* total;     // 2 int64
     void* scan_tmp;
@@ -240,11 +307,13 @@ Work carve(void* base, int64_t nn, int64_t ne, int nv) {
     char* p = reinterpret_cast<char*>(base);
     size_t off = 0;
     auto take = [&](size_t b) { char* r = p ? p + off : nullptr; off += al(b); return r; };
+    w.stamp = (Stamp*)take(sizeof(Stamp));
     w.cursor = (int32_t*)take(4 * (nn + 1));
     w.nptr = (int32_t*)take(4 * (nn + 1));
     w.node_elem = (int32_t*)take(4 * (size_t)nv * ne + 4);
     w.row_len = (int32_t*)take(4 * (nn + 1));
     w.ovf = (int32_t*)take(4 * (nn + 1));
+    w.rowlist = (int32_t*)take(4 * (size_t)nn * RL + 4);
     w.flags = (int*)take(64);
     w.total = (int64_t*)take(64);
     int64_t smax = nn > nv * ne ? nn : nv * ne;
@@ -252,6 +321,8 @@ Work carve(void* base, int64_t nn, int64_t ne, int nv) {
     w.bytes = off;
     return w;
 }
+
+__global__ void write_stamp_k(Stamp* st, Stamp v) { *st = v; }
 
 template <int SH, int CAP, int BLOCK>
 vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
@@ -279,27 +350,34 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
     }
     w = carve(work, nn, ne, nv);
     cudaStream_t s = cs(stream);
-    int32_t* nptr = node_elem_ptr ? node_elem_ptr : w.nptr;
-    int32_t* nelem = node_elem ? node_elem : w.node_elem;
-
-    // 1. node -> element incidences
-    cudaMemsetAsync(w.cursor, 0, 4 * (nn + 1), s);
-    cudaMemsetAsync(w.flags, 0, 64, s);
-    unsigned ge = grid_for(ne, 256, 8);
-    if (ne > 0) degree_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor);
-    vb_status st = exclusive_scan_i32(w.cursor, nptr, nn, w.scan_tmp, s, nullptr);
-    if (st != VB_OK) return st;
-    cudaMemcpyAsync(w.cursor, nptr, 4 * (nn + 1), cudaMemcpyDeviceToDevice, s);
-    if (ne > 0) bucket_fill_k<SH><<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor, nelem);
-    if (nn > 0) sort_incidences_k<<<grid_for(nn, SORT_BLOCK, 8), SORT_BLOCK, 0, s>>>(nn, nptr, nelem);
-    if ((st = launch_check(fn)) != VB_OK) return st;
-
+    const Stamp mine{STAMP_MAGIC, nn, ne, nv, elem_ld, elems, {0, 0}};
+    vb_status st = VB_OK;
     unsigned gr = grid_for(nn, BLOCK, 4);
+
+    // 1. node -> element incidences (into work; the fill phase reuses them)
+    auto incidences = [&]() -> vb_status {
+        cudaMemsetAsync(w.cursor, 0, 4 * (nn + 1), s);
+        unsigned ge = grid_for(ne, 256, 8);
+        if (ne > 0) degree_k<<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor);
+        vb_status r = exclusive_scan_i32(w.cursor, w.nptr, nn, w.scan_tmp, s, nullptr);
+        if (r != VB_OK) return r;
+        cudaMemcpyAsync(w.cursor, w.nptr, 4 * (nn + 1), cudaMemcpyDeviceToDevice, s);
+        if (ne > 0) bucket_fill_k<SH><<<ge, 256, 0, s>>>(ne, nv, elems, elem_ld, w.cursor, w.node_elem);
+        if (nn > 0) sort_incidences_k<<<grid_for(nn, SORT_BLOCK, 8), SORT_BLOCK, 0, s>>>(nn, w.nptr, w.node_elem);
+        return launch_check(fn);
+    };
+
     if (!col_idx) {
-        // 2. count
-        if (nn > 0) row_count_k<SH, CAP, BLOCK><<<gr, BLOCK, 0, s>>>(nn, nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
-        row_count_big_k<SH><<<64, 32, 0, s>>>(nv, elems, elem_ld, nptr, nelem, w.row_len, w.ovf, w.flags);
+        // count phase: incidences, row lists (kept for the fill phase), row_ptr, nnz
+        cudaMemsetAsync(w.flags, 0, 64, s);
+        Stamp none{};
+        write_stamp_k<<<1, 1, 0, s>>>(w.stamp, none);
+        if ((st = incidences()) != VB_OK) return st;
+        if (nn > 0) row_count_k<SH, CAP, BLOCK><<<gr, BLOCK, 0, s>>>(nn, nv, elems, elem_ld, w.nptr, w.node_elem, w.row_len, w.ovf, w.rowlist, w.flags);
+        row_count_big_k<SH><<<64, 32, 0, s>>>(nv, elems, elem_ld, w.nptr, w.node_elem, w.row_len, w.ovf, w.flags);
         if ((st = exclusive_scan_i32(w.row_len, row_ptr, nn, w.scan_tmp, s, w.total)) != VB_OK) return st;
+        write_stamp_k<<<1, 1, 0, s>>>(w.stamp, mine);
+        if ((st = launch_check(fn)) != VB_OK) return st;
         int64_t host[2] = {0, 0};
         int hflags[4] = {0, 0, 0, 0};
         if ((st = read_small(s, w.total, sizeof(int64_t), host, fn)) != VB_OK) return st;
@@ -309,15 +387,28 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
         if (nnz_out) *nnz_out = host[0];
         return VB_OK;
     }
-    // 3. fill (row_ptr from the count phase); check the capacity before writing
+    // fill phase (row_ptr from the count phase); check the capacity before writing.
+    // With the count phase's work buffer (stamp matches) its incidence lists and
+    // row lists are reused; otherwise they are rebuilt here.
     int32_t nnz32 = 0;
+    Stamp seen{};
     if ((st = read_small(s, row_ptr + nn, 4, &nnz32, fn)) != VB_OK) return st;
+    if ((st = read_small(s, w.stamp, sizeof(Stamp), &seen, fn)) != VB_OK) return st;
     if (nnz32 < 0 || nnz32 > col_cap) { set_error("%s: col_cap=%lld < nnz=%d", fn, (long long)col_cap, nnz32); return VB_ERR_ARG; }
+    const bool reuse = seen.magic == mine.magic && seen.nn == nn && seen.ne == ne && seen.nv == nv &&
+                       seen.elem_ld == elem_ld && seen.elems == elems;
+    cudaMemsetAsync(w.flags, 0, 64, s);
+    if (!reuse && (st = incidences()) != VB_OK) return st;
+    if (node_elem_ptr) {
+        cudaMemcpyAsync(node_elem_ptr, w.nptr, 4 * (nn + 1), cudaMemcpyDeviceToDevice, s);
+        if (ne > 0) cudaMemcpyAsync(node_elem, w.node_elem, 4 * (size_t)nv * ne, cudaMemcpyDeviceToDevice, s);
+    }
     if (nn > 0) {
         // rows longer than CAP are collected by row_fill_k and filled by the fallback
-        row_fill_k<SH, CAP, BLOCK><<<gr, BLOCK, 0, s>>>(nn, ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx,
-                                                        elem2nnz, node_elem_slot, w.ovf, w.flags);
-        row_fill_big_k<SH><<<64, 32, 0, s>>>(ne, nv, elems, elem_ld, nptr, nelem, row_ptr, col_idx, elem2nnz,
+        row_fill_k<SH, CAP, BLOCK><<<gr, BLOCK, 0, s>>>(nn, ne, nv, elems, elem_ld, w.nptr, w.node_elem, row_ptr, col_idx,
+                                                        elem2nnz, node_elem_slot, reuse ? w.rowlist : nullptr,
+                                                        w.ovf, w.flags);
+        row_fill_big_k<SH><<<64, 32, 0, s>>>(ne, nv, elems, elem_ld, w.nptr, w.node_elem, row_ptr, col_idx, elem2nnz,
                                               node_elem_slot, w.ovf, w.flags);
     }
     if ((st = launch_check(fn)) != VB_OK) return st;

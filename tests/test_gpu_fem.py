@@ -295,3 +295,37 @@ def test_delaunay_meshes_parity(dev, dim, n, permute):
     for mode in MODES:
         K, M = vb.fem_p1_assemble_coef(g(coords, dev), g(elems, dev), plan, gqo=2, cK=cK, cM=cM, mode=mode)[:2]
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+
+
+@pytest.mark.parametrize("kind,n", [("3d", 5), ("2d", 20)])
+def test_fill_phase_without_count_state(dev, kind, n):
+    """The fill phase reuses the count phase's lists when it gets the count
+    phase's work buffer; given a different (zeroed) work buffer it rebuilds them
+    and must produce identical plans."""
+    import ctypes as C
+    coords, elems = mesh(kind, n, seed=3)
+    nn = coords.shape[1]
+    ed = g(elems, dev)
+    ref = vb.P1Plan(ed, nn)
+    L = vb.lib()
+    nv, ne = elems.shape
+    sz, nnz = C.c_size_t(0), C.c_int64(0)
+    vb._check(L.fem_p1_pattern(nv - 1, nn, ne, None, ne, None, C.byref(sz), None, None, 0, None, None, None, None,
+                               None, None))
+    w1 = torch.empty(sz.value, dtype=torch.uint8, device=dev)
+    w2 = torch.zeros(sz.value, dtype=torch.uint8, device=dev)
+    rp = torch.empty(nn + 1, dtype=torch.int32, device=dev)
+    vb._check(L.fem_p1_pattern(nv - 1, nn, ne, vb._ptr(ed), ne, vb._ptr(w1), C.byref(sz), vb._ptr(rp), None, 0, None,
+                               None, None, None, C.byref(nnz), None))
+    k = int(nnz.value)
+    ci = torch.zeros(k + 4, dtype=torch.int32, device=dev)
+    e2n = torch.empty((nv * nv, ne), dtype=torch.int32, device=dev)
+    nptr = torch.empty(nn + 1, dtype=torch.int32, device=dev)
+    nel = torch.empty(nv * ne, dtype=torch.int32, device=dev)
+    nsl = torch.zeros(nv * ne + 4, dtype=torch.int32, device=dev)
+    vb._check(L.fem_p1_pattern(nv - 1, nn, ne, vb._ptr(ed), ne, vb._ptr(w2), C.byref(sz), vb._ptr(rp), vb._ptr(ci),
+                               k + 4, vb._ptr(e2n), vb._ptr(nptr), vb._ptr(nel), vb._ptr(nsl), C.byref(nnz), None))
+    assert np.array_equal(h(rp), h(ref.row_ptr)) and np.array_equal(h(ci)[:k], h(ref.col_idx))
+    assert np.array_equal(h(e2n), h(ref.elem2nnz))
+    assert np.array_equal(h(nptr), h(ref.node_elem_ptr)) and np.array_equal(h(nel), h(ref.node_elem))
+    assert np.array_equal(h(nsl)[:nv * ne], h(ref.node_elem_slot)[:nv * ne])
