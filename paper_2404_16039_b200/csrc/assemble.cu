@@ -260,11 +260,7 @@ struct GatherCfg {
     static constexpr int ACC_N = LANE_CAP + OVF;                         // accumulator / edge-vector slots
     static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_CAP2 : VB_GATHER_CAP3);  // CSR entries of a block
     static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_SLOT2 : VB_GATHER_SLOT3);  // plan words
-#ifdef VB_GATHER_SLOTS_GLOBAL
-    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = 0;   // plan words read through L1
-#else
     static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
-#endif
     static constexpr int RING = 2;                                       // plan words: double-buffered
     static constexpr size_t COLS_BYTES = (size_t)COLS_PAD * 4;           // columns: one buffer (consumed early)
     static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * 4;
@@ -545,10 +541,7 @@ __device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, 
     B.p1 = __ldg(row_ptr + B.r1);
     B.q0 = __ldg(nptr + B.r0);
     B.q1 = __ldg(nptr + B.r1);
-    B.fit = (B.p1 - B.p0) <= GatherCfg<DIM>::CAP;
-#ifndef VB_GATHER_SLOTS_GLOBAL
-    B.fit = B.fit && (B.q1 - B.q0) <= GatherCfg<DIM>::SLOT_CAP;
-#endif
+    B.fit = (B.p1 - B.p0) <= GatherCfg<DIM>::CAP && (B.q1 - B.q0) <= GatherCfg<DIM>::SLOT_CAP;
     return B;
 }
 
@@ -580,6 +573,10 @@ struct GatherSmem {
 // Accumulators: (K, M) pair of slot s < RS at [slot][lane], else overflow.
 // Blocks without overflow rows (all of Kuhn's) use the map without the select
 // (OV = false): the select on every access cost 20 % on config 5.
+// Measured and not kept: plan words read through L1 instead of TMA staging
+// (0.572 vs 0.540 ms, even with 9 instead of 7 CTAs per SM); two warps per
+// block sharing the staged data, each with its own accumulators over half of
+// every row's incidences (10 warps per SM: 0.62 vs 0.55 ms).
 // (Interleaving (x, y) pairs for 128-bit F loads measured slower: 0.549 vs 0.530 ms.)
 template <int DIM, bool OV>
 struct LaneMap {
@@ -613,14 +610,7 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
     uint32_t s0 = (uint32_t)B.q0 & ~3u, s1 = ((uint32_t)B.q1 + 3u) & ~3u;
     uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * 4;
     // generic-proxy reads of the column buffer (previous block) before the async-proxy overwrite
-#ifndef VB_GATHER_NOFENCE
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
-#ifdef VB_GATHER_SLOTS_GLOBAL
-    bs = 0;
-    (void)s0;
-    (void)s1;
-#endif
     mbar_expect_tx(S.bar(r), bc + bs);
     if (bc) tma_load_1d(S.cols(), col_idx + c0, bc, S.bar(r));
     if (bs) tma_load_1d(S.slots(r), nslot + s0, bs, S.bar(r));
@@ -658,10 +648,6 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, BlockBounds& B
     R.ov = inc - ex;
     R.fast = staged && R.own && R.L > 0 && (ex == 0 || inc <= C::OVF);
     R.ovb = __any_sync(0xffffffffu, R.fast && ex > 0);
-#ifdef VB_GATHER_NOOVF
-    if (ex > 0) R.fast = false;
-    R.ovb = false;
-#endif
     if (R.fast) {
         const int32_t* cols = S.cols() + tma_shift(B.p0) + (R.lo - B.p0);
         double* F = S.F();
@@ -724,12 +710,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         cp_async_wait<0>();
         __syncwarp();
         if (staged) {
-#ifdef VB_GATHER_SLOTS_GLOBAL
-            const uint32_t* slots = nslot;
-            (void)rc;
-#else
             const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
-#endif
             const int np = B0.p1 - B0.p0;
             auto run = [&](auto lm) {
                 double mrow = 0.0;
