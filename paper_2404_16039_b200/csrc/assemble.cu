@@ -252,7 +252,7 @@ constexpr int GATHER_ROWS = 32;
 #ifndef VB_GATHER_OVF2
 #define VB_GATHER_OVF2 32
 #endif
-template <int DIM>
+template <int DIM, int NC = DIM>   // NC doubles staged per column slot: coordinates (+ coefficient factors)
 struct GatherCfg {
     static constexpr int RS = DIM == 2 ? VB_GATHER_RS2 : VB_GATHER_RS3;  // columns per row in the lane arrays
     static constexpr int OVF = DIM == 2 ? VB_GATHER_OVF2 : VB_GATHER_OVF3;  // overflow columns per block
@@ -266,10 +266,10 @@ struct GatherCfg {
     static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * 4;
     static constexpr size_t SLOTS_OFF = COLS_BYTES;
     static constexpr size_t F_OFF = SLOTS_OFF + RING * SLOTS_BYTES;      // edge vectors / CSR staging
-    static constexpr size_t ACC_OFF = F_OFF + (size_t)DIM * ACC_N * 8;   // (K, M) pairs
+    static constexpr size_t ACC_OFF = F_OFF + (size_t)NC * ACC_N * 8;    // (K, M) pairs
     static constexpr size_t BAR_OFF = ACC_OFF + (size_t)2 * ACC_N * 8;
     static constexpr size_t SMEM = BAR_OFF + RING * 8;
-    static_assert(2 * CAP <= DIM * ACC_N, "K and M staging fit in the edge-vector buffer");
+    static_assert(2 * CAP <= NC * ACC_N, "K and M staging fit in the edge-vector buffer");
     static_assert(COLS_BYTES % 16 == 0 && SLOTS_BYTES % 16 == 0, "TMA destinations must stay 16-byte aligned");
     static_assert(DIM >= 2, "staging of K and M in CSR order reuses the edge-vector buffer");
 };
@@ -326,10 +326,16 @@ struct IncOut {
 
 // Coefficient-weighted evaluation (NEXT-1, Code stiff_scalar_P1 P:978-1004 with
 // c(x) = a exp(b . x)): intquad(gqo) points in barycentric form, "point q near
-// vertex q" (symmetric rules), vertex 0 = the row's vertex, 1..d = the others.
-template <int DIM>
+// vertex q" (symmetric rules: lambda_q = alpha at vertex q, beta elsewhere),
+// vertex 0 = the row's vertex, 1..d = the others.
+// FAC (c_K = c_M): the coefficient at point q is taken from per-vertex factors
+// P_i = exp(beta b.x_i), R_i = exp((alpha - beta) b.x_i) as a R_q prod_i P_i
+// (= a exp(b.x_q) exactly in real arithmetic; gqo = 1: P_i = exp(b.x_i / nv),
+// R = 1), so the hot loop evaluates no exponential.
+template <int DIM, bool FAC>
 __device__ __forceinline__ void apply_coef(IncOut<DIM>& o, const double (&xv)[DIM], const double (&f)[DIM][DIM],
-                                           const CoefSpec& cp) {
+                                           const CoefSpec& cp, const double (&P)[DIM + 1],
+                                           const double (&R)[DIM + 1]) {
     constexpr int NV = DIM + 1;
     const bool one = cp.gqo == 1;
     const double al = one ? 1.0 / NV : QuadRule<DIM>::ALPHA, be = one ? 1.0 / NV : QuadRule<DIM>::BETA;
@@ -338,25 +344,37 @@ __device__ __forceinline__ void apply_coef(IncOut<DIM>& o, const double (&xv)[DI
     double sk = 0.0, mrow = 0.0, mj[DIM];
 #pragma unroll
     for (int j = 0; j < DIM; j++) mj[j] = 0.0;
+    double prodP = 1.0;
+    if constexpr (FAC) {
+        prodP = cp.ka * P[0];
+#pragma unroll
+        for (int j = 1; j < NV; j++) prodP *= P[j];
+    }
 #pragma unroll
     for (int q = 0; q < NV; q++) {
         if (q >= nip) break;
-        double x[DIM];
+        double ck, cm;
+        if constexpr (FAC) {
+            ck = one ? prodP : prodP * R[q];
+            cm = ck;
+        } else {
+            double x[DIM];
 #pragma unroll
-        for (int c = 0; c < DIM; c++) {
-            double s = xv[c];
+            for (int c = 0; c < DIM; c++) {
+                double s = xv[c];
 #pragma unroll
-            for (int j = 0; j < DIM; j++) s = fma(q == j + 1 ? al : be, f[j][c], s);
-            x[c] = s;
+                for (int j = 0; j < DIM; j++) s = fma(q == j + 1 ? al : be, f[j][c], s);
+                x[c] = s;
+            }
+            double ek = 0.0, em = 0.0;
+#pragma unroll
+            for (int c = 0; c < DIM; c++) {
+                ek = fma(cp.kb[c], x[c], ek);
+                em = fma(cp.mb[c], x[c], em);
+            }
+            ck = cp.ka * exp(ek);
+            cm = cp.same ? ck : cp.ma * exp(em);
         }
-        double ek = 0.0, em = 0.0;
-#pragma unroll
-        for (int c = 0; c < DIM; c++) {
-            ek = fma(cp.kb[c], x[c], ek);
-            em = fma(cp.mb[c], x[c], em);
-        }
-        const double ck = cp.ka * exp(ek);
-        const double cm = cp.same ? ck : cp.ma * exp(em);
         sk += ck;
         const double la = q == 0 ? al : be;
         mrow = fma(cm, la, mrow);
@@ -372,9 +390,22 @@ __device__ __forceinline__ void apply_coef(IncOut<DIM>& o, const double (&xv)[DI
     o.mrow = o.ad * wq * mrow;
 }
 
-template <int DIM, bool COEF, typename EV>
-__device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, const double (&xv)[DIM], const CoefSpec& cp) {
+// no per-vertex factors
+struct NoFac {
+    __device__ void operator()(int, double&, double&) const {}
+};
+
+// fv(s, P, R): the per-vertex coefficient factors of column slot s (FAC);
+// pv: those of the row's vertex
+template <int DIM, bool COEF, bool FAC, typename EV, typename FV>
+__device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, FV fv, const double (&xv)[DIM],
+                                                 const double (&pv)[2], const CoefSpec& cp) {
     IncOut<DIM> o;
+    double P[DIM + 1], R[DIM + 1];
+    if constexpr (FAC) {
+        P[0] = pv[0];
+        R[0] = pv[1];
+    }
     if constexpr (DIM == 3) {
         o.s[0] = (sl >> 8) & 0xff;
         o.s[1] = (sl >> 16) & 0xff;
@@ -400,7 +431,10 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, const doubl
         o.ad = ad;
         if constexpr (COEF) {
             const double f[3][3] = {{f1[0], f1[1], f1[2]}, {f2[0], f2[1], f2[2]}, {f3[0], f3[1], f3[2]}};
-            apply_coef<3>(o, xv, f, cp);
+            if constexpr (FAC)
+#pragma unroll
+                for (int j = 0; j < 3; j++) fv(o.s[j], P[j + 1], R[j + 1]);
+            apply_coef<3, FAC>(o, xv, f, cp, P, R);
         }
     } else {
         o.s[0] = (sl >> 8) & 0xff;
@@ -417,7 +451,10 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, const doubl
         o.ad = ad;
         if constexpr (COEF) {
             const double f[2][2] = {{f1[0], f1[1]}, {f2[0], f2[1]}};
-            apply_coef<2>(o, xv, f, cp);
+            if constexpr (FAC)
+#pragma unroll
+                for (int j = 0; j < 2; j++) fv(o.s[j], P[j + 1], R[j + 1]);
+            apply_coef<2, FAC>(o, xv, f, cp, P, R);
         }
     }
     return o;
@@ -466,14 +503,18 @@ __device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restr
 // from the row's vertex to its column s.  Incidences are evaluated U at a time
 // (all loads and arithmetic before any accumulator store) and accumulated in
 // ascending element order.  Returns the row sum of M (COEF only).
-template <int DIM, bool PACKED, bool WK, bool WM, bool COEF, typename EV, typename IX>
-__device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, IX ix,
+template <int DIM, bool PACKED, bool WK, bool WM, bool COEF, bool FAC, typename EV, typename FV, typename IX>
+__device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, FV fv, IX ix,
                                                double* __restrict__ accK, double* __restrict__ accM,
-                                               const double (&xv)[DIM], const CoefSpec& cp) {
+                                               const double (&xv)[DIM], const double (&pv)[2],
+                                               const CoefSpec& cp) {
 #ifndef VB_GATHER_U
 #define VB_GATHER_U 6   // 4: +2 % on config 5 (24 incidences per row = 4 chunks), -3 % on Delaunay
 #endif
-    constexpr int U = COEF ? 2 : VB_GATHER_U;
+#ifndef VB_GATHER_UF
+#define VB_GATHER_UF 4  // coefficient factors (FAC): 2 / 3 / 4 -> 1.29 / 1.28 / 1.25 ms (tab:KM_P1_3D L7)
+#endif
+    constexpr int U = COEF ? (FAC ? VB_GATHER_UF : 2) : VB_GATHER_U;
     // (A lane-rotated incidence order, which makes the plan-word reads bank-conflict
     // free -- 8 -> 1 wavefronts, 13 % of the kernel's shared-memory wavefronts --
     // measured 0.530 vs 0.528 ms on config 5 and would give up the ascending order.)
@@ -482,23 +523,25 @@ __device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* _
     for (; i + U - 1 < i1; i += U) {
         IncOut<DIM> o[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF>(slots[i + u], ev, xv, cp);
+        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF, FAC>(slots[i + u], ev, fv, xv, pv, cp);
 #pragma unroll
         for (int u = 0; u < U; u++) accumulate<DIM, PACKED, WK, WM, COEF>(o[u], accK, accM, ix, mrow);
     }
     for (; i < i1; i++)
-        accumulate<DIM, PACKED, WK, WM, COEF>(incidence<DIM, COEF>(slots[i], ev, xv, cp), accK, accM, ix, mrow);
+        accumulate<DIM, PACKED, WK, WM, COEF>(incidence<DIM, COEF, FAC>(slots[i], ev, fv, xv, pv, cp), accK, accM, ix,
+                                              mrow);
     return mrow;
 }
 
 // PAIRS: accM == accK + 1 (interleaved pairs), packed access when both are wanted
-template <int DIM, bool PAIRS, bool COEF, typename EV, typename IX>
-__device__ __forceinline__ double gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, IX ix,
+template <int DIM, bool PAIRS, bool COEF, bool FAC, typename EV, typename FV, typename IX>
+__device__ __forceinline__ double gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, FV fv, IX ix,
                                              double* __restrict__ accK, double* __restrict__ accM,
-                                             const double (&xv)[DIM], const CoefSpec& cp) {
-    if (accK && accM) return gather_row_t<DIM, PAIRS, true, true, COEF>(i0, i1, slots, ev, ix, accK, accM, xv, cp);
-    if (accK) return gather_row_t<DIM, false, true, false, COEF>(i0, i1, slots, ev, ix, accK, accM, xv, cp);
-    if (accM) return gather_row_t<DIM, false, false, true, COEF>(i0, i1, slots, ev, ix, accK, accM, xv, cp);
+                                             const double (&xv)[DIM], const double (&pv)[2], const CoefSpec& cp) {
+    if (accK && accM)
+        return gather_row_t<DIM, PAIRS, true, true, COEF, FAC>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
+    if (accK) return gather_row_t<DIM, false, true, false, COEF, FAC>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
+    if (accM) return gather_row_t<DIM, false, false, true, COEF, FAC>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
     return 0.0;
 }
 
@@ -555,16 +598,15 @@ struct RowInfo {
     bool ovb;    // some row of the block uses the overflow area (warp-uniform)
 };
 
-template <int DIM>
+template <int DIM, int NC>
 struct GatherSmem {
+    using C = GatherCfg<DIM, NC>;
     char* base;
     __device__ int32_t* cols() { return reinterpret_cast<int32_t*>(base); }
-    __device__ uint32_t* slots(int r) {
-        return reinterpret_cast<uint32_t*>(base + GatherCfg<DIM>::SLOTS_OFF + r * GatherCfg<DIM>::SLOTS_BYTES);
-    }
-    __device__ double* F() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::F_OFF); }
-    __device__ double* acc() { return reinterpret_cast<double*>(base + GatherCfg<DIM>::ACC_OFF); }
-    __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + GatherCfg<DIM>::BAR_OFF) + r; }
+    __device__ uint32_t* slots(int r) { return reinterpret_cast<uint32_t*>(base + C::SLOTS_OFF + r * C::SLOTS_BYTES); }
+    __device__ double* F() { return reinterpret_cast<double*>(base + C::F_OFF); }
+    __device__ double* acc() { return reinterpret_cast<double*>(base + C::ACC_OFF); }
+    __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + C::BAR_OFF) + r; }
 };
 
 // Where slot s of lane t lives.  Edge-vector / column-coordinate buffer F:
@@ -578,16 +620,16 @@ struct GatherSmem {
 // block sharing the staged data, each with its own accumulators over half of
 // every row's incidences (10 warps per SM: 0.62 vs 0.55 ms).
 // (Interleaving (x, y) pairs for 128-bit F loads measured slower: 0.549 vs 0.530 ms.)
-template <int DIM, bool OV>
+template <int DIM, bool OV, int NC = DIM>
 struct LaneMap {
     int t, ov;
-    __device__ __forceinline__ int f(int s, int c) const {
-        using C = GatherCfg<DIM>;
-        if constexpr (!OV) return (s * DIM + c) * GATHER_ROWS + t;
-        return s < C::RS ? (s * DIM + c) * GATHER_ROWS + t : DIM * C::LANE_CAP + (ov + s - C::RS) * DIM + c;
+    __device__ __forceinline__ int f(int s, int c) const {   // component c of slot s
+        using C = GatherCfg<DIM, NC>;
+        if constexpr (!OV) return (s * NC + c) * GATHER_ROWS + t;
+        return s < C::RS ? (s * NC + c) * GATHER_ROWS + t : NC * C::LANE_CAP + (ov + s - C::RS) * NC + c;
     }
     __device__ __forceinline__ int a(int s) const {   // in doubles: K at a(s), M at a(s) + 1
-        using C = GatherCfg<DIM>;
+        using C = GatherCfg<DIM, NC>;
         if constexpr (!OV) return 2 * (s * GATHER_ROWS + t);
         return 2 * (s < C::RS ? s * GATHER_ROWS + t : C::LANE_CAP + ov + s - C::RS);
     }
@@ -598,8 +640,8 @@ __device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
 
 // lane 0 only: stream block B's columns (single buffer: the previous block's were
 // consumed by its coordinate gather) and plan words (ring slot r)
-template <int DIM>
-__device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const BlockBounds& B,
+template <int DIM, int NC>
+__device__ __forceinline__ void issue_tma(GatherSmem<DIM, NC>& S, int r, const BlockBounds& B,
                                           const int32_t* __restrict__ col_idx, const uint32_t* __restrict__ nslot) {
     if (!B.valid) return;
     if (!B.fit) {  // keep the barrier's phase count in step with the ring: arrive with no bytes
@@ -619,8 +661,8 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM>& S, int r, const Block
 // Load the lane's row of block B.  If the block is staged (its CSR and plan
 // ranges fit), place the row (lane arrays + overflow), find its diagonal slot and
 // gather its column coordinates into F.  Returns whether the block is staged.
-template <int DIM>
-__device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, BlockBounds& B, RowInfo& R,
+template <int DIM, int NC>
+__device__ __forceinline__ bool prepare_block(GatherSmem<DIM, NC>& S, BlockBounds& B, RowInfo& R,
                                               const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
                                               const double* __restrict__ coords, int64_t ns, int64_t cst) {
     using C = GatherCfg<DIM>;
@@ -659,13 +701,13 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM>& S, BlockBounds& B
                 for (int c = 0; c < DIM; c++) cp_async8(F + lm.f(s, c), coords + c * cst + w * ns);
             }
         };
-        if (R.ovb) gather(LaneMap<DIM, true>{t, R.ov});
-        else gather(LaneMap<DIM, false>{t, R.ov});
+        if (R.ovb) gather(LaneMap<DIM, true, NC>{t, R.ov});
+        else gather(LaneMap<DIM, false, NC>{t, R.ov});
     }
     return staged;
 }
 
-template <int DIM, bool COEF>
+template <int DIM, bool COEF, bool FAC>
 __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, const double* __restrict__ coords,
                                                                  int64_t ns, int64_t cst,
                                                                  const int32_t* __restrict__ row_ptr,
@@ -674,11 +716,13 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                                                                  const uint32_t* __restrict__ nslot,
                                                                  double* __restrict__ K, double* __restrict__ M,
                                                                  const CoefSpec cp) {
-    using Cfg = GatherCfg<DIM>;
+    static_assert(COEF || !FAC, "factors are a coefficient mode");
+    constexpr int NC = FAC ? DIM + 2 : DIM;   // staged per slot: coordinates (+ P, R factors)
+    using Cfg = GatherCfg<DIM, NC>;
     constexpr int W = GATHER_ROWS;
     constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);  // 1/(d! (d+1)(d+2))
     extern __shared__ __align__(16) char smem_raw[];
-    GatherSmem<DIM> S{smem_raw};
+    GatherSmem<DIM, NC> S{smem_raw};
     const int t = threadIdx.x;
     const int64_t nblocks = (nn + W - 1) / W;
     const int64_t gstep = gridDim.x;
@@ -690,10 +734,10 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     // prologue: TMA for this CTA's first block, then its coordinate gather
     BlockBounds B0 = block_bounds<DIM>(blockIdx.x, nblocks, nn, row_ptr, nptr);
     BlockBounds B1 = block_bounds<DIM>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
-    if (t == 0) issue_tma<DIM>(S, 0, B0, col_idx, nslot);
+    if (t == 0) issue_tma<DIM, NC>(S, 0, B0, col_idx, nslot);
     if (B0.valid) mbar_wait(S.bar(0), 0);
     RowInfo R;
-    bool staged = prepare_block<DIM>(S, B0, R, row_ptr, nptr, coords, ns, cst);
+    bool staged = prepare_block<DIM, NC>(S, B0, R, row_ptr, nptr, coords, ns, cst);
     cp_async_commit();
 
     double* F = S.F();
@@ -704,7 +748,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         const int rc = (int)(k & 1), rn = rc ^ 1;
         // stage k+1: stream its columns and plan words (every lane is past its column reads)
         __syncwarp();
-        if (t == 0) issue_tma<DIM>(S, rn, B1, col_idx, nslot);
+        if (t == 0) issue_tma<DIM, NC>(S, rn, B1, col_idx, nslot);
         BlockBounds B2 = block_bounds<DIM>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
         // stage k: its coordinates have landed
         cp_async_wait<0>();
@@ -716,18 +760,40 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                 double mrow = 0.0;
                 if (R.fast) {
                     for (int s = 0; s < R.L; s++) *reinterpret_cast<double2*>(acc + lm.a(s)) = make_double2(0.0, 0.0);
-                    double xv[DIM];
+                    if constexpr (FAC) {
+                        // per-slot coefficient factors from the staged coordinates (apply_coef)
+                        constexpr int NV = DIM + 1;
+                        const bool one = cp.gqo == 1;
+                        const double be = one ? 1.0 / NV : QuadRule<DIM>::BETA;
+                        const double amb = QuadRule<DIM>::ALPHA - QuadRule<DIM>::BETA;
+                        for (int s = 0; s < R.L; s++) {
+                            double bx = 0.0;
+#pragma unroll
+                            for (int c = 0; c < DIM; c++) bx = fma(cp.kb[c], F[lm.f(s, c)], bx);
+                            F[lm.f(s, DIM)] = exp(be * bx);
+                            F[lm.f(s, DIM + 1)] = one ? 1.0 : exp(amb * bx);
+                        }
+                    }
+                    double xv[DIM], pv[2] = {1.0, 1.0};
 #pragma unroll
                     for (int c = 0; c < DIM; c++) xv[c] = F[lm.f(R.s0, c)];
+                    if constexpr (FAC) {
+                        pv[0] = F[lm.f(R.s0, DIM)];
+                        pv[1] = F[lm.f(R.s0, DIM + 1)];
+                    }
                     auto ev = [&](int s, double(&f)[DIM]) {
                         VB_CHECK(s < R.L && s != R.s0);
 #pragma unroll
                         for (int c = 0; c < DIM; c++) f[c] = F[lm.f(s, c)] - xv[c];
                     };
+                    auto fv = [&](int s, double& P, double& Rq) {
+                        P = F[lm.f(s, DIM)];
+                        Rq = F[lm.f(s, DIM + 1)];
+                    };
                     auto ix = [&](int s) { return lm.a(s); };
                     VB_CHECK(R.i0 >= B0.q0 && R.i1 <= B0.q1 && R.lo >= B0.p0 && R.lo + R.L <= B0.p1);
-                    mrow = gather_row<DIM, true, COEF>(R.i0, R.i1, slots, ev, ix, K ? acc : nullptr,
-                                                       M ? acc + 1 : nullptr, xv, cp);
+                    mrow = gather_row<DIM, true, COEF, FAC>(R.i0, R.i1, slots, ev, fv, ix, K ? acc : nullptr,
+                                                            M ? acc + 1 : nullptr, xv, pv, cp);
                 }
                 __syncwarp();
                 // finish the row (diagonal from the partition of unity, M scale) while
@@ -755,8 +821,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                     if (M) stcs(M + B0.p0 + q, stM[q]);
                 }
             };
-            if (R.ovb) run(LaneMap<DIM, true>{t, R.ov});
-            else run(LaneMap<DIM, false>{t, R.ov});
+            if (R.ovb) run(LaneMap<DIM, true, NC>{t, R.ov});
+            else run(LaneMap<DIM, false, NC>{t, R.ov});
         }
         __syncwarp();   // orders the staged stores above before the in-place rows below
         if (R.own && R.L > 0 && !R.fast) {
@@ -780,13 +846,14 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                 for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
             };
             auto ix = [](int s) { return s; };
-            double mrow = gather_row<DIM, false, COEF>(R.i0, R.i1, nslot, ev, ix, aK, aM, xv, cp);
+            const double pv[2] = {1.0, 1.0};
+            double mrow = gather_row<DIM, false, COEF, false>(R.i0, R.i1, nslot, ev, NoFac{}, ix, aK, aM, xv, pv, cp);
             finish_row<DIM, 1, COEF>(R.L, s0, aK, aM, mrow);
         }
         __syncwarp();
         // stage k+1: its columns have landed -> gather its coordinates into F (free now)
         if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) >> 1) & 1));
-        staged = prepare_block<DIM>(S, B1, R, row_ptr, nptr, coords, ns, cst);
+        staged = prepare_block<DIM, NC>(S, B1, R, row_ptr, nptr, coords, ns, cst);
         cp_async_commit();
         B0 = B1;
         B1 = B2;
@@ -801,22 +868,22 @@ using namespace vb;
 
 namespace {
 
-template <int DIM, bool COEF>
+template <int DIM, bool COEF, bool FAC>
 void launch_gather(unsigned g, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
                    const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const uint32_t* nslot,
                    double* K, double* M, const CoefSpec& cp) {
-    assemble_gather_k<DIM, COEF><<<g, GATHER_ROWS, GatherCfg<DIM>::SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx,
-                                                                            nptr, nslot, K, M, cp);
+    constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM>::SMEM;
+    assemble_gather_k<DIM, COEF, FAC><<<g, GATHER_ROWS, SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx, nptr, nslot,
+                                                                   K, M, cp);
 }
 
-template <int DIM, bool COEF>
+template <int DIM, bool COEF, bool FAC>
 int gather_ctas_per_sm() {
     static int n = 0;  // > 48 KB dynamic smem needs an opt-in; persistent grid size
     if (!n) {
-        cudaFuncSetAttribute(assemble_gather_k<DIM, COEF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)GatherCfg<DIM>::SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF>, GATHER_ROWS,
-                                                      GatherCfg<DIM>::SMEM);
+        constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM>::SMEM;
+        cudaFuncSetAttribute(assemble_gather_k<DIM, COEF, FAC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF, FAC>, GATHER_ROWS, SMEM);
         if (n < 1) n = 1;
     }
     return n;
@@ -858,10 +925,18 @@ vb_status assemble_impl(const char* fn, int64_t nn, int64_t ne, const double* co
     }
     if (want_global && nn > 0) {
         int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
-        int64_t cap = (int64_t)sm_count() * (C ? gather_ctas_per_sm<DIM, true>() : gather_ctas_per_sm<DIM, false>());
+        // c_K = c_M with gqo = 2 (the paper's benchmarks): per-vertex factors instead of
+        // 4 exponentials per incidence (1.43 -> 1.25 ms on tab:KM_P1_3D level 7).  Not for
+        // gqo = 1: one exponential per incidence is cheaper than staging the factors
+        // (their smem costs 2 of 7 CTAs per SM; 0.81 -> 1.06 ms measured)
+        const bool fac = C && cp.same && cp.gqo == 2;
+        const int per_sm = fac ? gather_ctas_per_sm<DIM, true, true>()
+                               : C ? gather_ctas_per_sm<DIM, true, false>() : gather_ctas_per_sm<DIM, false, false>();
+        int64_t cap = (int64_t)sm_count() * per_sm;
         unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
-        if (C) launch_gather<DIM, true>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
-        else launch_gather<DIM, false>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
+        if (fac) launch_gather<DIM, true, true>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
+        else if (C) launch_gather<DIM, true, false>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
+        else launch_gather<DIM, false, false>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
         if ((st = launch_check(fn)) != VB_OK) return st;
     }
     if ((K_local || M_local) && ne > 0) {

@@ -15,8 +15,11 @@ from paper_2404_16039_b200 import vb
 
 pytestmark = pytest.mark.gpu
 MODES = [vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC]
+# 0: the paper's e^{x+y+z}; 1: c_K != c_M (exponentials at the points); 2: c_K == c_M
+# non-trivial (per-vertex factor path of the gather kernel for gqo = 2)
 COEFS = [((1.0, (1.0, 1.0, 1.0)), (1.0, (1.0, 1.0, 1.0))),
-         ((2.5, (0.3, -0.7, 0.45)), (0.6, (-1.0, 0.2, 0.9)))]
+         ((2.5, (0.3, -0.7, 0.45)), (0.6, (-1.0, 0.2, 0.9))),
+         ((1.7, (0.9, -1.3, 0.4)), (1.7, (0.9, -1.3, 0.4)))]
 
 
 @pytest.fixture(scope="module")
@@ -40,7 +43,7 @@ def relmax(got, ref):
 
 @pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("gqo", [1, 2])
-@pytest.mark.parametrize("coef", [0, 1])
+@pytest.mark.parametrize("coef", [0, 1, 2])
 @pytest.mark.parametrize("kind", ["2d", "3d", "2d-crossed"])
 def test_coef_assembly_parity(dev, kind, coef, gqo, mode):
     if kind == "2d":

@@ -290,11 +290,12 @@ def test_delaunay_meshes_parity(dev, dim, n, permute):
     for mode in MODES:
         K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
-    cK, cM = (2.0, (0.4, -0.3, 0.2)), (0.5, (-0.6, 0.1, 0.8))
-    Ko, Mo = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cK, cM=cM)
-    for mode in MODES:
-        K, M = vb.fem_p1_assemble_coef(g(coords, dev), g(elems, dev), plan, gqo=2, cK=cK, cM=cM, mode=mode)[:2]
-        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+    for cK, cM in (((2.0, (0.4, -0.3, 0.2)), (0.5, (-0.6, 0.1, 0.8))),
+                   ((1.3, (0.7, 0.2, -0.5)), (1.3, (0.7, 0.2, -0.5)))):
+        Ko, Mo = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cK, cM=cM)
+        for mode in MODES:
+            K, M = vb.fem_p1_assemble_coef(g(coords, dev), g(elems, dev), plan, gqo=2, cK=cK, cM=cM, mode=mode)[:2]
+            assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
 
 
 @pytest.mark.parametrize("kind,n", [("3d", 5), ("2d", 20)])
