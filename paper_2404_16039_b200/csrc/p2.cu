@@ -109,14 +109,17 @@ __device__ __forceinline__ void p2_basis(int k, const double* lam, const double 
     }
 }
 
+constexpr int P2_BLOCK = 64;   // 55 x 64 doubles of M staging (28 KB static smem in 3D)
+
 template <int DIM>
-__global__ void __launch_bounds__(128) p2_assemble_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
+__global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
                                                      int64_t cst, const int32_t* __restrict__ elems, int64_t eld,
                                                      const int32_t* __restrict__ e2n, const P2Rule R, const P2Coef cp,
                                                      double* __restrict__ K, double* __restrict__ M,
                                                      double* __restrict__ Kl, double* __restrict__ Ml) {
     using T = P2Topo<DIM>;
     constexpr int NV = T::NV, NLB = T::NLB;
+    __shared__ double Mst[NLB * (NLB + 1) / 2 * P2_BLOCK];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
         double x[NV][DIM];
@@ -182,53 +185,84 @@ __global__ void __launch_bounds__(128) p2_assemble_k(int64_t ne, const double* _
             cK[q] = R.w[q] * ad * cp.ka * exp(ek);
             cM[q] = cp.same ? cK[q] : R.w[q] * ad * cp.ma * exp(em);
         }
-        int32_t vid[NLB];
+        // Two passes over the points (M, then K), each with the unique entries b >= a
+        // of the element matrix in registers and the basis evaluated once per point
+        // (55 + 30 live doubles for K in 3D); the M entries wait in a thread-private
+        // shared-memory strip so each element-to-nnz position is loaded once and its
+        // K and M atomics go out together.
+        constexpr int NP = NLB * (NLB + 1) / 2;
+        double* mst = Mst + threadIdx.x;   // entry p at mst[p * blockDim.x]
+        if (M || Ml) {
+            double acc[NP];
 #pragma unroll
-        for (int k = 0; k < NLB; k++) vid[k] = __ldg(elems + k * eld + e);
-        (void)vid;
-#pragma unroll 1
-        for (int a = 0; a < NLB; a++) {
-            double rk[NLB], rm[NLB];
-#pragma unroll
-            for (int b = 0; b < NLB; b++) rk[b] = rm[b] = 0.0;
+            for (int p = 0; p < NP; p++) acc[p] = 0.0;
             for (int q = 0; q < R.nip; q++) {
-                double pa, ga[DIM];
-                p2_basis<DIM>(a, R.lam[q], gl, pa, ga);
+                double ph[NLB];
 #pragma unroll
-                for (int b = 0; b < NLB; b++) {
-                    if (b < a) continue;
-                    double pb, gb[DIM];
-                    p2_basis<DIM>(b, R.lam[q], gl, pb, gb);
-                    double d = ga[0] * gb[0];
+                for (int k = 0; k < NLB; k++) {
+                    double g[DIM];
+                    p2_basis<DIM>(k, R.lam[q], gl, ph[k], g);
+                }
+                int p = 0;
 #pragma unroll
-                    for (int c = 1; c < DIM; c++) d = fma(ga[c], gb[c], d);
-                    rk[b] = fma(cK[q], d, rk[b]);
-                    rm[b] = fma(cM[q], pa * pb, rm[b]);
+                for (int a = 0; a < NLB; a++) {
+                    const double ca = cM[q] * ph[a];
+#pragma unroll
+                    for (int b = a; b < NLB; b++, p++) acc[p] = fma(ca, ph[b], acc[p]);
                 }
             }
 #pragma unroll
-            for (int b = 0; b < NLB; b++) {
-                if (b < a) continue;
+            for (int p = 0; p < NP; p++) mst[p * P2_BLOCK] = acc[p];
+        }
+        double acc[NP];
+#pragma unroll
+        for (int p = 0; p < NP; p++) acc[p] = 0.0;
+        if (K || Kl) {
+            for (int q = 0; q < R.nip; q++) {
+                double g[NLB][DIM];
+#pragma unroll
+                for (int k = 0; k < NLB; k++) {
+                    double phi;
+                    p2_basis<DIM>(k, R.lam[q], gl, phi, g[k]);
+                }
+                int p = 0;
+#pragma unroll
+                for (int a = 0; a < NLB; a++)
+#pragma unroll
+                    for (int b = a; b < NLB; b++, p++) {
+                        double d = g[a][0] * g[b][0];
+#pragma unroll
+                        for (int c = 1; c < DIM; c++) d = fma(g[a][c], g[b][c], d);
+                        acc[p] = fma(cK[q], d, acc[p]);
+                    }
+            }
+        }
+        int p = 0;
+#pragma unroll
+        for (int a = 0; a < NLB; a++)
+#pragma unroll
+            for (int b = a; b < NLB; b++, p++) {
+                const double kv = acc[p];
+                const double mv = (M || Ml) ? mst[p * P2_BLOCK] : 0.0;
                 if (K || M) {
                     const int32_t pab = __ldcs(e2n + (int64_t)(a * NLB + b) * ne + e);
-                    if (K) atomicAdd(K + pab, rk[b]);
-                    if (M) atomicAdd(M + pab, rm[b]);
+                    if (K) atomicAdd(K + pab, kv);
+                    if (M) atomicAdd(M + pab, mv);
                     if (b != a) {
                         const int32_t pba = __ldcs(e2n + (int64_t)(b * NLB + a) * ne + e);
-                        if (K) atomicAdd(K + pba, rk[b]);
-                        if (M) atomicAdd(M + pba, rm[b]);
+                        if (K) atomicAdd(K + pba, kv);
+                        if (M) atomicAdd(M + pba, mv);
                     }
                 }
                 if (Kl) {
-                    stcs(Kl + (int64_t)(a + b * NLB) * ne + e, rk[b]);
-                    stcs(Kl + (int64_t)(b + a * NLB) * ne + e, rk[b]);
+                    stcs(Kl + (int64_t)(a + b * NLB) * ne + e, kv);
+                    if (b != a) stcs(Kl + (int64_t)(b + a * NLB) * ne + e, kv);
                 }
                 if (Ml) {
-                    stcs(Ml + (int64_t)(a + b * NLB) * ne + e, rm[b]);
-                    stcs(Ml + (int64_t)(b + a * NLB) * ne + e, rm[b]);
+                    stcs(Ml + (int64_t)(a + b * NLB) * ne + e, mv);
+                    if (b != a) stcs(Ml + (int64_t)(b + a * NLB) * ne + e, mv);
                 }
             }
-        }
     }
 }
 
@@ -267,9 +301,9 @@ extern "C" vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne, const doub
     cudaStream_t s = cs(stream);
     if ((K_vals || M_vals) && nnz > 0) zero2_p2_k<<<grid_for(nnz, 256, 8), 256, 0, s>>>(K_vals, M_vals, nnz);
     if (ne > 0 && (K_vals || M_vals || K_local || M_local)) {
-        unsigned g = grid_for(ne, 128, 8);
-        if (dim == 2) p2_assemble_k<2><<<g, 128, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, K_vals, M_vals, K_local, M_local);
-        else p2_assemble_k<3><<<g, 128, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, K_vals, M_vals, K_local, M_local);
+        unsigned g = grid_for(ne, P2_BLOCK, 8);
+        if (dim == 2) p2_assemble_k<2><<<g, P2_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, K_vals, M_vals, K_local, M_local);
+        else p2_assemble_k<3><<<g, P2_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, K_vals, M_vals, K_local, M_local);
     }
     return launch_check("fem_p2_assemble");
 }
