@@ -279,15 +279,23 @@ VB_API vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A,
                                   double* s, vb_stream_t stream);
 
 /* ---------------------------------------------------------- NEXT-3: P2 elements
- * Topological CSR pattern (as fem_p1_pattern, same two phases and
- * synchronisation) for elements with nv nodes, 2 <= nv <= 16 (P2: 6 in 2D, 10
- * in 3D; sparse() of P:1033-1036), with the nv^2-plane element-to-nnz map
- * elem2nnz (nullable).  Requires ne < 2^27.  No gather plan. */
+ * Topological CSR pattern (as fem_p1_pattern, same two phases, synchronisation
+ * and work-buffer reuse) for elements with nv nodes, 2 <= nv <= 16 (P2: 6 in
+ * 2D, 10 in 3D; sparse() of P:1033-1036).  Requires ne < 2^27.  Optional plans:
+ *   elem2nnz (nullable): the nv^2-plane element-to-nnz map (atomic scatter);
+ *   node_elem_ptr (nn+1) / node_elem (nv*ne, packed e*16 + a, ascending e per
+ *     node) / node_elem_slot (nullable; W = ceil(nv/4) uint32 words per
+ *     incidence, byte b of the W words = in-row offset of node b of the
+ *     element, natural order; rows must have <= 255 entries): the gather plan
+ *     of VB_ASSEMBLE_GATHER in fem_p2_assemble.  Given together or not at all
+ *     (node_elem_slot may be NULL). */
 VB_API vb_status fem_pattern(int nv, int64_t nn, int64_t ne,
                              const int32_t* elems, int64_t elem_ld,
                              void* work, size_t* work_bytes,
                              int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
-                             int32_t* elem2nnz, int64_t* nnz_out, vb_stream_t stream);
+                             int32_t* elem2nnz,
+                             int32_t* node_elem_ptr, int32_t* node_elem, uint32_t* node_elem_slot,
+                             int64_t* nnz_out, vb_stream_t stream);
 
 /* P2 stiffness and mass matrices (stiffness_matrixP2 / mass_matrixP2,
  * P:1009-1049) with c_K = cK_a exp(cK_b . x), c_M = cM_a exp(cM_b . x) (host
@@ -296,16 +304,25 @@ VB_API vb_status fem_pattern(int nv, int64_t nn, int64_t ne,
  * DESIGN.md §4).  elems: nlb = 6 (2D) / 10 (3D) node planes, vertices first,
  * then edge midpoints in the order (1,2),(2,3),(1,3) / (1,2),(1,3),(1,4),(2,3),
  * (2,4),(3,4); edges must be straight (midpoints exact).
- * K_vals/M_vals (nnz, nullable) are zero-filled and accumulated with fp64
- * atomics through elem2nnz from fem_pattern; K_local/M_local (nullable):
- * nlb x nlb page arrays (ld = ne). */
+ * mode VB_ASSEMBLE_ATOMIC: K_vals/M_vals (nnz, nullable) are zero-filled and
+ *   accumulated with fp64 atomics through elem2nnz (fem_pattern); work unused.
+ * mode VB_ASSEMBLE_GATHER: deterministic.  Call with work == NULL to query
+ *   *work_bytes (2 nlb^2 ne doubles + 16; nothing else happens).  The element
+ *   matrices are computed once into `work` (element-major), then one thread
+ *   per row sums its incidences' rows of them
+ *   in ascending element order (the oracle's order) and writes each CSR entry
+ *   once.  Needs row_ptr, node_elem_ptr, node_elem and node_elem_slot of
+ *   fem_pattern (elem2nnz unused).  Bitwise reproducible.
+ * K_local/M_local (nullable): nlb x nlb page arrays (ld = ne). */
 VB_API vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne,
                                  const double* coords, int64_t node_stride, int64_t comp_stride,
                                  const int32_t* elems, int64_t elem_ld,
-                                 const int32_t* elem2nnz, int64_t nnz,
+                                 const int32_t* row_ptr, const int32_t* elem2nnz, int64_t nnz,
+                                 const int32_t* node_elem_ptr, const int32_t* node_elem,
+                                 const uint32_t* node_elem_slot,
                                  int gqo, double cK_a, const double* cK_b, double cM_a, const double* cM_b,
                                  double* K_vals, double* M_vals, double* K_local, double* M_local,
-                                 vb_stream_t stream);
+                                 int mode, void* work, size_t* work_bytes, vb_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -109,19 +109,26 @@ __device__ __forceinline__ void p2_basis(int k, const double* lam, const double 
     }
 }
 
-constexpr int P2_BLOCK = 64;   // 55 x 64 doubles of M staging (28 KB static smem in 3D)
+constexpr int P2_BLOCK = 64;   // elements per block; 2 x 55 x 64 doubles of strips (56 KB in 3D)
 
 template <int DIM>
 __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
                                                      int64_t cst, const int32_t* __restrict__ elems, int64_t eld,
                                                      const int32_t* __restrict__ e2n, const P2Rule R, const P2Coef cp,
                                                      double* __restrict__ K, double* __restrict__ M,
-                                                     double* __restrict__ Kl, double* __restrict__ Ml) {
+                                                     double* __restrict__ Kl, double* __restrict__ Ml,
+                                                     double* __restrict__ Kst, double* __restrict__ Mst_g) {
     using T = P2Topo<DIM>;
     constexpr int NV = T::NV, NLB = T::NLB;
-    __shared__ double Mst[NLB * (NLB + 1) / 2 * P2_BLOCK];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+    constexpr int NP = NLB * (NLB + 1) / 2;   // unique entries b >= a (odd: 21 / 55)
+    extern __shared__ double p2_smem[];       // thread-private strips [tid][NP]: M, then K (staging)
+    double* MS = p2_smem;
+    double* KS = p2_smem + P2_BLOCK * NP;
+    const int64_t stride = (int64_t)gridDim.x * P2_BLOCK;
+    for (int64_t base = (int64_t)blockIdx.x * P2_BLOCK; base < ne; base += stride) {
+        const int64_t e = base + threadIdx.x;
+        const bool active = e < ne;
+        if (active) {
         double x[NV][DIM];
 #pragma unroll
         for (int a = 0; a < NV; a++) {
@@ -190,9 +197,8 @@ __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const doub
         // (55 + 30 live doubles for K in 3D); the M entries wait in a thread-private
         // shared-memory strip so each element-to-nnz position is loaded once and its
         // K and M atomics go out together.
-        constexpr int NP = NLB * (NLB + 1) / 2;
-        double* mst = Mst + threadIdx.x;   // entry p at mst[p * blockDim.x]
-        if (M || Ml) {
+        double* mst = MS + threadIdx.x * NP;   // entry p at mst[p] (odd stride: 2-way conflicts at most)
+        if (M || Ml || Mst_g) {
             double acc[NP];
 #pragma unroll
             for (int p = 0; p < NP; p++) acc[p] = 0.0;
@@ -212,12 +218,12 @@ __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const doub
                 }
             }
 #pragma unroll
-            for (int p = 0; p < NP; p++) mst[p * P2_BLOCK] = acc[p];
+            for (int p = 0; p < NP; p++) mst[p] = acc[p];
         }
         double acc[NP];
 #pragma unroll
         for (int p = 0; p < NP; p++) acc[p] = 0.0;
-        if (K || Kl) {
+        if (K || Kl || Kst) {
             for (int q = 0; q < R.nip; q++) {
                 double g[NLB][DIM];
 #pragma unroll
@@ -243,7 +249,7 @@ __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const doub
 #pragma unroll
             for (int b = a; b < NLB; b++, p++) {
                 const double kv = acc[p];
-                const double mv = (M || Ml) ? mst[p * P2_BLOCK] : 0.0;
+                const double mv = (M || Ml || Mst_g) ? mst[p] : 0.0;
                 if (K || M) {
                     const int32_t pab = __ldcs(e2n + (int64_t)(a * NLB + b) * ne + e);
                     if (K) atomicAdd(K + pab, kv);
@@ -262,7 +268,110 @@ __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const doub
                     stcs(Ml + (int64_t)(a + b * NLB) * ne + e, mv);
                     if (b != a) stcs(Ml + (int64_t)(b + a * NLB) * ne + e, mv);
                 }
+                if (Kst) KS[threadIdx.x * NP + p] = kv;
             }
+        }
+        if (Kst || Mst_g) {
+            // gather staging: element-major full matrices (row a of element e contiguous),
+            // written cooperatively by the block from the strips -> coalesced stores
+            __syncthreads();
+            const int nact = (int)(ne - base < P2_BLOCK ? ne - base : P2_BLOCK);
+            constexpr int NN = NLB * NLB;
+            double2* out = reinterpret_cast<double2*>(Kst);   // (K, M) pairs, [e][a][b]
+            for (int j = 0; j < nact; j++)
+                for (int r = threadIdx.x; r < NN; r += P2_BLOCK) {
+                    const int a = r / NLB, b = r - a * NLB;
+                    const int lo = a < b ? a : b, hi = a < b ? b : a;
+                    const int pp = lo * NLB - lo * (lo - 1) / 2 + (hi - lo);
+                    __stcs(out + (base + j) * NN + r, make_double2(KS[j * NP + pp], MS[j * NP + pp]));
+                }
+            __syncthreads();
+        }
+    }
+}
+
+// Deterministic P2 assembly, phase 2: one thread per row v sums, in ascending
+// element order, row a of the staged K_e / M_e of each incidence (e, a) into
+// per-slot accumulators ([slot][lane] in shared memory, rows of up to P2_RS
+// entries; longer rows accumulate in place in HBM), then writes the row once.
+constexpr int P2_RS = 72;
+constexpr int P2_GROWS = 32;
+constexpr int P2_U = 4;
+
+template <int NLB>
+__global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_t* __restrict__ row_ptr,
+                                                        const int32_t* __restrict__ nptr,
+                                                        const int32_t* __restrict__ nelem,
+                                                        const uint32_t* __restrict__ nslot,
+                                                        const double2* __restrict__ KMst,
+                                                        double* __restrict__ K, double* __restrict__ M) {
+    constexpr int NW = (NLB + 3) / 4;
+    constexpr int ST = P2_RS + 1;   // [lane][slot] rows of odd length: the cooperative write-back is conflict-free
+    __shared__ double2 acc_s[ST * P2_GROWS];
+    const int t = threadIdx.x;
+    double2* acc = acc_s + t * ST;
+    for (int64_t v0 = (int64_t)blockIdx.x * P2_GROWS; v0 < nn; v0 += (int64_t)gridDim.x * P2_GROWS) {
+        const int64_t v = v0 + t;
+        const bool own = v < nn;
+        const int lo = own ? __ldg(row_ptr + v) : 0, L = own ? __ldg(row_ptr + v + 1) - lo : 0;
+        const int i0 = own ? __ldg(nptr + v) : 0, i1 = own ? __ldg(nptr + v + 1) : 0;
+        const bool fast = L <= P2_RS;
+        if (fast) {
+            for (int s = 0; s < L; s++) acc[s] = make_double2(0.0, 0.0);
+        } else {
+            for (int s = 0; s < L; s++) {
+                if (K) K[lo + s] = 0.0;
+                if (M) M[lo + s] = 0.0;
+            }
+        }
+        // P2_U incidences in flight: their element ids, then their rows and slot words
+        // are loaded before any is accumulated (the accumulation order stays ascending)
+        auto add = [&](const uint32_t (&w)[NW], const double2 (&km)[NLB]) {
+#pragma unroll
+            for (int b = 0; b < NLB; b++) {
+                const int sl = (w[b / 4] >> (8 * (b % 4))) & 0xff;
+                if (fast) {
+                    double2 x = acc[sl];
+                    x.x += km[b].x;
+                    x.y += km[b].y;
+                    acc[sl] = x;
+                } else {
+                    if (K) K[lo + sl] += km[b].x;
+                    if (M) M[lo + sl] += km[b].y;
+                }
+            }
+        };
+        for (int i = i0; i < i1; i += P2_U) {
+            int32_t ea[P2_U];
+#pragma unroll
+            for (int u = 0; u < P2_U; u++) ea[u] = i + u < i1 ? __ldg(nelem + i + u) : -1;
+            uint32_t w[P2_U][NW];
+            double2 km[P2_U][NLB];
+#pragma unroll
+            for (int u = 0; u < P2_U; u++) {
+                if (ea[u] < 0) continue;
+                const double2* row = KMst + (int64_t)(ea[u] >> 4) * (NLB * NLB) + (ea[u] & 15) * NLB;
+#pragma unroll
+                for (int j = 0; j < NW; j++) w[u][j] = __ldg(nslot + (int64_t)(i + u) * NW + j);
+#pragma unroll
+                for (int b = 0; b < NLB; b++) km[u][b] = __ldcs(row + b);
+            }
+#pragma unroll
+            for (int u = 0; u < P2_U; u++)
+                if (ea[u] >= 0) add(w[u], km[u]);
+        }
+        // write-back: the warp stores each staged row in turn, lane j writing entry j
+        __syncwarp();
+        for (int r = 0; r < P2_GROWS; r++) {
+            const int Lr = __shfl_sync(0xffffffffu, fast ? L : 0, r);
+            const int lor = __shfl_sync(0xffffffffu, lo, r);
+            for (int j = t; j < Lr; j += P2_GROWS) {
+                const double2 x = acc_s[r * ST + j];
+                if (K) stcs(K + lor + j, x.x);
+                if (M) stcs(M + lor + j, x.y);
+            }
+        }
+        __syncwarp();
     }
 }
 
@@ -281,17 +390,39 @@ using namespace vb;
 
 extern "C" vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
                                      int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
-                                     const int32_t* elem2nnz, int64_t nnz, int gqo, double cK_a, const double* cK_b,
+                                     const int32_t* row_ptr, const int32_t* elem2nnz, int64_t nnz,
+                                     const int32_t* node_elem_ptr, const int32_t* node_elem,
+                                     const uint32_t* node_elem_slot, int gqo, double cK_a, const double* cK_b,
                                      double cM_a, const double* cM_b, double* K_vals, double* M_vals, double* K_local,
-                                     double* M_local, vb_stream_t stream) {
+                                     double* M_local, int mode, void* work, size_t* work_bytes, vb_stream_t stream) {
     clear_error();
-    if (dim != 2 && dim != 3) { set_error("fem_p2_assemble: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
-    if (nn < 0 || ne < 0 || nnz < 0) { set_error("fem_p2_assemble: negative size"); return VB_ERR_ARG; }
+    const char* fn = "fem_p2_assemble";
+    if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
+    if (nn < 0 || ne < 0 || nnz < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
+    if (mode != VB_ASSEMBLE_ATOMIC && mode != VB_ASSEMBLE_GATHER) { set_error("%s: unknown mode %d", fn, mode); return VB_ERR_ARG; }
+    const int nlb = dim == 2 ? 6 : 10;
+    const bool want_global = K_vals || M_vals;
+    const size_t wbytes = (size_t)2 * nlb * nlb * (size_t)ne * 8 + 16;
+    if (mode == VB_ASSEMBLE_GATHER && !work) {   // size query (CUB convention)
+        if (!work_bytes) { set_error("%s: gather mode: work and work_bytes both NULL", fn); return VB_ERR_ARG; }
+        *work_bytes = wbytes;
+        return VB_OK;
+    }
     P2Rule R;
-    if (!p2_rule(dim, gqo, R)) { set_error("fem_p2_assemble: gqo=%d unsupported (1, 2, 4)", gqo); return VB_ERR_UNSUPPORTED; }
-    if (ne > 0 && (!coords || !elems)) { set_error("fem_p2_assemble: NULL coords or elems"); return VB_ERR_ARG; }
-    if ((K_vals || M_vals) && !elem2nnz) { set_error("fem_p2_assemble: K/M need elem2nnz (fem_pattern)"); return VB_ERR_ARG; }
-    if (elem_ld < ne) { set_error("fem_p2_assemble: elem_ld < ne"); return VB_ERR_ARG; }
+    if (!p2_rule(dim, gqo, R)) { set_error("%s: gqo=%d unsupported (1, 2, 4)", fn, gqo); return VB_ERR_UNSUPPORTED; }
+    if (ne > 0 && (!coords || !elems)) { set_error("%s: NULL coords or elems", fn); return VB_ERR_ARG; }
+    if (elem_ld < ne) { set_error("%s: elem_ld < ne", fn); return VB_ERR_ARG; }
+    if (mode == VB_ASSEMBLE_ATOMIC && want_global && !elem2nnz) { set_error("%s: atomic mode needs elem2nnz (fem_pattern)", fn); return VB_ERR_ARG; }
+    if (mode == VB_ASSEMBLE_GATHER && want_global) {
+        if (!row_ptr || !node_elem_ptr || !node_elem || !node_elem_slot) {
+            set_error("%s: gather mode needs row_ptr, node_elem_ptr, node_elem, node_elem_slot", fn);
+            return VB_ERR_ARG;
+        }
+        if (work_bytes && *work_bytes < wbytes) {
+            set_error("%s: work buffer too small (%zu < %zu)", fn, *work_bytes, wbytes);
+            return VB_ERR_WORKSPACE;
+        }
+    }
     P2Coef cp{cK_a, {0, 0, 0}, cM_a, {0, 0, 0}, false};
     for (int c = 0; c < dim; c++) {
         cp.kb[c] = cK_b ? cK_b[c] : 0.0;
@@ -299,11 +430,31 @@ extern "C" vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne, const doub
     }
     cp.same = cK_a == cM_a && cp.kb[0] == cp.mb[0] && cp.kb[1] == cp.mb[1] && cp.kb[2] == cp.mb[2];
     cudaStream_t s = cs(stream);
-    if ((K_vals || M_vals) && nnz > 0) zero2_p2_k<<<grid_for(nnz, 256, 8), 256, 0, s>>>(K_vals, M_vals, nnz);
-    if (ne > 0 && (K_vals || M_vals || K_local || M_local)) {
+    const bool gather = mode == VB_ASSEMBLE_GATHER && want_global;
+    // gather staging: (K, M) pairs of the full element matrices, element-major
+    double* Kst = gather ? reinterpret_cast<double*>(work) : nullptr;
+    double* Mst = Kst;   // non-null: the M pass runs (its strip feeds the pairs)
+    double* Ka = gather ? nullptr : K_vals;
+    double* Ma = gather ? nullptr : M_vals;
+    if ((Ka || Ma) && nnz > 0) zero2_p2_k<<<grid_for(nnz, 256, 8), 256, 0, s>>>(Ka, Ma, nnz);
+    if (ne > 0 && (Ka || Ma || K_local || M_local || Kst || Mst)) {
         unsigned g = grid_for(ne, P2_BLOCK, 8);
-        if (dim == 2) p2_assemble_k<2><<<g, P2_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, K_vals, M_vals, K_local, M_local);
-        else p2_assemble_k<3><<<g, P2_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, K_vals, M_vals, K_local, M_local);
+        const size_t sm2 = (size_t)2 * P2_BLOCK * 21 * 8, sm3 = (size_t)2 * P2_BLOCK * 55 * 8;
+        static bool attr = false;   // > 48 KB dynamic shared memory needs an opt-in
+        if (!attr) {
+            cudaFuncSetAttribute(p2_assemble_k<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+            attr = true;
+        }
+        if (dim == 2) p2_assemble_k<2><<<g, P2_BLOCK, sm2, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, Ka, Ma, K_local, M_local, Kst, Mst);
+        else p2_assemble_k<3><<<g, P2_BLOCK, sm3, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, Ka, Ma, K_local, M_local, Kst, Mst);
     }
-    return launch_check("fem_p2_assemble");
+    if (gather && nn > 0) {
+        const int64_t need = (nn + P2_GROWS - 1) / P2_GROWS;
+        const int64_t cap = (int64_t)sm_count() * 6;   // 37 KB of accumulators per warp-CTA
+        const unsigned g = (unsigned)(need < cap ? need : cap);
+        const double2* km = reinterpret_cast<const double2*>(work);
+        if (dim == 2) p2_gather_k<6><<<g, P2_GROWS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem, node_elem_slot, km, K_vals, M_vals);
+        else p2_gather_k<10><<<g, P2_GROWS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem, node_elem_slot, km, K_vals, M_vals);
+    }
+    return launch_check(fn);
 }

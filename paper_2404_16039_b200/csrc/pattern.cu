@@ -167,20 +167,42 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
             if (ea[k] < 0) break;
             int64_t e = ea[k] >> SH;
             int a = ea[k] & (NVM - 1);
-            // byte 0: in-row offset of the row's own vertex (the diagonal); bytes
-            // 1..nv-1: offsets of the element's other vertices, ascending local index
-            uint32_t packed = 0;
-            int byte = 1;
+            if constexpr (SH == 2) {
+                // P1: byte 0: in-row offset of the row's own vertex (the diagonal);
+                // bytes 1..nv-1: offsets of the element's other vertices, ascending b
+                uint32_t packed = 0;
+                int byte = 1;
 #pragma unroll
-            for (int b = 0; b < NVM; b++) {
-                if (b >= nv) break;
-                int pos = lower_bound_s(L, st, cnt, w[k][b]);
-                VB_CHECK(pos < cnt && L[pos * st] == w[k][b]);   // every vertex is in the row
-                if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
-                int sh = (b == a) ? 0 : 8 * byte++;
-                if (sh < 32) packed |= (uint32_t)(pos & 0xff) << sh;
+                for (int b = 0; b < NVM; b++) {
+                    if (b >= nv) break;
+                    int pos = lower_bound_s(L, st, cnt, w[k][b]);
+                    VB_CHECK(pos < cnt && L[pos * st] == w[k][b]);   // every vertex is in the row
+                    if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
+                    int sh = (b == a) ? 0 : 8 * byte++;
+                    if (sh < 32) packed |= (uint32_t)(pos & 0xff) << sh;
+                }
+                if (slots) slots[i0 + k] = packed;
+            } else {
+                // generic: byte b (word b / 4) = in-row offset of node b, natural order
+                constexpr int NW = NVM / 4;
+                uint32_t packed[NW];
+#pragma unroll
+                for (int j = 0; j < NW; j++) packed[j] = 0;
+#pragma unroll
+                for (int b = 0; b < NVM; b++) {
+                    if (b >= nv) break;
+                    int pos = lower_bound_s(L, st, cnt, w[k][b]);
+                    VB_CHECK(pos < cnt && L[pos * st] == w[k][b]);
+                    if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
+                    packed[b / 4] |= (uint32_t)(pos & 0xff) << (8 * (b % 4));
+                }
+                if (slots) {
+                    const int nw = (nv + 3) / 4;
+#pragma unroll
+                    for (int j = 0; j < NW; j++)
+                        if (j < nw) slots[(int64_t)(i0 + k) * nw + j] = packed[j];
+                }
             }
-            if (slots) slots[i0 + k] = packed;
         }
     }
 }
@@ -438,9 +460,10 @@ extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32
 
 extern "C" vb_status fem_pattern(int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld, void* work,
                                  size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
-                                 int32_t* elem2nnz, int64_t* nnz_out, vb_stream_t stream) {
+                                 int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem,
+                                 uint32_t* node_elem_slot, int64_t* nnz_out, vb_stream_t stream) {
     clear_error();
     if (nv < 2 || nv > 16) { set_error("fem_pattern: nv=%d, need 2..16 nodes per element", nv); return VB_ERR_UNSUPPORTED; }
     return pattern_impl<4, 128, 64>("fem_pattern", nv, nn, ne, elems, elem_ld, work, work_bytes, row_ptr, col_idx,
-                                    col_cap, elem2nnz, nullptr, nullptr, nullptr, nnz_out, stream);
+                                    col_cap, elem2nnz, node_elem_ptr, node_elem, node_elem_slot, nnz_out, stream);
 }

@@ -67,9 +67,9 @@ def lib():
             "vb_quad_rule": (i32, [i32, i32, p, p]),
             "fem_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p, p, p, i32, p]),
             "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
-            "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, C.POINTER(C.c_int64), p]),
-            "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, i64, i32, d, p, d, p, p, p, p, p,
-                                      p]),
+            "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
+            "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
+                                      p, p, p, p, i32, p, sz, p]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -348,9 +348,11 @@ def vb_page_bilinear(A, Mx, B, s=None, stream=None):
 
 # ------------------------------------------------------------------ NEXT-3 (P2)
 class Plan:
-    """Generic CSR pattern + scatter map (fem_pattern) for elements with any node count."""
+    """Generic CSR pattern (fem_pattern) for elements with any node count, with
+    the scatter map (elem2nnz) and / or the gather plan (node_elem_ptr,
+    node_elem, node_elem_slot: ceil(nv/4) words per incidence)."""
 
-    def __init__(self, elems, nn, scatter_map=True, stream=None):
+    def __init__(self, elems, nn, scatter_map=True, gather_plan=True, stream=None):
         if elems.dtype != torch.int32:
             raise TypeError("elems must be int32")
         nv, ne = elems.shape
@@ -360,26 +362,38 @@ class Plan:
         sz = C.c_size_t(0)
         nnz = C.c_int64(0)
         st = _stream(stream)
-        _check(L.fem_pattern(nv, nn, ne, None, ne, None, C.byref(sz), None, None, 0, None, None, st))
+        _check(L.fem_pattern(nv, nn, ne, None, ne, None, C.byref(sz), None, None, 0, None, None, None, None, None, st))
         work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
         self.row_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
         _check(L.fem_pattern(nv, nn, ne, _ptr(elems), ne, _ptr(work), C.byref(sz), _ptr(self.row_ptr), None, 0, None,
-                             C.byref(nnz), st))
+                             None, None, None, C.byref(nnz), st))
         self.nnz = int(nnz.value)
         col = torch.zeros((max(4, (self.nnz + 3) // 4 * 4),), dtype=torch.int32, device=dev)
         self.elem2nnz = torch.empty((nv * nv, ne), dtype=torch.int32, device=dev) if scatter_map else None
+        if gather_plan:
+            self.slot_words = (nv + 3) // 4
+            self.node_elem_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
+            self.node_elem = torch.empty((max(nv * ne, 1),), dtype=torch.int32, device=dev)
+            self.node_elem_slot = torch.empty((max(nv * ne * self.slot_words, 1),), dtype=torch.int32, device=dev)
+        else:
+            self.slot_words = 0
+            self.node_elem_ptr = self.node_elem = self.node_elem_slot = None
         _check(L.fem_pattern(nv, nn, ne, _ptr(elems), ne, _ptr(work), C.byref(sz), _ptr(self.row_ptr), _ptr(col),
-                             col.numel(), _ptr(self.elem2nnz), C.byref(nnz), st))
+                             col.numel(), _ptr(self.elem2nnz), _ptr(self.node_elem_ptr), _ptr(self.node_elem),
+                             _ptr(self.node_elem_slot), C.byref(nnz), st))
         self.col_idx = col[:self.nnz]
 
 
-def fem_pattern(elems, nn, scatter_map=True, stream=None):
-    return Plan(elems, nn, scatter_map, stream)
+def fem_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
+    return Plan(elems, nn, scatter_map, gather_plan, stream)
 
 
 def fem_p2_assemble(coords, elems, plan, gqo=4, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0)),
-                    want_K=True, want_M=True, want_local=False, K=None, M=None, stream=None):
-    """P2 stiffness / mass (NEXT-3).  Returns (K_vals, M_vals, K_local, M_local)."""
+                    mode=VB_ASSEMBLE_ATOMIC, want_K=True, want_M=True, want_local=False, K=None, M=None,
+                    stream=None):
+    """P2 stiffness / mass (NEXT-3).  mode VB_ASSEMBLE_ATOMIC (needs the plan's
+    elem2nnz) or VB_ASSEMBLE_GATHER (deterministic; needs its gather plan).
+    Returns (K_vals, M_vals, K_local, M_local)."""
     _f64(coords)
     dim, nn = coords.shape
     nlb, ne = elems.shape
@@ -390,7 +404,16 @@ def fem_p2_assemble(coords, elems, plan, gqo=4, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1
     Ml = torch.empty((nlb, nlb, ne), dtype=torch.float64, device=dev) if want_local else None
     kb = (C.c_double * 3)(*(list(map(float, cK[1]))[:3] + [0.0] * (3 - len(list(cK[1])[:3]))))
     mb = (C.c_double * 3)(*(list(map(float, cM[1]))[:3] + [0.0] * (3 - len(list(cM[1])[:3]))))
-    _check(lib().fem_p2_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.elem2nnz), plan.nnz,
-                                 int(gqo), float(cK[0]), C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p),
-                                 _ptr(K), _ptr(M), _ptr(Kl), _ptr(Ml), _stream(stream)))
+    L = lib()
+    work, sz = None, C.c_size_t(0)
+    if mode == VB_ASSEMBLE_GATHER:
+        _check(L.fem_p2_assemble(dim, nn, ne, None, 1, nn, None, ne, None, None, plan.nnz, None, None, None,
+                                 int(gqo), 0.0, None, 0.0, None, None, None, None, None, mode, None, C.byref(sz),
+                                 None))
+        work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
+    _check(L.fem_p2_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
+                             _ptr(plan.elem2nnz), plan.nnz, _ptr(plan.node_elem_ptr), _ptr(plan.node_elem),
+                             _ptr(plan.node_elem_slot), int(gqo), float(cK[0]), C.cast(kb, C.c_void_p),
+                             float(cM[0]), C.cast(mb, C.c_void_p), _ptr(K), _ptr(M), _ptr(Kl), _ptr(Ml), int(mode),
+                             _ptr(work), C.byref(sz), _stream(stream)))
     return K, M, Kl, Ml

@@ -13,6 +13,7 @@ import synth
 from paper_2404_16039_b200 import vb
 
 pytestmark = pytest.mark.gpu
+MODES = [vb.VB_ASSEMBLE_ATOMIC, vb.VB_ASSEMBLE_GATHER]
 COEFS = [((1.0, (1.0, 1.0, 1.0)), (1.0, (1.0, 1.0, 1.0))),
          ((2.0, (0.4, -0.3, 0.2)), (0.5, (-0.6, 0.1, 0.8)))]
 
@@ -56,19 +57,35 @@ def test_generic_pattern_bit_exact(dev, dim, n):
             p = e2n[a * nlb + b]
             assert np.all(ci[p] == elems[b])
             assert np.all((p >= rp[elems[a]]) & (p < rp[elems[a] + 1]))
+    # gather plan: incidences ascending e per node; slot bytes = in-row offsets, natural order
+    nptr, nel = h(plan.node_elem_ptr), h(plan.node_elem)
+    W = plan.slot_words
+    nsl = h(plan.node_elem_slot).view(np.uint32).reshape(-1, W)
+    for v in range(0, nn, max(1, nn // 61)):
+        inc = nel[nptr[v]:nptr[v + 1]]
+        e, a = inc >> 4, inc & 15
+        assert np.all(np.diff(e) > 0) and np.all(elems[a, e] == v)
+        assert len(inc) == np.count_nonzero(elems == v)
+        for k, ee in enumerate(e):
+            words = nsl[nptr[v] + k]
+            for b in range(nlb):
+                off = (int(words[b // 4]) >> (8 * (b % 4))) & 0xFF
+                assert ci[rp[v] + off] == elems[b, ee]
 
 
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("coef", [0, 1])
 @pytest.mark.parametrize("gqo", [2, 4])
 @pytest.mark.parametrize("dim,n", [(2, 12), (3, 4)])
-def test_p2_assembly_parity(dev, dim, n, gqo, coef):
+def test_p2_assembly_parity(dev, dim, n, gqo, coef, mode):
     coords, elems = p2_mesh(dim, n, jitter=0.1 if dim == 2 else 0.05, seed=3)
     cK, cM = COEFS[coef]
     nn = coords.shape[1]
     rp, ci = oracle.pattern(elems, nn)
     Ko, Mo = oracle.p2_assemble_coef(coords, elems, rp, ci, gqo=gqo, cK=cK, cM=cM)
     plan = vb.Plan(g(elems, dev), nn)
-    K, M, Kl, Ml = vb.fem_p2_assemble(g(coords, dev), g(elems, dev), plan, gqo=gqo, cK=cK, cM=cM, want_local=True)
+    K, M, Kl, Ml = vb.fem_p2_assemble(g(coords, dev), g(elems, dev), plan, gqo=gqo, cK=cK, cM=cM, want_local=True,
+                                      mode=mode)
     assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
     Kl, Ml = h(Kl), h(Ml)
     for e in (0, 11, elems.shape[1] - 1):
@@ -81,8 +98,31 @@ def within_last_digit(x, printed, units=1.0):
     return abs(x - printed) <= units * 10 ** (e - 2) * 1.0001
 
 
+def test_p2_gather_bitwise_reproducible_and_unstructured(dev):
+    """Gather mode: identical bits on every call; Delaunay P2 meshes in a random
+    numbering (rows longer than the 72-entry shared-memory budget included)."""
+    coords, elems = synth.p2_from_p1(*synth.permute_mesh(*synth.delaunay_p1(3, 5, seed=2), seed=3))
+    nn = coords.shape[1]
+    rp, ci = oracle.pattern(elems, nn)
+    assert np.diff(rp).max() > 72
+    Ko, Mo = oracle.p2_assemble_coef(coords, elems, rp, ci, gqo=4, cK=COEFS[1][0], cM=COEFS[1][1])
+    plan = vb.Plan(g(elems, dev), nn)
+    cd, ed = g(coords, dev), g(elems, dev)
+    K1, M1, _, _ = vb.fem_p2_assemble(cd, ed, plan, gqo=4, cK=COEFS[1][0], cM=COEFS[1][1], mode=vb.VB_ASSEMBLE_GATHER)
+    K1, M1 = h(K1), h(M1)
+    assert relmax(K1, Ko) <= 1e-12 and relmax(M1, Mo) <= 1e-12
+    for _ in range(2):
+        K2, M2, _, _ = vb.fem_p2_assemble(cd, ed, plan, gqo=4, cK=COEFS[1][0], cM=COEFS[1][1],
+                                          mode=vb.VB_ASSEMBLE_GATHER)
+        assert np.array_equal(h(K2), K1) and np.array_equal(h(M2), M1)
+    Ka, Ma, _, _ = vb.fem_p2_assemble(cd, ed, plan, gqo=4, cK=COEFS[1][0], cM=COEFS[1][1],
+                                      mode=vb.VB_ASSEMBLE_ATOMIC)
+    assert relmax(h(Ka), Ko) <= 1e-12 and relmax(h(Ma), Mo) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", MODES)
 @pytest.mark.parametrize("dim,level", [(2, 6), (3, 4), (3, 5), (3, 6)])
-def test_paper_p2_tables_on_gpu(dev, golden, dim, level):
+def test_paper_p2_tables_on_gpu(dev, golden, dim, level, mode):
     # (2D level 7, e_K = 3.67e-9 against I_K = 14.56, sits at the round-off floor of
     # the quadratic form: the 1e-12 entrywise agreement does not fix its third digit)
     g1, g2 = golden("paper_tables_p1.json"), golden("paper_tables_p2.json")
@@ -95,7 +135,7 @@ def test_paper_p2_tables_on_gpu(dev, golden, dim, level):
         v = np.cos(np.pi * coords[0]) * np.cos(np.pi * coords[1]) * np.cos(np.pi * coords[2])
     assert coords.shape[1] == row["size"]
     plan = vb.Plan(g(elems, dev), coords.shape[1])
-    K, M, _, _ = vb.fem_p2_assemble(g(coords, dev), g(elems, dev), plan, gqo=4)
+    K, M, _, _ = vb.fem_p2_assemble(g(coords, dev), g(elems, dev), plan, gqo=4, mode=mode)
     rp, ci = h(plan.row_ptr), h(plan.col_idx)
     rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
     eK = abs(math.fsum(v[rows] * h(K) * v[ci]) - g1["I_K_%dd" % dim])

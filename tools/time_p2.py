@@ -30,5 +30,7 @@ def t(fn, reps=10):
 
 K, M, _, _ = vb.fem_p2_assemble(cd, ed, plan)
 print("%s P2 L6 (ne=%d): global K+M %.3f ms" % (tag, e.shape[1], t(lambda: vb.fem_p2_assemble(cd, ed, plan, K=K, M=M))))
+G = vb.VB_ASSEMBLE_GATHER
+print("%s P2 L6: gather K+M %.3f ms" % (tag, t(lambda: vb.fem_p2_assemble(cd, ed, plan, K=K, M=M, mode=G))))
 print("%s P2 L6: K only %.3f ms" % (tag, t(lambda: vb.fem_p2_assemble(cd, ed, plan, want_M=False, K=K))))
 print("%s P2 L6: local only %.3f ms" % (tag, t(lambda: vb.fem_p2_assemble(cd, ed, plan, want_K=False, want_M=False, want_local=True))))
