@@ -401,10 +401,12 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     p2p = vb.Plan(ed2, c2_.shape[1])
     K2 = torch.empty(p2p.nnz, dtype=torch.float64, device=dev)
     M2 = torch.empty(p2p.nnz, dtype=torch.float64, device=dev)
-    rec("NEXT-3 paper tab:KM_P2_3D level 6, P2, c=exp(x+y+z), gqo=4, atomic (paper: K 87.6 s + M 16.4 s, MATLAB, "
-        "hardware not stated)", e2_.shape[1], "elements",
-        c2_.shape[1] * 24 + e2_.size * 4 + e2_.shape[1] * 100 * 4 + 2 * p2p.nnz * 8 * 3,
-        time_kernel(lambda: vb.fem_p2_assemble(cd2, ed2, p2p, gqo=4, K=K2, M=M2), 5))
+    # ALG bytes: coords + elems read, K and M written once (as the P1 rows)
+    for name, mode in (("gather", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+        rec("NEXT-3 paper tab:KM_P2_3D level 6, P2, c=exp(x+y+z), gqo=4, variant=%s (paper: K 87.6 s + M 16.4 s, "
+            "MATLAB, hardware not stated)" % name, e2_.shape[1], "elements",
+            c2_.shape[1] * 24 + e2_.size * 4 + 2 * p2p.nnz * 8,
+            time_kernel(lambda: vb.fem_p2_assemble(cd2, ed2, p2p, gqo=4, K=K2, M=M2, mode=mode), 5))
     del p2p, K2, M2, cd2, ed2
     # config 4: 2D at scale
     c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
