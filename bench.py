@@ -137,7 +137,8 @@ def load_traffic(kernel_key):
     try:
         with open(path) as f:
             d = json.load(f)
-        for k in (kernel_key, kernel_key.replace(">", ", 0>")):      # template spelling of later captures
+        # newest capture first: the c = 1 instantiation is <d, 0, 0> (COEF, FAC), older <d, 0> / <d>
+        for k in (kernel_key.replace(">", ", 0, 0>"), kernel_key.replace(">", ", 0>"), kernel_key):
             if k in d["kernels"]:
                 return d["kernels"][k]["dram_bytes_per_launch"]
         return None
