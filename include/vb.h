@@ -184,6 +184,14 @@ VB_API vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne,
                          int32_t* node_elem_ptr, int32_t* node_elem, uint32_t* node_elem_slot,
                          int64_t* nnz_out, vb_stream_t stream);
 
+/* Plan statistics for choosing the gather kernel's shared-memory budget
+ * (VB_GATHER_HINT_COMPACT): stats_out (HOST, 3 values) = maximum row length,
+ * maximum CSR entries of a 32-row block, maximum incidences of a 32-row block
+ * (node_elem_ptr nullable: then 0).  work: DEVICE scratch of >= 16 bytes.
+ * Synchronises the stream. */
+VB_API vb_status fem_plan_stats(int64_t nn, const int32_t* row_ptr, const int32_t* node_elem_ptr, void* work,
+                                int64_t* stats_out, vb_stream_t stream);
+
 /* ---------------------------------------------------------- a7..a17 assembly
  * Global P1 stiffness and mass matrices with c_K = c_M = 1 (eq:K_M P:967-975,
  * stiffness_matrixP1 P:978-1004, mass_matrixP1 P:1007), written
@@ -211,6 +219,13 @@ VB_API vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne,
  * Degenerate elements (det = 0) propagate inf/nan. */
 #define VB_ASSEMBLE_ATOMIC 0
 #define VB_ASSEMBLE_GATHER 1
+/* Hint OR'ed into a gather mode (3D; ignored otherwise): every 32-row block of
+ * the plan has rows of <= 15 columns, <= 16*32 CSR entries and <= 25*32
+ * incidences (fem_p1_pattern's stats_out tells; Kuhn cubes qualify).  The
+ * kernel then runs with a smaller shared-memory budget (8 instead of 7 CTAs
+ * per SM).  Blocks or rows that do not fit it are still assembled correctly
+ * (in place in HBM), only slower. */
+#define VB_GATHER_HINT_COMPACT 0x100
 VB_API vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne,
                           const double* coords, int64_t node_stride, int64_t comp_stride,
                           const int32_t* elems, int64_t elem_ld,

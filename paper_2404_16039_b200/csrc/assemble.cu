@@ -252,16 +252,24 @@ constexpr int GATHER_ROWS = 32;
 #ifndef VB_GATHER_OVF2
 #define VB_GATHER_OVF2 32
 #endif
-template <int DIM, int NC = DIM>   // NC doubles staged per column slot: coordinates (+ coefficient factors)
+// BUD = 1: the compact budget for meshes whose 32-row blocks all have rows of <= 15
+// columns, <= 16*32 CSR entries and <= 25*32 incidences (Kuhn cubes; fem_p1_pattern
+// reports the plan's maxima, the caller passes VB_GATHER_HINT_COMPACT): 8 instead
+// of 7 CTAs per SM in 3D.  Blocks that do not fit stay correct (in-place path).
+template <int DIM, int NC = DIM, int BUD = 0>   // NC doubles staged per column slot: coordinates (+ coefficient factors)
 struct GatherCfg {
-    static constexpr int RS = DIM == 2 ? VB_GATHER_RS2 : VB_GATHER_RS3;  // columns per row in the lane arrays
-    static constexpr int OVF = DIM == 2 ? VB_GATHER_OVF2 : VB_GATHER_OVF3;  // overflow columns per block
+    static constexpr bool CMP = BUD == 1 && DIM == 3;
+    static constexpr int RS = CMP ? 15 : (DIM == 2 ? VB_GATHER_RS2 : VB_GATHER_RS3);  // columns per row in the lane arrays
+    static constexpr int OVF = CMP ? 0 : (DIM == 2 ? VB_GATHER_OVF2 : VB_GATHER_OVF3);  // overflow columns per block
     static constexpr int LANE_CAP = GATHER_ROWS * RS;
     static constexpr int ACC_N = LANE_CAP + OVF;                         // accumulator / edge-vector slots
-    static constexpr int CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_CAP2 : VB_GATHER_CAP3);  // CSR entries of a block
-    static constexpr int SLOT_CAP = GATHER_ROWS * (DIM == 2 ? VB_GATHER_SLOT2 : VB_GATHER_SLOT3);  // plan words
+    static constexpr int CAP = GATHER_ROWS * (CMP ? 16 : (DIM == 2 ? VB_GATHER_CAP2 : VB_GATHER_CAP3));  // CSR entries of a block
+    static constexpr int SLOT_CAP = GATHER_ROWS * (CMP ? 25 : (DIM == 2 ? VB_GATHER_SLOT2 : VB_GATHER_SLOT3));  // plan words
     static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
-    static constexpr int RING = 2;                                       // plan words: double-buffered
+#ifndef VB_GATHER_RING
+#define VB_GATHER_RING 2
+#endif
+    static constexpr int RING = VB_GATHER_RING;                          // plan-word buffers (2: double-buffered)
     static constexpr size_t COLS_BYTES = (size_t)COLS_PAD * 4;           // columns: one buffer (consumed early)
     static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * 4;
     static constexpr size_t SLOTS_OFF = COLS_BYTES;
@@ -571,7 +579,7 @@ struct BlockBounds {
     bool valid, fit;
 };
 
-template <int DIM>
+template <int DIM, int BUD>
 __device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, int64_t nn,
                                                     const int32_t* __restrict__ row_ptr,
                                                     const int32_t* __restrict__ nptr) {
@@ -584,7 +592,8 @@ __device__ __forceinline__ BlockBounds block_bounds(int64_t b, int64_t nblocks, 
     B.p1 = __ldg(row_ptr + B.r1);
     B.q0 = __ldg(nptr + B.r0);
     B.q1 = __ldg(nptr + B.r1);
-    B.fit = (B.p1 - B.p0) <= GatherCfg<DIM>::CAP && (B.q1 - B.q0) <= GatherCfg<DIM>::SLOT_CAP;
+    using C = GatherCfg<DIM, DIM, BUD>;
+    B.fit = (B.p1 - B.p0) <= C::CAP && (B.q1 - B.q0) <= C::SLOT_CAP;
     return B;
 }
 
@@ -598,9 +607,9 @@ struct RowInfo {
     bool ovb;    // some row of the block uses the overflow area (warp-uniform)
 };
 
-template <int DIM, int NC>
+template <int DIM, int NC, int BUD>
 struct GatherSmem {
-    using C = GatherCfg<DIM, NC>;
+    using C = GatherCfg<DIM, NC, BUD>;
     char* base;
     __device__ int32_t* cols() { return reinterpret_cast<int32_t*>(base); }
     __device__ uint32_t* slots(int r) { return reinterpret_cast<uint32_t*>(base + C::SLOTS_OFF + r * C::SLOTS_BYTES); }
@@ -620,16 +629,16 @@ struct GatherSmem {
 // block sharing the staged data, each with its own accumulators over half of
 // every row's incidences (10 warps per SM: 0.62 vs 0.55 ms).
 // (Interleaving (x, y) pairs for 128-bit F loads measured slower: 0.549 vs 0.530 ms.)
-template <int DIM, bool OV, int NC = DIM>
+template <int DIM, bool OV, int NC, int BUD>
 struct LaneMap {
     int t, ov;
     __device__ __forceinline__ int f(int s, int c) const {   // component c of slot s
-        using C = GatherCfg<DIM, NC>;
+        using C = GatherCfg<DIM, NC, BUD>;
         if constexpr (!OV) return (s * NC + c) * GATHER_ROWS + t;
         return s < C::RS ? (s * NC + c) * GATHER_ROWS + t : NC * C::LANE_CAP + (ov + s - C::RS) * NC + c;
     }
     __device__ __forceinline__ int a(int s) const {   // in doubles: K at a(s), M at a(s) + 1
-        using C = GatherCfg<DIM, NC>;
+        using C = GatherCfg<DIM, NC, BUD>;
         if constexpr (!OV) return 2 * (s * GATHER_ROWS + t);
         return 2 * (s < C::RS ? s * GATHER_ROWS + t : C::LANE_CAP + ov + s - C::RS);
     }
@@ -640,8 +649,8 @@ __device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
 
 // lane 0 only: stream block B's columns (single buffer: the previous block's were
 // consumed by its coordinate gather) and plan words (ring slot r)
-template <int DIM, int NC>
-__device__ __forceinline__ void issue_tma(GatherSmem<DIM, NC>& S, int r, const BlockBounds& B,
+template <int DIM, int NC, int BUD>
+__device__ __forceinline__ void issue_tma(GatherSmem<DIM, NC, BUD>& S, int r, const BlockBounds& B,
                                           const int32_t* __restrict__ col_idx, const uint32_t* __restrict__ nslot) {
     if (!B.valid) return;
     if (!B.fit) {  // keep the barrier's phase count in step with the ring: arrive with no bytes
@@ -661,11 +670,11 @@ __device__ __forceinline__ void issue_tma(GatherSmem<DIM, NC>& S, int r, const B
 // Load the lane's row of block B.  If the block is staged (its CSR and plan
 // ranges fit), place the row (lane arrays + overflow), find its diagonal slot and
 // gather its column coordinates into F.  Returns whether the block is staged.
-template <int DIM, int NC>
-__device__ __forceinline__ bool prepare_block(GatherSmem<DIM, NC>& S, BlockBounds& B, RowInfo& R,
+template <int DIM, int NC, int BUD>
+__device__ __forceinline__ bool prepare_block(GatherSmem<DIM, NC, BUD>& S, BlockBounds& B, RowInfo& R,
                                               const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
                                               const double* __restrict__ coords, int64_t ns, int64_t cst) {
-    using C = GatherCfg<DIM>;
+    using C = GatherCfg<DIM, NC, BUD>;
     const int t = threadIdx.x;
     R.v = B.r0 + t;
     R.own = B.valid && R.v < B.r1;
@@ -701,13 +710,13 @@ __device__ __forceinline__ bool prepare_block(GatherSmem<DIM, NC>& S, BlockBound
                 for (int c = 0; c < DIM; c++) cp_async8(F + lm.f(s, c), coords + c * cst + w * ns);
             }
         };
-        if (R.ovb) gather(LaneMap<DIM, true, NC>{t, R.ov});
-        else gather(LaneMap<DIM, false, NC>{t, R.ov});
+        if (R.ovb) gather(LaneMap<DIM, true, NC, BUD>{t, R.ov});
+        else gather(LaneMap<DIM, false, NC, BUD>{t, R.ov});
     }
     return staged;
 }
 
-template <int DIM, bool COEF, bool FAC>
+template <int DIM, bool COEF, bool FAC, int BUD>
 __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, const double* __restrict__ coords,
                                                                  int64_t ns, int64_t cst,
                                                                  const int32_t* __restrict__ row_ptr,
@@ -718,11 +727,11 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                                                                  const CoefSpec cp) {
     static_assert(COEF || !FAC, "factors are a coefficient mode");
     constexpr int NC = FAC ? DIM + 2 : DIM;   // staged per slot: coordinates (+ P, R factors)
-    using Cfg = GatherCfg<DIM, NC>;
+    using Cfg = GatherCfg<DIM, NC, BUD>;
     constexpr int W = GATHER_ROWS;
     constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);  // 1/(d! (d+1)(d+2))
     extern __shared__ __align__(16) char smem_raw[];
-    GatherSmem<DIM, NC> S{smem_raw};
+    GatherSmem<DIM, NC, BUD> S{smem_raw};
     const int t = threadIdx.x;
     const int64_t nblocks = (nn + W - 1) / W;
     const int64_t gstep = gridDim.x;
@@ -732,12 +741,12 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     __syncwarp();
 
     // prologue: TMA for this CTA's first block, then its coordinate gather
-    BlockBounds B0 = block_bounds<DIM>(blockIdx.x, nblocks, nn, row_ptr, nptr);
-    BlockBounds B1 = block_bounds<DIM>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
-    if (t == 0) issue_tma<DIM, NC>(S, 0, B0, col_idx, nslot);
+    BlockBounds B0 = block_bounds<DIM, BUD>(blockIdx.x, nblocks, nn, row_ptr, nptr);
+    BlockBounds B1 = block_bounds<DIM, BUD>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
+    if (t == 0) issue_tma<DIM, NC, BUD>(S, 0, B0, col_idx, nslot);
     if (B0.valid) mbar_wait(S.bar(0), 0);
     RowInfo R;
-    bool staged = prepare_block<DIM, NC>(S, B0, R, row_ptr, nptr, coords, ns, cst);
+    bool staged = prepare_block<DIM, NC, BUD>(S, B0, R, row_ptr, nptr, coords, ns, cst);
     cp_async_commit();
 
     double* F = S.F();
@@ -745,11 +754,16 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     for (int64_t k = 0;; k++) {
         const int64_t b = blockIdx.x + k * gstep;
         if (b >= nblocks) break;
-        const int rc = (int)(k & 1), rn = rc ^ 1;
-        // stage k+1: stream its columns and plan words (every lane is past its column reads)
-        __syncwarp();
-        if (t == 0) issue_tma<DIM, NC>(S, rn, B1, col_idx, nslot);
-        BlockBounds B2 = block_bounds<DIM>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
+        constexpr bool DB = Cfg::RING == 2;
+        const int rc = DB ? (int)(k & 1) : 0, rn = DB ? rc ^ 1 : 0;
+        // stage k+1: stream its columns and plan words (every lane is past its column
+        // reads); with a single plan buffer only once block k's incidences are done
+        auto issue_next = [&]() {
+            __syncwarp();
+            if (t == 0) issue_tma<DIM, NC, BUD>(S, rn, B1, col_idx, nslot);
+        };
+        if (DB || !staged) issue_next();
+        BlockBounds B2 = block_bounds<DIM, BUD>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
         // stage k: its coordinates have landed
         cp_async_wait<0>();
         __syncwarp();
@@ -795,6 +809,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                     mrow = gather_row<DIM, true, COEF, FAC>(R.i0, R.i1, slots, ev, fv, ix, K ? acc : nullptr,
                                                             M ? acc + 1 : nullptr, xv, pv, cp);
                 }
+                if constexpr (!DB) issue_next();
                 __syncwarp();
                 // finish the row (diagonal from the partition of unity, M scale) while
                 // transposing it to CSR order through the (now dead) edge-vector buffer
@@ -821,8 +836,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                     if (M) stcs(M + B0.p0 + q, stM[q]);
                 }
             };
-            if (R.ovb) run(LaneMap<DIM, true, NC>{t, R.ov});
-            else run(LaneMap<DIM, false, NC>{t, R.ov});
+            if (R.ovb) run(LaneMap<DIM, true, NC, BUD>{t, R.ov});
+            else run(LaneMap<DIM, false, NC, BUD>{t, R.ov});
         }
         __syncwarp();   // orders the staged stores above before the in-place rows below
         if (R.own && R.L > 0 && !R.fast) {
@@ -852,8 +867,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         }
         __syncwarp();
         // stage k+1: its columns have landed -> gather its coordinates into F (free now)
-        if (B1.valid) mbar_wait(S.bar(rn), (uint32_t)(((k + 1) >> 1) & 1));
-        staged = prepare_block<DIM, NC>(S, B1, R, row_ptr, nptr, coords, ns, cst);
+        if (B1.valid) mbar_wait(S.bar(rn), DB ? (uint32_t)(((k + 1) >> 1) & 1) : (uint32_t)((k + 1) & 1));
+        staged = prepare_block<DIM, NC, BUD>(S, B1, R, row_ptr, nptr, coords, ns, cst);
         cp_async_commit();
         B0 = B1;
         B1 = B2;
@@ -868,25 +883,37 @@ using namespace vb;
 
 namespace {
 
-template <int DIM, bool COEF, bool FAC>
+template <int DIM, bool COEF, bool FAC, int BUD>
 void launch_gather(unsigned g, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
                    const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const uint32_t* nslot,
                    double* K, double* M, const CoefSpec& cp) {
-    constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM>::SMEM;
-    assemble_gather_k<DIM, COEF, FAC><<<g, GATHER_ROWS, SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx, nptr, nslot,
-                                                                   K, M, cp);
+    constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM, BUD>::SMEM;
+    assemble_gather_k<DIM, COEF, FAC, BUD><<<g, GATHER_ROWS, SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx, nptr,
+                                                                        nslot, K, M, cp);
 }
 
-template <int DIM, bool COEF, bool FAC>
+template <int DIM, bool COEF, bool FAC, int BUD>
 int gather_ctas_per_sm() {
     static int n = 0;  // > 48 KB dynamic smem needs an opt-in; persistent grid size
     if (!n) {
-        constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM>::SMEM;
-        cudaFuncSetAttribute(assemble_gather_k<DIM, COEF, FAC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF, FAC>, GATHER_ROWS, SMEM);
+        constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM, BUD>::SMEM;
+        cudaFuncSetAttribute(assemble_gather_k<DIM, COEF, FAC, BUD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)SMEM);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF, FAC, BUD>, GATHER_ROWS, SMEM);
         if (n < 1) n = 1;
     }
     return n;
+}
+
+template <int DIM, bool COEF, bool FAC, int BUD>
+vb_status run_gather(const char* fn, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
+                     const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const uint32_t* nslot,
+                     double* K, double* M, const CoefSpec& cp) {
+    const int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
+    const int64_t cap = (int64_t)sm_count() * gather_ctas_per_sm<DIM, COEF, FAC, BUD>();
+    const unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
+    launch_gather<DIM, COEF, FAC, BUD>(g, s, nn, coords, ns, cst, row_ptr, col_idx, nptr, nslot, K, M, cp);
+    return launch_check(fn);
 }
 
 template <int DIM, bool COEF>
@@ -902,6 +929,8 @@ vb_status assemble_impl(const char* fn, int64_t nn, int64_t ne, const double* co
                         const int32_t* col_idx, int64_t nnz, const int32_t* elem2nnz, const int32_t* node_elem_ptr,
                         const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
                         double* M_local, int mode, const CoefSpec* coef, cudaStream_t s) {
+    const bool compact = (mode & VB_GATHER_HINT_COMPACT) != 0;
+    mode &= ~VB_GATHER_HINT_COMPACT;
     const bool want_global = K_vals || M_vals;
     const CoefSpec cp = coef ? *coef : CoefSpec{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
     const bool C = coef != nullptr;
@@ -924,20 +953,20 @@ vb_status assemble_impl(const char* fn, int64_t nn, int64_t ne, const double* co
         return VB_ERR_ARG;
     }
     if (want_global && nn > 0) {
-        int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
         // c_K = c_M with gqo = 2 (the paper's benchmarks): per-vertex factors instead of
         // 4 exponentials per incidence (1.43 -> 1.25 ms on tab:KM_P1_3D level 7).  Not for
         // gqo = 1: one exponential per incidence is cheaper than staging the factors
         // (their smem costs 2 of 7 CTAs per SM; 0.81 -> 1.06 ms measured)
         const bool fac = C && cp.same && cp.gqo == 2;
-        const int per_sm = fac ? gather_ctas_per_sm<DIM, true, true>()
-                               : C ? gather_ctas_per_sm<DIM, true, false>() : gather_ctas_per_sm<DIM, false, false>();
-        int64_t cap = (int64_t)sm_count() * per_sm;
-        unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
-        if (fac) launch_gather<DIM, true, true>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
-        else if (C) launch_gather<DIM, true, false>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
-        else launch_gather<DIM, false, false>(g, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, cp);
-        if ((st = launch_check(fn)) != VB_OK) return st;
+        const bool cmp = compact && DIM == 3;
+#define VB_RUN_GATHER(CO, FA, BU) \
+    run_gather<DIM, CO, FA, BU>(fn, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, \
+                                node_elem_slot, K_vals, M_vals, cp)
+        if (fac) st = cmp ? VB_RUN_GATHER(true, true, 1) : VB_RUN_GATHER(true, true, 0);
+        else if (C) st = cmp ? VB_RUN_GATHER(true, false, 1) : VB_RUN_GATHER(true, false, 0);
+        else st = cmp ? VB_RUN_GATHER(false, false, 1) : VB_RUN_GATHER(false, false, 0);
+#undef VB_RUN_GATHER
+        if (st != VB_OK) return st;
     }
     if ((K_local || M_local) && ne > 0) {
         unsigned g = grid_for(ne, 256, 8);
@@ -956,7 +985,8 @@ vb_status assemble_entry(const char* fn, int dim, int64_t nn, int64_t ne, const 
     clear_error();
     if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
     if (nn < 0 || ne < 0 || nnz < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
-    if (mode != VB_ASSEMBLE_ATOMIC && mode != VB_ASSEMBLE_GATHER) { set_error("%s: unknown mode %d", fn, mode); return VB_ERR_ARG; }
+    const int base_mode = mode & ~VB_GATHER_HINT_COMPACT;
+    if (base_mode != VB_ASSEMBLE_ATOMIC && base_mode != VB_ASSEMBLE_GATHER) { set_error("%s: unknown mode %d", fn, mode); return VB_ERR_ARG; }
     if (ne > 0 && (!coords || !elems)) { set_error("%s: NULL %s", fn, !coords ? "coords" : "elems"); return VB_ERR_ARG; }
     if (elem_ld < ne) { set_error("%s: elem_ld < ne", fn); return VB_ERR_ARG; }
     auto f = dim == 2 ? assemble_impl<2> : assemble_impl<3>;

@@ -467,3 +467,42 @@ extern "C" vb_status fem_pattern(int nv, int64_t nn, int64_t ne, const int32_t* 
     return pattern_impl<4, 128, 64>("fem_pattern", nv, nn, ne, elems, elem_ld, work, work_bytes, row_ptr, col_idx,
                                     col_cap, elem2nnz, node_elem_ptr, node_elem, node_elem_slot, nnz_out, stream);
 }
+
+// ------------------------------------------------------------------ plan statistics
+namespace vb {
+namespace {
+// maxima over 32-row blocks: [0] row length, [1] CSR entries of a block, [2] incidences of a block
+__global__ void plan_stats_k(int64_t nn, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
+                             int* __restrict__ out) {
+    int m0 = 0, m1 = 0, m2 = 0;
+    const int64_t nb = (nn + 31) / 32;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r0 = b * 32, r1 = r0 + 32 < nn ? r0 + 32 : nn;
+        for (int64_t r = r0; r < r1; r++) m0 = max(m0, row_ptr[r + 1] - row_ptr[r]);
+        m1 = max(m1, row_ptr[r1] - row_ptr[r0]);
+        if (nptr) m2 = max(m2, nptr[r1] - nptr[r0]);
+    }
+    atomicMax(out, m0);
+    atomicMax(out + 1, m1);
+    atomicMax(out + 2, m2);
+}
+}  // namespace
+}  // namespace vb
+
+extern "C" vb_status fem_plan_stats(int64_t nn, const int32_t* row_ptr, const int32_t* node_elem_ptr, void* work,
+                                    int64_t* stats_out, vb_stream_t stream) {
+    clear_error();
+    const char* fn = "fem_plan_stats";
+    if (nn < 0) { set_error("%s: negative nn", fn); return VB_ERR_ARG; }
+    if (!row_ptr || !work || !stats_out) { set_error("%s: NULL row_ptr, work or stats_out", fn); return VB_ERR_ARG; }
+    cudaStream_t s = cs(stream);
+    int* d = reinterpret_cast<int*>(work);
+    cudaMemsetAsync(d, 0, 3 * sizeof(int), s);
+    if (nn > 0) plan_stats_k<<<grid_for((nn + 31) / 32, 256, 4), 256, 0, s>>>(nn, row_ptr, node_elem_ptr, d);
+    vb_status st = launch_check(fn);
+    if (st != VB_OK) return st;
+    int h[3] = {0, 0, 0};
+    if ((st = read_small(s, d, sizeof(h), h, fn)) != VB_OK) return st;
+    for (int i = 0; i < 3; i++) stats_out[i] = h[i];
+    return VB_OK;
+}

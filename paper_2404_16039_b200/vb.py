@@ -21,6 +21,16 @@ LIB_PATH = os.environ.get("VB_LIBVB") or os.path.join(_HERE, "libvb.so")   # VB_
 
 VB_ASSEMBLE_ATOMIC = 0
 VB_ASSEMBLE_GATHER = 1
+VB_GATHER_HINT_COMPACT = 0x100
+
+
+def _gather_mode(mode, plan, compact):
+    """mode plus the compact-budget hint: from the plan's block maxima (compact=None)
+    or forced (True / False; a wrong hint costs speed only, never correctness)."""
+    if mode != VB_ASSEMBLE_GATHER:
+        return int(mode)
+    use = getattr(plan, "compact", False) if compact is None else bool(compact)
+    return int(mode) | (VB_GATHER_HINT_COMPACT if use else 0)
 
 _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORTED",
            -4: "VB_ERR_OVERFLOW", -5: "VB_ERR_WORKSPACE", -6: "VB_ERR_CUDA"}
@@ -28,7 +38,7 @@ _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORT
 EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
-           "fem_pattern", "fem_p2_assemble")
+           "fem_pattern", "fem_p2_assemble", "fem_plan_stats")
 
 
 class VbError(RuntimeError):
@@ -67,6 +77,7 @@ def lib():
             "vb_quad_rule": (i32, [i32, i32, p, p]),
             "fem_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p, p, p, i32, p]),
             "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
+            "fem_plan_stats": (i32, [i64, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -253,6 +264,13 @@ class P1Plan:
         self.col_idx_padded = self.col_idx
         self.col_idx = self.col_idx[:self.nnz]
         self.work = None   # the pattern workspace is not needed after the plan exists
+        # block maxima -> the gather kernel's compact shared-memory budget where it fits (3D)
+        stats = (C.c_int64 * 3)()
+        scratch = torch.empty((16,), dtype=torch.uint8, device=dev)
+        _check(L.fem_plan_stats(nn, _ptr(self.row_ptr), _ptr(self.node_elem_ptr), _ptr(scratch), stats, st))
+        self.stats = tuple(int(x) for x in stats)   # (max row, max block entries, max block incidences)
+        self.compact = (self.dim == 3 and gather_plan and self.stats[0] <= 15 and self.stats[1] <= 16 * 32
+                        and self.stats[2] <= 25 * 32)
 
 
 def fem_p1_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
@@ -260,7 +278,7 @@ def fem_p1_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
 
 
 def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False,
-                    K=None, M=None, stream=None):
+                    K=None, M=None, stream=None, compact=None):
     """Returns (K_vals, M_vals, K_local, M_local) (None where not requested)."""
     _f64(coords)
     dim, nn = coords.shape
@@ -279,13 +297,13 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
     _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                  _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
                                  _ptr(plan.node_elem), _ptr(plan.node_elem_slot), _ptr(K), _ptr(M), _ptr(Kl),
-                                 _ptr(Ml), int(mode), _stream(stream)))
+                                 _ptr(Ml), _gather_mode(mode, plan, compact), _stream(stream)))
     return K, M, Kl, Ml
 
 
 def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0)),
                          mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False, K=None, M=None,
-                         stream=None):
+                         stream=None, compact=None):
     """Coefficient-weighted K, M with c(x) = a * exp(b . x) (NEXT-1).  Returns
     (K_vals, M_vals, K_local, M_local)."""
     _f64(coords)
@@ -302,7 +320,7 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
                                       _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
                                       _ptr(plan.node_elem), _ptr(plan.node_elem_slot), int(gqo), float(cK[0]),
                                       C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), _ptr(K), _ptr(M),
-                                      _ptr(Kl), _ptr(Ml), int(mode), _stream(stream)))
+                                      _ptr(Kl), _ptr(Ml), _gather_mode(mode, plan, compact), _stream(stream)))
     return K, M, Kl, Ml
 
 

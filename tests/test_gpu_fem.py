@@ -330,3 +330,40 @@ def test_fill_phase_without_count_state(dev, kind, n):
     assert np.array_equal(h(e2n), h(ref.elem2nnz))
     assert np.array_equal(h(nptr), h(ref.node_elem_ptr)) and np.array_equal(h(nel), h(ref.node_elem))
     assert np.array_equal(h(nsl)[:nv * ne], h(ref.node_elem_slot)[:nv * ne])
+
+
+@pytest.mark.parametrize("kind", ["kuhn", "delaunay", "fan"])
+def test_gather_budgets_and_plan_stats(dev, kind):
+    """fem_plan_stats reports the block maxima; the gather kernel gives the same
+    bits with the wide and the compact shared-memory budget, also where the
+    compact hint is wrong (Delaunay / fan rows longer than 15 columns)."""
+    if kind == "kuhn":
+        coords, elems = synth.cube_kuhn_p1(9, jitter=0.05, seed=6)
+    elif kind == "delaunay":
+        coords, elems = synth.delaunay_p1(3, 9, seed=6)
+    else:
+        coords, elems = fan_mesh(40, fans=3)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    plan = vb.P1Plan(g(elems, dev), nn)
+    L = np.diff(rp)
+    nptr = h(plan.node_elem_ptr)
+    nb = (nn + 31) // 32
+    blk = [min(32 * (b + 1), nn) for b in range(nb)]
+    exp = (int(L.max()), max(int(rp[e] - rp[32 * b]) for b, e in enumerate(blk)),
+           max(int(nptr[e] - nptr[32 * b]) for b, e in enumerate(blk)))
+    assert plan.stats == exp
+    assert plan.compact == (kind == "kuhn" and elems.shape[0] == 4)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    cd, ed = g(coords, dev), g(elems, dev)
+    out = []
+    for compact in (False, True):
+        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, compact=compact)
+        K, M = h(K), h(M)
+        assert relmax(K, Ko) <= 1e-12 and relmax(M, Mo) <= 1e-12
+        out.append((K, M))
+        cf = (1.3, (0.7, 0.2, -0.5))
+        Kc, Mc, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, compact=compact)
+        Kco, Mco = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cf, cM=cf)
+        assert relmax(h(Kc), Kco) <= 1e-12 and relmax(h(Mc), Mco) <= 1e-12
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
