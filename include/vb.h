@@ -192,6 +192,16 @@ VB_API vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne,
 VB_API vb_status fem_plan_stats(int64_t nn, const int32_t* row_ptr, const int32_t* node_elem_ptr, void* work,
                                 int64_t* stats_out, vb_stream_t stream);
 
+/* Packed 16-bit form of the P1 gather plan words, required with
+ * VB_GATHER_HINT_COMPACT: packed[i] = o1 | o2 << 4 | o3 << 8 (2D: o1 | o2 << 4)
+ * with o_j the in-row offsets of the incidence's other vertices (bytes 1..nv-1
+ * of node_elem_slot[i]).  packed (n_inc uint16, DEVICE) must be readable up to
+ * the next multiple of 8 entries.  work: DEVICE scratch of >= 16 bytes.
+ * VB_ERR_UNSUPPORTED if an offset is >= 16 (a row with more than 16 entries).
+ * Synchronises the stream. */
+VB_API vb_status fem_plan_pack_slots(int dim, int64_t n_inc, const uint32_t* node_elem_slot, uint16_t* packed,
+                                     void* work, vb_stream_t stream);
+
 /* ---------------------------------------------------------- a7..a17 assembly
  * Global P1 stiffness and mass matrices with c_K = c_M = 1 (eq:K_M P:967-975,
  * stiffness_matrixP1 P:978-1004, mass_matrixP1 P:1007), written
@@ -222,9 +232,10 @@ VB_API vb_status fem_plan_stats(int64_t nn, const int32_t* row_ptr, const int32_
 /* Hint OR'ed into a gather mode (3D; ignored otherwise): every 32-row block of
  * the plan has rows of <= 15 columns, <= 16*32 CSR entries and <= 25*32
  * incidences (fem_p1_pattern's stats_out tells; Kuhn cubes qualify).  The
- * kernel then runs with a smaller shared-memory budget (8 instead of 7 CTAs
- * per SM).  Blocks or rows that do not fit it are still assembled correctly
- * (in place in HBM), only slower. */
+ * kernel then runs with a smaller shared-memory budget (9 instead of 7 CTAs
+ * per SM) and node_elem_slot must point to the packed 16-bit plan words of
+ * fem_plan_pack_slots.  Blocks that do not fit the budget are still assembled
+ * correctly (in place in HBM), only slower. */
 #define VB_GATHER_HINT_COMPACT 0x100
 VB_API vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne,
                           const double* coords, int64_t node_stride, int64_t comp_stride,

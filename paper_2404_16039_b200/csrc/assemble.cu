@@ -14,6 +14,8 @@
 //     is added into the row's slots kept in shared memory, and the CTA's
 //     contiguous CSR range is written once with coalesced stores (no atomics,
 //     no zero-fill, no read-modify-write of K/M in HBM).
+#include <type_traits>
+
 #include "vb_internal.cuh"
 
 namespace vb {
@@ -253,9 +255,10 @@ constexpr int GATHER_ROWS = 32;
 #define VB_GATHER_OVF2 32
 #endif
 // BUD = 1: the compact budget for meshes whose 32-row blocks all have rows of <= 15
-// columns, <= 16*32 CSR entries and <= 25*32 incidences (Kuhn cubes; fem_p1_pattern
-// reports the plan's maxima, the caller passes VB_GATHER_HINT_COMPACT): 8 instead
-// of 7 CTAs per SM in 3D.  Blocks that do not fit stay correct (in-place path).
+// columns, <= 16*32 CSR entries and <= 25*32 incidences (Kuhn cubes; fem_plan_stats
+// reports the plan's maxima, the caller passes VB_GATHER_HINT_COMPACT) with 16-bit
+// plan words (fem_plan_pack_slots): 24.6 KB per CTA, 8 CTAs per SM in 3D (9 fit;
+// see gather_ctas_per_sm).  Blocks that do not fit stay correct (in-place path).
 template <int DIM, int NC = DIM, int BUD = 0>   // NC doubles staged per column slot: coordinates (+ coefficient factors)
 struct GatherCfg {
     static constexpr bool CMP = BUD == 1 && DIM == 3;
@@ -265,13 +268,16 @@ struct GatherCfg {
     static constexpr int ACC_N = LANE_CAP + OVF;                         // accumulator / edge-vector slots
     static constexpr int CAP = GATHER_ROWS * (CMP ? 16 : (DIM == 2 ? VB_GATHER_CAP2 : VB_GATHER_CAP3));  // CSR entries of a block
     static constexpr int SLOT_CAP = GATHER_ROWS * (CMP ? 25 : (DIM == 2 ? VB_GATHER_SLOT2 : VB_GATHER_SLOT3));  // plan words
-    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 8;  // 16-byte alignment slack of TMA copies
+    // plan words: the packed 16-bit form (fem_plan_pack_slots) with the compact budget
+    using SW = std::conditional_t<CMP, uint16_t, uint32_t>;
+    static constexpr int SW_PER16 = 16 / (int)sizeof(SW);                // words per 16-byte TMA chunk
+    static constexpr int COLS_PAD = CAP + 8, SLOTS_PAD = SLOT_CAP + 2 * SW_PER16;  // alignment slack of TMA copies
 #ifndef VB_GATHER_RING
 #define VB_GATHER_RING 2
 #endif
     static constexpr int RING = VB_GATHER_RING;                          // plan-word buffers (2: double-buffered)
     static constexpr size_t COLS_BYTES = (size_t)COLS_PAD * 4;           // columns: one buffer (consumed early)
-    static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * 4;
+    static constexpr size_t SLOTS_BYTES = (size_t)SLOTS_PAD * sizeof(SW);
     static constexpr size_t SLOTS_OFF = COLS_BYTES;
     static constexpr size_t F_OFF = SLOTS_OFF + RING * SLOTS_BYTES;      // edge vectors / CSR staging
     static constexpr size_t ACC_OFF = F_OFF + (size_t)NC * ACC_N * 8;    // (K, M) pairs
@@ -405,7 +411,8 @@ struct NoFac {
 
 // fv(s, P, R): the per-vertex coefficient factors of column slot s (FAC);
 // pv: those of the row's vertex
-template <int DIM, bool COEF, bool FAC, typename EV, typename FV>
+// sl: the incidence's plan word; PK: packed 16-bit form (4 bits per other vertex)
+template <int DIM, bool COEF, bool FAC, bool PK, typename EV, typename FV>
 __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, FV fv, const double (&xv)[DIM],
                                                  const double (&pv)[2], const CoefSpec& cp) {
     IncOut<DIM> o;
@@ -415,9 +422,9 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, FV fv, cons
         R[0] = pv[1];
     }
     if constexpr (DIM == 3) {
-        o.s[0] = (sl >> 8) & 0xff;
-        o.s[1] = (sl >> 16) & 0xff;
-        o.s[2] = sl >> 24;
+        o.s[0] = PK ? (sl & 15) : ((sl >> 8) & 0xff);
+        o.s[1] = PK ? ((sl >> 4) & 15) : ((sl >> 16) & 0xff);
+        o.s[2] = PK ? ((sl >> 8) & 15) : (sl >> 24);
         double f1[3], f2[3], f3[3];
         ev(o.s[0], f1);
         ev(o.s[1], f2);
@@ -445,8 +452,8 @@ __device__ __forceinline__ IncOut<DIM> incidence(uint32_t sl, EV ev, FV fv, cons
             apply_coef<3, FAC>(o, xv, f, cp, P, R);
         }
     } else {
-        o.s[0] = (sl >> 8) & 0xff;
-        o.s[1] = (sl >> 16) & 0xff;
+        o.s[0] = PK ? (sl & 15) : ((sl >> 8) & 0xff);
+        o.s[1] = PK ? ((sl >> 4) & 15) : ((sl >> 16) & 0xff);
         double f1[2], f2[2];
         ev(o.s[0], f1);
         ev(o.s[1], f2);
@@ -511,8 +518,9 @@ __device__ __forceinline__ void accumulate(const IncOut<DIM>& o, double* __restr
 // from the row's vertex to its column s.  Incidences are evaluated U at a time
 // (all loads and arithmetic before any accumulator store) and accumulated in
 // ascending element order.  Returns the row sum of M (COEF only).
-template <int DIM, bool PACKED, bool WK, bool WM, bool COEF, bool FAC, typename EV, typename FV, typename IX>
-__device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, FV fv, IX ix,
+template <int DIM, bool PACKED, bool WK, bool WM, bool COEF, bool FAC, typename SW, typename EV, typename FV,
+          typename IX>
+__device__ __forceinline__ double gather_row_t(int i0, int i1, const SW* __restrict__ slots, EV ev, FV fv, IX ix,
                                                double* __restrict__ accK, double* __restrict__ accM,
                                                const double (&xv)[DIM], const double (&pv)[2],
                                                const CoefSpec& cp) {
@@ -523,6 +531,7 @@ __device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* _
 #define VB_GATHER_UF 4  // coefficient factors (FAC): 2 / 3 / 4 -> 1.29 / 1.28 / 1.25 ms (tab:KM_P1_3D L7)
 #endif
     constexpr int U = COEF ? (FAC ? VB_GATHER_UF : 2) : VB_GATHER_U;
+    constexpr bool PK = sizeof(SW) == 2;
     // (A lane-rotated incidence order, which makes the plan-word reads bank-conflict
     // free -- 8 -> 1 wavefronts, 13 % of the kernel's shared-memory wavefronts --
     // measured 0.530 vs 0.528 ms on config 5 and would give up the ascending order.)
@@ -531,25 +540,27 @@ __device__ __forceinline__ double gather_row_t(int i0, int i1, const uint32_t* _
     for (; i + U - 1 < i1; i += U) {
         IncOut<DIM> o[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF, FAC>(slots[i + u], ev, fv, xv, pv, cp);
+        for (int u = 0; u < U; u++) o[u] = incidence<DIM, COEF, FAC, PK>(slots[i + u], ev, fv, xv, pv, cp);
 #pragma unroll
         for (int u = 0; u < U; u++) accumulate<DIM, PACKED, WK, WM, COEF>(o[u], accK, accM, ix, mrow);
     }
     for (; i < i1; i++)
-        accumulate<DIM, PACKED, WK, WM, COEF>(incidence<DIM, COEF, FAC>(slots[i], ev, fv, xv, pv, cp), accK, accM, ix,
+        accumulate<DIM, PACKED, WK, WM, COEF>(incidence<DIM, COEF, FAC, PK>(slots[i], ev, fv, xv, pv, cp), accK, accM, ix,
                                               mrow);
     return mrow;
 }
 
 // PAIRS: accM == accK + 1 (interleaved pairs), packed access when both are wanted
-template <int DIM, bool PAIRS, bool COEF, bool FAC, typename EV, typename FV, typename IX>
-__device__ __forceinline__ double gather_row(int i0, int i1, const uint32_t* __restrict__ slots, EV ev, FV fv, IX ix,
+template <int DIM, bool PAIRS, bool COEF, bool FAC, typename SW, typename EV, typename FV, typename IX>
+__device__ __forceinline__ double gather_row(int i0, int i1, const SW* __restrict__ slots, EV ev, FV fv, IX ix,
                                              double* __restrict__ accK, double* __restrict__ accM,
                                              const double (&xv)[DIM], const double (&pv)[2], const CoefSpec& cp) {
     if (accK && accM)
-        return gather_row_t<DIM, PAIRS, true, true, COEF, FAC>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
-    if (accK) return gather_row_t<DIM, false, true, false, COEF, FAC>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
-    if (accM) return gather_row_t<DIM, false, false, true, COEF, FAC>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
+        return gather_row_t<DIM, PAIRS, true, true, COEF, FAC, SW>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
+    if (accK)
+        return gather_row_t<DIM, false, true, false, COEF, FAC, SW>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
+    if (accM)
+        return gather_row_t<DIM, false, false, true, COEF, FAC, SW>(i0, i1, slots, ev, fv, ix, accK, accM, xv, pv, cp);
     return 0.0;
 }
 
@@ -612,7 +623,9 @@ struct GatherSmem {
     using C = GatherCfg<DIM, NC, BUD>;
     char* base;
     __device__ int32_t* cols() { return reinterpret_cast<int32_t*>(base); }
-    __device__ uint32_t* slots(int r) { return reinterpret_cast<uint32_t*>(base + C::SLOTS_OFF + r * C::SLOTS_BYTES); }
+    __device__ typename C::SW* slots(int r) {
+        return reinterpret_cast<typename C::SW*>(base + C::SLOTS_OFF + r * C::SLOTS_BYTES);
+    }
     __device__ double* F() { return reinterpret_cast<double*>(base + C::F_OFF); }
     __device__ double* acc() { return reinterpret_cast<double*>(base + C::ACC_OFF); }
     __device__ uint64_t* bar(int r) { return reinterpret_cast<uint64_t*>(base + C::BAR_OFF) + r; }
@@ -651,15 +664,18 @@ __device__ __forceinline__ int tma_shift(int32_t x) { return x & 3; }
 // consumed by its coordinate gather) and plan words (ring slot r)
 template <int DIM, int NC, int BUD>
 __device__ __forceinline__ void issue_tma(GatherSmem<DIM, NC, BUD>& S, int r, const BlockBounds& B,
-                                          const int32_t* __restrict__ col_idx, const uint32_t* __restrict__ nslot) {
+                                          const int32_t* __restrict__ col_idx,
+                                          const typename GatherCfg<DIM, NC, BUD>::SW* __restrict__ nslot) {
+    using C = GatherCfg<DIM, NC, BUD>;
+    constexpr uint32_t WM = C::SW_PER16 - 1;
     if (!B.valid) return;
     if (!B.fit) {  // keep the barrier's phase count in step with the ring: arrive with no bytes
         mbar_expect_tx(S.bar(r), 0);
         return;
     }
     uint32_t c0 = (uint32_t)B.p0 & ~3u, c1 = ((uint32_t)B.p1 + 3u) & ~3u;
-    uint32_t s0 = (uint32_t)B.q0 & ~3u, s1 = ((uint32_t)B.q1 + 3u) & ~3u;
-    uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * 4;
+    uint32_t s0 = (uint32_t)B.q0 & ~WM, s1 = ((uint32_t)B.q1 + WM) & ~WM;
+    uint32_t bc = (c1 - c0) * 4, bs = (s1 - s0) * (uint32_t)sizeof(typename C::SW);
     // generic-proxy reads of the column buffer (previous block) before the async-proxy overwrite
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(S.bar(r), bc + bs);
@@ -722,7 +738,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                                                                  const int32_t* __restrict__ row_ptr,
                                                                  const int32_t* __restrict__ col_idx,
                                                                  const int32_t* __restrict__ nptr,
-                                                                 const uint32_t* __restrict__ nslot,
+                                                                 const void* __restrict__ nslot_v,
                                                                  double* __restrict__ K, double* __restrict__ M,
                                                                  const CoefSpec cp) {
     static_assert(COEF || !FAC, "factors are a coefficient mode");
@@ -732,6 +748,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);  // 1/(d! (d+1)(d+2))
     extern __shared__ __align__(16) char smem_raw[];
     GatherSmem<DIM, NC, BUD> S{smem_raw};
+    using SW = typename Cfg::SW;
+    const SW* __restrict__ nslot = static_cast<const SW*>(nslot_v);
     const int t = threadIdx.x;
     const int64_t nblocks = (nn + W - 1) / W;
     const int64_t gstep = gridDim.x;
@@ -768,7 +786,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
         cp_async_wait<0>();
         __syncwarp();
         if (staged) {
-            const uint32_t* slots = S.slots(rc) + tma_shift(B0.q0) - B0.q0;
+            const SW* slots = S.slots(rc) + (B0.q0 & (Cfg::SW_PER16 - 1)) - B0.q0;
             const int np = B0.p1 - B0.p0;
             auto run = [&](auto lm) {
                 double mrow = 0.0;
@@ -862,7 +880,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             };
             auto ix = [](int s) { return s; };
             const double pv[2] = {1.0, 1.0};
-            double mrow = gather_row<DIM, false, COEF, false>(R.i0, R.i1, nslot, ev, NoFac{}, ix, aK, aM, xv, pv, cp);
+            double mrow = gather_row<DIM, false, COEF, false, SW>(R.i0, R.i1, nslot, ev, NoFac{}, ix, aK, aM, xv, pv, cp);
             finish_row<DIM, 1, COEF>(R.L, s0, aK, aM, mrow);
         }
         __syncwarp();
@@ -885,7 +903,7 @@ namespace {
 
 template <int DIM, bool COEF, bool FAC, int BUD>
 void launch_gather(unsigned g, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
-                   const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const uint32_t* nslot,
+                   const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const void* nslot,
                    double* K, double* M, const CoefSpec& cp) {
     constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM, BUD>::SMEM;
     assemble_gather_k<DIM, COEF, FAC, BUD><<<g, GATHER_ROWS, SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx, nptr,
@@ -900,6 +918,10 @@ int gather_ctas_per_sm() {
         cudaFuncSetAttribute(assemble_gather_k<DIM, COEF, FAC, BUD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF, FAC, BUD>, GATHER_ROWS, SMEM);
+        // One warp per CTA and a static block schedule: with 4k+1 resident warps one
+        // SM sub-partition runs 3 warps against 2 elsewhere and every CTA waits for
+        // it (compact budget: 9 CTAs 0.521 ms, capped at 8 0.476 ms, 7 0.515 ms).
+        if (n > 4 && n % 4 == 1) n -= 1;
         if (n < 1) n = 1;
     }
     return n;
@@ -907,7 +929,7 @@ int gather_ctas_per_sm() {
 
 template <int DIM, bool COEF, bool FAC, int BUD>
 vb_status run_gather(const char* fn, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
-                     const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const uint32_t* nslot,
+                     const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const void* nslot,
                      double* K, double* M, const CoefSpec& cp) {
     const int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
     const int64_t cap = (int64_t)sm_count() * gather_ctas_per_sm<DIM, COEF, FAC, BUD>();

@@ -506,3 +506,40 @@ extern "C" vb_status fem_plan_stats(int64_t nn, const int32_t* row_ptr, const in
     for (int i = 0; i < 3; i++) stats_out[i] = h[i];
     return VB_OK;
 }
+
+// ------------------------------------------------------------------ packed plan words
+namespace vb {
+namespace {
+__global__ void pack_slots_k(int dim, int64_t n, const uint32_t* __restrict__ in, uint16_t* __restrict__ out,
+                             int* __restrict__ bad) {
+    int b = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t w = in[i];
+        const uint32_t s1 = (w >> 8) & 0xff, s2 = (w >> 16) & 0xff, s3 = dim == 3 ? w >> 24 : 0;
+        b |= (s1 | s2 | s3) >= 16;
+        out[i] = (uint16_t)(s1 | (s2 << 4) | (s3 << 8));
+    }
+    if (b) atomicOr(bad, 1);
+}
+}  // namespace
+}  // namespace vb
+
+extern "C" vb_status fem_plan_pack_slots(int dim, int64_t n_inc, const uint32_t* node_elem_slot, uint16_t* packed,
+                                         void* work, vb_stream_t stream) {
+    clear_error();
+    const char* fn = "fem_plan_pack_slots";
+    if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
+    if (n_inc < 0) { set_error("%s: negative n_inc", fn); return VB_ERR_ARG; }
+    if (n_inc > 0 && (!node_elem_slot || !packed || !work)) { set_error("%s: NULL argument", fn); return VB_ERR_ARG; }
+    if (n_inc == 0) return VB_OK;
+    cudaStream_t s = cs(stream);
+    int* d = reinterpret_cast<int*>(work);
+    cudaMemsetAsync(d, 0, sizeof(int), s);
+    pack_slots_k<<<grid_for(n_inc, 256, 8), 256, 0, s>>>(dim, n_inc, node_elem_slot, packed, d);
+    vb_status st = launch_check(fn);
+    if (st != VB_OK) return st;
+    int bad = 0;
+    if ((st = read_small(s, d, sizeof(int), &bad, fn)) != VB_OK) return st;
+    if (bad) { set_error("%s: a row has more than 16 entries; the packed form needs offsets < 16", fn); return VB_ERR_UNSUPPORTED; }
+    return VB_OK;
+}

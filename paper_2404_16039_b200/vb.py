@@ -25,12 +25,18 @@ VB_GATHER_HINT_COMPACT = 0x100
 
 
 def _gather_mode(mode, plan, compact):
-    """mode plus the compact-budget hint: from the plan's block maxima (compact=None)
-    or forced (True / False; a wrong hint costs speed only, never correctness)."""
+    """(mode, plan words): the compact-budget hint from the plan's block maxima
+    (compact=None) or forced (True / False), with the packed 16-bit plan words it
+    needs (packing fails for rows of more than 16 entries; blocks beyond the
+    budget only cost speed)."""
     if mode != VB_ASSEMBLE_GATHER:
-        return int(mode)
+        return int(mode), plan.node_elem_slot
     use = getattr(plan, "compact", False) if compact is None else bool(compact)
-    return int(mode) | (VB_GATHER_HINT_COMPACT if use else 0)
+    if not use:
+        return int(mode), plan.node_elem_slot
+    if getattr(plan, "node_elem_slot16", None) is None:
+        plan.node_elem_slot16 = plan.pack_slots()
+    return int(mode) | VB_GATHER_HINT_COMPACT, plan.node_elem_slot16
 
 _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORTED",
            -4: "VB_ERR_OVERFLOW", -5: "VB_ERR_WORKSPACE", -6: "VB_ERR_CUDA"}
@@ -38,7 +44,7 @@ _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORT
 EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
-           "fem_pattern", "fem_p2_assemble", "fem_plan_stats")
+           "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots")
 
 
 class VbError(RuntimeError):
@@ -78,6 +84,7 @@ def lib():
             "fem_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p, p, p, i32, p]),
             "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
             "fem_plan_stats": (i32, [i64, p, p, p, C.POINTER(C.c_int64), p]),
+            "fem_plan_pack_slots": (i32, [i32, i64, p, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -271,6 +278,16 @@ class P1Plan:
         self.stats = tuple(int(x) for x in stats)   # (max row, max block entries, max block incidences)
         self.compact = (self.dim == 3 and gather_plan and self.stats[0] <= 15 and self.stats[1] <= 16 * 32
                         and self.stats[2] <= 25 * 32)
+        self.node_elem_slot16 = self.pack_slots() if self.compact else None
+
+    def pack_slots(self):
+        """The packed 16-bit plan words of the compact gather budget (fem_plan_pack_slots)."""
+        n = self.nv * self.ne
+        out = torch.zeros((max(8, (n + 7) // 8 * 8),), dtype=torch.int16, device=self.row_ptr.device)
+        scratch = torch.empty((16,), dtype=torch.uint8, device=self.row_ptr.device)
+        _check(lib().fem_plan_pack_slots(self.dim, n, _ptr(self.node_elem_slot), _ptr(out), _ptr(scratch),
+                                         _stream()))
+        return out
 
 
 def fem_p1_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
@@ -294,10 +311,11 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         M = None
     Kl = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
     Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    gmode, words = _gather_mode(mode, plan, compact)
     _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                  _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
-                                 _ptr(plan.node_elem), _ptr(plan.node_elem_slot), _ptr(K), _ptr(M), _ptr(Kl),
-                                 _ptr(Ml), _gather_mode(mode, plan, compact), _stream(stream)))
+                                 _ptr(plan.node_elem), _ptr(words), _ptr(K), _ptr(M), _ptr(Kl),
+                                 _ptr(Ml), gmode, _stream(stream)))
     return K, M, Kl, Ml
 
 
@@ -316,11 +334,12 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
     Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
     kb = (C.c_double * 3)(*[float(x) for x in list(cK[1])[:3]] + [0.0] * (3 - len(list(cK[1])[:3])))
     mb = (C.c_double * 3)(*[float(x) for x in list(cM[1])[:3]] + [0.0] * (3 - len(list(cM[1])[:3])))
+    gmode, words = _gather_mode(mode, plan, compact)
     _check(lib().fem_p1_assemble_coef(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                       _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
-                                      _ptr(plan.node_elem), _ptr(plan.node_elem_slot), int(gqo), float(cK[0]),
+                                      _ptr(plan.node_elem), _ptr(words), int(gqo), float(cK[0]),
                                       C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), _ptr(K), _ptr(M),
-                                      _ptr(Kl), _ptr(Ml), _gather_mode(mode, plan, compact), _stream(stream)))
+                                      _ptr(Kl), _ptr(Ml), gmode, _stream(stream)))
     return K, M, Kl, Ml
 
 

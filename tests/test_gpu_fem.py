@@ -332,13 +332,16 @@ def test_fill_phase_without_count_state(dev, kind, n):
     assert np.array_equal(h(nsl)[:nv * ne], h(ref.node_elem_slot)[:nv * ne])
 
 
-@pytest.mark.parametrize("kind", ["kuhn", "delaunay", "fan"])
+@pytest.mark.parametrize("kind", ["kuhn", "kuhn-permuted", "delaunay", "fan"])
 def test_gather_budgets_and_plan_stats(dev, kind):
     """fem_plan_stats reports the block maxima; the gather kernel gives the same
-    bits with the wide and the compact shared-memory budget, also where the
-    compact hint is wrong (Delaunay / fan rows longer than 15 columns)."""
+    bits with the wide and the compact shared-memory budget (packed 16-bit plan
+    words), also for a random numbering whose blocks may exceed the compact
+    budget; the packed form refuses rows of more than 16 entries."""
     if kind == "kuhn":
         coords, elems = synth.cube_kuhn_p1(9, jitter=0.05, seed=6)
+    elif kind == "kuhn-permuted":
+        coords, elems = synth.permute_mesh(*synth.cube_kuhn_p1(9, jitter=0.05, seed=6), seed=7)
     elif kind == "delaunay":
         coords, elems = synth.delaunay_p1(3, 9, seed=6)
     else:
@@ -353,11 +356,19 @@ def test_gather_budgets_and_plan_stats(dev, kind):
     exp = (int(L.max()), max(int(rp[e] - rp[32 * b]) for b, e in enumerate(blk)),
            max(int(nptr[e] - nptr[32 * b]) for b, e in enumerate(blk)))
     assert plan.stats == exp
-    assert plan.compact == (kind == "kuhn" and elems.shape[0] == 4)
+    if kind == "kuhn":
+        assert plan.compact
     Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
     cd, ed = g(coords, dev), g(elems, dev)
+    if L.max() > 16:
+        assert not plan.compact
+        with pytest.raises(vb.VbError, match="16"):
+            plan.pack_slots()
+        budgets = (False,)
+    else:
+        budgets = (False, True)
     out = []
-    for compact in (False, True):
+    for compact in budgets:
         K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, compact=compact)
         K, M = h(K), h(M)
         assert relmax(K, Ko) <= 1e-12 and relmax(M, Mo) <= 1e-12
@@ -366,4 +377,5 @@ def test_gather_budgets_and_plan_stats(dev, kind):
         Kc, Mc, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, compact=compact)
         Kco, Mco = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cf, cM=cf)
         assert relmax(h(Kc), Kco) <= 1e-12 and relmax(h(Mc), Mco) <= 1e-12
-    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    for K, M in out[1:]:
+        assert np.array_equal(out[0][0], K) and np.array_equal(out[0][1], M)
