@@ -14,6 +14,7 @@
 //     is added into the row's slots kept in shared memory, and the CTA's
 //     contiguous CSR range is written once with coalesced stores (no atomics,
 //     no zero-fill, no read-modify-write of K/M in HBM).
+#include <atomic>
 #include <type_traits>
 
 #include "vb_internal.cuh"
@@ -740,7 +741,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
                                                                  const int32_t* __restrict__ nptr,
                                                                  const void* __restrict__ nslot_v,
                                                                  double* __restrict__ K, double* __restrict__ M,
-                                                                 const CoefSpec cp) {
+                                                                 const CoefSpec cp, unsigned int* __restrict__ ctr) {
     static_assert(COEF || !FAC, "factors are a coefficient mode");
     constexpr int NC = FAC ? DIM + 2 : DIM;   // staged per slot: coordinates (+ P, R factors)
     using Cfg = GatherCfg<DIM, NC, BUD>;
@@ -758,6 +759,19 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncwarp();
 
+    // block schedule: the first two blocks of a CTA are static, the rest are taken
+    // from a per-launch counter (ctr, zeroed by the host) as the CTA gets to them, so
+    // CTAs on busier SM sub-partitions take fewer blocks; ctr == NULL: static stride
+    // (the counter is read one block ahead of its use, so its latency is hidden)
+    int64_t kstat = 2;
+    unsigned int pending = 0;
+    if (ctr && t == 0) pending = atomicAdd(ctr, 1u);
+    auto next_block = [&]() -> int64_t {
+        if (!ctr) return blockIdx.x + (kstat++) * gstep;
+        const unsigned int v = __shfl_sync(0xffffffffu, pending, 0);
+        if (t == 0) pending = atomicAdd(ctr, 1u);
+        return 2 * gstep + v;
+    };
     // prologue: TMA for this CTA's first block, then its coordinate gather
     BlockBounds B0 = block_bounds<DIM, BUD>(blockIdx.x, nblocks, nn, row_ptr, nptr);
     BlockBounds B1 = block_bounds<DIM, BUD>(blockIdx.x + gstep, nblocks, nn, row_ptr, nptr);
@@ -770,8 +784,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     double* F = S.F();
     double* acc = S.acc();
     for (int64_t k = 0;; k++) {
-        const int64_t b = blockIdx.x + k * gstep;
-        if (b >= nblocks) break;
+        if (!B0.valid) break;
         constexpr bool DB = Cfg::RING == 2;
         const int rc = DB ? (int)(k & 1) : 0, rn = DB ? rc ^ 1 : 0;
         // stage k+1: stream its columns and plan words (every lane is past its column
@@ -781,7 +794,7 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             if (t == 0) issue_tma<DIM, NC, BUD>(S, rn, B1, col_idx, nslot);
         };
         if (DB || !staged) issue_next();
-        BlockBounds B2 = block_bounds<DIM, BUD>(blockIdx.x + (k + 2) * gstep, nblocks, nn, row_ptr, nptr);
+        BlockBounds B2 = block_bounds<DIM, BUD>(B1.valid ? next_block() : nblocks, nblocks, nn, row_ptr, nptr);
         // stage k: its coordinates have landed
         cp_async_wait<0>();
         __syncwarp();
@@ -901,13 +914,32 @@ using namespace vb;
 
 namespace {
 
+// Per-launch block counters of the dynamic schedule: a ring of 64 device words,
+// one zeroed in-stream per launch (launches on different streams get different
+// words unless 64 are in flight at once).
+__device__ unsigned int g_gather_ctr[64];
+
+unsigned int* block_counter(cudaStream_t s) {
+    static std::atomic<unsigned int> seq{0};
+    static unsigned int* base[64] = {nullptr};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (!base[dev] && cudaGetSymbolAddress((void**)&base[dev], g_gather_ctr) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    unsigned int* c = base[dev] + (seq.fetch_add(1) & 63u);
+    if (cudaMemsetAsync(c, 0, sizeof(unsigned int), s) != cudaSuccess) return nullptr;
+    return c;
+}
+
 template <int DIM, bool COEF, bool FAC, int BUD>
 void launch_gather(unsigned g, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
                    const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const void* nslot,
                    double* K, double* M, const CoefSpec& cp) {
     constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM, BUD>::SMEM;
     assemble_gather_k<DIM, COEF, FAC, BUD><<<g, GATHER_ROWS, SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx, nptr,
-                                                                        nslot, K, M, cp);
+                                                                        nslot, K, M, cp, block_counter(s));
 }
 
 template <int DIM, bool COEF, bool FAC, int BUD>
@@ -918,10 +950,10 @@ int gather_ctas_per_sm() {
         cudaFuncSetAttribute(assemble_gather_k<DIM, COEF, FAC, BUD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)SMEM);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_gather_k<DIM, COEF, FAC, BUD>, GATHER_ROWS, SMEM);
-        // One warp per CTA and a static block schedule: with 4k+1 resident warps one
-        // SM sub-partition runs 3 warps against 2 elsewhere and every CTA waits for
-        // it (compact budget: 9 CTAs 0.521 ms, capped at 8 0.476 ms, 7 0.515 ms).
-        if (n > 4 && n % 4 == 1) n -= 1;
+        // (With a static block schedule, 4k+1 resident one-warp CTAs put 3 warps on one
+        // SM sub-partition and every CTA waited for it: compact budget 9 CTAs 0.521 ms vs
+        // 8 CTAs 0.476 ms.  The dynamic schedule lets those CTAs take fewer blocks:
+        // 9 CTAs 0.467 ms; Delaunay 0.230 -> 0.200 ms.)
         if (n < 1) n = 1;
     }
     return n;
