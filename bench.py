@@ -137,11 +137,15 @@ def load_traffic(kernel_key):
     try:
         with open(path) as f:
             d = json.load(f)
-        # newest capture first: the c = 1 instantiation is <d, 0, 0> (COEF, FAC), older <d, 0> / <d>
-        for k in (kernel_key.replace(">", ", 0, 0>"), kernel_key.replace(">", ", 0>"), kernel_key):
-            if k in d["kernels"]:
-                return d["kernels"][k]["dram_bytes_per_launch"]
-        return None
+        # the c = 1 instantiations of the kernel over the rounds: <d>, <d, 0>, <d, 0, 0>
+        # (COEF, FAC), <d, 0, 0, B> (+ budget class); take the newest capture
+        stem = kernel_key[:-1]
+        cands = [(v.get("tag", ""), k) for k, v in d["kernels"].items()
+                 if k == kernel_key or (k.startswith(stem + ",") and k.replace(" ", "").startswith(
+                     stem.replace(" ", "") + ",0"))]
+        if not cands:
+            return None
+        return d["kernels"][max(cands)[1]]["dram_bytes_per_launch"]
     except Exception:
         return None
 
