@@ -379,3 +379,44 @@ def test_gather_budgets_and_plan_stats(dev, kind):
         assert relmax(h(Kc), Kco) <= 1e-12 and relmax(h(Mc), Mco) <= 1e-12
     for K, M in out[1:]:
         assert np.array_equal(out[0][0], K) and np.array_equal(out[0][1], M)
+
+
+@pytest.mark.parametrize("layout", ["aos", "aos4", "wide_elems"])
+def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
+    """The C ABI's strided addressing: coords[c*comp_stride + v*node_stride]
+    (AoS: stride dim; padded AoS: stride 4) and elems[a*elem_ld + e] with
+    elem_ld > ne, in both assembly variants, against the SoA result."""
+    import ctypes as C
+    coords, elems = synth.cube_kuhn_p1(6, jitter=0.05, seed=8)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan = vb.P1Plan(g(elems, dev), nn)
+    node_stride, comp_stride, eld = 1, nn, ne
+    if layout == "aos":
+        cbuf = g(np.ascontiguousarray(coords.T), dev)                         # (nn, 3)
+        node_stride, comp_stride = dim, 1
+    elif layout == "aos4":
+        pad = np.zeros((nn, 4))
+        pad[:, :dim] = coords.T
+        cbuf = g(pad, dev)
+        node_stride, comp_stride = 4, 1
+    else:
+        cbuf = g(coords, dev)
+    if layout == "wide_elems":
+        eld = ne + 37
+        wide = np.full((nv, eld), -1, dtype=np.int32)
+        wide[:, :ne] = elems
+        ebuf = g(wide, dev)
+    else:
+        ebuf = g(elems, dev)
+    L = vb.lib()
+    for mode in MODES:
+        K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+        M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+        vb._check(L.fem_p1_assemble(dim, nn, ne, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(ebuf), eld,
+                                    vb._ptr(plan.row_ptr), vb._ptr(plan.col_idx), plan.nnz, vb._ptr(plan.elem2nnz),
+                                    vb._ptr(plan.node_elem_ptr), vb._ptr(plan.node_elem),
+                                    vb._ptr(plan.node_elem_slot), vb._ptr(K), vb._ptr(M), None, None, mode, None))
+        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
