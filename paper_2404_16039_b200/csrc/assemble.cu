@@ -405,11 +405,6 @@ __device__ __forceinline__ void apply_coef(IncOut<DIM>& o, const double (&xv)[DI
     o.mrow = o.ad * wq * mrow;
 }
 
-// no per-vertex factors
-struct NoFac {
-    __device__ void operator()(int, double&, double&) const {}
-};
-
 // fv(s, P, R): the per-vertex coefficient factors of column slot s (FAC);
 // pv: those of the row's vertex
 // sl: the incidence's plan word; PK: packed 16-bit form (4 bits per other vertex)
@@ -893,7 +888,8 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
             };
             auto ix = [](int s) { return s; };
             const double pv[2] = {1.0, 1.0};
-            double mrow = gather_row<DIM, false, COEF, false, SW>(R.i0, R.i1, nslot, ev, NoFac{}, ix, aK, aM, xv, pv, cp);
+            auto nofac = [](int, double&, double&) {};   // no per-vertex factors on this path
+            double mrow = gather_row<DIM, false, COEF, false, SW>(R.i0, R.i1, nslot, ev, nofac, ix, aK, aM, xv, pv, cp);
             finish_row<DIM, 1, COEF>(R.L, s0, aK, aM, mrow);
         }
         __syncwarp();
