@@ -108,21 +108,19 @@ mtimes_fn pick_mtimes(int m, int k, int n) {
 }
 
 // ------------------------------------------------------------ a2 transpose
+// A page transpose in SoA layout is a permutation of planes: Z plane (j + i*cols)
+// = X plane (i + j*rows).  blockIdx.y picks the plane, threads stream pairs of
+// pages of it (128-bit loads and stores), so every access is coalesced and there
+// is no per-page register array.
 __global__ void __launch_bounds__(PAGE_BLOCK) transpose_k(int64_t np, const double* __restrict__ X, int rows, int cols,
                                                           int64_t ldx, double* __restrict__ Z, int64_t ldz, bool vec) {
+    const int q = blockIdx.y;
+    const int i = q % rows, j = q / rows;   // X(i, j) -> Z(j, i), Z is cols x rows
     const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
-    const int nplanes = rows * cols;
     for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; p < np; p += stride) {
-        double v[16][2];
-#pragma unroll
-        for (int q = 0; q < 16; q++)
-            if (q < nplanes) ld_pair(X, ldx, q, p, np, vec, v[q][0], v[q][1]);
-#pragma unroll
-        for (int q = 0; q < 16; q++)
-            if (q < nplanes) {
-                int i = q % rows, j = q / rows;              // X(i,j) -> Z(j,i), Z is cols x rows
-                st_pair(Z, ldz, j + i * cols, p, np, vec, v[q][0], v[q][1]);
-            }
+        double v0, v1;
+        ld_pair(X, ldx, q, p, np, vec, v0, v1);
+        st_pair(Z, ldz, j + i * cols, p, np, vec, v0, v1);
     }
 }
 
@@ -376,7 +374,10 @@ extern "C" vb_status vb_page_transpose(int64_t npages, const double* X, int rows
     if (!X || !Z) { set_error("vb_page_transpose: NULL %s", !X ? "X" : "Z"); return VB_ERR_ARG; }
     if (!ld_ok(ldx, npages, true) || !ld_ok(ldz, npages, false)) { set_error("vb_page_transpose: ld < npages"); return VB_ERR_ARG; }
     bool vec = vec_ok({{X, ldx}, {Z, ldz}});
-    unsigned g = grid_for((npages + 1) / 2, PAGE_BLOCK, PAGE_BLOCKS_PER_SM);
+    // rows*cols planes side by side in grid.y; about PAGE_BLOCKS_PER_SM resident CTAs per SM in all
+    const int nplanes = rows * cols;
+    const int bps = PAGE_BLOCKS_PER_SM / nplanes > 0 ? PAGE_BLOCKS_PER_SM / nplanes : 1;
+    const dim3 g(grid_for((npages + 1) / 2, PAGE_BLOCK, bps, nplanes < PAGE_BLOCKS_PER_SM ? 1 : 2), nplanes);
     transpose_k<<<g, PAGE_BLOCK, 0, cs(stream)>>>(npages, X, rows, cols, ldx, Z, ldz, vec);
     return launch_check("vb_page_transpose");
 }

@@ -1,0 +1,73 @@
+"""Runs every kernel family of libvb once (after a warm-up) on the BASELINE shapes,
+for one ncu metric capture of all of them (tools/ncu_all.sh):
+config 2 page ops (n = 2, 3, 4), config 3 surface, config 5 pattern + assembly
+(gather / atomic, c = 1 and NEXT-1 coefficients), config 4 2D assembly, NEXT-2
+load vector, NEXT-3 P2 (level 6, both variants), coords3D gather, bilinear."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2404_16039_b200 import vb  # noqa: E402
+
+dev = torch.device("cuda:0")
+N = 1 << 20
+
+
+def twice(fn):
+    fn()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("measured")
+    fn()
+    torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
+
+
+for n in (2, 3, 4):
+    A = torch.from_numpy(synth.normal_pages(n, n, N, stream=10)).to(dev)
+    B = torch.from_numpy(synth.normal_pages(n, n, N, stream=11)).to(dev)
+    X = torch.from_numpy(synth.inverse_pages(n, N, seed=0)[0]).to(dev)
+    twice(lambda: vb.vb_page_mtimes(A, B))
+    twice(lambda: vb.vb_page_transpose(A))
+    twice(lambda: vb.vb_page_det(A))
+    twice(lambda: vb.vb_page_inv(X))
+a3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=10)).to(dev)
+b3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=11)).to(dev)
+twice(lambda: vb.vb_page_cross(a3, b3))
+xyz, tri = synth.icosphere(10, perturb=0.01, seed=0)
+xd, td = torch.from_numpy(xyz).to(dev), torch.from_numpy(tri).to(dev)
+twice(lambda: vb.vb_tri_surface(xd, td))
+del xd, td
+
+c5, e5 = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
+cd, ed = torch.from_numpy(c5).to(dev), torch.from_numpy(e5).to(dev)
+twice(lambda: vb.P1Plan(ed, c5.shape[1]))
+plan = vb.P1Plan(ed, c5.shape[1])
+K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
+    twice(lambda: vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M))
+    twice(lambda: vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, mode=mode, K=K, M=M))
+twice(lambda: vb.vb_create_coords3D(cd, ed))
+fq = torch.ones((4, e5.shape[1]), dtype=torch.float64, device=dev)
+twice(lambda: vb.fem_p1_rhs(cd, ed, fq, plan=plan, gqo=2))
+Kl = torch.from_numpy(synth.normal_pages(4, 4, e5.shape[1], stream=10)).to(dev)
+u = torch.from_numpy(synth.normal_pages(4, 1, e5.shape[1], stream=11)).to(dev)
+twice(lambda: vb.vb_page_bilinear(u, Kl, u))
+del plan, K, M, cd, ed, Kl, u, fq
+
+c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
+cd4, ed4 = torch.from_numpy(c4).to(dev), torch.from_numpy(e4).to(dev)
+p4 = vb.P1Plan(ed4, c4.shape[1])
+for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
+    twice(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode))
+del p4, cd4, ed4
+
+c2, e2 = synth.p2_from_p1(*synth.cube_kuhn_p1(64, jitter=0.0, flip=(0, 0, 1)))
+cd2, ed2 = torch.from_numpy(c2).to(dev), torch.from_numpy(e2).to(dev)
+p2 = vb.Plan(ed2, c2.shape[1])
+for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
+    twice(lambda: vb.fem_p2_assemble(cd2, ed2, p2, mode=mode))
+print("ok")
