@@ -124,6 +124,62 @@ __global__ void __launch_bounds__(PAGE_BLOCK) transpose_k(int64_t np, const doub
     }
 }
 
+// ------------------------------------------------------------ avtamav (NEXT-2)
+// s_k = a_k^T M_k b_k = sum_i a_i (sum_j M_ij b_j) (eq:layeredBilin
+// P:292-301): every plane of a pair of pages loaded first (128-bit), then the
+// arithmetic.  a is n x 1, M is n x m, b is m x 1; ld 0 broadcasts.
+template <int N, int M>
+__global__ void __launch_bounds__(PAGE_BLOCK) bilinear_k(int64_t np, const double* __restrict__ A, int64_t lda,
+                                                         const double* __restrict__ Mx, int64_t ldm,
+                                                         const double* __restrict__ B, int64_t ldb,
+                                                         double* __restrict__ s, bool vec) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 2;
+    for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; p < np; p += stride) {
+        double a[N][2], b[M][2], m[N][M][2];
+#pragma unroll
+        for (int i = 0; i < N; i++) ld_pair(A, lda, i, p, np, vec, a[i][0], a[i][1]);
+#pragma unroll
+        for (int j = 0; j < M; j++) ld_pair(B, ldb, j, p, np, vec, b[j][0], b[j][1]);
+#pragma unroll
+        for (int j = 0; j < M; j++)
+#pragma unroll
+            for (int i = 0; i < N; i++) ld_pair(Mx, ldm, i + j * N, p, np, vec, m[i][j][0], m[i][j][1]);
+        double acc[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            double r = 0.0;
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                double t = 0.0;
+#pragma unroll
+                for (int j = 0; j < M; j++) t = fma(m[i][j][h], b[j][h], t);
+                r = fma(a[i][h], t, r);
+            }
+            acc[h] = r;
+        }
+        st_pair(s, np, 0, p, np, vec, acc[0], acc[1]);
+    }
+}
+
+typedef void (*bil_fn)(int64_t, const double*, int64_t, const double*, int64_t, const double*, int64_t, double*, bool);
+template <int N>
+bil_fn pick_bil_m(int m) {
+    switch (m) {
+        case 1: return bilinear_k<N, 1>;
+        case 2: return bilinear_k<N, 2>;
+        case 3: return bilinear_k<N, 3>;
+        default: return bilinear_k<N, 4>;
+    }
+}
+bil_fn pick_bilinear(int n, int m) {
+    switch (n) {
+        case 1: return pick_bil_m<1>(m);
+        case 2: return pick_bil_m<2>(m);
+        case 3: return pick_bil_m<3>(m);
+        default: return pick_bil_m<4>(m);
+    }
+}
+
 // ------------------------------------------------------------ closed forms
 template <int n>
 struct Page {
@@ -460,4 +516,21 @@ extern "C" vb_status vb_create_coords3D(int dim, int nv, int64_t ne, const doubl
     }
 #undef VB_GATHER
     return launch_check("vb_create_coords3D");
+}
+
+extern "C" vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A, int64_t lda, const double* Mx,
+                                      int64_t ldm, const double* B, int64_t ldb, double* s, vb_stream_t stream) {
+    clear_error();
+    if (npages < 0) { set_error("vb_page_bilinear: npages < 0"); return VB_ERR_ARG; }
+    if (n < 1 || n > 4 || m < 1 || m > 4) { set_error("vb_page_bilinear: n, m must be 1..4"); return VB_ERR_UNSUPPORTED; }
+    if (npages == 0) return VB_OK;
+    if (!A || !Mx || !B || !s) { set_error("vb_page_bilinear: NULL argument"); return VB_ERR_ARG; }
+    if (!ld_ok(lda, npages, true) || !ld_ok(ldm, npages, true) || !ld_ok(ldb, npages, true)) {
+        set_error("vb_page_bilinear: leading dimension < npages");
+        return VB_ERR_ARG;
+    }
+    const bool vec = vec_ok({{A, lda}, {Mx, ldm}, {B, ldb}, {s, npages}});
+    const unsigned g = grid_for((npages + 1) / 2, PAGE_BLOCK, PAGE_BLOCKS_PER_SM);
+    pick_bilinear(n, m)<<<g, PAGE_BLOCK, 0, cs(stream)>>>(npages, A, lda, Mx, ldm, B, ldb, s, vec);
+    return launch_check("vb_page_bilinear");
 }

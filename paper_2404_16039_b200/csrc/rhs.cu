@@ -103,46 +103,6 @@ __global__ void zero_k(double* __restrict__ a, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) a[i] = 0.0;
 }
 
-// s_k = a_k^T M_k b_k: sum_i a_i (sum_j M_ij b_j), pages in registers
-template <int N, int M>
-__global__ void __launch_bounds__(256) bilinear_k(int64_t np, const double* __restrict__ A, int64_t lda,
-                                                  const double* __restrict__ Mx, int64_t ldm,
-                                                  const double* __restrict__ B, int64_t ldb, double* __restrict__ s) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < np; k += stride) {
-        double bj[M];
-#pragma unroll
-        for (int j = 0; j < M; j++) bj[j] = ldb ? __ldcs(B + (int64_t)j * ldb + k) : __ldg(B + j);
-        double acc = 0.0;
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            double t = 0.0;
-#pragma unroll
-            for (int j = 0; j < M; j++) t = fma(ldm ? __ldcs(Mx + (int64_t)(i + j * N) * ldm + k) : __ldg(Mx + i + j * N), bj[j], t);
-            acc = fma(lda ? __ldcs(A + (int64_t)i * lda + k) : __ldg(A + i), t, acc);
-        }
-        stcs(s + k, acc);
-    }
-}
-
-typedef void (*bil_fn)(int64_t, const double*, int64_t, const double*, int64_t, const double*, int64_t, double*);
-template <int N>
-bil_fn pick_m(int m) {
-    switch (m) {
-        case 1: return bilinear_k<N, 1>;
-        case 2: return bilinear_k<N, 2>;
-        case 3: return bilinear_k<N, 3>;
-        default: return bilinear_k<N, 4>;
-    }
-}
-bil_fn pick_bilinear(int n, int m) {
-    switch (n) {
-        case 1: return pick_m<1>(m);
-        case 2: return pick_m<2>(m);
-        case 3: return pick_m<3>(m);
-        default: return pick_m<4>(m);
-    }
-}
 
 }  // namespace
 }  // namespace vb
@@ -194,15 +154,3 @@ extern "C" vb_status fem_p1_rhs(int dim, int64_t nn, int64_t ne, const double* c
     return launch_check("fem_p1_rhs");
 }
 
-extern "C" vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A, int64_t lda, const double* Mx,
-                                      int64_t ldm, const double* B, int64_t ldb, double* s, vb_stream_t stream) {
-    clear_error();
-    if (npages < 0) { set_error("vb_page_bilinear: npages < 0"); return VB_ERR_ARG; }
-    if (n < 1 || n > 4 || m < 1 || m > 4) { set_error("vb_page_bilinear: n, m must be 1..4"); return VB_ERR_UNSUPPORTED; }
-    if (npages == 0) return VB_OK;
-    if (!A || !Mx || !B || !s) { set_error("vb_page_bilinear: NULL argument"); return VB_ERR_ARG; }
-    for (int64_t ld : {lda, ldm, ldb})
-        if (ld != 0 && ld < npages) { set_error("vb_page_bilinear: leading dimension < npages"); return VB_ERR_ARG; }
-    pick_bilinear(n, m)<<<grid_for(npages, 256, 8), 256, 0, cs(stream)>>>(npages, A, lda, Mx, ldm, B, ldb, s);
-    return launch_check("vb_page_bilinear");
-}
