@@ -202,6 +202,29 @@ VB_API vb_status fem_plan_stats(int64_t nn, const int32_t* row_ptr, const int32_
 VB_API vb_status fem_plan_pack_slots(int dim, int64_t n_inc, const uint32_t* node_elem_slot, uint16_t* packed,
                                      void* work, vb_stream_t stream);
 
+/* Row classes of the P1 gather plan (the plan of the class variant,
+ * fem_p1_assemble_classes).  The row of node v is assembled from its
+ * incidences (plan words node_elem_slot[node_elem_ptr[v] ..], ascending
+ * element); its signature is (row length, incidence count, plan
+ * words).  Rows with equal signatures run the same operations on different
+ * coordinates, so a warp assembles up to 32 of them with one uniform loop.
+ * Outputs (DEVICE, caller-owned):
+ *   class_rows (nn int32): all rows, grouped by class (ascending row id within
+ *     a class); rows in classes of fewer than 8 rows, rows with more than 16
+ *     (3D) / 8 (2D) entries and rows without incidences form the last,
+ *     "mixed" class;
+ *   groups (groups_cap x 4 int32): group g = (first position in class_rows,
+ *     row count <= 32, first row of its class or -1 for the mixed class, 0).
+ * stats_out (HOST, 3 int64): number of groups, number of classes (mixed
+ * excluded), rows in classes.  work: DEVICE scratch; work == NULL queries its
+ * size into *work_bytes.  VB_ERR_WORKSPACE if the groups do not fit groups_cap
+ * (stats_out[0] then holds the count needed).  Deterministic; synchronises the
+ * stream (one small read-back). */
+VB_API vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_ptr, const int32_t* node_elem_ptr,
+                                  const uint32_t* node_elem_slot, void* work, size_t* work_bytes,
+                                  int32_t* class_rows, int32_t* groups, int64_t groups_cap,
+                                  int64_t* stats_out, vb_stream_t stream);
+
 /* ---------------------------------------------------------- a7..a17 assembly
  * Global P1 stiffness and mass matrices with c_K = c_M = 1 (eq:K_M P:967-975,
  * stiffness_matrixP1 P:978-1004, mass_matrixP1 P:1007), written
@@ -247,6 +270,21 @@ VB_API vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne,
                           double* K_vals, double* M_vals,
                           double* K_local, double* M_local,
                           int mode, vb_stream_t stream);
+
+/* The gather variant of fem_p1_assemble (c_K = c_M = 1; same arithmetic,
+ * ownership and summation order: ascending element per entry, diagonal from
+ * the partition of unity) driven by the row classes of fem_plan_classes: a warp
+ * takes one group (<= 32 rows of one class) and keeps each row's K and M sums
+ * in registers.  Rows of the mixed class are assembled in place in HBM.
+ * Arguments as fem_p1_assemble (node_elem_slot: the 32-bit plan words) plus
+ * class_rows, groups, ngroups from fem_plan_classes on the same plan.
+ * K_vals / M_vals (nnz, nullable) are overwritten.  Deterministic: the same
+ * bits as every run of this call. */
+VB_API vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                         int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx,
+                                         int64_t nnz, const int32_t* node_elem_ptr, const uint32_t* node_elem_slot,
+                                         const int32_t* class_rows, const int32_t* groups, int64_t ngroups,
+                                         double* K_vals, double* M_vals, vb_stream_t stream);
 
 /* ---------------------------------------------------------- NEXT-1: coefficients
  * As fem_p1_assemble, with the coefficient functions of eq:K_M

@@ -903,6 +903,200 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
     cp_async_wait<0>();
 }
 
+
+// ------------------------------------------------------------ class variant (row classes)
+// Same ownership, arithmetic and summation order as assemble_gather_k (one lane
+// per row, incidences in ascending element order, diagonal from the partition
+// of unity), but a warp takes up to 32 rows of one row class (fem_plan_classes:
+// rows with identical signature -- row length, incidence count and plan words).
+// The incidence loop is then warp-uniform: the class's plan words are read once
+// per warp (one per lane, broadcast with shuffles), the slots of an incidence
+// are the same on every lane, and each lane keeps its row's K and M sums in
+// registers (a uniform slot selects the register; no shared-memory
+// read-modify-write).  Edge vectors f_s = x_col(s) - x_v stay in shared memory
+// ([slot][coord][lane], conflict free).  Rows of the mixed class are assembled
+// by their lane in place in HBM (as assemble_gather_k's fallback).
+template <int DIM>
+struct ClassCfg {
+    static constexpr int MAXL = DIM == 3 ? 16 : 8;   // columns per row (fem_plan_classes' maxl)
+    static constexpr int FN = MAXL * DIM * 32;       // doubles of the edge-vector buffer
+};
+
+template <int N>
+__device__ __forceinline__ void acc_slot(double (&aK)[N], double (&aM)[N], int s, double k, double m) {
+#pragma unroll
+    for (int i = 0; i < N; i++)
+        if (s == i) {
+            aK[i] += k;
+            aM[i] += m;
+        }
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(32) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
+                                                       const int32_t* __restrict__ class_rows,
+                                                       const double* __restrict__ coords, int64_t ns, int64_t cst,
+                                                       const int32_t* __restrict__ row_ptr,
+                                                       const int32_t* __restrict__ col_idx,
+                                                       const int32_t* __restrict__ nptr,
+                                                       const uint32_t* __restrict__ nslot, double* __restrict__ K,
+                                                       double* __restrict__ M, unsigned int* __restrict__ ctr) {
+    constexpr int MAXL = ClassCfg<DIM>::MAXL;
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;   // 1/(d! (d+1)(d+2))
+    constexpr double KS = DIM == 2 ? -0.5 : -1.0 / 6.0;          // -1/d!
+    __shared__ __align__(16) double F[ClassCfg<DIM>::FN];
+    const int t = threadIdx.x;
+    unsigned int pending = 0;
+    if (t == 0) pending = atomicAdd(ctr, 1u);
+    int64_t g = blockIdx.x;
+    while (g < ngroups) {
+        const int4 G = groups[g];
+        {   // next group (dynamic schedule, fetched one group ahead)
+            const unsigned int nx = __shfl_sync(FULL, pending, 0);
+            if (t == 0) pending = atomicAdd(ctr, 1u);
+            g = (int64_t)gridDim.x + nx;
+        }
+        const int cnt = G.y, head = G.z;
+        const bool own = t < cnt;
+        const int32_t v = own ? __ldg(class_rows + G.x + t) : 0;
+        const int lo = own ? __ldg(row_ptr + v) : 0;
+        if (head >= 0) {
+            const int L = __ldg(row_ptr + head + 1) - __ldg(row_ptr + head);
+            const int ih = __ldg(nptr + head), n = __ldg(nptr + head + 1) - ih;
+            const int s0 = (int)(__ldg(nslot + ih) & 0xffu);
+            double xv[DIM];
+            if (own) {
+                for (int s = 0; s < L; s++) {
+                    const int64_t w = __ldg(col_idx + lo + s);
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) cp_async8(F + (s * DIM + c) * 32 + t, coords + c * cst + w * ns);
+                }
+#pragma unroll
+                for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + (int64_t)v * ns);
+            } else {
+#pragma unroll
+                for (int c = 0; c < DIM; c++) xv[c] = 0.0;
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+            __syncwarp();
+            // edge vectors from the row's vertex (lanes without a row hold garbage: never stored)
+#pragma unroll
+            for (int s = 0; s < MAXL; s++)
+                if (s < L && s != s0)
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) F[(s * DIM + c) * 32 + t] -= xv[c];
+            double aK[MAXL], aM[MAXL];
+#pragma unroll
+            for (int s = 0; s < MAXL; s++) aK[s] = aM[s] = 0.0;
+            auto ld = [&](int s, double (&f)[DIM]) {
+#pragma unroll
+                for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * 32 + t];
+            };
+            for (int i0 = 0; i0 < n; i0 += 32) {
+                const uint32_t pw = i0 + t < n ? __ldg(nslot + ih + i0 + t) : 0u;
+                const int m = n - i0 < 32 ? n - i0 : 32;
+                for (int j = 0; j < m; j++) {
+                    const uint32_t w = __shfl_sync(FULL, pw, j);
+                    if constexpr (DIM == 3) {
+                        const int s1 = (w >> 8) & 0xff, s2 = (w >> 16) & 0xff, s3 = w >> 24;
+                        double f1[3], f2[3], f3[3];
+                        ld(s1, f1);
+                        ld(s2, f2);
+                        ld(s3, f3);
+                        const double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
+                                              fma(f2[0], f3[1], -f2[1] * f3[0])};
+                        const double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
+                                              fma(f3[0], f1[1], -f3[1] * f1[0])};
+                        const double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
+                                              fma(f1[0], f2[1], -f1[1] * f2[0])};
+                        const double ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
+                        const double r = rcp_nr(ad);
+                        double S[3];
+#pragma unroll
+                        for (int c = 0; c < 3; c++) S[c] = r * ((h1[c] + h2[c]) + h3[c]);
+                        acc_slot<MAXL>(aK, aM, s1, fma(S[0], h1[0], fma(S[1], h1[1], S[2] * h1[2])), ad);
+                        acc_slot<MAXL>(aK, aM, s2, fma(S[0], h2[0], fma(S[1], h2[1], S[2] * h2[2])), ad);
+                        acc_slot<MAXL>(aK, aM, s3, fma(S[0], h3[0], fma(S[1], h3[1], S[2] * h3[2])), ad);
+                    } else {
+                        const int s1 = (w >> 8) & 0xff, s2 = (w >> 16) & 0xff;
+                        double f1[2], f2[2];
+                        ld(s1, f1);
+                        ld(s2, f2);
+                        // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
+                        const double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
+                        const double r = rcp_nr(ad);
+                        const double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
+                        acc_slot<MAXL>(aK, aM, s1, fma(hax, f2[1], -hay * f2[0]), ad);
+                        acc_slot<MAXL>(aK, aM, s2, fma(-hax, f1[1], hay * f1[0]), ad);
+                    }
+                }
+            }
+            __syncwarp();   // every lane is done with the edge vectors
+            // finish the rows (diagonal from the partition of unity) and stage them in
+            // CSR order: row t of the group at [t*L, t*L + L)
+            double* stK = F;
+            double* stM = F + 32 * MAXL;
+            if (own) {
+                double sk = 0.0, sm = 0.0;
+#pragma unroll
+                for (int s = 0; s < MAXL; s++)
+                    if (s < L && s != s0) {
+                        const double kk = aK[s] * KS, mm = aM[s] * MS;
+                        sk += kk;
+                        sm += mm;
+                        stK[t * L + s] = kk;
+                        stM[t * L + s] = mm;
+                    }
+                stK[t * L + s0] = -sk;
+                stM[t * L + s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
+            }
+            __syncwarp();
+            const int tot = cnt * L;
+            for (int q0 = 0; q0 < tot; q0 += 32) {
+                const int q = q0 + t;
+                int r = q / L;
+                r = r < 31 ? r : 31;
+                const int p = __shfl_sync(FULL, lo, r) + (q - r * L);
+                if (q < tot) {
+                    if (K) stcs(K + p, stK[q]);
+                    if (M) stcs(M + p, stM[q]);
+                }
+            }
+            __syncwarp();   // the staging area is the next group's edge-vector buffer
+        } else if (own) {
+            // mixed class: the lane's row in place in HBM
+            const int L = __ldg(row_ptr + v + 1) - lo;
+            const int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
+            if (L > 0) {
+                double* aK = K ? K + lo : nullptr;
+                double* aM = M ? M + lo : nullptr;
+                int s0 = 0;
+                for (int q = 0; q < L; q++) {
+                    if (aK) aK[q] = 0.0;
+                    if (aM) aM[q] = 0.0;
+                    if (__ldg(col_idx + lo + q) == v) s0 = q;
+                }
+                double xv[DIM];
+#pragma unroll
+                for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + (int64_t)v * ns);
+                auto ev = [&](int s, double(&f)[DIM]) {
+                    int64_t w = __ldg(col_idx + lo + s);
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
+                };
+                auto ix = [](int s) { return s; };
+                const double pv[2] = {1.0, 1.0};
+                auto nofac = [](int, double&, double&) {};
+                const CoefSpec cp{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
+                gather_row<DIM, false, false, false, uint32_t>(i0, i1, nslot, ev, nofac, ix, aK, aM, xv, pv, cp);
+                finish_row<DIM, 1, false>(L, s0, aK, aM, 0.0);
+            }
+        }
+    }
+}
+
 }  // namespace
 }  // namespace vb
 
@@ -1079,4 +1273,40 @@ extern "C" vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const
     return assemble_entry("fem_p1_assemble_coef", dim, nn, ne, coords, node_stride, comp_stride, elems, elem_ld,
                           row_ptr, col_idx, nnz, elem2nnz, node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local,
                           M_local, mode, &cp, stream);
+}
+
+extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                             int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx,
+                                             int64_t nnz, const int32_t* node_elem_ptr,
+                                             const uint32_t* node_elem_slot, const int32_t* class_rows,
+                                             const int32_t* groups, int64_t ngroups, double* K_vals,
+                                             double* M_vals, vb_stream_t stream) {
+    const char* fn = "fem_p1_assemble_classes";
+    clear_error();
+    if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
+    if (nn < 0 || nnz < 0 || ngroups < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
+    if (!K_vals && !M_vals) return VB_OK;
+    if (nn > 0 && (!coords || !row_ptr || !col_idx || !node_elem_ptr || !node_elem_slot || !class_rows || !groups)) {
+        set_error("%s: NULL argument", fn);
+        return VB_ERR_ARG;
+    }
+    if (ngroups == 0) return VB_OK;
+    cudaStream_t s = cs(stream);
+    unsigned int* ctr = block_counter(s);
+    if (!ctr) { set_error("%s: block counter unavailable", fn); return VB_ERR_CUDA; }
+    auto launch = [&](auto kern) {
+        static int occ[2] = {0, 0};
+        int& n = occ[dim - 2];
+        if (!n) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32, 0);
+            if (n < 1) n = 1;
+        }
+        const int64_t cap = (int64_t)sm_count() * n;
+        const unsigned g = (unsigned)(ngroups < cap ? ngroups : cap);
+        kern<<<g, 32, 0, s>>>(ngroups, reinterpret_cast<const int4*>(groups), class_rows, coords, node_stride,
+                              comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr);
+    };
+    if (dim == 3) launch(assemble_class_k<3>);
+    else launch(assemble_class_k<2>);
+    return launch_check(fn);
 }

@@ -44,7 +44,8 @@ _STATUS = {0: "VB_OK", -1: "VB_ERR_ARG", -2: "VB_ERR_DIM", -3: "VB_ERR_UNSUPPORT
 EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpose", "vb_page_det",
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
-           "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots")
+           "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
+           "fem_p1_assemble_classes")
 
 
 class VbError(RuntimeError):
@@ -85,6 +86,8 @@ def lib():
             "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
             "fem_plan_stats": (i32, [i64, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_plan_pack_slots": (i32, [i32, i64, p, p, p, p]),
+            "fem_plan_classes": (i32, [i32, i64, p, p, p, p, sz, p, p, i64, C.POINTER(C.c_int64), p]),
+            "fem_p1_assemble_classes": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -280,6 +283,43 @@ class P1Plan:
                         and self.stats[2] <= 25 * 32)
         self.node_elem_slot16 = self.pack_slots() if self.compact else None
 
+    def classes(self):
+        """Row classes of the gather plan (fem_plan_classes), built once and kept:
+        class_rows (nn,) int32, groups (ngroups, 4) int32, class_stats = (groups,
+        classes, rows in classes).  None without a gather plan."""
+        if self.node_elem_ptr is None:
+            return None
+        if getattr(self, "class_rows", None) is None:
+            dev = self.row_ptr.device
+            L = lib()
+            sz = C.c_size_t(0)
+            st = _stream()
+            stats = (C.c_int64 * 3)()
+            _check(L.fem_plan_classes(self.dim, self.nn, None, None, None, None, C.byref(sz), None, None, 0, stats,
+                                      st))
+            work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
+            self.class_rows = torch.empty((max(self.nn, 1),), dtype=torch.int32, device=dev)
+            cap = self.nn // 32 + 1024
+            while True:
+                groups = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+                rc = L.fem_plan_classes(self.dim, self.nn, _ptr(self.row_ptr), _ptr(self.node_elem_ptr),
+                                        _ptr(self.node_elem_slot), _ptr(work), C.byref(sz), _ptr(self.class_rows),
+                                        _ptr(groups), cap, stats, st)
+                if rc == -5 and stats[0] > cap:
+                    cap = int(stats[0])
+                    continue
+                _check(rc)
+                break
+            self.groups = groups[:int(stats[0])]
+            self.class_stats = tuple(int(x) for x in stats)
+        return self.class_rows
+
+    def class_coverage(self):
+        """Fraction of rows that the class variant assembles with the uniform loop."""
+        if self.classes() is None or self.nn == 0:
+            return 0.0
+        return self.class_stats[2] / self.nn
+
     def pack_slots(self):
         """The packed 16-bit plan words of the compact gather budget (fem_plan_pack_slots)."""
         n = self.nv * self.ne
@@ -294,9 +334,38 @@ def fem_p1_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
     return P1Plan(elems, nn, scatter_map, gather_plan, stream)
 
 
+def _use_classes(plan, variant):
+    """Gather variant: "class" (row classes, fem_p1_assemble_classes), "block"
+    (32-row blocks, fem_p1_assemble) or None = "class" when at least 90 % of the
+    rows fall into row classes (meshes from uniform refinement), else "block"."""
+    if variant not in (None, "class", "block"):
+        raise ValueError("variant must be None, 'class' or 'block'")
+    if variant == "block" or plan.node_elem_ptr is None:
+        return False
+    if variant == "class":
+        return True
+    return plan.class_coverage() >= 0.9
+
+
+def fem_p1_assemble_classes(coords, plan, K=None, M=None, want_K=True, want_M=True, stream=None):
+    """Gather-variant K, M through the row classes of the plan (fem_p1_assemble_classes)."""
+    _f64(coords)
+    dim, nn = coords.shape
+    dev = coords.device
+    K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
+    M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
+    plan.classes()
+    _check(lib().fem_p1_assemble_classes(dim, nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr), _ptr(plan.col_idx),
+                                         plan.nnz, _ptr(plan.node_elem_ptr), _ptr(plan.node_elem_slot),
+                                         _ptr(plan.class_rows), _ptr(plan.groups), plan.groups.shape[0], _ptr(K),
+                                         _ptr(M), _stream(stream)))
+    return K, M
+
+
 def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False,
-                    K=None, M=None, stream=None, compact=None):
-    """Returns (K_vals, M_vals, K_local, M_local) (None where not requested)."""
+                    K=None, M=None, stream=None, compact=None, variant=None):
+    """Returns (K_vals, M_vals, K_local, M_local) (None where not requested).
+    Gather mode: `variant` as _use_classes."""
     _f64(coords)
     dim, nn = coords.shape
     nv, ne = elems.shape
@@ -311,6 +380,13 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         M = None
     Kl = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
     Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    if mode == VB_ASSEMBLE_GATHER and (K is not None or M is not None) and _use_classes(plan, variant):
+        fem_p1_assemble_classes(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
+        if want_local:
+            _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
+                                         None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
+                                         _stream(stream)))
+        return K, M, Kl, Ml
     gmode, words = _gather_mode(mode, plan, compact)
     _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                  _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),

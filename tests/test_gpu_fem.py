@@ -15,7 +15,9 @@ import synth
 from paper_2404_16039_b200 import vb
 
 pytestmark = pytest.mark.gpu
-MODES = [vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC]
+# (mode, gather variant): row classes, 32-row blocks, atomic scatter
+MODES = [(vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"), (vb.VB_ASSEMBLE_ATOMIC, None)]
+MODE_IDS = ["class", "block", "atomic"]
 
 
 @pytest.fixture(scope="module")
@@ -87,7 +89,7 @@ def test_pattern_and_plans_bit_exact(dev, kind, n):
 
 
 # ---------------------------------------------------------------- assembly
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
 @pytest.mark.parametrize("kind,n", [("2d", 1), ("2d", 32), ("2d", 50), ("3d", 1), ("3d", 6), ("3d", 11)])
 def test_assembly_parity(dev, kind, n, mode):
     coords, elems = mesh(kind, n, seed=1)
@@ -96,22 +98,63 @@ def test_assembly_parity(dev, kind, n, mode):
     Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
     cd, ed = g(coords, dev), g(elems, dev)
     plan = vb.P1Plan(ed, nn)
-    K, M, Kl, Ml = vb.fem_p1_assemble(cd, ed, plan, mode=mode, want_local=True)
+    K, M, Kl, Ml = vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1], want_local=True)
     assert relmax(h(K), Ko) <= 1e-12
     assert relmax(h(M), Mo) <= 1e-12
     K3o, M3o = oracle.p1_local_all(coords, elems)
     assert relmax(h(Kl), K3o) <= 1e-12 and relmax(h(Ml), M3o) <= 1e-12
 
 
-def test_gather_variant_bitwise_reproducible(dev):
+@pytest.mark.parametrize("variant", ["class", "block"])
+def test_gather_variant_bitwise_reproducible(dev, variant):
     coords, elems = mesh("3d", 12, seed=2)
     cd, ed = g(coords, dev), g(elems, dev)
     plan = vb.P1Plan(ed, coords.shape[1])
-    K1, M1, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER)
+    K1, M1, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER, variant=variant)
     K1, M1 = h(K1), h(M1)
     for _ in range(3):
-        K2, M2, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER)
+        K2, M2, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER, variant=variant)
         assert np.array_equal(h(K2), K1) and np.array_equal(h(M2), M1)
+
+
+def signature(v, rp, nptr, nsl):
+    return (int(rp[v + 1] - rp[v]), tuple(int(x) for x in nsl[nptr[v]:nptr[v + 1]]))
+
+
+@pytest.mark.parametrize("kind,n", [("2d", 9), ("3d", 1), ("3d", 7), ("3d", 10), ("delaunay3", 6)])
+def test_row_classes_plan(dev, kind, n):
+    """fem_plan_classes: class_rows is a permutation of the rows; every group is
+    up to 32 rows of one class, all with the signature of the class's first
+    row (row length and plan words, checked here word by word on the host);
+    mixed rows are the last groups; Kuhn cubes put >= 90 % of rows in classes."""
+    if kind == "delaunay3":
+        coords, elems = synth.delaunay_p1(3, n, seed=0)
+    else:
+        coords, elems = mesh(kind, n)
+    nn = coords.shape[1]
+    plan = vb.P1Plan(g(elems, dev), nn)
+    plan.classes()
+    rows, groups = h(plan.class_rows)[:nn], h(plan.groups)
+    assert np.array_equal(np.sort(rows), np.arange(nn))
+    rp, nptr, nsl = h(plan.row_ptr), h(plan.node_elem_ptr), h(plan.node_elem_slot).view(np.uint32)
+    assert groups[0, 0] == 0 and np.all(groups[1:, 0] == groups[:-1, 0] + groups[:-1, 1])
+    assert groups[-1, 0] + groups[-1, 1] == nn
+    assert np.all((groups[:, 1] >= 1) & (groups[:, 1] <= 32))
+    seen_mixed = False
+    in_classes = 0
+    for pos, cnt, head, _ in groups:
+        if head < 0:
+            seen_mixed = True
+            continue
+        assert not seen_mixed                        # mixed rows come last
+        ref = signature(head, rp, nptr, nsl)
+        assert ref[0] <= (16 if elems.shape[0] == 4 else 8)
+        for v in rows[pos:pos + cnt]:
+            assert signature(v, rp, nptr, nsl) == ref
+        in_classes += cnt
+    assert plan.class_stats[0] == len(groups) and plan.class_stats[2] == in_classes
+    if kind in ("2d", "3d") and n >= 9:
+        assert plan.class_coverage() >= 0.9
 
 
 def test_unjittered_square_stencil_bitwise_on_gpu(dev):
@@ -122,7 +165,7 @@ def test_unjittered_square_stencil_bitwise_on_gpu(dev):
     cd, ed = g(coords, dev), g(elems, dev)
     plan = vb.P1Plan(ed, nn)
     for mode in MODES:
-        K, _, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode)
+        K, _, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1])
         assert np.array_equal(h(K), Ko)           # dyadic values: exact in any order
 
 
@@ -152,7 +195,7 @@ def test_empty_mesh_and_isolated_nodes(dev):
     assert plan.nnz == 0 and np.array_equal(h(plan.row_ptr), np.zeros(6, dtype=np.int32))
     cd = torch.zeros((3, 5), dtype=torch.float64, device=dev)
     for mode in MODES:
-        vb.fem_p1_assemble(cd, ed, plan, mode=mode)
+        vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1])
     # one element plus isolated nodes (empty rows)
     coords = np.zeros((3, 9))
     coords[:, [2, 5, 6, 8]] = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], dtype=np.float64).T
@@ -162,7 +205,7 @@ def test_empty_mesh_and_isolated_nodes(dev):
     plan = vb.P1Plan(g(elems, dev), 9)
     assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
     for mode in MODES:
-        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
+        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode[0], variant=mode[1])
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
 
 
@@ -195,7 +238,7 @@ def test_long_rows_fallback_paths(dev, k, fans):
     plan = vb.P1Plan(g(elems, dev), nn)
     assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
     for mode in MODES:
-        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
+        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode[0], variant=mode[1])
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
 
 
@@ -239,7 +282,7 @@ def test_full_size_assembly_sampled(dev, cfg):
     rows = np.repeat(np.arange(nn), np.diff(rp))
     sel = mask[rows] == 1
     for mode in MODES:
-        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode)
+        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1])
         K, M = h(K), h(M)
         assert relmax(K[sel], Ko[sel]) <= 1e-12
         assert relmax(M[sel], Mo[sel]) <= 1e-12
@@ -288,13 +331,13 @@ def test_delaunay_meshes_parity(dev, dim, n, permute):
     assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
     assert np.array_equal(h(plan.elem2nnz), expected_elem2nnz(elems, rp, ci))
     for mode in MODES:
-        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode)
+        K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan, mode=mode[0], variant=mode[1])
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
     for cK, cM in (((2.0, (0.4, -0.3, 0.2)), (0.5, (-0.6, 0.1, 0.8))),
                    ((1.3, (0.7, 0.2, -0.5)), (1.3, (0.7, 0.2, -0.5)))):
         Ko, Mo = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cK, cM=cM)
         for mode in MODES:
-            K, M = vb.fem_p1_assemble_coef(g(coords, dev), g(elems, dev), plan, gqo=2, cK=cK, cM=cM, mode=mode)[:2]
+            K, M = vb.fem_p1_assemble_coef(g(coords, dev), g(elems, dev), plan, gqo=2, cK=cK, cM=cM, mode=mode[0])[:2]
             assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
 
 
@@ -412,7 +455,7 @@ def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
     else:
         ebuf = g(elems, dev)
     L = vb.lib()
-    for mode in MODES:
+    for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
         K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
         M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
         vb._check(L.fem_p1_assemble(dim, nn, ne, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(ebuf), eld,
@@ -420,3 +463,12 @@ def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
                                     vb._ptr(plan.node_elem_ptr), vb._ptr(plan.node_elem),
                                     vb._ptr(plan.node_elem_slot), vb._ptr(K), vb._ptr(M), None, None, mode, None))
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+    # the class variant with the same strided coordinates
+    plan.classes()
+    K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+    M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+    vb._check(L.fem_p1_assemble_classes(dim, nn, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(plan.row_ptr),
+                                        vb._ptr(plan.col_idx), plan.nnz, vb._ptr(plan.node_elem_ptr),
+                                        vb._ptr(plan.node_elem_slot), vb._ptr(plan.class_rows), vb._ptr(plan.groups),
+                                        plan.groups.shape[0], vb._ptr(K), vb._ptr(M), None))
+    assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
