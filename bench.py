@@ -13,7 +13,11 @@ API from pinned host buffers: H2D of coords+elems, fem_p1_pattern (both
 phases), fem_p1_assemble, D2H of row_ptr, col_idx, K and M -- every step.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl vb|reference]
-       [--variant gather|atomic] [--quick]
+       [--variant class|block|atomic] [--quick]
+Variants of the numeric phase: "class" (default; deterministic gather over the
+row classes of the plan, fem_p1_assemble_classes), "block" (deterministic gather
+over 32-row blocks, fem_p1_assemble VB_ASSEMBLE_GATHER), "atomic" (fp64 atomics
+through the scatter map, VB_ASSEMBLE_ATOMIC).
 Multi-GPU (torchrun): one independent replica of the workload per rank
 ("replicas only"), weak scaling, max-over-ranks time.
 """
@@ -164,7 +168,8 @@ def run_vb(args):
     if ws > 1:
         tdist.init_process_group("nccl", device_id=dev)
     peak, peak_src = peaks()
-    mode = vb.VB_ASSEMBLE_GATHER if args.variant == "gather" else vb.VB_ASSEMBLE_ATOMIC
+    mode = vb.VB_ASSEMBLE_ATOMIC if args.variant == "atomic" else vb.VB_ASSEMBLE_GATHER
+    gvar = args.variant if args.variant != "atomic" else None
 
     coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
     dim, nn = coords.shape
@@ -176,8 +181,11 @@ def run_vb(args):
     # load, allocator growth), then the median of 3 warm builds (host wall clock; the
     # count phase has a documented nnz read-back)
     def build_plan():
-        return vb.P1Plan(ed, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
-                         gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+        p = vb.P1Plan(ed, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
+                      gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+        if gvar == "class":
+            p.classes()    # the row classes are part of this variant's plan
+        return p
     plan = build_plan()
     pts = []
     for _ in range(3):
@@ -192,7 +200,7 @@ def run_vb(args):
     M = torch.empty(nnz, dtype=torch.float64, device=dev)
 
     def step():
-        vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M)
+        vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M, variant=gvar)
 
     for _ in range(args.warmup):
         step()
@@ -221,7 +229,7 @@ def run_vb(args):
     avg_launch_ms = statistics.mean(launch_ms)
     alg = alg_bytes_assembly(dim, nn, ne, nnz)
     achieved = alg / (avg_launch_ms * 1e-3) / 1e9
-    kname = "assemble_gather_k<3>" if mode == vb.VB_ASSEMBLE_GATHER else "assemble_atomic_k<3>"
+    kname = {"class": "assemble_class_k<3>", "block": "assemble_gather_k<3>"}.get(gvar, "assemble_atomic_k<3>")
     traffic = load_traffic(kname)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -271,7 +279,7 @@ def run_vb(args):
             with torch.cuda.stream(s):
                 p2 = vb.P1Plan(e2, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
                                gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
-                K2, M2, _, _ = vb.fem_p1_assemble(c2, e2, p2, mode=mode)
+                K2, M2, _, _ = vb.fem_p1_assemble(c2, e2, p2, mode=mode, variant=gvar)
                 done = torch.cuda.Event()
                 done.record(s)
             down.wait_event(done)
@@ -302,7 +310,7 @@ def run_vb(args):
                "d2h_bytes_per_step": (nn + 1) * 4 + nnz * 4 + 2 * nnz * 8,
                "steps": n_e2e, "ms_per_step": e2e_ms / n_e2e,
                "includes": "per step: H2D coords+elems from pinned memory, fem_p1_pattern (count+fill), "
-                           "fem_p1_assemble, D2H row_ptr/col_idx/K/M to pinned memory; upload / 2 compute / "
+                           "fem_plan_classes (class variant), the assembly, D2H row_ptr/col_idx/K/M to pinned memory; upload / 2 compute / "
                            "download streams, host wall clock with device syncs on both sides"}
 
     secondary = None
@@ -322,7 +330,8 @@ def run_vb(args):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded Kuhn-cube mesh, synth/)",
         "config": {"workload": WORKLOAD5, "variant": args.variant,
-                   "timed": "fem_p1_assemble per step (numeric K+M assembly on the resident plan)",
+                   "timed": "one numeric K+M assembly per step on the resident plan (%s)" % (
+                       "fem_p1_assemble_classes" if gvar == "class" else "fem_p1_assemble"),
                    "pattern_ms": round(pattern_ms, 3), "nnz": nnz, "ne": ne, "nn": nn,
                    "l2": "no flush: every step streams %.0f MB (> 126 MB L2)" % (alg / 1e6),
                    "parallelism": "replicas" if ws > 1 else "single GPU"},
@@ -368,16 +377,31 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
                     unit_name + "_per_s": units / (med * 1e-3), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1),
                     "frac": round(nbytes / (med * 1e-3) / 1e9 / peak, 4)})
 
-    # other assembly variant on config 5
+    # the other assembly variants on config 5
     nn5, ne5 = coords5.shape[1], elems5.shape[1]
-    other = "atomic" if args.variant == "gather" else "gather"
-    p_other = vb.P1Plan(ed5, nn5, scatter_map=(other == "atomic"), gather_plan=(other == "gather"))
-    mo = vb.VB_ASSEMBLE_ATOMIC if other == "atomic" else vb.VB_ASSEMBLE_GATHER
-    K = torch.empty(p_other.nnz, dtype=torch.float64, device=dev)
-    M = torch.empty(p_other.nnz, dtype=torch.float64, device=dev)
-    rec("config5 assembly variant=%s" % other, ne5, "elements", alg_bytes_assembly(3, nn5, ne5, p_other.nnz),
-        time_kernel(lambda: vb.fem_p1_assemble(cd5, ed5, p_other, mode=mo, K=K, M=M), 10))
-    del p_other, K, M
+    for other in ("class", "block", "atomic"):
+        if other == args.variant:
+            continue
+        p_other = vb.P1Plan(ed5, nn5, scatter_map=(other == "atomic"), gather_plan=(other != "atomic"))
+        mo = vb.VB_ASSEMBLE_ATOMIC if other == "atomic" else vb.VB_ASSEMBLE_GATHER
+        gv = None if other == "atomic" else other
+        K = torch.empty(p_other.nnz, dtype=torch.float64, device=dev)
+        M = torch.empty(p_other.nnz, dtype=torch.float64, device=dev)
+        rec("config5 assembly variant=%s" % other, ne5, "elements", alg_bytes_assembly(3, nn5, ne5, p_other.nnz),
+            time_kernel(lambda: vb.fem_p1_assemble(cd5, ed5, p_other, mode=mo, K=K, M=M, variant=gv), 10))
+        del p_other, K, M
+    # class plan build on config 5 (one-time, after the pattern)
+    if plan5.node_elem_ptr is None:
+        plan5 = vb.P1Plan(ed5, nn5, scatter_map=False, gather_plan=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        plan5.class_rows = None
+        plan5.classes()
+    torch.cuda.synchronize()
+    res.append({"name": "config5 fem_plan_classes (row classes of the gather plan)",
+                "ms": round((time.perf_counter() - t0) * 1e3 / 2, 3), "classes": plan5.class_stats[1],
+                "groups": plan5.class_stats[0], "rows_in_classes": plan5.class_stats[2]})
     # pattern build on config 5 (one-time plan)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -419,10 +443,12 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     p4 = vb.P1Plan(ed4, c4.shape[1])
     K4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
     M4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
-    for name, mode in (("gather", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+    for name, mode in (("class", vb.VB_ASSEMBLE_GATHER), ("block", vb.VB_ASSEMBLE_GATHER),
+                       ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+        gv = None if name == "atomic" else name
         rec("config4 2D assembly variant=%s" % name, e4.shape[1], "elements",
             alg_bytes_assembly(2, c4.shape[1], e4.shape[1], p4.nnz),
-            time_kernel(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode, K=K4, M=M4), 10))
+            time_kernel(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode, K=K4, M=M4, variant=gv), 10))
     del p4, K4, M4, cd4, ed4
     # config 1: latency only
     c1, e1 = synth.square_p1(32, jitter=0.1, seed=0)
@@ -569,7 +595,8 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="vb", choices=["vb", "reference"])
-    ap.add_argument("--variant", default="gather", choices=["gather", "atomic"])
+    ap.add_argument("--variant", default="class", choices=["class", "block", "gather", "atomic"],
+                    help="gather = block (older name)")
     ap.add_argument("--quick", action="store_true", help="headline only (no secondary rows)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -577,6 +604,8 @@ def main():
     ap.add_argument("--cpu-layers", type=int, default=8)
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
     args = ap.parse_args()
+    if args.variant == "gather":
+        args.variant = "block"
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
     if args.impl == "reference":

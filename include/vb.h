@@ -210,8 +210,9 @@ VB_API vb_status fem_plan_pack_slots(int dim, int64_t n_inc, const uint32_t* nod
  * coordinates, so a warp assembles up to 32 of them with one uniform loop.
  * Outputs (DEVICE, caller-owned):
  *   class_rows (nn int32): all rows, grouped by class (ascending row id within
- *     a class); rows in classes of fewer than 8 rows, rows with more than 16
- *     (3D) / 8 (2D) entries and rows without incidences form the last,
+ *     a class); rows in classes of fewer than 8 rows, rows with more than 15
+ *     (3D) / 8 (2D) entries or more than 32 (3D) / 16 (2D) incidences and rows
+ *     without incidences form the last,
  *     "mixed" class;
  *   groups (groups_cap x 4 int32): group g = (first position in class_rows,
  *     row count <= 32, first row of its class or -1 for the mixed class, 0).

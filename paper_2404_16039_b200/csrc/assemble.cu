@@ -909,136 +909,296 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 // per row, incidences in ascending element order, diagonal from the partition
 // of unity), but a warp takes up to 32 rows of one row class (fem_plan_classes:
 // rows with identical signature -- row length, incidence count and plan words).
-// The incidence loop is then warp-uniform: the class's plan words are read once
-// per warp (one per lane, broadcast with shuffles), the slots of an incidence
-// are the same on every lane, and each lane keeps its row's K and M sums in
-// registers (a uniform slot selects the register; no shared-memory
-// read-modify-write).  Edge vectors f_s = x_col(s) - x_v stay in shared memory
-// ([slot][coord][lane], conflict free).  Rows of the mixed class are assembled
-// by their lane in place in HBM (as assemble_gather_k's fallback).
+// The incidence loop is then warp-uniform: the class's plan words are decoded
+// once per warp into a shared-memory table (the edge-vector offsets of each
+// incidence, read with one broadcast load), the slots of an incidence are the
+// same on every lane, and each lane keeps its row's K and M sums in registers:
+// a uniform slot picks the register through an indexed branch (brx.idx, one
+// jump-table load + branch per update) instead of a shared-memory
+// read-modify-write.  Edge vectors f_s = x_col(s) - x_v stay in shared memory
+// ([slot][coord][lane], conflict free).  Loads are pipelined one group ahead:
+// the next group's rows and columns (cp.async) are requested before the
+// current group's incidence loop.  Rows of the mixed class are assembled by
+// their lane in place in HBM (as assemble_gather_k's fallback).
 template <int DIM>
 struct ClassCfg {
-    static constexpr int MAXL = DIM == 3 ? 16 : 8;   // columns per row (fem_plan_classes' maxl)
-    static constexpr int FN = MAXL * DIM * 32;       // doubles of the edge-vector buffer
+    static constexpr int MAXL = DIM == 3 ? 16 : 8;   // register accumulators per row (acc_slot)
+    static constexpr int FSLOTS = DIM == 3 ? 15 : 8; // columns per row (fem_plan_classes' maxl)
+    static constexpr int MAXN = DIM == 3 ? 32 : 16;  // incidences per row (fem_plan_classes' maxn)
+    static constexpr int FN = FSLOTS * DIM * 32;     // doubles of the edge-vector buffer
+    static constexpr int MOFF = 32 * FSLOTS + 2;     // staging: K at [1, ..), M at [MOFF + 1, ..) (16-byte phase)
+    static constexpr int SLOT_BYTES = DIM * 32 * 8;  // stride of one slot in the edge-vector buffer
 };
 
-template <int N>
-__device__ __forceinline__ void acc_slot(double (&aK)[N], double (&aM)[N], int s, double k, double m) {
-#pragma unroll
-    for (int i = 0; i < N; i++)
-        if (s == i) {
-            aK[i] += k;
-            aM[i] += m;
-        }
+// aK[s] += k, aM[s] += m for a warp-uniform slot s (0 <= s < N): one indexed branch
+#define VB_ACC_IN(i) "+d"(aK[i])
+#define VB_ACC_IM(i) "+d"(aM[i])
+__device__ __forceinline__ void acc_slot(double (&aK)[16], double (&aM)[16], int s, double k, double m) {
+    asm(
+        "{\n\t"
+        "BT: .branchtargets L0, L1, L2, L3, L4, L5, L6, L7, L8, L9, L10, L11, L12, L13, L14, L15;\n\t"
+        "brx.idx.uni %32, BT;\n\t"
+        "L0: add.f64 %0, %0, %33; add.f64 %16, %16, %34; bra.uni END;\n\t"
+        "L1: add.f64 %1, %1, %33; add.f64 %17, %17, %34; bra.uni END;\n\t"
+        "L2: add.f64 %2, %2, %33; add.f64 %18, %18, %34; bra.uni END;\n\t"
+        "L3: add.f64 %3, %3, %33; add.f64 %19, %19, %34; bra.uni END;\n\t"
+        "L4: add.f64 %4, %4, %33; add.f64 %20, %20, %34; bra.uni END;\n\t"
+        "L5: add.f64 %5, %5, %33; add.f64 %21, %21, %34; bra.uni END;\n\t"
+        "L6: add.f64 %6, %6, %33; add.f64 %22, %22, %34; bra.uni END;\n\t"
+        "L7: add.f64 %7, %7, %33; add.f64 %23, %23, %34; bra.uni END;\n\t"
+        "L8: add.f64 %8, %8, %33; add.f64 %24, %24, %34; bra.uni END;\n\t"
+        "L9: add.f64 %9, %9, %33; add.f64 %25, %25, %34; bra.uni END;\n\t"
+        "L10: add.f64 %10, %10, %33; add.f64 %26, %26, %34; bra.uni END;\n\t"
+        "L11: add.f64 %11, %11, %33; add.f64 %27, %27, %34; bra.uni END;\n\t"
+        "L12: add.f64 %12, %12, %33; add.f64 %28, %28, %34; bra.uni END;\n\t"
+        "L13: add.f64 %13, %13, %33; add.f64 %29, %29, %34; bra.uni END;\n\t"
+        "L14: add.f64 %14, %14, %33; add.f64 %30, %30, %34; bra.uni END;\n\t"
+        "L15: add.f64 %15, %15, %33; add.f64 %31, %31, %34;\n\t"
+        "END: }\n"
+        : VB_ACC_IN(0), VB_ACC_IN(1), VB_ACC_IN(2), VB_ACC_IN(3), VB_ACC_IN(4), VB_ACC_IN(5), VB_ACC_IN(6),
+          VB_ACC_IN(7), VB_ACC_IN(8), VB_ACC_IN(9), VB_ACC_IN(10), VB_ACC_IN(11), VB_ACC_IN(12), VB_ACC_IN(13),
+          VB_ACC_IN(14), VB_ACC_IN(15), VB_ACC_IM(0), VB_ACC_IM(1), VB_ACC_IM(2), VB_ACC_IM(3), VB_ACC_IM(4),
+          VB_ACC_IM(5), VB_ACC_IM(6), VB_ACC_IM(7), VB_ACC_IM(8), VB_ACC_IM(9), VB_ACC_IM(10), VB_ACC_IM(11),
+          VB_ACC_IM(12), VB_ACC_IM(13), VB_ACC_IM(14), VB_ACC_IM(15)
+        : "r"(s), "d"(k), "d"(m));
+}
+__device__ __forceinline__ void acc_slot(double (&aK)[8], double (&aM)[8], int s, double k, double m) {
+    asm(
+        "{\n\t"
+        "BT: .branchtargets L0, L1, L2, L3, L4, L5, L6, L7;\n\t"
+        "brx.idx.uni %16, BT;\n\t"
+        "L0: add.f64 %0, %0, %17; add.f64 %8, %8, %18; bra.uni END;\n\t"
+        "L1: add.f64 %1, %1, %17; add.f64 %9, %9, %18; bra.uni END;\n\t"
+        "L2: add.f64 %2, %2, %17; add.f64 %10, %10, %18; bra.uni END;\n\t"
+        "L3: add.f64 %3, %3, %17; add.f64 %11, %11, %18; bra.uni END;\n\t"
+        "L4: add.f64 %4, %4, %17; add.f64 %12, %12, %18; bra.uni END;\n\t"
+        "L5: add.f64 %5, %5, %17; add.f64 %13, %13, %18; bra.uni END;\n\t"
+        "L6: add.f64 %6, %6, %17; add.f64 %14, %14, %18; bra.uni END;\n\t"
+        "L7: add.f64 %7, %7, %17; add.f64 %15, %15, %18;\n\t"
+        "END: }\n"
+        : VB_ACC_IN(0), VB_ACC_IN(1), VB_ACC_IN(2), VB_ACC_IN(3), VB_ACC_IN(4), VB_ACC_IN(5), VB_ACC_IN(6),
+          VB_ACC_IN(7), VB_ACC_IM(0), VB_ACC_IM(1), VB_ACC_IM(2), VB_ACC_IM(3), VB_ACC_IM(4), VB_ACC_IM(5),
+          VB_ACC_IM(6), VB_ACC_IM(7)
+        : "r"(s), "d"(k), "d"(m));
+}
+#undef VB_ACC_IN
+#undef VB_ACC_IM
+
+// shared -> global bulk copy (TMA engine), bytes a multiple of 16, both ends 16-byte aligned
+__device__ __forceinline__ void bulk_store(double* dst, const double* src, int bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+// one group of the class plan as seen by lane t
+struct ClassGroup {
+    int pos, cnt, head;   // head < 0: mixed rows (or no group)
+    int32_t v;            // the lane's row (t < cnt)
+    int lo;               // row_ptr[v]
+};
+
+#ifndef VB_CLASS_MINB
+#define VB_CLASS_MINB 16
+#endif
 template <int DIM>
-__global__ void __launch_bounds__(32) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
+__global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
                                                        const int32_t* __restrict__ class_rows,
                                                        const double* __restrict__ coords, int64_t ns, int64_t cst,
                                                        const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx,
                                                        const int32_t* __restrict__ nptr,
                                                        const uint32_t* __restrict__ nslot, double* __restrict__ K,
-                                                       double* __restrict__ M, unsigned int* __restrict__ ctr) {
-    constexpr int MAXL = ClassCfg<DIM>::MAXL;
+                                                       double* __restrict__ M, unsigned int* __restrict__ ctr,
+                                                       bool bulk) {
+    using C = ClassCfg<DIM>;
+    constexpr int MAXL = C::MAXL;
     constexpr unsigned FULL = 0xffffffffu;
     constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;   // 1/(d! (d+1)(d+2))
     constexpr double KS = DIM == 2 ? -0.5 : -1.0 / 6.0;          // -1/d!
-    __shared__ __align__(16) double F[ClassCfg<DIM>::FN];
+    __shared__ __align__(16) double F[C::FN];                    // edge vectors; then the CSR staging of K, M
+    __shared__ __align__(16) int32_t colbuf[C::FSLOTS * 32];     // columns of the next group ([slot][lane])
+    __shared__ __align__(16) int4 pat[C::MAXN];                  // decoded plan words of the current class
     const int t = threadIdx.x;
+    const double* __restrict__ X[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; c++) X[c] = coords + c * cst;
+
+    // dynamic schedule: group ids come from a per-launch counter, fetched two groups ahead
     unsigned int pending = 0;
     if (t == 0) pending = atomicAdd(ctr, 1u);
-    int64_t g = blockIdx.x;
-    while (g < ngroups) {
-        const int4 G = groups[g];
-        {   // next group (dynamic schedule, fetched one group ahead)
-            const unsigned int nx = __shfl_sync(FULL, pending, 0);
-            if (t == 0) pending = atomicAdd(ctr, 1u);
-            g = (int64_t)gridDim.x + nx;
+    auto next_id = [&]() -> int64_t {
+        const unsigned int nx = __shfl_sync(FULL, pending, 0);
+        if (t == 0) pending = atomicAdd(ctr, 1u);
+        return (int64_t)gridDim.x + nx;
+    };
+    auto load_group = [&](int64_t g) -> int4 { return g < ngroups ? groups[g] : make_int4(0, 0, -1, 1); };
+    auto rows_of = [&](const int4& G, ClassGroup& R) {   // R.v, R.lo for lane t
+        R.pos = G.x;
+        R.cnt = G.w ? 0 : G.y;   // w = 1 marks "no group"
+        R.head = G.w ? -2 : G.z;
+        R.v = 0;
+        R.lo = 0;
+        if (t < R.cnt) {
+            R.v = __ldg(class_rows + R.pos + t);
+            R.lo = __ldg(row_ptr + R.v);
         }
-        const int cnt = G.y, head = G.z;
-        const bool own = t < cnt;
-        const int32_t v = own ? __ldg(class_rows + G.x + t) : 0;
-        const int lo = own ? __ldg(row_ptr + v) : 0;
-        if (head >= 0) {
-            const int L = __ldg(row_ptr + head + 1) - __ldg(row_ptr + head);
-            const int ih = __ldg(nptr + head), n = __ldg(nptr + head + 1) - ih;
-            const int s0 = (int)(__ldg(nslot + ih) & 0xffu);
-            double xv[DIM];
-            if (own) {
+    };
+    auto issue_cols = [&](const ClassGroup& R, int L) {   // columns of a class group -> colbuf
+        if (t < R.cnt)
+            for (int s = 0; s < L; s++) cp_async4(colbuf + s * 32 + t, col_idx + R.lo + s);
+        cp_async_commit();
+    };
+
+    ClassGroup cur, nxt;
+    int4 G1, G2;
+    {
+        const int4 G0 = load_group(blockIdx.x);
+        G1 = load_group(next_id());
+        rows_of(G0, cur);
+        if (cur.head >= 0) issue_cols(cur, __ldg(row_ptr + cur.head + 1) - __ldg(row_ptr + cur.head));
+    }
+    int pat_head = -1, L = 0, n = 0, s0 = 0;
+    while (cur.head != -2) {
+        const bool fast = cur.head >= 0;
+        double xv[DIM];
+        if (fast) {
+            if (cur.head != pat_head) {   // class of this group: row length, incidences, decoded plan words
+                pat_head = cur.head;
+                L = __ldg(row_ptr + pat_head + 1) - __ldg(row_ptr + pat_head);
+                const int ih = __ldg(nptr + pat_head);
+                n = __ldg(nptr + pat_head + 1) - ih;
+                s0 = (int)(__ldg(nslot + ih) & 0xffu);
+                __syncwarp();
+                for (int j = t; j < n; j += 32) {
+                    const uint32_t w = __ldg(nslot + ih + j);
+                    const int a = (w >> 8) & 0xff, b = (w >> 16) & 0xff, c = w >> 24;
+                    pat[j] = make_int4(a * C::SLOT_BYTES, b * C::SLOT_BYTES, DIM == 3 ? c * C::SLOT_BYTES : 0,
+                                       a | b << 8 | (DIM == 3 ? c : 0) << 16);
+                }
+            }
+            // this group's columns have landed: request their coordinates (into F, once the
+            // previous group's bulk stores have read their staging from it)
+            cp_async_wait<0>();
+            if (t == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            if (t < cur.cnt) {
                 for (int s = 0; s < L; s++) {
-                    const int64_t w = __ldg(col_idx + lo + s);
+                    const int64_t w = colbuf[s * 32 + t];
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) cp_async8(F + (s * DIM + c) * 32 + t, coords + c * cst + w * ns);
+                    for (int c = 0; c < DIM; c++) cp_async8(F + (s * DIM + c) * 32 + t, X[c] + w * ns);
                 }
 #pragma unroll
-                for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + (int64_t)v * ns);
+                for (int c = 0; c < DIM; c++) xv[c] = __ldg(X[c] + (int64_t)cur.v * ns);
             } else {
 #pragma unroll
                 for (int c = 0; c < DIM; c++) xv[c] = 0.0;
             }
             cp_async_commit();
+        }
+        // next group: its rows now, its columns once this group's coordinates have landed
+        rows_of(G1, nxt);
+        G2 = load_group(next_id());
+        const int Ln = nxt.head >= 0 ? (nxt.head == pat_head ? L : __ldg(row_ptr + nxt.head + 1) - __ldg(row_ptr + nxt.head)) : 0;
+        if (fast) {
             cp_async_wait<0>();
             __syncwarp();
+            if (nxt.head >= 0) issue_cols(nxt, Ln);
             // edge vectors from the row's vertex (lanes without a row hold garbage: never stored)
 #pragma unroll
             for (int s = 0; s < MAXL; s++)
                 if (s < L && s != s0)
 #pragma unroll
                     for (int c = 0; c < DIM; c++) F[(s * DIM + c) * 32 + t] -= xv[c];
+            __syncwarp();
             double aK[MAXL], aM[MAXL];
 #pragma unroll
             for (int s = 0; s < MAXL; s++) aK[s] = aM[s] = 0.0;
-            auto ld = [&](int s, double (&f)[DIM]) {
+            const char* Fb = reinterpret_cast<const char*>(F) + t * 8;
+            auto ld = [&](int off, double(&f)[DIM]) {
 #pragma unroll
-                for (int c = 0; c < DIM; c++) f[c] = F[(s * DIM + c) * 32 + t];
+                for (int c = 0; c < DIM; c++) f[c] = *reinterpret_cast<const double*>(Fb + off + c * 256);
             };
-            for (int i0 = 0; i0 < n; i0 += 32) {
-                const uint32_t pw = i0 + t < n ? __ldg(nslot + ih + i0 + t) : 0u;
-                const int m = n - i0 < 32 ? n - i0 : 32;
-                for (int j = 0; j < m; j++) {
-                    const uint32_t w = __shfl_sync(FULL, pw, j);
-                    if constexpr (DIM == 3) {
-                        const int s1 = (w >> 8) & 0xff, s2 = (w >> 16) & 0xff, s3 = w >> 24;
-                        double f1[3], f2[3], f3[3];
-                        ld(s1, f1);
-                        ld(s2, f2);
-                        ld(s3, f3);
-                        const double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
-                                              fma(f2[0], f3[1], -f2[1] * f3[0])};
-                        const double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
-                                              fma(f3[0], f1[1], -f3[1] * f1[0])};
-                        const double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
-                                              fma(f1[0], f2[1], -f1[1] * f2[0])};
-                        const double ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
-                        const double r = rcp_nr(ad);
-                        double S[3];
+            // incidence values: K_e[a][o_j] * (-d!) for the d other vertices, and |det|
+            struct Inc {
+                double k[DIM], ad;
+                int w;
+            };
+            auto inc = [&](const int4& P) {
+                Inc o;
+                o.w = P.w;
+                if constexpr (DIM == 3) {
+                    double f1[3], f2[3], f3[3];
+                    ld(P.x, f1);
+                    ld(P.y, f2);
+                    ld(P.z, f3);
+                    const double h1[3] = {fma(f2[1], f3[2], -f2[2] * f3[1]), fma(f2[2], f3[0], -f2[0] * f3[2]),
+                                          fma(f2[0], f3[1], -f2[1] * f3[0])};
+                    const double h2[3] = {fma(f3[1], f1[2], -f3[2] * f1[1]), fma(f3[2], f1[0], -f3[0] * f1[2]),
+                                          fma(f3[0], f1[1], -f3[1] * f1[0])};
+                    const double h3[3] = {fma(f1[1], f2[2], -f1[2] * f2[1]), fma(f1[2], f2[0], -f1[0] * f2[2]),
+                                          fma(f1[0], f2[1], -f1[1] * f2[0])};
+                    o.ad = fabs(fma(f1[0], h1[0], fma(f1[1], h1[1], f1[2] * h1[2])));
+                    const double r = rcp_nr(o.ad);
+                    double S[3];
 #pragma unroll
-                        for (int c = 0; c < 3; c++) S[c] = r * ((h1[c] + h2[c]) + h3[c]);
-                        acc_slot<MAXL>(aK, aM, s1, fma(S[0], h1[0], fma(S[1], h1[1], S[2] * h1[2])), ad);
-                        acc_slot<MAXL>(aK, aM, s2, fma(S[0], h2[0], fma(S[1], h2[1], S[2] * h2[2])), ad);
-                        acc_slot<MAXL>(aK, aM, s3, fma(S[0], h3[0], fma(S[1], h3[1], S[2] * h3[2])), ad);
-                    } else {
-                        const int s1 = (w >> 8) & 0xff, s2 = (w >> 16) & 0xff;
-                        double f1[2], f2[2];
-                        ld(s1, f1);
-                        ld(s2, f2);
-                        // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
-                        const double ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
-                        const double r = rcp_nr(ad);
-                        const double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
-                        acc_slot<MAXL>(aK, aM, s1, fma(hax, f2[1], -hay * f2[0]), ad);
-                        acc_slot<MAXL>(aK, aM, s2, fma(-hax, f1[1], hay * f1[0]), ad);
-                    }
+                    for (int c = 0; c < 3; c++) S[c] = r * ((h1[c] + h2[c]) + h3[c]);
+                    o.k[0] = fma(S[0], h1[0], fma(S[1], h1[1], S[2] * h1[2]));
+                    o.k[1] = fma(S[0], h2[0], fma(S[1], h2[1], S[2] * h2[2]));
+                    o.k[2] = fma(S[0], h3[0], fma(S[1], h3[1], S[2] * h3[2]));
+                } else {
+                    double f1[2], f2[2];
+                    ld(P.x, f1);
+                    ld(P.y, f2);
+                    // tjac rows f1, f2: adj columns h1 = (f2y, -f2x), h2 = (-f1y, f1x)
+                    o.ad = fabs(fma(f1[0], f2[1], -f1[1] * f2[0]));
+                    const double r = rcp_nr(o.ad);
+                    const double hax = r * (f2[1] - f1[1]), hay = r * (f1[0] - f2[0]);
+                    o.k[0] = fma(hax, f2[1], -hay * f2[0]);
+                    o.k[1] = fma(-hax, f1[1], hay * f1[0]);
+                }
+                return o;
+            };
+            auto acc = [&](const Inc& o) {
+#pragma unroll
+                for (int q = 0; q < DIM; q++) acc_slot(aK, aM, (o.w >> (8 * q)) & 0xff, o.k[q], o.ad);
+            };
+            // two incidences in flight (loads and arithmetic of both before their updates;
+            // the updates keep ascending element order)
+#ifndef VB_CLASS_U
+#define VB_CLASS_U 1
+#endif
+            int j = 0;
+            if constexpr (VB_CLASS_U == 2) {
+                int4 Pa = pat[0], Pb = pat[n > 1 ? 1 : 0];   // plan words one step ahead
+                for (; j + 1 < n; j += 2) {
+                    const Inc o0 = inc(Pa);
+                    const Inc o1 = inc(Pb);
+                    Pa = pat[j + 2 < n ? j + 2 : 0];
+                    Pb = pat[j + 3 < n ? j + 3 : 0];
+                    acc(o0);
+                    acc(o1);
+                }
+                if (j < n) acc(inc(Pa));
+            } else {
+                int4 Pa = pat[0];
+                for (; j < n; j++) {
+                    const Inc o0 = inc(Pa);
+                    Pa = pat[j + 1 < n ? j + 1 : 0];
+                    acc(o0);
                 }
             }
             __syncwarp();   // every lane is done with the edge vectors
             // finish the rows (diagonal from the partition of unity) and stage them in
             // CSR order: row t of the group at [t*L, t*L + L)
-            double* stK = F;
-            double* stM = F + 32 * MAXL;
-            if (own) {
+            const int lo0 = __shfl_sync(FULL, cur.lo, 0);
+            const int sh = lo0 & 1;   // staging phase: entry q of the group at [sh + q] (16-byte aligned pairs)
+            double* stK = F + sh;
+            double* stM = F + C::MOFF + sh;
+            if (t < cur.cnt) {
                 double sk = 0.0, sm = 0.0;
 #pragma unroll
                 for (int s = 0; s < MAXL; s++)
@@ -1053,48 +1213,78 @@ __global__ void __launch_bounds__(32) assemble_class_k(int64_t ngroups, const in
                 stM[t * L + s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
             }
             __syncwarp();
-            const int tot = cnt * L;
-            for (int q0 = 0; q0 < tot; q0 += 32) {
-                const int q = q0 + t;
-                int r = q / L;
-                r = r < 31 ? r : 31;
-                const int p = __shfl_sync(FULL, lo, r) + (q - r * L);
-                if (q < tot) {
-                    if (K) stcs(K + p, stK[q]);
-                    if (M) stcs(M + p, stM[q]);
+            const int tot = cur.cnt * L;
+            const bool contiguous = __shfl_sync(FULL, cur.lo, cur.cnt - 1) == lo0 + (cur.cnt - 1) * L;
+            if (contiguous && bulk) {
+                // consecutive rows: one CSR range [lo0, lo0 + tot).  Its 16-byte aligned body
+                // goes out as bulk copies (cp.async.bulk, issued by lane 0); the odd first /
+                // last entries as plain stores
+                const int body = (tot - sh) & ~1;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (t == 0 && body > 0) {
+                    if (K) bulk_store(K + lo0 + sh, stK + sh, body * 8);
+                    if (M) bulk_store(M + lo0 + sh, stM + sh, body * 8);
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                const int q = t == 1 ? 0 : tot - 1;   // lane 1: a leading odd entry, lane 2: a trailing one
+                if ((t == 1 && sh) || (t == 2 && sh + body < tot && !(sh && tot == 1))) {
+                    if (K) stcs(K + lo0 + q, stK[q]);
+                    if (M) stcs(M + lo0 + q, stM[q]);
+                }
+            } else {
+                for (int q0 = 0; q0 < tot; q0 += 32) {
+                    const int q = q0 + t;
+                    int r = q / L;
+                    r = r < 31 ? r : 31;
+                    const int p = __shfl_sync(FULL, cur.lo, r) + (q - r * L);
+                    if (q < tot) {
+                        if (K) stcs(K + p, stK[q]);
+                        if (M) stcs(M + p, stM[q]);
+                    }
                 }
             }
             __syncwarp();   // the staging area is the next group's edge-vector buffer
-        } else if (own) {
-            // mixed class: the lane's row in place in HBM
-            const int L = __ldg(row_ptr + v + 1) - lo;
-            const int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
-            if (L > 0) {
-                double* aK = K ? K + lo : nullptr;
-                double* aM = M ? M + lo : nullptr;
-                int s0 = 0;
-                for (int q = 0; q < L; q++) {
-                    if (aK) aK[q] = 0.0;
-                    if (aM) aM[q] = 0.0;
-                    if (__ldg(col_idx + lo + q) == v) s0 = q;
+        } else {
+            if (nxt.head >= 0) issue_cols(nxt, Ln);
+            if (t < cur.cnt) {
+                // mixed class: the lane's row in place in HBM
+                const int32_t v = cur.v;
+                const int lo = cur.lo;
+                const int Lr = __ldg(row_ptr + v + 1) - lo;
+                const int i0 = __ldg(nptr + v), i1 = __ldg(nptr + v + 1);
+                if (Lr > 0) {
+                    double* aK = K ? K + lo : nullptr;
+                    double* aM = M ? M + lo : nullptr;
+                    int z0 = 0;
+                    for (int q = 0; q < Lr; q++) {
+                        if (aK) aK[q] = 0.0;
+                        if (aM) aM[q] = 0.0;
+                        if (__ldg(col_idx + lo + q) == v) z0 = q;
+                    }
+                    double xr[DIM];
+#pragma unroll
+                    for (int c = 0; c < DIM; c++) xr[c] = __ldg(X[c] + (int64_t)v * ns);
+                    auto ev = [&](int s, double(&f)[DIM]) {
+                        int64_t w = __ldg(col_idx + lo + s);
+#pragma unroll
+                        for (int c = 0; c < DIM; c++) f[c] = __ldg(X[c] + w * ns) - xr[c];
+                    };
+                    auto ix = [](int s) { return s; };
+                    const double pv[2] = {1.0, 1.0};
+                    auto nofac = [](int, double&, double&) {};
+                    const CoefSpec cp{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
+                    gather_row<DIM, false, false, false, uint32_t>(i0, i1, nslot, ev, nofac, ix, aK, aM, xr, pv, cp);
+                    finish_row<DIM, 1, false>(Lr, z0, aK, aM, 0.0);
                 }
-                double xv[DIM];
-#pragma unroll
-                for (int c = 0; c < DIM; c++) xv[c] = __ldg(coords + c * cst + (int64_t)v * ns);
-                auto ev = [&](int s, double(&f)[DIM]) {
-                    int64_t w = __ldg(col_idx + lo + s);
-#pragma unroll
-                    for (int c = 0; c < DIM; c++) f[c] = __ldg(coords + c * cst + w * ns) - xv[c];
-                };
-                auto ix = [](int s) { return s; };
-                const double pv[2] = {1.0, 1.0};
-                auto nofac = [](int, double&, double&) {};
-                const CoefSpec cp{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
-                gather_row<DIM, false, false, false, uint32_t>(i0, i1, nslot, ev, nofac, ix, aK, aM, xv, pv, cp);
-                finish_row<DIM, 1, false>(L, s0, aK, aM, 0.0);
             }
+            __syncwarp();
         }
+        cur = nxt;
+        G1 = G2;
     }
+    cp_async_wait<0>();
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace
@@ -1294,6 +1484,8 @@ extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* 
     cudaStream_t s = cs(stream);
     unsigned int* ctr = block_counter(s);
     if (!ctr) { set_error("%s: block counter unavailable", fn); return VB_ERR_CUDA; }
+    // bulk (TMA) stores of contiguous groups need 16-byte aligned value arrays
+    const bool bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
     auto launch = [&](auto kern) {
         static int occ[2] = {0, 0};
         int& n = occ[dim - 2];
@@ -1304,7 +1496,8 @@ extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* 
         const int64_t cap = (int64_t)sm_count() * n;
         const unsigned g = (unsigned)(ngroups < cap ? ngroups : cap);
         kern<<<g, 32, 0, s>>>(ngroups, reinterpret_cast<const int4*>(groups), class_rows, coords, node_stride,
-                              comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr);
+                              comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr,
+                              bulk);
     };
     if (dim == 3) launch(assemble_class_k<3>);
     else launch(assemble_class_k<2>);

@@ -38,14 +38,14 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t h) {
 }
 
 __global__ void cls_hash_k(int64_t nn, const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ nptr,
-                           const uint32_t* __restrict__ nslot, int maxl, uint64_t* __restrict__ keys,
+                           const uint32_t* __restrict__ nslot, int maxl, int maxn, uint64_t* __restrict__ keys,
                            int32_t* __restrict__ rows) {
     const int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nn) return;
     const int L = row_ptr[v + 1] - row_ptr[v];
     const int i0 = nptr[v], n = nptr[v + 1] - i0;
     uint64_t key = MIXED;
-    if (L >= 2 && L <= maxl && n > 0) {
+    if (L >= 2 && L <= maxl && n > 0 && n <= maxn) {
         uint64_t h = fmix64(((uint64_t)L << 32) | (uint32_t)n);
         for (int i = 0; i < n; i++) h = (h ^ __ldg(nslot + i0 + i)) * 0x100000001b3ull + 0x9e3779b97f4a7c15ull;
         key = fmix64(h) >> 1;
@@ -223,10 +223,11 @@ extern "C" vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_pt
     cudaStream_t s = cs(stream);
     ClsWork W;
     cls_layout(n1, static_cast<char*>(work), &W);
-    const int maxl = dim == 3 ? 16 : 8;   // register budget of assemble_class_k (columns per row)
+    const int maxl = dim == 3 ? 15 : 8;   // edge-vector buffer of assemble_class_k (columns per row)
+    const int maxn = dim == 3 ? 32 : 16;  // its decoded plan-word table (incidences per row)
     const unsigned g = (unsigned)((nn + 255) / 256);
     vb_status st;
-    cls_hash_k<<<g, 256, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem_slot, maxl, W.k1, W.r1);
+    cls_hash_k<<<g, 256, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem_slot, maxl, maxn, W.k1, W.r1);
     if ((st = launch_check(fn)) != VB_OK) return st;
     if ((st = sort_rle(W, nn, W.k1, W.r1, W.k2, W.r2, s, fn)) != VB_OK) return st;
     if ((st = exclusive_scan_i32(W.cnt, W.roff, nn, W.scan, s, nullptr)) != VB_OK) return st;

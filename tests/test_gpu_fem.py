@@ -148,7 +148,7 @@ def test_row_classes_plan(dev, kind, n):
             continue
         assert not seen_mixed                        # mixed rows come last
         ref = signature(head, rp, nptr, nsl)
-        assert ref[0] <= (16 if elems.shape[0] == 4 else 8)
+        assert ref[0] <= (15 if elems.shape[0] == 4 else 8)
         for v in rows[pos:pos + cnt]:
             assert signature(v, rp, nptr, nsl) == ref
         in_classes += cnt
