@@ -1004,7 +1004,7 @@ struct ClassGroup {
 #ifndef VB_CLASS_MINB
 #define VB_CLASS_MINB 16
 #endif
-template <int DIM>
+template <int DIM, bool NS1>   // NS1: node_stride == 1 (SoA coordinate planes)
 __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
                                                        const int32_t* __restrict__ class_rows,
                                                        const double* __restrict__ coords, int64_t ns, int64_t cst,
@@ -1026,6 +1026,7 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
     const double* __restrict__ X[DIM];
 #pragma unroll
     for (int c = 0; c < DIM; c++) X[c] = coords + c * cst;
+    if constexpr (NS1) ns = 1;
 
     // dynamic schedule: group ids come from a per-launch counter, fetched two groups ahead
     unsigned int pending = 0;
@@ -1087,9 +1088,10 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
             __syncwarp();
             if (t < cur.cnt) {
                 for (int s = 0; s < L; s++) {
-                    const int64_t w = colbuf[s * 32 + t];
+                    const int w = colbuf[s * 32 + t];
 #pragma unroll
-                    for (int c = 0; c < DIM; c++) cp_async8(F + (s * DIM + c) * 32 + t, X[c] + w * ns);
+                    for (int c = 0; c < DIM; c++)
+                        cp_async8(F + (s * DIM + c) * 32 + t, NS1 ? X[c] + w : X[c] + (int64_t)w * ns);
                 }
 #pragma unroll
                 for (int c = 0; c < DIM; c++) xv[c] = __ldg(X[c] + (int64_t)cur.v * ns);
@@ -1166,24 +1168,11 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
 #pragma unroll
                 for (int q = 0; q < DIM; q++) acc_slot(aK, aM, (o.w >> (8 * q)) & 0xff, o.k[q], o.ad);
             };
-            // two incidences in flight (loads and arithmetic of both before their updates;
-            // the updates keep ascending element order)
-#ifndef VB_CLASS_U
-#define VB_CLASS_U 1
-#endif
+            // one incidence at a time in ascending element order (two in flight, or the next
+            // incidence's edge vectors loaded a step ahead, need registers the accumulators
+            // hold: both measured slower)
             int j = 0;
-            if constexpr (VB_CLASS_U == 2) {
-                int4 Pa = pat[0], Pb = pat[n > 1 ? 1 : 0];   // plan words one step ahead
-                for (; j + 1 < n; j += 2) {
-                    const Inc o0 = inc(Pa);
-                    const Inc o1 = inc(Pb);
-                    Pa = pat[j + 2 < n ? j + 2 : 0];
-                    Pb = pat[j + 3 < n ? j + 3 : 0];
-                    acc(o0);
-                    acc(o1);
-                }
-                if (j < n) acc(inc(Pa));
-            } else {
+            {
                 int4 Pa = pat[0];
                 for (; j < n; j++) {
                     const Inc o0 = inc(Pa);
@@ -1233,15 +1222,17 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                     if (M) stcs(M + lo0 + q, stM[q]);
                 }
             } else {
-                for (int q0 = 0; q0 < tot; q0 += 32) {
-                    const int q = q0 + t;
-                    int r = q / L;
-                    r = r < 31 ? r : 31;
-                    const int p = __shfl_sync(FULL, cur.lo, r) + (q - r * L);
-                    if (q < tot) {
-                        if (K) stcs(K + p, stK[q]);
-                        if (M) stcs(M + p, stM[q]);
+                // runs of consecutive rows, each one contiguous CSR range
+                for (int k = 0; k < cur.cnt;) {
+                    const int lok = __shfl_sync(FULL, cur.lo, k);
+                    const unsigned brk =
+                        __ballot_sync(FULL, t > k && t < cur.cnt && cur.lo != lok + (t - k) * L);
+                    const int e = brk ? __ffs(brk) - 1 : cur.cnt;
+                    for (int q = k * L + t; q < e * L; q += 32) {
+                        if (K) stcs(K + lok + (q - k * L), stK[q]);
+                        if (M) stcs(M + lok + (q - k * L), stM[q]);
                     }
+                    k = e;
                 }
             }
             __syncwarp();   // the staging area is the next group's edge-vector buffer
@@ -1499,7 +1490,12 @@ extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* 
                               comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr,
                               bulk);
     };
-    if (dim == 3) launch(assemble_class_k<3>);
-    else launch(assemble_class_k<2>);
+    if (node_stride == 1) {
+        if (dim == 3) launch(assemble_class_k<3, true>);
+        else launch(assemble_class_k<2, true>);
+    } else {
+        if (dim == 3) launch(assemble_class_k<3, false>);
+        else launch(assemble_class_k<2, false>);
+    }
     return launch_check(fn);
 }
