@@ -143,10 +143,12 @@ def load_traffic(kernel_key):
             d = json.load(f)
         # the c = 1 instantiations of the kernel over the rounds: <d>, <d, 0>, <d, 0, 0>
         # (COEF, FAC), <d, 0, 0, B> (+ budget class); take the newest capture
+        # (gather); the class kernel's template argument is the coordinate layout (<d, NS1>)
         stem = kernel_key[:-1]
+        first = ",1" if kernel_key.startswith("assemble_class_k") else ",0"
         cands = [(v.get("tag", ""), k) for k, v in d["kernels"].items()
                  if k == kernel_key or (k.startswith(stem + ",") and k.replace(" ", "").startswith(
-                     stem.replace(" ", "") + ",0"))]
+                     stem.replace(" ", "") + first))]
         if not cands:
             return None
         return d["kernels"][max(cands)[1]]["dram_bytes_per_launch"]

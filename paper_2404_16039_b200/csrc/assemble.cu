@@ -915,8 +915,10 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 // same on every lane, and each lane keeps its row's K and M sums in registers:
 // a uniform slot picks the register through an indexed branch (brx.idx, one
 // jump-table load + branch per update) instead of a shared-memory
-// read-modify-write.  Edge vectors f_s = x_col(s) - x_v stay in shared memory
-// ([slot][coord][lane], conflict free).  Loads are pipelined one group ahead:
+// read-modify-write.  Column coordinates stay in shared memory ([slot][coord][lane],
+// conflict free); the edge vectors f_s = x_col(s) - x_v are formed as they are
+// loaded (converting the buffer once per group measured 1.5 % slower: its shared
+// traffic costs more than 9 subtractions per incidence).  Loads are pipelined one group ahead:
 // the next group's rows and columns (cp.async) are requested before the
 // current group's incidence loop.  Rows of the mixed class are assembled by
 // their lane in place in HBM (as assemble_gather_k's fallback).
@@ -1109,20 +1111,14 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
             cp_async_wait<0>();
             __syncwarp();
             if (nxt.head >= 0) issue_cols(nxt, Ln);
-            // edge vectors from the row's vertex (lanes without a row hold garbage: never stored)
-#pragma unroll
-            for (int s = 0; s < MAXL; s++)
-                if (s < L && s != s0)
-#pragma unroll
-                    for (int c = 0; c < DIM; c++) F[(s * DIM + c) * 32 + t] -= xv[c];
-            __syncwarp();
             double aK[MAXL], aM[MAXL];
 #pragma unroll
             for (int s = 0; s < MAXL; s++) aK[s] = aM[s] = 0.0;
             const char* Fb = reinterpret_cast<const char*>(F) + t * 8;
             auto ld = [&](int off, double(&f)[DIM]) {
 #pragma unroll
-                for (int c = 0; c < DIM; c++) f[c] = *reinterpret_cast<const double*>(Fb + off + c * 256);
+                for (int c = 0; c < DIM; c++)   // edge vector from the row's vertex
+                    f[c] = *reinterpret_cast<const double*>(Fb + off + c * 256) - xv[c];
             };
             // incidence values: K_e[a][o_j] * (-d!) for the d other vertices, and |det|
             struct Inc {
