@@ -922,6 +922,9 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 // the next group's rows and columns (cp.async) are requested before the
 // current group's incidence loop.  Rows of the mixed class are assembled by
 // their lane in place in HBM (as assemble_gather_k's fallback).
+#ifndef VB_CLASS_PAIRS
+#define VB_CLASS_PAIRS 1   // 3D: incidences paired over shared link edges (build_pairs)
+#endif
 template <int DIM>
 struct ClassCfg {
     static constexpr int MAXL = DIM == 3 ? 16 : 8;   // register accumulators per row (acc_slot)
@@ -996,6 +999,47 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 
+// 3D: pair up a class's incidences whose link triangles share an edge (a, b):
+// triangles (a, b, c) and (a, b, d) share fa x fb (the h of c and of d), so a
+// pair loads 4 edge vectors instead of 6, forms 5 cross products instead of 6
+// and makes 4 slot updates instead of 6.  Greedy in incidence order; a step is
+// (x, y, z) = edge-vector offsets of a, b, c and w = a | b << 4 | c << 8 |
+// d << 12 | CLASS_PAIR (slots < 16).  Reads and rewrites pat in place (step k
+// is written after incidence k has been read; pairs only look ahead).
+constexpr int CLASS_PAIR = 1 << 16;
+__device__ int build_pairs(int4* pat, int n, int slot_bytes) {
+    uint32_t used = 0;
+    int k = 0;
+    for (int i = 0; i < n; i++) {
+        if ((used >> i) & 1) continue;
+        used |= 1u << i;
+        const int wi = pat[i].w;
+        const int x = wi & 0xff, y = (wi >> 8) & 0xff, z = (wi >> 16) & 0xff;
+        int step = x | y << 4 | z << 8, a = x, b = y, c = z;
+        for (int j = i + 1; j < n; j++) {
+            if ((used >> j) & 1) continue;
+            const int wj = pat[j].w;
+            const int u[3] = {wj & 0xff, (wj >> 8) & 0xff, (wj >> 16) & 0xff};
+            int shared = 0, d = -1;
+            for (int q = 0; q < 3; q++) {
+                if (u[q] == x || u[q] == y || u[q] == z) shared++;
+                else d = u[q];
+            }
+            if (shared != 2) continue;
+            // the shared edge (a, b) and the third vertices c (of i) and d (of j)
+            if (d == -1) break;
+            if (x != u[0] && x != u[1] && x != u[2]) { a = y; b = z; c = x; }
+            else if (y != u[0] && y != u[1] && y != u[2]) { a = z; b = x; c = y; }
+            else { a = x; b = y; c = z; }
+            used |= 1u << j;
+            step = a | b << 4 | c << 8 | d << 12 | CLASS_PAIR;
+            break;
+        }
+        pat[k++] = make_int4(a * slot_bytes, b * slot_bytes, c * slot_bytes, step);
+    }
+    return k;
+}
+
 // one group of the class plan as seen by lane t
 struct ClassGroup {
     int pos, cnt, head;   // head < 0: mixed rows (or no group)
@@ -1064,7 +1108,7 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
         rows_of(G0, cur);
         if (cur.head >= 0) issue_cols(cur, __ldg(row_ptr + cur.head + 1) - __ldg(row_ptr + cur.head));
     }
-    int pat_head = -1, L = 0, n = 0, s0 = 0;
+    int pat_head = -1, L = 0, n = 0, s0 = 0, nst = 0;   // nst: steps of the class's loop
     while (cur.head != -2) {
         const bool fast = cur.head >= 0;
         double xv[DIM];
@@ -1081,6 +1125,15 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                     const int a = (w >> 8) & 0xff, b = (w >> 16) & 0xff, c = w >> 24;
                     pat[j] = make_int4(a * C::SLOT_BYTES, b * C::SLOT_BYTES, DIM == 3 ? c * C::SLOT_BYTES : 0,
                                        a | b << 8 | (DIM == 3 ? c : 0) << 16);
+                }
+                if constexpr (DIM == 3 && VB_CLASS_PAIRS) {
+                    __syncwarp();
+                    int k = 0;
+                    if (t == 0) k = build_pairs(pat, n, C::SLOT_BYTES);
+                    nst = __shfl_sync(FULL, k, 0);
+                    __syncwarp();
+                } else {
+                    nst = n;
                 }
             }
             // this group's columns have landed: request their coordinates (into F, once the
@@ -1167,10 +1220,61 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
             // one incidence at a time in ascending element order (two in flight, or the next
             // incidence's edge vectors loaded a step ahead, need registers the accumulators
             // hold: both measured slower)
-            int j = 0;
-            {
+            if constexpr (DIM == 3 && VB_CLASS_PAIRS) {
+                auto cross = [](const double(&u)[3], const double(&v)[3], double(&o)[3]) {
+                    o[0] = fma(u[1], v[2], -u[2] * v[1]);
+                    o[1] = fma(u[2], v[0], -u[0] * v[2]);
+                    o[2] = fma(u[0], v[1], -u[1] * v[0]);
+                };
+                auto dot = [](const double(&u)[3], const double(&v)[3]) {
+                    return fma(u[0], v[0], fma(u[1], v[1], u[2] * v[2]));
+                };
+                int4 Pn = pat[0];
+                for (int j = 0; j < nst; j++) {
+                    const int4 St = Pn;
+                    Pn = pat[j + 1 < nst ? j + 1 : 0];
+                    const int w = St.w;
+                    double fa[3], fb[3], fc[3], P[3], ha[3], hb[3], Sv[3];
+                    ld(St.x, fa);
+                    ld(St.y, fb);
+                    ld(St.z, fc);
+                    // triangle (a, b, c): h_a = fb x fc, h_b = fc x fa, h_c = fa x fb = P
+                    cross(fa, fb, P);
+                    cross(fb, fc, ha);
+                    cross(fc, fa, hb);
+                    const double ad = fabs(dot(fc, P));
+                    const double r = rcp_nr(ad);
+#pragma unroll
+                    for (int c = 0; c < 3; c++) Sv[c] = r * ((P[c] + ha[c]) + hb[c]);
+                    double ka = dot(Sv, ha), kb = dot(Sv, hb);
+                    const double kc = dot(Sv, P);
+                    if (w & CLASS_PAIR) {
+                        // triangle (a, b, d): h_a = fb x fd, h_b = fd x fa, h_d = P
+                        double fd[3];
+                        ld(((w >> 12) & 15) * C::SLOT_BYTES, fd);
+                        cross(fb, fd, ha);
+                        cross(fd, fa, hb);
+                        const double ad2 = fabs(dot(fd, P));
+                        const double r2 = rcp_nr(ad2);
+#pragma unroll
+                        for (int c = 0; c < 3; c++) Sv[c] = r2 * ((P[c] + ha[c]) + hb[c]);
+                        ka += dot(Sv, ha);
+                        kb += dot(Sv, hb);
+                        const double kd = dot(Sv, P);
+                        const double ab = ad + ad2;
+                        acc_slot(aK, aM, w & 15, ka, ab);
+                        acc_slot(aK, aM, (w >> 4) & 15, kb, ab);
+                        acc_slot(aK, aM, (w >> 8) & 15, kc, ad);
+                        acc_slot(aK, aM, (w >> 12) & 15, kd, ad2);
+                    } else {
+                        acc_slot(aK, aM, w & 15, ka, ad);
+                        acc_slot(aK, aM, (w >> 4) & 15, kb, ad);
+                        acc_slot(aK, aM, (w >> 8) & 15, kc, ad);
+                    }
+                }
+            } else {
                 int4 Pa = pat[0];
-                for (; j < n; j++) {
+                for (int j = 0; j < n; j++) {
                     const Inc o0 = inc(Pa);
                     Pa = pat[j + 1 < n ? j + 1 : 0];
                     acc(o0);
