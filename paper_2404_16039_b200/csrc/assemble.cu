@@ -14,6 +14,7 @@
 //     is added into the row's slots kept in shared memory, and the CTA's
 //     contiguous CSR range is written once with coalesced stores (no atomics,
 //     no zero-fill, no read-modify-write of K/M in HBM).
+#include <algorithm>
 #include <atomic>
 #include <type_traits>
 
@@ -1059,7 +1060,7 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                                                        const int32_t* __restrict__ nptr,
                                                        const uint32_t* __restrict__ nslot, double* __restrict__ K,
                                                        double* __restrict__ M, unsigned int* __restrict__ ctr,
-                                                       bool bulk) {
+                                                       bool bulk, int rounds) {
     using C = ClassCfg<DIM>;
     constexpr int MAXL = C::MAXL;
     constexpr unsigned FULL = 0xffffffffu;
@@ -1074,13 +1075,20 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
     for (int c = 0; c < DIM; c++) X[c] = coords + c * cst;
     if constexpr (NS1) ns = 1;
 
-    // dynamic schedule: group ids come from a per-launch counter, fetched two groups ahead
+    // schedule: the first `rounds` groups of a CTA are static (blockIdx.x + i * gridDim.x),
+    // the rest come from a per-launch counter, fetched one group ahead (a counter fetch
+    // per group made the counter's atomics a hot spot)
     unsigned int pending = 0;
-    if (t == 0) pending = atomicAdd(ctr, 1u);
+    int64_t stat = 0;
+    if (t == 0 && rounds <= 1) pending = atomicAdd(ctr, 1u);
     auto next_id = [&]() -> int64_t {
+        if (++stat < rounds) {
+            if (stat == rounds - 1 && t == 0) pending = atomicAdd(ctr, 1u);
+            return (int64_t)blockIdx.x + stat * gridDim.x;
+        }
         const unsigned int nx = __shfl_sync(FULL, pending, 0);
         if (t == 0) pending = atomicAdd(ctr, 1u);
-        return (int64_t)gridDim.x + nx;
+        return (int64_t)rounds * gridDim.x + nx;
     };
     auto load_group = [&](int64_t g) -> int4 { return g < ngroups ? groups[g] : make_int4(0, 0, -1, 1); };
     auto rows_of = [&](const int4& G, ClassGroup& R) {   // R.v, R.lo for lane t
@@ -1586,9 +1594,14 @@ extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* 
         }
         const int64_t cap = (int64_t)sm_count() * n;
         const unsigned g = (unsigned)(ngroups < cap ? ngroups : cap);
+        // static rounds: about 3/4 of the groups, at least 1 (the first group)
+#ifndef VB_CLASS_STATIC_Q
+#define VB_CLASS_STATIC_Q 3
+#endif
+        const int rounds = (int)std::max<int64_t>(1, (ngroups / g) * VB_CLASS_STATIC_Q / 4);
         kern<<<g, 32, 0, s>>>(ngroups, reinterpret_cast<const int4*>(groups), class_rows, coords, node_stride,
                               comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr,
-                              bulk);
+                              bulk, rounds);
     };
     if (node_stride == 1) {
         if (dim == 3) launch(assemble_class_k<3, true>);
