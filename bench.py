@@ -187,6 +187,8 @@ def run_vb(args):
                       gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
         if gvar == "class":
             p.classes()    # the row classes are part of this variant's plan
+        if gvar == "tile" and not p.tiles(cd, ed):   # the tile plan is part of this variant's plan
+            raise RuntimeError("tile plan refused: " + p.tile_reason)
         return p
     plan = build_plan()
     pts = []
@@ -231,7 +233,8 @@ def run_vb(args):
     avg_launch_ms = statistics.mean(launch_ms)
     alg = alg_bytes_assembly(dim, nn, ne, nnz)
     achieved = alg / (avg_launch_ms * 1e-3) / 1e9
-    kname = {"class": "assemble_class_k<3>", "block": "assemble_gather_k<3>"}.get(gvar, "assemble_atomic_k<3>")
+    kname = {"class": "assemble_class_k<3>", "block": "assemble_gather_k<3>",
+             "tile": "assemble_tile_k<3>"}.get(gvar, "assemble_atomic_k<3>")
     traffic = load_traffic(kname)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -312,7 +315,7 @@ def run_vb(args):
                "d2h_bytes_per_step": (nn + 1) * 4 + nnz * 4 + 2 * nnz * 8,
                "steps": n_e2e, "ms_per_step": e2e_ms / n_e2e,
                "includes": "per step: H2D coords+elems from pinned memory, fem_p1_pattern (count+fill), "
-                           "fem_plan_classes (class variant), the assembly, D2H row_ptr/col_idx/K/M to pinned memory; upload / 2 compute / "
+                           "fem_plan_classes (class variant) / fem_plan_tiles (tile variant), the assembly, D2H row_ptr/col_idx/K/M to pinned memory; upload / 2 compute / "
                            "download streams, host wall clock with device syncs on both sides"}
 
     secondary = None
@@ -333,7 +336,8 @@ def run_vb(args):
         "dtype": "f64", "data": "synthetic (seeded Kuhn-cube mesh, synth/)",
         "config": {"workload": WORKLOAD5, "variant": args.variant,
                    "timed": "one numeric K+M assembly per step on the resident plan (%s)" % (
-                       "fem_p1_assemble_classes" if gvar == "class" else "fem_p1_assemble"),
+                       {"class": "fem_p1_assemble_classes", "tile": "fem_p1_assemble_tiles"}.get(
+                           gvar, "fem_p1_assemble")),
                    "pattern_ms": round(pattern_ms, 3), "nnz": nnz, "ne": ne, "nn": nn,
                    "l2": "no flush: every step streams %.0f MB (> 126 MB L2)" % (alg / 1e6),
                    "parallelism": "replicas" if ws > 1 else "single GPU"},
@@ -381,7 +385,7 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
 
     # the other assembly variants on config 5
     nn5, ne5 = coords5.shape[1], elems5.shape[1]
-    for other in ("class", "block", "atomic"):
+    for other in ("class", "block", "tile", "atomic"):
         if other == args.variant:
             continue
         p_other = vb.P1Plan(ed5, nn5, scatter_map=(other == "atomic"), gather_plan=(other != "atomic"))
@@ -404,6 +408,17 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     res.append({"name": "config5 fem_plan_classes (row classes of the gather plan)",
                 "ms": round((time.perf_counter() - t0) * 1e3 / 2, 3), "classes": plan5.class_stats[1],
                 "groups": plan5.class_stats[0], "rows_in_classes": plan5.class_stats[2]})
+    # tile plan build on config 5 (one-time, after the pattern)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(2):
+        plan5.tile_ok = None
+        plan5.tiles(cd5, ed5)
+    torch.cuda.synchronize()
+    res.append({"name": "config5 fem_plan_tiles (Morton tiles, entries, coloring)",
+                "ms": round((time.perf_counter() - t0) * 1e3 / 2, 3), "entries": plan5.tile_stats[0],
+                "entries_per_element": round(plan5.tile_stats[0] / ne5, 4), "max_colors": plan5.tile_stats[3],
+                "max_local_nodes": plan5.tile_stats[2]})
     # pattern build on config 5 (one-time plan)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -446,7 +461,7 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     K4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
     M4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
     for name, mode in (("class", vb.VB_ASSEMBLE_GATHER), ("block", vb.VB_ASSEMBLE_GATHER),
-                       ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+                       ("tile", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
         gv = None if name == "atomic" else name
         rec("config4 2D assembly variant=%s" % name, e4.shape[1], "elements",
             alg_bytes_assembly(2, c4.shape[1], e4.shape[1], p4.nnz),
@@ -597,7 +612,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="vb", choices=["vb", "reference"])
-    ap.add_argument("--variant", default="class", choices=["class", "block", "gather", "atomic"],
+    ap.add_argument("--variant", default="class", choices=["class", "block", "tile", "gather", "atomic"],
                     help="gather = block (older name)")
     ap.add_argument("--quick", action="store_true", help="headline only (no secondary rows)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -287,6 +287,57 @@ VB_API vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* coor
                                          const int32_t* class_rows, const int32_t* groups, int64_t ngroups,
                                          double* K_vals, double* M_vals, vb_stream_t stream);
 
+/* ---------------------------------------------------------- tile variant
+ * Element-once deterministic assembly (same K, M as fem_p1_assemble, c = 1:
+ * eq:K_M P:967-975, stiffness_matrixP1 P:978-1004, mass_matrixP1 P:1007,
+ * accumulated as sparse(X3D(:),Y3D(:),..) P:1001-1003).  The rows are ordered
+ * along a Morton curve of the node coordinates and cut into tiles of
+ * VB_TILE_ROWS rows; every element is evaluated once per tile it has a vertex
+ * in, and adds its off-diagonal K_e/M_e entries into the tile's rows in shared
+ * memory, in the color order of the plan (elements of one color update
+ * disjoint entries).  Diagonals from the partition of unity (K_vv = -sum_{w!=v}
+ * K_vw, M_vv = (2/d) sum_{w!=v} M_vw).  Each CSR entry is written once, no
+ * atomics; bitwise reproducible.
+ *
+ * fem_plan_tiles builds the plan from the CSR pattern of fem_p1_pattern
+ * (row_ptr, col_idx) and the mesh; the coordinates only choose the tiles (any
+ * coordinates give a correct plan; near ones give compact tiles).  Outputs
+ * (DEVICE, caller-owned; ntiles = ceil(nn / VB_TILE_ROWS)):
+ *   tile_meta   (ntiles x 4 int32): owned rows, local nodes, colors, first entry;
+ *   tile_nodes  (ntiles x VB_TILE_NLOC int32): local node table (owned rows in
+ *               tile order, then the halo in ascending node id);
+ *   tile_rows   (ntiles x VB_TILE_ROWS x 2 int32): row_ptr[v], L | diag slot << 8;
+ *   tile_colors (ntiles x (VB_TILE_MAXC + 1) int32): entry offsets per color;
+ *   tile_elems  (elems_cap x 4 uint32): one entry per (tile, element): the
+ *               local ids of the element's vertices and the in-row slots.
+ * stats_out (HOST, 6 int64): entries, max elements per tile, max local nodes
+ * (pass it as nloc_max), max colors, refusal reason (0 = none), ntiles.
+ * VB_ERR_WORKSPACE when the entries do not fit elems_cap (stats_out[0] holds
+ * the count; nv * ne always suffices); VB_ERR_UNSUPPORTED when a row has more
+ * than 16 entries or a tile needs more than 3072 elements, VB_TILE_NLOC local
+ * nodes or VB_TILE_MAXC colors (unstructured meshes with long rows: use the
+ * other variants).  work: DEVICE scratch, work == NULL queries its size.
+ * Synchronises the stream (two small read-backs). */
+#define VB_TILE_ROWS 128
+#define VB_TILE_NLOC 1024
+#define VB_TILE_MAXC 32
+VB_API vb_status fem_plan_tiles(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
+                                int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                                const int32_t* row_ptr, const int32_t* col_idx, void* work, size_t* work_bytes,
+                                int32_t* tile_meta, int32_t* tile_nodes, int32_t* tile_rows,
+                                int32_t* tile_colors, uint32_t* tile_elems, int64_t elems_cap,
+                                int64_t* stats_out, vb_stream_t stream);
+/* K_vals / M_vals (nnz each, nullable) overwritten; coords strided as in
+ * vb_create_coords3D; plan arrays, nloc_max (stats_out[2], <= VB_TILE_NLOC)
+ * and elems_max (stats_out[1]: sizes the shared-memory staging of a tile's
+ * entries) from fem_plan_tiles on the same mesh and pattern.  tile_elems must
+ * be 16-byte aligned (bulk copies). */
+VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                       int64_t comp_stride, int64_t nnz, const int32_t* tile_meta,
+                                       const int32_t* tile_nodes, const int32_t* tile_rows,
+                                       const int32_t* tile_colors, const uint32_t* tile_elems, int nloc_max,
+                                       int elems_max, double* K_vals, double* M_vals, vb_stream_t stream);
+
 /* ---------------------------------------------------------- NEXT-1: coefficients
  * As fem_p1_assemble, with the coefficient functions of eq:K_M
  *   c_K(x) = cK_a * exp(cK_b . x),   c_M(x) = cM_a * exp(cM_b . x)

@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("VB_LIBVB") or os.path.join(_HERE, "libvb.so")   # VB_
 VB_ASSEMBLE_ATOMIC = 0
 VB_ASSEMBLE_GATHER = 1
 VB_GATHER_HINT_COMPACT = 0x100
+TILE_ROWS, TILE_NLOC, TILE_MAXC = 128, 1024, 32   # VB_TILE_ROWS, VB_TILE_NLOC, VB_TILE_MAXC
 
 
 def _gather_mode(mode, plan, compact):
@@ -45,7 +46,7 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
-           "fem_p1_assemble_classes")
+           "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles")
 
 
 class VbError(RuntimeError):
@@ -88,6 +89,9 @@ def lib():
             "fem_plan_pack_slots": (i32, [i32, i64, p, p, p, p]),
             "fem_plan_classes": (i32, [i32, i64, p, p, p, p, sz, p, p, i64, C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_classes": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, p, p, p]),
+            "fem_plan_tiles": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, p, sz, p, p, p, p, p, i64,
+                                     C.POINTER(C.c_int64), p]),
+            "fem_p1_assemble_tiles": (i32, [i32, i64, p, i64, i64, i64, p, p, p, p, p, i32, i32, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -314,6 +318,44 @@ class P1Plan:
             self.class_stats = tuple(int(x) for x in stats)
         return self.class_rows
 
+    def tiles(self, coords, elems):
+        """Tile plan (fem_plan_tiles), built once and kept; coords only choose the
+        tiles.  Returns True, or False when the mesh is outside the tile
+        variant's limits (plan.tile_reason says why)."""
+        if getattr(self, "tile_ok", None) is not None:
+            return self.tile_ok
+        _f64(coords)
+        dev = coords.device
+        L = lib()
+        sz = C.c_size_t(0)
+        st = _stream()
+        stats = (C.c_int64 * 6)()
+        dim, nn = coords.shape
+        ne = elems.shape[1]
+        _check(L.fem_plan_tiles(self.dim, nn, ne, None, 1, nn, None, ne, None, None, None, C.byref(sz), None, None,
+                                None, None, None, 0, stats, st))
+        work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
+        T = (nn + TILE_ROWS - 1) // TILE_ROWS
+        self.tile_meta = torch.empty((max(T, 1), 4), dtype=torch.int32, device=dev)
+        self.tile_nodes = torch.empty((max(T, 1), TILE_NLOC), dtype=torch.int32, device=dev)
+        self.tile_rows = torch.empty((max(T, 1), TILE_ROWS, 2), dtype=torch.int32, device=dev)
+        self.tile_colors = torch.empty((max(T, 1), TILE_MAXC + 1), dtype=torch.int32, device=dev)
+        cap = max(self.nv * ne, 1)
+        elems_buf = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+        rc = L.fem_plan_tiles(self.dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(self.row_ptr),
+                              _ptr(self.col_idx), _ptr(work), C.byref(sz), _ptr(self.tile_meta),
+                              _ptr(self.tile_nodes), _ptr(self.tile_rows), _ptr(self.tile_colors), _ptr(elems_buf),
+                              cap, stats, st)
+        self.tile_stats = tuple(int(x) for x in stats)   # entries, max elems/tile, max nodes/tile, colors, reason, T
+        if rc == -3:
+            self.tile_ok, self.tile_reason = False, lib().vb_last_error().decode()
+            self.tile_meta = self.tile_nodes = self.tile_rows = self.tile_colors = self.tile_elems = None
+            return False
+        _check(rc)
+        self.tile_elems = elems_buf[:max(self.tile_stats[0], 1)].clone()   # keep only the used entries
+        self.tile_ok, self.tile_reason = True, ""
+        return True
+
     def class_coverage(self):
         """Fraction of rows that the class variant assembles with the uniform loop."""
         if self.classes() is None or self.nn == 0:
@@ -334,12 +376,28 @@ def fem_p1_pattern(elems, nn, scatter_map=True, gather_plan=True, stream=None):
     return P1Plan(elems, nn, scatter_map, gather_plan, stream)
 
 
+def fem_p1_assemble_tiles(coords, plan, K=None, M=None, want_K=True, want_M=True, stream=None):
+    """Tile-variant K, M (fem_p1_assemble_tiles) on a plan whose tiles() were built."""
+    _f64(coords)
+    dim, nn = coords.shape
+    dev = coords.device
+    if not getattr(plan, "tile_ok", False):
+        raise ValueError("plan has no tile plan: call plan.tiles(coords, elems) first (and check it returned True)")
+    K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
+    M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
+    _check(lib().fem_p1_assemble_tiles(dim, nn, _ptr(coords), 1, nn, plan.nnz, _ptr(plan.tile_meta),
+                                       _ptr(plan.tile_nodes), _ptr(plan.tile_rows), _ptr(plan.tile_colors),
+                                       _ptr(plan.tile_elems), plan.tile_stats[2], plan.tile_stats[1], _ptr(K), _ptr(M),
+                                       _stream(stream)))
+    return K, M
+
+
 def _use_classes(plan, variant):
     """Gather variant: "class" (row classes, fem_p1_assemble_classes), "block"
     (32-row blocks, fem_p1_assemble) or None = "class" when at least 90 % of the
     rows fall into row classes (meshes from uniform refinement), else "block"."""
-    if variant not in (None, "class", "block"):
-        raise ValueError("variant must be None, 'class' or 'block'")
+    if variant not in (None, "class", "block", "tile"):
+        raise ValueError("variant must be None, 'class', 'block' or 'tile'")
     if variant == "block" or plan.node_elem_ptr is None:
         return False
     if variant == "class":
@@ -380,6 +438,16 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         M = None
     Kl = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
     Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+    if (mode == VB_ASSEMBLE_GATHER and variant == "tile" and (K is not None or M is not None)
+            and plan.tiles(coords, elems)):
+        fem_p1_assemble_tiles(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
+        if want_local:
+            _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
+                                         None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
+                                         _stream(stream)))
+        return K, M, Kl, Ml
+    if variant == "tile":
+        variant = "block"   # outside the tile variant's limits (plan.tile_reason)
     if mode == VB_ASSEMBLE_GATHER and (K is not None or M is not None) and _use_classes(plan, variant):
         fem_p1_assemble_classes(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
         if want_local:

@@ -15,9 +15,11 @@ import synth
 from paper_2404_16039_b200 import vb
 
 pytestmark = pytest.mark.gpu
-# (mode, gather variant): row classes, 32-row blocks, atomic scatter
-MODES = [(vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"), (vb.VB_ASSEMBLE_ATOMIC, None)]
-MODE_IDS = ["class", "block", "atomic"]
+# (mode, gather variant): row classes, 32-row blocks, element-once tiles (falls
+# back to blocks outside its limits), atomic scatter
+MODES = [(vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"), (vb.VB_ASSEMBLE_GATHER, "tile"),
+         (vb.VB_ASSEMBLE_ATOMIC, None)]
+MODE_IDS = ["class", "block", "tile", "atomic"]
 
 
 @pytest.fixture(scope="module")
@@ -105,7 +107,7 @@ def test_assembly_parity(dev, kind, n, mode):
     assert relmax(h(Kl), K3o) <= 1e-12 and relmax(h(Ml), M3o) <= 1e-12
 
 
-@pytest.mark.parametrize("variant", ["class", "block"])
+@pytest.mark.parametrize("variant", ["class", "block", "tile"])
 def test_gather_variant_bitwise_reproducible(dev, variant):
     coords, elems = mesh("3d", 12, seed=2)
     cd, ed = g(coords, dev), g(elems, dev)
@@ -115,6 +117,73 @@ def test_gather_variant_bitwise_reproducible(dev, variant):
     for _ in range(3):
         K2, M2, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=vb.VB_ASSEMBLE_GATHER, variant=variant)
         assert np.array_equal(h(K2), K1) and np.array_equal(h(M2), M1)
+
+
+@pytest.mark.parametrize("kind,n,permute", [("3d", 1, False), ("3d", 9, False), ("3d", 9, True), ("2d", 40, False),
+                                            ("delaunay2", 30, True)])
+def test_tile_plan(dev, kind, n, permute):
+    """fem_plan_tiles: the tiles' owned rows partition the rows; each tile holds
+    exactly the elements with a vertex in it, with local ids that map back to
+    the element's vertices; the slots point at the right CSR columns; the halo
+    is ascending; within a color no two entries update the same (row, slot)."""
+    if kind == "delaunay2":
+        coords, elems = synth.delaunay_p1(2, n, seed=3)
+    else:
+        coords, elems = mesh(kind, n, seed=3)
+    if permute:
+        coords, elems = synth.permute_mesh(coords, elems, seed=6)
+    nn = coords.shape[1]
+    nv, ne = elems.shape
+    rp, ci = oracle.p1_pattern(elems, nn)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    assert plan.tiles(cd, ed), plan.tile_reason
+    meta, nodes, rows = h(plan.tile_meta), h(plan.tile_nodes), h(plan.tile_rows)
+    cols, ent = h(plan.tile_colors), h(plan.tile_elems).view(np.uint32)
+    T = (nn + vb.TILE_ROWS - 1) // vb.TILE_ROWS
+    assert plan.tile_stats[5] == T and plan.tile_stats[2] <= vb.TILE_NLOC
+    owned = np.concatenate([nodes[t, :meta[t, 0]] for t in range(T)])
+    assert np.array_equal(np.sort(owned), np.arange(nn))
+    tile_of = np.empty(nn, dtype=np.int64)
+    for t in range(T):
+        tile_of[nodes[t, :meta[t, 0]]] = t
+    total = 0
+    for t in range(T):
+        nown, nloc, ncol, e0 = meta[t]
+        tn = nodes[t, :nloc]
+        assert np.all(np.diff(tn[nown:]) > 0) and not np.any(tile_of[tn[nown:]] == t)
+        for i in range(nown):
+            v = tn[i]
+            lo, info = rows[t, i]
+            assert lo == rp[v] and (info & 0xFF) == rp[v + 1] - rp[v] and ci[lo + (info >> 8)] == v
+        assert cols[t, 0] == e0
+        E = ent[cols[t, 0]:cols[t, ncol]]
+        total += len(E)
+        loc = np.stack([E[:, 0] & 0xFFFF, E[:, 0] >> 16, E[:, 1] & 0xFFFF, E[:, 1] >> 16])[:nv]
+        verts = tn[loc]                                            # (nv, entries) global vertex ids
+        want = elems[:, np.any(tile_of[elems] == t, axis=0)]
+        assert sorted(map(tuple, verts.T)) == sorted(map(tuple, want.T))
+        sb = E[:, 2].astype(np.uint64) | (E[:, 3].astype(np.uint64) << np.uint64(32))
+        for c in range(ncol):
+            seen = set()
+            for k in range(cols[t, c] - e0, cols[t, c + 1] - e0):
+                for a in range(nv):
+                    if loc[a, k] >= nown:
+                        continue
+                    others = [b for b in range(nv) if b != a]
+                    for j, b in enumerate(others):
+                        sl = int((sb[k] >> np.uint64(4 * (nv - 1) * a + 4 * j)) & np.uint64(15))
+                        assert ci[rp[verts[a, k]] + sl] == verts[b, k]
+                        key = (int(loc[a, k]), sl)
+                        assert key not in seen
+                        seen.add(key)
+    assert total == plan.tile_stats[0]
+
+
+def test_tile_plan_refuses_long_rows(dev):
+    coords, elems = fan_mesh(40)
+    plan = vb.P1Plan(g(elems, dev), coords.shape[1])
+    assert not plan.tiles(g(coords, dev), g(elems, dev)) and "longer than 16" in plan.tile_reason
 
 
 def signature(v, rp, nptr, nsl):
