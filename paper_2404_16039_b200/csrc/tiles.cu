@@ -253,9 +253,9 @@ __global__ void __launch_bounds__(TR) tl_build_k(int64_t nn, const int32_t* __re
             S.rcol[tid * TS + q] = c;
             if (c == g) s0 = q;
         }
-        if (L > TS || s0 < 0) atomicExch(&S.err, TE_ROW);
+        if (L > TS || (L > 0 && s0 < 0)) atomicExch(&S.err, TE_ROW);   // L = 0: an isolated node
         S.rL[tid] = L;
-        trows[t * TR + tid] = make_int2(lo, L | s0 << 8);
+        trows[t * TR + tid] = make_int2(lo, L | (s0 & 0xff) << 8);
         tnodes[t * NLOC + tid] = g;
     }
     // elements and their halo vertices
@@ -521,7 +521,7 @@ __global__ void __launch_bounds__(TR, 3) assemble_tile_k(int64_t T, const int4* 
             __syncthreads();
         }
         // diagonals from the partition of unity
-        if (tid < nown) {
+        if (tid < nown && (rinfo[tid].y & 0xff) > 0) {
             const int L = rinfo[tid].y & 0xff, s0 = rinfo[tid].y >> 8;
             double sk = 0.0, sm = 0.0;
 #pragma unroll
@@ -629,8 +629,8 @@ extern "C" vb_status fem_plan_tiles(int dim, int64_t nn, int64_t ne, const doubl
     const int64_t T = (nn + TR - 1) / TR;
     stats_out[5] = T;
     if (nn == 0) return VB_OK;
-    if (!coords || !elems || !row_ptr || !col_idx || !tile_meta || !tile_nodes || !tile_rows || !tile_colors ||
-        (!tile_elems && ne > 0)) {
+    if (!coords || !row_ptr || !tile_meta || !tile_nodes || !tile_rows || !tile_colors ||
+        (ne > 0 && (!elems || !col_idx || !tile_elems))) {
         set_error("%s: NULL argument", fn);
         return VB_ERR_ARG;
     }
