@@ -338,6 +338,24 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
                                        const int32_t* tile_colors, const uint32_t* tile_elems, int nloc_max,
                                        int elems_max, double* K_vals, double* M_vals, vb_stream_t stream);
 
+/* ---------------------------------------------------------- exact-order check
+ * The verification path of SURVEY §8(c) ("bitwise mode"): K and M (c = 1) with
+ * every operation of the definition as an IEEE round-to-nearest fp64
+ * operation (no FMA contraction) in the written order -- tjac = D X^T,
+ * det by Laplace expansion along row 0, |T| = |det|/d!,
+ * Jinv = adjugate/det, G = Jinv D, K_e = |T| sum_r G_ra G_rb
+ * (P:996), M_e = |T|/((d+1)(d+2)) (1+delta_ab) -- and duplicates
+ * summed per CSR entry from 0 in ascending element id.  Any
+ * plain IEEE fp64 program doing the same gets the same bits.  One thread per
+ * row over node_elem (fem_p1_pattern's gather plan, entries e*4 + a, ascending
+ * e); slow by design, for checking the fast variants.  K_vals / M_vals (nnz,
+ * nullable) overwritten; coords and elems strided as fem_p1_assemble. */
+VB_API vb_status fem_p1_assemble_exact(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                       int64_t comp_stride, const int32_t* elems, int64_t elem_ld,
+                                       const int32_t* row_ptr, const int32_t* col_idx,
+                                       const int32_t* node_elem_ptr, const int32_t* node_elem, double* K_vals,
+                                       double* M_vals, vb_stream_t stream);
+
 /* ---------------------------------------------------------- NEXT-1: coefficients
  * As fem_p1_assemble, with the coefficient functions of eq:K_M
  *   c_K(x) = cK_a * exp(cK_b . x),   c_M(x) = cM_a * exp(cM_b . x)

@@ -46,7 +46,8 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "vb_page_inv", "vb_page_cross", "vb_create_coords3D", "vb_tri_surface", "fem_p1_pattern",
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
-           "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles")
+           "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
+           "fem_p1_assemble_exact")
 
 
 class VbError(RuntimeError):
@@ -92,6 +93,7 @@ def lib():
             "fem_plan_tiles": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, p, sz, p, p, p, p, p, i64,
                                      C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_tiles": (i32, [i32, i64, p, i64, i64, i64, p, p, p, p, p, i32, i32, p, p, p]),
+            "fem_p1_assemble_exact": (i32, [i32, i64, p, i64, i64, p, i64, p, p, p, p, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -389,6 +391,24 @@ def fem_p1_assemble_tiles(coords, plan, K=None, M=None, want_K=True, want_M=True
                                        _ptr(plan.tile_nodes), _ptr(plan.tile_rows), _ptr(plan.tile_colors),
                                        _ptr(plan.tile_elems), plan.tile_stats[2], plan.tile_stats[1], _ptr(K), _ptr(M),
                                        _stream(stream)))
+    return K, M
+
+
+def fem_p1_assemble_exact(coords, elems, plan, want_K=True, want_M=True, stream=None):
+    """K, M in the definition's exact operation order (fem_p1_assemble_exact):
+    bitwise equal to any plain IEEE fp64 evaluation of it in that order.  Slow;
+    for checking.  Needs the plan's gather lists (node_elem)."""
+    _f64(coords)
+    dim, nn = coords.shape
+    ne = elems.shape[1]
+    dev = coords.device
+    if plan.node_elem_ptr is None:
+        raise ValueError("fem_p1_assemble_exact needs a plan with gather_plan=True")
+    K = torch.empty((plan.nnz,), dtype=torch.float64, device=dev) if want_K else None
+    M = torch.empty((plan.nnz,), dtype=torch.float64, device=dev) if want_M else None
+    _check(lib().fem_p1_assemble_exact(dim, nn, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
+                                       _ptr(plan.col_idx), _ptr(plan.node_elem_ptr), _ptr(plan.node_elem), _ptr(K),
+                                       _ptr(M), _stream(stream)))
     return K, M
 
 

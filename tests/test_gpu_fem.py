@@ -180,6 +180,34 @@ def test_tile_plan(dev, kind, n, permute):
     assert total == plan.tile_stats[0]
 
 
+@pytest.mark.parametrize("kind,n,permute", [("2d", 20, False), ("3d", 6, False), ("delaunay3", 7, True),
+                                            ("delaunay2", 30, False), ("fan", 40, False)])
+def test_exact_order_bitwise_equals_oracle(dev, kind, n, permute):
+    """fem_p1_assemble_exact (SURVEY §8(c) bitwise mode) reproduces the oracle bit
+    for bit on jittered and unstructured meshes: the same definition, the same
+    operation order, IEEE round-to-nearest without contraction on both sides."""
+    if kind.startswith("delaunay"):
+        coords, elems = synth.delaunay_p1(int(kind[-1]), n, seed=8)
+    elif kind == "fan":
+        coords, elems = fan_mesh(n, 3)
+    else:
+        coords, elems = mesh(kind, n, seed=8)
+    if permute:
+        coords, elems = synth.permute_mesh(coords, elems, seed=9)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    K, M = vb.fem_p1_assemble_exact(cd, ed, plan)
+    assert np.array_equal(h(K).view(np.uint64), Ko.view(np.uint64))
+    assert np.array_equal(h(M).view(np.uint64), Mo.view(np.uint64))
+    # M only, K only
+    _, M2 = vb.fem_p1_assemble_exact(cd, ed, plan, want_K=False)
+    K2, _ = vb.fem_p1_assemble_exact(cd, ed, plan, want_M=False)
+    assert np.array_equal(h(M2), h(M)) and np.array_equal(h(K2), h(K))
+
+
 def test_tile_plan_refuses_long_rows(dev):
     coords, elems = fan_mesh(40)
     plan = vb.P1Plan(g(elems, dev), coords.shape[1])
@@ -335,7 +363,9 @@ def sampled_rows(nn, count=4000, seed=0):
 @pytest.mark.parametrize("cfg", ["config5", "config4"])
 def test_full_size_assembly_sampled(dev, cfg):
     """configs[4] (128^3 Kuhn, 12.58M tets) and configs[3] (2048^2 square,
-    8.39M triangles): pattern bit-exact in full, K/M on sampled rows."""
+    8.39M triangles): pattern bit-exact in full; K/M against the oracle on
+    sampled rows, and over every entry against the exact-order path, which is
+    itself bitwise equal to the oracle on the sampled rows."""
     if cfg == "config5":
         coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
     else:
@@ -350,11 +380,18 @@ def test_full_size_assembly_sampled(dev, cfg):
     Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci, row_mask=mask)
     rows = np.repeat(np.arange(nn), np.diff(rp))
     sel = mask[rows] == 1
+    # the exact-order path: bitwise equal to the oracle on the sampled rows, then the
+    # whole-matrix reference for every fast variant
+    Kx, Mx = vb.fem_p1_assemble_exact(cd, ed, plan)
+    Kx, Mx = h(Kx), h(Mx)
+    assert np.array_equal(Kx[sel].view(np.uint64), Ko[sel].view(np.uint64))
+    assert np.array_equal(Mx[sel].view(np.uint64), Mo[sel].view(np.uint64))
     for mode in MODES:
         K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1])
         K, M = h(K), h(M)
         assert relmax(K[sel], Ko[sel]) <= 1e-12
         assert relmax(M[sel], Mo[sel]) <= 1e-12
+        assert relmax(K, Kx) <= 1e-12 and relmax(M, Mx) <= 1e-12    # every entry of both matrices
         assert abs(math.fsum(M) - 1.0) <= 1e-12                      # whole-matrix property
 
 
