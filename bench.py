@@ -481,7 +481,15 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     F, V = tri.shape[1], xyz.shape[1]
     rec("config3 tri_surface (n, nhat, area, volume)", F, "triangles", F * (12 + 56) + V * 24,
         time_kernel(lambda: vb.vb_tri_surface(xd, td, out=out, work=out["work"]), 10, flush))
-    del xd, td, out
+    # config 3, K5 alone: the cross products as a page op on pre-gathered
+    # edge-vector pages (vectors3D of create_coords3D, 2 x 3 planes of F pages): 48 B in + 24 B out
+    _, v3 = vb.vb_create_coords3D(xd, td, want_coords3D=False)
+    ea, eb = v3[0].contiguous(), v3[1].contiguous()
+    del v3
+    cr = torch.empty((1, 3, F), dtype=torch.float64, device=dev)
+    rec("config3 page_cross on pre-gathered edge-vector pages (K5 alone)", F, "pages", F * 72,
+        time_kernel(lambda: vb.vb_page_cross(ea, eb, Cout=cr), 10, flush))
+    del xd, td, out, ea, eb, cr
     # config 2: page sweep
     N = 1 << 20
     for n in (2, 3, 4):
