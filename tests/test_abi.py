@@ -91,3 +91,29 @@ def test_fem_argument_errors(L):
     assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, None,
                              None, None, 0, None) == -1                     # atomic mode without elem2nnz
     assert b"elem2nnz" in L.vb_last_error()
+
+
+def test_tile_and_exact_argument_errors(L):
+    sz = C.c_size_t(0)
+    stats = (C.c_int64 * 6)()
+    # fem_plan_tiles: unsupported dim, NULL work_bytes, size overflow; the work-size query needs no GPU
+    assert L.fem_plan_tiles(4, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, None, C.byref(sz), None, None, None, None,
+                            None, 0, stats, None) == -3
+    assert L.fem_plan_tiles(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, None, None, None, None, None, None,
+                            None, 0, stats, None) == -1
+    assert L.fem_plan_tiles(3, 1 << 30, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, None, C.byref(sz), None, None, None,
+                            None, None, 0, stats, None) == -4
+    assert L.fem_plan_tiles(3, 1000, 6000, None, 1, 1000, None, 6000, None, None, None, C.byref(sz), None, None, None,
+                            None, None, 0, stats, None) == 0
+    assert sz.value > 0
+    # fem_p1_assemble_tiles: nloc_max beyond the node table, bad dim
+    assert L.fem_p1_assemble_tiles(3, 10, FAKE, 1, 10, 5, FAKE, FAKE, FAKE, FAKE, FAKE, 4096, 10, FAKE, FAKE,
+                                   None) == -1
+    assert b"nloc_max" in L.vb_last_error()
+    assert L.fem_p1_assemble_tiles(1, 10, FAKE, 1, 10, 5, FAKE, FAKE, FAKE, FAKE, FAKE, 10, 10, FAKE, FAKE,
+                                   None) == -3
+    # fem_p1_assemble_exact: bad dim, missing gather lists
+    assert L.fem_p1_assemble_exact(5, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, FAKE, FAKE, FAKE, FAKE, None) == -3
+    assert L.fem_p1_assemble_exact(3, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, None, None, FAKE, FAKE, None) == -1
+    # nothing requested: a no-op
+    assert L.fem_p1_assemble_exact(3, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, None, None, None, None, None) == 0
