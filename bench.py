@@ -434,11 +434,12 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     pp = vb.P1Plan(edp, cp_.shape[1])
     Kp = torch.empty(pp.nnz, dtype=torch.float64, device=dev)
     Mp = torch.empty(pp.nnz, dtype=torch.float64, device=dev)
-    for name, mode in (("gather", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+    for name, mode, gv in (("class", vb.VB_ASSEMBLE_GATHER, "class"), ("block", vb.VB_ASSEMBLE_GATHER, "block"),
+                           ("atomic", vb.VB_ASSEMBLE_ATOMIC, None)):
         rec("NEXT-1 paper tab:KM_P1_3D level 7, c=exp(x+y+z), gqo=2, variant=%s (paper: K 66.6 s + M 20.4 s, "
             "MATLAB, hardware not stated)" % name, ep_.shape[1], "elements",
             alg_bytes_assembly(3, cp_.shape[1], ep_.shape[1], pp.nnz),
-            time_kernel(lambda: vb.fem_p1_assemble_coef(cdp, edp, pp, gqo=2, mode=mode, K=Kp, M=Mp), 10))
+            time_kernel(lambda: vb.fem_p1_assemble_coef(cdp, edp, pp, gqo=2, mode=mode, K=Kp, M=Mp, variant=gv), 10))
     del pp, Kp, Mp, cdp, edp
     # NEXT-3: P2, Table tab:KM_P2_3D level 6 (64^3 cells, 2,146,689 P2 nodes, c = e^{x+y+z}, gqo = 4);
     # paper: K 87.6 s + M 16.4 s, hardware not stated

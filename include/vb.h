@@ -379,6 +379,23 @@ VB_API vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne,
                           double* K_local, double* M_local,
                           int mode, vb_stream_t stream);
 
+/* NEXT-1 through the row classes: fem_p1_assemble_classes with c_K = c_M =
+ * c_a exp(c_b . x) (c_b: HOST array of 3 doubles, NULL = 0) and the gqo = 2
+ * rule of fem_p1_assemble_coef (Code stiff_scalar_P1 P:978-1004, the paper's
+ * benchmark case P:1149-1176).  The coefficient at a quadrature point is formed
+ * from per-node factors P = exp(beta c_b.x), R = exp((alpha - beta) c_b.x)
+ * computed into work (DEVICE, 2 nn doubles, caller-owned) at the start of the
+ * call.  dim = 3 and gqo = 2 only (VB_ERR_UNSUPPORTED otherwise: use
+ * fem_p1_assemble_coef).  Other arguments and guarantees as
+ * fem_p1_assemble_classes. */
+VB_API vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                              int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx,
+                                              int64_t nnz, const int32_t* node_elem_ptr,
+                                              const uint32_t* node_elem_slot, const int32_t* class_rows,
+                                              const int32_t* groups, int64_t ngroups, int gqo, double c_a,
+                                              const double* c_b, double* work, double* K_vals, double* M_vals,
+                                              vb_stream_t stream);
+
 /* ---------------------------------------------------------- NEXT-2: rhs, energies
  * intquad(gqo, dim) as used by the kernels: writes the barycentric
  * points lam[q*(dim+1) + a] and weights w[q] (HOST arrays, nullable; at most 4

@@ -926,14 +926,14 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #ifndef VB_CLASS_PAIRS
 #define VB_CLASS_PAIRS 1   // 3D: incidences paired over shared link edges (build_pairs)
 #endif
-template <int DIM>
+template <int DIM, int NC = DIM>   // NC doubles staged per column slot: coordinates (+ P, R coefficient factors)
 struct ClassCfg {
     static constexpr int MAXL = DIM == 3 ? 16 : 8;   // register accumulators per row (acc_slot)
     static constexpr int FSLOTS = DIM == 3 ? 15 : 8; // columns per row (fem_plan_classes' maxl)
     static constexpr int MAXN = DIM == 3 ? 32 : 16;  // incidences per row (fem_plan_classes' maxn)
-    static constexpr int FN = FSLOTS * DIM * 32;     // doubles of the edge-vector buffer
+    static constexpr int FN = FSLOTS * NC * 32;      // doubles of the edge-vector buffer
     static constexpr int MOFF = 32 * FSLOTS + 2;     // staging: K at [1, ..), M at [MOFF + 1, ..) (16-byte phase)
-    static constexpr int SLOT_BYTES = DIM * 32 * 8;  // stride of one slot in the edge-vector buffer
+    static constexpr int SLOT_BYTES = NC * 32 * 8;   // stride of one slot in the edge-vector buffer
 };
 
 // aK[s] += k, aM[s] += m for a warp-uniform slot s (0 <= s < N): one indexed branch
@@ -1051,8 +1051,14 @@ struct ClassGroup {
 #ifndef VB_CLASS_MINB
 #define VB_CLASS_MINB 16
 #endif
-template <int DIM, bool NS1>   // NS1: node_stride == 1 (SoA coordinate planes)
-__global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
+// COEF (3D): c_K = c_M = a exp(b . x) with the gqo = 2 rule (NEXT-1, Code
+// stiff_scalar_P1 P:978-1004): per-node factors P_i = exp(beta b.x_i), R_i =
+// exp((alpha - beta) b.x_i) (facP, facR) are staged next to the coordinates,
+// so c at point q of an element is a R_q prod_i P_i (apply_coef); K_e is the
+// c = 1 K_e times kbar = d! w sum_q c_q, M_e[v][x] = |det| w sum_q c_q
+// lam_v(q) lam_x(q), and M_vv = row sum - off-diagonals.
+template <int DIM, bool NS1, bool COEF = false>   // NS1: node_stride == 1 (SoA coordinate planes)
+__global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
                                                        const int32_t* __restrict__ class_rows,
                                                        const double* __restrict__ coords, int64_t ns, int64_t cst,
                                                        const int32_t* __restrict__ row_ptr,
@@ -1060,11 +1066,14 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                                                        const int32_t* __restrict__ nptr,
                                                        const uint32_t* __restrict__ nslot, double* __restrict__ K,
                                                        double* __restrict__ M, unsigned int* __restrict__ ctr,
-                                                       bool bulk, int rounds) {
-    using C = ClassCfg<DIM>;
+                                                       bool bulk, int rounds, const double* __restrict__ facP,
+                                                       const double* __restrict__ facR, CoefSpec cp) {
+    static_assert(!COEF || DIM == 3, "the class coefficient path is 3D");
+    constexpr int NC = COEF ? DIM + 2 : DIM;
+    using C = ClassCfg<DIM, NC>;
     constexpr int MAXL = C::MAXL;
     constexpr unsigned FULL = 0xffffffffu;
-    constexpr double MS = DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0;   // 1/(d! (d+1)(d+2))
+    constexpr double MS = COEF ? 1.0 : (DIM == 2 ? 1.0 / 24.0 : 1.0 / 120.0);   // 1/(d! (d+1)(d+2))
     constexpr double KS = DIM == 2 ? -0.5 : -1.0 / 6.0;          // -1/d!
     __shared__ __align__(16) double F[C::FN];                    // edge vectors; then the CSR staging of K, M
     __shared__ __align__(16) int32_t colbuf[C::FSLOTS * 32];     // columns of the next group ([slot][lane])
@@ -1119,7 +1128,7 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
     int pat_head = -1, L = 0, n = 0, s0 = 0, nst = 0;   // nst: steps of the class's loop
     while (cur.head != -2) {
         const bool fast = cur.head >= 0;
-        double xv[DIM];
+        double xv[DIM], pvP = 0.0, pvR = 0.0;
         if (fast) {
             if (cur.head != pat_head) {   // class of this group: row length, incidences, decoded plan words
                 pat_head = cur.head;
@@ -1154,10 +1163,18 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                     const int w = colbuf[s * 32 + t];
 #pragma unroll
                     for (int c = 0; c < DIM; c++)
-                        cp_async8(F + (s * DIM + c) * 32 + t, NS1 ? X[c] + w : X[c] + (int64_t)w * ns);
+                        cp_async8(F + (s * NC + c) * 32 + t, NS1 ? X[c] + w : X[c] + (int64_t)w * ns);
+                    if constexpr (COEF) {
+                        cp_async8(F + (s * NC + DIM) * 32 + t, facP + w);
+                        cp_async8(F + (s * NC + DIM + 1) * 32 + t, facR + w);
+                    }
                 }
 #pragma unroll
                 for (int c = 0; c < DIM; c++) xv[c] = __ldg(X[c] + (int64_t)cur.v * ns);
+                if constexpr (COEF) {
+                    pvP = __ldg(facP + cur.v);
+                    pvR = __ldg(facR + cur.v);
+                }
             } else {
 #pragma unroll
                 for (int c = 0; c < DIM; c++) xv[c] = 0.0;
@@ -1172,7 +1189,7 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
             cp_async_wait<0>();
             __syncwarp();
             if (nxt.head >= 0) issue_cols(nxt, Ln);
-            double aK[MAXL], aM[MAXL];
+            double aK[MAXL], aM[MAXL], mrow = 0.0;   // mrow: row sum of M (COEF)
 #pragma unroll
             for (int s = 0; s < MAXL; s++) aK[s] = aM[s] = 0.0;
             const char* Fb = reinterpret_cast<const char*>(F) + t * 8;
@@ -1238,6 +1255,76 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                     return fma(u[0], v[0], fma(u[1], v[1], u[2] * v[2]));
                 };
                 int4 Pn = pat[0];
+                if constexpr (COEF) {
+                    constexpr double AL = QuadRule<3>::ALPHA, BE = QuadRule<3>::BETA, WQ = QuadRule<3>::W;
+                    constexpr double B2 = BE * BE, GA = AL * BE - BE * BE, KW = QuadRule<3>::DFACT * WQ;
+                    // per-row constants: a P_v, gamma R_v, (alpha - beta) R_v
+                    const double aPv = cp.ka * pvP, gRv = GA * pvR, dRv = (AL - BE) * pvR;
+                    auto lf = [&](int off, double& Pf, double& Rf) {   // the slot's staged P, R factors
+                        Pf = *reinterpret_cast<const double*>(Fb + off + DIM * 256);
+                        Rf = *reinterpret_cast<const double*>(Fb + off + (DIM + 1) * 256);
+                    };
+                    for (int j = 0; j < nst; j++) {
+                        const int4 St = Pn;
+                        Pn = pat[j + 1 < nst ? j + 1 : 0];
+                        const int w = St.w;
+                        double fa[3], fb[3], fc[3], P[3], ha[3], hb[3], Sv[3];
+                        double Pa, Ra, Pb, Rb, Pc, Rc;
+                        ld(St.x, fa);
+                        ld(St.y, fb);
+                        ld(St.z, fc);
+                        lf(St.x, Pa, Ra);
+                        lf(St.y, Pb, Rb);
+                        lf(St.z, Pc, Rc);
+                        cross(fa, fb, P);
+                        cross(fb, fc, ha);
+                        cross(fc, fa, hb);
+                        const double ad = fabs(dot(fc, P));
+                        const double r = rcp_nr(ad);
+#pragma unroll
+                        for (int c = 0; c < 3; c++) Sv[c] = r * ((P[c] + ha[c]) + hb[c]);
+                        // element (v, a, b, c): c_q = a R_q P_v P_a P_b P_c
+                        const double base = aPv * Pa * Pb, sRab = (pvR + Ra) + Rb;
+                        const double p1 = base * Pc, sR1 = sRab + Rc;
+                        const double kb1 = KW * p1 * sR1, mw1 = ad * WQ * p1, t1 = fma(B2, sR1, gRv);
+                        double ka = kb1 * dot(Sv, ha), kb = kb1 * dot(Sv, hb);
+                        const double kc = kb1 * dot(Sv, P);
+                        double ma = mw1 * fma(GA, Ra, t1), mb = mw1 * fma(GA, Rb, t1);
+                        const double mc = mw1 * fma(GA, Rc, t1);
+                        double mr = mw1 * fma(BE, sR1, dRv);
+                        if (w & CLASS_PAIR) {
+                            // element (v, a, b, d)
+                            double fd[3], Pd, Rd;
+                            const int od = ((w >> 12) & 15) * C::SLOT_BYTES;
+                            ld(od, fd);
+                            lf(od, Pd, Rd);
+                            cross(fb, fd, ha);
+                            cross(fd, fa, hb);
+                            const double ad2 = fabs(dot(fd, P));
+                            const double r2 = rcp_nr(ad2);
+#pragma unroll
+                            for (int c = 0; c < 3; c++) Sv[c] = r2 * ((P[c] + ha[c]) + hb[c]);
+                            const double p2 = base * Pd, sR2 = sRab + Rd;
+                            const double kb2 = KW * p2 * sR2, mw2 = ad2 * WQ * p2, t2 = fma(B2, sR2, gRv);
+                            ka = fma(kb2, dot(Sv, ha), ka);
+                            kb = fma(kb2, dot(Sv, hb), kb);
+                            const double kd = kb2 * dot(Sv, P);
+                            ma = fma(mw2, fma(GA, Ra, t2), ma);
+                            mb = fma(mw2, fma(GA, Rb, t2), mb);
+                            const double md = mw2 * fma(GA, Rd, t2);
+                            mr = fma(mw2, fma(BE, sR2, dRv), mr);
+                            acc_slot(aK, aM, w & 15, ka, ma);
+                            acc_slot(aK, aM, (w >> 4) & 15, kb, mb);
+                            acc_slot(aK, aM, (w >> 8) & 15, kc, mc);
+                            acc_slot(aK, aM, (w >> 12) & 15, kd, md);
+                        } else {
+                            acc_slot(aK, aM, w & 15, ka, ma);
+                            acc_slot(aK, aM, (w >> 4) & 15, kb, mb);
+                            acc_slot(aK, aM, (w >> 8) & 15, kc, mc);
+                        }
+                        mrow += mr;
+                    }
+                } else
                 for (int j = 0; j < nst; j++) {
                     const int4 St = Pn;
                     Pn = pat[j + 1 < nst ? j + 1 : 0];
@@ -1307,7 +1394,7 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                         stM[t * L + s] = mm;
                     }
                 stK[t * L + s0] = -sk;
-                stM[t * L + s0] = DIM == 3 ? sm * (2.0 / 3.0) : sm;
+                stM[t * L + s0] = COEF ? mrow - sm : (DIM == 3 ? sm * (2.0 / 3.0) : sm);
             }
             __syncwarp();
             const int tot = cur.cnt * L;
@@ -1370,11 +1457,24 @@ __global__ void __launch_bounds__(32, VB_CLASS_MINB) assemble_class_k(int64_t ng
                         for (int c = 0; c < DIM; c++) f[c] = __ldg(X[c] + w * ns) - xr[c];
                     };
                     auto ix = [](int s) { return s; };
-                    const double pv[2] = {1.0, 1.0};
-                    auto nofac = [](int, double&, double&) {};
-                    const CoefSpec cp{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
-                    gather_row<DIM, false, false, false, uint32_t>(i0, i1, nslot, ev, nofac, ix, aK, aM, xr, pv, cp);
-                    finish_row<DIM, 1, false>(Lr, z0, aK, aM, 0.0);
+                    if constexpr (COEF) {
+                        const double pv[2] = {__ldg(facP + v), __ldg(facR + v)};
+                        auto fv = [&](int s, double& Pf, double& Rf) {
+                            const int64_t w = __ldg(col_idx + lo + s);
+                            Pf = __ldg(facP + w);
+                            Rf = __ldg(facR + w);
+                        };
+                        const double mr =
+                            gather_row<DIM, false, true, true, uint32_t>(i0, i1, nslot, ev, fv, ix, aK, aM, xr, pv, cp);
+                        finish_row<DIM, 1, true>(Lr, z0, aK, aM, mr);
+                    } else {
+                        const double pv[2] = {1.0, 1.0};
+                        auto nofac = [](int, double&, double&) {};
+                        const CoefSpec c1{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
+                        gather_row<DIM, false, false, false, uint32_t>(i0, i1, nslot, ev, nofac, ix, aK, aM, xr, pv,
+                                                                       c1);
+                        finish_row<DIM, 1, false>(Lr, z0, aK, aM, 0.0);
+                    }
                 }
             }
             __syncwarp();
@@ -1564,14 +1664,48 @@ extern "C" vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const
                           M_local, mode, &cp, stream);
 }
 
-extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* coords, int64_t node_stride,
-                                             int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx,
-                                             int64_t nnz, const int32_t* node_elem_ptr,
-                                             const uint32_t* node_elem_slot, const int32_t* class_rows,
-                                             const int32_t* groups, int64_t ngroups, double* K_vals,
-                                             double* M_vals, vb_stream_t stream) {
-    const char* fn = "fem_p1_assemble_classes";
-    clear_error();
+namespace vb {
+namespace {
+
+// per-node coefficient factors of the class coefficient path: P = exp(beta b.x), R = exp((alpha - beta) b.x)
+__global__ void class_factors_k(int64_t nn, const double* __restrict__ coords, int64_t ns, int64_t cst, double b0,
+                                double b1, double b2, double* __restrict__ P, double* __restrict__ R) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
+        const double bx = fma(b0, coords[v * ns], fma(b1, coords[cst + v * ns], b2 * coords[2 * cst + v * ns]));
+        P[v] = exp(QuadRule<3>::BETA * bx);
+        R[v] = exp((QuadRule<3>::ALPHA - QuadRule<3>::BETA) * bx);
+    }
+}
+
+template <typename Kern>
+void class_launch(Kern kern, cudaStream_t s, int64_t ngroups, const int32_t* groups, const int32_t* class_rows,
+                  const double* coords, int64_t node_stride, int64_t comp_stride, const int32_t* row_ptr,
+                  const int32_t* col_idx, const int32_t* node_elem_ptr, const uint32_t* node_elem_slot, double* K,
+                  double* M, unsigned int* ctr, bool bulk, const double* facP, const double* facR,
+                  const CoefSpec& cp) {
+    static int n = 0;   // resident CTAs per SM of this instantiation
+    if (!n) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32, 0);
+        if (n < 1) n = 1;
+    }
+    const int64_t cap = (int64_t)sm_count() * n;
+    const unsigned g = (unsigned)(ngroups < cap ? ngroups : cap);
+    // static rounds: about 3/4 of the groups, at least 1 (the first group)
+#ifndef VB_CLASS_STATIC_Q
+#define VB_CLASS_STATIC_Q 3
+#endif
+    const int rounds = (int)std::max<int64_t>(1, (ngroups / g) * VB_CLASS_STATIC_Q / 4);
+    kern<<<g, 32, 0, s>>>(ngroups, reinterpret_cast<const int4*>(groups), class_rows, coords, node_stride,
+                          comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K, M, ctr, bulk, rounds, facP,
+                          facR, cp);
+}
+
+vb_status class_entry(const char* fn, int dim, int64_t nn, const double* coords, int64_t node_stride,
+                      int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
+                      const int32_t* node_elem_ptr, const uint32_t* node_elem_slot, const int32_t* class_rows,
+                      const int32_t* groups, int64_t ngroups, double* K_vals, double* M_vals, const CoefSpec* coef,
+                      double* fac, vb_stream_t stream) {
     if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
     if (nn < 0 || nnz < 0 || ngroups < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
     if (!K_vals && !M_vals) return VB_OK;
@@ -1585,30 +1719,66 @@ extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* 
     if (!ctr) { set_error("%s: block counter unavailable", fn); return VB_ERR_CUDA; }
     // bulk (TMA) stores of contiguous groups need 16-byte aligned value arrays
     const bool bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
-    auto launch = [&](auto kern) {
-        static int occ[2] = {0, 0};
-        int& n = occ[dim - 2];
-        if (!n) {
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32, 0);
-            if (n < 1) n = 1;
-        }
-        const int64_t cap = (int64_t)sm_count() * n;
-        const unsigned g = (unsigned)(ngroups < cap ? ngroups : cap);
-        // static rounds: about 3/4 of the groups, at least 1 (the first group)
-#ifndef VB_CLASS_STATIC_Q
-#define VB_CLASS_STATIC_Q 3
-#endif
-        const int rounds = (int)std::max<int64_t>(1, (ngroups / g) * VB_CLASS_STATIC_Q / 4);
-        kern<<<g, 32, 0, s>>>(ngroups, reinterpret_cast<const int4*>(groups), class_rows, coords, node_stride,
-                              comp_stride, row_ptr, col_idx, node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr,
-                              bulk, rounds);
-    };
-    if (node_stride == 1) {
-        if (dim == 3) launch(assemble_class_k<3, true>);
-        else launch(assemble_class_k<2, true>);
-    } else {
-        if (dim == 3) launch(assemble_class_k<3, false>);
-        else launch(assemble_class_k<2, false>);
+    const CoefSpec c1{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
+    const double* fP = nullptr;
+    const double* fR = nullptr;
+    if (coef) {
+        fP = fac;
+        fR = fac + nn;
+        class_factors_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, coords, node_stride, comp_stride, coef->kb[0],
+                                                              coef->kb[1], coef->kb[2], fac, fac + nn);
+        vb_status st = launch_check(fn);
+        if (st != VB_OK) return st;
     }
+    const CoefSpec& cp = coef ? *coef : c1;
+#define VB_CLASS_LAUNCH(KERN)                                                                                      \
+    class_launch(KERN, s, ngroups, groups, class_rows, coords, node_stride, comp_stride, row_ptr, col_idx,          \
+                 node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr, bulk, fP, fR, cp)
+    if (coef) {
+        if (node_stride == 1) VB_CLASS_LAUNCH((assemble_class_k<3, true, true>));
+        else VB_CLASS_LAUNCH((assemble_class_k<3, false, true>));
+    } else if (node_stride == 1) {
+        if (dim == 3) VB_CLASS_LAUNCH((assemble_class_k<3, true>));
+        else VB_CLASS_LAUNCH((assemble_class_k<2, true>));
+    } else {
+        if (dim == 3) VB_CLASS_LAUNCH((assemble_class_k<3, false>));
+        else VB_CLASS_LAUNCH((assemble_class_k<2, false>));
+    }
+#undef VB_CLASS_LAUNCH
     return launch_check(fn);
+}
+
+}  // namespace
+}  // namespace vb
+
+extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                             int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx,
+                                             int64_t nnz, const int32_t* node_elem_ptr,
+                                             const uint32_t* node_elem_slot, const int32_t* class_rows,
+                                             const int32_t* groups, int64_t ngroups, double* K_vals,
+                                             double* M_vals, vb_stream_t stream) {
+    clear_error();
+    return class_entry("fem_p1_assemble_classes", dim, nn, coords, node_stride, comp_stride, row_ptr, col_idx, nnz,
+                       node_elem_ptr, node_elem_slot, class_rows, groups, ngroups, K_vals, M_vals, nullptr, nullptr,
+                       stream);
+}
+
+extern "C" vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const double* coords, int64_t node_stride,
+                                                  int64_t comp_stride, const int32_t* row_ptr,
+                                                  const int32_t* col_idx, int64_t nnz,
+                                                  const int32_t* node_elem_ptr, const uint32_t* node_elem_slot,
+                                                  const int32_t* class_rows, const int32_t* groups, int64_t ngroups,
+                                                  int gqo, double c_a, const double* c_b, double* work,
+                                                  double* K_vals, double* M_vals, vb_stream_t stream) {
+    const char* fn = "fem_p1_assemble_classes_coef";
+    clear_error();
+    if (dim != 3 || gqo != 2) {
+        set_error("%s: dim=%d gqo=%d: the class coefficient path is 3D with gqo = 2", fn, dim, gqo);
+        return VB_ERR_UNSUPPORTED;
+    }
+    if (nn > 0 && (K_vals || M_vals) && !work) { set_error("%s: NULL work (2 nn doubles)", fn); return VB_ERR_ARG; }
+    CoefSpec cp{c_a, {0, 0, 0}, c_a, {0, 0, 0}, 2, true};
+    for (int c = 0; c < 3; c++) cp.kb[c] = cp.mb[c] = c_b ? c_b[c] : 0.0;
+    return class_entry(fn, dim, nn, coords, node_stride, comp_stride, row_ptr, col_idx, nnz, node_elem_ptr,
+                       node_elem_slot, class_rows, groups, ngroups, K_vals, M_vals, &cp, work, stream);
 }

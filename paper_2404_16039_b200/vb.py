@@ -47,7 +47,7 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
-           "fem_p1_assemble_exact")
+           "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef")
 
 
 class VbError(RuntimeError):
@@ -94,6 +94,8 @@ def lib():
                                      C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_tiles": (i32, [i32, i64, p, i64, i64, i64, p, p, p, p, p, i32, i32, p, p, p]),
             "fem_p1_assemble_exact": (i32, [i32, i64, p, i64, i64, p, i64, p, p, p, p, p, p, p]),
+            "fem_p1_assemble_classes_coef": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, i32, d, p, p,
+                                                   p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -485,9 +487,12 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
 
 def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), cM=(1.0, (1.0, 1.0, 1.0)),
                          mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False, K=None, M=None,
-                         stream=None, compact=None):
+                         stream=None, compact=None, variant=None):
     """Coefficient-weighted K, M with c(x) = a * exp(b . x) (NEXT-1).  Returns
-    (K_vals, M_vals, K_local, M_local)."""
+    (K_vals, M_vals, K_local, M_local).  Gather mode, 3D, gqo = 2, c_K = c_M:
+    `variant` as _use_classes picks the row-class kernel
+    (fem_p1_assemble_classes_coef) or the 32-row blocks; other cases run the
+    blocks."""
     _f64(coords)
     dim, nn = coords.shape
     nv, ne = elems.shape
@@ -498,6 +503,24 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
     Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
     kb = (C.c_double * 3)(*[float(x) for x in list(cK[1])[:3]] + [0.0] * (3 - len(list(cK[1])[:3])))
     mb = (C.c_double * 3)(*[float(x) for x in list(cM[1])[:3]] + [0.0] * (3 - len(list(cM[1])[:3])))
+    same = float(cK[0]) == float(cM[0]) and list(kb) == list(mb)
+    if (mode == VB_ASSEMBLE_GATHER and dim == 3 and int(gqo) == 2 and same and (K is not None or M is not None)
+            and variant != "tile" and _use_classes(plan, variant)):
+        plan.classes()
+        if getattr(plan, "fac_work", None) is None or plan.fac_work.numel() < 2 * nn:
+            plan.fac_work = torch.empty((max(2 * nn, 2),), dtype=torch.float64, device=dev)
+        _check(lib().fem_p1_assemble_classes_coef(dim, nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr),
+                                                  _ptr(plan.col_idx), plan.nnz, _ptr(plan.node_elem_ptr),
+                                                  _ptr(plan.node_elem_slot), _ptr(plan.class_rows),
+                                                  _ptr(plan.groups), plan.groups.shape[0], 2, float(cK[0]),
+                                                  C.cast(kb, C.c_void_p), _ptr(plan.fac_work), _ptr(K), _ptr(M),
+                                                  _stream(stream)))
+        if want_local:
+            _check(lib().fem_p1_assemble_coef(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None,
+                                              plan.nnz, None, None, None, None, int(gqo), float(cK[0]),
+                                              C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), None,
+                                              None, _ptr(Kl), _ptr(Ml), int(mode), _stream(stream)))
+        return K, M, Kl, Ml
     gmode, words = _gather_mode(mode, plan, compact)
     _check(lib().fem_p1_assemble_coef(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                       _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),

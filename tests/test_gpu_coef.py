@@ -14,7 +14,10 @@ import synth
 from paper_2404_16039_b200 import vb
 
 pytestmark = pytest.mark.gpu
-MODES = [vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC]
+# (mode, gather variant): the row-class kernel (3D, gqo = 2, c_K = c_M; other cases
+# fall back to the blocks), the 32-row blocks, the atomic scatter
+MODES = [(vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"), (vb.VB_ASSEMBLE_ATOMIC, None)]
+MODE_IDS = ["class", "block", "atomic"]
 # 0: the paper's e^{x+y+z}; 1: c_K != c_M (exponentials at the points); 2: c_K == c_M
 # non-trivial (per-vertex factor path of the gather kernel for gqo = 2)
 COEFS = [((1.0, (1.0, 1.0, 1.0)), (1.0, (1.0, 1.0, 1.0))),
@@ -41,7 +44,7 @@ def relmax(got, ref):
     return np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)
 
 
-@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
 @pytest.mark.parametrize("gqo", [1, 2])
 @pytest.mark.parametrize("coef", [0, 1, 2])
 @pytest.mark.parametrize("kind", ["2d", "3d", "2d-crossed"])
@@ -58,7 +61,8 @@ def test_coef_assembly_parity(dev, kind, coef, gqo, mode):
     Ko, Mo = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=gqo, cK=cK, cM=cM)
     cd, ed = g(coords, dev), g(elems, dev)
     plan = vb.P1Plan(ed, nn)
-    K, M, Kl, Ml = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=gqo, cK=cK, cM=cM, mode=mode, want_local=True)
+    K, M, Kl, Ml = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=gqo, cK=cK, cM=cM, mode=mode[0], variant=mode[1],
+                                           want_local=True)
     assert relmax(h(K), Ko) <= 1e-12
     assert relmax(h(M), Mo) <= 1e-12
     # local matrices vs the oracle element routine on a few elements
@@ -109,3 +113,8 @@ def test_paper_tables_on_gpu(dev, golden, dim, level):
     rp, ci = h(plan.row_ptr), h(plan.col_idx)
     assert printed_close(abs(quad_form(rp, ci, h(K), v) - IK), row["e_K"])
     assert printed_close(abs(quad_form(rp, ci, h(M), v) - IM), row["e_M"])
+    if dim == 3:
+        # the default (row classes for these meshes) against the 32-row blocks on every entry
+        assert plan.class_coverage() >= 0.9
+        K2, M2, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, variant="block")
+        assert relmax(h(K), h(K2)) <= 1e-12 and relmax(h(M), h(M2)) <= 1e-12

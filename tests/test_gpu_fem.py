@@ -518,12 +518,12 @@ def test_gather_budgets_and_plan_stats(dev, kind):
         budgets = (False, True)
     out = []
     for compact in budgets:
-        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, compact=compact)
+        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, compact=compact, variant="block")
         K, M = h(K), h(M)
         assert relmax(K, Ko) <= 1e-12 and relmax(M, Mo) <= 1e-12
         out.append((K, M))
         cf = (1.3, (0.7, 0.2, -0.5))
-        Kc, Mc, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, compact=compact)
+        Kc, Mc, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, compact=compact, variant="block")
         Kco, Mco = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cf, cM=cf)
         assert relmax(h(Kc), Kco) <= 1e-12 and relmax(h(Mc), Mco) <= 1e-12
     for K, M in out[1:]:
