@@ -441,6 +441,18 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
             alg_bytes_assembly(3, cp_.shape[1], ep_.shape[1], pp.nnz),
             time_kernel(lambda: vb.fem_p1_assemble_coef(cdp, edp, pp, gqo=2, mode=mode, K=Kp, M=Mp, variant=gv), 10))
     del pp, Kp, Mp, cdp, edp
+    # NEXT-1 2D: Table tab:KM_P1_2D level 11 (crossed-diagonal square, 2^11, 8,392,705 nodes, c = e^{x+y}, gqo = 2)
+    cq_, eq_ = synth.square_crossed_p1(2 ** 11)
+    cdq, edq = torch.from_numpy(cq_).to(dev), torch.from_numpy(eq_).to(dev)
+    pq = vb.P1Plan(edq, cq_.shape[1], scatter_map=False)
+    Kq = torch.empty(pq.nnz, dtype=torch.float64, device=dev)
+    Mq = torch.empty(pq.nnz, dtype=torch.float64, device=dev)
+    for name, gv in (("class", "class"), ("block", "block")):
+        rec("NEXT-1 paper tab:KM_P1_2D level 11, c=exp(x+y), gqo=2, variant=%s (MATLAB timings in the paper, "
+            "hardware not stated)" % name, eq_.shape[1], "elements",
+            alg_bytes_assembly(2, cq_.shape[1], eq_.shape[1], pq.nnz),
+            time_kernel(lambda: vb.fem_p1_assemble_coef(cdq, edq, pq, gqo=2, K=Kq, M=Mq, variant=gv), 10))
+    del pq, Kq, Mq, cdq, edq
     # NEXT-3: P2, Table tab:KM_P2_3D level 6 (64^3 cells, 2,146,689 P2 nodes, c = e^{x+y+z}, gqo = 4);
     # paper: K 87.6 s + M 16.4 s, hardware not stated
     c2_, e2_ = synth.p2_from_p1(*synth.cube_kuhn_p1(64, jitter=0.0, flip=(0, 0, 1)))

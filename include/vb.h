@@ -211,13 +211,14 @@ VB_API vb_status fem_plan_pack_slots(int dim, int64_t n_inc, const uint32_t* nod
  * Outputs (DEVICE, caller-owned):
  *   class_rows (nn int32): all rows, grouped by class (ascending row id within
  *     a class); rows in classes of fewer than 8 rows, rows with more than 15
- *     (3D) / 8 (2D) entries or more than 32 (3D) / 16 (2D) incidences and rows
+ *     (3D) / 12 (2D) entries or more than 32 (3D) / 16 (2D) incidences and rows
  *     without incidences form the last,
  *     "mixed" class;
  *   groups (groups_cap x 4 int32): group g = (first position in class_rows,
  *     row count <= 32, first row of its class or -1 for the mixed class, 0).
- * stats_out (HOST, 3 int64): number of groups, number of classes (mixed
- * excluded), rows in classes.  work: DEVICE scratch; work == NULL queries its
+ * stats_out (HOST, 4 int64): number of groups, number of classes (mixed
+ * excluded), rows in classes, longest row in a class (the c = 1 kernel takes
+ * 2D classes of up to 8 entries and assembles longer ones like mixed rows).  work: DEVICE scratch; work == NULL queries its
  * size into *work_bytes.  VB_ERR_WORKSPACE if the groups do not fit groups_cap
  * (stats_out[0] then holds the count needed).  Deterministic; synchronises the
  * stream (one small read-back). */
@@ -380,12 +381,12 @@ VB_API vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne,
                           int mode, vb_stream_t stream);
 
 /* NEXT-1 through the row classes: fem_p1_assemble_classes with c_K = c_M =
- * c_a exp(c_b . x) (c_b: HOST array of 3 doubles, NULL = 0) and the gqo = 2
+ * c_a exp(c_b . x) (c_b: HOST array of dim doubles, NULL = 0) and the gqo = 2
  * rule of fem_p1_assemble_coef (Code stiff_scalar_P1 P:978-1004, the paper's
- * benchmark case P:1149-1176).  The coefficient at a quadrature point is formed
- * from per-node factors P = exp(beta c_b.x), R = exp((alpha - beta) c_b.x)
+ * benchmark case P:1149-1176; c_b: dim doubles).  The coefficient at a
+ * quadrature point is formed from per-node factors P = exp(beta c_b.x), R = exp((alpha - beta) c_b.x)
  * computed into work (DEVICE, 2 nn doubles, caller-owned) at the start of the
- * call.  dim = 3 and gqo = 2 only (VB_ERR_UNSUPPORTED otherwise: use
+ * call.  gqo = 2 only (VB_ERR_UNSUPPORTED otherwise: use
  * fem_p1_assemble_coef).  Other arguments and guarantees as
  * fem_p1_assemble_classes. */
 VB_API vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const double* coords, int64_t node_stride,

@@ -928,8 +928,11 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #endif
 template <int DIM, int NC = DIM>   // NC doubles staged per column slot: coordinates (+ P, R coefficient factors)
 struct ClassCfg {
-    static constexpr int MAXL = DIM == 3 ? 16 : 8;   // register accumulators per row (acc_slot)
-    static constexpr int FSLOTS = DIM == 3 ? 15 : 8; // columns per row (fem_plan_classes' maxl)
+    // 2D: 8 columns for c = 1 (square meshes: rows of <= 7), 12 with coefficients (the
+    // crossed-diagonal mesh of the paper's 2D tables: rows of 9); rows of a class longer
+    // than FSLOTS are assembled in place like the mixed rows
+    static constexpr int MAXL = DIM == 3 ? 16 : (NC > DIM ? 12 : 8);   // register accumulators per row
+    static constexpr int FSLOTS = DIM == 3 ? 15 : (NC > DIM ? 12 : 8); // columns per row (<= the plan's maxl)
     static constexpr int MAXN = DIM == 3 ? 32 : 16;  // incidences per row (fem_plan_classes' maxn)
     static constexpr int FN = FSLOTS * NC * 32;      // doubles of the edge-vector buffer
     static constexpr int MOFF = 32 * FSLOTS + 2;     // staging: K at [1, ..), M at [MOFF + 1, ..) (16-byte phase)
@@ -966,6 +969,30 @@ __device__ __forceinline__ void acc_slot(double (&aK)[16], double (&aM)[16], int
           VB_ACC_IN(14), VB_ACC_IN(15), VB_ACC_IM(0), VB_ACC_IM(1), VB_ACC_IM(2), VB_ACC_IM(3), VB_ACC_IM(4),
           VB_ACC_IM(5), VB_ACC_IM(6), VB_ACC_IM(7), VB_ACC_IM(8), VB_ACC_IM(9), VB_ACC_IM(10), VB_ACC_IM(11),
           VB_ACC_IM(12), VB_ACC_IM(13), VB_ACC_IM(14), VB_ACC_IM(15)
+        : "r"(s), "d"(k), "d"(m));
+}
+__device__ __forceinline__ void acc_slot(double (&aK)[12], double (&aM)[12], int s, double k, double m) {
+    asm(
+        "{\n\t"
+        "BT: .branchtargets L0, L1, L2, L3, L4, L5, L6, L7, L8, L9, L10, L11;\n\t"
+        "brx.idx.uni %24, BT;\n\t"
+        "L0: add.f64 %0, %0, %25; add.f64 %12, %12, %26; bra.uni END;\n\t"
+        "L1: add.f64 %1, %1, %25; add.f64 %13, %13, %26; bra.uni END;\n\t"
+        "L2: add.f64 %2, %2, %25; add.f64 %14, %14, %26; bra.uni END;\n\t"
+        "L3: add.f64 %3, %3, %25; add.f64 %15, %15, %26; bra.uni END;\n\t"
+        "L4: add.f64 %4, %4, %25; add.f64 %16, %16, %26; bra.uni END;\n\t"
+        "L5: add.f64 %5, %5, %25; add.f64 %17, %17, %26; bra.uni END;\n\t"
+        "L6: add.f64 %6, %6, %25; add.f64 %18, %18, %26; bra.uni END;\n\t"
+        "L7: add.f64 %7, %7, %25; add.f64 %19, %19, %26; bra.uni END;\n\t"
+        "L8: add.f64 %8, %8, %25; add.f64 %20, %20, %26; bra.uni END;\n\t"
+        "L9: add.f64 %9, %9, %25; add.f64 %21, %21, %26; bra.uni END;\n\t"
+        "L10: add.f64 %10, %10, %25; add.f64 %22, %22, %26; bra.uni END;\n\t"
+        "L11: add.f64 %11, %11, %25; add.f64 %23, %23, %26;\n\t"
+        "END: }\n"
+        : VB_ACC_IN(0), VB_ACC_IN(1), VB_ACC_IN(2), VB_ACC_IN(3), VB_ACC_IN(4), VB_ACC_IN(5), VB_ACC_IN(6),
+          VB_ACC_IN(7), VB_ACC_IN(8), VB_ACC_IN(9), VB_ACC_IN(10), VB_ACC_IN(11), VB_ACC_IM(0), VB_ACC_IM(1),
+          VB_ACC_IM(2), VB_ACC_IM(3), VB_ACC_IM(4), VB_ACC_IM(5), VB_ACC_IM(6), VB_ACC_IM(7), VB_ACC_IM(8),
+          VB_ACC_IM(9), VB_ACC_IM(10), VB_ACC_IM(11)
         : "r"(s), "d"(k), "d"(m));
 }
 __device__ __forceinline__ void acc_slot(double (&aK)[8], double (&aM)[8], int s, double k, double m) {
@@ -1048,6 +1075,9 @@ struct ClassGroup {
     int lo;               // row_ptr[v]
 };
 
+#ifndef VB_CLASS_WIDTH_CHECK
+#define VB_CLASS_WIDTH_CHECK 1   // 0: A/B timing only (unsafe for plans with 2D class rows of 9-12 entries)
+#endif
 #ifndef VB_CLASS_MINB
 #define VB_CLASS_MINB 16
 #endif
@@ -1068,7 +1098,6 @@ __global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_
                                                        double* __restrict__ M, unsigned int* __restrict__ ctr,
                                                        bool bulk, int rounds, const double* __restrict__ facP,
                                                        const double* __restrict__ facR, CoefSpec cp) {
-    static_assert(!COEF || DIM == 3, "the class coefficient path is 3D");
     constexpr int NC = COEF ? DIM + 2 : DIM;
     using C = ClassCfg<DIM, NC>;
     constexpr int MAXL = C::MAXL;
@@ -1111,6 +1140,9 @@ __global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_
             R.lo = __ldg(row_ptr + R.v);
         }
     };
+    // columns to prefetch for a group: its row length, capped at the buffer (longer classes
+    // are assembled in place and do not use the prefetched columns)
+    auto clampL = [](int l) { return (DIM == 2 && !COEF && l > C::FSLOTS) ? C::FSLOTS : l; };
     auto issue_cols = [&](const ClassGroup& R, int L) {   // columns of a class group -> colbuf
         if (t < R.cnt)
             for (int s = 0; s < L; s++) cp_async4(colbuf + s * 32 + t, col_idx + R.lo + s);
@@ -1123,11 +1155,16 @@ __global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_
         const int4 G0 = load_group(blockIdx.x);
         G1 = load_group(next_id());
         rows_of(G0, cur);
-        if (cur.head >= 0) issue_cols(cur, __ldg(row_ptr + cur.head + 1) - __ldg(row_ptr + cur.head));
+        if (cur.head >= 0) issue_cols(cur, clampL(__ldg(row_ptr + cur.head + 1) - __ldg(row_ptr + cur.head)));
     }
     int pat_head = -1, L = 0, n = 0, s0 = 0, nst = 0;   // nst: steps of the class's loop
     while (cur.head != -2) {
-        const bool fast = cur.head >= 0;
+        bool fast = cur.head >= 0;
+        // a class whose rows do not fit this kernel's column buffer (2D c = 1: the plan admits
+        // 12 columns, the buffer holds 8) is assembled in place like the mixed rows
+        if (VB_CLASS_WIDTH_CHECK && DIM == 2 && !COEF && fast && cur.head != pat_head &&
+            __ldg(row_ptr + cur.head + 1) - __ldg(row_ptr + cur.head) > C::FSLOTS)
+            fast = false;
         double xv[DIM], pvP = 0.0, pvR = 0.0;
         if (fast) {
             if (cur.head != pat_head) {   // class of this group: row length, incidences, decoded plan words
@@ -1184,7 +1221,8 @@ __global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_
         // next group: its rows now, its columns once this group's coordinates have landed
         rows_of(G1, nxt);
         G2 = load_group(next_id());
-        const int Ln = nxt.head >= 0 ? (nxt.head == pat_head ? L : __ldg(row_ptr + nxt.head + 1) - __ldg(row_ptr + nxt.head)) : 0;
+        const int Ln = clampL(
+            nxt.head >= 0 ? (nxt.head == pat_head ? L : __ldg(row_ptr + nxt.head + 1) - __ldg(row_ptr + nxt.head)) : 0);
         if (fast) {
             cp_async_wait<0>();
             __syncwarp();
@@ -1369,6 +1407,25 @@ __global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_
                 }
             } else {
                 int4 Pa = pat[0];
+                if constexpr (COEF && DIM == 2) {
+                    // 2D coefficient path, one triangle (v, a, b) per step (as the 3D pairs)
+                    constexpr double AL = QuadRule<2>::ALPHA, BE = QuadRule<2>::BETA, WQ = QuadRule<2>::W;
+                    constexpr double B2 = BE * BE, GA = AL * BE - BE * BE, KW = QuadRule<2>::DFACT * WQ;
+                    const double aPv = cp.ka * pvP, gRv = GA * pvR, dRv = (AL - BE) * pvR;
+                    for (int j = 0; j < n; j++) {
+                        const Inc o0 = inc(Pa);
+                        const double Pa1 = *reinterpret_cast<const double*>(Fb + Pa.x + DIM * 256);
+                        const double Ra1 = *reinterpret_cast<const double*>(Fb + Pa.x + (DIM + 1) * 256);
+                        const double Pb1 = *reinterpret_cast<const double*>(Fb + Pa.y + DIM * 256);
+                        const double Rb1 = *reinterpret_cast<const double*>(Fb + Pa.y + (DIM + 1) * 256);
+                        Pa = pat[j + 1 < n ? j + 1 : 0];
+                        const double p1 = aPv * Pa1 * Pb1, sR = (pvR + Ra1) + Rb1;
+                        const double kb1 = KW * p1 * sR, mw = o0.ad * WQ * p1, t1 = fma(B2, sR, gRv);
+                        acc_slot(aK, aM, o0.w & 0xff, kb1 * o0.k[0], mw * fma(GA, Ra1, t1));
+                        acc_slot(aK, aM, (o0.w >> 8) & 0xff, kb1 * o0.k[1], mw * fma(GA, Rb1, t1));
+                        mrow = fma(mw, fma(BE, sR, dRv), mrow);
+                    }
+                } else
                 for (int j = 0; j < n; j++) {
                     const Inc o0 = inc(Pa);
                     Pa = pat[j + 1 < n ? j + 1 : 0];
@@ -1432,6 +1489,9 @@ __global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_
             }
             __syncwarp();   // the staging area is the next group's edge-vector buffer
         } else {
+            // (a too-wide class's prefetched columns may still be landing in colbuf)
+            cp_async_wait<0>();
+            __syncwarp();
             if (nxt.head >= 0) issue_cols(nxt, Ln);
             if (t < cur.cnt) {
                 // mixed class: the lane's row in place in HBM
@@ -1668,13 +1728,15 @@ namespace vb {
 namespace {
 
 // per-node coefficient factors of the class coefficient path: P = exp(beta b.x), R = exp((alpha - beta) b.x)
+template <int DIM>
 __global__ void class_factors_k(int64_t nn, const double* __restrict__ coords, int64_t ns, int64_t cst, double b0,
                                 double b1, double b2, double* __restrict__ P, double* __restrict__ R) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
-        const double bx = fma(b0, coords[v * ns], fma(b1, coords[cst + v * ns], b2 * coords[2 * cst + v * ns]));
-        P[v] = exp(QuadRule<3>::BETA * bx);
-        R[v] = exp((QuadRule<3>::ALPHA - QuadRule<3>::BETA) * bx);
+        double bx = fma(b0, coords[v * ns], b1 * coords[cst + v * ns]);
+        if (DIM == 3) bx = fma(b0, coords[v * ns], fma(b1, coords[cst + v * ns], b2 * coords[2 * cst + v * ns]));
+        P[v] = exp(QuadRule<DIM>::BETA * bx);
+        R[v] = exp((QuadRule<DIM>::ALPHA - QuadRule<DIM>::BETA) * bx);
     }
 }
 
@@ -1684,10 +1746,21 @@ void class_launch(Kern kern, cudaStream_t s, int64_t ngroups, const int32_t* gro
                   const int32_t* col_idx, const int32_t* node_elem_ptr, const uint32_t* node_elem_slot, double* K,
                   double* M, unsigned int* ctr, bool bulk, const double* facP, const double* facR,
                   const CoefSpec& cp) {
-    static int n = 0;   // resident CTAs per SM of this instantiation
+    // resident CTAs per SM, cached per kernel (all instantiations share Kern's type)
+    static const void* keys[16] = {};
+    static int vals[16] = {};
+    int n = 0, slot = -1;
+    for (int i = 0; i < 16; i++) {
+        if (keys[i] == reinterpret_cast<const void*>(kern)) { n = vals[i]; break; }
+        if (!keys[i] && slot < 0) slot = i;
+    }
     if (!n) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 32, 0);
         if (n < 1) n = 1;
+        if (slot >= 0) {
+            vals[slot] = n;
+            keys[slot] = reinterpret_cast<const void*>(kern);
+        }
     }
     const int64_t cap = (int64_t)sm_count() * n;
     const unsigned g = (unsigned)(ngroups < cap ? ngroups : cap);
@@ -1725,8 +1798,9 @@ vb_status class_entry(const char* fn, int dim, int64_t nn, const double* coords,
     if (coef) {
         fP = fac;
         fR = fac + nn;
-        class_factors_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, coords, node_stride, comp_stride, coef->kb[0],
-                                                              coef->kb[1], coef->kb[2], fac, fac + nn);
+        auto fk = dim == 3 ? class_factors_k<3> : class_factors_k<2>;
+        fk<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, coords, node_stride, comp_stride, coef->kb[0], coef->kb[1],
+                                                coef->kb[2], fac, fac + nn);
         vb_status st = launch_check(fn);
         if (st != VB_OK) return st;
     }
@@ -1735,8 +1809,13 @@ vb_status class_entry(const char* fn, int dim, int64_t nn, const double* coords,
     class_launch(KERN, s, ngroups, groups, class_rows, coords, node_stride, comp_stride, row_ptr, col_idx,          \
                  node_elem_ptr, node_elem_slot, K_vals, M_vals, ctr, bulk, fP, fR, cp)
     if (coef) {
-        if (node_stride == 1) VB_CLASS_LAUNCH((assemble_class_k<3, true, true>));
-        else VB_CLASS_LAUNCH((assemble_class_k<3, false, true>));
+        if (node_stride == 1) {
+            if (dim == 3) VB_CLASS_LAUNCH((assemble_class_k<3, true, true>));
+            else VB_CLASS_LAUNCH((assemble_class_k<2, true, true>));
+        } else {
+            if (dim == 3) VB_CLASS_LAUNCH((assemble_class_k<3, false, true>));
+            else VB_CLASS_LAUNCH((assemble_class_k<2, false, true>));
+        }
     } else if (node_stride == 1) {
         if (dim == 3) VB_CLASS_LAUNCH((assemble_class_k<3, true>));
         else VB_CLASS_LAUNCH((assemble_class_k<2, true>));
@@ -1772,8 +1851,8 @@ extern "C" vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const dou
                                                   double* K_vals, double* M_vals, vb_stream_t stream) {
     const char* fn = "fem_p1_assemble_classes_coef";
     clear_error();
-    if (dim != 3 || gqo != 2) {
-        set_error("%s: dim=%d gqo=%d: the class coefficient path is 3D with gqo = 2", fn, dim, gqo);
+    if ((dim != 2 && dim != 3) || gqo != 2) {
+        set_error("%s: dim=%d gqo=%d: the class coefficient path needs gqo = 2", fn, dim, gqo);
         return VB_ERR_UNSUPPORTED;
     }
     if (nn > 0 && (K_vals || M_vals) && !work) { set_error("%s: NULL work (2 nn doubles)", fn); return VB_ERR_ARG; }

@@ -118,18 +118,26 @@ __global__ void cls_groups_k(int64_t nn, const uint64_t* __restrict__ skeys, con
     groups[g] = make_int4((int)i, cnt, skeys[i] == MIXED ? -1 : srows[roff[r]], 0);
 }
 
-// stats: [0] groups, [1] classes (runs with a class key), [2] rows in classes
+// stats: [0] groups, [1] classes (runs with a class key), [2] rows in classes,
+// [3] longest row in a class
 __global__ void cls_stats_k(const int* __restrict__ nruns_p, const uint64_t* __restrict__ ukeys,
                             const int32_t* __restrict__ rcnt, const int32_t* __restrict__ gofs,
-                            int64_t* __restrict__ out) {
+                            const int32_t* __restrict__ roff, const int32_t* __restrict__ srows,
+                            const int32_t* __restrict__ row_ptr, int64_t* __restrict__ out) {
     const int nr = *nruns_p;
     if (threadIdx.x == 0) {
         out[0] = gofs[nr];
         const bool mixed_last = nr > 0 && ukeys[nr - 1] == MIXED;
         out[1] = nr - (mixed_last ? 1 : 0);
-        int64_t rows = 0;
-        for (int r = 0; r < nr - (mixed_last ? 1 : 0); r++) rows += rcnt[r];
+        int64_t rows = 0, lmax = 0;
+        for (int r = 0; r < nr - (mixed_last ? 1 : 0); r++) {
+            rows += rcnt[r];
+            const int32_t v = srows[roff[r]];
+            const int64_t L = row_ptr[v + 1] - row_ptr[v];
+            lmax = L > lmax ? L : lmax;
+        }
         out[2] = rows;
+        out[3] = lmax;
     }
 }
 
@@ -217,13 +225,13 @@ extern "C" vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_pt
         return VB_ERR_ARG;
     }
     if (nn == 0) {
-        stats_out[0] = stats_out[1] = stats_out[2] = 0;
+        stats_out[0] = stats_out[1] = stats_out[2] = stats_out[3] = 0;
         return VB_OK;
     }
     cudaStream_t s = cs(stream);
     ClsWork W;
     cls_layout(n1, static_cast<char*>(work), &W);
-    const int maxl = dim == 3 ? 15 : 8;   // edge-vector buffer of assemble_class_k (columns per row)
+    const int maxl = dim == 3 ? 15 : 12;  // widest edge-vector buffer of assemble_class_k (columns per row)
     const int maxn = dim == 3 ? 32 : 16;  // its decoded plan-word table (incidences per row)
     const unsigned g = (unsigned)((nn + 255) / 256);
     vb_status st;
@@ -241,9 +249,9 @@ extern "C" vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_pt
     cls_groups_k<<<g, 256, 0, s>>>(nn, W.k2, class_rows, W.nruns, W.roff, W.cnt, W.gofs,
                                    reinterpret_cast<int4*>(groups), groups_cap);
     if ((st = launch_check(fn)) != VB_OK) return st;
-    cls_stats_k<<<1, 32, 0, s>>>(W.nruns, W.uk, W.cnt, W.gofs, W.stats);
+    cls_stats_k<<<1, 32, 0, s>>>(W.nruns, W.uk, W.cnt, W.gofs, W.roff, class_rows, row_ptr, W.stats);
     if ((st = launch_check(fn)) != VB_OK) return st;
-    if ((st = read_small(s, W.stats, 3 * sizeof(int64_t), stats_out, fn)) != VB_OK) return st;
+    if ((st = read_small(s, W.stats, 4 * sizeof(int64_t), stats_out, fn)) != VB_OK) return st;
     if (stats_out[0] > groups_cap) {
         set_error("%s: %lld groups, groups_cap %lld", fn, (long long)stats_out[0], (long long)groups_cap);
         return VB_ERR_WORKSPACE;

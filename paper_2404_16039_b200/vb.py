@@ -302,7 +302,7 @@ class P1Plan:
             L = lib()
             sz = C.c_size_t(0)
             st = _stream()
-            stats = (C.c_int64 * 3)()
+            stats = (C.c_int64 * 4)()
             _check(L.fem_plan_classes(self.dim, self.nn, None, None, None, None, C.byref(sz), None, None, 0, stats,
                                       st))
             work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
@@ -414,17 +414,20 @@ def fem_p1_assemble_exact(coords, elems, plan, want_K=True, want_M=True, stream=
     return K, M
 
 
-def _use_classes(plan, variant):
+def _use_classes(plan, variant, coef=False):
     """Gather variant: "class" (row classes, fem_p1_assemble_classes), "block"
     (32-row blocks, fem_p1_assemble) or None = "class" when at least 90 % of the
-    rows fall into row classes (meshes from uniform refinement), else "block"."""
+    rows fall into row classes (meshes from uniform refinement) that the kernel
+    keeps on chip (2D c = 1: rows of <= 8 entries), else "block"."""
     if variant not in (None, "class", "block", "tile"):
         raise ValueError("variant must be None, 'class', 'block' or 'tile'")
     if variant == "block" or plan.node_elem_ptr is None:
         return False
     if variant == "class":
         return True
-    return plan.class_coverage() >= 0.9
+    if plan.class_coverage() < 0.9:
+        return False
+    return coef or plan.dim == 3 or plan.class_stats[3] <= 8
 
 
 def fem_p1_assemble_classes(coords, plan, K=None, M=None, want_K=True, want_M=True, stream=None):
@@ -489,7 +492,7 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
                          mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False, K=None, M=None,
                          stream=None, compact=None, variant=None):
     """Coefficient-weighted K, M with c(x) = a * exp(b . x) (NEXT-1).  Returns
-    (K_vals, M_vals, K_local, M_local).  Gather mode, 3D, gqo = 2, c_K = c_M:
+    (K_vals, M_vals, K_local, M_local).  Gather mode, gqo = 2, c_K = c_M:
     `variant` as _use_classes picks the row-class kernel
     (fem_p1_assemble_classes_coef) or the 32-row blocks; other cases run the
     blocks."""
@@ -504,8 +507,8 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
     kb = (C.c_double * 3)(*[float(x) for x in list(cK[1])[:3]] + [0.0] * (3 - len(list(cK[1])[:3])))
     mb = (C.c_double * 3)(*[float(x) for x in list(cM[1])[:3]] + [0.0] * (3 - len(list(cM[1])[:3])))
     same = float(cK[0]) == float(cM[0]) and list(kb) == list(mb)
-    if (mode == VB_ASSEMBLE_GATHER and dim == 3 and int(gqo) == 2 and same and (K is not None or M is not None)
-            and variant != "tile" and _use_classes(plan, variant)):
+    if (mode == VB_ASSEMBLE_GATHER and int(gqo) == 2 and same and (K is not None or M is not None)
+            and variant != "tile" and _use_classes(plan, variant, coef=True)):
         plan.classes()
         if getattr(plan, "fac_work", None) is None or plan.fac_work.numel() < 2 * nn:
             plan.fac_work = torch.empty((max(2 * nn, 2),), dtype=torch.float64, device=dev)

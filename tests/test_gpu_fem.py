@@ -214,11 +214,29 @@ def test_tile_plan_refuses_long_rows(dev):
     assert not plan.tiles(g(coords, dev), g(elems, dev)) and "longer than 16" in plan.tile_reason
 
 
+def test_class_rows_wider_than_the_c1_kernel(dev):
+    """The crossed-diagonal square: its 9-entry vertex rows form classes (2D plan
+    budget 12) that the c = 1 class kernel (8 columns) assembles in place; the
+    auto choice then takes the blocks; both match the oracle."""
+    coords, elems = synth.square_crossed_p1(12)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    plan.classes()
+    assert plan.class_stats[3] == 9 and plan.class_coverage() >= 0.9
+    assert not vb._use_classes(plan, None) and vb._use_classes(plan, None, coef=True)
+    for variant in ("class", None):
+        K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, variant=variant)
+        assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+
+
 def signature(v, rp, nptr, nsl):
     return (int(rp[v + 1] - rp[v]), tuple(int(x) for x in nsl[nptr[v]:nptr[v + 1]]))
 
 
-@pytest.mark.parametrize("kind,n", [("2d", 9), ("3d", 1), ("3d", 7), ("3d", 10), ("delaunay3", 6)])
+@pytest.mark.parametrize("kind,n", [("2d", 9), ("3d", 1), ("3d", 7), ("3d", 10), ("delaunay3", 6), ("crossed", 12)])
 def test_row_classes_plan(dev, kind, n):
     """fem_plan_classes: class_rows is a permutation of the rows; every group is
     up to 32 rows of one class, all with the signature of the class's first
@@ -226,6 +244,8 @@ def test_row_classes_plan(dev, kind, n):
     mixed rows are the last groups; Kuhn cubes put >= 90 % of rows in classes."""
     if kind == "delaunay3":
         coords, elems = synth.delaunay_p1(3, n, seed=0)
+    elif kind == "crossed":
+        coords, elems = synth.square_crossed_p1(n)
     else:
         coords, elems = mesh(kind, n)
     nn = coords.shape[1]
@@ -239,17 +259,20 @@ def test_row_classes_plan(dev, kind, n):
     assert np.all((groups[:, 1] >= 1) & (groups[:, 1] <= 32))
     seen_mixed = False
     in_classes = 0
+    lmax = 0
     for pos, cnt, head, _ in groups:
         if head < 0:
             seen_mixed = True
             continue
         assert not seen_mixed                        # mixed rows come last
         ref = signature(head, rp, nptr, nsl)
-        assert ref[0] <= (15 if elems.shape[0] == 4 else 8)
+        assert ref[0] <= (15 if elems.shape[0] == 4 else 12)
+        lmax = max(lmax, ref[0])
         for v in rows[pos:pos + cnt]:
             assert signature(v, rp, nptr, nsl) == ref
         in_classes += cnt
     assert plan.class_stats[0] == len(groups) and plan.class_stats[2] == in_classes
+    assert plan.class_stats[3] == lmax
     if kind in ("2d", "3d") and n >= 9:
         assert plan.class_coverage() >= 0.9
 

@@ -1,4 +1,4 @@
-"""NEXT-1 (paper tab:KM_P1_3D level 7: c = e^{x+y+z}, gqo = 2) on the config-5-sized mesh: class vs block."""
+"""NEXT-1 (paper tab:KM_P1_3D level 7 / tab:KM_P1_2D level 11 with --dim 2: c = e^{sum x}, gqo = 2): class vs block."""
 import statistics
 import sys
 
@@ -25,7 +25,10 @@ def tm(fn, reps=10):
 
 
 dev = torch.device("cuda:0")
-c, e = synth.cube_kuhn_p1(128, jitter=0.0, flip=(0, 0, 1))
+if "--dim" in sys.argv and sys.argv[sys.argv.index("--dim") + 1] == "2":
+    c, e = synth.square_crossed_p1(2 ** 11)
+else:
+    c, e = synth.cube_kuhn_p1(128, jitter=0.0, flip=(0, 0, 1))
 cd, ed = torch.from_numpy(c).to(dev), torch.from_numpy(e).to(dev)
 plan = vb.P1Plan(ed, c.shape[1], scatter_map=False)
 plan.classes()
