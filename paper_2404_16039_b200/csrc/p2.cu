@@ -294,11 +294,20 @@ __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const doub
 // element order, row a of the staged K_e / M_e of each incidence (e, a) into
 // per-slot accumulators ([slot][lane] in shared memory, rows of up to P2_RS
 // entries; longer rows accumulate in place in HBM), then writes the row once.
-constexpr int P2_RS = 72;
+constexpr int P2_RS = 72;        // wide launch: rows of up to 72 entries on chip (longer: in place in HBM)
+constexpr int P2_RS_NARROW = 28; // narrow launch: blocks whose rows all have <= 28 entries (P2 edge-node rows)
 constexpr int P2_GROWS = 32;
 constexpr int P2_U = 4;
 
-template <int NLB>
+// RS: row capacity of the accumulators; LO: the launch takes the 32-row blocks whose
+// longest row is in (LO, RS] (narrow: LO = -1) or > LO (wide: LO = P2_RS_NARROW,
+// rows beyond RS in place).  Two launches cover every block once: most blocks of a
+// P2 mesh are edge-node rows (<= 27 entries on Kuhn cubes) and run with 2.5x the
+// resident warps of the vertex-row blocks (65 entries).
+#ifndef VB_P2_UN
+#define VB_P2_UN 4   // incidences in flight in the narrow launch (1 / 2 / 4: 2.96 / 2.87 / 2.70 ms, level 6)
+#endif
+template <int NLB, int RS, int LO, int U = P2_U>
 __global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_t* __restrict__ row_ptr,
                                                         const int32_t* __restrict__ nptr,
                                                         const int32_t* __restrict__ nelem,
@@ -306,7 +315,7 @@ __global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_
                                                         const double2* __restrict__ KMst,
                                                         double* __restrict__ K, double* __restrict__ M) {
     constexpr int NW = (NLB + 3) / 4;
-    constexpr int ST = P2_RS + 1;   // [lane][slot] rows of odd length: the cooperative write-back is conflict-free
+    constexpr int ST = RS + 1;   // [lane][slot] rows of odd length: the cooperative write-back is conflict-free
     __shared__ double2 acc_s[ST * P2_GROWS];
     const int t = threadIdx.x;
     double2* acc = acc_s + t * ST;
@@ -314,8 +323,10 @@ __global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_
         const int64_t v = v0 + t;
         const bool own = v < nn;
         const int lo = own ? __ldg(row_ptr + v) : 0, L = own ? __ldg(row_ptr + v + 1) - lo : 0;
+        const int bmax = __reduce_max_sync(0xffffffffu, L);
+        if (LO < 0 ? bmax > RS : bmax <= LO) continue;   // the other launch's block
         const int i0 = own ? __ldg(nptr + v) : 0, i1 = own ? __ldg(nptr + v + 1) : 0;
-        const bool fast = L <= P2_RS;
+        const bool fast = L <= RS;
         if (fast) {
             for (int s = 0; s < L; s++) acc[s] = make_double2(0.0, 0.0);
         } else {
@@ -341,14 +352,14 @@ __global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_
                 }
             }
         };
-        for (int i = i0; i < i1; i += P2_U) {
-            int32_t ea[P2_U];
+        for (int i = i0; i < i1; i += U) {
+            int32_t ea[U];
 #pragma unroll
-            for (int u = 0; u < P2_U; u++) ea[u] = i + u < i1 ? __ldg(nelem + i + u) : -1;
-            uint32_t w[P2_U][NW];
-            double2 km[P2_U][NLB];
+            for (int u = 0; u < U; u++) ea[u] = i + u < i1 ? __ldg(nelem + i + u) : -1;
+            uint32_t w[U][NW];
+            double2 km[U][NLB];
 #pragma unroll
-            for (int u = 0; u < P2_U; u++) {
+            for (int u = 0; u < U; u++) {
                 if (ea[u] < 0) continue;
                 const double2* row = KMst + (int64_t)(ea[u] >> 4) * (NLB * NLB) + (ea[u] & 15) * NLB;
 #pragma unroll
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_
                 for (int b = 0; b < NLB; b++) km[u][b] = __ldcs(row + b);
             }
 #pragma unroll
-            for (int u = 0; u < P2_U; u++)
+            for (int u = 0; u < U; u++)
                 if (ea[u] >= 0) add(w[u], km[u]);
         }
         // write-back: the warp stores each staged row in turn, lane j writing entry j
@@ -450,11 +461,21 @@ extern "C" vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne, const doub
     }
     if (gather && nn > 0) {
         const int64_t need = (nn + P2_GROWS - 1) / P2_GROWS;
-        const int64_t cap = (int64_t)sm_count() * 6;   // 37 KB of accumulators per warp-CTA
-        const unsigned g = (unsigned)(need < cap ? need : cap);
         const double2* km = reinterpret_cast<const double2*>(work);
-        if (dim == 2) p2_gather_k<6><<<g, P2_GROWS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem, node_elem_slot, km, K_vals, M_vals);
-        else p2_gather_k<10><<<g, P2_GROWS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem, node_elem_slot, km, K_vals, M_vals);
+        auto run = [&](auto kern) {
+            int occ = 1;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P2_GROWS, 0);
+            const int64_t cap = (int64_t)sm_count() * (occ > 0 ? occ : 1);
+            const unsigned g = (unsigned)(need < cap ? need : cap);
+            kern<<<g, P2_GROWS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem, node_elem_slot, km, K_vals, M_vals);
+        };
+        if (dim == 2) {
+            run(p2_gather_k<6, P2_RS_NARROW, -1, VB_P2_UN>);
+            run(p2_gather_k<6, P2_RS, P2_RS_NARROW>);
+        } else {
+            run(p2_gather_k<10, P2_RS_NARROW, -1, VB_P2_UN>);
+            run(p2_gather_k<10, P2_RS, P2_RS_NARROW>);
+        }
     }
     return launch_check(fn);
 }
