@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(TR, 3) assemble_tile_k(int64_t T, const int4* 
             parity ^= 1u;
         }
         __syncthreads();
+        VB_CHECK(ne_t <= ek && nloc <= xstride && ncol <= MAXC);
         for (int c = 0; c < ncol; c++) {
             const int i1 = cptr[c + 1];
             for (int i = cptr[c] + tid; i < i1; i += TR) {
@@ -448,6 +449,8 @@ __global__ void __launch_bounds__(TR, 3) assemble_tile_k(int64_t T, const int4* 
 #pragma unroll
                 for (int a = 0; a < NV; a++) l[a] = l4[a];
                 const uint64_t sb = (uint64_t)q.z | (uint64_t)q.w << 32;
+#pragma unroll
+                for (int a = 0; a < NV; a++) VB_CHECK(l[a] < nloc);
                 double k[NV][NV], ad;
                 if constexpr (DIM == 3) {
                     double f[3][3];
@@ -503,6 +506,7 @@ __global__ void __launch_bounds__(TR, 3) assemble_tile_k(int64_t T, const int4* 
                     for (int b = 0; b < NV; b++) {
                         if (b == a) continue;
                         adr[a][j] = (int)((sb >> (SB * a + 4 * j)) & 15) * TR + l[a];
+                        VB_CHECK(l[a] >= nown || (int)((sb >> (SB * a + 4 * j)) & 15) < (rinfo[l[a]].y & 0xff));
                         if (l[a] < nown) v[a][j] = acc[adr[a][j]];
                         j++;
                     }

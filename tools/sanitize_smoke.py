@@ -33,6 +33,10 @@ for dim, (c, e) in ((2, synth.square_p1(20)), (3, synth.cube_kuhn_p1(6)), (2, sy
     for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
         vb.fem_p1_assemble(cd, ed, plan, mode=mode, want_local=True)
         vb.fem_p1_assemble_coef(cd, ed, plan, mode=mode, gqo=2)
+    for variant in ("class", "block", "tile"):
+        vb.fem_p1_assemble(cd, ed, plan, variant=variant)
+        vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, variant=variant)
+    vb.fem_p1_assemble_exact(cd, ed, plan)
     lam, w = vb.vb_quad_rule(dim, 2)
     vb.fem_p1_rhs(cd, ed, torch.ones((len(w), e.shape[1]), dtype=torch.float64, device=dev), plan=plan)
     vb.vb_create_coords3D(cd, ed)
