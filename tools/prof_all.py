@@ -47,9 +47,22 @@ twice(lambda: vb.P1Plan(ed, c5.shape[1]))
 plan = vb.P1Plan(ed, c5.shape[1])
 K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
 M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
-for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
-    twice(lambda: vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M))
-    twice(lambda: vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, mode=mode, K=K, M=M))
+plan.classes()
+plan.tiles(cd, ed)
+for mode, variant in ((vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"),
+                      (vb.VB_ASSEMBLE_GATHER, "tile"), (vb.VB_ASSEMBLE_ATOMIC, None)):
+    twice(lambda: vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M, variant=variant))
+    if variant != "tile":
+        twice(lambda: vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, mode=mode, K=K, M=M, variant=variant))
+twice(lambda: vb.fem_p1_assemble_exact(cd, ed, plan))
+
+
+def tile_plan():
+    plan.tile_ok = None
+    plan.tiles(cd, ed)
+
+
+twice(tile_plan)
 twice(lambda: vb.vb_create_coords3D(cd, ed))
 fq = torch.ones((4, e5.shape[1]), dtype=torch.float64, device=dev)
 twice(lambda: vb.fem_p1_rhs(cd, ed, fq, plan=plan, gqo=2))
@@ -61,9 +74,17 @@ del plan, K, M, cd, ed, Kl, u, fq
 c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
 cd4, ed4 = torch.from_numpy(c4).to(dev), torch.from_numpy(e4).to(dev)
 p4 = vb.P1Plan(ed4, c4.shape[1])
-for mode in (vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC):
-    twice(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode))
+for mode, variant in ((vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"),
+                      (vb.VB_ASSEMBLE_GATHER, "tile"), (vb.VB_ASSEMBLE_ATOMIC, None)):
+    twice(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode, variant=variant))
 del p4, cd4, ed4
+# NEXT-1 2D: the crossed-diagonal square of tab:KM_P1_2D, level 11
+cq, eq = synth.square_crossed_p1(2 ** 11)
+cdq, edq = torch.from_numpy(cq).to(dev), torch.from_numpy(eq).to(dev)
+pq = vb.P1Plan(edq, cq.shape[1], scatter_map=False)
+for variant in ("class", "block"):
+    twice(lambda: vb.fem_p1_assemble_coef(cdq, edq, pq, gqo=2, variant=variant))
+del pq, cdq, edq
 
 c2, e2 = synth.p2_from_p1(*synth.cube_kuhn_p1(64, jitter=0.0, flip=(0, 0, 1)))
 cd2, ed2 = torch.from_numpy(c2).to(dev), torch.from_numpy(e2).to(dev)
