@@ -601,3 +601,14 @@ def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
                                         vb._ptr(plan.node_elem_slot), vb._ptr(plan.class_rows), vb._ptr(plan.groups),
                                         plan.groups.shape[0], vb._ptr(K), vb._ptr(M), None))
     assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
+    # the class coefficient path (its per-node factor pass reads the strided coordinates too)
+    cb = (C.c_double * 3)(0.7, -0.4, 0.9)
+    Kco, Mco = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=(1.3, (0.7, -0.4, 0.9)),
+                                       cM=(1.3, (0.7, -0.4, 0.9)))
+    work = torch.empty(2 * nn, dtype=torch.float64, device=dev)
+    vb._check(L.fem_p1_assemble_classes_coef(dim, nn, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(plan.row_ptr),
+                                             vb._ptr(plan.col_idx), plan.nnz, vb._ptr(plan.node_elem_ptr),
+                                             vb._ptr(plan.node_elem_slot), vb._ptr(plan.class_rows),
+                                             vb._ptr(plan.groups), plan.groups.shape[0], 2, 1.3, C.cast(cb, C.c_void_p),
+                                             vb._ptr(work), vb._ptr(K), vb._ptr(M), None))
+    assert relmax(h(K), Kco) <= 1e-12 and relmax(h(M), Mco) <= 1e-12
