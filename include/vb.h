@@ -357,6 +357,23 @@ VB_API vb_status fem_p1_assemble_exact(int dim, int64_t nn, const double* coords
                                        const int32_t* node_elem_ptr, const int32_t* node_elem, double* K_vals,
                                        double* M_vals, vb_stream_t stream);
 
+/* ---------------------------------------------------------- NEXT-4: GI
+ * Code GI, the Gauss integration of the paper's volume and
+ * surface integrals:
+ *   f_e(c) = sum_q w_q fip(c, q, e)                      (amsv(fip, w))
+ *   g_e = sum_c f_e(c) normals(c, e)  (normals given: a vector field against
+ *         outer normals), else g_e = f_e(0)               (d must be 1)
+ *   *value = sum_e sizes_e g_e
+ * fip: npages d x nip pages (SoA, entry (c, q) of page e at fip[(c + q d) ldf
+ * + e]); w: HOST array of nip weights (GI averages: they sum to 1 when sizes
+ * are element measures; reading B20); sizes: npages values; normals: d planes
+ * (plane stride ldn) or NULL; value: DEVICE scalar.  d in 1..4, nip in 1..16.
+ * work: DEVICE scratch, work == NULL queries its size.  The reduction has a
+ * fixed shape: bitwise reproducible.  VB_ERR_DIM for d != 1 without normals. */
+VB_API vb_status vb_gi(int64_t npages, int d, int nip, const double* fip, int64_t ldf, const double* w,
+                       const double* sizes, const double* normals, int64_t ldn, double* value, void* work,
+                       size_t* work_bytes, vb_stream_t stream);
+
 /* ---------------------------------------------------------- NEXT-1: coefficients
  * As fem_p1_assemble, with the coefficient functions of eq:K_M
  *   c_K(x) = cK_a * exp(cK_b . x),   c_M(x) = cM_a * exp(cM_b . x)

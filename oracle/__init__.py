@@ -56,6 +56,7 @@ def lib():
             "orc_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p]),
             "orc_pattern": (i64, [i32, i64, i64, p, i64, p, p]),
             "orc_p2_local_coef": (i32, [i32, p, i32, d, p, d, p, p, p]),
+            "orc_gi": (i32, [i64, i32, i32, p, i64, p, p, p, i64, p]),
             "orc_p2_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i32, d, p, d, p, p, p]),
         }
         for name, (res, args) in sig.items():
@@ -322,3 +323,16 @@ def p2_assemble_coef(coords, elems, row_ptr, col_idx, gqo=4, cK=(1.0, (1.0, 1.0,
     _check(lib().orc_p2_assemble_coef(dim, nn, ne, _p(coords), 1, nn, _p(elems), ne, _p(row_ptr), _p(col_idx),
                                       gqo, ka, _p(kb), ma, _p(mb), _p(K), _p(M)), "p2_assemble")
     return K, M
+
+
+def gi(fip, w, sizes, normals=None):
+    """Code GI: fip (nip, d, ne) page array (entry (c, q) of page e at
+    [q, c, e]), w (nip,), sizes (ne,), normals (d, ne) or None.  Returns the integral."""
+    fip = _f64(fip)
+    nip, d, ne = fip.shape
+    w, sizes = _f64(w), _f64(sizes)
+    nrm = _f64(normals) if normals is not None else None
+    out = np.empty(1)
+    _check(lib().orc_gi(ne, d, nip, _p(fip), ne, _p(w), _p(sizes), _p(nrm) if nrm is not None else None, ne,
+                        _p(out)), "gi")
+    return float(out[0])

@@ -727,3 +727,34 @@ int orc_p2_assemble_coef(int dim, int64_t nn, int64_t ne, const double* coords, 
     }
     return ORC_OK;
 }
+
+/* ------------------------------------------------- NEXT-4: GI */
+
+/* Code GI as written:
+ *   f_elems(e, c) = sum_q fip(c, q, e) w(q)             (amsv(fip, w), q ascending)
+ *   with normals:  g_e = sum_c f_elems(e, c) normals(e, c)   (c ascending)
+ *   without:       g_e = f_elems(e, 0)                  (d must be 1)
+ *   value = sum_e sizes(e) g_e                          (sum over e ascending, Neumaier-compensated)
+ * fip: d x nip pages, entry (c, q) of page e at fip[(c + q*d)*ld + e]; normals:
+ * d planes of ne (plane stride nld), NULL for a scalar integrand.
+ * Returns 0, or -1 for d != 1 without normals. */
+int orc_gi(int64_t ne, int d, int nip, const double* fip, int64_t ld, const double* w, const double* sizes,
+           const double* normals, int64_t nld, double* value) {
+    if (!normals && d != 1) return -1;
+    double s = 0.0, comp = 0.0;
+    for (int64_t e = 0; e < ne; e++) {
+        double g = 0.0;
+        for (int c = 0; c < d; c++) {
+            double f = 0.0;
+            for (int q = 0; q < nip; q++) f = f + at(fip, ld, d, c, q, e) * w[q];
+            g = normals ? g + f * normals[c * nld + e] : f;
+        }
+        double x = sizes[e] * g;
+        double t = s + x;
+        if (fabs(s) >= fabs(x)) comp += (s - t) + x;
+        else comp += (x - t) + s;
+        s = t;
+    }
+    *value = s + comp;
+    return ORC_OK;
+}

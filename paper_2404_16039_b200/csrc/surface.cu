@@ -71,10 +71,92 @@ __global__ void __launch_bounds__(1024) sum_parts_k(const double* __restrict__ p
     }
 }
 
+// NEXT-4: Code GI: value = sum_e sizes_e g_e with g_e = sum_c
+// f_e(c) normals_e(c) (or f_e(0)) and f_e(c) = sum_q w_q fip(c, q, e) (amsv).
+// One thread per page (grid-stride, streaming loads), the same fixed-shape
+// reduction as the surface volume (bitwise reproducible).
+constexpr int GI_MAXQ = 16;
+struct GIW {
+    double w[GI_MAXQ];
+};
+
+__global__ void __launch_bounds__(SURF_BLOCK) gi_k(int64_t ne, int d, int nip, const double* __restrict__ fip,
+                                                   int64_t ld, GIW w, const double* __restrict__ sizes,
+                                                   const double* __restrict__ normals, int64_t nld,
+                                                   double* __restrict__ part) {
+    double acc = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+        double g = 0.0;
+        for (int c = 0; c < d; c++) {
+            double f = 0.0;
+            for (int q = 0; q < nip; q++) f = fma(__ldcs(fip + (int64_t)(c + q * d) * ld + e), w.w[q], f);
+            g = normals ? fma(f, __ldcs(normals + c * nld + e), g) : f;
+        }
+        acc = fma(__ldcs(sizes + e), g, acc);
+    }
+    __shared__ double sh[SURF_BLOCK / 32];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = (threadIdx.x < SURF_BLOCK / 32) ? sh[threadIdx.x] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) part[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) gi_sum_k(const double* __restrict__ part, int n, double* __restrict__ out) {
+    __shared__ double sh[32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = sh[threadIdx.x];
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) *out = t;
+    }
+}
+
 }  // namespace
 }  // namespace vb
 
 using namespace vb;
+
+extern "C" vb_status vb_gi(int64_t npages, int d, int nip, const double* fip, int64_t ldf, const double* w,
+                           const double* sizes, const double* normals, int64_t ldn, double* value, void* work,
+                           size_t* work_bytes, vb_stream_t stream) {
+    const char* fn = "vb_gi";
+    clear_error();
+    if (npages < 0) { set_error("%s: negative npages", fn); return VB_ERR_ARG; }
+    if (d < 1 || d > 4) { set_error("%s: d=%d, need 1..4", fn, d); return VB_ERR_UNSUPPORTED; }
+    if (nip < 1 || nip > GI_MAXQ) { set_error("%s: nip=%d, need 1..%d", fn, nip, GI_MAXQ); return VB_ERR_UNSUPPORTED; }
+    if (!normals && d != 1) { set_error("%s: d=%d needs normals (a vector field is integrated against them)", fn, d); return VB_ERR_DIM; }
+    const unsigned g = grid_for(npages, SURF_BLOCK, SURF_BLOCKS_PER_SM);
+    const size_t need = ((size_t)g * sizeof(double) + 255) & ~(size_t)255;
+    if (!work) {
+        if (!work_bytes) { set_error("%s: work and work_bytes both NULL", fn); return VB_ERR_ARG; }
+        *work_bytes = need;
+        return VB_OK;
+    }
+    if (work_bytes && *work_bytes < need) { set_error("%s: work buffer too small (%zu < %zu)", fn, *work_bytes, need); return VB_ERR_WORKSPACE; }
+    if (!value || !w) { set_error("%s: NULL value or w", fn); return VB_ERR_ARG; }
+    if (npages > 0 && (!fip || !sizes)) { set_error("%s: NULL fip or sizes", fn); return VB_ERR_ARG; }
+    if (ldf < npages || (normals && ldn < npages)) { set_error("%s: leading dimension < npages", fn); return VB_ERR_ARG; }
+    auto s = cs(stream);
+    if (npages == 0) {
+        cudaMemsetAsync(value, 0, sizeof(double), s);
+        return launch_check(fn);
+    }
+    GIW ww{};
+    for (int q = 0; q < nip; q++) ww.w[q] = w[q];
+    double* part = reinterpret_cast<double*>(work);
+    gi_k<<<g, SURF_BLOCK, 0, s>>>(npages, d, nip, fip, ldf, ww, sizes, normals, ldn, part);
+    gi_sum_k<<<1, 1024, 0, s>>>(part, (int)g, value);
+    return launch_check(fn);
+}
 
 extern "C" vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, int64_t nverts, const double* xyz,
                                     int64_t node_stride, int64_t comp_stride, double* n, double* nhat, double* area,

@@ -47,7 +47,7 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
-           "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef")
+           "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi")
 
 
 class VbError(RuntimeError):
@@ -96,6 +96,7 @@ def lib():
             "fem_p1_assemble_exact": (i32, [i32, i64, p, i64, i64, p, i64, p, p, p, p, p, p, p]),
             "fem_p1_assemble_classes_coef": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, i32, d, p, p,
                                                    p, p, p]),
+            "vb_gi": (i32, [i64, i32, i32, p, i64, p, p, p, i64, p, p, sz, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -236,6 +237,26 @@ def vb_tri_surface(xyz, tri, want_n=True, want_nhat=True, want_area=True, want_v
                                 _stream(stream)))
     o["work"] = work
     return o
+
+
+def vb_gi(fip, w, sizes, normals=None, value=None, work=None, stream=None):
+    """Code GI: fip (nip, d, N) page array, w (nip,) host weights,
+    sizes (N,), normals (d, N) or None.  Returns (value (1,) device tensor, work)."""
+    _f64(fip)
+    nip, d, N = fip.shape
+    dev = fip.device
+    if value is None:
+        value = torch.empty((1,), dtype=torch.float64, device=dev)
+    wb = (C.c_double * nip)(*[float(x) for x in w])
+    sz = C.c_size_t(0)
+    _check(lib().vb_gi(N, d, nip, None, N, C.cast(wb, C.c_void_p), None, None, N, None, None, C.byref(sz),
+                       _stream(stream)))
+    if work is None or work.numel() < sz.value:
+        work = torch.empty((max(sz.value, 256),), dtype=torch.uint8, device=dev)
+    sz2 = C.c_size_t(work.numel())
+    _check(lib().vb_gi(N, d, nip, _ptr(fip), N, C.cast(wb, C.c_void_p), _ptr(sizes), _ptr(normals), N, _ptr(value),
+                       _ptr(work), C.byref(sz2), _stream(stream)))
+    return value, work
 
 
 # ------------------------------------------------------------------ FEM P1
