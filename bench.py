@@ -552,6 +552,21 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
         ne5 * (16 + 72 * 2 + 8) + nn5 * 24, time_kernel(volumes, 10))
     rec("NEXT-4 tet normals config5 (create_coords3D + page_inv + page_transpose + page_mtimes)", ne5, "elements",
         ne5 * (16 + 72 * 6 + 96) + nn5 * 24, time_kernel(normals, 5))
+    # NEXT-4 GI (Code GI P:838-847): the volume integral of rho = x1^2 + x2^2 over the config-5 mesh with the
+    # degree-2 rule, GI alone on resident fip (4 points) and sizes: 40 B per tet
+    import numpy as np
+    lam, wq = vb.vb_quad_rule(3, 2)
+    ip = torch.from_numpy(np.ascontiguousarray(np.asarray(lam, dtype=np.float64).reshape(len(wq), 4)[:, :, None])).to(dev)
+    c3, v3 = vb.vb_create_coords3D(cd5, ed5)
+    Xip = vb.vb_page_mtimes(c3, ip)
+    sizes = vb.vb_page_det(v3).abs_() / 6.0
+    fip = (Xip[:, 0] ** 2 + Xip[:, 1] ** 2).unsqueeze(1).contiguous()
+    del c3, v3, Xip
+    gval, gwork = vb.vb_gi(fip, np.asarray(wq) * 6.0, sizes)
+    rec("NEXT-4 GI volume integral config5 (rho = x1^2 + x2^2, 4 points; value %.15f, exact 2/3)" % gval.item(),
+        ne5, "elements", ne5 * 40, time_kernel(lambda: vb.vb_gi(fip, np.asarray(wq) * 6.0, sizes, value=gval,
+                                                                work=gwork), 10, flush))
+    del fip, sizes
     return res
 
 

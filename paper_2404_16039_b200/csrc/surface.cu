@@ -133,14 +133,14 @@ extern "C" vb_status vb_gi(int64_t npages, int d, int nip, const double* fip, in
     if (npages < 0) { set_error("%s: negative npages", fn); return VB_ERR_ARG; }
     if (d < 1 || d > 4) { set_error("%s: d=%d, need 1..4", fn, d); return VB_ERR_UNSUPPORTED; }
     if (nip < 1 || nip > GI_MAXQ) { set_error("%s: nip=%d, need 1..%d", fn, nip, GI_MAXQ); return VB_ERR_UNSUPPORTED; }
-    if (!normals && d != 1) { set_error("%s: d=%d needs normals (a vector field is integrated against them)", fn, d); return VB_ERR_DIM; }
     const unsigned g = grid_for(npages, SURF_BLOCK, SURF_BLOCKS_PER_SM);
     const size_t need = ((size_t)g * sizeof(double) + 255) & ~(size_t)255;
-    if (!work) {
+    if (!work) {   // size query: needs only npages
         if (!work_bytes) { set_error("%s: work and work_bytes both NULL", fn); return VB_ERR_ARG; }
         *work_bytes = need;
         return VB_OK;
     }
+    if (!normals && d != 1) { set_error("%s: d=%d needs normals (a vector field is integrated against them)", fn, d); return VB_ERR_DIM; }
     if (work_bytes && *work_bytes < need) { set_error("%s: work buffer too small (%zu < %zu)", fn, *work_bytes, need); return VB_ERR_WORKSPACE; }
     if (!value || !w) { set_error("%s: NULL value or w", fn); return VB_ERR_ARG; }
     if (npages > 0 && (!fip || !sizes)) { set_error("%s: NULL fip or sizes", fn); return VB_ERR_ARG; }
