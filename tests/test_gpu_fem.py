@@ -612,3 +612,29 @@ def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
                                              vb._ptr(plan.groups), plan.groups.shape[0], 2, 1.3, C.cast(cb, C.c_void_p),
                                              vb._ptr(work), vb._ptr(K), vb._ptr(M), None))
     assert relmax(h(K), Kco) <= 1e-12 and relmax(h(M), Mco) <= 1e-12
+
+
+@pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)
+@pytest.mark.parametrize("kind", ["2d", "3d"])
+def test_k_only_and_m_only(dev, kind, mode):
+    """One matrix requested (the other pointer NULL) through every variant, c = 1
+    and, in gather mode, the coefficient path (row classes where they apply)."""
+    coords, elems = mesh(kind, 7, seed=5)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    cf = (1.1, (0.3, -0.6, 0.5))
+    Kc, Mc = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=cf, cM=cf)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, nn)
+    K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1], want_M=False)
+    assert M is None and relmax(h(K), Ko) <= 1e-12
+    K, M, _, _ = vb.fem_p1_assemble(cd, ed, plan, mode=mode[0], variant=mode[1], want_K=False)
+    assert K is None and relmax(h(M), Mo) <= 1e-12
+    if mode[1] != "tile":
+        K, M, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, mode=mode[0], variant=mode[1],
+                                             want_M=False)
+        assert M is None and relmax(h(K), Kc) <= 1e-12
+        K, M, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, mode=mode[0], variant=mode[1],
+                                             want_K=False)
+        assert K is None and relmax(h(M), Mc) <= 1e-12
