@@ -1078,6 +1078,12 @@ struct ClassGroup {
 #ifndef VB_CLASS_WIDTH_CHECK
 #define VB_CLASS_WIDTH_CHECK 1   // 0: A/B timing only (unsafe for plans with 2D class rows of 9-12 entries)
 #endif
+#ifndef VB_CLASS_MINB2
+#define VB_CLASS_MINB2 32   // 2D c = 1 kernel: 64 registers, 32 warps/SM (16 / 24 / 32: 0.204 / 0.184 / 0.165 ms, config 4)
+#endif
+#ifndef VB_CLASS_MINBC2
+#define VB_CLASS_MINBC2 16  // 2D coefficient kernel (10 / 16 / 20: 0.704 / 0.637 / 0.723 ms, tab:KM_P1_2D L11)
+#endif
 #ifndef VB_CLASS_MINB
 #define VB_CLASS_MINB 16
 #endif
@@ -1088,7 +1094,8 @@ struct ClassGroup {
 // c = 1 K_e times kbar = d! w sum_q c_q, M_e[v][x] = |det| w sum_q c_q
 // lam_v(q) lam_x(q), and M_vv = row sum - off-diagonals.
 template <int DIM, bool NS1, bool COEF = false>   // NS1: node_stride == 1 (SoA coordinate planes)
-__global__ void __launch_bounds__(32, COEF ? 10 : VB_CLASS_MINB) assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
+__global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) : (DIM == 2 ? VB_CLASS_MINB2 : VB_CLASS_MINB))
+    assemble_class_k(int64_t ngroups, const int4* __restrict__ groups,
                                                        const int32_t* __restrict__ class_rows,
                                                        const double* __restrict__ coords, int64_t ns, int64_t cst,
                                                        const int32_t* __restrict__ row_ptr,
