@@ -80,20 +80,46 @@ struct GIW {
     double w[GI_MAXQ];
 };
 
+// D, Q > 0: compile-time shape (every load of a page issued before the arithmetic);
+// 0: runtime d / nip
+template <int D, int Q>
 __global__ void __launch_bounds__(SURF_BLOCK) gi_k(int64_t ne, int d, int nip, const double* __restrict__ fip,
                                                    int64_t ld, GIW w, const double* __restrict__ sizes,
                                                    const double* __restrict__ normals, int64_t nld,
                                                    double* __restrict__ part) {
     double acc = 0.0;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
-        double g = 0.0;
-        for (int c = 0; c < d; c++) {
-            double f = 0.0;
-            for (int q = 0; q < nip; q++) f = fma(__ldcs(fip + (int64_t)(c + q * d) * ld + e), w.w[q], f);
-            g = normals ? fma(f, __ldcs(normals + c * nld + e), g) : f;
+    if constexpr (D > 0 && Q > 0) {
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+            double v[D][Q], nv[D];
+#pragma unroll
+            for (int c = 0; c < D; c++)
+#pragma unroll
+                for (int q = 0; q < Q; q++) v[c][q] = __ldcs(fip + (int64_t)(c + q * D) * ld + e);
+            if (normals)
+#pragma unroll
+                for (int c = 0; c < D; c++) nv[c] = __ldcs(normals + c * nld + e);
+            const double sz = __ldcs(sizes + e);
+            double g = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; c++) {
+                double f = 0.0;
+#pragma unroll
+                for (int q = 0; q < Q; q++) f = fma(v[c][q], w.w[q], f);
+                g = normals ? fma(f, nv[c], g) : f;
+            }
+            acc = fma(sz, g, acc);
         }
-        acc = fma(__ldcs(sizes + e), g, acc);
+    } else {
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+            double g = 0.0;
+            for (int c = 0; c < d; c++) {
+                double f = 0.0;
+                for (int q = 0; q < nip; q++) f = fma(__ldcs(fip + (int64_t)(c + q * d) * ld + e), w.w[q], f);
+                g = normals ? fma(f, __ldcs(normals + c * nld + e), g) : f;
+            }
+            acc = fma(__ldcs(sizes + e), g, acc);
+        }
     }
     __shared__ double sh[SURF_BLOCK / 32];
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -153,7 +179,13 @@ extern "C" vb_status vb_gi(int64_t npages, int d, int nip, const double* fip, in
     GIW ww{};
     for (int q = 0; q < nip; q++) ww.w[q] = w[q];
     double* part = reinterpret_cast<double*>(work);
-    gi_k<<<g, SURF_BLOCK, 0, s>>>(npages, d, nip, fip, ldf, ww, sizes, normals, ldn, part);
+    auto k = gi_k<0, 0>;   // the shapes of the paper's integrals: scalar densities at 1 / 3 / 4 points, fields at 1
+    if (d == 1 && nip == 1) k = gi_k<1, 1>;
+    else if (d == 1 && nip == 3) k = gi_k<1, 3>;
+    else if (d == 1 && nip == 4) k = gi_k<1, 4>;
+    else if (d == 3 && nip == 1) k = gi_k<3, 1>;
+    else if (d == 2 && nip == 1) k = gi_k<2, 1>;
+    k<<<g, SURF_BLOCK, 0, s>>>(npages, d, nip, fip, ldf, ww, sizes, normals, ldn, part);
     gi_sum_k<<<1, 1024, 0, s>>>(part, (int)g, value);
     return launch_check(fn);
 }
