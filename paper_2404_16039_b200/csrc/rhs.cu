@@ -38,13 +38,16 @@ bool make_rule(int dim, int gqo, Rule& R) {
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(256) rhs_elem_k(int64_t ne, const double* __restrict__ coords, int64_t ns, int64_t cst,
-                                                  const int32_t* __restrict__ elems, int64_t eld,
-                                                  const double* __restrict__ fq, const Rule R, double* __restrict__ b2D,
-                                                  double* __restrict__ b) {
+__device__ __forceinline__ void rhs_elem(int64_t e, int64_t ne, const double* __restrict__ coords, int64_t ns,
+                                         int64_t cst, const int32_t* __restrict__ elems, int64_t eld,
+                                         const double* __restrict__ fq, const Rule& R, double* __restrict__ b2D,
+                                         double* __restrict__ b) {
     constexpr int NV = DIM + 1;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+    {
+        // the streamed f values first: in flight while the vertex gather (elems -> coords) runs
+        double fv[NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) fv[i] = i < R.nip ? __ldcs(fq + (int64_t)i * ne + e) : 0.0;
         int32_t vid[NV];
         double x[NV][DIM];
 #pragma unroll
@@ -70,8 +73,10 @@ __global__ void __launch_bounds__(256) rhs_elem_k(int64_t ne, const double* __re
         double loc[NV];
 #pragma unroll
         for (int a = 0; a < NV; a++) loc[a] = 0.0;
-        for (int i = 0; i < R.nip; i++) {
-            const double fw = R.w[i] * ad * __ldcs(fq + (int64_t)i * ne + e);
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            if (i >= R.nip) break;
+            const double fw = R.w[i] * ad * fv[i];
 #pragma unroll
             for (int a = 0; a < NV; a++) loc[a] = fma(fw, R.lam[i][a], loc[a]);
         }
@@ -80,6 +85,19 @@ __global__ void __launch_bounds__(256) rhs_elem_k(int64_t ne, const double* __re
             if (b2D) stcs(b2D + (int64_t)a * ne + e, loc[a]);
             if (b) atomicAdd(b + vid[a], loc[a]);
         }
+    }
+}
+
+// two elements per thread and step: both elements' loads in flight together
+template <int DIM>
+__global__ void __launch_bounds__(256) rhs_elem_k(int64_t ne, const double* __restrict__ coords, int64_t ns, int64_t cst,
+                                                  const int32_t* __restrict__ elems, int64_t eld,
+                                                  const double* __restrict__ fq, const Rule R, double* __restrict__ b2D,
+                                                  double* __restrict__ b) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += 2 * stride) {
+        rhs_elem<DIM>(e, ne, coords, ns, cst, elems, eld, fq, R, b2D, b);
+        if (e + stride < ne) rhs_elem<DIM>(e + stride, ne, coords, ns, cst, elems, eld, fq, R, b2D, b);
     }
 }
 
