@@ -926,6 +926,9 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #ifndef VB_CLASS_PAIRS
 #define VB_CLASS_PAIRS 1   // 3D: incidences paired over shared link edges (build_pairs)
 #endif
+#ifndef VB_CLASS_SKIP_DIAG
+#define VB_CLASS_SKIP_DIAG 1
+#endif
 template <int DIM, int NC = DIM>   // NC doubles staged per column slot: coordinates (+ P, R coefficient factors)
 struct ClassCfg {
     // 2D: 8 columns for c = 1 (square meshes: rows of <= 7), 12 with coefficients (the
@@ -934,8 +937,12 @@ struct ClassCfg {
     static constexpr int MAXL = DIM == 3 ? 16 : (NC > DIM ? 12 : 8);   // register accumulators per row
     static constexpr int FSLOTS = DIM == 3 ? 15 : (NC > DIM ? 12 : 8); // columns per row (<= the plan's maxl)
     static constexpr int MAXN = DIM == 3 ? 32 : 16;  // incidences per row (fem_plan_classes' maxn)
-    static constexpr int FN = FSLOTS * NC * 32;      // doubles of the edge-vector buffer
+    // the diagonal column is the row's own vertex: its coordinates are never read from the
+    // buffer (VB_CLASS_SKIP_DIAG: the buffer holds FSLOTS - 1 slots, slot s > s0 at s - 1)
+    static constexpr bool SKIPD = VB_CLASS_SKIP_DIAG && DIM == 3 && NC == DIM;   // 3D c = 1 only (measured)
+    static constexpr int FSTAGED = SKIPD ? FSLOTS - 1 : FSLOTS;
     static constexpr int MOFF = 32 * FSLOTS + 2;     // staging: K at [1, ..), M at [MOFF + 1, ..) (16-byte phase)
+    static constexpr int FN = FSTAGED * NC * 32 > 2 * MOFF ? FSTAGED * NC * 32 : 2 * MOFF;   // doubles of the buffer
     static constexpr int SLOT_BYTES = NC * 32 * 8;   // stride of one slot in the edge-vector buffer
 };
 
@@ -1035,7 +1042,8 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src) {
 // d << 12 | CLASS_PAIR (slots < 16).  Reads and rewrites pat in place (step k
 // is written after incidence k has been read; pairs only look ahead).
 constexpr int CLASS_PAIR = 1 << 16;
-__device__ int build_pairs(int4* pat, int n, int slot_bytes) {
+__device__ __forceinline__ int staged_slot(int s, int s0, bool skip) { return skip ? s - (s > s0) : s; }
+__device__ int build_pairs(int4* pat, int n, int slot_bytes, int s0, bool skip) {
     uint32_t used = 0;
     int k = 0;
     for (int i = 0; i < n; i++) {
@@ -1063,7 +1071,8 @@ __device__ int build_pairs(int4* pat, int n, int slot_bytes) {
             step = a | b << 4 | c << 8 | d << 12 | CLASS_PAIR;
             break;
         }
-        pat[k++] = make_int4(a * slot_bytes, b * slot_bytes, c * slot_bytes, step);
+        pat[k++] = make_int4(staged_slot(a, s0, skip) * slot_bytes, staged_slot(b, s0, skip) * slot_bytes,
+                             staged_slot(c, s0, skip) * slot_bytes, step);
     }
     return k;
 }
@@ -1075,6 +1084,9 @@ struct ClassGroup {
     int lo;               // row_ptr[v]
 };
 
+#ifndef VB_CLASS_SKIP_DIAG
+#define VB_CLASS_SKIP_DIAG 1
+#endif
 #ifndef VB_CLASS_WIDTH_CHECK
 #define VB_CLASS_WIDTH_CHECK 1   // 0: A/B timing only (unsafe for plans with 2D class rows of 9-12 entries)
 #endif
@@ -1184,13 +1196,15 @@ __global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) :
                 for (int j = t; j < n; j += 32) {
                     const uint32_t w = __ldg(nslot + ih + j);
                     const int a = (w >> 8) & 0xff, b = (w >> 16) & 0xff, c = w >> 24;
-                    pat[j] = make_int4(a * C::SLOT_BYTES, b * C::SLOT_BYTES, DIM == 3 ? c * C::SLOT_BYTES : 0,
+                    pat[j] = make_int4(staged_slot(a, s0, C::SKIPD) * C::SLOT_BYTES,
+                                       staged_slot(b, s0, C::SKIPD) * C::SLOT_BYTES,
+                                       DIM == 3 ? staged_slot(c, s0, C::SKIPD) * C::SLOT_BYTES : 0,
                                        a | b << 8 | (DIM == 3 ? c : 0) << 16);
                 }
                 if constexpr (DIM == 3 && VB_CLASS_PAIRS) {
                     __syncwarp();
                     int k = 0;
-                    if (t == 0) k = build_pairs(pat, n, C::SLOT_BYTES);
+                    if (t == 0) k = build_pairs(pat, n, C::SLOT_BYTES, s0, C::SKIPD);
                     nst = __shfl_sync(FULL, k, 0);
                     __syncwarp();
                 } else {
@@ -1204,13 +1218,15 @@ __global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) :
             __syncwarp();
             if (t < cur.cnt) {
                 for (int s = 0; s < L; s++) {
+                    if (C::SKIPD && s == s0) continue;   // the row's own vertex (xv)
                     const int w = colbuf[s * 32 + t];
+                    const int sf = staged_slot(s, s0, C::SKIPD);
 #pragma unroll
                     for (int c = 0; c < DIM; c++)
-                        cp_async8(F + (s * NC + c) * 32 + t, NS1 ? X[c] + w : X[c] + (int64_t)w * ns);
+                        cp_async8(F + (sf * NC + c) * 32 + t, NS1 ? X[c] + w : X[c] + (int64_t)w * ns);
                     if constexpr (COEF) {
-                        cp_async8(F + (s * NC + DIM) * 32 + t, facP + w);
-                        cp_async8(F + (s * NC + DIM + 1) * 32 + t, facR + w);
+                        cp_async8(F + (sf * NC + DIM) * 32 + t, facP + w);
+                        cp_async8(F + (sf * NC + DIM + 1) * 32 + t, facR + w);
                     }
                 }
 #pragma unroll
@@ -1340,7 +1356,7 @@ __global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) :
                         if (w & CLASS_PAIR) {
                             // element (v, a, b, d)
                             double fd[3], Pd, Rd;
-                            const int od = ((w >> 12) & 15) * C::SLOT_BYTES;
+                            const int od = staged_slot((w >> 12) & 15, s0, C::SKIPD) * C::SLOT_BYTES;
                             ld(od, fd);
                             lf(od, Pd, Rd);
                             cross(fb, fd, ha);
@@ -1391,7 +1407,7 @@ __global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) :
                     if (w & CLASS_PAIR) {
                         // triangle (a, b, d): h_a = fb x fd, h_b = fd x fa, h_d = P
                         double fd[3];
-                        ld(((w >> 12) & 15) * C::SLOT_BYTES, fd);
+                        ld(staged_slot((w >> 12) & 15, s0, C::SKIPD) * C::SLOT_BYTES, fd);
                         cross(fb, fd, ha);
                         cross(fd, fa, hb);
                         const double ad2 = fabs(dot(fd, P));
