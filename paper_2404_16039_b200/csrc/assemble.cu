@@ -929,6 +929,9 @@ __global__ void __launch_bounds__(GATHER_ROWS) assemble_gather_k(int64_t nn, con
 #ifndef VB_CLASS_SKIP_DIAG
 #define VB_CLASS_SKIP_DIAG 1
 #endif
+#ifndef VB_CLASS_SKIP_DIAG_C2
+#define VB_CLASS_SKIP_DIAG_C2 1   // the 2D coefficient kernel too: 16 instead of 15 CTAs/SM (0.629 -> 0.614 ms, tab:KM_P1_2D L11)
+#endif
 template <int DIM, int NC = DIM>   // NC doubles staged per column slot: coordinates (+ P, R coefficient factors)
 struct ClassCfg {
     // 2D: 8 columns for c = 1 (square meshes: rows of <= 7), 12 with coefficients (the
@@ -939,7 +942,8 @@ struct ClassCfg {
     static constexpr int MAXN = DIM == 3 ? 32 : 16;  // incidences per row (fem_plan_classes' maxn)
     // the diagonal column is the row's own vertex: its coordinates are never read from the
     // buffer (VB_CLASS_SKIP_DIAG: the buffer holds FSLOTS - 1 slots, slot s > s0 at s - 1)
-    static constexpr bool SKIPD = VB_CLASS_SKIP_DIAG && DIM == 3 && NC == DIM;   // 3D c = 1 only (measured)
+    static constexpr bool SKIPD =
+        VB_CLASS_SKIP_DIAG && ((DIM == 3 && NC == DIM) || (VB_CLASS_SKIP_DIAG_C2 && DIM == 2 && NC > DIM));
     static constexpr int FSTAGED = SKIPD ? FSLOTS - 1 : FSLOTS;
     static constexpr int MOFF = 32 * FSLOTS + 2;     // staging: K at [1, ..), M at [MOFF + 1, ..) (16-byte phase)
     static constexpr int FN = FSTAGED * NC * 32 > 2 * MOFF ? FSTAGED * NC * 32 : 2 * MOFF;   // doubles of the buffer
