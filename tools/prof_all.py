@@ -69,6 +69,15 @@ twice(lambda: vb.fem_p1_rhs(cd, ed, fq, plan=plan, gqo=2))
 Kl = torch.from_numpy(synth.normal_pages(4, 4, e5.shape[1], stream=10)).to(dev)
 u = torch.from_numpy(synth.normal_pages(4, 1, e5.shape[1], stream=11)).to(dev)
 twice(lambda: vb.vb_page_bilinear(u, Kl, u))
+# NEXT-4 GI: the volume integral of rho = x1^2 + x2^2 (4 points) on the config-5 mesh
+lam, wq = vb.vb_quad_rule(3, 2)
+c3, v3 = vb.vb_create_coords3D(cd, ed)
+Xip = vb.vb_page_mtimes(c3, torch.from_numpy(lam.reshape(len(wq), 4, 1).copy()).to(dev))
+gsz = vb.vb_page_det(v3).abs_() / 6.0
+gfip = (Xip[:, 0] ** 2 + Xip[:, 1] ** 2).unsqueeze(1).contiguous()
+del c3, v3, Xip
+twice(lambda: vb.vb_gi(gfip, wq * 6.0, gsz))
+del gfip, gsz
 del plan, K, M, cd, ed, Kl, u, fq
 
 c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
