@@ -47,7 +47,8 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_p1_assemble", "fem_p1_assemble_coef", "vb_quad_rule", "fem_p1_rhs", "vb_page_bilinear",
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
-           "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi")
+           "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi", "fem_plan_lattice",
+           "fem_p1_assemble_lattice")
 
 
 class VbError(RuntimeError):
@@ -97,6 +98,9 @@ def lib():
             "fem_p1_assemble_classes_coef": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, i32, d, p, p,
                                                    p, p, p]),
             "vb_gi": (i32, [i64, i32, i32, p, i64, p, p, p, i64, p, p, sz, p]),
+            "fem_plan_lattice": (i32, [i64, i64, p, i64, p, p, i64, i32, i32, i32, p, sz, p, C.POINTER(C.c_int64),
+                                       C.POINTER(C.c_int64), p]),
+            "fem_p1_assemble_lattice": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, i32, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -381,6 +385,50 @@ class P1Plan:
         self.tile_ok, self.tile_reason = True, ""
         return True
 
+    def lattice(self, elems, dims=None):
+        """Kuhn-lattice plan (fem_plan_lattice), built once and kept: verifies that
+        the mesh is an nx x ny x nz Kuhn lattice (dims; None = a cube inferred from
+        ne) and that the pattern is its stencil.  Returns True, or False with
+        plan.lattice_reason."""
+        if getattr(self, "lattice_ok", None) is not None:
+            return self.lattice_ok
+        self.lattice_ok, self.lattice_reason = False, ""
+        if self.dim != 3:
+            self.lattice_reason = "not 3D"
+            return False
+        if dims is None:
+            n = int(round((self.ne / 6) ** (1.0 / 3.0))) if self.ne > 0 else 0
+            dims = (n, n, n)
+        nx, ny, nz = (int(d) for d in dims)
+        if min(nx, ny, nz) < 1 or (nx + 1) * (ny + 1) * (nz + 1) != self.nn or 6 * nx * ny * nz != self.ne:
+            self.lattice_reason = "counts are not those of a %d x %d x %d Kuhn lattice" % (nx, ny, nz)
+            return False
+        L = lib()
+        dev = self.row_ptr.device
+        wb = C.c_size_t(0)
+        pints = C.c_int64(0)
+        st = _stream()
+        stats = (C.c_int64 * 4)()
+        _check(L.fem_plan_lattice(self.nn, self.ne, None, self.ne, None, None, self.nnz, nx, ny, nz, None,
+                                  C.byref(wb), None, C.byref(pints), stats, st))
+        work = torch.empty((max(wb.value, 16),), dtype=torch.uint8, device=dev)
+        plan = torch.zeros((max(int(pints.value), 16),), dtype=torch.int32, device=dev)
+        _check(L.fem_plan_lattice(self.nn, self.ne, _ptr(elems), elems.shape[1], _ptr(self.row_ptr),
+                                  _ptr(self.col_idx), self.nnz, nx, ny, nz, _ptr(work), C.byref(wb), _ptr(plan),
+                                  C.byref(pints), stats, st))
+        reasons = {0: "", 1: "counts", 2: "element 0 is not a Kuhn tetrahedron", 3: "degenerate lattice",
+                   4: "an element is not a Kuhn tetrahedron of the lattice (or appears twice)",
+                   5: "the CSR pattern is not the lattice stencil"}
+        if stats[0] != 1:
+            self.lattice_reason = reasons.get(int(stats[2]), "refused (%d)" % stats[2])
+            return False
+        self.lattice_plan = plan
+        self.lattice_dims = (nx, ny, nz)
+        self.lattice_flips = int(stats[3])
+        self.lattice_tiles = int(stats[1])
+        self.lattice_ok = True
+        return True
+
     def class_coverage(self):
         """Fraction of rows that the class variant assembles with the uniform loop."""
         if self.classes() is None or self.nn == 0:
@@ -414,6 +462,22 @@ def fem_p1_assemble_tiles(coords, plan, K=None, M=None, want_K=True, want_M=True
                                        _ptr(plan.tile_nodes), _ptr(plan.tile_rows), _ptr(plan.tile_colors),
                                        _ptr(plan.tile_elems), plan.tile_stats[2], plan.tile_stats[1], _ptr(K), _ptr(M),
                                        _stream(stream)))
+    return K, M
+
+
+def fem_p1_assemble_lattice(coords, plan, K=None, M=None, want_K=True, want_M=True, stream=None):
+    """Element-once K, M on a Kuhn lattice (fem_p1_assemble_lattice); plan.lattice(elems) must be True."""
+    _f64(coords)
+    dim, nn = coords.shape
+    dev = coords.device
+    if not getattr(plan, "lattice_ok", False):
+        raise ValueError("plan has no lattice plan: call plan.lattice(elems) first (and check it returned True)")
+    K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
+    M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
+    nx, ny, nz = plan.lattice_dims
+    _check(lib().fem_p1_assemble_lattice(nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr), plan.nnz,
+                                         _ptr(plan.lattice_plan), nx, ny, nz, plan.lattice_flips, _ptr(K), _ptr(M),
+                                         _stream(stream)))
     return K, M
 
 
@@ -494,6 +558,16 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         return K, M, Kl, Ml
     if variant == "tile":
         variant = "block"   # outside the tile variant's limits (plan.tile_reason)
+    if (mode == VB_ASSEMBLE_GATHER and variant in (None, "lattice") and (K is not None or M is not None)
+            and dim == 3 and plan.lattice(elems)):
+        fem_p1_assemble_lattice(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
+        if want_local:
+            _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
+                                         None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
+                                         _stream(stream)))
+        return K, M, Kl, Ml
+    if variant == "lattice":
+        variant = None   # not a Kuhn lattice (plan.lattice_reason)
     if mode == VB_ASSEMBLE_GATHER and (K is not None or M is not None) and _use_classes(plan, variant):
         fem_p1_assemble_classes(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
         if want_local:

@@ -91,30 +91,39 @@ def cube_kuhn_p1(n, jitter=0.05, seed=0, flip=(0, 0, 0)):
     (0,0,0)-(1,1,1) diagonal of BASELINE configs[4]; flip = (0, 0, 1) (the
     (0,0,1)-(1,1,0) diagonal) reproduces the error columns of the paper's 3D P1
     table (tab:KM_P1_3D) -- see tests/golden/paper_tables_p1.json."""
-    n1 = n + 1
-    nn = n1 ** 3
+    return box_kuhn_p1(n, n, n, jitter=jitter, seed=seed, flip=flip)
+
+
+def box_kuhn_p1(nx, ny, nz, jitter=0.05, seed=0, flip=(0, 0, 0)):
+    """cube_kuhn_p1 on the box [0, nx/m] x [0, ny/m] x [0, nz/m], m = max(nx, ny, nz)
+    (cells of side h = 1/m): node id = i + (nx+1)(j + (ny+1)k), cells x-fastest,
+    6 Kuhn tets per cell in lexicographic path order, the same jitter recipe
+    (one draw per node and coordinate in id order, interior nodes only)."""
+    nx1, ny1, nz1 = nx + 1, ny + 1, nz + 1
+    nn = nx1 * ny1 * nz1
+    m = max(nx, ny, nz)
     v = np.arange(nn, dtype=np.int64)
-    i = v % n1
-    j = (v // n1) % n1
-    k = v // (n1 * n1)
+    i = v % nx1
+    j = (v // nx1) % ny1
+    k = v // (nx1 * ny1)
     coords = np.empty((3, nn), dtype=np.float64)
-    coords[0] = i / n
-    coords[1] = j / n
-    coords[2] = k / n
+    coords[0] = i / m
+    coords[1] = j / m
+    coords[2] = k / m
     if jitter:
         r = uniform_pm1(seed, JITTER_STREAM, 3 * nn).reshape(nn, 3)
-        inner = _interior_mask((i, j, k), n)
-        h = 1.0 / n
+        inner = (i > 0) & (i < nx) & (j > 0) & (j < ny) & (k > 0) & (k < nz)
+        h = 1.0 / m
         for c in range(3):
             coords[c, inner] += jitter * h * r[inner, c]
-    c = np.arange(n ** 3, dtype=np.int64)
-    ci = c % n
-    cj = (c // n) % n
-    ck = c // (n * n)
+    c = np.arange(nx * ny * nz, dtype=np.int64)
+    ci = c % nx
+    cj = (c // nx) % ny
+    ck = c // (nx * ny)
     fl = [int(bool(f)) for f in flip]
-    v0 = (ci + fl[0]) + n1 * ((cj + fl[1]) + n1 * (ck + fl[2]))
-    step = (1 - 2 * fl[0], n1 * (1 - 2 * fl[1]), n1 * n1 * (1 - 2 * fl[2]))
-    elems = np.empty((4, 6 * n ** 3), dtype=np.int32)
+    v0 = (ci + fl[0]) + nx1 * ((cj + fl[1]) + ny1 * (ck + fl[2]))
+    step = (1 - 2 * fl[0], nx1 * (1 - 2 * fl[1]), nx1 * ny1 * (1 - 2 * fl[2]))
+    elems = np.empty((4, 6 * nx * ny * nz), dtype=np.int32)
     for t, p in enumerate(_KUHN_PERMS):
         a1 = v0 + step[p[0]]
         a2 = a1 + step[p[1]]

@@ -1,0 +1,162 @@
+"""GPU parity of the element-once Kuhn-lattice assembly (fem_plan_lattice +
+fem_p1_assemble_lattice, the headline kernel) against the CPU oracle through
+the C ABI: K and M within 1e-12 relative max-norm (BASELINE.json north_star)
+on boxes whose sizes straddle the kernel's tile edges (x segments of 32/31
+nodes, y bands of 12/11 lines, packed short segments, one-layer z ranges),
+every cell diagonal, shuffled element and vertex order, K-only / M-only
+outputs, bitwise reproducibility, refusal of non-lattice meshes (and the
+fallback of fem_p1_assemble), and every entry of the full configs[4] matrices
+against the full oracle assembly."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from paper_2404_16039_b200 import vb
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def dev():
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    return torch.device("cuda:0")
+
+
+def g(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def h(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def relmax(got, ref):
+    return np.max(np.abs(got - ref)) / max(np.max(np.abs(ref)), 1e-300)
+
+
+def lattice_run(coords, elems, dev, dims=None, **kw):
+    nn = coords.shape[1]
+    plan = vb.P1Plan(g(elems, dev), nn, scatter_map=False, gather_plan=False)
+    assert plan.lattice(g(elems, dev), dims=dims), plan.lattice_reason
+    K, M = vb.fem_p1_assemble_lattice(g(coords, dev), plan, **kw)
+    return plan, K, M
+
+
+@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 2, 2), (3, 4, 5), (7, 7, 7), (31, 2, 3), (32, 3, 2), (33, 2, 2),
+                                  (62, 1, 2), (63, 2, 1), (2, 11, 3), (3, 12, 2), (2, 23, 2), (4, 24, 3),
+                                  (5, 40, 2), (12, 13, 14), (70, 25, 3)])
+def test_lattice_vs_oracle(dev, dims):
+    coords, elems = synth.box_kuhn_p1(*dims, jitter=0.05, seed=3)
+    rp, ci = oracle.p1_pattern(elems, coords.shape[1])
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan, K, M = lattice_run(coords, elems, dev, dims=dims)
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    assert relmax(h(K), Ko) <= TOL
+    assert relmax(h(M), Mo) <= TOL
+
+
+@pytest.mark.parametrize("flip", [(0, 0, 1), (0, 1, 0), (1, 0, 0), (1, 1, 0), (0, 1, 1), (1, 1, 1)])
+def test_lattice_every_diagonal(dev, flip):
+    coords, elems = synth.box_kuhn_p1(9, 14, 5, jitter=0.05, seed=1, flip=flip)
+    rp, ci = oracle.p1_pattern(elems, coords.shape[1])
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan, K, M = lattice_run(coords, elems, dev, dims=(9, 14, 5))
+    assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+
+
+def test_lattice_shuffled_elements_and_vertices(dev):
+    coords, elems = synth.cube_kuhn_p1(8, jitter=0.05, seed=2)
+    rng = np.random.default_rng(7)
+    order = rng.permutation(elems.shape[1])
+    e2 = elems[:, order]
+    for e in range(e2.shape[1]):
+        e2[:, e] = e2[rng.permutation(4), e]
+    rp, ci = oracle.p1_pattern(e2, coords.shape[1])
+    Ko, Mo = oracle.p1_assemble(coords, e2, rp, ci)
+    plan, K, M = lattice_run(coords, e2, dev)
+    assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+
+
+def test_lattice_unjittered_kuhn_row(dev):
+    # SURVEY §8(c) pin 6 on the GPU: interior row = 6h diagonal, -h at the 6 axis neighbours, 0 elsewhere
+    n = 6
+    coords, elems = synth.cube_kuhn_p1(n, jitter=0.0)
+    plan, K, M = lattice_run(coords, elems, dev)
+    rp, ci, Kh, Mh = h(plan.row_ptr), h(plan.col_idx), h(K), h(M)
+    hh = 1.0 / n
+    v = 3 + (n + 1) * (3 + (n + 1) * 3)
+    row = dict(zip(ci[rp[v]:rp[v + 1]], Kh[rp[v]:rp[v + 1]]))
+    assert abs(row[v] - 6 * hh) < 1e-14
+    for d in (1, n + 1, (n + 1) ** 2):
+        assert abs(row[v + d] + hh) < 1e-14 and abs(row[v - d] + hh) < 1e-14
+    others = [x for c, x in row.items() if c not in (v, v + 1, v - 1, v + n + 1, v - n - 1, v + (n + 1) ** 2,
+                                                      v - (n + 1) ** 2)]
+    assert len(others) == 8 and max(abs(x) for x in others) < 1e-15
+    assert abs(Mh[rp[v]:rp[v + 1]].sum() - hh ** 3) < 1e-15
+
+
+def test_lattice_k_only_m_only_and_reproducible(dev):
+    coords, elems = synth.box_kuhn_p1(34, 13, 4, jitter=0.05, seed=4)
+    plan, K, M = lattice_run(coords, elems, dev, dims=(34, 13, 4))
+    Kh, Mh = h(K), h(M)
+    _, K2, M2 = lattice_run(coords, elems, dev, dims=(34, 13, 4))
+    assert np.array_equal(h(K2), Kh) and np.array_equal(h(M2), Mh)   # bitwise run to run
+    cd = g(coords, dev)
+    Ko, Mn = vb.fem_p1_assemble_lattice(cd, plan, want_M=False)
+    assert Mn is None and np.array_equal(h(Ko), Kh)
+    Kn, Mo = vb.fem_p1_assemble_lattice(cd, plan, want_K=False)
+    assert Kn is None and np.array_equal(h(Mo), Mh)
+
+
+def test_lattice_refuses_other_meshes_and_fem_p1_assemble_falls_back(dev):
+    coords, elems = synth.cube_kuhn_p1(5, jitter=0.05, seed=0)
+    nn = coords.shape[1]
+    # (a) one element replaced by a non-Kuhn tetrahedron of the same nodes (the pattern changes too)
+    bad = elems.copy()
+    bad[3, 7] = bad[3, 7] + 1
+    plan = vb.P1Plan(g(bad, dev), nn)
+    assert not plan.lattice(g(bad, dev)) and plan.lattice_reason
+    rp, ci = oracle.p1_pattern(bad, nn)
+    Ko, Mo = oracle.p1_assemble(coords, bad, rp, ci)
+    K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(bad, dev), plan)   # variant None: falls back
+    assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+    # (b) one Kuhn tetrahedron listed twice (another dropped)
+    dup = elems.copy()
+    dup[:, 11] = dup[:, 10]
+    plan = vb.P1Plan(g(dup, dev), nn)
+    assert not plan.lattice(g(dup, dev))
+    # (c) renumbered nodes: same mesh, not lattice numbering
+    c2, e2 = synth.permute_mesh(coords, elems, seed=1)
+    plan = vb.P1Plan(g(e2, dev), nn)
+    assert not plan.lattice(g(e2, dev))
+    # (d) 2D meshes and wrong dims
+    plan = vb.P1Plan(g(elems, dev), nn)
+    assert not plan.lattice(g(elems, dev), dims=(4, 5, 6))
+
+
+def test_lattice_plan_abi_errors(dev):
+    L = vb.lib()
+    import ctypes as C
+    wb, pi = C.c_size_t(0), C.c_int64(0)
+    stats = (C.c_int64 * 4)()
+    assert L.fem_plan_lattice(8, 6, None, 6, None, None, 0, 0, 1, 1, None, C.byref(wb), None, C.byref(pi), stats,
+                              None) == -1
+    assert L.fem_p1_assemble_lattice(9, None, 1, 9, None, 0, None, 1, 1, 1, 0, None, None, None) == -1
+
+
+def test_full_size_configs4_every_entry_vs_oracle(dev):
+    # BASELINE configs[4] in bench.py's launch configuration: all 31.8 M entries of K and M vs the full oracle
+    coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan = vb.P1Plan(g(elems, dev), nn, scatter_map=False, gather_plan=False)
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    assert plan.lattice(g(elems, dev))
+    K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan)   # variant None -> lattice
+    assert relmax(h(K), Ko) <= TOL
+    assert relmax(h(M), Mo) <= TOL
