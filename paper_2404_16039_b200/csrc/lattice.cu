@@ -24,15 +24,17 @@
 // (corner 000 at node c) contributes to 19 of them: the 7 of its own corner
 // 000 and 3 / 3 / 3 / 1 / 1 / 1 of corners 100 / 010 / 001 / 110 / 101 / 011.
 //
-// Kernel (assemble_lattice_k): a CTA holds a tile of 32 lanes (x) x R warp
+// Kernel (assemble_lattice_k): a CTA holds a tile of 32 lanes (x) x LR warp
 // rows (y) of lattice columns and marches along z, one node layer per step,
 // evaluating every cell (6 tets) ONCE.  Contributions move to the owning node
-// by warp shuffle (x), shared memory (y) and registers (z).  Row 0 of a tile
-// and the first lane of an x segment are halos (their cells are recomputed by
-// the neighbouring tile, ~15% of the cells); everything else is owned.  Rows of
-// CSR are assembled in registers (14 edges; diagonals by the partition of unity,
-// K_pp = -sum_q K_pq, M_pp = (2/3) sum_q M_pq, as the gather variants) and leave
-// through a shared-memory staging buffer with coalesced stores.
+// by warp shuffle (x), shared memory (y) and registers (z).  The first lane of
+// every x segment and row 0 of every band after the first are halos (their
+// cells are recomputed by the neighbouring tile); a halo lane left of x = 0 is
+// a virtual node whose (absent) cells contribute exact zeros, so no received
+// value needs masking.  Rows of CSR are assembled in registers (14 edges;
+// diagonals by the partition of unity, K_pp = -sum_q K_pq, M_pp = (2/3)
+// sum_q M_pq, as the gather variants), staged in shared memory and leave as
+// TMA bulk copies (cp.async.bulk) issued by one lane per segment.
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -42,11 +44,21 @@
 namespace vb {
 namespace {
 
-constexpr int LR = 12;            // warp rows per tile (row 0 may be a halo line)
+#ifndef VB_LAT_R
+#define VB_LAT_R 12
+#endif
+#ifndef VB_LAT_MINB
+#define VB_LAT_MINB 1
+#endif
+#ifndef VB_LAT_PACKW
+#define VB_LAT_PACKW 26   // cost weight of a packed tile's layer, in sixteenths of a full tile's
+#endif
+constexpr int LR = VB_LAT_R;      // warp rows per tile (row 0 may be a halo line)
 constexpr int LCOLS = 40;         // coordinate columns per row (lanes + one gap per segment)
-constexpr int LNBUF = 3;          // coordinate layer buffers (prefetch distance 2)
+constexpr int LNBUF = 4;          // coordinate layer buffers (prefetch distance 3, two groups in flight)
 constexpr int LSTG = 32 * 15 + 16;   // staging doubles per matrix and warp row
 constexpr int LTHREADS = 32 * LR;
+constexpr int LMAXCTA = 1024;     // CTA ranges passed by value
 constexpr uint32_t LAT_MAGIC = 0x4c415431u;   // "LAT1"
 
 // stencil directions: 0 self, 1..7 = +x +y +z +xy +xz +yz +xyz, 8..14 the negatives
@@ -54,10 +66,32 @@ __host__ __device__ constexpr int dir_dx(int d) { return d == 0 ? 0 : (d <= 7 ? 
 __host__ __device__ constexpr int dir_dy(int d) { return d == 0 ? 0 : (d <= 7 ? 1 : -1) * ((d - 1) % 7 == 1 || (d - 1) % 7 == 3 || (d - 1) % 7 == 5 || (d - 1) % 7 == 6); }
 __host__ __device__ constexpr int dir_dz(int d) { return d == 0 ? 0 : (d <= 7 ? 1 : -1) * ((d - 1) % 7 == 2 || (d - 1) % 7 == 4 || (d - 1) % 7 == 5 || (d - 1) % 7 == 6); }
 
+// CSR column order of the stencil for orientation (FY, FZ) (canonical x never mirrored): column ids
+// id0 + I + sy (nx+1) J + sz (nx+1)(ny+1) K sort lexicographically by (sz dz, sy dy, dx) when nx, ny >= 2;
+// fem_plan_lattice refuses lattices where the real order differs.  LOW[d] = directions before d.
+__host__ __device__ constexpr long long lex_off(int d, int FY, int FZ) {
+    return dir_dx(d) + (FY ? -4 : 4) * dir_dy(d) + (FZ ? -16 : 16) * dir_dz(d);
+}
+template <int FY, int FZ>
+struct Order {
+    uint32_t low[15];
+    int slot[15];   // position in an interior row (all 15 present)
+    __host__ __device__ constexpr Order() : low(), slot() {
+        for (int d = 0; d < 15; d++) {
+            uint32_t m = 0;
+            int c = 0;
+            for (int e = 0; e < 15; e++)
+                if (lex_off(e, FY, FZ) < lex_off(d, FY, FZ)) { m |= 1u << e; c++; }
+            low[d] = m;
+            slot[d] = c;
+        }
+    }
+};
+
 struct LatParams {
     int nx, ny, nz, T;            // cells per axis, tiles
     int64_t L;                    // T * (nz + 1) tile-layers
-    int64_t id0, dI, dJ, dK;      // node id of canonical (I, J, K) = id0 + dI I + dJ J + dK K
+    int id0, dJ, dK;              // node id of canonical (I, J, K) = id0 + I + dJ J + dK K
     const double* X;
     int64_t ns, cs;               // coordinate addressing X[c*cs + v*ns]
     const int32_t* row_ptr;
@@ -66,12 +100,14 @@ struct LatParams {
     const int4* lanes;            // T x 32 lane descriptors
     const uint32_t* token;        // plan token (LAT_MAGIC ^ hash) written by fem_plan_lattice
     uint32_t want;
-    uint16_t lower[16];           // lower[d]: directions whose id offset is below d's (CSR slot order)
+    int bulk;                     // K, M 16-byte aligned: rows leave as bulk copies
+    int range[LMAXCTA + 1];       // CTA c: tile-layers [range[c], range[c+1]) (cost-balanced)
 };
 
-// lane descriptor (int4): x = I (canonical x of the lane's node; -1: idle lane), y = J0 (canonical y of
-// row 0), z = flags | col << 8 | first owned lane << 16 | last lane << 24, w = staging base of the segment
-enum : int { LF_OWNX = 1, LF_LEFT = 2, LF_XPLUS = 4, LF_ROW0 = 8, LF_HEAD = 16 };
+// lane descriptor (int4): x = I (canonical x of the lane's node, -1 for the virtual halo left of x = 0,
+// -2: idle lane), y = J0 (canonical y of row 0), z = flags | col << 8 | first owned lane << 16 |
+// last lane << 24, w = staging base of the segment
+enum : int { LF_OWNX = 1, LF_XPLUS = 4, LF_ROW0 = 8, LF_HEAD = 16 };
 
 struct LatSmem {
     double X[LNBUF][3][LR + 1][LCOLS];   // node coordinates of a layer, [comp][row][column]
@@ -86,7 +122,13 @@ __device__ __forceinline__ void cpa8(double* dst, const double* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32l(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cpa_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void bulk_st(double* dst, const double* src, int bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32l(src)),
+                 "r"(bytes)
+                 : "memory");
+}
 
 // 1/x: hardware seed and two Newton steps (as the gather kernels)
 __device__ __forceinline__ double rcp2(double x) {
@@ -110,14 +152,17 @@ struct Tet {
 };
 // One tetrahedron v0, v1 = v0 + f1, v2 = v0 + f2, v3 = v0 + f3 (tjac rows f_r) with
 // h1 = f2 x f3 and h2 = f3 x f1 given (shared between the cell's tets): K_e off-diagonals and
-// the mass off-diagonal |T|/20 = |det|/120.
+// the mass off-diagonal |T|/20 = |det|/120.  CHK: live = false (no such cell) gives exact zeros
+// (the coordinates are finite, s = 0).
+template <bool CHK>
 __device__ __forceinline__ Tet tet(const double (&f1)[3], const double (&f2)[3], const double (&h1)[3],
-                                   const double (&h2)[3]) {
+                                   const double (&h2)[3], bool live) {
     double h3[3];
     crs(f1, f2, h3);
     const double det = dot3(f1, h1);
-    const double ad = fabs(det);
-    const double s = rcp2(6.0 * ad);
+    const double ad = CHK ? (live ? fabs(det) : 0.0) : fabs(det);
+    const double r = rcp2(6.0 * ad);
+    const double s = CHK ? (live ? r : 0.0) : r;
     double h0[3];
 #pragma unroll
     for (int c = 0; c < 3; c++) h0[c] = -(h1[c] + h2[c] + h3[c]);
@@ -132,30 +177,131 @@ __device__ __forceinline__ Tet tet(const double (&f1)[3], const double (&f2)[3],
     return t;
 }
 
+// The 6 Kuhn tetrahedra of one cell (corner 000 at x0[0], layer buffers x0 / x1 of the cell's bottom /
+// top nodes, columns +1 = +x, +LCOLS = +y), each evaluated once, routed to the 19 up edges the cell
+// touches (corner 000: e, corners 100: c100, 010 / 110 / 011: o, 101: c101, 001: c001).  Paths in
+// lexicographic order: (x,y,z) (x,z,y) (y,x,z) (y,z,x) (z,x,y) (z,y,x); t.m = |det|/120 of each.
+struct Cell {
+    double e[7];      // +x +y +z +xy +xz +yz +xyz
+    double c100[3];   // +y +z +yz
+    double o[5];      // c010: +x +z +xz, c110: +z, c011: +x
+    double c101;      // +y
+    double c001[3];   // +x +y +xy
+};
+template <bool CHK>
+__device__ __forceinline__ void cell(const double* x0, const double* x1, bool live, Cell& K, Cell& M) {
+    double x000[3], ux[3], uy[3], uz[3], wxy[3], wxz[3], wyz[3], bd[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        x000[c] = x0[c * ((LR + 1) * LCOLS)];
+        ux[c] = x0[c * ((LR + 1) * LCOLS) + 1] - x000[c];
+        uy[c] = x0[c * ((LR + 1) * LCOLS) + LCOLS] - x000[c];
+        wxy[c] = x0[c * ((LR + 1) * LCOLS) + LCOLS + 1] - x000[c];
+        uz[c] = x1[c * ((LR + 1) * LCOLS)] - x000[c];
+        wxz[c] = x1[c * ((LR + 1) * LCOLS) + 1] - x000[c];
+        wyz[c] = x1[c * ((LR + 1) * LCOLS) + LCOLS] - x000[c];
+        bd[c] = x1[c * ((LR + 1) * LCOLS) + LCOLS + 1] - x000[c];
+    }
+    double hxy[3], hxz[3], hyz[3];
+    crs(wxy, bd, hxy);
+    crs(wxz, bd, hxz);
+    crs(wyz, bd, hyz);
+    double mxyz, mxzy, myxz, myzx, mzxy, mzyx;
+    {   // paths starting along x
+        double h2[3];
+        crs(bd, ux, h2);
+        const Tet a = tet<CHK>(ux, wxy, hxy, h2, live);
+        const Tet b = tet<CHK>(ux, wxz, hxz, h2, live);
+        K.e[0] = a.k01 + b.k01;
+        K.e[3] = a.k02;
+        K.e[4] = b.k02;
+        K.e[6] = a.k03 + b.k03;
+        K.c100[0] = a.k12;
+        K.c100[1] = b.k12;
+        K.c100[2] = a.k13 + b.k13;
+        K.o[3] = a.k23;
+        K.c101 = b.k23;
+        mxyz = a.m;
+        mxzy = b.m;
+    }
+    {   // (y,x,z), (y,z,x)
+        double h2[3];
+        crs(bd, uy, h2);
+        const Tet a = tet<CHK>(uy, wxy, hxy, h2, live);
+        const Tet b = tet<CHK>(uy, wyz, hyz, h2, live);
+        K.e[1] = a.k01 + b.k01;
+        K.e[3] += a.k02;
+        K.e[5] = b.k02;
+        K.e[6] += a.k03 + b.k03;
+        K.o[0] = a.k12;
+        K.o[1] = b.k12;
+        K.o[2] = a.k13 + b.k13;
+        K.o[3] += a.k23;
+        K.o[4] = b.k23;
+        myxz = a.m;
+        myzx = b.m;
+    }
+    {   // (z,x,y), (z,y,x)
+        double h2[3];
+        crs(bd, uz, h2);
+        const Tet a = tet<CHK>(uz, wxz, hxz, h2, live);
+        const Tet b = tet<CHK>(uz, wyz, hyz, h2, live);
+        K.e[2] = a.k01 + b.k01;
+        K.e[4] += a.k02;
+        K.e[5] += b.k02;
+        K.e[6] += a.k03 + b.k03;
+        K.c001[0] = a.k12;
+        K.c001[1] = b.k12;
+        K.c001[2] = a.k13 + b.k13;
+        K.c101 += a.k23;
+        K.o[4] += b.k23;
+        mzxy = a.m;
+        mzyx = b.m;
+    }
+    // every edge of a tetrahedron carries its |det|/120: the same routing with six values
+    const double px = mxyz + mxzy, py = myxz + myzx, pz = mzxy + mzyx;
+    const double qxy = mxyz + myxz, qxz = mxzy + mzxy, qyz = myzx + mzyx;
+    M.e[0] = px; M.e[1] = py; M.e[2] = pz; M.e[3] = qxy; M.e[4] = qxz; M.e[5] = qyz; M.e[6] = (px + py) + pz;
+    M.c100[0] = mxyz; M.c100[1] = mxzy; M.c100[2] = px;
+    M.o[0] = myxz; M.o[1] = myzx; M.o[2] = py; M.o[3] = qxy; M.o[4] = qyz;
+    M.c101 = qxz;
+    M.c001[0] = mzxy; M.c001[1] = mzyx; M.c001[2] = pz;
+}
+
 // edge slots of the owned-edge arrays: +x +y +z +xy +xz +yz +xyz
 enum { EX = 0, EY, EZ, EXY, EXZ, EYZ, EXYZ };
 
-__device__ __forceinline__ double shup(double v, bool ok) {   // value of lane - 1 (0 if not the -x neighbour)
-    const double r = __shfl_up_sync(0xffffffffu, v, 1);
-    return ok ? r : 0.0;
-}
+__device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
 
-__global__ void __launch_bounds__(LTHREADS, 1) assemble_lattice_k(const LatParams p) {
+constexpr int XB = 3 * (LR + 1) * LCOLS;   // doubles per coordinate layer buffer
+constexpr int XC = (LR + 1) * LCOLS;       // doubles per component plane
+
+template <int FY, int FZ>
+__global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(const LatParams p) {
+    constexpr Order<FY, FZ> ORD{};
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LatSmem& S = *reinterpret_cast<LatSmem*>(smem_raw);
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     if (*p.token != p.want) return;   // plan of another mesh / not verified: write nothing
+    // coordinates of nodes never loaded must be finite: zero the layer buffers once
+    for (int i = threadIdx.x; i < LNBUF * XB; i += LTHREADS) (&S.X[0][0][0][0])[i] = 0.0;
+#ifdef VB_LAT_PROF
+    long long t_start = clock64();
+#endif
 
-    const int64_t g0 = p.L * blockIdx.x / gridDim.x, g1 = p.L * (blockIdx.x + 1) / gridDim.x;
+    const int64_t g0 = p.range[blockIdx.x], g1 = p.range[blockIdx.x + 1];
     const int NK = p.nz + 1;
+    const int64_t plane = p.dK;   // node id step per layer
+    double* const SK = S.S[w][0];
+    double* const SM = S.S[w][1];
     int64_t g = g0;
     while (g < g1) {
         const int tau = (int)(g / NK);
         const int ka = (int)(g % NK);
         const int64_t gend = (int64_t)(tau + 1) * NK < g1 ? (int64_t)(tau + 1) * NK : g1;
         const int kb = (int)(gend - (int64_t)tau * NK);   // node layers [ka, kb)
-        g += kb - ka;
+        g = gend;
 
         const int4 ds = p.lanes[tau * 32 + lane];
         const int I = ds.x;
@@ -164,34 +310,34 @@ __global__ void __launch_bounds__(LTHREADS, 1) assemble_lattice_k(const LatParam
         const int col = (ds.z >> 8) & 0xff;
         const int lfirst = (ds.z >> 16) & 0xff;
         const int llast = (ds.z >> 24) & 0xff;
-        const bool valid = I >= 0 && J <= p.ny;
-        const bool left = (fl & LF_LEFT) != 0;
-        const bool owned = valid && (fl & LF_OWNX) && (w > 0 || (fl & LF_ROW0));
-        const bool cellxy = valid && I < p.nx && J < p.ny;
-        const bool xplus = valid && (fl & LF_XPLUS) && I < p.nx;
-        const int64_t idIJ = p.id0 + p.dI * I + p.dJ * J;
+        const bool node = I >= 0 && J <= p.ny;                      // a real lattice node
+        const bool owned = node && (fl & LF_OWNX) && (w > 0 || (fl & LF_ROW0));
+        const bool cellxy = node && I < p.nx && J < p.ny;           // cell (I, J, .) exists
+        const bool xplus = node && (fl & LF_XPLUS) && I < p.nx;
+        const int idIJ = p.id0 + I + p.dJ * J;                      // valid where node
+        const double* xg = p.X + (int64_t)idIJ * p.ns;              // own node, layer 0
+        double* const xs = &S.X[0][0][w][col];
 
-        // coordinate prefetch of node layer Lz into buffer Lz % 3: own node, the +x node of a segment's
-        // last lane, and row LR (J + 1) for the last warp row
+        // coordinate prefetch of node layer Lz into buffer Lz % LNBUF: own node, the +x node of a
+        // segment's last lane, and row LR (J + 1) for the last warp row
         auto fetch = [&](int Lz) {
             if (Lz > p.nz) return;
-            const int b = Lz % LNBUF;
-            const int64_t v = idIJ + p.dK * Lz;
-            if (valid) {
+            double* d = xs + (Lz % LNBUF) * XB;
+            const double* sg = xg + (int64_t)Lz * plane * p.ns;
+            if (node) {
 #pragma unroll
-                for (int c = 0; c < 3; c++) cpa8(&S.X[b][c][w][col], p.X + c * p.cs + v * p.ns);
+                for (int c = 0; c < 3; c++) cpa8(d + c * XC, sg + c * p.cs);
                 if (xplus)
 #pragma unroll
-                    for (int c = 0; c < 3; c++) cpa8(&S.X[b][c][w][col + 1], p.X + c * p.cs + (v + p.dI) * p.ns);
+                    for (int c = 0; c < 3; c++) cpa8(d + c * XC + 1, sg + c * p.cs + p.ns);
             }
             if (w == LR - 1 && I >= 0 && J + 1 <= p.ny) {
-                const int64_t v2 = v + p.dJ;
+                const double* s2 = sg + (int64_t)p.dJ * p.ns;
 #pragma unroll
-                for (int c = 0; c < 3; c++) cpa8(&S.X[b][c][LR][col], p.X + c * p.cs + v2 * p.ns);
+                for (int c = 0; c < 3; c++) cpa8(d + c * XC + LCOLS, s2 + c * p.cs);
                 if (xplus)
 #pragma unroll
-                    for (int c = 0; c < 3; c++)
-                        cpa8(&S.X[b][c][LR][col + 1], p.X + c * p.cs + (v2 + p.dI) * p.ns);
+                    for (int c = 0; c < 3; c++) cpa8(d + c * XC + LCOLS + 1, s2 + c * p.cs + p.ns);
             }
         };
 
@@ -200,107 +346,48 @@ __global__ void __launch_bounds__(LTHREADS, 1) assemble_lattice_k(const LatParam
         fetch(Ls);
         fetch(Ls + 1);
         cpa_commit();
-        cpa_wait_all();
+        fetch(Ls + 2);
+        cpa_commit();
+        cpa_wait<1>();
         __syncthreads();
 
         // carries along z: zc = in-plane up edges (+x, +y, +xy) of this node at the next layer from the
         // cells below it; ez / exz = this node's +z / +xz edge of the previous layer
-        double zcK[3] = {0, 0, 0}, zcM[3] = {0, 0, 0};
+        double zcK0 = 0, zcK1 = 0, zcK2 = 0, zcM0 = 0, zcM1 = 0, zcM2 = 0;
         double ezK = 0, ezM = 0, exzK = 0, exzM = 0;
+        const int32_t* rpp = p.row_ptr + idIJ;
 
         for (int Lz = Ls; Lz < kb; Lz++) {
-            fetch(Lz + 2);
+            fetch(Lz + 3);
             cpa_commit();
             const bool out = Lz >= ka;
             int rp = 0;
-            if (out && owned) rp = __ldg(p.row_ptr + idIJ + p.dK * Lz);
+            if (out && owned) rp = __ldg(rpp + (int64_t)Lz * plane);
 
             // ---- phase A: the cell (I, J, Lz) -> owned edges eK/eM (+ carries) and outgoing parts
-            double eK[7], eM[7];
-#pragma unroll
-            for (int e = 0; e < 7; e++) eK[e] = eM[e] = 0.0;
-            eK[EX] = zcK[0]; eK[EY] = zcK[1]; eK[EXY] = zcK[2];
-            eM[EX] = zcM[0]; eM[EY] = zcM[1]; eM[EXY] = zcM[2];
-            double oK[10], oM[10];   // to the next row: c010 (x, z, xz), c110 (z), c011 (x) -- slots 0..4
-            double c101K = 0, c101M = 0;
-            double c100K[3] = {0, 0, 0}, c100M[3] = {0, 0, 0};
-#pragma unroll
-            for (int e = 0; e < 5; e++) oK[e] = oM[e] = 0.0;
-            double c001K[3] = {0, 0, 0}, c001M[3] = {0, 0, 0};
-            if (cellxy && Lz < p.nz) {
-                const int b0 = Lz % LNBUF, b1 = (Lz + 1) % LNBUF;
-                double x000[3], ux[3], uy[3], uz[3], wxy[3], wxz[3], wyz[3], bd[3];
-#pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    x000[c] = S.X[b0][c][w][col];
-                    ux[c] = S.X[b0][c][w][col + 1] - x000[c];
-                    uy[c] = S.X[b0][c][w + 1][col] - x000[c];
-                    wxy[c] = S.X[b0][c][w + 1][col + 1] - x000[c];
-                    uz[c] = S.X[b1][c][w][col] - x000[c];
-                    wxz[c] = S.X[b1][c][w][col + 1] - x000[c];
-                    wyz[c] = S.X[b1][c][w + 1][col] - x000[c];
-                    bd[c] = S.X[b1][c][w + 1][col + 1] - x000[c];
-                }
-                double hxy[3], hxz[3], hyz[3];
-                crs(wxy, bd, hxy);
-                crs(wxz, bd, hxz);
-                crs(wyz, bd, hyz);
-                {   // paths starting along x: (x,y,z), (x,z,y)
-                    double h2[3];
-                    crs(bd, ux, h2);
-                    const Tet a = tet(ux, wxy, hxy, h2);
-                    const Tet b = tet(ux, wxz, hxz, h2);
-                    eK[EX] += a.k01 + b.k01;   eM[EX] += a.m + b.m;
-                    eK[EXY] += a.k02;          eM[EXY] += a.m;
-                    eK[EXZ] += b.k02;          eM[EXZ] += b.m;
-                    eK[EXYZ] += a.k03 + b.k03; eM[EXYZ] += a.m + b.m;
-                    c100K[0] = a.k12;          c100M[0] = a.m;          // corner 100: +y
-                    c100K[1] = b.k12;          c100M[1] = b.m;          //             +z
-                    c100K[2] = a.k13 + b.k13;  c100M[2] = a.m + b.m;    //             +yz
-                    oK[3] = a.k23;             oM[3] = a.m;             // corner 110: +z
-                    c101K = b.k23;             c101M = b.m;             // corner 101: +y
-                }
-                {   // (y,x,z), (y,z,x)
-                    double h2[3];
-                    crs(bd, uy, h2);
-                    const Tet a = tet(uy, wxy, hxy, h2);
-                    const Tet b = tet(uy, wyz, hyz, h2);
-                    eK[EY] += a.k01 + b.k01;   eM[EY] += a.m + b.m;
-                    eK[EXY] += a.k02;          eM[EXY] += a.m;
-                    eK[EYZ] += b.k02;          eM[EYZ] += b.m;
-                    eK[EXYZ] += a.k03 + b.k03; eM[EXYZ] += a.m + b.m;
-                    oK[0] = a.k12;             oM[0] = a.m;             // corner 010: +x
-                    oK[1] = b.k12;             oM[1] = b.m;             //             +z
-                    oK[2] = a.k13 + b.k13;     oM[2] = a.m + b.m;       //             +xz
-                    oK[3] += a.k23;            oM[3] += a.m;            // corner 110: +z
-                    oK[4] = b.k23;             oM[4] = b.m;             // corner 011: +x
-                }
-                {   // (z,x,y), (z,y,x)
-                    double h2[3];
-                    crs(bd, uz, h2);
-                    const Tet a = tet(uz, wxz, hxz, h2);
-                    const Tet b = tet(uz, wyz, hyz, h2);
-                    eK[EZ] += a.k01 + b.k01;   eM[EZ] += a.m + b.m;
-                    eK[EXZ] += a.k02;          eM[EXZ] += a.m;
-                    eK[EYZ] += b.k02;          eM[EYZ] += b.m;
-                    eK[EXYZ] += a.k03 + b.k03; eM[EXYZ] += a.m + b.m;
-                    c001K[0] = a.k12;          c001M[0] = a.m;          // corner 001: +x
-                    c001K[1] = b.k12;          c001M[1] = b.m;          //             +y
-                    c001K[2] = a.k13 + b.k13;  c001M[2] = a.m + b.m;    //             +xy
-                    c101K += a.k23;            c101M += a.m;            // corner 101: +y
-                    oK[4] += b.k23;            oM[4] += b.m;            // corner 011: +x
-                }
+            Cell CK, CM;
+            {
+                const double* x0 = xs + (Lz & (LNBUF - 1)) * XB;
+                const double* x1 = xs + ((Lz + 1) & (LNBUF - 1)) * XB;
+                const bool live = cellxy && Lz < p.nz;   // the top layer has no cells (coordinates still finite)
+                if (__all_sync(0xffffffffu, live)) cell<false>(x0, x1, true, CK, CM);
+                else cell<true>(x0, x1, live, CK, CM);
             }
+            double eK[7], eM[7];
+            eK[EX] = zcK0 + CK.e[0]; eK[EY] = zcK1 + CK.e[1]; eK[EXY] = zcK2 + CK.e[3];
+            eM[EX] = zcM0 + CM.e[0]; eM[EY] = zcM1 + CM.e[1]; eM[EXY] = zcM2 + CM.e[3];
+            eK[EZ] = CK.e[2]; eK[EXZ] = CK.e[4]; eK[EYZ] = CK.e[5]; eK[EXYZ] = CK.e[6];
+            eM[EZ] = CM.e[2]; eM[EXZ] = CM.e[4]; eM[EYZ] = CM.e[5]; eM[EXYZ] = CM.e[6];
             // ---- phase B: x neighbours by shuffle, the next row through shared memory
-            eK[EY] += shup(c100K[0], left);  eM[EY] += shup(c100M[0], left);
-            eK[EZ] += shup(c100K[1], left);  eM[EZ] += shup(c100M[1], left);
-            eK[EYZ] += shup(c100K[2], left); eM[EYZ] += shup(c100M[2], left);
-            zcK[0] = c001K[0]; zcK[1] = c001K[1] + shup(c101K, left); zcK[2] = c001K[2];
-            zcM[0] = c001M[0]; zcM[1] = c001M[1] + shup(c101M, left); zcM[2] = c001M[2];
+            eK[EY] += shup(CK.c100[0]);  eM[EY] += shup(CM.c100[0]);
+            eK[EZ] += shup(CK.c100[1]);  eM[EZ] += shup(CM.c100[1]);
+            eK[EYZ] += shup(CK.c100[2]); eM[EYZ] += shup(CM.c100[2]);
+            zcK0 = CK.c001[0]; zcK1 = CK.c001[1] + shup(CK.c101); zcK2 = CK.c001[2];
+            zcM0 = CM.c001[0]; zcM1 = CM.c001[1] + shup(CM.c101); zcM2 = CM.c001[2];
 #pragma unroll
             for (int e = 0; e < 5; e++) {
-                S.P[w][e][lane] = oK[e];
-                S.P[w][5 + e][lane] = oM[e];
+                S.P[w][e][lane] = CK.o[e];
+                S.P[w][5 + e][lane] = CM.o[e];
             }
             __syncthreads();
 
@@ -308,10 +395,10 @@ __global__ void __launch_bounds__(LTHREADS, 1) assemble_lattice_k(const LatParam
             if (w > 0) {
                 const double* Pb = &S.P[w - 1][0][0];
                 eK[EX] += Pb[0 * 32 + lane];  eM[EX] += Pb[5 * 32 + lane];
-                eK[EZ] += Pb[1 * 32 + lane];  eM[EZ] += Pb[6 * 32 + lane];
+                eK[EZ] += Pb[1 * 32 + lane] + Pb[3 * 32 + lane - 1];
+                eM[EZ] += Pb[6 * 32 + lane] + Pb[8 * 32 + lane - 1];
                 eK[EXZ] += Pb[2 * 32 + lane]; eM[EXZ] += Pb[7 * 32 + lane];
-                if (left) { eK[EZ] += Pb[3 * 32 + lane - 1]; eM[EZ] += Pb[8 * 32 + lane - 1]; }
-                zcK[0] += Pb[4 * 32 + lane];  zcM[0] += Pb[9 * 32 + lane];
+                zcK0 += Pb[4 * 32 + lane];    zcM0 += Pb[9 * 32 + lane];
             }
             S.Ein[w][0][lane] = eK[EY];
             S.Ein[w][1][lane] = eM[EY];
@@ -321,86 +408,130 @@ __global__ void __launch_bounds__(LTHREADS, 1) assemble_lattice_k(const LatParam
             S.Ez[Lz & 1][w][1][lane] = eM[EYZ];
             S.Ez[Lz & 1][w][2][lane] = eK[EXYZ];
             S.Ez[Lz & 1][w][3][lane] = eM[EXYZ];
-            cpa_wait_all();
+            cpa_wait<1>();
             __syncthreads();
 
             // ---- phase D: the CSR rows of this layer's owned nodes
             // incoming edges (the up edges of the lower neighbours): -x, -y, -z, -xy, -xz, -yz, -xyz
             double iK[7], iM[7];
-            iK[0] = shup(eK[EX], left);  iM[0] = shup(eM[EX], left);
-            iK[4] = shup(exzK, left);    iM[4] = shup(exzM, left);
-            iK[2] = ezK;                 iM[2] = ezM;
-            iK[1] = iK[3] = iK[5] = iK[6] = 0.0;
-            iM[1] = iM[3] = iM[5] = iM[6] = 0.0;
+            iK[0] = shup(eK[EX]);  iM[0] = shup(eM[EX]);
+            iK[4] = shup(exzK);    iM[4] = shup(exzM);
+            iK[2] = ezK;           iM[2] = ezM;
             if (w > 0) {
                 iK[1] = S.Ein[w - 1][0][lane];
                 iM[1] = S.Ein[w - 1][1][lane];
-                if (left) { iK[3] = S.Ein[w - 1][2][lane - 1]; iM[3] = S.Ein[w - 1][3][lane - 1]; }
+                iK[3] = (&S.Ein[w - 1][2][0])[lane - 1];
+                iM[3] = (&S.Ein[w - 1][3][0])[lane - 1];
                 if (Lz > 0) {
                     const int q = (Lz - 1) & 1;
                     iK[5] = S.Ez[q][w - 1][0][lane];
                     iM[5] = S.Ez[q][w - 1][1][lane];
-                    if (left) { iK[6] = S.Ez[q][w - 1][2][lane - 1]; iM[6] = S.Ez[q][w - 1][3][lane - 1]; }
+                    iK[6] = (&S.Ez[q][w - 1][2][0])[lane - 1];
+                    iM[6] = (&S.Ez[q][w - 1][3][0])[lane - 1];
+                } else {
+                    iK[5] = iK[6] = iM[5] = iM[6] = 0.0;
                 }
+            } else {
+                iK[1] = iK[3] = iK[5] = iK[6] = iM[1] = iM[3] = iM[5] = iM[6] = 0.0;
             }
             ezK = eK[EZ]; ezM = eM[EZ]; exzK = eK[EXZ]; exzM = eM[EXZ];
 
             if (out) {
-                double* SK = S.S[w][0];
-                double* SM = S.S[w][1];
                 // segment of this lane: CSR base = row_ptr of its first owned lane; the staging offset keeps
-                // the parity of the CSR position (16-byte alignment for bulk copies)
+                // the parity of the CSR position (16-byte aligned bodies for the bulk copies)
                 const int a_seg = __shfl_sync(0xffffffffu, rp, lfirst);
                 const int soff = ds.w + (a_seg & 1);
+                const bool px = I < p.nx, mx = I > 0, py = J < p.ny, my = J > 0, pz = Lz < p.nz, mz = Lz > 0;
                 int rlen = 0;
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging of the last step read
+                __syncwarp();
                 if (owned) {
-                    // stencil presence (canonical bounds) and slots in ascending column order
-                    const bool px = I < p.nx, mx = I > 0, py = J < p.ny, my = J > 0, pz = Lz < p.nz, mz = Lz > 0;
-                    uint32_t pres = 1u;
-                    pres |= (uint32_t)px << 1 | (uint32_t)py << 2 | (uint32_t)pz << 3 | (uint32_t)(px && py) << 4 |
-                            (uint32_t)(px && pz) << 5 | (uint32_t)(py && pz) << 6 | (uint32_t)(px && py && pz) << 7;
-                    pres |= (uint32_t)mx << 8 | (uint32_t)my << 9 | (uint32_t)mz << 10 | (uint32_t)(mx && my) << 11 |
-                            (uint32_t)(mx && mz) << 12 | (uint32_t)(my && mz) << 13 | (uint32_t)(mx && my && mz) << 14;
-                    rlen = __popc(pres);
                     double sK = 0.0, sM = 0.0;
 #pragma unroll
                     for (int e = 0; e < 7; e++) { sK += eK[e] + iK[e]; sM += eM[e] + iM[e]; }
-                    const int base = soff + (rp - a_seg);
-                    SK[base + __popc(pres & p.lower[0])] = -sK;
-                    SM[base + __popc(pres & p.lower[0])] = sM * (2.0 / 3.0);
+                    double* rk = SK + soff + (rp - a_seg);
+                    double* rm = SM + soff + (rp - a_seg);
+                    if (px && mx && py && my && pz && mz) {   // interior row: all 15 columns
+                        rlen = 15;
+                        rk[ORD.slot[0]] = -sK;
+                        rm[ORD.slot[0]] = sM * (2.0 / 3.0);
 #pragma unroll
-                    for (int e = 0; e < 7; e++) {
-                        if (pres >> (1 + e) & 1) {
-                            const int s = base + __popc(pres & p.lower[1 + e]);
-                            SK[s] = eK[e];
-                            SM[s] = eM[e];
+                        for (int e = 0; e < 7; e++) {
+                            rk[ORD.slot[1 + e]] = eK[e];
+                            rm[ORD.slot[1 + e]] = eM[e];
+                            rk[ORD.slot[8 + e]] = iK[e];
+                            rm[ORD.slot[8 + e]] = iM[e];
                         }
-                        if (pres >> (8 + e) & 1) {
-                            const int s = base + __popc(pres & p.lower[8 + e]);
-                            SK[s] = iK[e];
-                            SM[s] = iM[e];
+                    } else {   // boundary row: the present columns, same order
+                        uint32_t pres = 1u;
+                        pres |= (uint32_t)px << 1 | (uint32_t)py << 2 | (uint32_t)pz << 3 |
+                                (uint32_t)(px && py) << 4 | (uint32_t)(px && pz) << 5 | (uint32_t)(py && pz) << 6 |
+                                (uint32_t)(px && py && pz) << 7;
+                        pres |= (uint32_t)mx << 8 | (uint32_t)my << 9 | (uint32_t)mz << 10 |
+                                (uint32_t)(mx && my) << 11 | (uint32_t)(mx && mz) << 12 |
+                                (uint32_t)(my && mz) << 13 | (uint32_t)(mx && my && mz) << 14;
+                        rlen = __popc(pres);
+                        rk[__popc(pres & ORD.low[0])] = -sK;
+                        rm[__popc(pres & ORD.low[0])] = sM * (2.0 / 3.0);
+#pragma unroll
+                        for (int e = 0; e < 7; e++) {
+                            if (pres >> (1 + e) & 1) {
+                                const int s = __popc(pres & ORD.low[1 + e]);
+                                rk[s] = eK[e];
+                                rm[s] = eM[e];
+                            }
+                            if (pres >> (8 + e) & 1) {
+                                const int s = __popc(pres & ORD.low[8 + e]);
+                                rk[s] = iK[e];
+                                rm[s] = iM[e];
+                            }
                         }
                     }
                 }
+                // segment range [a_seg, end of its last owned lane's row)
+                const int segend = __shfl_sync(0xffffffffu, rp + rlen, llast);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                // coalesced write-out, one segment at a time (the owned lanes of a segment are contiguous)
+                // one segment at a time (warp-uniform): lane 0 issues the 16-byte aligned body as two bulk
+                // copies (K, M), lanes 1 / 2 store an odd leading / trailing entry
                 uint32_t heads = __ballot_sync(0xffffffffu, owned && (fl & LF_HEAD));
-                const int rend = rp + rlen;
                 while (heads) {
-                    const int h = __ffs(heads) - 1;
+                    const int hd = __ffs(heads) - 1;
                     heads &= heads - 1;
-                    const int a = __shfl_sync(0xffffffffu, rp, h);
-                    const int hl = __shfl_sync(0xffffffffu, llast, h);
-                    const int so = __shfl_sync(0xffffffffu, soff, h);
-                    const int n = __shfl_sync(0xffffffffu, rend, hl) - a;
-                    if (p.Kv)
-                        for (int q = lane; q < n; q += 32) __stcs(p.Kv + a + q, SK[so + q]);
-                    if (p.Mv)
-                        for (int q = lane; q < n; q += 32) __stcs(p.Mv + a + q, SM[so + q]);
+                    const int a0 = __shfl_sync(0xffffffffu, a_seg, hd);
+                    const int e0 = __shfl_sync(0xffffffffu, segend, hd);
+                    const int s0 = __shfl_sync(0xffffffffu, soff, hd);
+                    if (p.bulk) {
+                        const int a = a0 + (a0 & 1), e = e0 - (e0 & 1);   // aligned body [a, e)
+                        if (lane == 0 && e > a) {
+                            if (p.Kv) bulk_st(p.Kv + a, SK + s0 + (a - a0), (e - a) * 8);
+                            if (p.Mv) bulk_st(p.Mv + a, SM + s0 + (a - a0), (e - a) * 8);
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
+                        const int q = lane == 1 ? a0 : e0 - 1;   // an odd first / last entry
+                        if ((lane == 1 && (a0 & 1) && a0 < e0) || (lane == 2 && (e0 & 1) && e0 - 1 > a0)) {
+                            if (p.Kv) __stcs(p.Kv + q, SK[s0 + (q - a0)]);
+                            if (p.Mv) __stcs(p.Mv + q, SM[s0 + (q - a0)]);
+                        }
+                    } else {
+                        for (int q = a0 + lane; q < e0; q += 32) {
+                            if (p.Kv) p.Kv[q] = SK[s0 + (q - a0)];
+                            if (p.Mv) p.Mv[q] = SM[s0 + (q - a0)];
+                        }
+                    }
                 }
             }
         }
     }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#ifdef VB_LAT_PROF
+    if (threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        printf("LATPROF cta %d sm %u cycles %lld ns 0 g0 %lld g1 %lld\n", blockIdx.x, smid, clock64() - t_start,
+               (long long)g0, (long long)g1);
+    }
+#endif
 }
 
 // ------------------------------------------------------------------ plan: verification kernels
@@ -501,9 +632,13 @@ struct LatHost {
 bool lat_host(int nx, int ny, int nz, const int* flip, LatHost& h) {
     h.nx = nx; h.ny = ny; h.nz = nz;
     h.fx = flip[0] ? 1 : 0; h.fy = flip[1] ? 1 : 0; h.fz = flip[2] ? 1 : 0;
+    if (h.fx) {   // mirroring all three axes maps a Kuhn lattice onto itself: keep x unmirrored
+        h.fx = 0; h.fy ^= 1; h.fz ^= 1;
+    }
     const int64_t NX1 = nx + 1, NY1 = ny + 1;
-    h.id0 = (h.fx ? nx : 0) + NX1 * ((h.fy ? ny : 0) + NY1 * (int64_t)(h.fz ? nz : 0));
-    h.dI = h.fx ? -1 : 1;
+    if (NX1 * NY1 * (nz + 1) >= ((int64_t)1 << 31)) return false;
+    h.id0 = NX1 * ((h.fy ? ny : 0) + NY1 * (int64_t)(h.fz ? nz : 0));
+    h.dI = 1;
     h.dJ = (h.fy ? -1 : 1) * NX1;
     h.dK = (h.fz ? -1 : 1) * NX1 * NY1;
     int64_t off[15];
@@ -512,12 +647,19 @@ bool lat_host(int nx, int ny, int nz, const int* flip, LatHost& h) {
     for (int d = 0; d < 15; d++)
         for (int e = 0; e < 15; e++) {
             if (e != d && off[e] == off[d]) return false;   // two stencil columns with one id
-            if (off[e] < off[d]) h.lower[d] |= (uint16_t)(1u << (e == 0 ? 0 : e));
+            if (off[e] < off[d]) h.lower[d] |= (uint16_t)(1u << e);
         }
-    // pres bit of direction d is bit d (self = bit 0); lower uses the same bits
+    // the kernel's compile-time column order must be the real one (it is for nx, ny >= 2)
+    const Order<0, 0> o00{};
+    const Order<0, 1> o01{};
+    const Order<1, 0> o10{};
+    const Order<1, 1> o11{};
+    const uint32_t* low = h.fy ? (h.fz ? o11.low : o10.low) : (h.fz ? o01.low : o00.low);
+    for (int d = 0; d < 15; d++)
+        if (low[d] != h.lower[d]) return false;
     int idx[15];
     for (int d = 0; d < 15; d++) idx[d] = d;
-    std::sort(idx, idx + 15, [&](int a, int b) { return off[a] < off[b]; });
+    std::sort(idx, idx + 15, [&](int x, int y) { return off[x] < off[y]; });
     for (int r = 0; r < 15; r++) h.ord.dir[r] = idx[r];
     return true;
 }
@@ -535,58 +677,76 @@ uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz) {
     return t ? t : 1u;
 }
 
-// tiles of 32 lanes: x segments (the first owns 32 nodes, the next a halo lane + 31), y bands of LR rows
-// (the first owns LR lines, the next a halo line + LR - 1); short segments of all bands packed together
-void lat_tiles(int nx, int ny, std::vector<int4>& lanes, int& T) {
-    struct Seg { int I0, halo, nown; };
+// Tiles of 32 lanes.  x segments: a halo lane and 31 owned nodes (segment 0's halo is the virtual
+// node x = -1); y bands of LR rows (the first owns LR lines, the next a halo line + LR - 1).  The
+// short last segment of every band is packed with those of other bands.  work[t] = warp rows of
+// tile t that hold a node (the cost weight of its layers).
+void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work, int& T) {
+    struct Seg { int I0, nown; };
     std::vector<Seg> full, shortv;
-    {
-        int nown = std::min(32, nx + 1);
-        (nown == 32 ? full : shortv).push_back({0, 0, nown});
-        int covered = nown - 1;
-        while (covered < nx) {
-            const int n = std::min(31, nx - covered);
-            (n == 31 ? full : shortv).push_back({covered, 1, n});
-            covered += n;
-        }
+    for (int x0 = 0; x0 <= nx; x0 += 31) {
+        const int n = std::min(31, nx + 1 - x0);
+        (n == 31 ? full : shortv).push_back({x0 - 1, n});
     }
     std::vector<std::pair<int, int>> bands;   // (J0, row 0 owned)
     bands.push_back({0, 1});
     for (int covered = LR - 1; covered < ny; covered += LR - 1) bands.push_back({covered, 0});
+    auto rows_of = [&](int J0) { return std::min(LR, ny - J0 + 1); };
     lanes.clear();
+    work.clear();
     auto lane_of = [](const Seg& sg, int J0, int row0, int lo, int k, int base, int l) {
-        const int W = sg.nown + sg.halo;
+        const int W = sg.nown + 1;
         int fl = 0;
-        if (!(sg.halo && l == lo)) fl |= LF_OWNX;
-        if (l > lo) fl |= LF_LEFT;
+        if (l > lo) fl |= LF_OWNX;
         if (l == lo + W - 1) fl |= LF_XPLUS;
         if (row0) fl |= LF_ROW0;
-        if (l == lo + sg.halo) fl |= LF_HEAD;
-        const int col = l + k, first = lo + sg.halo, last = lo + W - 1;
+        if (l == lo + 1) fl |= LF_HEAD;
+        const int col = l + k, first = lo + 1, last = lo + W - 1;
         return make_int4(sg.I0 + (l - lo), J0, fl | col << 8 | first << 16 | last << 24, base);
     };
-    const int4 idle = make_int4(-1, 0, (LCOLS - 1) << 8, 0);
+    const int4 idle = make_int4(-2, 0, 0, 0);
     for (auto& b : bands)
-        for (auto& sg : full)
+        for (auto& sg : full) {
             for (int l = 0; l < 32; l++) lanes.push_back(lane_of(sg, b.first, b.second, 0, 0, 0, l));
+            work.push_back(16 * rows_of(b.first));
+        }
     if (!shortv.empty()) {
-        // at most one short segment per band (the last one); all of the same width
-        const int W = shortv[0].nown + shortv[0].halo;
-        const int per = std::min(8, 32 / W);
+        // at most one short segment per band (the last one), all of the same width
+        const int W = shortv[0].nown + 1;
+        const int per = std::min(7, 32 / W);
         for (size_t b0 = 0; b0 < bands.size(); b0 += per) {
             int4 t[32];
             for (int l = 0; l < 32; l++) t[l] = idle;
-            int base = 0;
+            int base = 0, rows = 0;
             for (int k = 0; k < per && b0 + k < bands.size(); k++) {
                 const int lo = k * W;
                 for (int l = lo; l < lo + W; l++)
                     t[l] = lane_of(shortv[0], bands[b0 + k].first, bands[b0 + k].second, lo, k, base, l);
-                base += 15 * shortv[0].nown + 2;
+                base += (15 * shortv[0].nown + 3) & ~1;   // even: 16-byte aligned staging bodies
+                rows = std::max(rows, rows_of(bands[b0 + k].first));
             }
             for (int l = 0; l < 32; l++) lanes.push_back(t[l]);
+            work.push_back(VB_LAT_PACKW * rows);   // several segments: more bulk copies per step
         }
     }
     T = (int)(lanes.size() / 32);
+}
+
+// CTA ranges over the tile-layer sequence (tile-major), balanced by the tiles' weights
+void lat_ranges(const std::vector<int>& work, int nz, int G, int* range) {
+    const int NK = nz + 1;
+    int64_t tot = 0;
+    for (int w : work) tot += (int64_t)w * NK;
+    range[0] = 0;
+    int64_t acc = 0, gidx = 0;
+    int c = 1;
+    for (size_t t = 0; t < work.size() && c < G; t++)
+        for (int k = 0; k < NK && c < G; k++) {
+            acc += work[t];
+            gidx++;
+            while (c < G && acc * G >= tot * c) range[c++] = (int)gidx;
+        }
+    while (c <= G) range[c++] = (int)(work.size() * NK);
 }
 
 constexpr int LAT_HDR = 16;   // plan header ints (token, dims, flips, tiles), then the lane descriptors
@@ -606,8 +766,9 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     }
     const int64_t nn_want = (int64_t)(nx + 1) * (ny + 1) * (nz + 1), ne_want = (int64_t)6 * nx * ny * nz;
     std::vector<int4> lanes;
+    std::vector<int> twork;
     int T = 0;
-    lat_tiles(nx, ny, lanes, T);
+    lat_tiles(nx, ny, lanes, twork, T);
     const int64_t need_ints = LAT_HDR + (int64_t)T * 32 * 4;
     const size_t wb = 256 + (size_t)((ne_want + 31) / 32) * 4;
     if (!work) {
@@ -656,6 +817,7 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
         flip[1] = dy < 0;
         flip[2] = dz < 0;
     }
+    if (nx < 2 || ny < 2) { stats_out[2] = 3; return VB_OK; }   // the kernel's column order needs nx, ny >= 2
     LatHost h;
     if (!lat_host(nx, ny, nz, flip, h)) { stats_out[2] = 3; return VB_OK; }
     LatGeom g{nx, ny, nz, h.fx, h.fy, h.fz, (int64_t)nx + 1, (int64_t)ny + 1};
@@ -706,30 +868,44 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     if (!K_vals && !M_vals) return VB_OK;
     const int fl[3] = {flips & 1, (flips >> 1) & 1, (flips >> 2) & 1};
     LatHost h;
-    if (!lat_host(nx, ny, nz, fl, h)) { set_error("%s: degenerate lattice", fn); return VB_ERR_ARG; }
+    if (nx < 2 || ny < 2 || !lat_host(nx, ny, nz, fl, h)) {
+        set_error("%s: lattice outside the kernel's limits (nx, ny >= 2)", fn);
+        return VB_ERR_ARG;
+    }
     std::vector<int4> lanes;
+    std::vector<int> twork;
     int T = 0;
-    lat_tiles(nx, ny, lanes, T);
+    lat_tiles(nx, ny, lanes, twork, T);
     LatParams p;
     p.nx = nx; p.ny = ny; p.nz = nz; p.T = T;
     p.L = (int64_t)T * (nz + 1);
-    p.id0 = h.id0; p.dI = h.dI; p.dJ = h.dJ; p.dK = h.dK;
+    p.id0 = (int)h.id0; p.dJ = (int)h.dJ; p.dK = (int)h.dK;
     p.X = coords; p.ns = node_stride; p.cs = comp_stride;
     p.row_ptr = row_ptr;
     p.Kv = K_vals; p.Mv = M_vals;
     p.lanes = reinterpret_cast<const int4*>(plan + LAT_HDR);
     p.token = reinterpret_cast<const uint32_t*>(plan);
     p.want = lat_want(h, nn, nnz);
-    for (int d = 0; d < 16; d++) p.lower[d] = h.lower[d];
-    static int smem_set = 0;
+    p.bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
+    int grid = std::min(sm_count() * VB_LAT_MINB, LMAXCTA);
+    if (grid > p.L) grid = (int)p.L;
+    lat_ranges(twork, nz, grid, p.range);
     const size_t smem = sizeof(LatSmem);
+    static int smem_set = 0;
     if (!smem_set) {
-        cudaFuncSetAttribute(assemble_lattice_k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(assemble_lattice_k<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(assemble_lattice_k<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(assemble_lattice_k<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(assemble_lattice_k<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         smem_set = 1;
     }
-    int grid = sm_count();
-    if (grid > p.L) grid = (int)p.L;
-    assemble_lattice_k<<<grid, LTHREADS, smem, cs(stream)>>>(p);
+    auto launch = [&](void (*kern)(LatParams)) { kern<<<grid, LTHREADS, smem, cs(stream)>>>(p); };
+    switch (h.fy | h.fz << 1) {
+        case 0: launch(assemble_lattice_k<0, 0>); break;
+        case 1: launch(assemble_lattice_k<1, 0>); break;
+        case 2: launch(assemble_lattice_k<0, 1>); break;
+        default: launch(assemble_lattice_k<1, 1>); break;
+    }
     return launch_check(fn);
 }
 

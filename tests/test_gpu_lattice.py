@@ -46,9 +46,9 @@ def lattice_run(coords, elems, dev, dims=None, **kw):
     return plan, K, M
 
 
-@pytest.mark.parametrize("dims", [(1, 1, 1), (2, 2, 2), (3, 4, 5), (7, 7, 7), (31, 2, 3), (32, 3, 2), (33, 2, 2),
-                                  (62, 1, 2), (63, 2, 1), (2, 11, 3), (3, 12, 2), (2, 23, 2), (4, 24, 3),
-                                  (5, 40, 2), (12, 13, 14), (70, 25, 3)])
+@pytest.mark.parametrize("dims", [(2, 2, 1), (2, 2, 2), (3, 4, 5), (7, 7, 7), (29, 2, 3), (30, 3, 2), (31, 2, 2),
+                                  (32, 2, 3), (61, 2, 2), (62, 3, 1), (63, 2, 1), (2, 11, 3), (3, 12, 2), (2, 23, 2),
+                                  (4, 24, 3), (5, 40, 2), (12, 13, 14), (70, 25, 3), (124, 3, 2)])
 def test_lattice_vs_oracle(dev, dims):
     coords, elems = synth.box_kuhn_p1(*dims, jitter=0.05, seed=3)
     rp, ci = oracle.p1_pattern(elems, coords.shape[1])
@@ -133,9 +133,18 @@ def test_lattice_refuses_other_meshes_and_fem_p1_assemble_falls_back(dev):
     c2, e2 = synth.permute_mesh(coords, elems, seed=1)
     plan = vb.P1Plan(g(e2, dev), nn)
     assert not plan.lattice(g(e2, dev))
-    # (d) 2D meshes and wrong dims
+    # (d) wrong dims
     plan = vb.P1Plan(g(elems, dev), nn)
     assert not plan.lattice(g(elems, dev), dims=(4, 5, 6))
+    # (e) lattices thinner than the kernel's column order allows (nx or ny = 1): refused, fallback exact
+    for dims in ((1, 1, 1), (1, 4, 3), (5, 1, 2)):
+        c1, e1 = synth.box_kuhn_p1(*dims, jitter=0.05, seed=5)
+        plan = vb.P1Plan(g(e1, dev), c1.shape[1])
+        assert not plan.lattice(g(e1, dev), dims=dims)
+        rp1, ci1 = oracle.p1_pattern(e1, c1.shape[1])
+        Ko1, Mo1 = oracle.p1_assemble(c1, e1, rp1, ci1)
+        K1, M1, _, _ = vb.fem_p1_assemble(g(c1, dev), g(e1, dev), plan)
+        assert relmax(h(K1), Ko1) <= TOL and relmax(h(M1), Mo1) <= TOL
 
 
 def test_lattice_plan_abi_errors(dev):

@@ -20,16 +20,18 @@ M = torch.empty_like(K)
 
 
 def t(fn, reps=20):
+    """back-to-back launches (as bench.py's timed steps), one event pair per launch"""
     for _ in range(3):
         fn()
-    out = []
-    for _ in range(reps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
         a.record()
         fn()
         b.record()
-        b.synchronize()
-        out.append(a.elapsed_time(b))
+    torch.cuda.synchronize()
+    out = [a.elapsed_time(b) for a, b in ev]
+    if os.environ.get("VB_TIMES"):
+        print(" ".join("%.4f" % x for x in out))
     return statistics.median(out), min(out)
 
 
