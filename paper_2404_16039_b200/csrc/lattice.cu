@@ -50,9 +50,6 @@ namespace {
 #ifndef VB_LAT_MINB
 #define VB_LAT_MINB 1
 #endif
-#ifndef VB_LAT_PACKW
-#define VB_LAT_PACKW 26   // cost weight of a packed tile's layer, in sixteenths of a full tile's
-#endif
 constexpr int LR = VB_LAT_R;      // warp rows per tile (row 0 may be a halo line)
 constexpr int LCOLS = 40;         // coordinate columns per row (lanes + one gap per segment)
 constexpr int LNBUF = 4;          // coordinate layer buffers (prefetch distance 3, two groups in flight)
@@ -107,7 +104,7 @@ struct LatParams {
 // lane descriptor (int4): x = I (canonical x of the lane's node, -1 for the virtual halo left of x = 0,
 // -2: idle lane), y = J0 (canonical y of row 0), z = flags | col << 8 | first owned lane << 16 |
 // last lane << 24, w = staging base of the segment
-enum : int { LF_OWNX = 1, LF_XPLUS = 4, LF_ROW0 = 8, LF_HEAD = 16 };
+enum : int { LF_OWNX = 1, LF_XPLUS = 4, LF_ROW0 = 8, LF_HEAD = 16, LF_BULK = 32 };
 
 struct LatSmem {
     double X[LNBUF][3][LR + 1][LCOLS];   // node coordinates of a layer, [comp][row][column]
@@ -440,7 +437,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                 // segment of this lane: CSR base = row_ptr of its first owned lane; the staging offset keeps
                 // the parity of the CSR position (16-byte aligned bodies for the bulk copies)
                 const int a_seg = __shfl_sync(0xffffffffu, rp, lfirst);
-                const int soff = ds.w + (a_seg & 1);
+                const int soff = ds.w + ((fl & LF_BULK) ? (a_seg & 1) : 0);
                 const bool px = I < p.nx, mx = I > 0, py = J < p.ny, my = J > 0, pz = Lz < p.nz, mz = Lz > 0;
                 int rlen = 0;
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // staging of the last step read
@@ -501,7 +498,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                     const int a0 = __shfl_sync(0xffffffffu, a_seg, hd);
                     const int e0 = __shfl_sync(0xffffffffu, segend, hd);
                     const int s0 = __shfl_sync(0xffffffffu, soff, hd);
-                    if (p.bulk) {
+                    if (p.bulk && (fl & LF_BULK)) {   // full segments via TMA (uniform per tile)
                         const int a = a0 + (a0 & 1), e = e0 - (e0 & 1);   // aligned body [a, e)
                         if (lane == 0 && e > a) {
                             if (p.Kv) bulk_st(p.Kv + a, SK + s0 + (a - a0), (e - a) * 8);
@@ -677,6 +674,11 @@ uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz) {
     return t ? t : 1u;
 }
 
+// Relative cost of one tile-layer (measured, B200, per-CTA clock64 of the VB_LAT_PROF build): a fixed
+// part (barriers, latencies) and a part per warp row holding nodes; a band without a halo row owns
+// all its rows (one more row of output, the boundary row J = 0).
+int lat_cost(int rows, int row0_owned) { return 200 + 39 * rows + (row0_owned ? 39 : 0); }
+
 // Tiles of 32 lanes.  x segments: a halo lane and 31 owned nodes (segment 0's halo is the virtual
 // node x = -1); y bands of LR rows (the first owns LR lines, the next a halo line + LR - 1).  The
 // short last segment of every band is packed with those of other bands.  work[t] = warp rows of
@@ -696,7 +698,7 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
     work.clear();
     auto lane_of = [](const Seg& sg, int J0, int row0, int lo, int k, int base, int l) {
         const int W = sg.nown + 1;
-        int fl = 0;
+        int fl = W == 32 ? LF_BULK : 0;   // full segments leave through TMA bulk copies
         if (l > lo) fl |= LF_OWNX;
         if (l == lo + W - 1) fl |= LF_XPLUS;
         if (row0) fl |= LF_ROW0;
@@ -708,7 +710,7 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
     for (auto& b : bands)
         for (auto& sg : full) {
             for (int l = 0; l < 32; l++) lanes.push_back(lane_of(sg, b.first, b.second, 0, 0, 0, l));
-            work.push_back(16 * rows_of(b.first));
+            work.push_back(lat_cost(rows_of(b.first), b.second));
         }
     if (!shortv.empty()) {
         // at most one short segment per band (the last one), all of the same width
@@ -717,16 +719,19 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
         for (size_t b0 = 0; b0 < bands.size(); b0 += per) {
             int4 t[32];
             for (int l = 0; l < 32; l++) t[l] = idle;
-            int base = 0, rows = 0;
+            int end = 0, rows = 0;
             for (int k = 0; k < per && b0 + k < bands.size(); k++) {
                 const int lo = k * W;
+                // staging base = -lo - 1 (mod 16), so that the rows of the lanes of a half warp (15 doubles
+                // apart) start in distinct bank pairs (packed tiles store with plain coalesced stores)
+                const int base = end + ((16 - ((end + lo + 1) & 15)) & 15);
                 for (int l = lo; l < lo + W; l++)
                     t[l] = lane_of(shortv[0], bands[b0 + k].first, bands[b0 + k].second, lo, k, base, l);
-                base += (15 * shortv[0].nown + 3) & ~1;   // even: 16-byte aligned staging bodies
+                end = base + 15 * shortv[0].nown + 1;
                 rows = std::max(rows, rows_of(bands[b0 + k].first));
             }
             for (int l = 0; l < 32; l++) lanes.push_back(t[l]);
-            work.push_back(VB_LAT_PACKW * rows);   // several segments: more bulk copies per step
+            work.push_back(lat_cost(rows, b0 == 0) * 36 / 25);   // several segments per warp: ~1.44x a full tile
         }
     }
     T = (int)(lanes.size() / 32);

@@ -6,6 +6,7 @@ import sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+SORT_STALL = len(sys.argv) > 3 and sys.argv[3] == "stall"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(out.splitlines()))
@@ -37,5 +38,5 @@ for r in rows[start:]:
     stalls[cur] += int(r[4] or 0)
 tot = sum(per.values())
 print("total", tot, "stall samples", sum(stalls.values()))
-for k, v in sorted(per.items(), key=lambda x: -x[1])[:top]:
+for k, v in sorted(per.items(), key=lambda x: -(stalls[x[0]] if SORT_STALL else x[1]))[:top]:
     print("%4d %6.2f%% st%5d %-60s %s" % (k[0], 100 * v / tot, stalls[k], k[1][:60], dict(ops[k].most_common(4))))
