@@ -677,7 +677,13 @@ uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz) {
 // Relative cost of one tile-layer (measured, B200, per-CTA clock64 of the VB_LAT_PROF build): a fixed
 // part (barriers, latencies) and a part per warp row holding nodes; a band without a halo row owns
 // all its rows (one more row of output, the boundary row J = 0).
-int lat_cost(int rows, int row0_owned) { return 200 + 39 * rows + (row0_owned ? 39 : 0); }
+// A tile whose segment holds x = 0 or x = nx runs the masked cell path (absent cells) and the boundary
+// row path in every warp: ~1.11x.  Packed tiles: ~1 + 0.05 (segments - 1)^2 more (per-segment store
+// passes; 5 segments measured at 1.8x).
+int lat_cost(int rows, int row0_owned, int xbnd = 0, int nseg = 1) {
+    const int c = 200 + 39 * rows + (row0_owned ? 39 : 0);
+    return c * (xbnd ? 111 : 100) * (100 + 5 * (nseg - 1) * (nseg - 1)) / 10000;
+}
 
 // Tiles of 32 lanes.  x segments: a halo lane and 31 owned nodes (segment 0's halo is the virtual
 // node x = -1); y bands of LR rows (the first owns LR lines, the next a halo line + LR - 1).  The
@@ -710,7 +716,7 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
     for (auto& b : bands)
         for (auto& sg : full) {
             for (int l = 0; l < 32; l++) lanes.push_back(lane_of(sg, b.first, b.second, 0, 0, 0, l));
-            work.push_back(lat_cost(rows_of(b.first), b.second));
+            work.push_back(lat_cost(rows_of(b.first), b.second, sg.I0 < 0 || sg.I0 + sg.nown >= nx));
         }
     if (!shortv.empty()) {
         // at most one short segment per band (the last one), all of the same width
@@ -731,7 +737,8 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
                 rows = std::max(rows, rows_of(bands[b0 + k].first));
             }
             for (int l = 0; l < 32; l++) lanes.push_back(t[l]);
-            work.push_back(lat_cost(rows, b0 == 0) * 36 / 25);   // several segments per warp: ~1.44x a full tile
+            const int nseg = (int)std::min<size_t>(per, bands.size() - b0);
+            work.push_back(lat_cost(rows, b0 == 0, 1, nseg));
         }
     }
     T = (int)(lanes.size() / 32);
