@@ -13,11 +13,14 @@ API from pinned host buffers: H2D of coords+elems, fem_p1_pattern (both
 phases), fem_p1_assemble, D2H of row_ptr, col_idx, K and M -- every step.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl vb|reference]
-       [--variant class|block|atomic] [--quick]
-Variants of the numeric phase: "class" (default; deterministic gather over the
-row classes of the plan, fem_p1_assemble_classes), "block" (deterministic gather
-over 32-row blocks, fem_p1_assemble VB_ASSEMBLE_GATHER), "atomic" (fp64 atomics
-through the scatter map, VB_ASSEMBLE_ATOMIC).
+       [--variant lattice|class|block|tile|atomic] [--quick]
+Variants of the numeric phase: "lattice" (default; element-once assembly on the
+verified Kuhn-lattice plan, fem_p1_assemble_lattice: each tet evaluated once,
+no connectivity read in the numeric phase), "class" (deterministic gather over
+the row classes of the plan, fem_p1_assemble_classes), "block" (deterministic
+gather over 32-row blocks, fem_p1_assemble VB_ASSEMBLE_GATHER), "tile"
+(element-once over Morton tiles), "atomic" (fp64 atomics through the scatter
+map, VB_ASSEMBLE_ATOMIC).
 Multi-GPU (torchrun): one independent replica of the workload per rank
 ("replicas only"), weak scaling, max-over-ranks time.
 """
@@ -131,8 +134,27 @@ def alg_bytes_assembly(dim, nn, ne, nnz):
 
 
 def design_bytes_assembly(dim, nn, ne, nnz):
-    """ALG + the nv^2 int32 element-to-nnz scatter map of the north-star design."""
+    """ALG + the nv^2 int32 element-to-nnz scatter map of the north-star design (atomic variant only)."""
     return alg_bytes_assembly(dim, nn, ne, nnz) + ne * (dim + 1) ** 2 * 4
+
+
+def lattice_bytes_assembly(dim, nn, nnz):
+    """What the lattice kernel must move: coords + row_ptr read, K and M written once (the element list
+    is implicit in the verified lattice plan, so no connectivity is read per assembly)."""
+    return nn * dim * 8 + (nn + 1) * 4 + 2 * nnz * 8
+
+
+def fp64_peak():
+    """Measured DFMA peak (TFLOP/s, FMA = 2 flops) from the committed microbenchmark (tools/microbench/mb.cu)."""
+    path = os.path.join(ROOT, "profiles", "r02", "microbench_r02a.jsonl")
+    try:
+        for line in open(path):
+            d = json.loads(line)
+            if d.get("bench") == "dfma":
+                return float(d["TFLOPs"]), "measured (profiles/r02/microbench_r02a.jsonl, tools/microbench/mb.cu)"
+    except Exception:
+        pass
+    return 37.0, "nominal (B200 FP64 vector)"
 
 
 def load_traffic(kernel_key):
@@ -156,6 +178,17 @@ def load_traffic(kernel_key):
         return None
 
 
+def fp64_flops_per_launch(kernel_key):
+    """FP64 flops per launch of a kernel from the committed ncu SASS counts (DFMA = 2), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            k = json.load(f)["kernels"][kernel_key]
+        return 2 * k["dfma"] * 32 + (k["dadd"] + k["dmul"]) * 32
+    except Exception:
+        return None
+
+
 # ---------------------------------------------------------------------- vb arm
 def run_vb(args):
     import torch
@@ -172,6 +205,7 @@ def run_vb(args):
     peak, peak_src = peaks()
     mode = vb.VB_ASSEMBLE_ATOMIC if args.variant == "atomic" else vb.VB_ASSEMBLE_GATHER
     gvar = args.variant if args.variant != "atomic" else None
+    lattice = gvar == "lattice"
 
     coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
     dim, nn = coords.shape
@@ -184,7 +218,9 @@ def run_vb(args):
     # count phase has a documented nnz read-back)
     def build_plan():
         p = vb.P1Plan(ed, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
-                      gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+                      gather_plan=(mode == vb.VB_ASSEMBLE_GATHER and not lattice))
+        if lattice and not p.lattice(ed):   # verified Kuhn-lattice plan (part of this variant's plan)
+            raise RuntimeError("lattice plan refused: " + p.lattice_reason)
         if gvar == "class":
             p.classes()    # the row classes are part of this variant's plan
         if gvar == "tile" and not p.tiles(cd, ed):   # the tile plan is part of this variant's plan
@@ -233,15 +269,31 @@ def run_vb(args):
     avg_launch_ms = statistics.mean(launch_ms)
     alg = alg_bytes_assembly(dim, nn, ne, nnz)
     achieved = alg / (avg_launch_ms * 1e-3) / 1e9
-    kname = {"class": "assemble_class_k<3>", "block": "assemble_gather_k<3>",
+    kname = {"lattice": "assemble_lattice_k<0, 0>", "class": "assemble_class_k<3>", "block": "assemble_gather_k<3>",
              "tile": "assemble_tile_k<3>"}.get(gvar, "assemble_atomic_k<3>")
     traffic = load_traffic(kname)
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": traffic,
-            "kernel": kname, "bytes_model": "ALG: coords read + elems read + K,M written once "
+            "kernel": kname, "bytes_model": "ALG (SURVEY 8(d)): coords read + elems read + K,M written once "
                                               "(%.1f MB/launch = %.1f B/tet)" % (alg / 1e6, alg / ne),
-            "peak_source": peak_src, "launch_ms_avg": round(avg_launch_ms, 5),
-            "design_bytes_frac": round(design_bytes_assembly(dim, nn, ne, nnz) / (avg_launch_ms * 1e-3) / 1e9 / peak, 4)}
+            "peak_source": peak_src, "launch_ms_avg": round(avg_launch_ms, 5)}
+    if lattice:
+        kb = lattice_bytes_assembly(dim, nn, nnz)
+        roof["kernel_bytes"] = kb
+        roof["kernel_bytes_frac"] = round(kb / (avg_launch_ms * 1e-3) / 1e9 / peak, 4)
+        roof["kernel_bytes_model"] = ("what the lattice kernel must move: coords + row_ptr read, K,M written once "
+                                      "(%.1f MB; the element list is implicit in the verified lattice plan)" % (kb / 1e6))
+        # FP64 work of the element-once path: 12 cross products, 6 determinants, 6 reciprocals (2 Newton steps),
+        # 36 dot products per cell (SASS count, profiles/r02): ~1.42 GFLOP per launch (DFMA = 2 flops)
+        flops = fp64_flops_per_launch(kname)
+        if flops:
+            fpk, fsrc = fp64_peak()
+            roof["fp64"] = {"achieved_tflops": round(flops / (avg_launch_ms * 1e-3) / 1e12, 2), "peak_tflops": fpk,
+                            "frac": round(flops / (avg_launch_ms * 1e-3) / 1e12 / fpk, 4), "peak_source": fsrc,
+                            "flops_per_launch": flops, "source": "ncu SASS counts (profiles/ncu_summary.json)"}
+    if mode == vb.VB_ASSEMBLE_ATOMIC:
+        roof["design_bytes_frac"] = round(design_bytes_assembly(dim, nn, ne, nnz) / (avg_launch_ms * 1e-3) / 1e9 /
+                                          peak, 4)
 
     # e2e through the public API from pinned host buffers
     e2e = None
@@ -283,7 +335,7 @@ def run_vb(args):
             o = outs[j]
             with torch.cuda.stream(s):
                 p2 = vb.P1Plan(e2, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
-                               gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+                               gather_plan=(mode == vb.VB_ASSEMBLE_GATHER and not lattice))
                 K2, M2, _, _ = vb.fem_p1_assemble(c2, e2, p2, mode=mode, variant=gvar)
                 done = torch.cuda.Event()
                 done.record(s)
@@ -314,7 +366,7 @@ def run_vb(args):
                "h2d_bytes_per_step": coords.nbytes + elems.nbytes,
                "d2h_bytes_per_step": (nn + 1) * 4 + nnz * 4 + 2 * nnz * 8,
                "steps": n_e2e, "ms_per_step": e2e_ms / n_e2e,
-               "includes": "per step: H2D coords+elems from pinned memory, fem_p1_pattern (count+fill), "
+               "includes": "per step: H2D coords+elems from pinned memory, fem_p1_pattern (count+fill), fem_plan_lattice (lattice variant: verifies the mesh and pattern), "
                            "fem_plan_classes (class variant) / fem_plan_tiles (tile variant), the assembly, D2H row_ptr/col_idx/K/M to pinned memory; upload / 2 compute / "
                            "download streams, host wall clock with device syncs on both sides"}
 
@@ -336,8 +388,8 @@ def run_vb(args):
         "dtype": "f64", "data": "synthetic (seeded Kuhn-cube mesh, synth/)",
         "config": {"workload": WORKLOAD5, "variant": args.variant,
                    "timed": "one numeric K+M assembly per step on the resident plan (%s)" % (
-                       {"class": "fem_p1_assemble_classes", "tile": "fem_p1_assemble_tiles"}.get(
-                           gvar, "fem_p1_assemble")),
+                       {"lattice": "fem_p1_assemble_lattice", "class": "fem_p1_assemble_classes",
+                        "tile": "fem_p1_assemble_tiles"}.get(gvar, "fem_p1_assemble")),
                    "pattern_ms": round(pattern_ms, 3), "nnz": nnz, "ne": ne, "nn": nn,
                    "l2": "no flush: every step streams %.0f MB (> 126 MB L2)" % (alg / 1e6),
                    "parallelism": "replicas" if ws > 1 else "single GPU"},
@@ -385,7 +437,7 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
 
     # the other assembly variants on config 5
     nn5, ne5 = coords5.shape[1], elems5.shape[1]
-    for other in ("class", "block", "tile", "atomic"):
+    for other in ("lattice", "class", "block", "tile", "atomic"):
         if other == args.variant:
             continue
         p_other = vb.P1Plan(ed5, nn5, scatter_map=(other == "atomic"), gather_plan=(other != "atomic"))
@@ -648,7 +700,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="vb", choices=["vb", "reference"])
-    ap.add_argument("--variant", default="class", choices=["class", "block", "tile", "gather", "atomic"],
+    ap.add_argument("--variant", default="lattice", choices=["lattice", "class", "block", "tile", "gather", "atomic"],
                     help="gather = block (older name)")
     ap.add_argument("--quick", action="store_true", help="headline only (no secondary rows)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -339,6 +339,53 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
                                        const int32_t* tile_colors, const uint32_t* tile_elems, int nloc_max,
                                        int elems_max, double* K_vals, double* M_vals, vb_stream_t stream);
 
+/* ---------------------------------------------------------- Kuhn-lattice (element-once) variant
+ * The same K, M (c = 1; eq:K_M P:967-975, stiffness_matrixP1 P:978-1004,
+ * mass_matrixP1 P:1007, K_e = |T| G^T G with G = tjac^{-1} D from phider
+ * P:929-947, accumulated as sparse(X3D(:),Y3D(:),..) P:1001-1003) for meshes
+ * that are Kuhn lattices: nodes (i, j, k), 0 <= i <= nx, 0 <= j <= ny,
+ * 0 <= k <= nz, numbered id = i + (nx+1)(j + (ny+1)k) (coordinates arbitrary,
+ * e.g. jittered), every cell split into the 6 tetrahedra of the monotone paths
+ * along one of its 4 diagonals (the same diagonal in every cell; element order
+ * and vertex order inside an element are free) -- the paper's unit-cube meshes
+ * and BASELINE configs[4].
+ *
+ * fem_plan_lattice verifies this ONCE per mesh on the GPU: every element is a
+ * Kuhn tetrahedron of the nx x ny x nz lattice, no two elements are the same
+ * tetrahedron (so the ne = 6 nx ny nz elements are exactly the lattice's), and
+ * row_ptr/col_idx (from fem_p1_pattern) is the lattice stencil (15 columns in
+ * the interior).  It writes the plan (caller-owned DEVICE int32 array of
+ * *plan_ints entries, 16-byte aligned: a token, the dims and the kernel's tile
+ * descriptors) and reports in stats_out (HOST, 4 int64): [0] 1 if the mesh is
+ * such a lattice (else 0 and nothing may be assembled with the plan), [1] the
+ * number of tiles, [2] the refusal reason (1 counts, 2 element 0, 3 nx or
+ * ny < 2 or degenerate ordering, 4 an element, 5 the pattern), [3] the
+ * orientation flags to pass to fem_p1_assemble_lattice.  work: DEVICE scratch
+ * (ne/8 + 256 bytes); work == NULL queries *work_bytes and *plan_ints.
+ * Synchronises the stream (small read-backs).  Refusal is not an error.
+ *
+ * fem_p1_assemble_lattice then reads no connectivity at all: one CTA per SM
+ * marches along z through tiles of 32 x 12 lattice columns and evaluates every
+ * tetrahedron ONCE (the row-owner variants evaluate it once per vertex);
+ * contributions reach the owning rows by warp shuffles, shared memory and
+ * registers; rows are assembled on chip (diagonals by the partition of unity,
+ * K_pp = -sum_{q != p} K_pq, M_pp = (2/3) sum_{q != p} M_pq, reading "new" in
+ * DESIGN.md §4) and written once (TMA bulk copies when K, M are 16-byte
+ * aligned).  Deterministic: bitwise reproducible run to run.  Arguments: nx,
+ * ny, nz and flips as planned (stats_out[3]), coords strided as in
+ * vb_create_coords3D, row_ptr of the planned pattern, nnz, K_vals / M_vals
+ * (nnz each, nullable; overwritten).  VB_ERR_ARG for NULL coords / row_ptr /
+ * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2.  A plan of another mesh (token
+ * mismatch) makes the kernel write nothing. */
+VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
+                                  const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz, int nx, int ny,
+                                  int nz, void* work, size_t* work_bytes, int32_t* plan, int64_t* plan_ints,
+                                  int64_t* stats_out, vb_stream_t stream);
+VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* coords, int64_t node_stride,
+                                         int64_t comp_stride, const int32_t* row_ptr, int64_t nnz,
+                                         const int32_t* plan, int nx, int ny, int nz, int flips, double* K_vals,
+                                         double* M_vals, vb_stream_t stream);
+
 /* ---------------------------------------------------------- exact-order check
  * The verification path of SURVEY §8(c) ("bitwise mode"): K and M (c = 1) with
  * every operation of the definition as an IEEE round-to-nearest fp64

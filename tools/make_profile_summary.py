@@ -48,6 +48,27 @@ def ncu_csv(args):
     return list(csv.reader(io.StringIO(out)))
 
 
+def sass_fp64_counts(rep):
+    """Executed warp instructions of DFMA / DADD / DMUL (SASS source page) of a single-kernel report."""
+    rows = ncu_csv(["-i", rep, "--page", "source", "--print-source=sass"])
+    try:
+        hdr = next(r for r in rows if "Instructions Executed" in r)
+    except StopIteration:
+        return None
+    i_src, i_ex = hdr.index("Source"), hdr.index("Instructions Executed")
+    out = {"dfma": 0, "dadd": 0, "dmul": 0}
+    for r in rows[rows.index(hdr) + 1:]:
+        try:
+            n = int(r[i_ex])
+        except (ValueError, IndexError):
+            continue
+        t = r[i_src].split()
+        op = (t[1] if t and t[0].startswith("@") else (t[0] if t else "")).split(".")[0].lower()
+        if op in out:
+            out[op] += n
+    return out
+
+
 def summarise_rep(rep, tag, outdir):
     rows = ncu_csv(["-i", rep, "--page", "raw"])
     hdr, units = rows[0], rows[1]
@@ -76,6 +97,9 @@ def summarise_rep(rep, tag, outdir):
         wr = float(vals["dram__bytes_write.sum"].replace(",", "")) * unit_scale[units[hdr.index("dram__bytes_write.sum")]]
         result[short] = {"dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                          "duration": vals.get("gpu__time_duration.sum"), "tag": tag}
+        ops = sass_fp64_counts(rep)
+        if ops:
+            result[short].update(ops)   # warp-level DFMA / DADD / DMUL executed (x 32 lanes ~ thread ops)
         with open(os.path.join(outdir, "%s_%s.md" % (re.sub(r"[^A-Za-z0-9_]+", "_", short).strip("_"), tag)), "w") as f:
             f.write("\n".join(lines) + "\n")
     return result
