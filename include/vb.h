@@ -65,7 +65,7 @@ typedef enum {
 
 /* Message of the last failing call on this host thread ("" if none). */
 VB_API const char* vb_last_error(void);
-/* ABI version, currently 1. */
+/* ABI version, currently 2 (work / degenerate arguments of the assembly calls). */
 VB_API int vb_abi_version(void);
 
 /* ---------------------------------------------------------- a1 page product
@@ -173,9 +173,14 @@ VB_API vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_ld, 
  *     byte 0 = offset of v itself (the diagonal), bytes 1..nv-1 = offsets of
  *     the element's other vertices elems[b][e], b != a, in ascending b (so
  *     rows must have <= 255 entries; VB_ERR_UNSUPPORTED otherwise).
+ * Validation mode: dim | VB_PATTERN_VALIDATE checks every vertex id against
+ *   [0, nn) before anything else (one more read-back) and returns VB_ERR_ARG
+ *   naming the first offending element and vertex (without it, out-of-range
+ *   ids are a precondition violation, not checked).
  * Errors: VB_ERR_OVERFLOW if nnz >= 2^31 or ne*nv*nv >= 2^31 or ne >= 2^29;
  *   VB_ERR_UNSUPPORTED if a row has more than 4096 distinct columns;
  *   VB_ERR_ARG if col_cap < nnz.  Deterministic: identical outputs every run. */
+#define VB_PATTERN_VALIDATE 0x100
 VB_API vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne,
                          const int32_t* elems, int64_t elem_ld,
                          void* work, size_t* work_bytes,
@@ -251,7 +256,17 @@ VB_API vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_ptr, c
  * K_local / M_local (nullable): K3D / M3D page arrays (nv x nv pages, ld = ne),
  *   the second outputs of stiffness_matrixP1 / mass_matrixP1.
  * coords strided as in vb_create_coords3D.
- * Degenerate elements (det = 0) propagate inf/nan. */
+ * work (DEVICE, caller-owned, 16-byte aligned, >= *work_bytes = 16 bytes):
+ *   holds this launch's block counter of the gather kernels' dynamic schedule
+ *   (zeroed in-stream by the call), so concurrent calls on different streams
+ *   are independent when each has its own work buffer.  work == NULL with
+ *   work_bytes != NULL is a size query (nothing else happens); work == NULL
+ *   with work_bytes == NULL runs the static block schedule (no counter).
+ * degenerate (nullable DEVICE int64): receives the number of elements with
+ *   det tjac = 0 (outside the domain of inverse_W; tjac rows
+ *   x_{r+1} - x_0, det by cofactor expansion along row 0) -- an extra pass
+ *   over the elements when requested.  Degenerate elements still propagate
+ *   inf/nan into K/M (IEEE; not an error code). */
 #define VB_ASSEMBLE_ATOMIC 0
 #define VB_ASSEMBLE_GATHER 1
 /* Hint OR'ed into a gather mode (3D; ignored otherwise): every 32-row block of
@@ -271,22 +286,27 @@ VB_API vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne,
                           const uint32_t* node_elem_slot,
                           double* K_vals, double* M_vals,
                           double* K_local, double* M_local,
-                          int mode, vb_stream_t stream);
+                          int mode, void* work, size_t* work_bytes, int64_t* degenerate,
+                          vb_stream_t stream);
 
-/* The gather variant of fem_p1_assemble (c_K = c_M = 1; same arithmetic,
- * ownership and summation order: ascending element per entry, diagonal from
- * the partition of unity) driven by the row classes of fem_plan_classes: a warp
+/* The gather variant of fem_p1_assemble (c_K = c_M = 1; same arithmetic and
+ * ownership, diagonal from the partition of unity) driven by the row classes of fem_plan_classes: a warp
  * takes one group (<= 32 rows of one class) and keeps each row's K and M sums
  * in registers.  Rows of the mixed class are assembled in place in HBM.
  * Arguments as fem_p1_assemble (node_elem_slot: the 32-bit plan words) plus
  * class_rows, groups, ngroups from fem_plan_classes on the same plan.
- * K_vals / M_vals (nnz, nullable) are overwritten.  Deterministic: the same
- * bits as every run of this call. */
+ * K_vals / M_vals (nnz, nullable) are overwritten.  work / work_bytes: the
+ * launch's group counter, as fem_p1_assemble (16 bytes; NULL, NULL: static
+ * group schedule).  Deterministic: the same bits as every run of this call
+ * (per entry, the order is ascending pair order of build_pairs: the two
+ * incidences of a pair are added together first, DESIGN.md §3.4 -- equal to
+ * fem_p1_assemble's ascending element order within rounding, not bitwise). */
 VB_API vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* coords, int64_t node_stride,
                                          int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx,
                                          int64_t nnz, const int32_t* node_elem_ptr, const uint32_t* node_elem_slot,
                                          const int32_t* class_rows, const int32_t* groups, int64_t ngroups,
-                                         double* K_vals, double* M_vals, vb_stream_t stream);
+                                         double* K_vals, double* M_vals, void* work, size_t* work_bytes,
+                                         vb_stream_t stream);
 
 /* ---------------------------------------------------------- tile variant
  * Element-once deterministic assembly (same K, M as fem_p1_assemble, c = 1:
@@ -374,7 +394,9 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
  * aligned).  Deterministic: bitwise reproducible run to run.  Arguments: nx,
  * ny, nz and flips as planned (stats_out[3]), coords strided as in
  * vb_create_coords3D, row_ptr of the planned pattern, nnz, K_vals / M_vals
- * (nnz each, nullable; overwritten).  VB_ERR_ARG for NULL coords / row_ptr /
+ * (nnz each, nullable; overwritten), degenerate (nullable DEVICE int64: the
+ * number of tetrahedra with det = 0 as the kernel evaluates it, each counted
+ * once).  VB_ERR_ARG for NULL coords / row_ptr /
  * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2.  A plan of another mesh (token
  * mismatch) makes the kernel write nothing. */
 VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
@@ -384,7 +406,7 @@ VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32_t* elems, 
 VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* coords, int64_t node_stride,
                                          int64_t comp_stride, const int32_t* row_ptr, int64_t nnz,
                                          const int32_t* plan, int nx, int ny, int nz, int flips, double* K_vals,
-                                         double* M_vals, vb_stream_t stream);
+                                         double* M_vals, int64_t* degenerate, vb_stream_t stream);
 
 /* ---------------------------------------------------------- exact-order check
  * The verification path of SURVEY §8(c) ("bitwise mode"): K and M (c = 1) with
@@ -430,7 +452,8 @@ VB_API vb_status vb_gi(int64_t npages, int d, int nip, const double* fip, int64_
  *   K_e = sum_q w_q |det| c_K(x_q) G^T G,   M_e = sum_q w_q |det| c_M(x_q) phi_q phi_q^T,
  * gqo = 1 (centroid) or 2 (symmetric degree-2 rules: 3 points in 2D, 4 in 3D;
  * reading in DESIGN.md §4).  Both modes; in gather mode the diagonal of M is
- * the row sum of M_e (sum_b phi_b = 1) minus the off-diagonals.
+ * the row sum of M_e (sum_b phi_b = 1) minus the off-diagonals.  work,
+ * work_bytes, degenerate as fem_p1_assemble.
  * Errors as fem_p1_assemble, plus VB_ERR_UNSUPPORTED for other gqo. */
 VB_API vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne,
                           const double* coords, int64_t node_stride, int64_t comp_stride,
@@ -442,15 +465,16 @@ VB_API vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne,
                           int gqo, double cK_a, const double* cK_b, double cM_a, const double* cM_b,
                           double* K_vals, double* M_vals,
                           double* K_local, double* M_local,
-                          int mode, vb_stream_t stream);
+                          int mode, void* work, size_t* work_bytes, int64_t* degenerate,
+                          vb_stream_t stream);
 
 /* NEXT-1 through the row classes: fem_p1_assemble_classes with c_K = c_M =
  * c_a exp(c_b . x) (c_b: HOST array of dim doubles, NULL = 0) and the gqo = 2
  * rule of fem_p1_assemble_coef (Code stiff_scalar_P1 P:978-1004, the paper's
  * benchmark case P:1149-1176; c_b: dim doubles).  The coefficient at a
  * quadrature point is formed from per-node factors P = exp(beta c_b.x), R = exp((alpha - beta) c_b.x)
- * computed into work (DEVICE, 2 nn doubles, caller-owned) at the start of the
- * call.  gqo = 2 only (VB_ERR_UNSUPPORTED otherwise: use
+ * computed into work (DEVICE, 2 nn + 2 doubles, caller-owned, 16-byte aligned;
+ * the last 16 bytes hold the launch's group counter) at the start of the call.  gqo = 2 only (VB_ERR_UNSUPPORTED otherwise: use
  * fem_p1_assemble_coef).  Other arguments and guarantees as
  * fem_p1_assemble_classes. */
 VB_API vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const double* coords, int64_t node_stride,
@@ -495,8 +519,8 @@ VB_API vb_status vb_page_bilinear(int64_t npages, int n, int m, const double* A,
                                   double* s, vb_stream_t stream);
 
 /* ---------------------------------------------------------- NEXT-3: P2 elements
- * Topological CSR pattern (as fem_p1_pattern, same two phases, synchronisation
- * and work-buffer reuse) for elements with nv nodes, 2 <= nv <= 16 (P2: 6 in
+ * Topological CSR pattern (as fem_p1_pattern, same two phases, synchronisation,
+ * work-buffer reuse and validation flag, OR'ed into nv) for elements with nv nodes, 2 <= nv <= 16 (P2: 6 in
  * 2D, 10 in 3D; sparse() of P:1033-1036).  Requires ne < 2^27.  Optional plans:
  *   elem2nnz (nullable): the nv^2-plane element-to-nnz map (atomic scatter);
  *   node_elem_ptr (nn+1) / node_elem (nv*ne, packed e*16 + a, ascending e per

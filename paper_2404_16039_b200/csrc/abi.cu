@@ -1,5 +1,6 @@
 // ABI glue: error reporting, device queries and the device-wide scan used by
 // the pattern build ("built once on the GPU by sort/unique/scan").
+#include <atomic>
 #include <cstdarg>
 #include <cstring>
 
@@ -34,36 +35,62 @@ namespace {
 __global__ void read_small_k(const unsigned char* __restrict__ src, unsigned char* dst, int bytes) {
     for (int i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
 }
-struct MappedSlot {
+// One 4 KB pinned, mapped host buffer per device (64 slots of 64 bytes, taken and returned
+// with an atomic bitmap), allocated on first use and freed at process exit: the only
+// allocation of the library, bounded (not per host thread).  With all 64 slots busy a
+// read-back falls back to a plain copy.
+constexpr int RS_SLOTS = 64;
+struct MappedPool {
     unsigned char* h = nullptr;
     unsigned char* d = nullptr;
-    int dev = -1;
+    std::atomic<unsigned long long> busy{0};
+    std::atomic<int> state{0};   // 0 none, 1 initialising, 2 ready, 3 unavailable
+    ~MappedPool() {
+        if (h) cudaFreeHost(h);   // best effort at exit (the context may already be gone)
+    }
 };
+MappedPool g_pool[16];
+
+int take_slot(MappedPool& P) {
+    unsigned long long b = P.busy.load();
+    while (~b) {
+        const int i = __builtin_ctzll(~b);
+        if (P.busy.compare_exchange_weak(b, b | (1ull << i))) return i;
+    }
+    return -1;
+}
 }  // namespace
 
 vb_status read_small(cudaStream_t s, const void* src, size_t bytes, void* dst, const char* fn) {
-    thread_local MappedSlot slot;   // one 64-byte mapped buffer per host thread (per device)
     int dev = 0;
     cudaGetDevice(&dev);
     if (bytes > 64) { set_error("%s: read_small of %zu bytes", fn, bytes); return VB_ERR_ARG; }
-    if (slot.h && slot.dev != dev) { cudaFreeHost(slot.h); slot.h = slot.d = nullptr; }
-    if (!slot.h) {
-        if (cudaHostAlloc((void**)&slot.h, 64, cudaHostAllocMapped) != cudaSuccess ||
-            cudaHostGetDevicePointer((void**)&slot.d, slot.h, 0) != cudaSuccess) {
-            cudaGetLastError();
-            if (slot.h) cudaFreeHost(slot.h);
-            slot.h = slot.d = nullptr;
-        } else {
-            slot.dev = dev;
+    MappedPool* P = (dev >= 0 && dev < 16) ? &g_pool[dev] : nullptr;
+    if (P) {
+        int st = P->state.load();
+        if (st == 0 && P->state.compare_exchange_strong(st, 1)) {
+            if (cudaHostAlloc((void**)&P->h, 64 * RS_SLOTS, cudaHostAllocMapped) != cudaSuccess ||
+                cudaHostGetDevicePointer((void**)&P->d, P->h, 0) != cudaSuccess) {
+                cudaGetLastError();
+                if (P->h) cudaFreeHost(P->h);
+                P->h = P->d = nullptr;
+                P->state.store(3);
+            } else {
+                P->state.store(2);
+            }
+        }
+        while (P->state.load() == 1) {
         }
     }
+    const int slot = (P && P->state.load() == 2) ? take_slot(*P) : -1;
     cudaError_t e;
-    if (slot.h) {
-        read_small_k<<<1, 32, 0, s>>>(static_cast<const unsigned char*>(src), slot.d, (int)bytes);
+    if (slot >= 0) {
+        read_small_k<<<1, 32, 0, s>>>(static_cast<const unsigned char*>(src), P->d + 64 * slot, (int)bytes);
         e = cudaGetLastError();
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        if (e == cudaSuccess) memcpy(dst, (const void*)slot.h, bytes);
-    } else {   // no mapped memory: plain copy
+        if (e == cudaSuccess) memcpy(dst, (const void*)(P->h + 64 * slot), bytes);
+        P->busy.fetch_and(~(1ull << slot));
+    } else {   // no mapped memory (or all slots busy): plain copy
         e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     }
@@ -186,4 +213,4 @@ vb_status exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* t
 }  // namespace vb
 
 extern "C" const char* vb_last_error(void) { return vb::g_err; }
-extern "C" int vb_abi_version(void) { return 1; }
+extern "C" int vb_abi_version(void) { return 2; }

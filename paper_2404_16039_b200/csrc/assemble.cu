@@ -1141,10 +1141,10 @@ __global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) :
     // per group made the counter's atomics a hot spot)
     unsigned int pending = 0;
     int64_t stat = 0;
-    if (t == 0 && rounds <= 1) pending = atomicAdd(ctr, 1u);
+    if (t == 0 && rounds <= 1 && ctr) pending = atomicAdd(ctr, 1u);
     auto next_id = [&]() -> int64_t {
-        if (++stat < rounds) {
-            if (stat == rounds - 1 && t == 0) pending = atomicAdd(ctr, 1u);
+        if (++stat < rounds || !ctr) {   // ctr == NULL: static schedule throughout
+            if (stat == rounds - 1 && t == 0 && ctr) pending = atomicAdd(ctr, 1u);
             return (int64_t)blockIdx.x + stat * gridDim.x;
         }
         const unsigned int nx = __shfl_sync(FULL, pending, 0);
@@ -1573,6 +1573,36 @@ __global__ void __launch_bounds__(32, COEF ? (DIM == 2 ? VB_CLASS_MINBC2 : 10) :
     if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// Elements outside the domain of inverse_W (det tjac = 0, layeredInverse P:343-352): tjac rows
+// x_{r+1} - x_0, det by cofactor expansion along row 0; warp-aggregated count into *out.
+template <int DIM>
+__global__ void count_degenerate_k(int64_t ne, const double* __restrict__ coords, int64_t ns, int64_t cst,
+                                   const int32_t* __restrict__ elems, int64_t eld, int64_t* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t mine = 0;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+        double x[DIM + 1][DIM];
+#pragma unroll
+        for (int a = 0; a <= DIM; a++) {
+            const int64_t v = elems[a * eld + e];
+#pragma unroll
+            for (int c = 0; c < DIM; c++) x[a][c] = coords[c * cst + v * ns];
+        }
+        double J[DIM][DIM];
+#pragma unroll
+        for (int r = 0; r < DIM; r++)
+#pragma unroll
+            for (int c = 0; c < DIM; c++) J[r][c] = x[r + 1][c] - x[0][c];
+        double det;
+        if (DIM == 2) det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+        else det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
+                   J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
+        mine += det == 0.0;
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)mine);
+}
+
 }  // namespace
 }  // namespace vb
 
@@ -1580,32 +1610,13 @@ using namespace vb;
 
 namespace {
 
-// Per-launch block counters of the dynamic schedule: a ring of 64 device words,
-// one zeroed in-stream per launch (launches on different streams get different
-// words unless 64 are in flight at once).
-__device__ unsigned int g_gather_ctr[64];
-
-unsigned int* block_counter(cudaStream_t s) {
-    static std::atomic<unsigned int> seq{0};
-    static unsigned int* base[64] = {nullptr};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    if (!base[dev] && cudaGetSymbolAddress((void**)&base[dev], g_gather_ctr) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    unsigned int* c = base[dev] + (seq.fetch_add(1) & 63u);
-    if (cudaMemsetAsync(c, 0, sizeof(unsigned int), s) != cudaSuccess) return nullptr;
-    return c;
-}
-
 template <int DIM, bool COEF, bool FAC, int BUD>
 void launch_gather(unsigned g, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
                    const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const void* nslot,
-                   double* K, double* M, const CoefSpec& cp) {
+                   double* K, double* M, const CoefSpec& cp, unsigned int* ctr) {
     constexpr size_t SMEM = GatherCfg<DIM, FAC ? DIM + 2 : DIM, BUD>::SMEM;
     assemble_gather_k<DIM, COEF, FAC, BUD><<<g, GATHER_ROWS, SMEM, s>>>(nn, coords, ns, cst, row_ptr, col_idx, nptr,
-                                                                        nslot, K, M, cp, block_counter(s));
+                                                                        nslot, K, M, cp, ctr);
 }
 
 template <int DIM, bool COEF, bool FAC, int BUD>
@@ -1628,11 +1639,11 @@ int gather_ctas_per_sm() {
 template <int DIM, bool COEF, bool FAC, int BUD>
 vb_status run_gather(const char* fn, cudaStream_t s, int64_t nn, const double* coords, int64_t ns, int64_t cst,
                      const int32_t* row_ptr, const int32_t* col_idx, const int32_t* nptr, const void* nslot,
-                     double* K, double* M, const CoefSpec& cp) {
+                     double* K, double* M, const CoefSpec& cp, unsigned int* ctr) {
     const int64_t nblocks = (nn + GATHER_ROWS - 1) / GATHER_ROWS;
     const int64_t cap = (int64_t)sm_count() * gather_ctas_per_sm<DIM, COEF, FAC, BUD>();
     const unsigned g = (unsigned)(nblocks < cap ? nblocks : cap);
-    launch_gather<DIM, COEF, FAC, BUD>(g, s, nn, coords, ns, cst, row_ptr, col_idx, nptr, nslot, K, M, cp);
+    launch_gather<DIM, COEF, FAC, BUD>(g, s, nn, coords, ns, cst, row_ptr, col_idx, nptr, nslot, K, M, cp, ctr);
     return launch_check(fn);
 }
 
@@ -1643,18 +1654,30 @@ void launch_element(unsigned g, cudaStream_t s, int64_t ne, const double* coords
     assemble_atomic_k<DIM, COEF><<<g, 256, 0, s>>>(ne, coords, ns, cst, elems, eld, e2n, K, M, Kl, Ml, cp);
 }
 
+constexpr int ASSEMBLE_WORK_BYTES = 16;   // the launch's block counter (gather / class kernels)
+
 template <int DIM>
 vb_status assemble_impl(const char* fn, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
                         int64_t comp_stride, const int32_t* elems, int64_t elem_ld, const int32_t* row_ptr,
                         const int32_t* col_idx, int64_t nnz, const int32_t* elem2nnz, const int32_t* node_elem_ptr,
                         const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
-                        double* M_local, int mode, const CoefSpec* coef, cudaStream_t s) {
+                        double* M_local, int mode, const CoefSpec* coef, unsigned int* ctr, int64_t* degenerate,
+                        cudaStream_t s) {
     const bool compact = (mode & VB_GATHER_HINT_COMPACT) != 0;
     mode &= ~VB_GATHER_HINT_COMPACT;
     const bool want_global = K_vals || M_vals;
     const CoefSpec cp = coef ? *coef : CoefSpec{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
     const bool C = coef != nullptr;
     vb_status st = VB_OK;
+    if (degenerate) {   // elements outside the domain of inverse_W (det = 0), counted first
+        cudaError_t e = cudaMemsetAsync(degenerate, 0, sizeof(int64_t), s);
+        if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+        if (ne > 0) {
+            count_degenerate_k<DIM><<<grid_for(ne, 256, 8), 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems,
+                                                                         elem_ld, degenerate);
+            if ((st = launch_check(fn)) != VB_OK) return st;
+        }
+    }
     if (mode == VB_ASSEMBLE_ATOMIC) {
         if (want_global && (!elem2nnz || !row_ptr)) { set_error("%s: atomic mode needs elem2nnz and row_ptr", fn); return VB_ERR_ARG; }
         if (want_global && nnz > 0) {
@@ -1681,7 +1704,7 @@ vb_status assemble_impl(const char* fn, int64_t nn, int64_t ne, const double* co
         const bool cmp = compact && DIM == 3;
 #define VB_RUN_GATHER(CO, FA, BU) \
     run_gather<DIM, CO, FA, BU>(fn, s, nn, coords, node_stride, comp_stride, row_ptr, col_idx, node_elem_ptr, \
-                                node_elem_slot, K_vals, M_vals, cp)
+                                node_elem_slot, K_vals, M_vals, cp, ctr)
         if (fac) st = cmp ? VB_RUN_GATHER(true, true, 1) : VB_RUN_GATHER(true, true, 0);
         else if (C) st = cmp ? VB_RUN_GATHER(true, false, 1) : VB_RUN_GATHER(true, false, 0);
         else st = cmp ? VB_RUN_GATHER(false, false, 1) : VB_RUN_GATHER(false, false, 0);
@@ -1701,17 +1724,34 @@ vb_status assemble_entry(const char* fn, int dim, int64_t nn, int64_t ne, const 
                          int64_t comp_stride, const int32_t* elems, int64_t elem_ld, const int32_t* row_ptr,
                          const int32_t* col_idx, int64_t nnz, const int32_t* elem2nnz, const int32_t* node_elem_ptr,
                          const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
-                         double* M_local, int mode, const CoefSpec* coef, vb_stream_t stream) {
+                         double* M_local, int mode, const CoefSpec* coef, void* work, size_t* work_bytes,
+                         int64_t* degenerate, vb_stream_t stream) {
     clear_error();
+    if (!work && work_bytes) {   // size query (CUB convention): the launch's block counter
+        *work_bytes = ASSEMBLE_WORK_BYTES;
+        return VB_OK;
+    }
+    if (work && work_bytes && *work_bytes < ASSEMBLE_WORK_BYTES) {
+        set_error("%s: work_bytes %zu < %d", fn, *work_bytes, ASSEMBLE_WORK_BYTES);
+        return VB_ERR_WORKSPACE;
+    }
     if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
     if (nn < 0 || ne < 0 || nnz < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
     const int base_mode = mode & ~VB_GATHER_HINT_COMPACT;
     if (base_mode != VB_ASSEMBLE_ATOMIC && base_mode != VB_ASSEMBLE_GATHER) { set_error("%s: unknown mode %d", fn, mode); return VB_ERR_ARG; }
     if (ne > 0 && (!coords || !elems)) { set_error("%s: NULL %s", fn, !coords ? "coords" : "elems"); return VB_ERR_ARG; }
     if (elem_ld < ne) { set_error("%s: elem_ld < ne", fn); return VB_ERR_ARG; }
+    unsigned int* ctr = nullptr;   // NULL work: static block schedule
+    if (work) {
+        if (!aligned16(work)) { set_error("%s: work must be 16-byte aligned", fn); return VB_ERR_ARG; }
+        ctr = static_cast<unsigned int*>(work);
+        cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), cs(stream));
+        if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    }
     auto f = dim == 2 ? assemble_impl<2> : assemble_impl<3>;
     return f(fn, nn, ne, coords, node_stride, comp_stride, elems, elem_ld, row_ptr, col_idx, nnz, elem2nnz,
-             node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local, M_local, mode, coef, cs(stream));
+             node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local, M_local, mode, coef, ctr, degenerate,
+             cs(stream));
 }
 
 }  // namespace
@@ -1721,11 +1761,12 @@ extern "C" vb_status fem_p1_assemble(int dim, int64_t nn, int64_t ne, const doub
                                      const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
                                      const int32_t* elem2nnz, const int32_t* node_elem_ptr, const int32_t* node_elem,
                                      const uint32_t* node_elem_slot, double* K_vals, double* M_vals, double* K_local,
-                                     double* M_local, int mode, vb_stream_t stream) {
+                                     double* M_local, int mode, void* work, size_t* work_bytes,
+                                     int64_t* degenerate, vb_stream_t stream) {
     (void)node_elem;
     return assemble_entry("fem_p1_assemble", dim, nn, ne, coords, node_stride, comp_stride, elems, elem_ld, row_ptr,
                           col_idx, nnz, elem2nnz, node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local, M_local,
-                          mode, nullptr, stream);
+                          mode, nullptr, work, work_bytes, degenerate, stream);
 }
 
 extern "C" vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const double* coords, int64_t node_stride,
@@ -1735,7 +1776,7 @@ extern "C" vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const
                                           const int32_t* node_elem, const uint32_t* node_elem_slot, int gqo,
                                           double cK_a, const double* cK_b, double cM_a, const double* cM_b,
                                           double* K_vals, double* M_vals, double* K_local, double* M_local, int mode,
-                                          vb_stream_t stream) {
+                                          void* work, size_t* work_bytes, int64_t* degenerate, vb_stream_t stream) {
     (void)node_elem;
     clear_error();
     if (gqo != 1 && gqo != 2) { set_error("fem_p1_assemble_coef: gqo=%d, supported 1 and 2", gqo); return VB_ERR_UNSUPPORTED; }
@@ -1748,7 +1789,7 @@ extern "C" vb_status fem_p1_assemble_coef(int dim, int64_t nn, int64_t ne, const
     cp.same = cK_a == cM_a && cp.kb[0] == cp.mb[0] && cp.kb[1] == cp.mb[1] && cp.kb[2] == cp.mb[2];
     return assemble_entry("fem_p1_assemble_coef", dim, nn, ne, coords, node_stride, comp_stride, elems, elem_ld,
                           row_ptr, col_idx, nnz, elem2nnz, node_elem_ptr, node_elem_slot, K_vals, M_vals, K_local,
-                          M_local, mode, &cp, stream);
+                          M_local, mode, &cp, work, work_bytes, degenerate, stream);
 }
 
 namespace vb {
@@ -1805,7 +1846,7 @@ vb_status class_entry(const char* fn, int dim, int64_t nn, const double* coords,
                       int64_t comp_stride, const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz,
                       const int32_t* node_elem_ptr, const uint32_t* node_elem_slot, const int32_t* class_rows,
                       const int32_t* groups, int64_t ngroups, double* K_vals, double* M_vals, const CoefSpec* coef,
-                      double* fac, vb_stream_t stream) {
+                      double* fac, unsigned int* ctr, vb_stream_t stream) {
     if (dim != 2 && dim != 3) { set_error("%s: dim=%d, need 2 or 3", fn, dim); return VB_ERR_UNSUPPORTED; }
     if (nn < 0 || nnz < 0 || ngroups < 0) { set_error("%s: negative size", fn); return VB_ERR_ARG; }
     if (!K_vals && !M_vals) return VB_OK;
@@ -1815,8 +1856,10 @@ vb_status class_entry(const char* fn, int dim, int64_t nn, const double* coords,
     }
     if (ngroups == 0) return VB_OK;
     cudaStream_t s = cs(stream);
-    unsigned int* ctr = block_counter(s);
-    if (!ctr) { set_error("%s: block counter unavailable", fn); return VB_ERR_CUDA; }
+    if (ctr) {   // the caller's counter (work): zeroed in-stream, owned by this launch
+        cudaError_t e = cudaMemsetAsync(ctr, 0, sizeof(unsigned int), s);
+        if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    }
     // bulk (TMA) stores of contiguous groups need 16-byte aligned value arrays
     const bool bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
     const CoefSpec c1{1.0, {0, 0, 0}, 1.0, {0, 0, 0}, 2, true};
@@ -1862,11 +1905,20 @@ extern "C" vb_status fem_p1_assemble_classes(int dim, int64_t nn, const double* 
                                              int64_t nnz, const int32_t* node_elem_ptr,
                                              const uint32_t* node_elem_slot, const int32_t* class_rows,
                                              const int32_t* groups, int64_t ngroups, double* K_vals,
-                                             double* M_vals, vb_stream_t stream) {
+                                             double* M_vals, void* work, size_t* work_bytes, vb_stream_t stream) {
+    const char* fn = "fem_p1_assemble_classes";
     clear_error();
-    return class_entry("fem_p1_assemble_classes", dim, nn, coords, node_stride, comp_stride, row_ptr, col_idx, nnz,
-                       node_elem_ptr, node_elem_slot, class_rows, groups, ngroups, K_vals, M_vals, nullptr, nullptr,
-                       stream);
+    if (!work && work_bytes) {
+        *work_bytes = ASSEMBLE_WORK_BYTES;
+        return VB_OK;
+    }
+    if (work && ((work_bytes && *work_bytes < ASSEMBLE_WORK_BYTES) || !aligned16(work))) {
+        set_error("%s: work needs %d bytes, 16-byte aligned", fn, ASSEMBLE_WORK_BYTES);
+        return VB_ERR_WORKSPACE;
+    }
+    return class_entry(fn, dim, nn, coords, node_stride, comp_stride, row_ptr, col_idx, nnz, node_elem_ptr,
+                       node_elem_slot, class_rows, groups, ngroups, K_vals, M_vals, nullptr, nullptr,
+                       static_cast<unsigned int*>(work), stream);
 }
 
 extern "C" vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const double* coords, int64_t node_stride,
@@ -1884,7 +1936,9 @@ extern "C" vb_status fem_p1_assemble_classes_coef(int dim, int64_t nn, const dou
     }
     if (nn > 0 && (K_vals || M_vals) && !work) { set_error("%s: NULL work (2 nn doubles)", fn); return VB_ERR_ARG; }
     CoefSpec cp{c_a, {0, 0, 0}, c_a, {0, 0, 0}, 2, true};
-    for (int c = 0; c < 3; c++) cp.kb[c] = cp.mb[c] = c_b ? c_b[c] : 0.0;
+    for (int c = 0; c < dim; c++) cp.kb[c] = cp.mb[c] = c_b ? c_b[c] : 0.0;   // c_b holds dim doubles
+    // work: 2 nn factors, then the launch's block counter
     return class_entry(fn, dim, nn, coords, node_stride, comp_stride, row_ptr, col_idx, nnz, node_elem_ptr,
-                       node_elem_slot, class_rows, groups, ngroups, K_vals, M_vals, &cp, work, stream);
+                       node_elem_slot, class_rows, groups, ngroups, K_vals, M_vals, &cp, work,
+                       work ? reinterpret_cast<unsigned int*>(work + 2 * nn) : nullptr, stream);
 }

@@ -98,6 +98,7 @@ struct LatParams {
     const uint32_t* token;        // plan token (LAT_MAGIC ^ hash) written by fem_plan_lattice
     uint32_t want;
     int bulk;                     // K, M 16-byte aligned: rows leave as bulk copies
+    unsigned long long* degen;    // nullable: count of tetrahedra with det = 0 (owned cells, counted once)
     int range[LMAXCTA + 1];       // CTA c: tile-layers [range[c], range[c+1]) (cost-balanced)
 };
 
@@ -369,6 +370,13 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                 const bool live = cellxy && Lz < p.nz;   // the top layer has no cells (coordinates still finite)
                 if (__all_sync(0xffffffffu, live)) cell<false>(x0, x1, true, CK, CM);
                 else cell<true>(x0, x1, live, CK, CM);
+                if (p.degen) {   // |det|/120 of the six tets: CM.c100[0..1], o[0..1], c001[0..1]
+                    const int z = (CM.c100[0] == 0.0) + (CM.c100[1] == 0.0) + (CM.o[0] == 0.0) + (CM.o[1] == 0.0) +
+                                  (CM.c001[0] == 0.0) + (CM.c001[1] == 0.0);
+                    int cnt = (live && owned && out) ? z : 0;
+                    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+                    if (lane == 0 && cnt) atomicAdd(p.degen, (unsigned long long)cnt);
+                }
             }
             double eK[7], eM[7];
             eK[EX] = zcK0 + CK.e[0]; eK[EY] = zcK1 + CK.e[1]; eK[EXY] = zcK2 + CK.e[3];
@@ -865,7 +873,8 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
 extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* coords, int64_t node_stride,
                                                     int64_t comp_stride, const int32_t* row_ptr, int64_t nnz,
                                                     const int32_t* plan, int nx, int ny, int nz, int flips,
-                                                    double* K_vals, double* M_vals, vb_stream_t stream) {
+                                                    double* K_vals, double* M_vals, int64_t* degenerate,
+                                                    vb_stream_t stream) {
     const char* fn = "fem_p1_assemble_lattice";
     clear_error();
     if (nx < 1 || ny < 1 || nz < 1 || (int64_t)(nx + 1) * (ny + 1) * (nz + 1) != nn) {
@@ -877,7 +886,7 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
         return VB_ERR_ARG;
     }
     if (!aligned16(plan)) { set_error("%s: plan must be 16-byte aligned", fn); return VB_ERR_ARG; }
-    if (!K_vals && !M_vals) return VB_OK;
+    if (!K_vals && !M_vals && !degenerate) return VB_OK;
     const int fl[3] = {flips & 1, (flips >> 1) & 1, (flips >> 2) & 1};
     LatHost h;
     if (nx < 2 || ny < 2 || !lat_host(nx, ny, nz, fl, h)) {
@@ -899,6 +908,11 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     p.token = reinterpret_cast<const uint32_t*>(plan);
     p.want = lat_want(h, nn, nnz);
     p.bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
+    p.degen = reinterpret_cast<unsigned long long*>(degenerate);
+    if (degenerate) {
+        cudaError_t e = cudaMemsetAsync(degenerate, 0, sizeof(int64_t), cs(stream));
+        if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+    }
     int grid = std::min(sm_count() * VB_LAT_MINB, LMAXCTA);
     if (grid > p.L) grid = (int)p.L;
     lat_ranges(twork, nz, grid, p.range);

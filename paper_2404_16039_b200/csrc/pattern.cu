@@ -346,11 +346,26 @@ Work carve(void* base, int64_t nn, int64_t ne, int nv) {
 
 __global__ void write_stamp_k(Stamp* st, Stamp v) { *st = v; }
 
+// optional validation (VB_PATTERN_VALIDATE): the first (element, vertex) slot, as e * nv + a, whose id is
+// outside [0, nn) -> *first (initialised to INT64_MAX)
+__global__ void init_first_k(long long* first) { *first = 0x7fffffffffffffffll; }
+__global__ void validate_k(int64_t ne, int nv, int64_t nn, const int32_t* __restrict__ elems, int64_t eld,
+                           long long* __restrict__ first) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x)
+        for (int a = 0; a < nv; a++) {
+            const int32_t v = elems[a * eld + e];
+            if (v < 0 || v >= nn) {
+                atomicMin(first, (long long)(e * nv + a));
+                break;
+            }
+        }
+}
+
 template <int SH, int CAP, int BLOCK>
 vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
                        void* work, size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
                        int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem, uint32_t* node_elem_slot,
-                       int64_t* nnz_out, vb_stream_t stream) {
+                       int64_t* nnz_out, vb_stream_t stream, bool validate) {
     if (nn < 0 || ne < 0) { set_error("%s: negative nn or ne", fn); return VB_ERR_ARG; }
     if (ne >= (1ll << (31 - SH)) || (int64_t)nv * nv * ne >= (1ll << 31) || nn >= (1ll << 31) - 1) {
         set_error("%s: ne=%lld / nn=%lld too large for int32 plans", fn, (long long)ne, (long long)nn);
@@ -374,6 +389,22 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
     cudaStream_t s = cs(stream);
     const Stamp mine{STAMP_MAGIC, nn, ne, nv, elem_ld, elems, {0, 0}};
     vb_status st = VB_OK;
+    if (validate && ne > 0) {   // before any kernel indexes by vertex id (one read-back)
+        long long* first = reinterpret_cast<long long*>(w.total) + 1;
+        init_first_k<<<1, 1, 0, s>>>(first);
+        validate_k<<<grid_for(ne, 256, 8), 256, 0, s>>>(ne, nv, nn, elems, elem_ld, first);
+        if ((st = launch_check(fn)) != VB_OK) return st;
+        long long bad = 0;
+        if ((st = read_small(s, first, sizeof(bad), &bad, fn)) != VB_OK) return st;
+        if (bad != 0x7fffffffffffffffll) {
+            int32_t v = 0;
+            const int64_t e = bad / nv, a = bad % nv;
+            if ((st = read_small(s, elems + a * elem_ld + e, 4, &v, fn)) != VB_OK) return st;
+            set_error("%s: vertex %lld of element %lld is %d, outside [0, nn=%lld)", fn, (long long)a, (long long)e, v,
+                      (long long)nn);
+            return VB_ERR_ARG;
+        }
+    }
     unsigned gr = grid_for(nn, BLOCK, 4);
 
     // 1. node -> element incidences (into work; the fill phase reuses them)
@@ -452,10 +483,12 @@ extern "C" vb_status fem_p1_pattern(int dim, int64_t nn, int64_t ne, const int32
                                     int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem,
                                     uint32_t* node_elem_slot, int64_t* nnz_out, vb_stream_t stream) {
     clear_error();
+    const bool validate = (dim & VB_PATTERN_VALIDATE) != 0;
+    dim &= ~VB_PATTERN_VALIDATE;
     if (dim != 2 && dim != 3) { set_error("fem_p1_pattern: dim=%d, need 2 or 3", dim); return VB_ERR_UNSUPPORTED; }
     return pattern_impl<2, 64, 128>("fem_p1_pattern", dim + 1, nn, ne, elems, elem_ld, work, work_bytes, row_ptr,
                                     col_idx, col_cap, elem2nnz, node_elem_ptr, node_elem, node_elem_slot, nnz_out,
-                                    stream);
+                                    stream, validate);
 }
 
 extern "C" vb_status fem_pattern(int nv, int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld, void* work,
@@ -463,9 +496,12 @@ extern "C" vb_status fem_pattern(int nv, int64_t nn, int64_t ne, const int32_t* 
                                  int32_t* elem2nnz, int32_t* node_elem_ptr, int32_t* node_elem,
                                  uint32_t* node_elem_slot, int64_t* nnz_out, vb_stream_t stream) {
     clear_error();
+    const bool validate = (nv & VB_PATTERN_VALIDATE) != 0;
+    nv &= ~VB_PATTERN_VALIDATE;
     if (nv < 2 || nv > 16) { set_error("fem_pattern: nv=%d, need 2..16 nodes per element", nv); return VB_ERR_UNSUPPORTED; }
     return pattern_impl<4, 128, 64>("fem_pattern", nv, nn, ne, elems, elem_ld, work, work_bytes, row_ptr, col_idx,
-                                    col_cap, elem2nnz, node_elem_ptr, node_elem, node_elem_slot, nnz_out, stream);
+                                    col_cap, elem2nnz, node_elem_ptr, node_elem, node_elem_slot, nnz_out, stream,
+                                    validate);
 }
 
 // ------------------------------------------------------------------ plan statistics

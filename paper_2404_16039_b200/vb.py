@@ -81,16 +81,16 @@ def lib():
             "fem_p1_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p,
                                      C.POINTER(C.c_int64), p]),
             "fem_p1_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, p,
-                                      p, p, p, p, i32, p]),
+                                      p, p, p, p, i32, p, sz, p, p]),
             "fem_p1_assemble_coef": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, p,
-                                           i32, d, p, d, p, p, p, p, p, i32, p]),
+                                           i32, d, p, d, p, p, p, p, p, i32, p, sz, p, p]),
             "vb_quad_rule": (i32, [i32, i32, p, p]),
             "fem_p1_rhs": (i32, [i32, i64, i64, p, i64, i64, p, i64, i32, p, p, p, p, p, i32, p]),
             "vb_page_bilinear": (i32, [i64, i32, i32, p, i64, p, i64, p, i64, p, p]),
             "fem_plan_stats": (i32, [i64, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_plan_pack_slots": (i32, [i32, i64, p, p, p, p]),
             "fem_plan_classes": (i32, [i32, i64, p, p, p, p, sz, p, p, i64, C.POINTER(C.c_int64), p]),
-            "fem_p1_assemble_classes": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, p, p, p]),
+            "fem_p1_assemble_classes": (i32, [i32, i64, p, i64, i64, p, p, i64, p, p, p, p, i64, p, p, p, sz, p]),
             "fem_plan_tiles": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, p, sz, p, p, p, p, p, i64,
                                      C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_tiles": (i32, [i32, i64, p, i64, i64, i64, p, p, p, p, p, i32, i32, p, p, p]),
@@ -100,7 +100,7 @@ def lib():
             "vb_gi": (i32, [i64, i32, i32, p, i64, p, p, p, i64, p, p, sz, p]),
             "fem_plan_lattice": (i32, [i64, i64, p, i64, p, p, i64, i32, i32, i32, p, sz, p, C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int64), p]),
-            "fem_p1_assemble_lattice": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, i32, p, p, p]),
+            "fem_p1_assemble_lattice": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, i32, p, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -264,6 +264,16 @@ def vb_gi(fip, w, sizes, normals=None, value=None, work=None, stream=None):
 
 
 # ------------------------------------------------------------------ FEM P1
+def _work16(dev):
+    """A fresh 16-byte device buffer for one launch's block counter (the caller-owned work of the
+    assembly calls); torch's stream-ordered allocator keeps it private to this launch."""
+    return torch.empty((2,), dtype=torch.float64, device=dev)
+
+
+def _wb(n=16):
+    return C.byref(C.c_size_t(n))
+
+
 def _pad4(n):
     return max(4, (n + 3) // 4 * 4)
 
@@ -465,8 +475,9 @@ def fem_p1_assemble_tiles(coords, plan, K=None, M=None, want_K=True, want_M=True
     return K, M
 
 
-def fem_p1_assemble_lattice(coords, plan, K=None, M=None, want_K=True, want_M=True, stream=None):
-    """Element-once K, M on a Kuhn lattice (fem_p1_assemble_lattice); plan.lattice(elems) must be True."""
+def fem_p1_assemble_lattice(coords, plan, K=None, M=None, want_K=True, want_M=True, stream=None, degenerate=None):
+    """Element-once K, M on a Kuhn lattice (fem_p1_assemble_lattice); plan.lattice(elems) must be True.
+    degenerate: optional device int64 tensor (1,) receiving the number of tets with det = 0."""
     _f64(coords)
     dim, nn = coords.shape
     dev = coords.device
@@ -477,7 +488,7 @@ def fem_p1_assemble_lattice(coords, plan, K=None, M=None, want_K=True, want_M=Tr
     nx, ny, nz = plan.lattice_dims
     _check(lib().fem_p1_assemble_lattice(nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr), plan.nnz,
                                          _ptr(plan.lattice_plan), nx, ny, nz, plan.lattice_flips, _ptr(K), _ptr(M),
-                                         _stream(stream)))
+                                         _ptr(degenerate), _stream(stream)))
     return K, M
 
 
@@ -523,17 +534,21 @@ def fem_p1_assemble_classes(coords, plan, K=None, M=None, want_K=True, want_M=Tr
     K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
     M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
     plan.classes()
+    work = _work16(dev)
     _check(lib().fem_p1_assemble_classes(dim, nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr), _ptr(plan.col_idx),
                                          plan.nnz, _ptr(plan.node_elem_ptr), _ptr(plan.node_elem_slot),
                                          _ptr(plan.class_rows), _ptr(plan.groups), plan.groups.shape[0], _ptr(K),
-                                         _ptr(M), _stream(stream)))
+                                         _ptr(M), _ptr(work), _wb(), _stream(stream)))
     return K, M
 
 
 def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, want_M=True, want_local=False,
-                    K=None, M=None, stream=None, compact=None, variant=None):
+                    K=None, M=None, stream=None, compact=None, variant=None, degenerate=None):
     """Returns (K_vals, M_vals, K_local, M_local) (None where not requested).
-    Gather mode: `variant` as _use_classes."""
+    Gather mode: `variant` None (auto: lattice, else class / block as _use_classes),
+    "lattice", "class", "block" or "tile".  degenerate: optional device int64 tensor (1,)
+    receiving the number of elements with det = 0 (block / atomic calls; the lattice
+    kernel counts its tets; the class and tile kernels do not count)."""
     _f64(coords)
     dim, nn = coords.shape
     nv, ne = elems.shape
@@ -554,17 +569,18 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         if want_local:
             _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
                                          None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
-                                         _stream(stream)))
+                                         None, None, None, _stream(stream)))
         return K, M, Kl, Ml
     if variant == "tile":
         variant = "block"   # outside the tile variant's limits (plan.tile_reason)
     if (mode == VB_ASSEMBLE_GATHER and variant in (None, "lattice") and (K is not None or M is not None)
             and dim == 3 and plan.lattice(elems)):
-        fem_p1_assemble_lattice(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
+        fem_p1_assemble_lattice(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream,
+                                degenerate=degenerate)
         if want_local:
             _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
                                          None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
-                                         _stream(stream)))
+                                         None, None, None, _stream(stream)))
         return K, M, Kl, Ml
     if variant == "lattice":
         variant = None   # not a Kuhn lattice (plan.lattice_reason)
@@ -573,13 +589,14 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         if want_local:
             _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
                                          None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
-                                         _stream(stream)))
+                                         None, None, None, _stream(stream)))
         return K, M, Kl, Ml
     gmode, words = _gather_mode(mode, plan, compact)
+    work = _work16(dev)
     _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                  _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
                                  _ptr(plan.node_elem), _ptr(words), _ptr(K), _ptr(M), _ptr(Kl),
-                                 _ptr(Ml), gmode, _stream(stream)))
+                                 _ptr(Ml), gmode, _ptr(work), _wb(), _ptr(degenerate), _stream(stream)))
     return K, M, Kl, Ml
 
 
@@ -605,26 +622,27 @@ def fem_p1_assemble_coef(coords, elems, plan, gqo=2, cK=(1.0, (1.0, 1.0, 1.0)), 
     if (mode == VB_ASSEMBLE_GATHER and int(gqo) == 2 and same and (K is not None or M is not None)
             and variant != "tile" and _use_classes(plan, variant, coef=True)):
         plan.classes()
-        if getattr(plan, "fac_work", None) is None or plan.fac_work.numel() < 2 * nn:
-            plan.fac_work = torch.empty((max(2 * nn, 2),), dtype=torch.float64, device=dev)
+        fac_work = torch.empty((2 * nn + 2,), dtype=torch.float64, device=dev)   # factors + the group counter
         _check(lib().fem_p1_assemble_classes_coef(dim, nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr),
                                                   _ptr(plan.col_idx), plan.nnz, _ptr(plan.node_elem_ptr),
                                                   _ptr(plan.node_elem_slot), _ptr(plan.class_rows),
                                                   _ptr(plan.groups), plan.groups.shape[0], 2, float(cK[0]),
-                                                  C.cast(kb, C.c_void_p), _ptr(plan.fac_work), _ptr(K), _ptr(M),
+                                                  C.cast(kb, C.c_void_p), _ptr(fac_work), _ptr(K), _ptr(M),
                                                   _stream(stream)))
         if want_local:
             _check(lib().fem_p1_assemble_coef(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None,
                                               plan.nnz, None, None, None, None, int(gqo), float(cK[0]),
                                               C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), None,
-                                              None, _ptr(Kl), _ptr(Ml), int(mode), _stream(stream)))
+                                              None, _ptr(Kl), _ptr(Ml), int(mode), None, None, None,
+                                              _stream(stream)))
         return K, M, Kl, Ml
     gmode, words = _gather_mode(mode, plan, compact)
+    work = _work16(dev)
     _check(lib().fem_p1_assemble_coef(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(plan.row_ptr),
                                       _ptr(plan.col_idx), plan.nnz, _ptr(plan.elem2nnz), _ptr(plan.node_elem_ptr),
                                       _ptr(plan.node_elem), _ptr(words), int(gqo), float(cK[0]),
                                       C.cast(kb, C.c_void_p), float(cM[0]), C.cast(mb, C.c_void_p), _ptr(K), _ptr(M),
-                                      _ptr(Kl), _ptr(Ml), gmode, _stream(stream)))
+                                      _ptr(Kl), _ptr(Ml), gmode, _ptr(work), _wb(), None, _stream(stream)))
     return K, M, Kl, Ml
 
 

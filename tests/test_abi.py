@@ -39,7 +39,7 @@ def test_library_exports_every_declared_symbol(L):
         assert n in exported, n
         assert hasattr(L, n)
     assert set(vb.EXPORTS) == set(declared_symbols())
-    assert L.vb_abi_version() == 1
+    assert L.vb_abi_version() == 2
 
 
 def test_sm100a_code_only(L):
@@ -87,10 +87,48 @@ def test_fem_argument_errors(L):
                             None, None) == 0
     assert sz.value > small
     assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, None,
-                             None, None, 7, None) == -1
+                             None, None, 7, None, None, None, None) == -1
     assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, None,
-                             None, None, 0, None) == -1                     # atomic mode without elem2nnz
+                             None, None, 0, None, None, None, None) == -1   # atomic mode without elem2nnz
     assert b"elem2nnz" in L.vb_last_error()
+
+
+def test_assembly_work_convention(L):
+    """The launch's block counter lives in caller-owned work (vb.h, fem_p1_assemble): work == NULL with
+    work_bytes is a size query that does nothing else; a buffer smaller than queried is refused."""
+    assert L.vb_abi_version() == 2
+    sz = C.c_size_t(0)
+    assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, FAKE,
+                             None, None, 1, None, C.byref(sz), None, None) == 0
+    assert sz.value == 16
+    small = C.c_size_t(8)
+    assert L.fem_p1_assemble(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, FAKE, FAKE,
+                             None, None, 1, FAKE, C.byref(small), None, None) == -5
+    sz = C.c_size_t(0)
+    assert L.fem_p1_assemble_coef(3, 10, 10, FAKE, 1, 10, FAKE, 10, FAKE, FAKE, 5, None, None, None, None, 2, 1.0,
+                                  None, 1.0, None, FAKE, FAKE, None, None, 1, None, C.byref(sz), None, None) == 0
+    assert sz.value == 16
+    sz = C.c_size_t(0)
+    assert L.fem_p1_assemble_classes(3, 10, FAKE, 1, 10, FAKE, FAKE, 5, FAKE, FAKE, FAKE, FAKE, 1, FAKE, FAKE, None,
+                                     C.byref(sz), None) == 0
+    assert sz.value == 16
+    assert L.fem_p1_assemble_classes(3, 10, FAKE, 1, 10, FAKE, FAKE, 5, FAKE, FAKE, FAKE, FAKE, 1, FAKE, FAKE, FAKE,
+                                     C.byref(small), None) == -5
+
+
+def test_lattice_plan_query_and_argument_errors(L):
+    wb, pi = C.c_size_t(0), C.c_int64(0)
+    stats = (C.c_int64 * 4)()
+    # size query (no GPU): plan ints = header + 32 lane descriptors (int4) per tile
+    assert L.fem_plan_lattice(129 ** 3, 6 * 128 ** 3, None, 6 * 128 ** 3, None, None, 0, 128, 128, 128, None,
+                              C.byref(wb), None, C.byref(pi), stats, None) == 0
+    assert wb.value > 6 * 128 ** 3 // 8 and (pi.value - 16) % 128 == 0 and pi.value > 16
+    assert L.fem_plan_lattice(8, 6, None, 6, None, None, 0, 0, 1, 1, None, C.byref(wb), None, C.byref(pi), stats,
+                              None) == -1
+    # the assembly refuses inconsistent counts and lattices below the kernel's limits, before any CUDA call
+    assert L.fem_p1_assemble_lattice(9, FAKE, 1, 9, FAKE, 0, FAKE, 1, 1, 1, 0, FAKE, FAKE, None, None) == -1
+    assert L.fem_p1_assemble_lattice(18, FAKE, 1, 18, FAKE, 0, FAKE, 1, 2, 2, 0, FAKE, FAKE, None, None) == -1
+    assert b"nx, ny >= 2" in L.vb_last_error() or b"nn" in L.vb_last_error()
 
 
 def test_tile_and_exact_argument_errors(L):

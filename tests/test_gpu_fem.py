@@ -590,7 +590,8 @@ def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
         vb._check(L.fem_p1_assemble(dim, nn, ne, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(ebuf), eld,
                                     vb._ptr(plan.row_ptr), vb._ptr(plan.col_idx), plan.nnz, vb._ptr(plan.elem2nnz),
                                     vb._ptr(plan.node_elem_ptr), vb._ptr(plan.node_elem),
-                                    vb._ptr(plan.node_elem_slot), vb._ptr(K), vb._ptr(M), None, None, mode, None))
+                                    vb._ptr(plan.node_elem_slot), vb._ptr(K), vb._ptr(M), None, None, mode,
+                                    vb._ptr(vb._work16(dev)), vb._wb(), None, None))
         assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
     # the class variant with the same strided coordinates
     plan.classes()
@@ -599,19 +600,27 @@ def test_strided_coords_and_elem_ld_through_the_abi(dev, layout):
     vb._check(L.fem_p1_assemble_classes(dim, nn, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(plan.row_ptr),
                                         vb._ptr(plan.col_idx), plan.nnz, vb._ptr(plan.node_elem_ptr),
                                         vb._ptr(plan.node_elem_slot), vb._ptr(plan.class_rows), vb._ptr(plan.groups),
-                                        plan.groups.shape[0], vb._ptr(K), vb._ptr(M), None))
+                                        plan.groups.shape[0], vb._ptr(K), vb._ptr(M), vb._ptr(vb._work16(dev)),
+                                        vb._wb(), None))
     assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
     # the class coefficient path (its per-node factor pass reads the strided coordinates too)
     cb = (C.c_double * 3)(0.7, -0.4, 0.9)
     Kco, Mco = oracle.p1_assemble_coef(coords, elems, rp, ci, gqo=2, cK=(1.3, (0.7, -0.4, 0.9)),
                                        cM=(1.3, (0.7, -0.4, 0.9)))
-    work = torch.empty(2 * nn, dtype=torch.float64, device=dev)
+    work = torch.empty(2 * nn + 2, dtype=torch.float64, device=dev)   # factors + the group counter
     vb._check(L.fem_p1_assemble_classes_coef(dim, nn, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(plan.row_ptr),
                                              vb._ptr(plan.col_idx), plan.nnz, vb._ptr(plan.node_elem_ptr),
                                              vb._ptr(plan.node_elem_slot), vb._ptr(plan.class_rows),
                                              vb._ptr(plan.groups), plan.groups.shape[0], 2, 1.3, C.cast(cb, C.c_void_p),
                                              vb._ptr(work), vb._ptr(K), vb._ptr(M), None))
     assert relmax(h(K), Kco) <= 1e-12 and relmax(h(M), Mco) <= 1e-12
+    # the lattice variant with the same strided coordinates
+    lp = vb.P1Plan(g(elems, dev), nn, scatter_map=False, gather_plan=False)
+    assert lp.lattice(g(elems, dev))
+    vb._check(L.fem_p1_assemble_lattice(nn, vb._ptr(cbuf), node_stride, comp_stride, vb._ptr(lp.row_ptr), lp.nnz,
+                                        vb._ptr(lp.lattice_plan), 6, 6, 6, lp.lattice_flips, vb._ptr(K), vb._ptr(M),
+                                        None, None))
+    assert relmax(h(K), Ko) <= 1e-12 and relmax(h(M), Mo) <= 1e-12
 
 
 @pytest.mark.parametrize("mode", MODES, ids=MODE_IDS)

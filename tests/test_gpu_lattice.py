@@ -154,7 +154,7 @@ def test_lattice_plan_abi_errors(dev):
     stats = (C.c_int64 * 4)()
     assert L.fem_plan_lattice(8, 6, None, 6, None, None, 0, 0, 1, 1, None, C.byref(wb), None, C.byref(pi), stats,
                               None) == -1
-    assert L.fem_p1_assemble_lattice(9, None, 1, 9, None, 0, None, 1, 1, 1, 0, None, None, None) == -1
+    assert L.fem_p1_assemble_lattice(9, None, 1, 9, None, 0, None, 1, 1, 1, 0, None, None, None, None) == -1
 
 
 def test_full_size_configs4_every_entry_vs_oracle(dev):
