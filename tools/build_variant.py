@@ -1,10 +1,9 @@
 """Build an experimental libvb.so variant with extra nvcc defines into tools/variants/
 (A/B timing in one gpurun call: VB_LIBVB=tools/variants/<name>.so python bench.py ...).
 
-usage: python tools/build_variant.py <name> -DVB_GATHER_U=8 ...
+usage: python tools/build_variant.py <name> [--only lattice.cu,...] -DVB_LAT_R=10 ...
 """
 import os
-import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -12,8 +11,10 @@ sys.path.insert(0, ROOT)
 from paper_2404_16039_b200 import _build  # noqa: E402
 
 if __name__ == "__main__":
-    name, defines = sys.argv[1], sys.argv[2:]
+    name, args = sys.argv[1], sys.argv[2:]
+    only = None
+    if args[:1] == ["--only"]:
+        only, args = set(args[1].split(",")), args[2:]
     out = os.path.join(ROOT, "tools", "variants", name + ".so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
-    subprocess.check_call([_build.NVCC, *_build.FLAGS, *defines, "-o", out, *_build.sources()])
-    print(out)
+    print(_build.build(extra=args, out=out, only=only, objdir=os.path.join(_build.HERE, "build", "obj_" + name)))
