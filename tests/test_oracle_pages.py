@@ -196,6 +196,32 @@ def test_paper_normals_example(golden):
     assert np.max(np.abs(to_mats(normals)[0] - expect)) <= 1e-15
 
 
+def test_create_coords3D_paper_nodes_and_fancy_index(golden):
+    """coords3D(:, a, e) = coords(elems(e, a), :) (Code coords3D).  Pins: the paper's
+    tetrahedron N1..N4 gathered by the identity element gives back the node matrix, by a
+    permuted element the permuted node matrix; on random meshes numpy fancy indexing (independent of
+    the oracle's loops) gives every plane, and vectors3D = coords3D(:, a) - coords3D(:, end)."""
+    g = golden("paper_tet_example.json")
+    nodes = np.array(g["nodes"], dtype=np.float64)             # rows N1..N4
+    coords = np.ascontiguousarray(nodes.T)                      # (3, 4)
+    c3, _ = oracle.create_coords3D(coords, np.arange(4, dtype=np.int32)[:, None])
+    # page layout (a, c, e): entry (c, a) of the dim x nv page is coordinate c of vertex a
+    assert c3.shape == (4, 3, 1)
+    assert np.array_equal(c3[:, :, 0], nodes)
+    perm = np.array([2, 0, 3, 1], dtype=np.int32)
+    c3p, v3p = oracle.create_coords3D(coords, perm[:, None])
+    assert np.array_equal(c3p[:, :, 0], nodes[perm])
+    assert np.array_equal(v3p[:, :, 0], nodes[perm][:3] - nodes[perm][3])
+    rng = np.random.default_rng(11)
+    for dim, nv, nn, ne in [(2, 3, 50, 333), (3, 4, 70, 1001), (3, 3, 40, 257), (3, 10, 90, 129)]:
+        coords = rng.standard_normal((dim, nn))
+        elems = rng.integers(0, nn, size=(nv, ne)).astype(np.int32)
+        c3, v3 = oracle.create_coords3D(coords, elems)
+        ref = coords.T[elems]                                   # (nv, ne, dim)
+        assert np.array_equal(c3, ref.transpose(0, 2, 1))
+        assert np.array_equal(v3, (ref[:-1] - ref[-1]).transpose(0, 2, 1))
+
+
 # ---------------------------------------------------------------- cross (O6)
 def test_cross_basis_and_numpy():
     e = np.eye(3)
