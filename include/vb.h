@@ -375,8 +375,10 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
  * tetrahedron (so the ne = 6 nx ny nz elements are exactly the lattice's), and
  * row_ptr/col_idx (from fem_p1_pattern) is the lattice stencil (15 columns in
  * the interior).  It writes the plan (caller-owned DEVICE int32 array of
- * *plan_ints entries, 16-byte aligned: a token, the dims and the kernel's tile
- * descriptors) and reports in stats_out (HOST, 4 int64): [0] 1 if the mesh is
+ * *plan_ints entries, 16-byte aligned: a token, the dims, the kernel's tile
+ * descriptors and the cost-balanced range of tile layers of every CTA, one CTA
+ * per SM of the current device -- the plan is for the device it was built on)
+ * and reports in stats_out (HOST, 4 int64): [0] 1 if the mesh is
  * such a lattice (else 0 and nothing may be assembled with the plan), [1] the
  * number of tiles, [2] the refusal reason (1 counts, 2 element 0, 3 nx or
  * ny < 2 or degenerate ordering, 4 an element, 5 the pattern), [3] the
@@ -397,8 +399,9 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
  * (nnz each, nullable; overwritten), degenerate (nullable DEVICE int64: the
  * number of tetrahedra with det = 0 as the kernel evaluates it, each counted
  * once).  VB_ERR_ARG for NULL coords / row_ptr /
- * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2.  A plan of another mesh (token
- * mismatch) makes the kernel write nothing. */
+ * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2.  A plan of another mesh or of
+ * a device with another SM count (token mismatch) makes the kernel write
+ * nothing. */
 VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
                                   const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz, int nx, int ny,
                                   int nz, void* work, size_t* work_bytes, int32_t* plan, int64_t* plan_ints,

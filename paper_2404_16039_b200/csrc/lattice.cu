@@ -50,12 +50,15 @@ namespace {
 #ifndef VB_LAT_MINB
 #define VB_LAT_MINB 1
 #endif
+#ifndef VB_LAT_KO
+#define VB_LAT_KO 0   // timing knock-outs (wrong results; tools/ab_time.sh): 1 no bulk stores, 2 no cell arithmetic, 3 both
+#endif
 constexpr int LR = VB_LAT_R;      // warp rows per tile (row 0 may be a halo line)
 constexpr int LCOLS = 40;         // coordinate columns per row (lanes + one gap per segment)
 constexpr int LNBUF = 4;          // coordinate layer buffers (prefetch distance 3, two groups in flight)
 constexpr int LSTG = 32 * 15 + 16;   // staging doubles per matrix and warp row
 constexpr int LTHREADS = 32 * LR;
-constexpr int LMAXCTA = 1024;     // CTA ranges passed by value
+constexpr int LMAXCTA = 1024;     // CTA ranges kept in the plan
 constexpr uint32_t LAT_MAGIC = 0x4c415431u;   // "LAT1"
 
 // stencil directions: 0 self, 1..7 = +x +y +z +xy +xz +yz +xyz, 8..14 the negatives
@@ -99,7 +102,7 @@ struct LatParams {
     uint32_t want;
     int bulk;                     // K, M 16-byte aligned: rows leave as bulk copies
     unsigned long long* degen;    // nullable: count of tetrahedra with det = 0 (owned cells, counted once)
-    int range[LMAXCTA + 1];       // CTA c: tile-layers [range[c], range[c+1]) (cost-balanced)
+    const int32_t* range;         // plan: CTA c owns tile-layers [range[c], range[c+1]) (cost-balanced)
 };
 
 // lane descriptor (int4): x = I (canonical x of the lane's node, -1 for the virtual halo left of x = 0,
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
     long long t_start = clock64();
 #endif
 
-    const int64_t g0 = p.range[blockIdx.x], g1 = p.range[blockIdx.x + 1];
+    const int64_t g0 = __ldg(p.range + blockIdx.x), g1 = __ldg(p.range + blockIdx.x + 1);
     const int NK = p.nz + 1;
     const int64_t plane = p.dK;   // node id step per layer
     double* const SK = S.S[w][0];
@@ -354,13 +357,14 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
         double zcK0 = 0, zcK1 = 0, zcK2 = 0, zcM0 = 0, zcM1 = 0, zcM2 = 0;
         double ezK = 0, ezM = 0, exzK = 0, exzM = 0;
         const int32_t* rpp = p.row_ptr + idIJ;
+        int rp_next = (Ls >= ka && owned) ? __ldg(rpp + (int64_t)Ls * plane) : 0;   // row_ptr, one step ahead
 
         for (int Lz = Ls; Lz < kb; Lz++) {
             fetch(Lz + 3);
             cpa_commit();
             const bool out = Lz >= ka;
-            int rp = 0;
-            if (out && owned) rp = __ldg(rpp + (int64_t)Lz * plane);
+            const int rp = rp_next;
+            if (Lz + 1 < kb && owned) rp_next = __ldg(rpp + (int64_t)(Lz + 1) * plane);
 
             // ---- phase A: the cell (I, J, Lz) -> owned edges eK/eM (+ carries) and outgoing parts
             Cell CK, CM;
@@ -368,8 +372,18 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                 const double* x0 = xs + (Lz & (LNBUF - 1)) * XB;
                 const double* x1 = xs + ((Lz + 1) & (LNBUF - 1)) * XB;
                 const bool live = cellxy && Lz < p.nz;   // the top layer has no cells (coordinates still finite)
+#if VB_LAT_KO >= 2
+                {
+                    const double v = x0[0] + x1[XC + 1 + LCOLS];
+                    for (int i = 0; i < 7; i++) CK.e[i] = CM.e[i] = v;
+                    for (int i = 0; i < 3; i++) CK.c100[i] = CM.c100[i] = CK.c001[i] = CM.c001[i] = v;
+                    for (int i = 0; i < 5; i++) CK.o[i] = CM.o[i] = v;
+                    CK.c101 = CM.c101 = v;
+                }
+#else
                 if (__all_sync(0xffffffffu, live)) cell<false>(x0, x1, true, CK, CM);
                 else cell<true>(x0, x1, live, CK, CM);
+#endif
                 if (p.degen) {   // |det|/120 of the six tets: CM.c100[0..1], o[0..1], c001[0..1]
                     const int z = (CM.c100[0] == 0.0) + (CM.c100[1] == 0.0) + (CM.o[0] == 0.0) + (CM.o[1] == 0.0) +
                                   (CM.c001[0] == 0.0) + (CM.c001[1] == 0.0);
@@ -495,30 +509,43 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                 }
                 // segment range [a_seg, end of its last owned lane's row)
                 const int segend = __shfl_sync(0xffffffffu, rp + rlen, llast);
+                const bool tma = p.bulk && (fl & LF_BULK);   // full segment (the whole warp): rows leave through TMA
+                if (tma && owned) {
+                    // the 16-byte aligned body [a_seg + (a_seg & 1), segend - (segend & 1)) leaves as bulk copies; an
+                    // odd first / last entry is stored by the lane that staged it (its own staging row: no fence
+                    // needed), ahead of the fence so that its latency overlaps the bulk issue
+                    const double* rk = SK + soff + (rp - a_seg);
+                    const double* rm = SM + soff + (rp - a_seg);
+                    if (lane == lfirst && (rp & 1) && rlen > 0) {
+                        if (p.Kv) __stcs(p.Kv + rp, rk[0]);
+                        if (p.Mv) __stcs(p.Mv + rp, rm[0]);
+                    }
+                    if (lane == llast && (segend & 1) && segend - 1 > a_seg) {
+                        if (p.Kv) __stcs(p.Kv + segend - 1, rk[rlen - 1]);
+                        if (p.Mv) __stcs(p.Mv + segend - 1, rm[rlen - 1]);
+                    }
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 __syncwarp();
-                // one segment at a time (warp-uniform): lane 0 issues the 16-byte aligned body as two bulk
-                // copies (K, M), lanes 1 / 2 store an odd leading / trailing entry
-                uint32_t heads = __ballot_sync(0xffffffffu, owned && (fl & LF_HEAD));
-                while (heads) {
-                    const int hd = __ffs(heads) - 1;
-                    heads &= heads - 1;
-                    const int a0 = __shfl_sync(0xffffffffu, a_seg, hd);
-                    const int e0 = __shfl_sync(0xffffffffu, segend, hd);
-                    const int s0 = __shfl_sync(0xffffffffu, soff, hd);
-                    if (p.bulk && (fl & LF_BULK)) {   // full segments via TMA (uniform per tile)
-                        const int a = a0 + (a0 & 1), e = e0 - (e0 & 1);   // aligned body [a, e)
-                        if (lane == 0 && e > a) {
-                            if (p.Kv) bulk_st(p.Kv + a, SK + s0 + (a - a0), (e - a) * 8);
-                            if (p.Mv) bulk_st(p.Mv + a, SM + s0 + (a - a0), (e - a) * 8);
-                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                        }
-                        const int q = lane == 1 ? a0 : e0 - 1;   // an odd first / last entry
-                        if ((lane == 1 && (a0 & 1) && a0 < e0) || (lane == 2 && (e0 & 1) && e0 - 1 > a0)) {
-                            if (p.Kv) __stcs(p.Kv + q, SK[s0 + (q - a0)]);
-                            if (p.Mv) __stcs(p.Mv + q, SM[s0 + (q - a0)]);
-                        }
-                    } else {
+                if (tma) {
+                    const int a = a_seg + (a_seg & 1), e = segend - (segend & 1);
+                    if (lane == 0 && e > a) {
+#if VB_LAT_KO != 1 && VB_LAT_KO != 3
+                        if (p.Kv) bulk_st(p.Kv + a, SK + soff + (a - a_seg), (e - a) * 8);
+                        if (p.Mv) bulk_st(p.Mv + a, SM + soff + (a - a_seg), (e - a) * 8);
+#endif
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else {
+                    // packed tiles (several short segments per warp) and unaligned K / M: one segment at a time
+                    // (warp-uniform), plain coalesced stores
+                    uint32_t heads = __ballot_sync(0xffffffffu, owned && (fl & LF_HEAD));
+                    while (heads) {
+                        const int hd = __ffs(heads) - 1;
+                        heads &= heads - 1;
+                        const int a0 = __shfl_sync(0xffffffffu, a_seg, hd);
+                        const int e0 = __shfl_sync(0xffffffffu, segend, hd);
+                        const int s0 = __shfl_sync(0xffffffffu, soff, hd);
                         for (int q = a0 + lane; q < e0; q += 32) {
                             if (p.Kv) p.Kv[q] = SK[s0 + (q - a0)];
                             if (p.Mv) p.Mv[q] = SM[s0 + (q - a0)];
@@ -669,7 +696,7 @@ bool lat_host(int nx, int ny, int nz, const int* flip, LatHost& h) {
     return true;
 }
 
-uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz) {
+uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz, int G) {
     uint64_t z = 0x9E3779B97F4A7C15ull;
     auto mix = [&](uint64_t v) {
         z ^= v + 0x9E3779B97F4A7C15ull + (z << 6) + (z >> 2);
@@ -677,20 +704,21 @@ uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz) {
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z ^= z >> 31;
     };
-    mix(h.nx); mix(h.ny); mix(h.nz); mix(h.fx | h.fy << 1 | h.fz << 2); mix(nn); mix(nnz);
+    mix(h.nx); mix(h.ny); mix(h.nz); mix(h.fx | h.fy << 1 | h.fz << 2); mix(nn); mix(nnz); mix(G);
     const uint32_t t = LAT_MAGIC ^ (uint32_t)z ^ (uint32_t)(z >> 32);
     return t ? t : 1u;
 }
 
-// Relative cost of one tile-layer (measured, B200, per-CTA clock64 of the VB_LAT_PROF build): a fixed
-// part (barriers, latencies) and a part per warp row holding nodes; a band without a halo row owns
-// all its rows (one more row of output, the boundary row J = 0).
-// A tile whose segment holds x = 0 or x = nx runs the masked cell path (absent cells) and the boundary
-// row path in every warp: ~1.11x.  Packed tiles: ~1 + 0.05 (segments - 1)^2 more (per-segment store
-// passes; 5 segments measured at 1.8x).
-int lat_cost(int rows, int row0_owned, int xbnd = 0, int nseg = 1) {
-    const int c = 200 + 39 * rows + (row0_owned ? 39 : 0);
-    return c * (xbnd ? 111 : 100) * (100 + 5 * (nseg - 1) * (nseg - 1)) / 10000;
+// Cost of one tile-layer in SM cycles (measured on B200 with the per-CTA clock64 of the VB_LAT_PROF build,
+// tools/latprof_run.py, configs[4]): a fixed part (barriers and the latency chains of a step) and a part per
+// warp row holding nodes: 12 rows 6440, 7 rows 5140; a band without a halo row owns all its rows (the
+// boundary row J = 0: +250).  A tile whose segment holds x = 0 or x = nx runs the masked cell path (absent
+// cells) and the boundary row path in every warp: x 1.13.  Packed tiles (always holding x = nx; plain stores,
+// one pass per segment): x 0.96 with 2 segments, x 1.62 with 5.
+int lat_cost(int rows, int row0_owned, int xbnd = 0, int nseg = 0) {   // nseg > 0: a packed tile
+    const int c = 3320 + 260 * rows + (row0_owned ? 250 : 0);
+    const int packed = 735 + 220 * (nseg - 1);   // per mille
+    return (int)((int64_t)c * (xbnd ? 113 : 100) / 100 * (nseg > 0 ? packed : 1000) / 1000);
 }
 
 // Tiles of 32 lanes.  x segments: a halo lane and 31 owned nodes (segment 0's halo is the virtual
@@ -752,24 +780,70 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
     T = (int)(lanes.size() / 32);
 }
 
-// CTA ranges over the tile-layer sequence (tile-major), balanced by the tiles' weights
-void lat_ranges(const std::vector<int>& work, int nz, int G, int* range) {
-    const int NK = nz + 1;
-    int64_t tot = 0;
-    for (int w : work) tot += (int64_t)w * NK;
-    range[0] = 0;
-    int64_t acc = 0, gidx = 0;
-    int c = 1;
-    for (size_t t = 0; t < work.size() && c < G; t++)
-        for (int k = 0; k < NK && c < G; k++) {
-            acc += work[t];
-            gidx++;
-            while (c < G && acc * G >= tot * c) range[c++] = (int)gidx;
-        }
-    while (c <= G) range[c++] = (int)(work.size() * NK);
+// the number of tiles lat_tiles makes (the assembly call needs only the count)
+int lat_tile_count(int nx, int ny) {
+    int nfull = 0, nshort = 0;
+    for (int x0 = 0; x0 <= nx; x0 += 31) {
+        const int n = std::min(31, nx + 1 - x0);
+        if (n == 31) nfull++;
+        else nshort = n;
+    }
+    int bands = 1;
+    for (int covered = LR - 1; covered < ny; covered += LR - 1) bands++;
+    int T = bands * nfull;
+    if (nshort) {
+        const int per = std::min(7, 32 / (nshort + 1));
+        T += (bands + per - 1) / per;
+    }
+    return T;
 }
 
-constexpr int LAT_HDR = 16;   // plan header ints (token, dims, flips, tiles), then the lane descriptors
+// CTA ranges over the tile-layer sequence (tile-major): contiguous, with the smallest possible maximum
+// cost per CTA.  A CTA pays work[t] per layer, LAT_START per tile it enters (prologue: barriers and the
+// latency of the first coordinate layers) and one more layer when its range starts inside a tile (the
+// halo layer below it).  Smallest feasible budget by bisection, each trial a greedy fill.
+constexpr int LAT_START = 4000;
+void lat_ranges(const std::vector<int>& work, int nz, int G, int* range) {
+    const int NK = nz + 1;
+    const int64_t L = (int64_t)work.size() * NK;
+    auto fill = [&](int64_t budget, int* out) {   // true if G CTAs cover everything within the budget
+        int64_t pos = 0;
+        for (int c = 0; c < G; c++) {
+            if (out) out[c] = (int)pos;
+            int64_t cost = 0;
+            while (pos < L) {
+                const int t = (int)(pos / NK), k = (int)(pos % NK);
+                int64_t add = work[t];
+                if (cost == 0) add += LAT_START + (k > 0 ? work[t] : 0);
+                else if (k == 0) add += LAT_START;
+                if (cost > 0 && cost + add > budget) break;   // a CTA takes at least one layer
+                cost += add;
+                pos++;
+            }
+        }
+        if (out) out[G] = (int)L;
+        return pos >= L;
+    };
+    int64_t lo = 0, hi = 0;
+    for (int w : work) hi += (int64_t)(w + 1) * NK + LAT_START;
+    hi += LAT_START;
+    while (lo + 1 < hi) {   // fill(hi) holds, fill(lo) fails
+        const int64_t mid = (lo + hi) / 2;
+        if (fill(mid, nullptr)) hi = mid;
+        else lo = mid;
+    }
+    fill(hi, range);
+    range[G] = (int)L;
+}
+
+constexpr int LAT_HDR = 16;   // plan header ints (token, dims, flips, tiles, CTAs), then the lane descriptors (T x 32
+                              // int4) and the CTA ranges (LMAXCTA + 1 ints)
+// one CTA per SM of the current device (the plan's ranges are for this grid: the token covers it)
+int lat_grid(int T, int nz) {
+    int64_t L = (int64_t)T * (nz + 1);
+    int g = std::min(sm_count() * VB_LAT_MINB, LMAXCTA);
+    return (int)std::min<int64_t>(g, L);
+}
 
 }  // namespace
 
@@ -789,7 +863,8 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     std::vector<int> twork;
     int T = 0;
     lat_tiles(nx, ny, lanes, twork, T);
-    const int64_t need_ints = LAT_HDR + (int64_t)T * 32 * 4;
+    if (T != lat_tile_count(nx, ny)) { set_error("%s: internal tile count mismatch", fn); return VB_ERR_UNSUPPORTED; }
+    const int64_t need_ints = LAT_HDR + (int64_t)T * 32 * 4 + LMAXCTA + 1;
     const size_t wb = 256 + (size_t)((ne_want + 31) / 32) * 4;
     if (!work) {
         *work_bytes = wb;
@@ -855,11 +930,18 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     int32_t hdr[LAT_HDR] = {0};
     hdr[1] = nx; hdr[2] = ny; hdr[3] = nz;
     hdr[4] = h.fx; hdr[5] = h.fy; hdr[6] = h.fz; hdr[7] = T;
+    const int G = lat_grid(T, nz);
+    hdr[8] = G;
+    std::vector<int> range(LMAXCTA + 1, (int)((int64_t)T * (nz + 1)));
+    lat_ranges(twork, nz, G, range.data());
     e = cudaMemcpyAsync(plan, hdr, sizeof(hdr), cudaMemcpyHostToDevice, s);
     if (e == cudaSuccess)
         e = cudaMemcpyAsync(plan + LAT_HDR, lanes.data(), lanes.size() * sizeof(int4), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(plan + LAT_HDR + (int64_t)T * 128, range.data(), range.size() * sizeof(int),
+                            cudaMemcpyHostToDevice, s);
     if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
-    lattice_token_k<<<1, 1, 0, s>>>(flags, reinterpret_cast<uint32_t*>(plan), lat_want(h, nn, nnz));
+    lattice_token_k<<<1, 1, 0, s>>>(flags, reinterpret_cast<uint32_t*>(plan), lat_want(h, nn, nnz, G));
     if ((st = launch_check(fn)) != VB_OK) return st;
     int fl2[2];
     if ((st = read_small(s, flags, 8, fl2, fn)) != VB_OK) return st;   // synchronises: host arrays outlive
@@ -893,10 +975,7 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
         set_error("%s: lattice outside the kernel's limits (nx, ny >= 2)", fn);
         return VB_ERR_ARG;
     }
-    std::vector<int4> lanes;
-    std::vector<int> twork;
-    int T = 0;
-    lat_tiles(nx, ny, lanes, twork, T);
+    const int T = lat_tile_count(nx, ny);
     LatParams p;
     p.nx = nx; p.ny = ny; p.nz = nz; p.T = T;
     p.L = (int64_t)T * (nz + 1);
@@ -906,16 +985,15 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     p.Kv = K_vals; p.Mv = M_vals;
     p.lanes = reinterpret_cast<const int4*>(plan + LAT_HDR);
     p.token = reinterpret_cast<const uint32_t*>(plan);
-    p.want = lat_want(h, nn, nnz);
+    const int grid = lat_grid(T, nz);
+    p.range = plan + LAT_HDR + (int64_t)T * 128;
+    p.want = lat_want(h, nn, nnz, grid);
     p.bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
     p.degen = reinterpret_cast<unsigned long long*>(degenerate);
     if (degenerate) {
         cudaError_t e = cudaMemsetAsync(degenerate, 0, sizeof(int64_t), cs(stream));
         if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
     }
-    int grid = std::min(sm_count() * VB_LAT_MINB, LMAXCTA);
-    if (grid > p.L) grid = (int)p.L;
-    lat_ranges(twork, nz, grid, p.range);
     const size_t smem = sizeof(LatSmem);
     static int smem_set = 0;
     if (!smem_set) {

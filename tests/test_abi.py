@@ -119,10 +119,10 @@ def test_assembly_work_convention(L):
 def test_lattice_plan_query_and_argument_errors(L):
     wb, pi = C.c_size_t(0), C.c_int64(0)
     stats = (C.c_int64 * 4)()
-    # size query (no GPU): plan ints = header + 32 lane descriptors (int4) per tile
+    # size query (no GPU): plan ints = header + 32 lane descriptors (int4) per tile + 1025 CTA range bounds
     assert L.fem_plan_lattice(129 ** 3, 6 * 128 ** 3, None, 6 * 128 ** 3, None, None, 0, 128, 128, 128, None,
                               C.byref(wb), None, C.byref(pi), stats, None) == 0
-    assert wb.value > 6 * 128 ** 3 // 8 and (pi.value - 16) % 128 == 0 and pi.value > 16
+    assert wb.value > 6 * 128 ** 3 // 8 and (pi.value - 16 - 1025) % 128 == 0 and pi.value > 16 + 1025
     assert L.fem_plan_lattice(8, 6, None, 6, None, None, 0, 0, 1, 1, None, C.byref(wb), None, C.byref(pi), stats,
                               None) == -1
     # the assembly refuses inconsistent counts and lattices below the kernel's limits, before any CUDA call
