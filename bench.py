@@ -374,9 +374,18 @@ def run_vb(args):
     if rank == 0 and not args.quick:
         secondary = run_secondary(args, dev, peak, plan, cd, ed, coords, elems)
 
-    cpu = None
+    cpu, orows = None, None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        cpu = cpu_baseline(coords, elems, args.cpu_layers)
+        if args.quick:
+            cpu = cpu_baseline(coords, elems, args.cpu_layers)
+        else:   # the full run times the oracle on every config; cpu_baseline is its whole-mesh configs[4] row
+            orows, _ = oracle_rows()
+            r5 = orows["rows"][-1]
+            cpu = {"value": r5["elements_per_s_numeric"], "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": "the whole configs[4] mesh (%d tets): K+M assembly %.3f s on the oracle's pattern (built in "
+                             "%.3f s, not in value); single-threaded C (oracle/oracle.c, gcc -O2 -ffp-contract=off)"
+                             % (r5["elements"], r5["numeric_s"], r5["pattern_s"]),
+                   "host_cpu": orows["host_cpu"], "seconds": r5["numeric_s"]}
 
     if ws > 1:
         tdist.destroy_process_group()
@@ -396,6 +405,8 @@ def run_vb(args):
         "roofline": roof, "gpu_launches": args.steps * (1 if mode == vb.VB_ASSEMBLE_GATHER else 2),
         "clocks": clk.summary(), "e2e": e2e, "cpu_baseline": cpu,
     }
+    if orows is not None:
+        line["oracle_timings"] = orows
     if secondary is not None:
         line["secondary"] = secondary
     print(json.dumps(line), flush=True)
@@ -429,11 +440,20 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     flush = torch.empty(2 * 132644864 // 4, dtype=torch.float32, device=dev)   # 2x L2
     res = []
 
-    def rec(name, units, unit_name, nbytes, t):
+    def rec(name, units, unit_name, nbytes, t, alg=None):
+        """nbytes: the bytes the row's fraction counts.  For a composition of page calls that is the
+        page-form traffic (every intermediate page array written and read back, as the paper's
+        vectorised chain does: "bytes" = "page-form"); alg = what the result needs at least (inputs
+        read once + outputs written once) gives the ALG fraction beside it."""
         med, mn = t
-        res.append({"name": name, "ms": round(med, 5), "ms_min": round(mn, 5),
-                    unit_name + "_per_s": units / (med * 1e-3), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1),
-                    "frac": round(nbytes / (med * 1e-3) / 1e9 / peak, 4)})
+        r = {"name": name, "ms": round(med, 5), "ms_min": round(mn, 5),
+             unit_name + "_per_s": units / (med * 1e-3), "GB/s": round(nbytes / (med * 1e-3) / 1e9, 1),
+             "frac": round(nbytes / (med * 1e-3) / 1e9 / peak, 4)}
+        if alg is not None:
+            r["bytes"] = "page-form (intermediate page arrays counted)"
+            r["alg_GB/s"] = round(alg / (med * 1e-3) / 1e9, 1)
+            r["alg_frac"] = round(alg / (med * 1e-3) / 1e9 / peak, 4)
+        res.append(r)
 
     # the other assembly variants on config 5
     nn5, ne5 = coords5.shape[1], elems5.shape[1]
@@ -585,7 +605,8 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     p5 = vb.P1Plan(ed5, nn5, scatter_map=False)
     rec("NEXT-2 fem_p1_rhs config5 (b2D + deterministic accumarray)", ne5, "elements",
         nn5 * 24 + ne5 * 16 + ne5 * nq * 8 + ne5 * 4 * 8 * 2 + nn5 * 8,
-        time_kernel(lambda: vb.fem_p1_rhs(cd5, ed5, fq, plan=p5), 10))
+        time_kernel(lambda: vb.fem_p1_rhs(cd5, ed5, fq, plan=p5), 10),
+        alg=nn5 * 24 + ne5 * 16 + ne5 * nq * 8 + nn5 * 8)   # without the b2D round trip
     del p5, fq
     # NEXT-4: volumes (amdet(vectors3D)/6) and normals (amsm(amt(aminv(vectors3D)), normalsRef)) of all
     # 12.58M tets of the config-5 mesh; paper (sphere, 12.58M tets): volumes 4.42 s incl. mesh generation
@@ -601,9 +622,9 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
         vinv, _, _ = vb.vb_page_inv(v3, want_det=False)
         return vb.vb_page_mtimes(vb.vb_page_transpose(vinv), nref)
     rec("NEXT-4 tet volumes config5 (create_coords3D + page_det)", ne5, "elements",
-        ne5 * (16 + 72 * 2 + 8) + nn5 * 24, time_kernel(volumes, 10))
+        ne5 * (16 + 72 * 2 + 8) + nn5 * 24, time_kernel(volumes, 10), alg=ne5 * (16 + 8) + nn5 * 24)
     rec("NEXT-4 tet normals config5 (create_coords3D + page_inv + page_transpose + page_mtimes)", ne5, "elements",
-        ne5 * (16 + 72 * 6 + 96) + nn5 * 24, time_kernel(normals, 5))
+        ne5 * (16 + 72 * 6 + 96) + nn5 * 24, time_kernel(normals, 5), alg=ne5 * (16 + 96) + nn5 * 24)
     # NEXT-4 GI (Code GI P:838-847): the volume integral of rho = x1^2 + x2^2 over the config-5 mesh with the
     # degree-2 rule, GI alone on resident fip (4 points) and sizes: 40 B per tet
     import numpy as np
@@ -644,10 +665,59 @@ def cpu_baseline(coords, elems, layers, plan_cache=None):
     oracle.p1_assemble(coords, el, rp, ci)
     t2 = time.perf_counter()
     return {"value": ne_s / (t2 - t1), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "first %d of 128 z-layers of the config-5 mesh (%d tets): K+M assembly %.3f s on the "
+            "sample": "%d of 128 z-layers of the config-5 mesh (%d tets): K+M assembly %.3f s on the "
                       "oracle's pattern (built in %.3f s, not in value); single-threaded C (oracle/oracle.c, "
                       "gcc -O2 -ffp-contract=off)" % (layers, ne_s, t2 - t1, t_pat),
             "host_cpu": host_cpu(), "seconds": t2 - t1}
+
+
+def oracle_rows():
+    """The oracle timed on this box's host cores for every BASELINE config (SURVEY §8(d) "Oracle timing"):
+    configs[0]-[1] best of 3, configs[2]-[4] one full run each; pattern and numeric phases separately;
+    single-threaded C (oracle/oracle.c), host CPU stated.  About 25 s in all."""
+    import oracle
+    import synth
+    rows = []
+
+    def best(fn, reps):
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return min(ts)
+
+    def fem(cfg, coords, elems, reps):
+        nn, ne = coords.shape[1], elems.shape[1]
+        pat = {}
+        t_pat = best(lambda: pat.update(zip(("rp", "ci"), oracle.p1_pattern(elems, nn))), reps)
+        t_num = best(lambda: oracle.p1_assemble(coords, elems, pat["rp"], pat["ci"]), reps)
+        rows.append({"config": cfg, "elements": ne, "nodes": nn, "nnz": int(pat["rp"][-1]), "pattern_s": round(t_pat, 4),
+                     "numeric_s": round(t_num, 4), "elements_per_s_numeric": ne / t_num,
+                     "elements_per_s_total": ne / (t_pat + t_num), "runs": "best of %d" % reps if reps > 1 else "one run"})
+        return t_num
+
+    fem("configs[0] 2D 32x32 P1 K+M", *synth.square_p1(32, jitter=0.1, seed=0), 3)
+    N = 1 << 20
+    for n in (2, 3, 4):
+        A, B = synth.normal_pages(n, n, N, stream=10), synth.normal_pages(n, n, N, stream=11)
+        X, _ = synth.inverse_pages(n, N, seed=0)
+        ops = {"mtimes A*B": lambda: oracle.page_mtimes(A, B), "mtimes A*B^T": lambda: oracle.page_mtimes(A, B, False, True),
+               "mtimes A^T*B": lambda: oracle.page_mtimes(A, B, True, False), "transpose": lambda: oracle.page_transpose(A),
+               "det": lambda: oracle.page_det(A), "inv+det": lambda: oracle.page_inv(X)}
+        for name, fn in ops.items():
+            t = best(fn, 3)
+            rows.append({"config": "configs[1] page sweep n=%d %s" % (n, name), "pages": N, "numeric_s": round(t, 4),
+                         "pages_per_s": N / t, "runs": "best of 3"})
+    xyz, tri = synth.icosphere(10, perturb=0.01, seed=0)
+    t = best(lambda: oracle.tri_surface(xyz, tri), 1)
+    rows.append({"config": "configs[2] surface geometry (n, nhat, area, volume)", "triangles": tri.shape[1],
+                 "numeric_s": round(t, 4), "triangles_per_s": tri.shape[1] / t, "runs": "one run"})
+    del xyz, tri
+    fem("configs[3] 2D 2048x2048 P1 K+M", *synth.square_p1(2048, jitter=0.1, seed=0), 1)
+    t5 = fem("configs[4] 3D 128^3 Kuhn P1 K+M (the whole mesh)", *synth.cube_kuhn_p1(128, jitter=0.05, seed=0), 1)
+    return {"cores": 1, "host_cpu": host_cpu(), "kind": "oracle (oracle/oracle.c, gcc -O2 -ffp-contract=off, one thread)",
+            "rows": rows}, t5
 
 
 def host_cpu():
@@ -706,7 +776,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=16)
-    ap.add_argument("--cpu-layers", type=int, default=8)
+    ap.add_argument("--cpu-layers", type=int, default=128,
+                    help="z-layers of the config-5 mesh the cpu_baseline assembles (128 = the whole mesh, ~12 s)")
     ap.add_argument("--ref-budget", type=float, default=90.0, help="seconds of oracle work for --impl reference")
     args = ap.parse_args()
     if args.variant == "gather":

@@ -247,8 +247,9 @@ VB_API vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_ptr, c
  *   (the oracle's order) in on-chip memory and writes each CSR entry once; no
  *   atomics, no zero-fill.  Needs col_idx, node_elem_ptr and node_elem_slot
  *   (node_elem is not read).  col_idx and node_elem_slot are streamed with
- *   16-byte TMA bulk copies: both must be 16-byte aligned and readable up to
- *   the next multiple of 4 entries (torch allocations satisfy this).
+ *   16-byte TMA bulk copies: both must be 16-byte aligned (VB_ERR_ARG
+ *   otherwise) and readable up to the next multiple of 4 entries (torch
+ *   allocations satisfy this).
  *   Diagonals follow from the partition of unity sum_b phi_b = 1
  *   (K_vv = -sum_{w!=v} K_vw, M_vv = (2/d) sum_{w!=v} M_vw).
  *   Bitwise reproducible.

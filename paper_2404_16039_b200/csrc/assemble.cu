@@ -1741,6 +1741,12 @@ vb_status assemble_entry(const char* fn, int dim, int64_t nn, int64_t ne, const 
     if (base_mode != VB_ASSEMBLE_ATOMIC && base_mode != VB_ASSEMBLE_GATHER) { set_error("%s: unknown mode %d", fn, mode); return VB_ERR_ARG; }
     if (ne > 0 && (!coords || !elems)) { set_error("%s: NULL %s", fn, !coords ? "coords" : "elems"); return VB_ERR_ARG; }
     if (elem_ld < ne) { set_error("%s: elem_ld < ne", fn); return VB_ERR_ARG; }
+    if (base_mode == VB_ASSEMBLE_GATHER && (K_vals || M_vals) && nn > 0 &&
+        ((col_idx && !aligned16(col_idx)) || (node_elem_slot && !aligned16(node_elem_slot)))) {
+        // the gather kernels stream these two arrays with bulk copies (cp.async.bulk: 16-byte aligned sources)
+        set_error("%s: col_idx and node_elem_slot must be 16-byte aligned in gather mode", fn);
+        return VB_ERR_ARG;
+    }
     unsigned int* ctr = nullptr;   // NULL work: static block schedule
     if (work) {
         if (!aligned16(work)) { set_error("%s: work must be 16-byte aligned", fn); return VB_ERR_ARG; }

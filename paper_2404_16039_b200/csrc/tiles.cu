@@ -409,6 +409,9 @@ __global__ void __launch_bounds__(TR, 3) assemble_tile_k(int64_t T, const int4* 
         const int e0 = tc[0], ne_t = tc[ncol] - e0;
         if (tid == 0 && ne_t > 0) {
             const uint32_t bytes = (uint32_t)ne_t * 16u;
+            // the generic-proxy reads of the previous tile's entries (ordered by the __syncthreads that ended
+            // it) before this async-proxy overwrite of the same buffer
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(&bar)), "r"(bytes)
                          : "memory");
             asm volatile(
@@ -726,6 +729,10 @@ extern "C" vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* co
     if (nn == 0 || (!K_vals && !M_vals)) return VB_OK;
     if (!coords || !tile_meta || !tile_nodes || !tile_rows || !tile_colors || !tile_elems) {
         set_error("%s: NULL argument", fn);
+        return VB_ERR_ARG;
+    }
+    if (!aligned16(tile_elems) || !aligned16(tile_meta)) {   // streamed with bulk copies / read as int4
+        set_error("%s: tile_elems and tile_meta must be 16-byte aligned", fn);
         return VB_ERR_ARG;
     }
     const int64_t T = (nn + TR - 1) / TR;
