@@ -575,8 +575,22 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     rec("config3 page_cross on pre-gathered edge-vector pages (K5 alone)", F, "pages", F * 72,
         time_kernel(lambda: vb.vb_page_cross(ea, eb, Cout=cr), 10, flush))
     del xd, td, out, ea, eb, cr
-    # config 2: page sweep
+    # config 2: page sweep.  These launches move 33-400 MB in 14-75 us, so launch latency, the ramp and the tail
+    # are a visible share: beside the HBM fraction every row gets the time of a plain device copy of the same
+    # traffic (torch copy_ of nbytes/2, timed the same way) and vs_copy = copy time / kernel time (1 = as fast
+    # as a copy of as many bytes can be launched on this box).
     N = 1 << 20
+    copy_ms = {}
+
+    def with_copy(nbytes):
+        if nbytes not in copy_ms:
+            src = torch.empty(nbytes // 16, dtype=torch.float64, device=dev).normal_()
+            dst = torch.empty_like(src)
+            copy_ms[nbytes] = time_kernel(lambda: dst.copy_(src), 20, flush)[0]
+            del src, dst
+        res[-1]["copy_same_bytes_ms"] = round(copy_ms[nbytes], 5)
+        res[-1]["vs_copy"] = round(copy_ms[nbytes] / res[-1]["ms"], 3)
+
     for n in (2, 3, 4):
         A = torch.from_numpy(synth.normal_pages(n, n, N, stream=10)).to(dev)
         B = torch.from_numpy(synth.normal_pages(n, n, N, stream=11)).to(dev)
@@ -584,20 +598,25 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
         for tag, tX, tY in (("A*B", 0, 0), ("A*B^T", 0, 1), ("A^T*B", 1, 0)):
             rec("config2 mtimes %s n=%d" % (tag, n), N, "pages", 24 * n * n * N,
                 time_kernel(lambda: vb.vb_page_mtimes(A, B, tX, tY, Z=Z), 20, flush))
+            with_copy(24 * n * n * N)
         rec("config2 transpose n=%d" % n, N, "pages", 16 * n * n * N,
             time_kernel(lambda: vb.vb_page_transpose(A, Z=Z), 20, flush))
+        with_copy(16 * n * n * N)
         d = torch.empty(N, dtype=torch.float64, device=dev)
         rec("config2 det n=%d" % n, N, "pages", (n * n + 1) * 8 * N,
             time_kernel(lambda: vb.vb_page_det(A, det=d), 20, flush))
+        with_copy((n * n + 1) * 8 * N)
         X, _ = synth.inverse_pages(n, N, seed=0)
         Xd = torch.from_numpy(X).to(dev)
         rec("config2 inv+det n=%d" % n, N, "pages", (2 * n * n + 1) * 8 * N,
             time_kernel(lambda: vb.vb_page_inv(Xd, Xinv=Z, det=d), 20, flush))
+        with_copy((2 * n * n + 1) * 8 * N)
         del A, B, Z, Xd
     a3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=60)).to(dev)
     b3 = torch.from_numpy(synth.normal_pages(3, 1, N, stream=61)).to(dev)
     c3 = torch.empty_like(a3)
     rec("config2 cross", N, "pages", 72 * N, time_kernel(lambda: vb.vb_page_cross(a3, b3, Cout=c3), 20, flush))
+    with_copy(72 * N)
     del a3, b3, c3
     # NEXT-2: load vector on the config-5 mesh (f given at the 4 integration points of every tet)
     nq = 4

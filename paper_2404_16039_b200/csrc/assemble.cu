@@ -153,6 +153,45 @@ __device__ __forceinline__ double elem_coef(const double (&x)[DIM + 1][DIM], dou
 }
 
 // ------------------------------------------------------------ atomic variant
+// Warp-aggregated scatter: lanes of one instruction that hit the same CSR entry (neighbouring elements
+// share edges and vertices: 16 -> about 6 distinct targets per tet and matrix in Kuhn cell order) are found
+// with match.any, every lane sums the values of its peers (one shuffle pair per round, rounds = the
+// largest group of the warp) and the lowest lane of each group issues one RED for K and one for M.
+// idx < 0: this lane has nothing to add.  Measured (tools/time_atomic.py): configs[4] 2.19 -> 1.85 ms (402.7 M
+// -> ~153 M REDs; the match and the shuffle rounds cost most of what the L2 saves), configs[3] 0.85 -> 1.07 ms
+// (6 of 9 targets per triangle are already distinct): aggregated in 3D only.
+#ifndef VB_ATOMIC_AGG
+#define VB_ATOMIC_AGG 1
+#endif
+template <bool AGG>
+__device__ __forceinline__ void red_pair(double* __restrict__ K, double* __restrict__ M, int idx, double k,
+                                         double m, int lane) {
+  if constexpr (AGG) {
+    const unsigned peers = __match_any_sync(0xffffffffu, idx < 0 ? -1 - lane : idx);
+    const int rounds = __reduce_max_sync(0xffffffffu, __popc(peers));
+    double ks = k, ms = m;
+    unsigned rem = peers & ~(1u << lane);
+    for (int r = 1; r < rounds; r++) {   // warp-uniform trip count
+        const int src = rem ? __ffs(rem) - 1 : lane;
+        rem &= rem - 1;
+        const double kv = __shfl_sync(0xffffffffu, k, src), mv = __shfl_sync(0xffffffffu, m, src);
+        if (src != lane) {
+            ks += kv;
+            ms += mv;
+        }
+    }
+    if (idx >= 0 && (peers & ((1u << lane) - 1)) == 0) {
+        if (K) atomicAdd(K + idx, ks);
+        if (M) atomicAdd(M + idx, ms);
+    }
+  } else {
+    if (idx >= 0) {
+        if (K) atomicAdd(K + idx, k);
+        if (M) atomicAdd(M + idx, m);
+    }
+  }
+}
+
 template <int DIM, bool COEF>
 __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
                                                          int64_t cst, const int32_t* __restrict__ elems, int64_t eld,
@@ -160,8 +199,13 @@ __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const doubl
                                                          double* __restrict__ M, double* __restrict__ Kl,
                                                          double* __restrict__ Ml, const CoefSpec cp) {
     constexpr int NV = DIM + 1;
+    constexpr bool AGG = VB_ATOMIC_AGG && DIM == 3;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += stride) {
+    const int lane = threadIdx.x & 31;
+    // whole warps run the loop (the aggregation is a warp collective); lanes past the end carry no element
+    for (int64_t eb = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); eb < ne; eb += stride) {
+        const bool valid = eb + lane < ne;
+        const int64_t e = valid ? eb + lane : ne - 1;
         int32_t vid[NV];
         double x[NV][DIM], H[DIM][NV];
         load_element<DIM>(e, elems, eld, coords, ns, cst, vid, x);
@@ -181,20 +225,22 @@ __global__ void __launch_bounds__(256) assemble_atomic_k(int64_t ne, const doubl
                 double k = s * d;
                 double mm = COEF ? Mloc[a][b] : ((a == b) ? 2.0 * m : m);
                 if (K || M) {
-                    int32_t pab = __ldcs(e2n + (int64_t)(a * NV + b) * ne + e);
-                    if (K) atomicAdd(K + pab, k);
-                    if (M) atomicAdd(M + pab, mm);
+                    const int32_t pab = __ldcs(e2n + (int64_t)(a * NV + b) * ne + e);
+                    red_pair<AGG>(K, M, valid ? pab : -1, k, mm, lane);
                 }
-                if (Kl) stcs(Kl + (int64_t)(a + b * NV) * ne + e, k);
-                if (Ml) stcs(Ml + (int64_t)(a + b * NV) * ne + e, mm);
+                if (valid) {
+                    if (Kl) stcs(Kl + (int64_t)(a + b * NV) * ne + e, k);
+                    if (Ml) stcs(Ml + (int64_t)(a + b * NV) * ne + e, mm);
+                }
                 if (a != b) {
                     if (K || M) {
-                        int32_t pba = __ldcs(e2n + (int64_t)(b * NV + a) * ne + e);
-                        if (K) atomicAdd(K + pba, k);
-                        if (M) atomicAdd(M + pba, mm);
+                        const int32_t pba = __ldcs(e2n + (int64_t)(b * NV + a) * ne + e);
+                        red_pair<AGG>(K, M, valid ? pba : -1, k, mm, lane);
                     }
-                    if (Kl) stcs(Kl + (int64_t)(b + a * NV) * ne + e, k);
-                    if (Ml) stcs(Ml + (int64_t)(b + a * NV) * ne + e, mm);
+                    if (valid) {
+                        if (Kl) stcs(Kl + (int64_t)(b + a * NV) * ne + e, k);
+                        if (Ml) stcs(Ml + (int64_t)(b + a * NV) * ne + e, mm);
+                    }
                 }
             }
     }

@@ -55,8 +55,13 @@ namespace {
 #endif
 constexpr int LR = VB_LAT_R;      // warp rows per tile (row 0 may be a halo line)
 constexpr int LCOLS = 40;         // coordinate columns per row (lanes + one gap per segment)
-constexpr int LNBUF = 4;          // coordinate layer buffers (prefetch distance 3, two groups in flight)
-constexpr int LSTG = 32 * 15 + 16;   // staging doubles per matrix and warp row
+#ifndef VB_LAT_NBUF
+#define VB_LAT_NBUF 5
+#endif
+constexpr int LNBUF = VB_LAT_NBUF;   // coordinate layer buffers: layer Lz + LNBUF - 1 is fetched at the start of step Lz
+constexpr int LDIST = LNBUF - 1;     // (configs[4]: 3 buffers 0.1725 ms, 4 buffers 0.1622, 5 buffers 0.1601; issuing the
+                                     // fetch behind the bulk wait, which shares its scoreboard, changed nothing)
+constexpr int LSTG = 31 * 15 + 3;    // staging doubles per matrix and warp row: 31 rows + the parity offset, 16-byte multiple
 constexpr int LTHREADS = 32 * LR;
 constexpr int LMAXCTA = 1024;     // CTA ranges kept in the plan
 constexpr uint32_t LAT_MAGIC = 0x4c415431u;   // "LAT1"
@@ -287,6 +292,8 @@ __device__ __forceinline__ double shup(double v) { return __shfl_up_sync(0xfffff
 constexpr int XB = 3 * (LR + 1) * LCOLS;   // doubles per coordinate layer buffer
 constexpr int XC = (LR + 1) * LCOLS;       // doubles per component plane
 
+// 12 warps: 3 per SM sub-partition, whose 16 K registers allow 168 per thread; a 13th warp (4 on one
+// sub-partition) would cap the kernel at 128 registers (ptxas then spills) and 16 rows do not fit 227 KB.
 template <int FY, int FZ>
 __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(const LatParams p) {
     constexpr Order<FY, FZ> ORD{};
@@ -354,12 +361,16 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
 
         const int Ls = ka > 0 ? ka - 1 : ka;   // one halo layer when the range starts inside the tile
         __syncthreads();                       // previous range's readers of every buffer are done
+        static_assert(LDIST >= 2 && LDIST <= 4, "prefetch distance");
         fetch(Ls);
         fetch(Ls + 1);
         cpa_commit();
-        fetch(Ls + 2);
-        cpa_commit();
-        cpa_wait<1>();
+#pragma unroll
+        for (int l = 2; l < LDIST; l++) {   // LDIST - 1 groups in flight
+            fetch(Ls + l);
+            cpa_commit();
+        }
+        cpa_wait<LDIST - 2>();
         __syncthreads();
 
         // carries along z: zc = in-plane up edges (+x, +y, +xy) of this node at the next layer from the
@@ -370,7 +381,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
         int rp_next = (Ls >= ka && owned) ? __ldg(rpp + (int64_t)Ls * plane) : 0;   // row_ptr, one step ahead
 
         for (int Lz = Ls; Lz < kb; Lz++) {
-            fetch(Lz + 3);
+            fetch(Lz + LDIST);
             cpa_commit();
             const bool out = Lz >= ka;
             const int rp = rp_next;
@@ -379,8 +390,8 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
             // ---- phase A: the cell (I, J, Lz) -> owned edges eK/eM (+ carries) and outgoing parts
             Cell CK, CM;
             {
-                const double* x0 = xs + (Lz & (LNBUF - 1)) * XB;
-                const double* x1 = xs + ((Lz + 1) & (LNBUF - 1)) * XB;
+                const double* x0 = xs + (Lz % LNBUF) * XB;
+                const double* x1 = xs + ((Lz + 1) % LNBUF) * XB;
                 const bool live = cellxy && Lz < p.nz;   // the top layer has no cells (coordinates still finite)
 #if VB_LAT_KO >= 2
                 {
@@ -437,7 +448,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
             S.Ez[Lz & 1][w][1][lane] = eM[EYZ];
             S.Ez[Lz & 1][w][2][lane] = eK[EXYZ];
             S.Ez[Lz & 1][w][3][lane] = eM[EXYZ];
-            cpa_wait<1>();
+            cpa_wait<LDIST - 2>();   // layer Lz + 2 has landed
             __syncthreads();
 
             // ---- phase D: the CSR rows of this layer's owned nodes
@@ -740,6 +751,14 @@ int lat_cost(int rows, int row0_owned, int xbnd = 0, int nseg = 0) {   // nseg >
     return (int)((int64_t)c * (xbnd ? 113 : 100) / 100 * (nseg > 0 ? packed : 1000) / 1000);
 }
 
+// short segments (W lanes: a halo and W - 1 owned nodes) packed into one tile: as many as the lanes and the
+// staging area (15 (W - 1) + 1 doubles and up to 15 of padding each) hold, at most 7 (coordinate columns)
+int lat_per(int W) {
+    int per = std::min(7, 32 / W);
+    while (per > 1 && per * (15 * (W - 1) + 16) > LSTG) per--;
+    return per;
+}
+
 // Tiles of 32 lanes.  x segments: a halo lane and 31 owned nodes (segment 0's halo is the virtual
 // node x = -1); y bands of LR rows (the first owns LR lines, the next a halo line + LR - 1).  The
 // short last segment of every band is packed with those of other bands.  work[t] = warp rows of
@@ -776,7 +795,7 @@ void lat_tiles(int nx, int ny, std::vector<int4>& lanes, std::vector<int>& work,
     if (!shortv.empty()) {
         // at most one short segment per band (the last one), all of the same width
         const int W = shortv[0].nown + 1;
-        const int per = std::min(7, 32 / W);
+        const int per = lat_per(W);
         for (size_t b0 = 0; b0 < bands.size(); b0 += per) {
             int4 t[32];
             for (int l = 0; l < 32; l++) t[l] = idle;
@@ -811,7 +830,7 @@ int lat_tile_count(int nx, int ny) {
     for (int covered = LR - 1; covered < ny; covered += LR - 1) bands++;
     int T = bands * nfull;
     if (nshort) {
-        const int per = std::min(7, 32 / (nshort + 1));
+        const int per = lat_per(nshort + 1);
         T += (bands + per - 1) / per;
     }
     return T;
