@@ -383,7 +383,8 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
  * such a lattice (else 0 and nothing may be assembled with the plan), [1] the
  * number of tiles, [2] the refusal reason (1 counts, 2 element 0, 3 nx or
  * ny < 2 or degenerate ordering, 4 an element, 5 the pattern), [3] the
- * orientation flags to pass to fem_p1_assemble_lattice.  work: DEVICE scratch
+ * value to pass as `flips` to fem_p1_assemble_lattice (bits 0-2 the
+ * orientation, bits 8.. the number of CTAs the plan's ranges are for).  work: DEVICE scratch
  * (ne/8 + 256 bytes); work == NULL queries *work_bytes and *plan_ints.
  * Synchronises the stream (small read-backs).  Refusal is not an error.
  *
@@ -400,9 +401,9 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
  * (nnz each, nullable; overwritten), degenerate (nullable DEVICE int64: the
  * number of tetrahedra with det = 0 as the kernel evaluates it, each counted
  * once).  VB_ERR_ARG for NULL coords / row_ptr /
- * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2.  A plan of another mesh or of
- * a device with another SM count (token mismatch) makes the kernel write
- * nothing. */
+ * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2, or a plan built for a device
+ * with another SM count (flips bits 8..).  A plan of another mesh (token
+ * mismatch, checked on the device) makes the kernel write nothing. */
 VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
                                   const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz, int nx, int ny,
                                   int nz, void* work, size_t* work_bytes, int32_t* plan, int64_t* plan_ints,

@@ -986,7 +986,7 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     if (fl2[0]) stats_out[2] = 4;       // an element is not a Kuhn tetrahedron of this lattice (or twice)
     else if (fl2[1]) stats_out[2] = 5;  // the CSR pattern is not the lattice stencil
     else stats_out[0] = 1;
-    stats_out[3] = h.fx | h.fy << 1 | h.fz << 2;
+    stats_out[3] = h.fx | h.fy << 1 | h.fz << 2 | (int64_t)G << 8;   // orientation, and the grid the ranges are for
     return VB_OK;
 }
 
@@ -1007,6 +1007,7 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     }
     if (!aligned16(plan)) { set_error("%s: plan must be 16-byte aligned", fn); return VB_ERR_ARG; }
     if (!K_vals && !M_vals && !degenerate) return VB_OK;
+    const int g_plan = flips >> 8;   // 0: not given (orientation only)
     const int fl[3] = {flips & 1, (flips >> 1) & 1, (flips >> 2) & 1};
     LatHost h;
     if (nx < 2 || ny < 2 || !lat_host(nx, ny, nz, fl, h)) {
@@ -1024,6 +1025,11 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     p.lanes = reinterpret_cast<const int4*>(plan + LAT_HDR);
     p.token = reinterpret_cast<const uint32_t*>(plan);
     const int grid = lat_grid(T, nz);
+    if (g_plan && g_plan != grid) {
+        set_error("%s: the plan was built for a device with another SM count (%d CTAs, this device: %d)", fn, g_plan,
+                  grid);
+        return VB_ERR_ARG;
+    }
     p.range = plan + LAT_HDR + (int64_t)T * 128;
     p.want = lat_want(h, nn, nnz, grid);
     p.bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
