@@ -216,11 +216,19 @@ def run_vb(args):
     # plan (pattern + scatter/gather plans), timed separately: one cold build (module
     # load, allocator growth), then the median of 3 warm builds (host wall clock; the
     # count phase has a documented nnz read-back)
+    def make_plan(e_dev):
+        if lattice:
+            # the lattice variant's plan: fem_plan_lattice verifies the elements, fem_lattice_pattern writes
+            # the stencil pattern in closed form (bit-identical to fem_p1_pattern's, tests/test_gpu_lattice.py)
+            p = vb.P1Plan.for_lattice(e_dev, nn)
+            if p is None:
+                raise RuntimeError("lattice plan refused")
+            return p
+        return vb.P1Plan(e_dev, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
+                         gather_plan=(mode == vb.VB_ASSEMBLE_GATHER))
+
     def build_plan():
-        p = vb.P1Plan(ed, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
-                      gather_plan=(mode == vb.VB_ASSEMBLE_GATHER and not lattice))
-        if lattice and not p.lattice(ed):   # verified Kuhn-lattice plan (part of this variant's plan)
-            raise RuntimeError("lattice plan refused: " + p.lattice_reason)
+        p = make_plan(ed)
         if gvar == "class":
             p.classes()    # the row classes are part of this variant's plan
         if gvar == "tile" and not p.tiles(cd, ed):   # the tile plan is part of this variant's plan
@@ -334,8 +342,7 @@ def run_vb(args):
             e2.record_stream(s)
             o = outs[j]
             with torch.cuda.stream(s):
-                p2 = vb.P1Plan(e2, nn, scatter_map=(mode == vb.VB_ASSEMBLE_ATOMIC),
-                               gather_plan=(mode == vb.VB_ASSEMBLE_GATHER and not lattice))
+                p2 = make_plan(e2)
                 K2, M2, _, _ = vb.fem_p1_assemble(c2, e2, p2, mode=mode, variant=gvar)
                 done = torch.cuda.Event()
                 done.record(s)
@@ -366,7 +373,7 @@ def run_vb(args):
                "h2d_bytes_per_step": coords.nbytes + elems.nbytes,
                "d2h_bytes_per_step": (nn + 1) * 4 + nnz * 4 + 2 * nnz * 8,
                "steps": n_e2e, "ms_per_step": e2e_ms / n_e2e,
-               "includes": "per step: H2D coords+elems from pinned memory, fem_p1_pattern (count+fill), fem_plan_lattice (lattice variant: verifies the mesh and pattern), "
+               "includes": "per step: H2D coords+elems from pinned memory, the plan (lattice variant: fem_plan_lattice verifies the elements + fem_lattice_pattern; other variants: fem_p1_pattern count+fill), "
                            "fem_plan_classes (class variant) / fem_plan_tiles (tile variant), the assembly, D2H row_ptr/col_idx/K/M to pinned memory; upload / 2 compute / "
                            "download streams, host wall clock with device syncs on both sides"}
 
@@ -399,7 +406,10 @@ def run_vb(args):
                    "timed": "one numeric K+M assembly per step on the resident plan (%s)" % (
                        {"lattice": "fem_p1_assemble_lattice", "class": "fem_p1_assemble_classes",
                         "tile": "fem_p1_assemble_tiles"}.get(gvar, "fem_p1_assemble")),
-                   "pattern_ms": round(pattern_ms, 3), "nnz": nnz, "ne": ne, "nn": nn,
+                   "pattern_ms": round(pattern_ms, 3),
+                   "plan": ("fem_plan_lattice (verifies the elements) + fem_lattice_pattern (closed-form stencil pattern)"
+                            if lattice else "fem_p1_pattern (count + fill) + the variant's plan"),
+                   "nnz": nnz, "ne": ne, "nn": nn,
                    "l2": "no flush: every step streams %.0f MB (> 126 MB L2)" % (alg / 1e6),
                    "parallelism": "replicas" if ws > 1 else "single GPU"},
         "roofline": roof, "gpu_launches": args.steps * (1 if mode == vb.VB_ASSEMBLE_GATHER else 2),
@@ -499,6 +509,17 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     torch.cuda.synchronize()
     res.append({"name": "config5 fem_p1_pattern (count+fill, elem2nnz + gather plan)",
                 "ms": round((time.perf_counter() - t0) * 1e3 / 2, 3)})
+    for label, fn in (("config5 fem_p1_pattern (count+fill, pattern only)",
+                       lambda: vb.P1Plan(ed5, nn5, scatter_map=False, gather_plan=False)),
+                      ("config5 lattice plan (fem_plan_lattice on the elements + fem_lattice_pattern, closed form)",
+                       lambda: vb.P1Plan.for_lattice(ed5, nn5))):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        res.append({"name": label, "ms": round((time.perf_counter() - t0) * 1e3 / 3, 3)})
     # NEXT-1: the paper's own timed workload, Table tab:KM_P1_3D level 7 (the config-5 mesh size, the
     # paper's Kuhn variant, c_K = c_M = e^{x1+x2+x3}, gqo = 2); paper: K 66.6 s + M 20.4 s, hardware not stated
     cp_, ep_ = synth.cube_kuhn_p1(128, jitter=0.0, flip=(0, 0, 1))

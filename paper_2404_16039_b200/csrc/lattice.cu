@@ -679,6 +679,37 @@ __global__ void lattice_check_csr_k(int64_t nn, int64_t nnz, const int32_t* __re
 }
 
 
+// the lattice stencil written out as a CSR pattern (fem_lattice_pattern): row lengths, then the columns of
+// every row in ascending order (ord: stencil directions by ascending column id)
+__global__ void lattice_rowlen_k(int64_t nn, LatGeom g, int32_t* __restrict__ row_len) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
+        int I, J, K;
+        canon(g, v, I, J, K);
+        int n = 0;
+#pragma unroll
+        for (int d = 0; d < 15; d++) {
+            const int x = I + dir_dx(d), y = J + dir_dy(d), z = K + dir_dz(d);
+            n += x >= 0 && x <= g.nx && y >= 0 && y <= g.ny && z >= 0 && z <= g.nz;
+        }
+        row_len[v] = n;
+    }
+}
+__global__ void lattice_cols_k(int64_t nn, LatGeom g, int64_t id0, int64_t dI, int64_t dJ, int64_t dK, LatOrder ord,
+                               const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
+        int I, J, K;
+        canon(g, v, I, J, K);
+        int64_t q = row_ptr[v];
+#pragma unroll
+        for (int r = 0; r < 15; r++) {
+            const int d = ord.dir[r];
+            const int x = I + dir_dx(d), y = J + dir_dy(d), z = K + dir_dz(d);
+            if (x < 0 || x > g.nx || y < 0 || y > g.ny || z < 0 || z > g.nz) continue;
+            col_idx[q++] = (int32_t)(id0 + dI * x + dJ * y + dK * z);
+        }
+    }
+}
+
 __global__ void lattice_token_k(const int* __restrict__ flags, uint32_t* __restrict__ token, uint32_t want) {
     *token = (flags[0] == 0 && flags[1] == 0) ? want : 0u;
 }
@@ -914,8 +945,8 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
         set_error("%s: plan needs %lld ints", fn, (long long)need_ints);
         return VB_ERR_WORKSPACE;
     }
-    if (!stats_out || !elems || !row_ptr || !col_idx || elem_ld < ne) {
-        set_error("%s: NULL argument or elem_ld < ne", fn);
+    if (!stats_out || !elems || (row_ptr == nullptr) != (col_idx == nullptr) || elem_ld < ne) {
+        set_error("%s: NULL argument, only one of row_ptr / col_idx, or elem_ld < ne", fn);
         return VB_ERR_ARG;
     }
     if (!aligned16(plan)) { set_error("%s: plan must be 16-byte aligned", fn); return VB_ERR_ARG; }
@@ -961,9 +992,11 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     lattice_check_elems_k<<<grid_for(ne, 256, 8), 256, 0, s>>>(ne, nn, elems, elem_ld, g, bits, flags);
     vb_status st = launch_check(fn);
     if (st != VB_OK) return st;
-    lattice_check_csr_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, nnz, row_ptr, col_idx, g, h.id0, h.dI, h.dJ, h.dK,
-                                                             h.ord, flags);
-    if ((st = launch_check(fn)) != VB_OK) return st;
+    if (row_ptr) {   // NULL, NULL: the pattern comes from fem_lattice_pattern (the stencil by construction)
+        lattice_check_csr_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, nnz, row_ptr, col_idx, g, h.id0, h.dI, h.dJ, h.dK,
+                                                                 h.ord, flags);
+        if ((st = launch_check(fn)) != VB_OK) return st;
+    }
     // header + lanes
     int32_t hdr[LAT_HDR] = {0};
     hdr[1] = nx; hdr[2] = ny; hdr[3] = nz;
@@ -988,6 +1021,52 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     else stats_out[0] = 1;
     stats_out[3] = h.fx | h.fy << 1 | h.fz << 2 | (int64_t)G << 8;   // orientation, and the grid the ranges are for
     return VB_OK;
+}
+
+// nnz of the lattice stencil: direction d is present at (nx+1-|dx|)(ny+1-|dy|)(nz+1-|dz|) nodes
+static int64_t lat_nnz(int nx, int ny, int nz) {
+    int64_t n = 0;
+    for (int d = 0; d < 15; d++)
+        n += (int64_t)(nx + 1 - std::abs(dir_dx(d))) * (ny + 1 - std::abs(dir_dy(d))) * (nz + 1 - std::abs(dir_dz(d)));
+    return n;
+}
+
+extern "C" VB_API vb_status fem_lattice_pattern(int64_t nn, int nx, int ny, int nz, int flips, void* work,
+                                                size_t* work_bytes, int32_t* row_ptr, int32_t* col_idx,
+                                                int64_t col_cap, int64_t* nnz_out, vb_stream_t stream) {
+    const char* fn = "fem_lattice_pattern";
+    clear_error();
+    if (nx < 1 || ny < 1 || nz < 1 || (int64_t)(nx + 1) * (ny + 1) * (nz + 1) != nn || !work_bytes) {
+        set_error("%s: nx, ny, nz >= 1, nn = (nx+1)(ny+1)(nz+1) and work_bytes non-NULL are required", fn);
+        return VB_ERR_ARG;
+    }
+    const int64_t nnz = lat_nnz(nx, ny, nz);
+    if (nnz >= ((int64_t)1 << 31)) { set_error("%s: nnz=%lld does not fit int32", fn, (long long)nnz); return VB_ERR_OVERFLOW; }
+    if (nnz_out) *nnz_out = nnz;
+    const size_t len_bytes = ((size_t)(nn + 1) * 4 + 255) & ~(size_t)255;
+    const size_t wb = len_bytes + scan_tmp_bytes(nn);
+    if (!work) {
+        *work_bytes = wb;
+        return VB_OK;
+    }
+    if (*work_bytes < wb) { set_error("%s: work_bytes %zu < %zu", fn, *work_bytes, wb); return VB_ERR_WORKSPACE; }
+    if (!row_ptr || !col_idx || col_cap < nnz) { set_error("%s: NULL row_ptr / col_idx or col_cap < nnz=%lld", fn, (long long)nnz); return VB_ERR_ARG; }
+    const int fl[3] = {flips & 1, (flips >> 1) & 1, (flips >> 2) & 1};
+    LatHost h;
+    if (nx < 2 || ny < 2 || !lat_host(nx, ny, nz, fl, h)) {
+        set_error("%s: lattice outside the kernel's limits (nx, ny >= 2)", fn);
+        return VB_ERR_UNSUPPORTED;
+    }
+    LatGeom g{nx, ny, nz, h.fx, h.fy, h.fz, (int64_t)nx + 1, (int64_t)ny + 1};
+    cudaStream_t s = cs(stream);
+    int32_t* row_len = reinterpret_cast<int32_t*>(work);
+    void* scan_tmp = static_cast<char*>(work) + len_bytes;
+    lattice_rowlen_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, g, row_len);
+    vb_status st = launch_check(fn);
+    if (st != VB_OK) return st;
+    if ((st = exclusive_scan_i32(row_len, row_ptr, nn, scan_tmp, s, nullptr)) != VB_OK) return st;
+    lattice_cols_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, g, h.id0, h.dI, h.dJ, h.dK, h.ord, row_ptr, col_idx);
+    return launch_check(fn);
 }
 
 extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* coords, int64_t node_stride,

@@ -48,7 +48,7 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
            "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi", "fem_plan_lattice",
-           "fem_p1_assemble_lattice")
+           "fem_p1_assemble_lattice", "fem_lattice_pattern")
 
 
 class VbError(RuntimeError):
@@ -101,6 +101,7 @@ def lib():
             "fem_plan_lattice": (i32, [i64, i64, p, i64, p, p, i64, i32, i32, i32, p, sz, p, C.POINTER(C.c_int64),
                                        C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_lattice": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, i32, p, p, p, p]),
+            "fem_lattice_pattern": (i32, [i64, i32, i32, i32, i32, p, sz, p, p, i64, C.POINTER(C.c_int64), p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -325,6 +326,52 @@ class P1Plan:
         self.compact = (self.dim == 3 and gather_plan and self.stats[0] <= 15 and self.stats[1] <= 16 * 32
                         and self.stats[2] <= 25 * 32)
         self.node_elem_slot16 = self.pack_slots() if self.compact else None
+
+    @classmethod
+    def for_lattice(cls, elems, nn, dims=None, stream=None):
+        """Plan of a Kuhn-lattice mesh without the generic pattern build: fem_plan_lattice verifies the
+        elements (row_ptr = col_idx = NULL), fem_lattice_pattern writes the stencil pattern in closed form
+        (bit-identical to fem_p1_pattern's).  dims: (nx, ny, nz), None = a cube inferred from ne.  Returns the
+        plan (pattern + lattice plan; no scatter map, no gather plan), or None if the mesh is refused."""
+        if elems.dtype != torch.int32:
+            raise TypeError("elems must be int32")
+        nv, ne = elems.shape
+        if nv != 4:
+            return None
+        if dims is None:
+            n = int(round((ne / 6) ** (1.0 / 3.0))) if ne > 0 else 0
+            dims = (n, n, n)
+        nx, ny, nz = (int(d) for d in dims)
+        if nx < 2 or ny < 2 or nz < 1 or (nx + 1) * (ny + 1) * (nz + 1) != nn or 6 * nx * ny * nz != ne:
+            return None   # the kernel needs nx, ny >= 2
+        self = cls.__new__(cls)
+        self.dim, self.nn, self.ne, self.nv = 3, int(nn), int(ne), 4
+        dev = elems.device
+        L = lib()
+        st = _stream(stream)
+        wb, pints, nnz, pwb = C.c_size_t(0), C.c_int64(0), C.c_int64(0), C.c_size_t(0)
+        stats = (C.c_int64 * 4)()
+        _check(L.fem_lattice_pattern(nn, nx, ny, nz, 0, None, C.byref(pwb), None, None, 0, C.byref(nnz), st))
+        self.nnz = int(nnz.value)
+        _check(L.fem_plan_lattice(nn, ne, None, ne, None, None, self.nnz, nx, ny, nz, None, C.byref(wb), None,
+                                  C.byref(pints), stats, st))
+        work = torch.empty((max(wb.value, pwb.value, 16),), dtype=torch.uint8, device=dev)
+        plan = torch.zeros((max(int(pints.value), 16),), dtype=torch.int32, device=dev)
+        _check(L.fem_plan_lattice(nn, ne, _ptr(elems), elems.shape[1], None, None, self.nnz, nx, ny, nz, _ptr(work),
+                                  C.byref(wb), _ptr(plan), C.byref(pints), stats, st))
+        if stats[0] != 1:
+            return None
+        self.row_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
+        self.col_idx_padded = torch.zeros((_pad4(self.nnz),), dtype=torch.int32, device=dev)
+        _check(L.fem_lattice_pattern(nn, nx, ny, nz, int(stats[3]) & 7, _ptr(work), C.byref(pwb), _ptr(self.row_ptr),
+                                     _ptr(self.col_idx_padded), self.col_idx_padded.numel(), C.byref(nnz), st))
+        self.col_idx = self.col_idx_padded[:self.nnz]
+        self.elem2nnz = self.node_elem_ptr = self.node_elem = self.node_elem_slot = None
+        self.node_elem_slot16, self.compact, self.work, self.stats = None, False, None, (15, 0, 0)
+        self.lattice_plan, self.lattice_dims = plan, (nx, ny, nz)
+        self.lattice_flips, self.lattice_tiles = int(stats[3]), int(stats[1])
+        self.lattice_ok, self.lattice_reason = True, ""
+        return self
 
     def classes(self):
         """Row classes of the gather plan (fem_plan_classes), built once and kept:

@@ -125,6 +125,11 @@ def test_lattice_plan_query_and_argument_errors(L):
     assert wb.value > 6 * 128 ** 3 // 8 and (pi.value - 16 - 1025) % 128 == 0 and pi.value > 16 + 1025
     assert L.fem_plan_lattice(8, 6, None, 6, None, None, 0, 0, 1, 1, None, C.byref(wb), None, C.byref(pi), stats,
                               None) == -1
+    # closed-form pattern: nnz of the 15-point stencil (query, no GPU) = sum over directions of the node boxes
+    nz_ = C.c_int64(0)
+    assert L.fem_lattice_pattern(129 ** 3, 128, 128, 128, 0, None, C.byref(wb), None, None, 0, C.byref(nz_), None) == 0
+    assert nz_.value == 31802497 and wb.value > 4 * 129 ** 3
+    assert L.fem_lattice_pattern(28, 2, 2, 2, 0, None, C.byref(wb), None, None, 0, C.byref(nz_), None) == -1
     # the assembly refuses inconsistent counts and lattices below the kernel's limits, before any CUDA call
     assert L.fem_p1_assemble_lattice(9, FAKE, 1, 9, FAKE, 0, FAKE, 1, 1, 1, 0, FAKE, FAKE, None, None) == -1
     assert L.fem_p1_assemble_lattice(18, FAKE, 1, 18, FAKE, 0, FAKE, 1, 2, 2, 0, FAKE, FAKE, None, None) == -1

@@ -157,6 +157,34 @@ def test_lattice_plan_abi_errors(dev):
     assert L.fem_p1_assemble_lattice(9, None, 1, 9, None, 0, None, 1, 1, 1, 0, None, None, None, None) == -1
 
 
+@pytest.mark.parametrize("dims,flip", [((2, 2, 1), (0, 0, 0)), ((3, 4, 5), (0, 1, 0)), ((31, 2, 2), (1, 0, 0)),
+                                       ((12, 13, 14), (0, 0, 1)), ((33, 25, 3), (1, 1, 0)), ((7, 7, 7), (1, 1, 1))])
+def test_lattice_pattern_closed_form_bit_exact(dev, dims, flip):
+    """fem_lattice_pattern (the stencil written directly) against the oracle's pattern built from the elements,
+    for every orientation, shuffled elements; then K, M assembled on that plan against the oracle."""
+    coords, elems = synth.box_kuhn_p1(*dims, jitter=0.05, seed=5, flip=flip)
+    rng = np.random.default_rng(1)
+    elems = np.ascontiguousarray(elems[:, rng.permutation(elems.shape[1])])
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    plan = vb.P1Plan.for_lattice(g(elems, dev), nn, dims=dims)
+    assert plan is not None
+    assert plan.nnz == int(rp[-1])
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan)
+    assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+
+
+def test_lattice_pattern_refuses_non_lattices(dev):
+    coords, elems = synth.cube_kuhn_p1(6, jitter=0.05, seed=0)
+    bad = elems.copy()
+    bad[:, 7] = bad[:, 8]                      # one element twice, one missing
+    assert vb.P1Plan.for_lattice(g(bad, dev), coords.shape[1]) is None
+    cd, ed = synth.delaunay_p1(3, 6, seed=1)
+    assert vb.P1Plan.for_lattice(g(ed, dev), cd.shape[1]) is None
+
+
 def test_full_size_configs4_every_entry_vs_oracle(dev):
     # BASELINE configs[4] in bench.py's launch configuration: all 31.8 M entries of K and M vs the full oracle
     coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
@@ -169,3 +197,8 @@ def test_full_size_configs4_every_entry_vs_oracle(dev):
     K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan)   # variant None -> lattice
     assert relmax(h(K), Ko) <= TOL
     assert relmax(h(M), Mo) <= TOL
+    # bench.py's plan: the closed-form pattern, bit-identical, and the same K, M bits on it
+    fast = vb.P1Plan.for_lattice(g(elems, dev), nn)
+    assert fast is not None and np.array_equal(h(fast.row_ptr), rp) and np.array_equal(h(fast.col_idx), ci)
+    K2, M2, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), fast)
+    assert torch.equal(K2, K) and torch.equal(M2, M)
