@@ -505,6 +505,23 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                             rk[ORD.slot[8 + e]] = iK[e];
                             rm[ORD.slot[8 + e]] = iM[e];
                         }
+                    } else if (px && !mx && py && my && pz && mz) {
+                        // a row of the face x = 0 (no -x, -xy, -xz, -xyz columns), one lane of every tile that
+                        // starts a line: compile-time slots as well (the general path below, run by the whole
+                        // warp for that one lane, made these tiles 13 % slower)
+                        constexpr uint32_t PX0 = 0x7fffu & ~(1u << 8 | 1u << 11 | 1u << 12 | 1u << 14);
+                        rlen = 11;
+                        rk[__popc(PX0 & ORD.low[0])] = -sK;
+                        rm[__popc(PX0 & ORD.low[0])] = sM * (2.0 / 3.0);
+#pragma unroll
+                        for (int e = 0; e < 7; e++) {
+                            rk[__popc(PX0 & ORD.low[1 + e])] = eK[e];
+                            rm[__popc(PX0 & ORD.low[1 + e])] = eM[e];
+                            if (PX0 >> (8 + e) & 1) {
+                                rk[__popc(PX0 & ORD.low[8 + e])] = iK[e];
+                                rm[__popc(PX0 & ORD.low[8 + e])] = iM[e];
+                            }
+                        }
                     } else {   // boundary row: the present columns, same order
                         uint32_t pres = 1u;
                         pres |= (uint32_t)px << 1 | (uint32_t)py << 2 | (uint32_t)pz << 3 |
@@ -710,6 +727,10 @@ __global__ void lattice_cols_k(int64_t nn, LatGeom g, int64_t id0, int64_t dI, i
     }
 }
 
+__global__ void lattice_elem0_k(const int32_t* __restrict__ elems, int64_t eld, int32_t* __restrict__ out) {
+    out[threadIdx.x] = elems[threadIdx.x * eld];
+}
+
 __global__ void lattice_token_k(const int* __restrict__ flags, uint32_t* __restrict__ token, uint32_t want) {
     *token = (flags[0] == 0 && flags[1] == 0) ? want : 0u;
 }
@@ -771,15 +792,16 @@ uint32_t lat_want(const LatHost& h, int64_t nn, int64_t nnz, int G) {
 }
 
 // Cost of one tile-layer in SM cycles (measured on B200 with the per-CTA clock64 of the VB_LAT_PROF build,
-// tools/latprof_run.py, configs[4]): a fixed part (barriers and the latency chains of a step) and a part per
-// warp row holding nodes: 12 rows 6440, 7 rows 5140; a band without a halo row owns all its rows (the
-// boundary row J = 0: +250).  A tile whose segment holds x = 0 or x = nx runs the masked cell path (absent
-// cells) and the boundary row path in every warp: x 1.13.  Packed tiles (always holding x = nx; plain stores,
-// one pass per segment): x 0.96 with 2 segments, x 1.62 with 5.
+// tools/latprof_run.py + latprof_sum.py, configs[4], refitted after every kernel change): a fixed part
+// (barriers and the latency chains of a step) and a part per warp row holding nodes: 12 rows 6230, 7 rows
+// 5160; a band without a halo row owns all its rows (the boundary row J = 0: +255).  A tile whose segment
+// holds x = 0 or x = nx runs the masked cell path (absent cells) and a boundary-row path in every warp:
+// x 1.11.  Packed tiles (always holding x = nx; plain stores, one pass per segment): x 1.0 with 2
+// segments, x 1.7 with 5.
 int lat_cost(int rows, int row0_owned, int xbnd = 0, int nseg = 0) {   // nseg > 0: a packed tile
-    const int c = 3320 + 260 * rows + (row0_owned ? 250 : 0);
-    const int packed = 735 + 220 * (nseg - 1);   // per mille
-    return (int)((int64_t)c * (xbnd ? 113 : 100) / 100 * (nseg > 0 ? packed : 1000) / 1000);
+    const int c = 3662 + 214 * rows + (row0_owned ? 255 : 0);
+    const int packed = 765 + 235 * (nseg - 1);   // per mille
+    return (int)((int64_t)c * (xbnd ? 111 : 100) / 100 * (nseg > 0 ? packed : 1000) / 1000);
 }
 
 // short segments (W lanes: a halo and W - 1 owned nodes) packed into one tile: as many as the lanes and the
@@ -960,8 +982,10 @@ extern "C" VB_API vb_status fem_plan_lattice(int64_t nn, int64_t ne, const int32
     cudaStream_t s = cs(stream);
     // orientation from element 0: the vertex pair at lattice distance 3 is the split diagonal
     int32_t v0[4];
-    for (int a = 0; a < 4; a++) {
-        vb_status st = read_small(s, elems + a * elem_ld, 4, &v0[a], fn);
+    {   // the four vertex ids of element 0 in one read-back
+        lattice_elem0_k<<<1, 4, 0, s>>>(elems, elem_ld, reinterpret_cast<int32_t*>(work));
+        vb_status st = launch_check(fn);
+        if (st == VB_OK) st = read_small(s, work, sizeof(v0), v0, fn);
         if (st != VB_OK) return st;
     }
     int flip[3] = {0, 0, 0};
