@@ -1,4 +1,4 @@
-tag=r02v
+tag=${1:-r02}
 CMD="python bench.py --steps 20 --warmup 3 --quick --no-e2e --no-cpu"
 $CMD > gpurun_out/bench_quick_$tag.json 2> gpurun_out/bench_quick_$tag.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$tag.csv $CMD > gpurun_out/ncu_launch_$tag.log 2>&1 && \
