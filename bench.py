@@ -566,8 +566,10 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
     p4 = vb.P1Plan(ed4, c4.shape[1])
     K4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
     M4 = torch.empty(p4.nnz, dtype=torch.float64, device=dev)
-    for name, mode in (("class", vb.VB_ASSEMBLE_GATHER), ("block", vb.VB_ASSEMBLE_GATHER),
-                       ("tile", vb.VB_ASSEMBLE_GATHER), ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
+    assert p4.lattice(ed4), p4.lattice_reason
+    for name, mode in (("lattice", vb.VB_ASSEMBLE_GATHER), ("class", vb.VB_ASSEMBLE_GATHER),
+                       ("block", vb.VB_ASSEMBLE_GATHER), ("tile", vb.VB_ASSEMBLE_GATHER),
+                       ("atomic", vb.VB_ASSEMBLE_ATOMIC)):
         gv = None if name == "atomic" else name
         rec("config4 2D assembly variant=%s" % name, e4.shape[1], "elements",
             alg_bytes_assembly(2, c4.shape[1], e4.shape[1], p4.nnz),

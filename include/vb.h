@@ -429,6 +429,35 @@ VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* coords, int64
                                          const int32_t* plan, int nx, int ny, int nz, int flips, double* K_vals,
                                          double* M_vals, int64_t* degenerate, vb_stream_t stream);
 
+/* ---------------------------------------------------------- 2D lattice (element-once) variant
+ * The 2D counterpart of the Kuhn-lattice variant, for BASELINE configs[0] and
+ * configs[3]: the same K, M as fem_p1_assemble (dim = 2, c = 1; eq:K_M
+ * P:967-975) for meshes whose nodes are (i, j), 0 <= i <= nx,
+ * 0 <= j <= ny, id = i + (nx+1) j (coordinates arbitrary, e.g. jittered), every
+ * cell split into two triangles by the same diagonal (either one; element
+ * order and vertex order free).  fem_plan_lattice2d verifies that once per
+ * mesh (elements and the 7-point CSR stencil) and writes the plan (token,
+ * dims, the range of (x segment, node row) items of every resident warp of the
+ * current device); arguments, work / plan query, stats_out ([0] accepted, [1]
+ * x segments, [2] refusal reason 1 counts, 2 element 0, 3 nx < 2, 4 an
+ * element, 5 the pattern, [3] the `flips` value for the assembly: bit 0 the
+ * diagonal, bits 8.. the number of warps) and errors as fem_plan_lattice.
+ * fem_p1_assemble_lattice2d: a warp marches along y over one x segment (31
+ * nodes), both triangles of a cell evaluated once, contributions passed by
+ * shuffle (x) and registers (y), no shared-memory exchange, no barrier; rows
+ * (diagonals by the partition of unity, K_pp = -sum K_pq, M_pp = sum M_pq)
+ * staged in CSR order and written once by TMA bulk copies (K, M 16-byte
+ * aligned; plain stores otherwise).  Deterministic, bitwise reproducible.
+ * degenerate: nullable DEVICE int64, the number of triangles with det = 0. */
+VB_API vb_status fem_plan_lattice2d(int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
+                                    const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz, int nx, int ny,
+                                    void* work, size_t* work_bytes, int32_t* plan, int64_t* plan_ints,
+                                    int64_t* stats_out, vb_stream_t stream);
+VB_API vb_status fem_p1_assemble_lattice2d(int64_t nn, const double* coords, int64_t node_stride,
+                                           int64_t comp_stride, const int32_t* row_ptr, int64_t nnz,
+                                           const int32_t* plan, int nx, int ny, int flips, double* K_vals,
+                                           double* M_vals, int64_t* degenerate, vb_stream_t stream);
+
 /* ---------------------------------------------------------- exact-order check
  * The verification path of SURVEY §8(c) ("bitwise mode"): K and M (c = 1) with
  * every operation of the definition as an IEEE round-to-nearest fp64

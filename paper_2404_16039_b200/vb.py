@@ -48,7 +48,7 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
            "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi", "fem_plan_lattice",
-           "fem_p1_assemble_lattice", "fem_lattice_pattern")
+           "fem_p1_assemble_lattice", "fem_lattice_pattern", "fem_plan_lattice2d", "fem_p1_assemble_lattice2d")
 
 
 class VbError(RuntimeError):
@@ -102,6 +102,9 @@ def lib():
                                        C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_lattice": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, i32, p, p, p, p]),
             "fem_lattice_pattern": (i32, [i64, i32, i32, i32, i32, p, sz, p, p, i64, C.POINTER(C.c_int64), p]),
+            "fem_plan_lattice2d": (i32, [i64, i64, p, i64, p, p, i64, i32, i32, p, sz, p, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64), p]),
+            "fem_p1_assemble_lattice2d": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, p, p, p, p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -450,9 +453,8 @@ class P1Plan:
         if getattr(self, "lattice_ok", None) is not None:
             return self.lattice_ok
         self.lattice_ok, self.lattice_reason = False, ""
-        if self.dim != 3:
-            self.lattice_reason = "not 3D"
-            return False
+        if self.dim == 2:
+            return self._lattice2d(elems, dims)
         if dims is None:
             n = int(round((self.ne / 6) ** (1.0 / 3.0))) if self.ne > 0 else 0
             dims = (n, n, n)
@@ -483,6 +485,37 @@ class P1Plan:
         self.lattice_dims = (nx, ny, nz)
         self.lattice_flips = int(stats[3])
         self.lattice_tiles = int(stats[1])
+        self.lattice_ok = True
+        return True
+
+    def _lattice2d(self, elems, dims):
+        """fem_plan_lattice2d: dims (nx, ny), None = a square inferred from ne."""
+        if dims is None:
+            n = int(round((self.ne / 2) ** 0.5)) if self.ne > 0 else 0
+            dims = (n, n)
+        nx, ny = (int(d) for d in dims[:2])
+        if nx < 2 or ny < 1 or (nx + 1) * (ny + 1) != self.nn or 2 * nx * ny != self.ne:
+            self.lattice_reason = "counts are not those of a %d x %d triangulated lattice" % (nx, ny)
+            return False
+        L = lib()
+        dev = self.row_ptr.device
+        wb, pints, st = C.c_size_t(0), C.c_int64(0), _stream()
+        stats = (C.c_int64 * 4)()
+        _check(L.fem_plan_lattice2d(self.nn, self.ne, None, self.ne, None, None, self.nnz, nx, ny, None, C.byref(wb),
+                                    None, C.byref(pints), stats, st))
+        work = torch.empty((max(wb.value, 16),), dtype=torch.uint8, device=dev)
+        plan = torch.zeros((max(int(pints.value), 16),), dtype=torch.int32, device=dev)
+        _check(L.fem_plan_lattice2d(self.nn, self.ne, _ptr(elems), elems.shape[1], _ptr(self.row_ptr),
+                                    _ptr(self.col_idx), self.nnz, nx, ny, _ptr(work), C.byref(wb), _ptr(plan),
+                                    C.byref(pints), stats, st))
+        reasons = {1: "counts", 2: "element 0 is not a triangle of a cell", 3: "nx < 2",
+                   4: "an element is not a triangle of the lattice (or appears twice)",
+                   5: "the CSR pattern is not the lattice stencil"}
+        if stats[0] != 1:
+            self.lattice_reason = reasons.get(int(stats[2]), "refused (%d)" % stats[2])
+            return False
+        self.lattice_plan, self.lattice_dims = plan, (nx, ny)
+        self.lattice_flips, self.lattice_tiles = int(stats[3]), int(stats[1])
         self.lattice_ok = True
         return True
 
@@ -532,6 +565,12 @@ def fem_p1_assemble_lattice(coords, plan, K=None, M=None, want_K=True, want_M=Tr
         raise ValueError("plan has no lattice plan: call plan.lattice(elems) first (and check it returned True)")
     K = (K if K is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_K else None
     M = (M if M is not None else torch.empty((plan.nnz,), dtype=torch.float64, device=dev)) if want_M else None
+    if len(plan.lattice_dims) == 2:
+        nx, ny = plan.lattice_dims
+        _check(lib().fem_p1_assemble_lattice2d(nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr), plan.nnz,
+                                               _ptr(plan.lattice_plan), nx, ny, plan.lattice_flips, _ptr(K), _ptr(M),
+                                               _ptr(degenerate), _stream(stream)))
+        return K, M
     nx, ny, nz = plan.lattice_dims
     _check(lib().fem_p1_assemble_lattice(nn, _ptr(coords), 1, nn, _ptr(plan.row_ptr), plan.nnz,
                                          _ptr(plan.lattice_plan), nx, ny, nz, plan.lattice_flips, _ptr(K), _ptr(M),
@@ -621,7 +660,7 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
     if variant == "tile":
         variant = "block"   # outside the tile variant's limits (plan.tile_reason)
     if (mode == VB_ASSEMBLE_GATHER and variant in (None, "lattice") and (K is not None or M is not None)
-            and dim == 3 and plan.lattice(elems)):
+            and plan.lattice(elems)):
         fem_p1_assemble_lattice(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream,
                                 degenerate=degenerate)
         if want_local:

@@ -17,14 +17,14 @@ Layouts produced here are the ones the C ABI consumes (include/vb.h):
   (vertex a of element e at ``elems[a, e]``, elem_ld = ne).
 """
 from .rng import splitmix64_u64, uniform01, uniform_pm1, normal
-from .meshes import (square_p1, square_crossed_p1, cube_kuhn_p1, box_kuhn_p1, icosphere, square_counts,
+from .meshes import (square_p1, rect_p1, square_crossed_p1, cube_kuhn_p1, box_kuhn_p1, icosphere, square_counts,
                      cube_counts, icosphere_counts, p2_from_p1, P2_EDGES, delaunay_p1,
                      permute_mesh)
 from .pages import normal_pages, inverse_pages, integer_pages
 
 __all__ = [
     "splitmix64_u64", "uniform01", "uniform_pm1", "normal",
-    "square_p1", "square_crossed_p1", "cube_kuhn_p1", "box_kuhn_p1", "icosphere",
+    "square_p1", "rect_p1", "square_crossed_p1", "cube_kuhn_p1", "box_kuhn_p1", "icosphere",
     "square_counts", "cube_counts", "icosphere_counts", "delaunay_p1", "permute_mesh",
     "normal_pages", "inverse_pages", "integer_pages",
 ]

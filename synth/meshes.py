@@ -80,6 +80,36 @@ def square_p1(n, jitter=0.1, seed=0):
     return coords, elems
 
 
+def rect_p1(nx, ny, jitter=0.1, seed=0, flip=0):
+    """square_p1's recipe on nx x ny cells of side h = 1/max(nx, ny): node id = i + (nx+1) j, cells x-fastest, two
+    triangles per cell along the diagonal (0,0)-(1,1) (flip = 0: (v00, v10, v11), (v00, v11, v01)) or
+    (1,0)-(0,1) (flip = 1: (v00, v10, v01), (v10, v11, v01)); interior nodes jittered by jitter * h."""
+    m = max(nx, ny)
+    nx1 = nx + 1
+    nn = nx1 * (ny + 1)
+    v = np.arange(nn, dtype=np.int64)
+    i, j = v % nx1, v // nx1
+    coords = np.empty((2, nn), dtype=np.float64)
+    coords[0], coords[1] = i / m, j / m
+    if jitter:
+        r = uniform_pm1(seed, JITTER_STREAM, 2 * nn).reshape(nn, 2)
+        inner = (i > 0) & (i < nx) & (j > 0) & (j < ny)
+        coords[0, inner] += jitter / m * r[inner, 0]
+        coords[1, inner] += jitter / m * r[inner, 1]
+    c = np.arange(nx * ny, dtype=np.int64)
+    v00 = c % nx + nx1 * (c // nx)
+    v10, v01 = v00 + 1, v00 + nx1
+    v11 = v01 + 1
+    elems = np.empty((3, 2 * nx * ny), dtype=np.int32)
+    if flip:
+        elems[:, 0::2] = np.stack([v00, v10, v01])
+        elems[:, 1::2] = np.stack([v10, v11, v01])
+    else:
+        elems[:, 0::2] = np.stack([v00, v10, v11])
+        elems[:, 1::2] = np.stack([v00, v11, v01])
+    return coords, elems
+
+
 _KUHN_PERMS = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
 
 
