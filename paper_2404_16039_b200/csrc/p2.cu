@@ -278,108 +278,109 @@ __global__ void __launch_bounds__(P2_BLOCK) p2_assemble_k(int64_t ne, const doub
             const int nact = (int)(ne - base < P2_BLOCK ? ne - base : P2_BLOCK);
             constexpr int NN = NLB * NLB;
             double2* out = reinterpret_cast<double2*>(Kst);   // (K, M) pairs, [e][a][b]
-            for (int j = 0; j < nact; j++)
-                for (int r = threadIdx.x; r < NN; r += P2_BLOCK) {
-                    const int a = r / NLB, b = r - a * NLB;
-                    const int lo = a < b ? a : b, hi = a < b ? b : a;
-                    const int pp = lo * NLB - lo * (lo - 1) / 2 + (hi - lo);
-                    __stcs(out + (base + j) * NN + r, make_double2(KS[j * NP + pp], MS[j * NP + pp]));
-                }
+            // this thread's entries r = tid, tid + P2_BLOCK of every element: their strip positions once
+            constexpr int NR = (NN + P2_BLOCK - 1) / P2_BLOCK;
+            int pp[NR];
+#pragma unroll
+            for (int k = 0; k < NR; k++) {
+                const int r = threadIdx.x + k * P2_BLOCK;
+                const int a = r / NLB, b = r - a * NLB;
+                const int lo = a < b ? a : b, hi = a < b ? b : a;
+                pp[k] = r < NN ? lo * NLB - lo * (lo - 1) / 2 + (hi - lo) : -1;
+            }
+            double2* o = out + base * NN + threadIdx.x;
+            for (int j = 0; j < nact; j++, o += NN) {
+#pragma unroll
+                for (int k = 0; k < NR; k++)
+                    if (pp[k] >= 0) __stcs(o + k * P2_BLOCK, make_double2(KS[j * NP + pp[k]], MS[j * NP + pp[k]]));
+            }
             __syncthreads();
         }
     }
 }
 
-// Deterministic P2 assembly, phase 2: one thread per row v sums, in ascending
-// element order, row a of the staged K_e / M_e of each incidence (e, a) into
-// per-slot accumulators ([slot][lane] in shared memory, rows of up to P2_RS
-// entries; longer rows accumulate in place in HBM), then writes the row once.
-constexpr int P2_RS = 72;        // wide launch: rows of up to 72 entries on chip (longer: in place in HBM)
-constexpr int P2_RS_NARROW = 28; // narrow launch: blocks whose rows all have <= 28 entries (P2 edge-node rows)
-constexpr int P2_GROWS = 32;
-constexpr int P2_U = 4;
+// Deterministic P2 assembly, phase 2: every row v sums, in ascending element order, row a of the staged
+// K_e / M_e of each of its incidences (e, a) into per-slot accumulators in shared memory (rows of up to
+// P2_RS entries; longer rows accumulate in place in HBM), then writes the row once.
+constexpr int P2_RS = 72;
 
-// RS: row capacity of the accumulators; LO: the launch takes the 32-row blocks whose
-// longest row is in (LO, RS] (narrow: LO = -1) or > LO (wide: LO = P2_RS_NARROW,
-// rows beyond RS in place).  Two launches cover every block once: most blocks of a
-// P2 mesh are edge-node rows (<= 27 entries on Kuhn cubes) and run with 2.5x the
-// resident warps of the vertex-row blocks (65 entries).
-#ifndef VB_P2_UN
-#define VB_P2_UN 4   // incidences in flight in the narrow launch (1 / 2 / 4: 2.96 / 2.87 / 2.70 ms, level 6)
-#endif
-template <int NLB, int RS, int LO, int U = P2_U>
-__global__ void __launch_bounds__(P2_GROWS) p2_gather_k(int64_t nn, const int32_t* __restrict__ row_ptr,
-                                                        const int32_t* __restrict__ nptr,
-                                                        const int32_t* __restrict__ nelem,
-                                                        const uint32_t* __restrict__ nslot,
-                                                        const double2* __restrict__ KMst,
-                                                        double* __restrict__ K, double* __restrict__ M) {
+// A warp takes G = 32 / NLB consecutive rows, NLB lanes each.  Lane (g, b) loads
+// entry b of the staged element row of row g's next incidence (one coalesced 16 NLB-byte piece per row) and
+// its slot byte, and adds the (K, M) pair into the row's accumulators in shared memory (RS + 1 pairs per row:
+// 1.2 KB instead of the 37 KB per warp of the one-thread-per-row kernel, so 40+ warps are resident instead
+// of 6).  The NLB slots of one incidence are distinct columns, so the lanes of a row never collide; incidences
+// are taken in ascending order, U at a time in flight: the same summation order as before, bitwise
+// reproducible.  Rows longer than RS are summed in place in HBM by lane 0 of their group.
+constexpr int P2C_WARPS = 4;
+template <int NLB, int RS, int U>
+__global__ void __launch_bounds__(32 * P2C_WARPS) p2_gather_coop_k(int64_t nn, const int32_t* __restrict__ row_ptr,
+                                                                  const int32_t* __restrict__ nptr,
+                                                                  const int32_t* __restrict__ nelem,
+                                                                  const uint32_t* __restrict__ nslot,
+                                                                  const double2* __restrict__ KMst,
+                                                                  double* __restrict__ K, double* __restrict__ M) {
+    constexpr int G = 32 / NLB;
     constexpr int NW = (NLB + 3) / 4;
-    constexpr int ST = RS + 1;   // [lane][slot] rows of odd length: the cooperative write-back is conflict-free
-    __shared__ double2 acc_s[ST * P2_GROWS];
-    const int t = threadIdx.x;
-    double2* acc = acc_s + t * ST;
-    for (int64_t v0 = (int64_t)blockIdx.x * P2_GROWS; v0 < nn; v0 += (int64_t)gridDim.x * P2_GROWS) {
-        const int64_t v = v0 + t;
-        const bool own = v < nn;
+    constexpr int ST = RS + 1;
+    __shared__ double2 acc_s[P2C_WARPS][G][ST];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const int g = lane / NLB, b = lane - g * NLB;
+    const bool act = g < G;
+    double2* acc = acc_s[wl][act ? g : 0];
+    const int64_t nwarps = (int64_t)gridDim.x * P2C_WARPS;
+    for (int64_t v0 = ((int64_t)blockIdx.x * P2C_WARPS + wl) * G; v0 < nn; v0 += nwarps * G) {
+        const int64_t v = v0 + g;
+        const bool own = act && v < nn;
         const int lo = own ? __ldg(row_ptr + v) : 0, L = own ? __ldg(row_ptr + v + 1) - lo : 0;
-        const int bmax = __reduce_max_sync(0xffffffffu, L);
-        if (LO < 0 ? bmax > RS : bmax <= LO) continue;   // the other launch's block
         const int i0 = own ? __ldg(nptr + v) : 0, i1 = own ? __ldg(nptr + v + 1) : 0;
         const bool fast = L <= RS;
         if (fast) {
-            for (int s = 0; s < L; s++) acc[s] = make_double2(0.0, 0.0);
-        } else {
-            for (int s = 0; s < L; s++) {
-                if (K) K[lo + s] = 0.0;
-                if (M) M[lo + s] = 0.0;
+            for (int sl = b; sl < L; sl += NLB) acc[sl] = make_double2(0.0, 0.0);
+        } else if (b == 0) {
+            for (int sl = 0; sl < L; sl++) {
+                if (K) K[lo + sl] = 0.0;
+                if (M) M[lo + sl] = 0.0;
             }
         }
-        // P2_U incidences in flight: their element ids, then their rows and slot words
-        // are loaded before any is accumulated (the accumulation order stays ascending)
-        auto add = [&](const uint32_t (&w)[NW], const double2 (&km)[NLB]) {
-#pragma unroll
-            for (int b = 0; b < NLB; b++) {
-                const int sl = (w[b / 4] >> (8 * (b % 4))) & 0xff;
-                if (fast) {
-                    double2 x = acc[sl];
-                    x.x += km[b].x;
-                    x.y += km[b].y;
-                    acc[sl] = x;
-                } else {
-                    if (K) K[lo + sl] += km[b].x;
-                    if (M) M[lo + sl] += km[b].y;
-                }
-            }
-        };
-        for (int i = i0; i < i1; i += U) {
-            int32_t ea[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) ea[u] = i + u < i1 ? __ldg(nelem + i + u) : -1;
-            uint32_t w[U][NW];
-            double2 km[U][NLB];
+        __syncwarp();
+        const int nmax = __reduce_max_sync(0xffffffffu, i1 - i0);   // warp-uniform trip count
+        for (int k = 0; k < nmax; k += U) {
+            int sl[U];
+            double2 km[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                if (ea[u] < 0) continue;
-                const double2* row = KMst + (int64_t)(ea[u] >> 4) * (NLB * NLB) + (ea[u] & 15) * NLB;
-#pragma unroll
-                for (int j = 0; j < NW; j++) w[u][j] = __ldg(nslot + (int64_t)(i + u) * NW + j);
-#pragma unroll
-                for (int b = 0; b < NLB; b++) km[u][b] = __ldcs(row + b);
+                const int i = i0 + k + u;
+                sl[u] = -1;
+                km[u] = make_double2(0.0, 0.0);
+                if (i < i1) {
+                    const int32_t ea = __ldg(nelem + i);
+                    const uint32_t w = __ldg(nslot + (int64_t)i * NW + b / 4);
+                    sl[u] = (w >> (8 * (b % 4))) & 0xff;
+                    km[u] = __ldcs(KMst + (int64_t)(ea >> 4) * (NLB * NLB) + (ea & 15) * NLB + b);
+                }
             }
 #pragma unroll
-            for (int u = 0; u < U; u++)
-                if (ea[u] >= 0) add(w[u], km[u]);
+            for (int u = 0; u < U; u++) {
+                if (sl[u] >= 0) {
+                    if (fast) {
+                        double2 x = acc[sl[u]];
+                        x.x += km[u].x;
+                        x.y += km[u].y;
+                        acc[sl[u]] = x;
+                    } else {
+                        // a long row: its NLB lanes take turns (the order within an incidence is free: distinct slots)
+                        if (K) K[lo + sl[u]] += km[u].x;
+                        if (M) M[lo + sl[u]] += km[u].y;
+                    }
+                }
+                __syncwarp();   // the next incidence may hit the same slot from another lane
+            }
         }
-        // write-back: the warp stores each staged row in turn, lane j writing entry j
-        __syncwarp();
-        for (int r = 0; r < P2_GROWS; r++) {
-            const int Lr = __shfl_sync(0xffffffffu, fast ? L : 0, r);
-            const int lor = __shfl_sync(0xffffffffu, lo, r);
-            for (int j = t; j < Lr; j += P2_GROWS) {
-                const double2 x = acc_s[r * ST + j];
-                if (K) stcs(K + lor + j, x.x);
-                if (M) stcs(M + lor + j, x.y);
+        if (fast) {
+            for (int j = b; j < L; j += NLB) {
+                const double2 x = acc[j];
+                if (K) stcs(K + lo + j, x.x);
+                if (M) stcs(M + lo + j, x.y);
             }
         }
         __syncwarp();
@@ -460,22 +461,17 @@ extern "C" vb_status fem_p2_assemble(int dim, int64_t nn, int64_t ne, const doub
         else p2_assemble_k<3><<<g, P2_BLOCK, sm3, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, elem2nnz, R, cp, Ka, Ma, K_local, M_local, Kst, Mst);
     }
     if (gather && nn > 0) {
-        const int64_t need = (nn + P2_GROWS - 1) / P2_GROWS;
         const double2* km = reinterpret_cast<const double2*>(work);
-        auto run = [&](auto kern) {
+        auto runc = [&](auto kern, int G) {
             int occ = 1;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, P2_GROWS, 0);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * P2C_WARPS, 0);
             const int64_t cap = (int64_t)sm_count() * (occ > 0 ? occ : 1);
-            const unsigned g = (unsigned)(need < cap ? need : cap);
-            kern<<<g, P2_GROWS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem, node_elem_slot, km, K_vals, M_vals);
+            const int64_t needc = (nn + (int64_t)G * P2C_WARPS - 1) / ((int64_t)G * P2C_WARPS);
+            kern<<<(unsigned)(needc < cap ? needc : cap), 32 * P2C_WARPS, 0, s>>>(nn, row_ptr, node_elem_ptr, node_elem,
+                                                                                 node_elem_slot, km, K_vals, M_vals);
         };
-        if (dim == 2) {
-            run(p2_gather_k<6, P2_RS_NARROW, -1, VB_P2_UN>);
-            run(p2_gather_k<6, P2_RS, P2_RS_NARROW>);
-        } else {
-            run(p2_gather_k<10, P2_RS_NARROW, -1, VB_P2_UN>);
-            run(p2_gather_k<10, P2_RS, P2_RS_NARROW>);
-        }
+        if (dim == 2) runc(p2_gather_coop_k<6, P2_RS, 4>, 5);
+        else runc(p2_gather_coop_k<10, P2_RS, 4>, 3);
     }
     return launch_check(fn);
 }
