@@ -598,8 +598,8 @@ VB_API vb_status fem_pattern(int nv, int64_t nn, int64_t ne,
  *   accumulated with fp64 atomics through elem2nnz (fem_pattern); work unused.
  * mode VB_ASSEMBLE_GATHER: deterministic.  Call with work == NULL to query
  *   *work_bytes (2 nlb^2 ne doubles + 16; nothing else happens).  The element
- *   matrices are computed once into `work` (element-major), then one thread
- *   per row sums its incidences' rows of them
+ *   matrices are computed once into `work` (element-major), then every row
+ *   sums its incidences' rows of them (a few rows per warp, nlb lanes each)
  *   in ascending element order (the oracle's order) and writes each CSR entry
  *   once.  Needs row_ptr, node_elem_ptr, node_elem and node_elem_slot of
  *   fem_pattern (elem2nnz unused).  Bitwise reproducible.
