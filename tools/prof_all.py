@@ -49,10 +49,13 @@ K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
 M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
 plan.classes()
 plan.tiles(cd, ed)
-for mode, variant in ((vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"),
+# round 2: the lattice plan (element check + closed-form pattern) and the headline kernel
+twice(lambda: vb.P1Plan.for_lattice(ed, c5.shape[1]))
+assert plan.lattice(ed)
+for mode, variant in ((vb.VB_ASSEMBLE_GATHER, "lattice"), (vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"),
                       (vb.VB_ASSEMBLE_GATHER, "tile"), (vb.VB_ASSEMBLE_ATOMIC, None)):
     twice(lambda: vb.fem_p1_assemble(cd, ed, plan, mode=mode, K=K, M=M, variant=variant))
-    if variant != "tile":
+    if variant not in ("tile", "lattice"):
         twice(lambda: vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, mode=mode, K=K, M=M, variant=variant))
 twice(lambda: vb.fem_p1_assemble_exact(cd, ed, plan))
 
@@ -83,7 +86,8 @@ del plan, K, M, cd, ed, Kl, u, fq
 c4, e4 = synth.square_p1(2048, jitter=0.1, seed=0)
 cd4, ed4 = torch.from_numpy(c4).to(dev), torch.from_numpy(e4).to(dev)
 p4 = vb.P1Plan(ed4, c4.shape[1])
-for mode, variant in ((vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"),
+assert p4.lattice(ed4)
+for mode, variant in ((vb.VB_ASSEMBLE_GATHER, "lattice"), (vb.VB_ASSEMBLE_GATHER, "class"), (vb.VB_ASSEMBLE_GATHER, "block"),
                       (vb.VB_ASSEMBLE_GATHER, "tile"), (vb.VB_ASSEMBLE_ATOMIC, None)):
     twice(lambda: vb.fem_p1_assemble(cd4, ed4, p4, mode=mode, variant=variant))
 del p4, cd4, ed4
