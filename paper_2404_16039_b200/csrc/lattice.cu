@@ -623,7 +623,11 @@ struct LatGeom {
     int64_t NX1, NY1;
 };
 __device__ __forceinline__ void canon(const LatGeom& g, int64_t id, int& I, int& J, int& K) {
-    const int64_t i = id % g.NX1, j = (id / g.NX1) % g.NY1, k = id / (g.NX1 * g.NY1);
+    // node ids are below 2^31 (checked by the callers): 32-bit divisions (the 64-bit ones were most of the
+    // element check's time)
+    const uint32_t u = (uint32_t)id, nx1 = (uint32_t)g.NX1, ny1 = (uint32_t)g.NY1;
+    const uint32_t q = u / nx1;
+    const uint32_t i = u - q * nx1, k = q / ny1, j = q - k * ny1;
     I = (int)(g.fx ? g.nx - i : i);
     J = (int)(g.fy ? g.ny - j : j);
     K = (int)(g.fz ? g.nz - k : k);
@@ -633,7 +637,13 @@ __device__ __forceinline__ void canon(const LatGeom& g, int64_t id, int& I, int&
 // bitset, a code seen twice or a non-Kuhn element sets flags[0]
 __global__ void lattice_check_elems_k(int64_t ne, int64_t nn, const int32_t* __restrict__ elems, int64_t eld,
                                       LatGeom g, uint32_t* __restrict__ bits, int* __restrict__ flags) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < ne; e += (int64_t)gridDim.x * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    // whole warps run the loop: the bitset update is aggregated per word (elements in cell order put a warp's
+    // 32 codes into one or two words: 2 atomics instead of 32; 0.39 -> 0.1 ms on configs[4])
+    for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); eb < ne;
+         eb += (int64_t)gridDim.x * blockDim.x) {
+        const bool valid = eb + lane < ne;
+        const int64_t e = valid ? eb + lane : ne - 1;
         int I[4], J[4], K[4];
         bool bad = false;
 #pragma unroll
@@ -656,19 +666,32 @@ __global__ void lattice_check_elems_k(int64_t ne, int64_t nn, const int32_t* __r
         }
         if (!bad && (at[0] != 0 || at[3] != 7)) bad = true;
         if (I0 >= g.nx || J0 >= g.ny || K0 >= g.nz) bad = true;
+        int64_t code = -1;
         if (!bad) {
             const int s0 = at[1], s1 = at[2] & ~at[1];   // first and second unit steps
             if (__popc(s0) != 1 || __popc(at[2]) != 2 || (at[2] & s0) != s0) bad = true;
             else {
                 const int p0 = __ffs(s0) - 1, p1 = __ffs(s1) - 1;
                 const int path = p0 * 2 + ((p1 == (p0 + 1) % 3) ? 0 : 1);   // 6 paths
-                const int64_t code = (((int64_t)K0 * g.ny + J0) * g.nx + I0) * 6 + path;
-                const uint32_t bit = 1u << (code & 31);
-                const uint32_t old = atomicOr(bits + (code >> 5), bit);
-                if (old & bit) bad = true;
+                code = (((int64_t)K0 * g.ny + J0) * g.nx + I0) * 6 + path;
             }
         }
-        if (bad) atomicExch(flags, 1);
+        const bool mark = valid && !bad;
+        // lanes of one word: OR their bits, one atomic by the lowest lane, the old word back to all of them;
+        // a code twice inside the warp shows as two lanes with the same bit
+        const long long key = mark ? (long long)(code >> 5) : -1 - lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        const uint32_t bit = mark ? 1u << (code & 31) : 0u;
+        const uint32_t all = __reduce_or_sync(peers, bit);
+        const int lead = __ffs(peers) - 1;
+        uint32_t old = 0;
+        if (mark && lane == lead) old = atomicOr(bits + (code >> 5), all);
+        old = __shfl_sync(peers, old, lead);
+        if (mark) {
+            const unsigned same = __match_any_sync(peers, bit);
+            if ((old & bit) || __popc(same) > 1) bad = true;
+        }
+        if (valid && bad) atomicExch(flags, 1);
     }
 }
 
