@@ -34,7 +34,9 @@
 // value needs masking.  Rows of CSR are assembled in registers (14 edges;
 // diagonals by the partition of unity, K_pp = -sum_q K_pq, M_pp = (2/3)
 // sum_q M_pq, as the gather variants), staged in shared memory and leave as
-// TMA bulk copies (cp.async.bulk) issued by one lane per segment.
+// TMA bulk copies (cp.async.bulk; K and M of a segment in one statement issued by
+// one elected lane, committed a step later).  The CTAs' ranges of the tile-layer
+// sequence are cost-balanced once per mesh and kept in the plan (lat_ranges).
 #include <algorithm>
 #include <cstdlib>
 #include <vector>

@@ -343,3 +343,29 @@ def test_delaunay_invariants_and_numbering_independence(dim, n):
     assert np.max(np.abs(D1[0][rows2, ci2] - K2)) <= 1e-13 * Kinf
     assert np.max(np.abs(D1[1][rows2, ci2] - M2)) <= 1e-13 * np.max(M)
     assert np.count_nonzero(np.diff(rp2)) == nn and len(ci2) == len(ci)
+
+
+def test_rect_p1_generator_and_oracle_invariants():
+    """synth.rect_p1 (inputs of the 2D lattice tests): flip = 0 on a square is square_p1's mesh bit for bit; on
+    rectangles and for both diagonals the oracle's K has zero row sums, sum(M) = the area nx ny / m^2, the
+    closed-form nnz of the 7-point stencil, and every triangle is positively oriented or consistently
+    negative (no inverted element after the jitter)."""
+    c0, e0 = synth.square_p1(9, jitter=0.1, seed=3)
+    c1, e1 = synth.rect_p1(9, 9, jitter=0.1, seed=3, flip=0)
+    assert np.array_equal(c0, c1) and np.array_equal(e0, e1)
+    for (nx, ny), flip in (((7, 4), 0), ((7, 4), 1), ((3, 11), 1)):
+        coords, elems = synth.rect_p1(nx, ny, jitter=0.1, seed=1, flip=flip)
+        nn = (nx + 1) * (ny + 1)
+        assert coords.shape == (2, nn) and elems.shape == (3, 2 * nx * ny)
+        rp, ci = oracle.p1_pattern(elems, nn)
+        # self + 2 axis neighbours per axis + the two diagonal neighbours along the split diagonal
+        nnz = nn + 2 * (nx * (ny + 1) + ny * (nx + 1)) + 2 * nx * ny
+        assert int(rp[-1]) == nnz
+        K, M = oracle.p1_assemble(coords, elems, rp, ci)
+        rows = np.repeat(np.arange(nn), np.diff(rp))
+        assert np.max(np.abs(np.bincount(rows, weights=K, minlength=nn))) <= 1e-12
+        m = max(nx, ny)
+        assert abs(M.sum() - nx * ny / m ** 2) <= 1e-13
+        x = coords[:, elems]                      # (2, 3, ne)
+        det = (x[0, 1] - x[0, 0]) * (x[1, 2] - x[1, 0]) - (x[1, 1] - x[1, 0]) * (x[0, 2] - x[0, 0])
+        assert np.all(det > 0) or np.all(det < 0)
