@@ -311,6 +311,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
 #endif
 
     const int64_t g0 = __ldg(p.range + blockIdx.x), g1 = __ldg(p.range + blockIdx.x + 1);
+    VB_CHECK(g0 >= 0 && g0 <= g1 && g1 <= p.L);
     const int NK = p.nz + 1;
     const int64_t plane = p.dK;   // node id step per layer
     double* const SK = S.S[w][0];
@@ -496,6 +497,7 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                     for (int e = 0; e < 7; e++) { sK += eK[e] + iK[e]; sM += eM[e] + iM[e]; }
                     double* rk = SK + soff + (rp - a_seg);
                     double* rm = SM + soff + (rp - a_seg);
+                    VB_CHECK(rp >= a_seg && soff + (rp - a_seg) + 15 <= LSTG);   // the row lies in the staging strip
                     if (px && mx && py && my && pz && mz) {   // interior row: all 15 columns
                         rlen = 15;
                         rk[ORD.slot[0]] = -sK;

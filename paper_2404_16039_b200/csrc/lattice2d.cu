@@ -122,6 +122,7 @@ __global__ void __launch_bounds__(L2_THREADS) assemble_lattice2d_k(const Lat2Par
     int64_t g = __ldg(p.range + 2 * gw);
     const int64_t g1 = __ldg(p.range + 2 * gw + 1);
     int ndeg = 0;
+    VB_CHECK(g >= 0 && g <= g1 && g1 <= (int64_t)p.S * NJ);
     while (g < g1) {
         const int sgm = (int)(g / NJ);
         const int ja = (int)(g % NJ);
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(L2_THREADS) assemble_lattice2d_k(const Lat2Par
                     const double sM = ((eXM + iXM) + (eYM + iYM)) + (eXYM + iXYM);
                     double* rk = SK + soff + (rp - a_seg);
                     double* rm = SM + soff + (rp - a_seg);
+                    VB_CHECK(rp >= a_seg && soff + (rp - a_seg) + 7 <= L2_STG);   // the row lies in the staging strip
                     if (px && mx && py && my) {   // interior row: all 7 columns
                         rlen = 7;
                         rk[ORD.slot[0]] = -sK;   rm[ORD.slot[0]] = sM;

@@ -42,3 +42,19 @@ for dim, (c, e) in ((2, synth.square_p1(20)), (3, synth.cube_kuhn_p1(6)), (2, sy
     vb.vb_create_coords3D(cd, ed)
 torch.cuda.synchronize()
 print("sanitize smoke ok")
+
+# round 2: lattice plans and kernels (3D: sizes with packed tiles and several bands; 2D: several segments)
+for dims in ((33, 14, 5), (7, 7, 7)):
+    c, e = synth.box_kuhn_p1(*dims, jitter=0.05, seed=1)
+    plan = vb.P1Plan.for_lattice(g(e), c.shape[1], dims=dims)
+    assert plan is not None
+    vb.fem_p1_assemble(g(c), g(e), plan, degenerate=torch.zeros(1, dtype=torch.int64, device=dev))
+    p2 = vb.P1Plan(g(e), c.shape[1], scatter_map=False, gather_plan=False)
+    assert p2.lattice(g(e), dims=dims)
+for dims in ((70, 45), (5, 3)):
+    c, e = synth.rect_p1(*dims, jitter=0.1, seed=1, flip=1)
+    plan = vb.P1Plan(g(e), c.shape[1], scatter_map=False, gather_plan=False)
+    assert plan.lattice(g(e), dims=dims), plan.lattice_reason
+    vb.fem_p1_assemble_lattice(g(c), plan, degenerate=torch.zeros(1, dtype=torch.int64, device=dev))
+torch.cuda.synchronize()
+print("lattice ok")
