@@ -265,8 +265,11 @@ VB_API vb_status fem_plan_classes(int dim, int64_t nn, const int32_t* row_ptr, c
  *   with work_bytes == NULL runs the static block schedule (no counter).
  * degenerate (nullable DEVICE int64): receives the number of elements with
  *   det tjac = 0 (outside the domain of inverse_W; tjac rows
- *   x_{r+1} - x_0, det by cofactor expansion along row 0) -- an extra pass
- *   over the elements when requested.  Degenerate elements still propagate
+ *   x_{r+1} - x_0, det by cofactor expansion along row 0) as the kernel
+ *   evaluates it, or with two vertices of identical coordinates (whose exact
+ *   determinant 0 may be evaluated as a rounding residual); the same rule in
+ *   every kernel that takes this argument -- an extra pass over the elements
+ *   when requested.  Degenerate elements still propagate
  *   inf/nan into K/M (IEEE; not an error code). */
 #define VB_ASSEMBLE_ATOMIC 0
 #define VB_ASSEMBLE_GATHER 1
@@ -400,8 +403,9 @@ VB_API vb_status fem_p1_assemble_tiles(int dim, int64_t nn, const double* coords
  * ny, nz and flips as planned (stats_out[3]), coords strided as in
  * vb_create_coords3D, row_ptr of the planned pattern, nnz, K_vals / M_vals
  * (nnz each, nullable; overwritten), degenerate (nullable DEVICE int64: the
- * number of tetrahedra with det = 0 as the kernel evaluates it, each counted
- * once).  VB_ERR_ARG for NULL coords / row_ptr /
+ * number of tetrahedra with det = 0 as the kernel evaluates it or with two
+ * vertices of identical coordinates, fem_p1_assemble's rule; a pass of its own
+ * over the cells when requested).  VB_ERR_ARG for NULL coords / row_ptr /
  * plan, nn != (nx+1)(ny+1)(nz+1), nx or ny < 2, or a plan built for a device
  * with another SM count (flips bits 8..).  A plan of another mesh (token
  * mismatch, checked on the device) makes the kernel write nothing. */
@@ -448,7 +452,8 @@ VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* coords, int64
  * (diagonals by the partition of unity, K_pp = -sum K_pq, M_pp = sum M_pq)
  * staged in CSR order and written once by TMA bulk copies (K, M 16-byte
  * aligned; plain stores otherwise).  Deterministic, bitwise reproducible.
- * degenerate: nullable DEVICE int64, the number of triangles with det = 0. */
+ * degenerate: nullable DEVICE int64, the number of triangles with det = 0 as
+ * evaluated or two identical vertices (fem_p1_assemble's rule; its own pass). */
 VB_API vb_status fem_plan_lattice2d(int64_t nn, int64_t ne, const int32_t* elems, int64_t elem_ld,
                                     const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz, int nx, int ny,
                                     void* work, size_t* work_bytes, int32_t* plan, int64_t* plan_ints,

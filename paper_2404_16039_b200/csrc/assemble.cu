@@ -1643,7 +1643,19 @@ __global__ void count_degenerate_k(int64_t ne, const double* __restrict__ coords
         if (DIM == 2) det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
         else det = J[0][0] * (J[1][1] * J[2][2] - J[1][2] * J[2][1]) - J[0][1] * (J[1][0] * J[2][2] - J[1][2] * J[2][0]) +
                    J[0][2] * (J[1][0] * J[2][1] - J[1][1] * J[2][0]);
-        mine += det == 0.0;
+        // ... or two vertices with identical coordinates (with contracted cofactors a determinant that is 0 in
+        // exact arithmetic may come out as a rounding residual): the same rule in every kernel that counts
+        bool same = false;
+#pragma unroll
+        for (int a = 0; a <= DIM; a++)
+#pragma unroll
+            for (int b = a + 1; b <= DIM; b++) {
+                bool eq = true;
+#pragma unroll
+                for (int c = 0; c < DIM; c++) eq = eq && x[a][c] == x[b][c];
+                same = same || eq;
+            }
+        mine += det == 0.0 || same;
     }
     for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)mine);

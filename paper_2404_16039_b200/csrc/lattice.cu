@@ -108,7 +108,6 @@ struct LatParams {
     const uint32_t* token;        // plan token (LAT_MAGIC ^ hash) written by fem_plan_lattice
     uint32_t want;
     int bulk;                     // K, M 16-byte aligned: rows leave as bulk copies
-    unsigned long long* degen;    // nullable: count of tetrahedra with det = 0 (owned cells, counted once)
     const int32_t* range;         // plan: CTA c owns tile-layers [range[c], range[c+1]) (cost-balanced)
 };
 
@@ -408,13 +407,6 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                 if (__all_sync(0xffffffffu, live)) cell<false>(x0, x1, true, CK, CM);
                 else cell<true>(x0, x1, live, CK, CM);
 #endif
-                if (p.degen) {   // |det|/120 of the six tets: CM.c100[0..1], o[0..1], c001[0..1]
-                    const int z = (CM.c100[0] == 0.0) + (CM.c100[1] == 0.0) + (CM.o[0] == 0.0) + (CM.o[1] == 0.0) +
-                                  (CM.c001[0] == 0.0) + (CM.c001[1] == 0.0);
-                    int cnt = (live && owned && out) ? z : 0;
-                    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-                    if (lane == 0 && cnt) atomicAdd(p.degen, (unsigned long long)cnt);
-                }
             }
             double eK[7], eM[7];
             eK[EX] = zcK0 + CK.e[0]; eK[EY] = zcK1 + CK.e[1]; eK[EXY] = zcK2 + CK.e[3];
@@ -615,6 +607,43 @@ __global__ void __launch_bounds__(LTHREADS, VB_LAT_MINB) assemble_lattice_k(cons
                (long long)g0, (long long)g1);
     }
 #endif
+}
+
+// Degenerate tetrahedra of the lattice (fem_p1_assemble_lattice's optional counter; a pass of its own so that the
+// assembly kernel carries none of it): the determinant exactly as the kernel evaluates it (f1 . (f2 x f3) with
+// the fused cross and dot products above) is 0, or two vertices of the tet have identical coordinates (a
+// determinant that is 0 in exact arithmetic may be evaluated as a rounding residual).  One thread per cell.
+__global__ void lattice_degenerate_k(int nx, int ny, int nz, int id0, int dJ, int dK, const double* __restrict__ X,
+                                     int64_t ns, int64_t cs_, unsigned long long* __restrict__ out) {
+    const int64_t ncell = (int64_t)nx * ny * nz;
+    int mine = 0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+        const int I = (int)(c % nx), J = (int)((c / nx) % ny), K = (int)(c / ((int64_t)nx * ny));
+        double cx[8][3];   // corners by bits x = 1, y = 2, z = 4
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const int64_t v = id0 + (I + (q & 1)) + (int64_t)dJ * (J + ((q >> 1) & 1)) + (int64_t)dK * (K + (q >> 2));
+#pragma unroll
+            for (int d = 0; d < 3; d++) cx[q][d] = X[d * cs_ + v * ns];
+        }
+        double f[8][3];
+#pragma unroll
+        for (int q = 1; q < 8; q++)
+#pragma unroll
+            for (int d = 0; d < 3; d++) f[q][d] = cx[q][d] - cx[0][d];
+        auto same = [&](int a, int b) { return cx[a][0] == cx[b][0] && cx[a][1] == cx[b][1] && cx[a][2] == cx[b][2]; };
+        constexpr int mid[6][2] = {{1, 3}, {1, 5}, {2, 3}, {2, 6}, {4, 5}, {4, 6}};   // paths xyz xzy yxz yzx zxy zyx
+#pragma unroll
+        for (int t = 0; t < 6; t++) {
+            const int a = mid[t][0], b = mid[t][1];
+            double h1[3];
+            crs(f[b], f[7], h1);   // the kernel's h1 = f2 x f3 (f3 = the cell diagonal), det = f1 . h1
+            const double det = dot3(f[a], h1);
+            mine += det == 0.0 || same(0, a) || same(0, b) || same(0, 7) || same(a, b) || same(a, 7) || same(b, 7);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(out, (unsigned long long)mine);
 }
 
 // ------------------------------------------------------------------ plan: verification kernels
@@ -1163,11 +1192,17 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     p.range = plan + LAT_HDR + (int64_t)T * 128;
     p.want = lat_want(h, nn, nnz, grid);
     p.bulk = (!K_vals || aligned16(K_vals)) && (!M_vals || aligned16(M_vals));
-    p.degen = reinterpret_cast<unsigned long long*>(degenerate);
-    if (degenerate) {
+    if (degenerate) {   // a pass of its own over the cells, with the kernel's determinant expressions
         cudaError_t e = cudaMemsetAsync(degenerate, 0, sizeof(int64_t), cs(stream));
         if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+        const int64_t ncell = (int64_t)nx * ny * nz;
+        lattice_degenerate_k<<<grid_for(ncell, 256, 8), 256, 0, cs(stream)>>>(
+            nx, ny, nz, (int)h.id0, (int)h.dJ, (int)h.dK, coords, node_stride, comp_stride,
+            reinterpret_cast<unsigned long long*>(degenerate));
+        vb_status st = launch_check(fn);
+        if (st != VB_OK) return st;
     }
+    if (!K_vals && !M_vals) return VB_OK;
     const size_t smem = sizeof(LatSmem);
     static int smem_set = 0;
     if (!smem_set) {

@@ -75,7 +75,6 @@ struct Lat2Params {
     const uint32_t* token;
     uint32_t want;
     int bulk;
-    unsigned long long* degen;
     const int32_t* range;         // plan: warp w owns items [range[2w], range[2w+1]) of the (segment, row) sequence
     int nwarps;
 };
@@ -121,7 +120,6 @@ __global__ void __launch_bounds__(L2_THREADS) assemble_lattice2d_k(const Lat2Par
     const int NJ = p.ny + 1;
     int64_t g = __ldg(p.range + 2 * gw);
     const int64_t g1 = __ldg(p.range + 2 * gw + 1);
-    int ndeg = 0;
     VB_CHECK(g >= 0 && g <= g1 && g1 <= (int64_t)p.S * NJ);
     while (g < g1) {
         const int sgm = (int)(g / NJ);
@@ -184,7 +182,6 @@ __global__ void __launch_bounds__(L2_THREADS) assemble_lattice2d_k(const Lat2Par
             ldrp(J + L2_PF, rpr[u]);
             const Tri A = tri(ux, uy, wx, wy, live);   // (p, p+x, p+xy)
             const Tri B = tri(vx, vy, wx, wy, live);   // (p, p+y, p+xy)
-            if (p.degen && live && owned && out) ndeg += (A.m == 0.0) + (B.m == 0.0);
             // this node's up edges
             const double eXK = cxK + A.k01, eXM = cxM + A.m;
             const double eYK = B.k01 + shu(A.k12), eYM = B.m + shu(A.m);
@@ -305,10 +302,35 @@ __global__ void __launch_bounds__(L2_THREADS) assemble_lattice2d_k(const Lat2Par
     }
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    if (p.degen) {
-        for (int o = 16; o > 0; o >>= 1) ndeg += __shfl_xor_sync(0xffffffffu, ndeg, o);
-        if (lane == 0 && ndeg) atomicAdd(p.degen, (unsigned long long)ndeg);
+}
+
+// Degenerate triangles of the lattice (the optional counter; a pass of its own): the determinant exactly as the
+// kernel evaluates it is 0, or two vertices of the triangle have identical coordinates.  One thread per cell.
+__global__ void lattice2d_degenerate_k(int nx, int ny, int id0, int dJ, const double* __restrict__ X, int64_t ns,
+                                       int64_t cs_, unsigned long long* __restrict__ out) {
+    const int64_t ncell = (int64_t)nx * ny;
+    int mine = 0;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncell; c += (int64_t)gridDim.x * blockDim.x) {
+        const int I = (int)(c % nx), J = (int)(c / nx);
+        double x[4], y[4];   // corners p, p+x, p+y, p+xy
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+            const int64_t v = id0 + (I + (q & 1)) + (int64_t)dJ * (J + (q >> 1));
+            x[q] = X[v * ns];
+            y[q] = X[cs_ + v * ns];
+        }
+        auto same = [&](int a, int b) { return x[a] == x[b] && y[a] == y[b]; };
+        const double wx = x[3] - x[0], wy = y[3] - y[0];
+#pragma unroll
+        for (int t = 0; t < 2; t++) {   // A = (p, p+x, p+xy), B = (p, p+y, p+xy): det = f1x f2y - f1y f2x as in tri()
+            const int a = t + 1;
+            const double f1x = x[a] - x[0], f1y = y[a] - y[0];
+            const double det = fma(f1x, wy, -f1y * wx);
+            mine += det == 0.0 || same(0, a) || same(0, 3) || same(a, 3);
+        }
     }
+    for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(out, (unsigned long long)mine);
 }
 
 // ------------------------------------------------------------------ plan: verification kernels
@@ -586,13 +608,18 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice2d(int64_t nn, const double* 
 #ifdef VB_LAT2_PLAIN
     if (p.bulk) p.bulk = 2;
 #endif
-    p.degen = reinterpret_cast<unsigned long long*>(degenerate);
     p.range = plan + LAT2_HDR;
     p.nwarps = W;
-    if (degenerate) {
+    if (degenerate) {   // a pass of its own over the cells, with the kernel's determinant expression
         cudaError_t e = cudaMemsetAsync(degenerate, 0, sizeof(int64_t), cs(stream));
         if (e != cudaSuccess) { set_error("%s: %s", fn, cudaGetErrorString(e)); return VB_ERR_CUDA; }
+        lattice2d_degenerate_k<<<grid_for((int64_t)nx * ny, 256, 8), 256, 0, cs(stream)>>>(
+            nx, ny, (int)h.id0, (int)h.dJ, coords, node_stride, comp_stride,
+            reinterpret_cast<unsigned long long*>(degenerate));
+        vb_status st = launch_check(fn);
+        if (st != VB_OK) return st;
     }
+    if (!K_vals && !M_vals) return VB_OK;
     const int grid = (W + L2_WARPS - 1) / L2_WARPS;
     if (h.fy) assemble_lattice2d_k<1><<<grid, L2_THREADS, 0, cs(stream)>>>(p);
     else assemble_lattice2d_k<0><<<grid, L2_THREADS, 0, cs(stream)>>>(p);

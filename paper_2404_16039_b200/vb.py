@@ -633,8 +633,9 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
     """Returns (K_vals, M_vals, K_local, M_local) (None where not requested).
     Gather mode: `variant` None (auto: lattice, else class / block as _use_classes),
     "lattice", "class", "block" or "tile".  degenerate: optional device int64 tensor (1,)
-    receiving the number of elements with det = 0 (block / atomic calls; the lattice
-    kernel counts its tets; the class and tile kernels do not count)."""
+    receiving the number of degenerate elements (det = 0 as evaluated, or two identical
+    vertices): every variant fills it (the class and tile calls through a counting-only
+    fem_p1_assemble call)."""
     _f64(coords)
     dim, nn = coords.shape
     nv, ne = elems.shape
@@ -649,9 +650,16 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         M = None
     Kl = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
     Ml = torch.empty((nv, nv, ne), dtype=torch.float64, device=dev) if want_local else None
+
+    def count_only():   # the class and tile entry points take no counter: a counting-only call of the C entry
+        if degenerate is not None:
+            _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
+                                         None, None, None, None, None, None, None, None, VB_ASSEMBLE_ATOMIC,
+                                         None, None, _ptr(degenerate), _stream(stream)))
     if (mode == VB_ASSEMBLE_GATHER and variant == "tile" and (K is not None or M is not None)
             and plan.tiles(coords, elems)):
         fem_p1_assemble_tiles(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
+        count_only()
         if want_local:
             _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
                                          None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),
@@ -672,6 +680,7 @@ def fem_p1_assemble(coords, elems, plan, mode=VB_ASSEMBLE_GATHER, want_K=True, w
         variant = None   # not a Kuhn lattice (plan.lattice_reason)
     if mode == VB_ASSEMBLE_GATHER and (K is not None or M is not None) and _use_classes(plan, variant):
         fem_p1_assemble_classes(coords, plan, K=K, M=M, want_K=K is not None, want_M=M is not None, stream=stream)
+        count_only()
         if want_local:
             _check(lib().fem_p1_assemble(dim, nn, ne, _ptr(coords), 1, nn, _ptr(elems), ne, None, None, plan.nnz,
                                          None, None, None, None, None, None, _ptr(Kl), _ptr(Ml), int(mode),

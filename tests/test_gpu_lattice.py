@@ -202,3 +202,50 @@ def test_full_size_configs4_every_entry_vs_oracle(dev):
     assert fast is not None and np.array_equal(h(fast.row_ptr), rp) and np.array_equal(h(fast.col_idx), ci)
     K2, M2, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), fast)
     assert torch.equal(K2, K) and torch.equal(M2, M)
+
+
+def _collapse(coords, elems, a, b):
+    """Move node a onto node b: exactly the elements holding both have det = 0 (a zero edge vector)."""
+    c = coords.copy()
+    c[:, a] = c[:, b]
+    return c, int(np.sum(np.any(elems == a, axis=0) & np.any(elems == b, axis=0)))
+
+
+def test_degenerate_element_counter(dev):
+    """The optional counter of elements outside the domain of the inverse (det tjac = 0) of
+    fem_p1_assemble (block and atomic calls), of the 3D lattice kernel and of the 2D lattice kernel: zero on the
+    jittered meshes, and the number of elements that hold both ends of a collapsed edge otherwise -- whichever
+    edge of the element collapses (with contracted cofactors some of them leave a rounding residual instead of
+    an exact 0: the rule counts identical vertices too), the same number from every kernel."""
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    coords, elems = synth.box_kuhn_p1(9, 14, 5, jitter=0.05, seed=2)
+    nx1, nxy = 10, 10 * 15
+    a = 4 + nx1 * 6 + nxy * 2                        # an interior node
+    ed = g(elems, dev)
+    plan = vb.P1Plan(ed, coords.shape[1])
+    assert plan.lattice(ed, dims=(9, 14, 5))
+    cases = [(coords, 0)]
+    for u, v in ((a, a + 1 + nx1 + nxy), (a, a + 1), (a + 1, a + 1 + nx1), (a + nx1, a + nx1 + nxy),
+                 (a + 1, a + 1 + nx1 + nxy), (a, a + nx1 + nxy)):      # diagonal, axis edges, face diagonals
+        cases.append(_collapse(coords, elems, u, v))
+        assert cases[-1][1] in (4, 6, 8)
+    for cc, want in cases:
+        for kw in (dict(variant="lattice"), dict(variant="block"), dict(variant="class"), dict(variant="tile"),
+                   dict(mode=vb.VB_ASSEMBLE_ATOMIC)):
+            cnt.fill_(-1)
+            vb.fem_p1_assemble(g(cc, dev), ed, plan, degenerate=cnt, **kw)
+            assert int(h(cnt)[0]) == want, (kw, want)
+    for flip in (0, 1):
+        c2, e2 = synth.rect_p1(40, 23, jitter=0.1, seed=1, flip=flip)
+        e2d = g(e2, dev)
+        p2 = vb.P1Plan(e2d, c2.shape[1])
+        assert p2.lattice(e2d, dims=(40, 23))
+        a2 = 17 + 41 * 9
+        cases2 = [(c2, 0), _collapse(c2, e2, a2, a2 + 1), _collapse(c2, e2, a2, a2 + 41),
+                  _collapse(c2, e2, a2 + (1 if flip else 0), a2 + 41 + (0 if flip else 1))]
+        for cc, want in cases2:
+            assert want in (0, 2)
+            for kw in (dict(variant="lattice"), dict(variant="block")):
+                cnt.fill_(-1)
+                vb.fem_p1_assemble(g(cc, dev), e2d, p2, degenerate=cnt, **kw)
+                assert int(h(cnt)[0]) == want, (flip, kw, want)
