@@ -22,6 +22,7 @@ LIB_PATH = os.environ.get("VB_LIBVB") or os.path.join(_HERE, "libvb.so")   # VB_
 VB_ASSEMBLE_ATOMIC = 0
 VB_ASSEMBLE_GATHER = 1
 VB_GATHER_HINT_COMPACT = 0x100
+VB_PATTERN_VALIDATE = 0x100   # fem_p1_pattern: dim | VB_PATTERN_VALIDATE checks every vertex id first
 TILE_ROWS, TILE_NLOC, TILE_MAXC = 128, 1024, 32   # VB_TILE_ROWS, VB_TILE_NLOC, VB_TILE_MAXC
 
 
@@ -289,7 +290,9 @@ class P1Plan:
     or None; node_elem_ptr (nn+1), node_elem (nv*ne) int32 and node_elem_slot
     (nv*ne) int32 (uint32 bits) or None; nnz."""
 
-    def __init__(self, elems, nn, scatter_map=True, gather_plan=True, stream=None):
+    def __init__(self, elems, nn, scatter_map=True, gather_plan=True, stream=None, validate=False):
+        """validate: check every vertex id against [0, nn) first (VB_PATTERN_VALIDATE; VbError naming the
+        first offending element and vertex)."""
         if elems.dtype != torch.int32:
             raise TypeError("elems must be int32")
         nv, ne = elems.shape
@@ -303,7 +306,8 @@ class P1Plan:
                                 None, st))
         self.work = torch.empty((max(sz.value, 16),), dtype=torch.uint8, device=dev)
         self.row_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
-        _check(L.fem_p1_pattern(self.dim, nn, ne, _ptr(elems), ne, _ptr(self.work), C.byref(sz), _ptr(self.row_ptr),
+        _check(L.fem_p1_pattern(self.dim | (VB_PATTERN_VALIDATE if validate else 0), nn, ne, _ptr(elems), ne,
+                                _ptr(self.work), C.byref(sz), _ptr(self.row_ptr),
                                 None, 0, None, None, None, None, C.byref(nnz), st))
         self.nnz = int(nnz.value)
         # gather mode streams col_idx / node_elem_slot in 16-byte chunks: pad to a multiple of 4 entries

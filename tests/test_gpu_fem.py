@@ -642,3 +642,51 @@ def test_k_only_and_m_only(dev, kind, mode):
         K, M, _, _ = vb.fem_p1_assemble_coef(cd, ed, plan, gqo=2, cK=cf, cM=cf, mode=mode[0], variant=mode[1],
                                              want_K=False)
         assert K is None and relmax(h(M), Mc) <= 1e-12
+
+
+# ---------------------------------------------------------------- ABI v2 conventions
+def test_pattern_validation_mode_names_the_bad_vertex(dev):
+    """fem_p1_pattern with VB_PATTERN_VALIDATE: an out-of-range vertex id is VB_ERR_ARG naming the first
+    offending element and vertex (before any kernel indexes by it); valid meshes build as usual."""
+    coords, elems = synth.cube_kuhn_p1(5, jitter=0.05, seed=0)
+    nn = coords.shape[1]
+    ok = vb.P1Plan(g(elems, dev), nn, validate=True)
+    rp, ci = oracle.p1_pattern(elems, nn)
+    assert np.array_equal(h(ok.row_ptr), rp) and np.array_equal(h(ok.col_idx), ci)
+    for e_bad, a_bad, val in ((137, 2, nn), (22, 0, -1), (elems.shape[1] - 1, 3, nn + 5)):
+        bad = elems.copy()
+        bad[a_bad, e_bad] = val
+        with pytest.raises(vb.VbError) as ei:
+            vb.P1Plan(g(bad, dev), nn, validate=True)
+        msg = str(ei.value)
+        assert "VB_ERR_ARG" in msg and "vertex %d of element %d" % (a_bad, e_bad) in msg and str(val) in msg
+
+
+@pytest.mark.parametrize("variant", ["class", "block", "lattice"])
+def test_many_concurrent_launches_on_two_streams(dev, variant):
+    """More than 64 assembly launches in flight on two streams (each with its own caller-owned work buffer
+    for the dynamic block schedule): every result bitwise equal to a serial run -- the library keeps no
+    per-launch state of its own (round 1's global counter ring could be reset by another launch)."""
+    coords, elems = synth.cube_kuhn_p1(20, jitter=0.05, seed=1)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, coords.shape[1])
+    if variant == "lattice":
+        assert plan.lattice(ed)
+    else:
+        plan.classes()
+    Kr, Mr, _, _ = vb.fem_p1_assemble(cd, ed, plan, variant=variant)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    outs = []
+    n = 80
+    for i in range(n):
+        for s in streams:
+            with torch.cuda.stream(s):
+                K = torch.full((plan.nnz,), float("nan"), dtype=torch.float64, device=dev)
+                M = torch.full((plan.nnz,), float("nan"), dtype=torch.float64, device=dev)
+                vb.fem_p1_assemble(cd, ed, plan, K=K, M=M, variant=variant)
+                outs.append((K, M))
+    torch.cuda.synchronize()
+    assert len(outs) == 2 * n
+    for K, M in outs:
+        assert torch.equal(K, Kr) and torch.equal(M, Mr)
