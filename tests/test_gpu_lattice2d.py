@@ -128,3 +128,29 @@ def test_full_size_configs3_every_entry_vs_oracle(dev):
     assert plan.lattice(g(elems, dev))
     K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan)   # variant None -> 2D lattice
     assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+
+
+@pytest.mark.parametrize("layout", ["aos", "aos4"])
+def test_lattice2d_strided_coords_through_the_abi(dev, layout):
+    """coords strided as in vb_create_coords3D (node-major xy pairs, padded xy__ records) through the C ABI,
+    with the degenerate counter requested (its pass reads the same strides)."""
+    coords, elems = synth.rect_p1(45, 31, jitter=0.1, seed=6, flip=1)
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    plan = vb.P1Plan(g(elems, dev), nn, scatter_map=False, gather_plan=False)
+    assert plan.lattice(g(elems, dev), dims=(45, 31))
+    if layout == "aos":
+        cbuf, ns = g(np.ascontiguousarray(coords.T), dev), 2
+    else:
+        pad = np.zeros((nn, 4))
+        pad[:, :2] = coords.T
+        cbuf, ns = g(pad, dev), 4
+    K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+    M = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+    cnt = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    vb._check(vb.lib().fem_p1_assemble_lattice2d(nn, vb._ptr(cbuf), ns, 1, vb._ptr(plan.row_ptr), plan.nnz,
+                                                 vb._ptr(plan.lattice_plan), 45, 31, plan.lattice_flips, vb._ptr(K),
+                                                 vb._ptr(M), vb._ptr(cnt), None))
+    assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+    assert int(h(cnt)[0]) == 0
