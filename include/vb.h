@@ -458,6 +458,13 @@ VB_API vb_status fem_plan_lattice2d(int64_t nn, int64_t ne, const int32_t* elems
                                     const int32_t* row_ptr, const int32_t* col_idx, int64_t nnz, int nx, int ny,
                                     void* work, size_t* work_bytes, int32_t* plan, int64_t* plan_ints,
                                     int64_t* stats_out, vb_stream_t stream);
+/* The 7-point stencil pattern of such a lattice in closed form, bit-identical to
+ * fem_p1_pattern's: arguments, query and errors as fem_lattice_pattern (flips:
+ * bit 0 of fem_plan_lattice2d's stats_out[3]); fem_plan_lattice2d accepts
+ * row_ptr = col_idx = NULL (elements only) for a pattern written by this call. */
+VB_API vb_status fem_lattice2d_pattern(int64_t nn, int nx, int ny, int flips, void* work, size_t* work_bytes,
+                                       int32_t* row_ptr, int32_t* col_idx, int64_t col_cap, int64_t* nnz_out,
+                                       vb_stream_t stream);
 VB_API vb_status fem_p1_assemble_lattice2d(int64_t nn, const double* coords, int64_t node_stride,
                                            int64_t comp_stride, const int32_t* row_ptr, int64_t nnz,
                                            const int32_t* plan, int nx, int ny, int flips, double* K_vals,

@@ -401,6 +401,36 @@ __global__ void lattice2d_check_csr_k(int64_t nn, int64_t nnz, const int32_t* __
     }
 }
 
+// the 7-point stencil written out as a CSR pattern (fem_lattice2d_pattern)
+__global__ void lattice2d_rowlen_k(int64_t nn, Lat2Geom g, int32_t* __restrict__ row_len) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
+        int I, J;
+        canon2(g, v, I, J);
+        int n = 0;
+#pragma unroll
+        for (int d = 0; d < 7; d++) {
+            const int x = I + d2x(d), y = J + d2y(d);
+            n += x >= 0 && x <= g.nx && y >= 0 && y <= g.ny;
+        }
+        row_len[v] = n;
+    }
+}
+__global__ void lattice2d_cols_k(int64_t nn, Lat2Geom g, int64_t id0, int64_t dJ, Lat2Order ord,
+                                 const int32_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nn; v += (int64_t)gridDim.x * blockDim.x) {
+        int I, J;
+        canon2(g, v, I, J);
+        int64_t q = row_ptr[v];
+#pragma unroll
+        for (int r = 0; r < 7; r++) {
+            const int d = ord.dir[r];
+            const int x = I + d2x(d), y = J + d2y(d);
+            if (x < 0 || x > g.nx || y < 0 || y > g.ny) continue;
+            col_idx[q++] = (int32_t)(id0 + x + dJ * y);
+        }
+    }
+}
+
 __global__ void lattice2d_elem0_k(const int32_t* __restrict__ elems, int64_t eld, int32_t* __restrict__ out) {
     out[threadIdx.x] = elems[threadIdx.x * eld];
 }
@@ -518,8 +548,8 @@ extern "C" VB_API vb_status fem_plan_lattice2d(int64_t nn, int64_t ne, const int
     }
     if (*work_bytes < wb) { set_error("%s: work_bytes %zu < %zu", fn, *work_bytes, wb); return VB_ERR_WORKSPACE; }
     if (!plan || *plan_ints < need_ints) { set_error("%s: plan needs %lld ints", fn, (long long)need_ints); return VB_ERR_WORKSPACE; }
-    if (!stats_out || !elems || !row_ptr || !col_idx || elem_ld < ne) {
-        set_error("%s: NULL argument or elem_ld < ne", fn);
+    if (!stats_out || !elems || (row_ptr == nullptr) != (col_idx == nullptr) || elem_ld < ne) {
+        set_error("%s: NULL argument, only one of row_ptr / col_idx, or elem_ld < ne", fn);
         return VB_ERR_ARG;
     }
     stats_out[0] = stats_out[1] = stats_out[2] = stats_out[3] = 0;
@@ -554,8 +584,11 @@ extern "C" VB_API vb_status fem_plan_lattice2d(int64_t nn, int64_t ne, const int
     lattice2d_check_elems_k<<<grid_for(ne, 256, 8), 256, 0, s>>>(ne, nn, elems, elem_ld, g, bits, flags);
     vb_status st = launch_check(fn);
     if (st != VB_OK) return st;
-    lattice2d_check_csr_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, nnz, row_ptr, col_idx, g, h.id0, h.dJ, h.ord, flags);
-    if ((st = launch_check(fn)) != VB_OK) return st;
+    if (row_ptr) {   // NULL, NULL: the pattern comes from fem_lattice2d_pattern (the stencil by construction)
+        lattice2d_check_csr_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, nnz, row_ptr, col_idx, g, h.id0, h.dJ, h.ord,
+                                                                   flags);
+        if ((st = launch_check(fn)) != VB_OK) return st;
+    }
     const int S = lat2_segments(nx), W = lat2_warps(nx, ny);
     int32_t hdr[LAT2_HDR] = {0};
     hdr[1] = nx; hdr[2] = ny; hdr[3] = h.fy; hdr[4] = S; hdr[5] = W;
@@ -575,6 +608,40 @@ extern "C" VB_API vb_status fem_plan_lattice2d(int64_t nn, int64_t ne, const int
     stats_out[1] = S;
     stats_out[3] = h.fy | (int64_t)W << 8;
     return VB_OK;
+}
+
+extern "C" VB_API vb_status fem_lattice2d_pattern(int64_t nn, int nx, int ny, int flips, void* work, size_t* work_bytes,
+                                                  int32_t* row_ptr, int32_t* col_idx, int64_t col_cap,
+                                                  int64_t* nnz_out, vb_stream_t stream) {
+    const char* fn = "fem_lattice2d_pattern";
+    clear_error();
+    if (nx < 1 || ny < 1 || (int64_t)(nx + 1) * (ny + 1) != nn || !work_bytes) {
+        set_error("%s: nx, ny >= 1, nn = (nx+1)(ny+1) and work_bytes non-NULL are required", fn);
+        return VB_ERR_ARG;
+    }
+    int64_t nnz = 0;   // direction d is present at (nx+1-|dx|)(ny+1-|dy|) nodes
+    for (int d = 0; d < 7; d++) nnz += (int64_t)(nx + 1 - std::abs(d2x(d))) * (ny + 1 - std::abs(d2y(d)));
+    if (nnz >= ((int64_t)1 << 31)) { set_error("%s: nnz=%lld does not fit int32", fn, (long long)nnz); return VB_ERR_OVERFLOW; }
+    if (nnz_out) *nnz_out = nnz;
+    const size_t len_bytes = ((size_t)(nn + 1) * 4 + 255) & ~(size_t)255;
+    const size_t wb = len_bytes + scan_tmp_bytes(nn);
+    if (!work) {
+        *work_bytes = wb;
+        return VB_OK;
+    }
+    if (*work_bytes < wb) { set_error("%s: work_bytes %zu < %zu", fn, *work_bytes, wb); return VB_ERR_WORKSPACE; }
+    if (!row_ptr || !col_idx || col_cap < nnz) { set_error("%s: NULL row_ptr / col_idx or col_cap < nnz=%lld", fn, (long long)nnz); return VB_ERR_ARG; }
+    Lat2Host h;
+    if (!lat2_host(nx, ny, flips & 1, h)) { set_error("%s: lattice outside the kernel's limits (nx >= 2)", fn); return VB_ERR_UNSUPPORTED; }
+    Lat2Geom g{nx, ny, h.fy, (int64_t)nx + 1};
+    cudaStream_t s = cs(stream);
+    int32_t* row_len = reinterpret_cast<int32_t*>(work);
+    lattice2d_rowlen_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, g, row_len);
+    vb_status st = launch_check(fn);
+    if (st != VB_OK) return st;
+    if ((st = exclusive_scan_i32(row_len, row_ptr, nn, static_cast<char*>(work) + len_bytes, s, nullptr)) != VB_OK) return st;
+    lattice2d_cols_k<<<grid_for(nn, 256, 8), 256, 0, s>>>(nn, g, h.id0, h.dJ, h.ord, row_ptr, col_idx);
+    return launch_check(fn);
 }
 
 extern "C" VB_API vb_status fem_p1_assemble_lattice2d(int64_t nn, const double* coords, int64_t node_stride,

@@ -49,7 +49,7 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
            "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi", "fem_plan_lattice",
-           "fem_p1_assemble_lattice", "fem_lattice_pattern", "fem_plan_lattice2d", "fem_p1_assemble_lattice2d")
+           "fem_p1_assemble_lattice", "fem_lattice_pattern", "fem_plan_lattice2d", "fem_p1_assemble_lattice2d", "fem_lattice2d_pattern")
 
 
 class VbError(RuntimeError):
@@ -106,6 +106,7 @@ def lib():
             "fem_plan_lattice2d": (i32, [i64, i64, p, i64, p, p, i64, i32, i32, p, sz, p, C.POINTER(C.c_int64),
                                          C.POINTER(C.c_int64), p]),
             "fem_p1_assemble_lattice2d": (i32, [i64, p, i64, i64, p, i64, p, i32, i32, i32, p, p, p, p]),
+            "fem_lattice2d_pattern": (i32, [i64, i32, i32, i32, p, sz, p, p, i64, C.POINTER(C.c_int64), p]),
             "fem_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p, C.POINTER(C.c_int64), p]),
             "fem_p2_assemble": (i32, [i32, i64, i64, p, i64, i64, p, i64, p, p, i64, p, p, p, i32, d, p, d, p,
                                       p, p, p, p, i32, p, sz, p]),
@@ -343,6 +344,8 @@ class P1Plan:
         if elems.dtype != torch.int32:
             raise TypeError("elems must be int32")
         nv, ne = elems.shape
+        if nv == 3:
+            return cls._for_lattice2d(elems, nn, dims, stream)
         if nv != 4:
             return None
         if dims is None:
@@ -376,6 +379,45 @@ class P1Plan:
         self.elem2nnz = self.node_elem_ptr = self.node_elem = self.node_elem_slot = None
         self.node_elem_slot16, self.compact, self.work, self.stats = None, False, None, (15, 0, 0)
         self.lattice_plan, self.lattice_dims = plan, (nx, ny, nz)
+        self.lattice_flips, self.lattice_tiles = int(stats[3]), int(stats[1])
+        self.lattice_ok, self.lattice_reason = True, ""
+        return self
+
+    @classmethod
+    def _for_lattice2d(cls, elems, nn, dims, stream):
+        """for_lattice in 2D: fem_plan_lattice2d on the elements + fem_lattice2d_pattern."""
+        ne = elems.shape[1]
+        if dims is None:
+            n = int(round((ne / 2) ** 0.5)) if ne > 0 else 0
+            dims = (n, n)
+        nx, ny = (int(d) for d in dims[:2])
+        if nx < 2 or ny < 1 or (nx + 1) * (ny + 1) != nn or 2 * nx * ny != ne:
+            return None
+        self = cls.__new__(cls)
+        self.dim, self.nn, self.ne, self.nv = 2, int(nn), int(ne), 3
+        dev = elems.device
+        L = lib()
+        st = _stream(stream)
+        wb, pints, nnz, pwb = C.c_size_t(0), C.c_int64(0), C.c_int64(0), C.c_size_t(0)
+        stats = (C.c_int64 * 4)()
+        _check(L.fem_lattice2d_pattern(nn, nx, ny, 0, None, C.byref(pwb), None, None, 0, C.byref(nnz), st))
+        self.nnz = int(nnz.value)
+        _check(L.fem_plan_lattice2d(nn, ne, None, ne, None, None, self.nnz, nx, ny, None, C.byref(wb), None,
+                                    C.byref(pints), stats, st))
+        work = torch.empty((max(wb.value, pwb.value, 16),), dtype=torch.uint8, device=dev)
+        plan = torch.zeros((max(int(pints.value), 16),), dtype=torch.int32, device=dev)
+        _check(L.fem_plan_lattice2d(nn, ne, _ptr(elems), elems.shape[1], None, None, self.nnz, nx, ny, _ptr(work),
+                                    C.byref(wb), _ptr(plan), C.byref(pints), stats, st))
+        if stats[0] != 1:
+            return None
+        self.row_ptr = torch.empty((nn + 1,), dtype=torch.int32, device=dev)
+        self.col_idx_padded = torch.zeros((_pad4(self.nnz),), dtype=torch.int32, device=dev)
+        _check(L.fem_lattice2d_pattern(nn, nx, ny, int(stats[3]) & 1, _ptr(work), C.byref(pwb), _ptr(self.row_ptr),
+                                       _ptr(self.col_idx_padded), self.col_idx_padded.numel(), C.byref(nnz), st))
+        self.col_idx = self.col_idx_padded[:self.nnz]
+        self.elem2nnz = self.node_elem_ptr = self.node_elem = self.node_elem_slot = None
+        self.node_elem_slot16, self.compact, self.work, self.stats = None, False, None, (7, 0, 0)
+        self.lattice_plan, self.lattice_dims = plan, (nx, ny)
         self.lattice_flips, self.lattice_tiles = int(stats[3]), int(stats[1])
         self.lattice_ok, self.lattice_reason = True, ""
         return self

@@ -154,3 +154,23 @@ def test_lattice2d_strided_coords_through_the_abi(dev, layout):
                                                  vb._ptr(M), vb._ptr(cnt), None))
     assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
     assert int(h(cnt)[0]) == 0
+
+
+@pytest.mark.parametrize("dims,flip", [((2, 1), 0), ((31, 4), 1), ((62, 7), 0), ((33, 100), 1), ((200, 150), 0)])
+def test_lattice2d_pattern_closed_form_bit_exact(dev, dims, flip):
+    """fem_lattice2d_pattern (P1Plan.for_lattice in 2D) against the oracle's pattern built from shuffled elements;
+    K, M assembled on that plan against the oracle."""
+    coords, elems = synth.rect_p1(*dims, jitter=0.1, seed=3, flip=flip)
+    rng = np.random.default_rng(2)
+    elems = np.ascontiguousarray(elems[:, rng.permutation(elems.shape[1])])
+    nn = coords.shape[1]
+    rp, ci = oracle.p1_pattern(elems, nn)
+    plan = vb.P1Plan.for_lattice(g(elems, dev), nn, dims=dims)
+    assert plan is not None and plan.nnz == int(rp[-1])
+    assert np.array_equal(h(plan.row_ptr), rp) and np.array_equal(h(plan.col_idx), ci)
+    Ko, Mo = oracle.p1_assemble(coords, elems, rp, ci)
+    K, M, _, _ = vb.fem_p1_assemble(g(coords, dev), g(elems, dev), plan)
+    assert relmax(h(K), Ko) <= TOL and relmax(h(M), Mo) <= TOL
+    bad = elems.copy()
+    bad[:, 0] = bad[:, 1]
+    assert vb.P1Plan.for_lattice(g(bad, dev), nn, dims=dims) is None
