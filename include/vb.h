@@ -15,6 +15,9 @@
  *   default stream).  Calls return after enqueueing, except where a host
  *   synchronisation is documented (fem_p1_pattern's count phase reads nnz).
  *   Calls on different streams with disjoint buffers are thread-safe.
+ * Devices.  Calls act on the current CUDA device of the calling thread; the
+ *   intended use is one process per GPU (the library caches launch attributes
+ *   of its larger kernels per process; the lattice entry points per device).
  * Page layout (SURVEY B2, P:248-266 with the index space W as the page index,
  *   S:32): a batch of N pages of r x c matrices is stored struct-of-arrays:
  *   entry (i, j) of page k is at  p[(i + j*r) * ld + k]  (column-major entry

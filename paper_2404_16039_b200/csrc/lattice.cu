@@ -1204,13 +1204,15 @@ extern "C" VB_API vb_status fem_p1_assemble_lattice(int64_t nn, const double* co
     }
     if (!K_vals && !M_vals) return VB_OK;
     const size_t smem = sizeof(LatSmem);
-    static int smem_set = 0;
-    if (!smem_set) {
+    static bool smem_set[64] = {};   // the attribute is per device (idempotent: a race only repeats the calls)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !smem_set[dev]) {
         cudaFuncSetAttribute(assemble_lattice_k<0, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(assemble_lattice_k<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(assemble_lattice_k<0, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         cudaFuncSetAttribute(assemble_lattice_k<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        smem_set = 1;
+        if (dev >= 0 && dev < 64) smem_set[dev] = true;
     }
     auto launch = [&](void (*kern)(LatParams)) { kern<<<grid, LTHREADS, smem, cs(stream)>>>(p); };
     switch (h.fy | h.fz << 1) {

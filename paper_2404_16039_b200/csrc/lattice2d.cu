@@ -485,12 +485,16 @@ int lat2_segments(int nx) { return (nx + 1 + L2_OWN - 1) / L2_OWN; }
 
 // resident warps of the current device (the plan's ranges are for this many: the token covers it)
 int lat2_warps(int nx, int ny) {
-    static int occ = 0;
+    static int occ_dev[64] = {};   // per device (idempotent)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int occ = (dev >= 0 && dev < 64) ? occ_dev[dev] : 0;
     if (!occ) {
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, assemble_lattice2d_k<0>, L2_THREADS, 0) != cudaSuccess || o < 1)
             o = 1;
         occ = o;
+        if (dev >= 0 && dev < 64) occ_dev[dev] = o;
     }
     const int64_t items = (int64_t)lat2_segments(nx) * (ny + 1);
     int64_t w = (int64_t)sm_count() * occ * L2_WARPS;
