@@ -687,22 +687,27 @@ __global__ void lattice_check_elems_k(int64_t ne, int64_t nn, const int32_t* __r
         }
         int I0 = min(min(I[0], I[1]), min(I[2], I[3])), J0 = min(min(J[0], J[1]), min(J[2], J[3]));
         int K0 = min(min(K[0], K[1]), min(K[2], K[3]));
-        // order the vertices by level (offset sum 0..3), each level exactly once
-        int at[4] = {-1, -1, -1, -1};
+        // order the vertices by level (offset sum 0..3), each level exactly once (selects, no indexed array:
+        // an array indexed by the level went to local memory)
+        int at0 = -1, at1 = -1, at2 = -1, at3 = -1;
 #pragma unroll
         for (int a = 0; a < 4; a++) {
             const int ox = I[a] - I0, oy = J[a] - J0, oz = K[a] - K0;
             if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) { bad = true; continue; }
-            const int lev = ox + oy + oz;
-            if (at[lev] >= 0) bad = true;
-            at[lev] = ox | oy << 1 | oz << 2;
+            const int lev = ox + oy + oz, cd = ox | oy << 1 | oz << 2;
+            const int prev = lev == 0 ? at0 : (lev == 1 ? at1 : (lev == 2 ? at2 : at3));
+            if (prev >= 0) bad = true;
+            at0 = lev == 0 ? cd : at0;
+            at1 = lev == 1 ? cd : at1;
+            at2 = lev == 2 ? cd : at2;
+            at3 = lev == 3 ? cd : at3;
         }
-        if (!bad && (at[0] != 0 || at[3] != 7)) bad = true;
+        if (!bad && (at0 != 0 || at3 != 7)) bad = true;
         if (I0 >= g.nx || J0 >= g.ny || K0 >= g.nz) bad = true;
         int64_t code = -1;
         if (!bad) {
-            const int s0 = at[1], s1 = at[2] & ~at[1];   // first and second unit steps
-            if (__popc(s0) != 1 || __popc(at[2]) != 2 || (at[2] & s0) != s0) bad = true;
+            const int s0 = at1, s1 = at2 & ~at1;   // first and second unit steps
+            if (__popc(s0) != 1 || __popc(at2) != 2 || (at2 & s0) != s0) bad = true;
             else {
                 const int p0 = __ffs(s0) - 1, p1 = __ffs(s1) - 1;
                 const int path = p0 * 2 + ((p1 == (p0 + 1) % 3) ? 0 : 1);   // 6 paths
