@@ -110,6 +110,12 @@ def test_lattice_k_only_m_only_and_reproducible(dev):
     assert Mn is None and np.array_equal(h(Ko), Kh)
     Kn, Mo = vb.fem_p1_assemble_lattice(cd, plan, want_K=False)
     assert Kn is None and np.array_equal(h(Mo), Mh)
+    # K, M that are not 16-byte aligned take the plain-store path of every tile: the same bits
+    buf = torch.empty(2 * plan.nnz + 3, dtype=torch.float64, device=dev)
+    Ku, Mu = buf[1:1 + plan.nnz], buf[plan.nnz + 2:2 * plan.nnz + 2]
+    assert Ku.data_ptr() % 16 == 8
+    vb.fem_p1_assemble_lattice(cd, plan, K=Ku, M=Mu)
+    assert np.array_equal(h(Ku), Kh) and np.array_equal(h(Mu), Mh)
 
 
 def test_lattice_refuses_other_meshes_and_fem_p1_assemble_falls_back(dev):
