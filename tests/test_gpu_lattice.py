@@ -48,7 +48,8 @@ def lattice_run(coords, elems, dev, dims=None, **kw):
 
 @pytest.mark.parametrize("dims", [(2, 2, 1), (2, 2, 2), (3, 4, 5), (7, 7, 7), (29, 2, 3), (30, 3, 2), (31, 2, 2),
                                   (32, 2, 3), (61, 2, 2), (62, 3, 1), (63, 2, 1), (2, 11, 3), (3, 12, 2), (2, 23, 2),
-                                  (4, 24, 3), (5, 40, 2), (12, 13, 14), (70, 25, 3), (124, 3, 2)])
+                                  (4, 24, 3), (5, 40, 2), (12, 13, 14), (70, 25, 3), (124, 3, 2),
+                                  (2, 2, 300), (95, 23, 9), (31, 12, 40), (64, 56, 20)])
 def test_lattice_vs_oracle(dev, dims):
     coords, elems = synth.box_kuhn_p1(*dims, jitter=0.05, seed=3)
     rp, ci = oracle.p1_pattern(elems, coords.shape[1])
