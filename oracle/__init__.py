@@ -147,6 +147,31 @@ def create_coords3D(coords, elems):
     return c3, v3
 
 
+NORMALS_REF = {   # outer normals of the reference simplex as columns (3D: P:562-570; 2D: the same construction)
+    2: np.array([[-1.0, 0.0, 1.0], [0.0, -1.0, 1.0]]),
+    3: np.array([[-1.0, 0.0, 0.0, 1.0], [0.0, -1.0, 0.0, 1.0], [0.0, 0.0, -1.0, 1.0]]),
+}
+
+
+def simplex_geometry(coords, elems):
+    """Signed sizes and (not normalised) outer normals of every simplex, the paper's two scripts written out
+    with the oracle's own page functions, step by step:
+        [~, vectors3D] = create_coords3D(coords, elems)
+        meass = amdet(vectors3D) / factorial(dim)
+        normals3D = amsm(amt(aminv(vectors3D)), normalsRef)
+    Returns (meass (ne,), normals3D (dim+1, dim, ne): column j of page e at [j, :, e])."""
+    coords, elems = _f64(coords), _i32(elems)
+    dim = coords.shape[0]
+    assert elems.shape[0] == dim + 1 and dim in (2, 3)
+    _, v3 = create_coords3D(coords, elems)
+    fact = 2.0 if dim == 2 else 6.0
+    meass = page_det(v3) / fact
+    vinv, _ = page_inv(v3)
+    nref = np.ascontiguousarray(NORMALS_REF[dim].T[:, :, None])   # one dim x (dim+1) object for every page (eq:copy)
+    normals = page_mtimes(page_transpose(vinv), nref)
+    return meass, normals
+
+
 def tri_surface(xyz, tri):
     """(n (3,F), nhat (3,F), area (F,), volume float)."""
     xyz, tri = _f64(xyz), _i32(tri)
