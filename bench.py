@@ -667,6 +667,19 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
         ne5 * (16 + 72 * 2 + 8) + nn5 * 24, time_kernel(volumes, 10), alg=ne5 * (16 + 8) + nn5 * 24)
     rec("NEXT-4 tet normals config5 (create_coords3D + page_inv + page_transpose + page_mtimes)", ne5, "elements",
         ne5 * (16 + 72 * 6 + 96) + nn5 * 24, time_kernel(normals, 5), alg=ne5 * (16 + 96) + nn5 * 24)
+    # the same two results from one fused pass over coords and elems (vb_simplex_geometry): ALG bytes only
+    gm = torch.empty(ne5, dtype=torch.float64, device=dev)
+    gn = torch.empty((4, 3, ne5), dtype=torch.float64, device=dev)
+    rec("NEXT-4 tet volumes config5, fused (vb_simplex_geometry, meass only)", ne5, "elements",
+        ne5 * (16 + 8) + nn5 * 24,
+        time_kernel(lambda: vb.vb_simplex_geometry(cd5, ed5, want_normals=False, meass=gm), 20))
+    rec("NEXT-4 tet normals config5, fused (vb_simplex_geometry, normals3D only)", ne5, "elements",
+        ne5 * (16 + 96) + nn5 * 24,
+        time_kernel(lambda: vb.vb_simplex_geometry(cd5, ed5, want_meass=False, normals=gn), 10))
+    rec("NEXT-4 tet volumes + normals config5, fused (vb_simplex_geometry)", ne5, "elements",
+        ne5 * (16 + 8 + 96) + nn5 * 24,
+        time_kernel(lambda: vb.vb_simplex_geometry(cd5, ed5, meass=gm, normals=gn), 10))
+    del gm, gn
     # NEXT-4 GI (Code GI P:838-847): the volume integral of rho = x1^2 + x2^2 over the config-5 mesh with the
     # degree-2 rule, GI alone on resident fip (4 points) and sizes: 40 B per tet
     import numpy as np

@@ -134,6 +134,30 @@ VB_API vb_status vb_create_coords3D(int dim, int nv, int64_t ne,
                              const int32_t* elems, int64_t elem_ld,
                              double* coords3D, double* vectors3D, vb_stream_t stream);
 
+/* NEXT-4, fused: signed sizes and (not normalised) outer normals of every simplex
+ * in one pass over coords and elems, the paper's two scripts
+ *   [~, vectors3D] = create_coords3D(coords, elems);
+ *   meass = amdet(vectors3D) / factorial(dim);
+ *   normals3D = amsm(amt(aminv(vectors3D)), normalsRef);
+ * without the intermediate page arrays (the chain of page calls above gives the
+ * same values and remains available).  dim in {2, 3}; elems: dim+1 vertex
+ * planes (elems[a*elem_ld + e]); coords strided as in vb_create_coords3D.
+ * meass (DEVICE, ne; nullable): det[v_0 .. v_{d-1}] / d!, v_a = x_a - x_d (vectors
+ * from the LAST local node); its sign is the orientation, meas =
+ * norm(meass, 1).  normals3D (DEVICE, nullable): dim x (dim+1) pages,
+ * entry (c, j) of page e at normals3D[(c + j*dim)*ldn + e], ldn >= ne; column
+ * j is the outer normal of the face opposite local node j, of length (face
+ * size) / (d |T|) (normalsRef = [-I | 1]; in 2D the same
+ * construction).  At least one output is required.  Planes that are 16-byte
+ * aligned with even ldn / elem_ld take the 128-bit path; any other layout is
+ * handled with scalar accesses (same values).  A degenerate element (det = 0)
+ * gives meass = 0 and non-finite normals, as aminv does; no
+ * validation of vertex ids.  Asynchronous on `stream`; errors as above. */
+VB_API vb_status vb_simplex_geometry(int dim, int64_t ne,
+                              const double* coords, int64_t node_stride, int64_t comp_stride,
+                              const int32_t* elems, int64_t elem_ld,
+                              double* meass, double* normals3D, int64_t ldn, vb_stream_t stream);
+
 /* ---------------------------------------------------------- a6 surface geometry
  * For each triangle f = (a, b, c) (tri[v*tri_ld + f], v = 0..2) of a closed
  * surface with vertex coordinates xyz (strided as above):

@@ -49,7 +49,8 @@ EXPORTS = ("vb_last_error", "vb_abi_version", "vb_page_mtimes", "vb_page_transpo
            "fem_pattern", "fem_p2_assemble", "fem_plan_stats", "fem_plan_pack_slots", "fem_plan_classes",
            "fem_p1_assemble_classes", "fem_plan_tiles", "fem_p1_assemble_tiles",
            "fem_p1_assemble_exact", "fem_p1_assemble_classes_coef", "vb_gi", "fem_plan_lattice",
-           "fem_p1_assemble_lattice", "fem_lattice_pattern", "fem_plan_lattice2d", "fem_p1_assemble_lattice2d", "fem_lattice2d_pattern")
+           "fem_p1_assemble_lattice", "fem_lattice_pattern", "fem_plan_lattice2d", "fem_p1_assemble_lattice2d", "fem_lattice2d_pattern",
+           "vb_simplex_geometry")
 
 
 class VbError(RuntimeError):
@@ -78,6 +79,7 @@ def lib():
             "vb_page_inv": (i32, [i64, i32, p, i64, p, i64, p, p, d, p]),
             "vb_page_cross": (i32, [i64, p, i64, p, i64, p, i64, p]),
             "vb_create_coords3D": (i32, [i32, i32, i64, p, i64, i64, p, i64, p, p, p]),
+            "vb_simplex_geometry": (i32, [i32, i64, p, i64, i64, p, i64, p, p, i64, p]),
             "vb_tri_surface": (i32, [i64, p, i64, i64, p, i64, i64, p, p, p, p, p, sz, p]),
             "fem_p1_pattern": (i32, [i32, i64, i64, p, i64, p, sz, p, p, i64, p, p, p, p,
                                      C.POINTER(C.c_int64), p]),
@@ -217,6 +219,22 @@ def vb_create_coords3D(coords, elems, want_coords3D=True, want_vectors3D=True, s
     _check(lib().vb_create_coords3D(dim, nv, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(c3), _ptr(v3),
                                     _stream(stream)))
     return c3, v3
+
+
+def vb_simplex_geometry(coords, elems, want_meass=True, want_normals=True, meass=None, normals=None, stream=None):
+    """(meass (ne,), normals3D (dim+1, dim, ne)): signed sizes and outer normals of every simplex."""
+    _f64(coords)
+    dim, nn = coords.shape
+    nv, ne = elems.shape
+    if nv != dim + 1:
+        raise ValueError("vb_simplex_geometry: elems must have dim+1 vertex planes")
+    if want_meass and meass is None:
+        meass = torch.empty((ne,), dtype=torch.float64, device=coords.device)
+    if want_normals and normals is None:
+        normals = torch.empty((nv, dim, ne), dtype=torch.float64, device=coords.device)
+    _check(lib().vb_simplex_geometry(dim, ne, _ptr(coords), 1, nn, _ptr(elems), ne, _ptr(meass), _ptr(normals), ne,
+                                     _stream(stream)))
+    return meass, normals
 
 
 def vb_tri_surface(xyz, tri, want_n=True, want_nhat=True, want_area=True, want_volume=True, work=None, out=None,

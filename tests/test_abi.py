@@ -72,6 +72,16 @@ def test_det_inv_transpose_cross_errors(L):
     assert L.vb_page_cross(4, FAKE, 2, FAKE, 4, FAKE, 4, None) == -1
 
 
+def test_simplex_geometry_argument_errors(L):
+    assert L.vb_simplex_geometry(3, -1, FAKE, 1, 8, FAKE, 8, FAKE, FAKE, 8, None) == -1      # ne < 0
+    assert L.vb_simplex_geometry(4, 8, FAKE, 1, 8, FAKE, 8, FAKE, FAKE, 8, None) == -3       # dim
+    assert L.vb_simplex_geometry(3, 0, None, 1, 8, None, 0, None, None, 0, None) == 0        # empty: nothing to do
+    assert L.vb_simplex_geometry(3, 8, FAKE, 1, 8, FAKE, 8, None, None, 8, None) == -1       # no output
+    assert L.vb_simplex_geometry(3, 8, FAKE, 1, 8, FAKE, 7, FAKE, FAKE, 8, None) == -1       # elem_ld < ne
+    assert L.vb_simplex_geometry(3, 8, FAKE, 1, 8, FAKE, 8, FAKE, FAKE, 7, None) == -1       # ldn < ne
+    assert b"ldn" in L.vb_last_error()
+
+
 def test_fem_argument_errors(L):
     nnz = C.c_int64(0)
     sz = C.c_size_t(0)
