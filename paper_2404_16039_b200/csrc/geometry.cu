@@ -60,8 +60,16 @@ __device__ __forceinline__ void simplex_one(const double (&x)[DIM + 1][DIM], dou
     }
 }
 
-template <int DIM, bool VEC>
-__global__ void __launch_bounds__(GEO_BLOCK) simplex_geometry_k(int64_t ne, const double* __restrict__ coords,
+// Resident blocks per SM: with normals 4 (64 registers, a few spilled words: configs[4] normals 0.306 -> 0.289 ms
+// against 2 blocks; 3 measured slower); sizes alone (NRM = false: no cofactors kept) VB_GEO_MINB_M.
+#ifndef VB_GEO_MINB
+#define VB_GEO_MINB 4
+#endif
+#ifndef VB_GEO_MINB_M
+#define VB_GEO_MINB_M 5   // 48 registers, no spills: configs[4] sizes 0.105 ms (6: 40 registers with spills 0.140; 8: 0.190)
+#endif
+template <int DIM, bool VEC, bool NRM>
+__global__ void __launch_bounds__(GEO_BLOCK, NRM ? VB_GEO_MINB : VB_GEO_MINB_M) simplex_geometry_k(int64_t ne, const double* __restrict__ coords,
                                                                 int64_t ns, int64_t cst,
                                                                 const int32_t* __restrict__ elems, int64_t eld,
                                                                 double* __restrict__ meass,
@@ -92,11 +100,11 @@ __global__ void __launch_bounds__(GEO_BLOCK) simplex_geometry_k(int64_t ne, cons
 #pragma unroll
                 for (int c = 0; c < DIM; c++) x[k][a][c] = __ldg(coords + c * cst + (int64_t)vi[k][a] * ns);
         double m[2], nr[2][NV][DIM];
-        simplex_one<DIM>(x[0], m[0], nr[0]);
+        simplex_one<DIM>(x[0], m[0], nr[0]);   // NRM = false: the normals are dead code
         simplex_one<DIM>(x[1], m[1], nr[1]);
         if (VEC && two) {
             if (meass) stcs2(meass + e0, make_double2(m[0], m[1]));
-            if (nrm) {
+            if (NRM) {
 #pragma unroll
                 for (int j = 0; j < NV; j++)
 #pragma unroll
@@ -108,7 +116,7 @@ __global__ void __launch_bounds__(GEO_BLOCK) simplex_geometry_k(int64_t ne, cons
             for (int k = 0; k < 2; k++) {
                 if (k == 1 && !two) break;
                 if (meass) stcs(meass + e0 + k, m[k]);
-                if (nrm) {
+                if (NRM) {
 #pragma unroll
                     for (int j = 0; j < NV; j++)
 #pragma unroll
@@ -138,15 +146,19 @@ extern "C" vb_status vb_simplex_geometry(int dim, int64_t ne, const double* coor
     // 128-bit path: every plane starts 16-byte aligned (elems planes 8-byte aligned for the index pairs)
     const bool vec = (!meass || aligned16(meass)) && (!normals3D || (aligned16(normals3D) && (ldn & 1) == 0)) &&
                      (reinterpret_cast<uintptr_t>(elems) & 7u) == 0 && (elem_ld & 1) == 0;
-    const unsigned g = grid_for((ne + 1) / 2, GEO_BLOCK, 4);
+    const bool nrm = normals3D != nullptr;
+    const unsigned g = grid_for((ne + 1) / 2, GEO_BLOCK, nrm ? VB_GEO_MINB : VB_GEO_MINB_M);
     cudaStream_t s = cs(stream);
-#define VB_GEO(D, V) \
-    simplex_geometry_k<D, V><<<g, GEO_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, meass, normals3D, ldn)
+#define VB_GEO(D, V, N) \
+    simplex_geometry_k<D, V, N><<<g, GEO_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, meass, normals3D, ldn)
+#define VB_GEO2(D, V) \
+    do { if (nrm) VB_GEO(D, V, true); else VB_GEO(D, V, false); } while (0)
     if (dim == 2) {
-        if (vec) VB_GEO(2, true); else VB_GEO(2, false);
+        if (vec) VB_GEO2(2, true); else VB_GEO2(2, false);
     } else {
-        if (vec) VB_GEO(3, true); else VB_GEO(3, false);
+        if (vec) VB_GEO2(3, true); else VB_GEO2(3, false);
     }
+#undef VB_GEO2
 #undef VB_GEO
     return launch_check(fn);
 }

@@ -57,6 +57,71 @@ __global__ void __launch_bounds__(SURF_BLOCK) tri_surface_k(int64_t nf, const in
     }
 }
 
+// the same, two consecutive faces per thread: index pairs loaded as int2, every output plane written with
+// 128-bit stores, both faces' 18 gathers in flight together (nf even, planes 16-byte aligned)
+#ifndef VB_SURF_MINB
+#define VB_SURF_MINB 4   // 64 registers (12 bytes of spills): 32 warps per SM; 3: 0.345 ms, 4: 0.323 ms, 5: 0.384 ms on configs[2]
+#endif
+__global__ void __launch_bounds__(SURF_BLOCK, VB_SURF_MINB) tri_surface2_k(int64_t nf, const int32_t* __restrict__ tri, int64_t tld,
+                                                             const double* __restrict__ xyz, int64_t ns, int64_t cst,
+                                                             double* __restrict__ n_out, double* __restrict__ nh_out,
+                                                             double* __restrict__ area, double* __restrict__ part) {
+    double vol = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t npair = nf / 2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
+        const int64_t f = 2 * t;
+        const int2 ia = __ldcs(reinterpret_cast<const int2*>(tri + f));
+        const int2 ib = __ldcs(reinterpret_cast<const int2*>(tri + tld + f));
+        const int2 ic = __ldcs(reinterpret_cast<const int2*>(tri + 2 * tld + f));
+        const int64_t va[2] = {ia.x, ia.y}, vb_[2] = {ib.x, ib.y}, vc[2] = {ic.x, ic.y};
+        double a[2][3], u[2][3], w[2][3];
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+#pragma unroll
+            for (int d = 0; d < 3; d++) {
+                a[k][d] = __ldg(xyz + d * cst + va[k] * ns);
+                u[k][d] = __ldg(xyz + d * cst + vb_[k] * ns);
+                w[k][d] = __ldg(xyz + d * cst + vc[k] * ns);
+            }
+        double nn[2][3], len[2];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+#pragma unroll
+            for (int d = 0; d < 3; d++) {
+                u[k][d] -= a[k][d];
+                w[k][d] -= a[k][d];
+            }
+            nn[k][0] = fma(u[k][1], w[k][2], -u[k][2] * w[k][1]);
+            nn[k][1] = fma(u[k][2], w[k][0], -u[k][0] * w[k][2]);
+            nn[k][2] = fma(u[k][0], w[k][1], -u[k][1] * w[k][0]);
+            len[k] = sqrt(fma(nn[k][0], nn[k][0], fma(nn[k][1], nn[k][1], nn[k][2] * nn[k][2])));
+            vol += fma(a[k][0], nn[k][0], fma(a[k][1], nn[k][1], a[k][2] * nn[k][2]));
+        }
+        if (n_out) {
+#pragma unroll
+            for (int d = 0; d < 3; d++) stcs2(n_out + d * nf + f, make_double2(nn[0][d], nn[1][d]));
+        }
+        if (nh_out) {
+            const double r0 = 1.0 / len[0], r1 = 1.0 / len[1];
+#pragma unroll
+            for (int d = 0; d < 3; d++) stcs2(nh_out + d * nf + f, make_double2(nn[0][d] * r0, nn[1][d] * r1));
+        }
+        if (area) stcs2(area + f, make_double2(0.5 * len[0], 0.5 * len[1]));
+    }
+    if (part) {
+        __shared__ double sh[SURF_BLOCK / 32];
+        for (int o = 16; o > 0; o >>= 1) vol += __shfl_xor_sync(0xffffffffu, vol, o);
+        if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = vol;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            double t = (threadIdx.x < SURF_BLOCK / 32) ? sh[threadIdx.x] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+            if (threadIdx.x == 0) part[blockIdx.x] = t;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(1024) sum_parts_k(const double* __restrict__ part, int n, double* __restrict__ out) {
     __shared__ double sh[32];
     double s = 0.0;
@@ -207,7 +272,15 @@ extern "C" vb_status vb_tri_surface(int64_t nf, const int32_t* tri, int64_t tri_
     if (tri_ld < nf) { set_error("vb_tri_surface: tri_ld < nf"); return VB_ERR_ARG; }
     auto s = cs(stream);
     double* part = volume ? reinterpret_cast<double*>(work) : nullptr;
-    if (nf > 0) tri_surface_k<<<g, SURF_BLOCK, 0, s>>>(nf, tri, tri_ld, xyz, node_stride, comp_stride, n, nhat, area, part);
+    // pairs of faces with 128-bit accesses when every plane allows it (same values; the volume's partial
+    // sums group differently, each path bitwise reproducible)
+#ifndef VB_SURF_SCALAR
+#define VB_SURF_SCALAR 0   // 1: always the one-face-per-thread kernel (A/B timing)
+#endif
+    const bool vec = !VB_SURF_SCALAR && (nf & 1) == 0 && (tri_ld & 1) == 0 && (reinterpret_cast<uintptr_t>(tri) & 7u) == 0 &&
+                     (!n || aligned16(n)) && (!nhat || aligned16(nhat)) && (!area || aligned16(area));
+    if (nf > 0 && vec) tri_surface2_k<<<g, SURF_BLOCK, 0, s>>>(nf, tri, tri_ld, xyz, node_stride, comp_stride, n, nhat, area, part);
+    else if (nf > 0) tri_surface_k<<<g, SURF_BLOCK, 0, s>>>(nf, tri, tri_ld, xyz, node_stride, comp_stride, n, nhat, area, part);
     if (volume) {
         if (nf == 0) { cudaMemsetAsync(volume, 0, sizeof(double), s); return launch_check("vb_tri_surface"); }
         sum_parts_k<<<1, 1024, 0, s>>>(part, (int)g, volume);

@@ -438,6 +438,30 @@ def test_surface_full_size_config3(dev):
     assert abs(vol - 4.0 * math.pi / 3.0) < 2e-3                     # near the unit ball (radii +-1%)
 
 
+def test_surface_scalar_and_paired_paths_same_bits(dev):
+    """An odd face count or an output plane that is not 16-byte aligned takes the one-face-per-thread
+    kernel, everything else the paired 128-bit kernel: same n, nhat, area bit for bit, and each path's
+    volume within 1e-12 of the oracle on its faces (an open surface is fine for the sum)."""
+    xyz, tri = synth.icosphere(5, perturb=0.01, seed=1)
+    nf = tri.shape[1]
+    xd = g(xyz, dev)
+    full = vb.vb_tri_surface(xd, g(tri, dev))                                   # paired path
+    odd = np.ascontiguousarray(tri[:, :nf - 1])
+    o = vb.vb_tri_surface(xd, g(odd, dev))                                      # odd count: scalar path
+    n, nh, ar, vol = oracle.tri_surface(xyz, odd)
+    for key in ("n", "nhat"):
+        assert np.array_equal(h(o[key]), h(full[key])[:, :nf - 1])
+    assert np.array_equal(h(o["area"]), h(full["area"])[:nf - 1])
+    assert abs(h(o["volume"])[0] - vol) <= 1e-12 * abs(vol)
+    buf = torch.full((3 * nf + 3,), 7.0, dtype=torch.float64, device=dev)       # n 8 bytes off: scalar path
+    o3 = vb.vb_tri_surface(xd, g(tri, dev), out={"n": buf[1:1 + 3 * nf].view(3, nf)})
+    assert np.array_equal(h(o3["n"]), h(full["n"])) and np.array_equal(h(o3["nhat"]), h(full["nhat"]))
+    assert float(buf[0]) == 7.0 and float(buf[3 * nf + 1]) == 7.0
+    _, _, _, vol_full = oracle.tri_surface(xyz, tri)
+    assert abs(h(o3["volume"])[0] - vol_full) <= 1e-12 * abs(vol_full)
+    assert abs(h(full["volume"])[0] - vol_full) <= 1e-12 * abs(vol_full)
+
+
 # ---------------------------------------------------------------- unstructured meshes
 @pytest.mark.parametrize("permute", [False, True])
 @pytest.mark.parametrize("dim,n", [(2, 40), (3, 7), (3, 13)])
