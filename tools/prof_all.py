@@ -43,6 +43,10 @@ del xd, td
 
 c5, e5 = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
 cd, ed = torch.from_numpy(c5).to(dev), torch.from_numpy(e5).to(dev)
+# fused simplex geometry (sizes alone, normals alone, both)
+twice(lambda: vb.vb_simplex_geometry(cd, ed, want_normals=False))
+twice(lambda: vb.vb_simplex_geometry(cd, ed, want_meass=False))
+twice(lambda: vb.vb_simplex_geometry(cd, ed))
 twice(lambda: vb.P1Plan(ed, c5.shape[1]))
 plan = vb.P1Plan(ed, c5.shape[1])
 K = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
