@@ -101,16 +101,99 @@ __global__ void __launch_bounds__(256) rhs_elem_k(int64_t ne, const double* __re
     }
 }
 
+// The same for two ADJACENT elements per thread (ne even, planes 16-byte aligned): index pairs as int2, f and
+// b2D planes with 128-bit accesses, both elements' gathers in flight together.
+#ifndef VB_RHS_MINB
+#define VB_RHS_MINB 3   // config-5 rhs: 2 blocks 0.339 ms, 3: 0.319, 4 (64 registers, spills): 0.321; scalar kernel 0.371
+#endif
+template <int DIM>
+__global__ void __launch_bounds__(256, VB_RHS_MINB) rhs_elem2_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
+                                                      int64_t cst, const int32_t* __restrict__ elems, int64_t eld,
+                                                      const double* __restrict__ fq, const Rule R,
+                                                      double* __restrict__ b2D, double* __restrict__ b) {
+    constexpr int NV = DIM + 1;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t npair = ne / 2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
+        const int64_t e = 2 * t;
+        double fv[2][NV];
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            const double2 f2 = i < R.nip ? ldcs2(fq + (int64_t)i * ne + e) : make_double2(0.0, 0.0);
+            fv[0][i] = f2.x;
+            fv[1][i] = f2.y;
+        }
+        int32_t vid[2][NV];
+#pragma unroll
+        for (int a = 0; a < NV; a++) {
+            const int2 p = __ldg(reinterpret_cast<const int2*>(elems + a * eld + e));
+            vid[0][a] = p.x;
+            vid[1][a] = p.y;
+        }
+        double x[2][NV][DIM];
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+#pragma unroll
+            for (int a = 0; a < NV; a++)
+#pragma unroll
+                for (int c = 0; c < DIM; c++) x[k][a][c] = __ldg(coords + c * cst + (int64_t)vid[k][a] * ns);
+        double loc[2][NV];
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            double det;
+            if constexpr (DIM == 2) {
+                det = fma(x[k][1][0] - x[k][0][0], x[k][2][1] - x[k][0][1],
+                          -(x[k][1][1] - x[k][0][1]) * (x[k][2][0] - x[k][0][0]));
+            } else {
+                double J[3][3];
+#pragma unroll
+                for (int r = 0; r < 3; r++)
+#pragma unroll
+                    for (int c = 0; c < 3; c++) J[r][c] = x[k][r + 1][c] - x[k][0][c];
+                det = J[0][0] * fma(J[1][1], J[2][2], -J[1][2] * J[2][1]) +
+                      J[0][1] * fma(J[1][2], J[2][0], -J[1][0] * J[2][2]) +
+                      J[0][2] * fma(J[1][0], J[2][1], -J[1][1] * J[2][0]);
+            }
+            const double ad = fabs(det);
+#pragma unroll
+            for (int a = 0; a < NV; a++) loc[k][a] = 0.0;
+#pragma unroll
+            for (int i = 0; i < NV; i++) {
+                if (i >= R.nip) break;
+                const double fw = R.w[i] * ad * fv[k][i];
+#pragma unroll
+                for (int a = 0; a < NV; a++) loc[k][a] = fma(fw, R.lam[i][a], loc[k][a]);
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < NV; a++) {
+            if (b2D) stcs2(b2D + (int64_t)a * ne + e, make_double2(loc[0][a], loc[1][a]));
+            if (b) {
+                atomicAdd(b + vid[0][a], loc[0][a]);
+                atomicAdd(b + vid[1][a], loc[1][a]);
+            }
+        }
+    }
+}
+
 // accumarray, deterministic: b_v = sum over v's incidences (ascending e) of b2D(a, e)
 __global__ void __launch_bounds__(256) rhs_gather_k(int64_t nn, int64_t ne, const int32_t* __restrict__ nptr,
                                                     const int32_t* __restrict__ nelem, const double* __restrict__ b2D,
                                                     double* __restrict__ b) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
+        // 8 incidences at a time: their ids, then their values, are loaded before the (ordered) additions
         double s = 0.0;
-        for (int i = __ldg(nptr + v), i1 = __ldg(nptr + v + 1); i < i1; i++) {
-            const int32_t ea = __ldg(nelem + i);
-            s += b2D[(int64_t)(ea & 3) * ne + (ea >> 2)];
+        for (int i = __ldg(nptr + v), i1 = __ldg(nptr + v + 1); i < i1; i += 8) {
+            int32_t ea[8];
+            double val[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) ea[k] = i + k < i1 ? __ldg(nelem + i + k) : -1;
+#pragma unroll
+            for (int k = 0; k < 8; k++) val[k] = ea[k] >= 0 ? __ldg(b2D + (int64_t)(ea[k] & 3) * ne + (ea[k] >> 2)) : 0.0;
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (ea[k] >= 0) s += val[k];
         }
         b[v] = s;
     }
@@ -164,7 +247,16 @@ extern "C" vb_status fem_p1_rhs(int dim, int64_t nn, int64_t ne, const double* c
     if (ne > 0 && (b2D || (b && atomic))) {
         unsigned g = grid_for(ne, 256, 8);
         double* bb = atomic ? b : nullptr;
-        if (dim == 2) rhs_elem_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
+#ifndef VB_RHS_SCALAR
+#define VB_RHS_SCALAR 0   // 1: always the scalar element kernel (A/B timing)
+#endif
+        const bool vec = !VB_RHS_SCALAR && (ne & 1) == 0 && (elem_ld & 1) == 0 && (reinterpret_cast<uintptr_t>(elems) & 7u) == 0 &&
+                         aligned16(fq) && (!b2D || aligned16(b2D));
+        if (vec) {
+            g = grid_for(ne / 2, 256, VB_RHS_MINB);
+            if (dim == 2) rhs_elem2_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
+            else rhs_elem2_k<3><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
+        } else if (dim == 2) rhs_elem_k<2><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
         else rhs_elem_k<3><<<g, 256, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, fq, R, b2D, bb);
     }
     if (b && !atomic && nn > 0)

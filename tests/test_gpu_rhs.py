@@ -57,6 +57,31 @@ def test_rhs_parity(dev, dim, gqo, mode):
     assert relmax(h(b2), b2o) <= 1e-12
 
 
+@pytest.mark.parametrize("mode", [vb.VB_ASSEMBLE_GATHER, vb.VB_ASSEMBLE_ATOMIC])
+@pytest.mark.parametrize("dim", [2, 3])
+def test_rhs_odd_element_count_scalar_path(dev, dim, mode):
+    """An odd element count takes the one-element-per-thread kernel (the paired kernel needs even planes):
+    same parity bar, and b2D equals the paired kernel's on the shared elements bit for bit."""
+    coords, elems = synth.delaunay_p1(dim, 14 if dim == 2 else 8, seed=3)
+    if elems.shape[1] % 2 == 0:
+        elems = np.ascontiguousarray(elems[:, :-1])
+    ne = elems.shape[1]
+    assert ne % 2 == 1
+    lam, w = oracle.quad_rule(dim, 2)
+    xq = np.einsum("qa,cae->qce", lam, coords[:, elems])
+    fq = np.ascontiguousarray(np.exp(xq.sum(1)) * np.cos(3 * xq[:, 0]))
+    bo, b2o = oracle.p1_rhs(coords, elems, fq, gqo=2)
+    cd, ed = g(coords, dev), g(elems, dev)
+    plan = vb.P1Plan(ed, coords.shape[1], scatter_map=False)
+    b, b2 = vb.fem_p1_rhs(cd, ed, g(fq, dev), plan=plan, gqo=2, mode=mode)
+    assert relmax(h(b), bo) <= 1e-12 and relmax(h(b2), b2o) <= 1e-12
+    ev = np.ascontiguousarray(elems[:, :ne - 1])                       # even count: the paired kernel
+    fv = np.ascontiguousarray(fq[:, :ne - 1])
+    pe = vb.P1Plan(g(ev, dev), coords.shape[1], scatter_map=False)
+    _, b2e = vb.fem_p1_rhs(cd, g(ev, dev), g(fv, dev), plan=pe, gqo=2, mode=mode)
+    assert np.array_equal(h(b2e), h(b2)[:, :ne - 1])
+
+
 def test_rhs_gather_is_bitwise_reproducible(dev):
     coords, elems = synth.cube_kuhn_p1(12, jitter=0.05, seed=6)
     lam, w = oracle.quad_rule(3, 2)
