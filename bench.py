@@ -650,6 +650,11 @@ def run_secondary(args, dev, peak, plan5, cd5, ed5, coords5, elems5):
         time_kernel(lambda: vb.fem_p1_rhs(cd5, ed5, fq, plan=p5), 10),
         alg=nn5 * 24 + ne5 * 16 + ne5 * nq * 8 + nn5 * 8)   # without the b2D round trip
     del p5, fq
+    # a7 alone: create_coords3D on the config-5 mesh (both outputs; vectors3D only, as the chains below call it)
+    rec("a7 create_coords3D config5 (coords3D + vectors3D)", ne5, "elements", ne5 * (16 + 96 + 72) + nn5 * 24,
+        time_kernel(lambda: vb.vb_create_coords3D(cd5, ed5), 10, flush))
+    rec("a7 create_coords3D config5 (vectors3D only)", ne5, "elements", ne5 * (16 + 72) + nn5 * 24,
+        time_kernel(lambda: vb.vb_create_coords3D(cd5, ed5, want_coords3D=False), 10, flush))
     # NEXT-4: volumes (amdet(vectors3D)/6) and normals (amsm(amt(aminv(vectors3D)), normalsRef)) of all
     # 12.58M tets of the config-5 mesh; paper (sphere, 12.58M tets): volumes 4.42 s incl. mesh generation
     nref = torch.tensor([[-1, 0, 0], [0, -1, 0], [0, 0, -1], [1, 1, 1]], dtype=torch.float64,

@@ -382,6 +382,51 @@ __global__ void __launch_bounds__(PAGE_BLOCK) gather_k(int64_t ne, const double*
     }
 }
 
+// the same for two adjacent elements per thread: index pairs as int2, every plane written with 128-bit stores
+// (ne even, planes 16-byte aligned)
+#ifndef VB_GATHER_MINB
+#define VB_GATHER_MINB 3
+#endif
+template <int DIM, int NV>
+__global__ void __launch_bounds__(PAGE_BLOCK, VB_GATHER_MINB) gather2_k(int64_t ne, const double* __restrict__ coords, int64_t ns,
+                                                           int64_t cs_, const int32_t* __restrict__ elems, int64_t eld,
+                                                           double* __restrict__ c3, double* __restrict__ v3) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t npair = ne / 2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += stride) {
+        const int64_t e = 2 * t;
+        int64_t v[2][NV];
+#pragma unroll
+        for (int a = 0; a < NV; a++) {
+            const int2 p = __ldcs(reinterpret_cast<const int2*>(elems + a * eld + e));
+            v[0][a] = p.x;
+            v[1][a] = p.y;
+        }
+        double x[2][NV][DIM];
+#pragma unroll
+        for (int k = 0; k < 2; k++)
+#pragma unroll
+            for (int a = 0; a < NV; a++)
+#pragma unroll
+                for (int c = 0; c < DIM; c++) x[k][a][c] = __ldg(coords + c * cs_ + v[k][a] * ns);
+        if (c3) {
+#pragma unroll
+            for (int a = 0; a < NV; a++)
+#pragma unroll
+                for (int c = 0; c < DIM; c++)
+                    stcs2(c3 + (int64_t)(c + a * DIM) * ne + e, make_double2(x[0][a][c], x[1][a][c]));
+        }
+        if (v3) {
+#pragma unroll
+            for (int a = 0; a < NV - 1; a++)
+#pragma unroll
+                for (int c = 0; c < DIM; c++)
+                    stcs2(v3 + (int64_t)(c + a * DIM) * ne + e,
+                          make_double2(x[0][a][c] - x[0][NV - 1][c], x[1][a][c] - x[1][NV - 1][c]));
+        }
+    }
+}
+
 bool ld_ok(int64_t ld, int64_t np, bool input) { return ld >= np || (input && ld == 0); }
 
 bool vec_ok(std::initializer_list<std::pair<const void*, int64_t>> ops) {
@@ -509,7 +554,20 @@ extern "C" vb_status vb_create_coords3D(int dim, int nv, int64_t ne, const doubl
     if (elem_ld < ne) { set_error("vb_create_coords3D: elem_ld < ne"); return VB_ERR_ARG; }
     unsigned g = grid_for(ne, PAGE_BLOCK, PAGE_BLOCKS_PER_SM);
     auto s = cs(stream);
-#define VB_GATHER(D, V) gather_k<D, V><<<g, PAGE_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, coords3D, vectors3D)
+    bool vec = (ne & 1) == 0 && (elem_ld & 1) == 0 && (reinterpret_cast<uintptr_t>(elems) & 7u) == 0 &&
+               (!coords3D || aligned16(coords3D)) && (!vectors3D || aligned16(vectors3D));
+    #ifndef VB_GATHER_SCALAR
+#define VB_GATHER_SCALAR 0
+#endif
+    // measured on the configs[4] mesh (tools/time_gather.py): one output 0.236 (scalar) -> 0.201 ms (paired, 3 blocks
+    // per SM); both outputs 0.452 (scalar) vs 0.465 (paired): the paired kernel takes the one-output calls only
+    if (VB_GATHER_SCALAR || (coords3D && vectors3D)) vec = false;
+    if (vec) g = grid_for(ne / 2, PAGE_BLOCK, VB_GATHER_MINB);
+#define VB_GATHER(D, V)                                                                                                     \
+    do {                                                                                                                    \
+        if (vec) gather2_k<D, V><<<g, PAGE_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, coords3D, vectors3D); \
+        else gather_k<D, V><<<g, PAGE_BLOCK, 0, s>>>(ne, coords, node_stride, comp_stride, elems, elem_ld, coords3D, vectors3D);      \
+    } while (0)
     if (dim == 1) {
         if (nv == 2) VB_GATHER(1, 2); else if (nv == 3) VB_GATHER(1, 3); else VB_GATHER(1, 4);
     } else if (dim == 2) {

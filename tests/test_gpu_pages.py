@@ -189,6 +189,37 @@ def test_create_coords3D_bitwise(dev, dim):
     assert np.array_equal(h(c3), oc3) and np.array_equal(h(v3), ov3)
 
 
+@pytest.mark.parametrize("dim", [2, 3])
+def test_create_coords3D_odd_count_and_surface_faces_bitwise(dev, dim):
+    """Odd element counts take the one-element-per-thread kernel, even ones the paired 128-bit kernel; also the
+    3 x 3 x |F_b| form for boundary faces (nv = 3 in 3D).  All bitwise equal to the oracle."""
+    coords, elems = synth.delaunay_p1(dim, 12 if dim == 2 else 7, seed=2)
+    for ne in (elems.shape[1], elems.shape[1] - 1, 1, 2):
+        el = np.ascontiguousarray(elems[:, :ne])
+        c3, v3 = vb.vb_create_coords3D(g(coords, dev), g(el, dev))
+        oc3, ov3 = oracle.create_coords3D(coords, el)
+        assert np.array_equal(h(c3), oc3) and np.array_equal(h(v3), ov3)
+        _, v3b = vb.vb_create_coords3D(g(coords, dev), g(el, dev), want_coords3D=False)
+        assert np.array_equal(h(v3b), ov3)
+    if dim == 3:
+        xyz, tri = synth.icosphere(3, perturb=0.01, seed=0)
+        for nf in (tri.shape[1], tri.shape[1] - 1):
+            t = np.ascontiguousarray(tri[:, :nf])
+            c3, v3 = vb.vb_create_coords3D(g(xyz, dev), g(t, dev))
+            oc3, ov3 = oracle.create_coords3D(xyz, t)
+            assert np.array_equal(h(c3), oc3) and np.array_equal(h(v3), ov3)
+
+
+def test_create_coords3D_full_size_configs4(dev):
+    """The configs[4] mesh (12.58 M tets) in the launch configuration bench.py times, every entry."""
+    coords, elems = synth.cube_kuhn_p1(128, jitter=0.05, seed=0)
+    c3, v3 = vb.vb_create_coords3D(g(coords, dev), g(elems, dev))
+    oc3, ov3 = oracle.create_coords3D(coords, elems)
+    assert np.array_equal(h(c3), oc3)
+    del c3, oc3
+    assert np.array_equal(h(v3), ov3)
+
+
 # ---------------------------------------------------------------- full size (config 2)
 @pytest.mark.parametrize("n", [2, 3, 4])
 def test_config2_full_size(dev, n):
