@@ -405,7 +405,10 @@ vb_status pattern_impl(const char* fn, int nv, int64_t nn, int64_t ne, const int
             return VB_ERR_ARG;
         }
     }
-    unsigned gr = grid_for(nn, BLOCK, 4);
+#ifndef VB_PATTERN_BPS
+#define VB_PATTERN_BPS 6   // resident row-kernel blocks per SM (32 KB of lists each: 6 fit); configs[4] pattern-only 2.11 (4) / 2.03 (5) / 1.98 (6) / 2.45 ms (7: a second wave)
+#endif
+    unsigned gr = grid_for(nn, BLOCK, VB_PATTERN_BPS);
 
     // 1. node -> element incidences (into work; the fill phase reuses them)
     auto incidences = [&]() -> vb_status {
