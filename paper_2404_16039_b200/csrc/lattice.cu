@@ -681,70 +681,91 @@ __device__ __forceinline__ void canon(const LatGeom& g, int64_t id, int& I, int&
     K = (int)(g.fz ? g.nz - k : k);
 }
 
+// (cell, path) code of one element, or -1 if it is not a Kuhn tetrahedron of the canonical lattice
+__device__ __forceinline__ int64_t lattice_elem_code(const LatGeom& g, int64_t nn, const int32_t (&vid)[4]) {
+    int I[4], J[4], K[4];
+    bool bad = false;
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        const int32_t v = vid[a];
+        if (v < 0 || v >= nn) { bad = true; I[a] = J[a] = K[a] = 0; continue; }
+        canon(g, v, I[a], J[a], K[a]);
+    }
+    int I0 = min(min(I[0], I[1]), min(I[2], I[3])), J0 = min(min(J[0], J[1]), min(J[2], J[3]));
+    int K0 = min(min(K[0], K[1]), min(K[2], K[3]));
+    // order the vertices by level (offset sum 0..3), each level exactly once (selects, no indexed array:
+    // an array indexed by the level went to local memory)
+    int at0 = -1, at1 = -1, at2 = -1, at3 = -1;
+#pragma unroll
+    for (int a = 0; a < 4; a++) {
+        const int ox = I[a] - I0, oy = J[a] - J0, oz = K[a] - K0;
+        if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) { bad = true; continue; }
+        const int lev = ox + oy + oz, cd = ox | oy << 1 | oz << 2;
+        const int prev = lev == 0 ? at0 : (lev == 1 ? at1 : (lev == 2 ? at2 : at3));
+        if (prev >= 0) bad = true;
+        at0 = lev == 0 ? cd : at0;
+        at1 = lev == 1 ? cd : at1;
+        at2 = lev == 2 ? cd : at2;
+        at3 = lev == 3 ? cd : at3;
+    }
+    if (!bad && (at0 != 0 || at3 != 7)) bad = true;
+    if (I0 >= g.nx || J0 >= g.ny || K0 >= g.nz) bad = true;
+    if (bad) return -1;
+    const int s0 = at1, s1 = at2 & ~at1;   // first and second unit steps
+    if (__popc(s0) != 1 || __popc(at2) != 2 || (at2 & s0) != s0) return -1;
+    const int p0 = __ffs(s0) - 1, p1 = __ffs(s1) - 1;
+    const int path = p0 * 2 + ((p1 == (p0 + 1) % 3) ? 0 : 1);   // 6 paths
+    return (((int64_t)K0 * g.ny + J0) * g.nx + I0) * 6 + path;
+}
+
 // every element is one Kuhn tetrahedron of the canonical lattice; its (cell, path) code is marked in a
 // bitset, a code seen twice or a non-Kuhn element sets flags[0]
+constexpr int LCHK_U = 4;   // groups of 32 elements per warp and step: their loads, then their atomics, in flight together
 __global__ void lattice_check_elems_k(int64_t ne, int64_t nn, const int32_t* __restrict__ elems, int64_t eld,
                                       LatGeom g, uint32_t* __restrict__ bits, int* __restrict__ flags) {
     const int lane = threadIdx.x & 31;
     // whole warps run the loop: the bitset update is aggregated per word (elements in cell order put a warp's
-    // 32 codes into one or two words: 2 atomics instead of 32; 0.39 -> 0.1 ms on configs[4])
-    for (int64_t eb = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); eb < ne;
-         eb += (int64_t)gridDim.x * blockDim.x) {
-        const bool valid = eb + lane < ne;
-        const int64_t e = valid ? eb + lane : ne - 1;
-        int I[4], J[4], K[4];
+    // 32 codes into one or two words: 2 atomics instead of 32; 0.39 -> 0.23 ms on configs[4]); a step was one
+    // dependent chain load -> code -> atomic (old word back) per warp, so LCHK_U groups run side by side
+    for (int64_t eb = (blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31)) * LCHK_U; eb < ne;
+         eb += (int64_t)gridDim.x * blockDim.x * LCHK_U) {
+        int32_t vid[LCHK_U][4];
+        bool valid[LCHK_U];
+#pragma unroll
+        for (int u = 0; u < LCHK_U; u++) {
+            valid[u] = eb + u * 32 + lane < ne;
+            const int64_t e = valid[u] ? eb + u * 32 + lane : ne - 1;
+#pragma unroll
+            for (int a = 0; a < 4; a++) vid[u][a] = elems[a * eld + e];
+        }
+        int64_t code[LCHK_U];
+        uint32_t old[LCHK_U], bit[LCHK_U];
+        unsigned peers[LCHK_U];
+#pragma unroll
+        for (int u = 0; u < LCHK_U; u++) {
+            code[u] = lattice_elem_code(g, nn, vid[u]);
+            const bool mark = valid[u] && code[u] >= 0;
+            // lanes of one word: OR their bits, one atomic by the lowest lane, the old word back to all of them;
+            // a code twice inside the warp shows as two lanes with the same bit
+            const long long key = mark ? (long long)(code[u] >> 5) : -1 - lane;
+            peers[u] = __match_any_sync(0xffffffffu, key);
+            bit[u] = mark ? 1u << (code[u] & 31) : 0u;
+            const uint32_t all = __reduce_or_sync(peers[u], bit[u]);
+            old[u] = 0;
+            if (mark && lane == __ffs(peers[u]) - 1) old[u] = atomicOr(bits + (code[u] >> 5), all);
+        }
         bool bad = false;
 #pragma unroll
-        for (int a = 0; a < 4; a++) {
-            const int32_t v = elems[a * eld + e];
-            if (v < 0 || v >= nn) { bad = true; I[a] = J[a] = K[a] = 0; continue; }
-            canon(g, v, I[a], J[a], K[a]);
-        }
-        int I0 = min(min(I[0], I[1]), min(I[2], I[3])), J0 = min(min(J[0], J[1]), min(J[2], J[3]));
-        int K0 = min(min(K[0], K[1]), min(K[2], K[3]));
-        // order the vertices by level (offset sum 0..3), each level exactly once (selects, no indexed array:
-        // an array indexed by the level went to local memory)
-        int at0 = -1, at1 = -1, at2 = -1, at3 = -1;
-#pragma unroll
-        for (int a = 0; a < 4; a++) {
-            const int ox = I[a] - I0, oy = J[a] - J0, oz = K[a] - K0;
-            if (ox < 0 || ox > 1 || oy < 0 || oy > 1 || oz < 0 || oz > 1) { bad = true; continue; }
-            const int lev = ox + oy + oz, cd = ox | oy << 1 | oz << 2;
-            const int prev = lev == 0 ? at0 : (lev == 1 ? at1 : (lev == 2 ? at2 : at3));
-            if (prev >= 0) bad = true;
-            at0 = lev == 0 ? cd : at0;
-            at1 = lev == 1 ? cd : at1;
-            at2 = lev == 2 ? cd : at2;
-            at3 = lev == 3 ? cd : at3;
-        }
-        if (!bad && (at0 != 0 || at3 != 7)) bad = true;
-        if (I0 >= g.nx || J0 >= g.ny || K0 >= g.nz) bad = true;
-        int64_t code = -1;
-        if (!bad) {
-            const int s0 = at1, s1 = at2 & ~at1;   // first and second unit steps
-            if (__popc(s0) != 1 || __popc(at2) != 2 || (at2 & s0) != s0) bad = true;
-            else {
-                const int p0 = __ffs(s0) - 1, p1 = __ffs(s1) - 1;
-                const int path = p0 * 2 + ((p1 == (p0 + 1) % 3) ? 0 : 1);   // 6 paths
-                code = (((int64_t)K0 * g.ny + J0) * g.nx + I0) * 6 + path;
+        for (int u = 0; u < LCHK_U; u++) {
+            const bool mark = valid[u] && code[u] >= 0;
+            const uint32_t o = __shfl_sync(peers[u], old[u], __ffs(peers[u]) - 1);
+            if (mark) {
+                const unsigned same = __match_any_sync(peers[u], bit[u]);
+                if ((o & bit[u]) || __popc(same) > 1) bad = true;
             }
+            if (valid[u] && code[u] < 0) bad = true;
         }
-        const bool mark = valid && !bad;
-        // lanes of one word: OR their bits, one atomic by the lowest lane, the old word back to all of them;
-        // a code twice inside the warp shows as two lanes with the same bit
-        const long long key = mark ? (long long)(code >> 5) : -1 - lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const uint32_t bit = mark ? 1u << (code & 31) : 0u;
-        const uint32_t all = __reduce_or_sync(peers, bit);
-        const int lead = __ffs(peers) - 1;
-        uint32_t old = 0;
-        if (mark && lane == lead) old = atomicOr(bits + (code >> 5), all);
-        old = __shfl_sync(peers, old, lead);
-        if (mark) {
-            const unsigned same = __match_any_sync(peers, bit);
-            if ((old & bit) || __popc(same) > 1) bad = true;
-        }
-        if (valid && bad) atomicExch(flags, 1);
+        if (bad) atomicExch(flags, 1);
     }
 }
 
