@@ -170,3 +170,29 @@ def test_fused_geometry_full_size_configs4_every_element(dev):
     per_page = np.max(np.abs(Nh - N_o), axis=(0, 1)) / np.max(np.abs(N_o), axis=(0, 1))
     assert np.max(per_page) <= 1e-10
     assert abs(math.fsum(np.abs(h(m))) - 1.0) <= 1e-11
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_fused_geometry_strided_coords_through_the_c_abi(dev, dim):
+    """coords addressed as coords[c*comp_stride + v*node_stride]: AoS (node_stride = dim) and padded AoS
+    (node_stride = 4) through the C ABI give the same bits as the SoA layout; ldn > ne leaves the gap untouched."""
+    import ctypes as C
+    coords, elems = synth.delaunay_p1(dim, 10 if dim == 2 else 7, seed=6)
+    nn, ne = coords.shape[1], elems.shape[1]
+    m0, N0 = vb.vb_simplex_geometry(g(coords, dev), g(elems, dev))
+    ed = g(elems, dev)
+    L = vb.lib()
+    for ns in (dim, 4):
+        aos = np.zeros((nn, ns))
+        aos[:, :dim] = coords.T
+        ad = g(aos, dev)
+        ldn = ne + 6
+        m = torch.full((ne,), 7.0, dtype=torch.float64, device=dev)
+        N = torch.full(((dim + 1) * dim, ldn), 7.0, dtype=torch.float64, device=dev)
+        rc = L.vb_simplex_geometry(dim, ne, C.c_void_p(ad.data_ptr()), ns, 1, C.c_void_p(ed.data_ptr()), ne,
+                                   C.c_void_p(m.data_ptr()), C.c_void_p(N.data_ptr()), ldn, None)
+        assert rc == 0, L.vb_last_error()
+        assert np.array_equal(h(m), h(m0))
+        Nh = h(N)
+        assert np.array_equal(Nh[:, :ne].reshape(dim + 1, dim, ne), h(N0))
+        assert np.all(Nh[:, ne:] == 7.0)
