@@ -43,6 +43,83 @@ __global__ void bucket_fill_k(int64_t ne, int nv, const int32_t* __restrict__ el
 // Lists of up to SORT_CAP entries are loaded into a per-thread shared-memory
 // strip (stride SORT_BLOCK, bank-conflict free), sorted there and written back;
 // longer lists are sorted in place in global memory.
+// Lists of up to 32 entries (every list of the Kuhn and square meshes: 24 / 6 incidences per interior node) are
+// sorted in registers by a bitonic network padded with INT_MAX (240 compare-exchanges for 32 values, all indices
+// compile-time): the bucket fill's atomics leave a list in arrival order, which is random within a wave of the
+// grid, so the insertion sort paid n^2/4 shared-memory moves per list (ncu r02g: 214 M warp instructions, 0.43 ms).
+#ifndef VB_SORT_NET
+#define VB_SORT_NET 1   // 0: insertion sort only; 2: networks with word accesses (A/B timing)
+#endif
+template <int N>
+__device__ __forceinline__ void sort_net(int32_t* __restrict__ p, int n) {
+    int32_t r[N];
+#pragma unroll
+    for (int i = 0; i < N; i++) r[i] = i < n ? p[i] : 0x7fffffff;
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int32_t lo = min(r[i], r[l]), hi = max(r[i], r[l]);
+                    const bool asc = (i & k) == 0;
+                    r[i] = asc ? lo : hi;
+                    r[l] = asc ? hi : lo;
+                }
+            }
+#pragma unroll
+    for (int i = 0; i < N; i++)
+        if (i < n) p[i] = r[i];
+}
+
+// The same through 128-bit accesses: the list [lo, lo + n) sits at offset h = lo & 3 of the aligned quads that cover
+// it (h + n <= N); values of the neighbouring lists in the first and last quad are replaced by -inf / +inf
+// sentinels, so after the network position j holds the sorted entry j - h, and only positions [h, h + n) are
+// written back (whole quads where they lie inside the list).  A per-thread list is 96 bytes apart from its
+// neighbour's: 6-8 quad loads instead of 24 word loads per list.
+template <int N>
+__device__ __forceinline__ void sort_net_quads(int32_t* __restrict__ pa, int h, int n) {
+    int32_t r[N];
+    const int4* q = reinterpret_cast<const int4*>(pa);
+#pragma unroll
+    for (int qi = 0; qi < N / 4; qi++) {
+        int4 t = make_int4(0, 0, 0, 0);
+        if (qi * 4 < h + n) t = q[qi];
+        r[4 * qi] = t.x;
+        r[4 * qi + 1] = t.y;
+        r[4 * qi + 2] = t.z;
+        r[4 * qi + 3] = t.w;
+    }
+#pragma unroll
+    for (int j = 0; j < N; j++) r[j] = j < h ? (int32_t)0x80000000 : (j < h + n ? r[j] : 0x7fffffff);
+#pragma unroll
+    for (int k = 2; k <= N; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int32_t lo = min(r[i], r[l]), hi = max(r[i], r[l]);
+                    const bool asc = (i & k) == 0;
+                    r[i] = asc ? lo : hi;
+                    r[l] = asc ? hi : lo;
+                }
+            }
+#pragma unroll
+    for (int qi = 0; qi < N / 4; qi++) {
+        if (4 * qi >= h && 4 * qi + 4 <= h + n) {
+            reinterpret_cast<int4*>(pa)[qi] = make_int4(r[4 * qi], r[4 * qi + 1], r[4 * qi + 2], r[4 * qi + 3]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 4; c++)
+                if (4 * qi + c >= h && 4 * qi + c < h + n) pa[4 * qi + c] = r[4 * qi + c];
+        }
+    }
+}
+
 constexpr int SORT_BLOCK = 128;
 constexpr int SORT_CAP = 48;
 __global__ void __launch_bounds__(SORT_BLOCK) sort_incidences_k(int64_t nn, const int32_t* __restrict__ nptr,
@@ -53,6 +130,19 @@ __global__ void __launch_bounds__(SORT_BLOCK) sort_incidences_k(int64_t nn, cons
     for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nn; v += stride) {
         int lo = nptr[v], hi = nptr[v + 1];
         const int n = hi - lo;
+        if (VB_SORT_NET && n <= 32) {
+            if (n <= 1) continue;
+            const int h = lo & 3;   // node_elem is 256-byte aligned in the work buffer (carve)
+            int32_t* pa = node_elem + (lo - h);
+            if (VB_SORT_NET == 2 || h + n > 32) {
+                if (n <= 8) sort_net<8>(node_elem + lo, n);
+                else if (n <= 16) sort_net<16>(node_elem + lo, n);
+                else sort_net<32>(node_elem + lo, n);
+            } else if (h + n <= 8) sort_net_quads<8>(pa, h, n);
+            else if (h + n <= 16) sort_net_quads<16>(pa, h, n);
+            else sort_net_quads<32>(pa, h, n);
+            continue;
+        }
         if (n <= SORT_CAP) {
             for (int i = 0; i < n; i++) {
                 int32_t x = node_elem[lo + i];
