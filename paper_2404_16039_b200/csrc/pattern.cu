@@ -249,6 +249,8 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
     if (!elem2nnz && !slots) return;
     if (slots && cnt > 255) atomicExch(flags + FLAG_SLOT_RANGE, 1);
     int lo = nptr[v], hi = nptr[v + 1];
+    // the row's own vertex (local vertex a of every incidence) has one position: searched once per row
+    const int pos_self = lower_bound_s(L, st, cnt, (int32_t)v);
     for (int i0 = lo; i0 < hi; i0 += CH) {
         int32_t ea[CH], w[CH][NVM];
         load_chunk<SH>(i0, hi, nv, elems, eld, node_elem, ea, w);
@@ -265,7 +267,7 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
 #pragma unroll
                 for (int b = 0; b < NVM; b++) {
                     if (b >= nv) break;
-                    int pos = lower_bound_s(L, st, cnt, w[k][b]);
+                    int pos = (b == a) ? pos_self : lower_bound_s(L, st, cnt, w[k][b]);
                     VB_CHECK(pos < cnt && L[pos * st] == w[k][b]);   // every vertex is in the row
                     if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
                     int sh = (b == a) ? 0 : 8 * byte++;
@@ -281,7 +283,7 @@ __device__ void emit_row(int64_t v, int cnt, int nv, int64_t ne, const int32_t* 
 #pragma unroll
                 for (int b = 0; b < NVM; b++) {
                     if (b >= nv) break;
-                    int pos = lower_bound_s(L, st, cnt, w[k][b]);
+                    int pos = (b == a) ? pos_self : lower_bound_s(L, st, cnt, w[k][b]);
                     VB_CHECK(pos < cnt && L[pos * st] == w[k][b]);
                     if (elem2nnz) elem2nnz[(int64_t)(a * nv + b) * ne + e] = base + pos;
                     packed[b / 4] |= (uint32_t)(pos & 0xff) << (8 * (b % 4));
